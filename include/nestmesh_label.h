@@ -1,0 +1,138 @@
+/*
+ * nestmesh_label.h — C ABI of libnestmesh_label.so, the B200 (sm_100a)
+ * implementation of the recursive solid-angle labeling path of nestmesh
+ * (arXiv 2203.10000).
+ *
+ * The reference library (/root/reference/proj/include/nestmesh) specifies the
+ * labeling module only in SPEC.md:210-272; it has no labeling code and no FFI.
+ * These entry points are what a maintainer binds behind the SPEC signatures
+ * (see include/nestmesh/labeling.hpp for the C++ drop-in and INTEGRATION.md
+ * for the binding):
+ *
+ *   nm_enclosure      <- enclosure_ratio(point, surface)
+ *   nm_label_nodes    <- node classification of initial_label
+ *   nm_label_tets     <- tet rule of initial_label
+ *   nm_label_mesh     <- initial_label(mesh, seg, params)
+ *   nm_flag_boundary  <- straddle layer of refine_boundary
+ *   nm_relabel        <- relabel_recursive(mesh, seg, params, prev_labels)
+ *                                                                SPEC.md:243-251
+ *
+ * Conventions
+ *   - Plain pointers and sizes; no torch or STL types cross this boundary.
+ *   - Host-buffer entry points borrow caller-owned buffers for the duration
+ *     of the call and are synchronous. *_device entry points take device
+ *     pointers and a cudaStream_t (passed as void*, NULL = the context's own
+ *     stream) and are asynchronous: they never synchronise with the host.
+ *   - Points are fp64 xyz triples (the layout of std::vector<nestmesh::Vec3>,
+ *     vec3.hpp:11-28); triangles are uint32 index triples into one fp64 vertex
+ *     array (std::vector<nestmesh::Triangle>, surface.hpp:16); tets are uint32
+ *     quadruples (std::vector<nestmesh::Tet>, mesh.hpp:19); labels are int32
+ *     (mesh.hpp:33), 0 = outside / bounding box.
+ *   - Compartments are given innermost (highest priority) first, at most 32;
+ *     bit k of a node mask means "inside compartment k" (s_k >= T).
+ *   - Return 0 on success, non-zero on failure; nm_last_error() returns a
+ *     thread-local message. There is no CPU fallback: without a usable
+ *     sm_100 device every compute entry point fails.
+ *   - Results are independent of the number of devices / ranks a point set is
+ *     sharded over.
+ */
+#ifndef NESTMESH_LABEL_H
+#define NESTMESH_LABEL_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define NM_ABI_VERSION 1
+
+typedef struct nm_ctx nm_ctx;
+
+/* Tunables of the solid-angle kernel (defaults from nm_default_options). */
+typedef struct nm_options {
+  int device;            /* CUDA device ordinal */
+  float tau;             /* near-face detector: |num| <= tau*r1r2r3 && den <= tau*r1r2r3 */
+  float delta_mm;        /* near-vertex detector: min r_i <= delta_mm */
+  double band;           /* |s - T| < band after the fp32 pass -> fp64 fix-up */
+  double tie_eps;        /* |s - T| < tie_eps after fix-up -> counted as a tie */
+  float far_ratio;       /* subtile is "far" for a point when d >= far_ratio * radius + far_abs_mm */
+  float far_abs_mm;
+  int sort_points;       /* 1: Morton-order points before the kernel (performance only) */
+} nm_options;
+
+/* Counters of one labeling call (accumulated by the call, not across calls). */
+typedef struct nm_stats {
+  uint64_t points;           /* points evaluated */
+  uint64_t triangles;        /* real triangles over all compartments */
+  uint64_t evals;            /* points x triangles (algorithmic point-triangle evaluations) */
+  uint64_t flagged_points;   /* points sent to the fp64 fix-up */
+  uint64_t flagged_pairs;    /* (point, compartment) pairs re-evaluated in fp64 */
+  uint64_t ties;             /* pairs with |s - T| < tie_eps after fix-up */
+  uint64_t near_subtiles;    /* warp x 32-triangle subtile visits that took the near path */
+  uint64_t far_subtiles;     /* ... that took the far path */
+  uint64_t launches;         /* kernels launched by this call */
+  float ms_label;            /* device time of the fp32 solid-angle kernel (CUDA events) */
+  float ms_fixup;            /* device time of compaction + fp64 fix-up */
+  float ms_tets;             /* device time of the tet kernels */
+  float ms_total;            /* device time of the whole call */
+} nm_stats;
+
+int nm_abi_version(void);
+const char* nm_last_error(void);
+void nm_default_options(nm_options* opt);
+
+int nm_create(nm_ctx** ctx, const nm_options* opt /* NULL = defaults */);
+int nm_destroy(nm_ctx* ctx);
+
+/* Replicated surface set: nv fp64 vertices, nt triangles (global indices),
+ * compartment k owns triangles [comp_tri_off[k], comp_tri_off[k+1]).
+ * label_ids[k] is the tet label of compartment k (> 0). */
+int nm_set_surfaces(nm_ctx* ctx, const double* xyz, size_t nv, const uint32_t* tri, size_t nt,
+                    const uint32_t* comp_tri_off, int K, const int* label_ids);
+
+/* Enclosure ratios s[i*K + k] (fp64; fp32 pass + fp64 fix-up of flagged pairs). */
+int nm_enclosure(nm_ctx* ctx, const double* pts, size_t n, double threshold, double* s_out, nm_stats* stats);
+
+/* Node masks (bit k = s_k >= T). */
+int nm_label_nodes(nm_ctx* ctx, const double* pts, size_t n, double threshold, uint32_t* masks_out,
+                   nm_stats* stats);
+
+/* Tet labels from node masks: label_ids[lowest k inside at all 4 nodes], else 0. */
+int nm_label_tets(nm_ctx* ctx, const uint32_t* tets, size_t nt, const uint32_t* masks, size_t n_nodes,
+                  int* labels_out, nm_stats* stats);
+
+/* initial_label: host nodes + tets in, host tet labels (and optional node masks) out. */
+int nm_label_mesh(nm_ctx* ctx, const double* nodes, size_t n_nodes, const uint32_t* tets, size_t nt,
+                  double threshold, int* labels_out, uint32_t* masks_out /* nullable */, nm_stats* stats);
+
+/* Tets whose node masks disagree on an active compartment (OR != AND on
+ * active_mask), ascending; *count receives how many were written. */
+int nm_flag_boundary(nm_ctx* ctx, const uint32_t* tets, size_t nt, const uint32_t* masks, size_t n_nodes,
+                     uint32_t active_mask, uint32_t* tet_ids_out, size_t* count);
+
+/* relabel_recursive: labels_io = prev_labels in, result out. Re-evaluates only
+ * nodes of tets adjacent to label-change faces, pass after pass, until a pass
+ * changes no label or max_iters passes ran. Returns 0 on success; *passes and
+ * *converged report the iteration; converged == 0 means NonConvergence (labels
+ * are the best found). evaluated (nullable, n_nodes bytes) marks evaluated nodes. */
+int nm_relabel(nm_ctx* ctx, const double* nodes, size_t n_nodes, const uint32_t* tets, size_t nt,
+               double threshold, int max_iters, int* labels_io, int* passes, int* converged,
+               uint8_t* evaluated /* nullable */, nm_stats* stats);
+
+/* ---- device-resident entry points (asynchronous on `stream`) -------------- */
+int nm_label_nodes_device(nm_ctx* ctx, const double* d_pts, size_t n, double threshold, uint32_t* d_masks,
+                          double* d_s_out /* nullable, n*K */, void* stream, nm_stats* stats);
+int nm_label_tets_device(nm_ctx* ctx, const uint32_t* d_tets, size_t nt, const uint32_t* d_masks,
+                         int* d_labels, void* stream, nm_stats* stats);
+int nm_flag_boundary_device(nm_ctx* ctx, const uint32_t* d_tets, size_t nt, const uint32_t* d_masks,
+                            uint32_t active_mask, uint32_t* d_ids, uint32_t* d_count, void* stream);
+
+/* Compartment count and total padded triangle count of the current surfaces. */
+int nm_surface_info(nm_ctx* ctx, int* K, size_t* triangles, size_t* padded_triangles);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NESTMESH_LABEL_H */

@@ -1,0 +1,278 @@
+"""ctypes binding of libnestmesh_label.so (include/nestmesh_label.h).
+
+The shared library is built in-tree by ``paper_2203_10000_b200.build`` and is
+the only compute path: there is no CPU fallback. Loading fails loudly when the
+library is missing; every compute call fails loudly without an sm_100 device.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from pathlib import Path
+
+import numpy as np
+
+PKG_DIR = Path(__file__).resolve().parent
+LIB_DIR = PKG_DIR / "lib"
+LABEL_LIB = LIB_DIR / "libnestmesh_label.so"
+SYNTH_LIB = LIB_DIR / "libnestmesh_synth.so"
+
+c_double_p = ctypes.POINTER(ctypes.c_double)
+c_u32_p = ctypes.POINTER(ctypes.c_uint32)
+c_i32_p = ctypes.POINTER(ctypes.c_int)
+c_u8_p = ctypes.POINTER(ctypes.c_uint8)
+c_size_p = ctypes.POINTER(ctypes.c_size_t)
+
+
+class NmOptions(ctypes.Structure):
+    _fields_ = [
+        ("device", ctypes.c_int),
+        ("tau", ctypes.c_float),
+        ("delta_mm", ctypes.c_float),
+        ("band", ctypes.c_double),
+        ("tie_eps", ctypes.c_double),
+        ("far_ratio", ctypes.c_float),
+        ("far_abs_mm", ctypes.c_float),
+        ("sort_points", ctypes.c_int),
+    ]
+
+
+class NmStats(ctypes.Structure):
+    _fields_ = [
+        ("points", ctypes.c_uint64),
+        ("triangles", ctypes.c_uint64),
+        ("evals", ctypes.c_uint64),
+        ("flagged_points", ctypes.c_uint64),
+        ("flagged_pairs", ctypes.c_uint64),
+        ("ties", ctypes.c_uint64),
+        ("near_subtiles", ctypes.c_uint64),
+        ("far_subtiles", ctypes.c_uint64),
+        ("launches", ctypes.c_uint64),
+        ("ms_label", ctypes.c_float),
+        ("ms_fixup", ctypes.c_float),
+        ("ms_tets", ctypes.c_float),
+        ("ms_total", ctypes.c_float),
+    ]
+
+    def as_dict(self) -> dict:
+        return {name: getattr(self, name) for name, _ in self._fields_}
+
+
+# name -> (restype, argtypes); mirrors include/nestmesh_label.h exactly.
+LABEL_API = {
+    "nm_abi_version": (ctypes.c_int, []),
+    "nm_last_error": (ctypes.c_char_p, []),
+    "nm_default_options": (None, [ctypes.POINTER(NmOptions)]),
+    "nm_create": (ctypes.c_int, [ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(NmOptions)]),
+    "nm_destroy": (ctypes.c_int, [ctypes.c_void_p]),
+    "nm_set_surfaces": (ctypes.c_int, [ctypes.c_void_p, c_double_p, ctypes.c_size_t, c_u32_p, ctypes.c_size_t,
+                                       c_u32_p, ctypes.c_int, c_i32_p]),
+    "nm_enclosure": (ctypes.c_int, [ctypes.c_void_p, c_double_p, ctypes.c_size_t, ctypes.c_double, c_double_p,
+                                    ctypes.POINTER(NmStats)]),
+    "nm_label_nodes": (ctypes.c_int, [ctypes.c_void_p, c_double_p, ctypes.c_size_t, ctypes.c_double, c_u32_p,
+                                      ctypes.POINTER(NmStats)]),
+    "nm_label_tets": (ctypes.c_int, [ctypes.c_void_p, c_u32_p, ctypes.c_size_t, c_u32_p, ctypes.c_size_t, c_i32_p,
+                                     ctypes.POINTER(NmStats)]),
+    "nm_label_mesh": (ctypes.c_int, [ctypes.c_void_p, c_double_p, ctypes.c_size_t, c_u32_p, ctypes.c_size_t,
+                                     ctypes.c_double, c_i32_p, c_u32_p, ctypes.POINTER(NmStats)]),
+    "nm_flag_boundary": (ctypes.c_int, [ctypes.c_void_p, c_u32_p, ctypes.c_size_t, c_u32_p, ctypes.c_size_t,
+                                        ctypes.c_uint32, c_u32_p, c_size_p]),
+    "nm_relabel": (ctypes.c_int, [ctypes.c_void_p, c_double_p, ctypes.c_size_t, c_u32_p, ctypes.c_size_t,
+                                  ctypes.c_double, ctypes.c_int, c_i32_p, c_i32_p, c_i32_p, c_u8_p,
+                                  ctypes.POINTER(NmStats)]),
+    "nm_label_nodes_device": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_double,
+                                             ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                             ctypes.POINTER(NmStats)]),
+    "nm_label_tets_device": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p,
+                                            ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(NmStats)]),
+    "nm_flag_boundary_device": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p,
+                                               ctypes.c_uint32, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
+    "nm_surface_info": (ctypes.c_int, [ctypes.c_void_p, c_i32_p, c_size_p, c_size_p]),
+}
+
+_lib = None
+
+
+def load_label_lib() -> ctypes.CDLL:
+    """Load the CUDA labeling library; raise if it was not built."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not LABEL_LIB.exists():
+        raise ImportError(
+            f"{LABEL_LIB} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+            "(the labeling path has no CPU fallback)")
+    lib = ctypes.CDLL(str(LABEL_LIB))
+    for name, (res, args) in LABEL_API.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+class NativeError(RuntimeError):
+    pass
+
+
+def check(rc: int) -> None:
+    if rc != 0:
+        msg = load_label_lib().nm_last_error()
+        raise NativeError(msg.decode() if msg else f"libnestmesh_label error {rc}")
+
+
+def ptr(a: np.ndarray, ctype):
+    return a.ctypes.data_as(ctypes.POINTER(ctype))
+
+
+def default_options(**overrides) -> NmOptions:
+    opt = NmOptions()
+    load_label_lib().nm_default_options(ctypes.byref(opt))
+    for k, v in overrides.items():
+        setattr(opt, k, v)
+    return opt
+
+
+class Context:
+    """One device + one stream + the replicated surface set (nm_ctx)."""
+
+    def __init__(self, device: int = 0, **options):
+        self.lib = load_label_lib()
+        opt = default_options(device=device, **options)
+        h = ctypes.c_void_p()
+        check(self.lib.nm_create(ctypes.byref(h), ctypes.byref(opt)))
+        self.handle = h
+        self.options = opt
+        self.K = 0
+
+    def close(self):
+        if getattr(self, "handle", None):
+            self.lib.nm_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    # -- surfaces ---------------------------------------------------------
+    def set_surfaces(self, xyz, tri, comp_off, label_ids):
+        xyz = np.ascontiguousarray(xyz, dtype=np.float64).reshape(-1, 3)
+        tri = np.ascontiguousarray(tri, dtype=np.uint32).reshape(-1, 3)
+        comp_off = np.ascontiguousarray(comp_off, dtype=np.uint32)
+        label_ids = np.ascontiguousarray(label_ids, dtype=np.int32)
+        K = len(label_ids)
+        check(self.lib.nm_set_surfaces(self.handle, ptr(xyz, ctypes.c_double), xyz.shape[0], ptr(tri, ctypes.c_uint32),
+                                       tri.shape[0], ptr(comp_off, ctypes.c_uint32), K, ptr(label_ids, ctypes.c_int)))
+        self.K = K
+
+    def surface_info(self):
+        K = ctypes.c_int()
+        t = ctypes.c_size_t()
+        tp = ctypes.c_size_t()
+        check(self.lib.nm_surface_info(self.handle, ctypes.byref(K), ctypes.byref(t), ctypes.byref(tp)))
+        return K.value, t.value, tp.value
+
+    # -- host-buffer entry points ----------------------------------------
+    def enclosure(self, pts, threshold=0.5):
+        pts = np.ascontiguousarray(pts, dtype=np.float64).reshape(-1, 3)
+        s = np.empty((pts.shape[0], self.K), dtype=np.float64)
+        st = NmStats()
+        check(self.lib.nm_enclosure(self.handle, ptr(pts, ctypes.c_double), pts.shape[0], threshold,
+                                    ptr(s, ctypes.c_double), ctypes.byref(st)))
+        return s, st.as_dict()
+
+    def label_nodes(self, pts, threshold=0.5):
+        pts = np.ascontiguousarray(pts, dtype=np.float64).reshape(-1, 3)
+        m = np.empty(pts.shape[0], dtype=np.uint32)
+        st = NmStats()
+        check(self.lib.nm_label_nodes(self.handle, ptr(pts, ctypes.c_double), pts.shape[0], threshold,
+                                      ptr(m, ctypes.c_uint32), ctypes.byref(st)))
+        return m, st.as_dict()
+
+    def label_tets(self, tets, masks):
+        tets = np.ascontiguousarray(tets, dtype=np.uint32).reshape(-1, 4)
+        masks = np.ascontiguousarray(masks, dtype=np.uint32)
+        out = np.empty(tets.shape[0], dtype=np.int32)
+        st = NmStats()
+        check(self.lib.nm_label_tets(self.handle, ptr(tets, ctypes.c_uint32), tets.shape[0],
+                                     ptr(masks, ctypes.c_uint32), masks.shape[0], ptr(out, ctypes.c_int),
+                                     ctypes.byref(st)))
+        return out
+
+    def label_mesh(self, nodes, tets, threshold=0.5, want_masks=False):
+        nodes = np.ascontiguousarray(nodes, dtype=np.float64).reshape(-1, 3)
+        tets = np.ascontiguousarray(tets, dtype=np.uint32).reshape(-1, 4)
+        labels = np.empty(tets.shape[0], dtype=np.int32)
+        masks = np.empty(nodes.shape[0], dtype=np.uint32) if want_masks else None
+        st = NmStats()
+        check(self.lib.nm_label_mesh(self.handle, ptr(nodes, ctypes.c_double), nodes.shape[0],
+                                     ptr(tets, ctypes.c_uint32), tets.shape[0], threshold, ptr(labels, ctypes.c_int),
+                                     ptr(masks, ctypes.c_uint32) if masks is not None else None, ctypes.byref(st)))
+        return labels, masks, st.as_dict()
+
+    def flag_boundary(self, tets, masks, active_mask=0xFFFFFFFF):
+        tets = np.ascontiguousarray(tets, dtype=np.uint32).reshape(-1, 4)
+        masks = np.ascontiguousarray(masks, dtype=np.uint32)
+        ids = np.empty(max(tets.shape[0], 1), dtype=np.uint32)
+        cnt = ctypes.c_size_t()
+        check(self.lib.nm_flag_boundary(self.handle, ptr(tets, ctypes.c_uint32), tets.shape[0],
+                                        ptr(masks, ctypes.c_uint32), masks.shape[0], active_mask,
+                                        ptr(ids, ctypes.c_uint32), ctypes.byref(cnt)))
+        return ids[: cnt.value].copy()
+
+    def relabel(self, nodes, tets, prev_labels, threshold=0.5, max_iters=64, want_evaluated=False):
+        nodes = np.ascontiguousarray(nodes, dtype=np.float64).reshape(-1, 3)
+        tets = np.ascontiguousarray(tets, dtype=np.uint32).reshape(-1, 4)
+        labels = np.array(prev_labels, dtype=np.int32, copy=True)
+        passes = ctypes.c_int()
+        conv = ctypes.c_int()
+        ev = np.zeros(nodes.shape[0], dtype=np.uint8) if want_evaluated else None
+        st = NmStats()
+        check(self.lib.nm_relabel(self.handle, ptr(nodes, ctypes.c_double), nodes.shape[0],
+                                  ptr(tets, ctypes.c_uint32), tets.shape[0], threshold, max_iters,
+                                  ptr(labels, ctypes.c_int), ctypes.byref(passes), ctypes.byref(conv),
+                                  ptr(ev, ctypes.c_uint8) if ev is not None else None, ctypes.byref(st)))
+        return labels, passes.value, bool(conv.value), ev, st.as_dict()
+
+    # -- device-resident entry points (torch tensors) ---------------------
+    def label_nodes_device(self, d_pts, d_masks, threshold=0.5, d_s=None, stream=None, stats=True):
+        """d_pts: CUDA float64 tensor (n,3); d_masks: CUDA uint32/int32 tensor (n,)."""
+        st = NmStats() if stats else None
+        check(self.lib.nm_label_nodes_device(self.handle, d_pts.data_ptr(), d_pts.shape[0], threshold,
+                                             d_masks.data_ptr(), d_s.data_ptr() if d_s is not None else None,
+                                             stream, ctypes.byref(st) if st is not None else None))
+        return st.as_dict() if st is not None else None
+
+    def label_tets_device(self, d_tets, d_masks, d_labels, stream=None, stats=True):
+        st = NmStats() if stats else None
+        check(self.lib.nm_label_tets_device(self.handle, d_tets.data_ptr(), d_tets.shape[0], d_masks.data_ptr(),
+                                            d_labels.data_ptr(), stream,
+                                            ctypes.byref(st) if st is not None else None))
+        return st.as_dict() if st is not None else None
+
+    def flag_boundary_device(self, d_tets, d_masks, d_ids, d_count, active_mask=0xFFFFFFFF, stream=None):
+        check(self.lib.nm_flag_boundary_device(self.handle, d_tets.data_ptr(), d_tets.shape[0], d_masks.data_ptr(),
+                                               active_mask, d_ids.data_ptr(), d_count.data_ptr(), stream))
+
+
+def exported_symbols(path=LABEL_LIB) -> set:
+    """Dynamic symbols exported by a shared library (for the ABI test)."""
+    import subprocess
+    out = subprocess.run(["nm", "-D", "--defined-only", str(path)], capture_output=True, text=True, check=True).stdout
+    return {line.split()[-1] for line in out.splitlines() if line.strip()}
+
+
+def cuda_device_available() -> bool:
+    try:
+        import torch
+        return torch.cuda.is_available()
+    except Exception:
+        return os.path.exists("/dev/nvidia0")

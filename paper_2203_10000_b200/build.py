@@ -1,0 +1,78 @@
+"""In-tree build of the native libraries (sm_100a only).
+
+    libnestmesh_label.so   CUDA kernels + C ABI (include/nestmesh_label.h)
+    libnestmesh_synth.so   synthetic-input generators (caller side)
+
+plus the oracle (test infrastructure, oracle/Makefile). Outputs stay in the
+repo tree so they travel to the GPU box with the gpurun snapshot.
+"""
+from __future__ import annotations
+
+import os
+import shutil
+import subprocess
+import sys
+from pathlib import Path
+
+PKG = Path(__file__).resolve().parent
+ROOT = PKG.parent
+CSRC = PKG / "csrc"
+LIB = PKG / "lib"
+NVCC = os.environ.get("NVCC", shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc")
+CXX = os.environ.get("CXX", shutil.which("g++") or "g++")
+
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "-shared", f"-I{ROOT / 'include'}",
+              "-Xptxas", "-v"]
+
+
+def _run(cmd, log=None):
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        sys.stderr.write(r.stdout + r.stderr)
+        raise RuntimeError(f"build failed: {' '.join(map(str, cmd))}")
+    if log is not None:
+        log.write_text(r.stdout + r.stderr)
+    return r
+
+
+def _stale(out: Path, deps) -> bool:
+    if not out.exists():
+        return True
+    t = out.stat().st_mtime
+    return any(Path(d).stat().st_mtime > t for d in deps)
+
+
+def build_label_lib(force=False) -> Path:
+    LIB.mkdir(exist_ok=True)
+    out = LIB / "libnestmesh_label.so"
+    deps = list(CSRC.glob("*.cu")) + list(CSRC.glob("*.cuh")) + [ROOT / "include" / "nestmesh_label.h"]
+    if force or _stale(out, deps):
+        _run([NVCC, *ARCH, *NVCC_FLAGS, str(CSRC / "nestmesh_label.cu"), "-o", str(out)], log=LIB / "ptxas_label.log")
+    return out
+
+
+def build_synth_lib(force=False) -> Path:
+    LIB.mkdir(exist_ok=True)
+    out = LIB / "libnestmesh_synth.so"
+    src = CSRC / "synth.cpp"
+    if force or _stale(out, [src]):
+        _run([CXX, "-std=c++20", "-O2", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared", "-Wall", "-Wextra",
+              str(src), "-o", str(out)])
+    return out
+
+
+def build_oracle() -> None:
+    """Test infrastructure: the fp64 oracle and, when /root/reference exists, oracle/_ref."""
+    _run(["make", "-s", "-C", str(ROOT / "oracle")])
+
+
+def build_all(force=False) -> None:
+    build_synth_lib(force)
+    build_label_lib(force)
+    build_oracle()
+
+
+if __name__ == "__main__":
+    build_all(force="--force" in sys.argv)
+    print("built:", *sorted(p.name for p in LIB.glob("*.so")))

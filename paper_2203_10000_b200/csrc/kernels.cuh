@@ -1,0 +1,361 @@
+// Kernels of the B200 labeling path (sm_100a). See DESIGN.md §3 for the
+// roofline each one is measured against.
+//
+//   k_morton_keys    30-bit Morton keys of the points (performance only)
+//   k_label<P>       K1: fp32 N-body tile loop over every triangle of every
+//                    compartment, fp64 fold per 256-triangle tile, inside
+//                    bits + near-surface flags
+//   k_select_*       order-preserving stream compaction (count / scan / write)
+//   k_fixup          K3: fp64 re-evaluation of flagged (point, compartment)
+//   k_label_tets     K4: tet label = id[ffs(AND of 4 node masks)]
+//   straddle         K4': OR != AND on active compartments
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "vos.cuh"
+
+namespace nm {
+
+constexpr int kTile = 256;              // triangles per shared-memory tile (fp64 fold granularity)
+constexpr int kSub = 32;                // triangles per subtile (near/far decision unit)
+constexpr int kSubPerTile = kTile / kSub;
+constexpr int kBlock = 256;             // threads per CTA of k_label
+constexpr unsigned kFull = 0xffffffffu;
+constexpr double kInv2Pi = 0.15915494309189533576888376337251;
+
+struct LabelIds {
+  int id[32];
+};
+
+struct LabelParams {
+  const double* pts;         // fp64 xyz, original frame
+  std::size_t n;
+  const std::uint32_t* order;  // evaluation order (Morton); nullptr = identity
+  const float4* tri;         // 3 float4 per padded triangle: (a.xyz,N.x) (b.xyz,N.y) (c.xyz,N.z)
+  const float4* sub;         // per subtile: fp32 centre c (centred frame), w = (far radius)^2;
+                             // the subtile's vertices are stored relative to c
+  const std::uint32_t* comp_tiles;  // K+1 tile offsets
+  int K;
+  double cx, cy, cz;         // centring offset of the fp32 frame
+  double T, band;
+  float tau, delta;
+  std::uint32_t* masks;      // n
+  std::uint32_t* flagmask;   // n (bit k: pair (i,k) needs the fp64 fix-up)
+  double* s_out;             // n*K or nullptr
+  unsigned long long* counters;  // [0] near subtile visits, [1] far subtile visits
+};
+
+template <int P>
+__global__ void __launch_bounds__(kBlock) k_label(const LabelParams prm) {
+  __shared__ float4 s_tri[kTile * 3];
+  __shared__ float4 s_sub[kSubPerTile];
+
+  const std::size_t base = (static_cast<std::size_t>(blockIdx.x) * kBlock + threadIdx.x) * P;
+  // Point in the centred frame as a double-single (hi + lo); per subtile the
+  // kernel forms p - c = (hi - c) + lo, exact up to one rounding of |p - c|.
+  float hx[P], hy[P], hz[P], lx[P], ly[P], lz[P];
+  std::size_t pid[P];
+  bool valid[P];
+#pragma unroll
+  for (int k = 0; k < P; ++k) {
+    const std::size_t i = base + k;
+    valid[k] = i < prm.n;
+    const std::size_t ii = valid[k] ? i : prm.n - 1;
+    const std::size_t j = prm.order ? prm.order[ii] : ii;
+    pid[k] = j;
+    const double dx = prm.pts[3 * j] - prm.cx, dy = prm.pts[3 * j + 1] - prm.cy, dz = prm.pts[3 * j + 2] - prm.cz;
+    hx[k] = static_cast<float>(dx);
+    hy[k] = static_cast<float>(dy);
+    hz[k] = static_cast<float>(dz);
+    lx[k] = static_cast<float>(dx - hx[k]);
+    ly[k] = static_cast<float>(dy - hy[k]);
+    lz[k] = static_cast<float>(dz - hz[k]);
+  }
+  std::uint32_t mask[P], fmask[P];
+#pragma unroll
+  for (int k = 0; k < P; ++k) mask[k] = fmask[k] = 0u;
+  unsigned n_near = 0, n_far = 0;
+
+  int tile = prm.comp_tiles[0];
+  for (int c = 0; c < prm.K; ++c) {
+    const int tile_end = prm.comp_tiles[c + 1];
+    double acc64[P];
+    bool det[P];
+#pragma unroll
+    for (int k = 0; k < P; ++k) {
+      acc64[k] = 0.0;
+      det[k] = false;
+    }
+    for (; tile < tile_end; ++tile) {
+      __syncthreads();
+      const float4* gt = prm.tri + static_cast<std::size_t>(tile) * kTile * 3;
+#pragma unroll
+      for (int i = threadIdx.x; i < kTile * 3; i += kBlock) s_tri[i] = __ldg(gt + i);
+      if (threadIdx.x < kSubPerTile) s_sub[threadIdx.x] = __ldg(prm.sub + static_cast<std::size_t>(tile) * kSubPerTile + threadIdx.x);
+      __syncthreads();
+
+      float acc[P];
+#pragma unroll
+      for (int k = 0; k < P; ++k) acc[k] = 0.0f;
+      for (int st = 0; st < kSubPerTile; ++st) {
+        const float4 sb = s_sub[st];
+        float px[P], py[P], pz[P];
+        bool far = true;
+#pragma unroll
+        for (int k = 0; k < P; ++k) {
+          px[k] = __fadd_rn(__fsub_rn(hx[k], sb.x), lx[k]);
+          py[k] = __fadd_rn(__fsub_rn(hy[k], sb.y), ly[k]);
+          pz[k] = __fadd_rn(__fsub_rn(hz[k], sb.z), lz[k]);
+          far &= (!valid[k]) || (px[k] * px[k] + py[k] * py[k] + pz[k] * pz[k] > sb.w);
+        }
+        const float4* tt = s_tri + st * kSub * 3;
+        if (__all_sync(kFull, far)) {
+          ++n_far;
+#pragma unroll 4
+          for (int t = 0; t < kSub; ++t) {
+            const float4 A = tt[3 * t], B = tt[3 * t + 1], C = tt[3 * t + 2];
+#pragma unroll
+            for (int k = 0; k < P; ++k) {
+              const VosTerms v = vos_terms(A, B, C, px[k], py[k], pz[k]);
+              acc[k] = acc_far(acc[k], v.num, v.den);
+            }
+          }
+        } else {
+          ++n_near;
+#pragma unroll 2
+          for (int t = 0; t < kSub; ++t) {
+            const float4 A = tt[3 * t], B = tt[3 * t + 1], C = tt[3 * t + 2];
+#pragma unroll
+            for (int k = 0; k < P; ++k) {
+              const VosTerms v = vos_terms(A, B, C, px[k], py[k], pz[k]);
+              acc[k] = acc_near(acc[k], v, prm.tau, prm.delta, det[k]);
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < P; ++k) acc64[k] += static_cast<double>(acc[k]);
+    }
+#pragma unroll
+    for (int k = 0; k < P; ++k) {
+      const double s = acc64[k] * kInv2Pi;
+      if (s >= prm.T) mask[k] |= 1u << c;
+      // NaN-safe: anything not provably outside the band is re-evaluated.
+      if (det[k] || !(fabs(s - prm.T) >= prm.band)) fmask[k] |= 1u << c;
+      if (prm.s_out && valid[k]) prm.s_out[pid[k] * prm.K + c] = s;
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < P; ++k) {
+    if (valid[k]) {
+      prm.masks[pid[k]] = mask[k];
+      prm.flagmask[pid[k]] = fmask[k];
+    }
+  }
+  if ((threadIdx.x & 31) == 0 && prm.counters) {
+    atomicAdd(prm.counters + 0, static_cast<unsigned long long>(n_near));
+    atomicAdd(prm.counters + 1, static_cast<unsigned long long>(n_far));
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Morton keys (10 bits per axis) of points in [lo, lo + 1/inv) — only the
+// evaluation order depends on them, never a result.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ std::uint32_t spread10(std::uint32_t v) {
+  v &= 0x3ffu;
+  v = (v | (v << 16)) & 0x030000ffu;
+  v = (v | (v << 8)) & 0x0300f00fu;
+  v = (v | (v << 4)) & 0x030c30c3u;
+  v = (v | (v << 2)) & 0x09249249u;
+  return v;
+}
+
+__global__ void k_morton_keys(const double* pts, std::size_t n, double lx, double ly, double lz, double inv,
+                              std::uint32_t* keys, std::uint32_t* idx) {
+  for (std::size_t i = blockIdx.x * static_cast<std::size_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<std::size_t>(gridDim.x) * blockDim.x) {
+    auto q = [&](double v, double l) {
+      const double t = (v - l) * inv;
+      return static_cast<std::uint32_t>(t < 0.0 ? 0.0 : (t > 1023.0 ? 1023.0 : t));
+    };
+    keys[i] = spread10(q(pts[3 * i], lx)) | (spread10(q(pts[3 * i + 1], ly)) << 1) |
+              (spread10(q(pts[3 * i + 2], lz)) << 2);
+    idx[i] = static_cast<std::uint32_t>(i);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Order-preserving stream compaction: out = [i for i in [0,n) if pred(i)].
+// Three launches (count per chunk, scan of chunk counts, ordered write); the
+// total lands in *d_count on the device, so consumers need no host sync.
+// ---------------------------------------------------------------------------
+constexpr int kSelBlock = 256;
+constexpr int kSelItems = 8;  // per thread
+constexpr int kSelChunk = kSelBlock * kSelItems;
+
+template <class Pred>
+__global__ void __launch_bounds__(kSelBlock) k_select_count(Pred pred, std::size_t n, std::uint32_t* chunk_counts) {
+  const std::size_t b0 = static_cast<std::size_t>(blockIdx.x) * kSelChunk;
+  int total = 0;
+#pragma unroll
+  for (int j = 0; j < kSelItems; ++j) {
+    const std::size_t i = b0 + j * kSelBlock + threadIdx.x;
+    total += __syncthreads_count(i < n && pred(i));
+  }
+  if (threadIdx.x == 0) chunk_counts[blockIdx.x] = static_cast<std::uint32_t>(total);
+}
+
+// Single-CTA exclusive scan of chunk counts; writes the grand total.
+__global__ void __launch_bounds__(1024) k_select_scan(std::uint32_t* counts, std::size_t nb, std::uint32_t* d_total) {
+  __shared__ std::uint32_t warp_sums[32];
+  __shared__ std::uint32_t carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (std::size_t b0 = 0; b0 < nb; b0 += 1024) {
+    const std::size_t i = b0 + threadIdx.x;
+    const std::uint32_t v = i < nb ? counts[i] : 0u;
+    // inclusive warp scan
+    std::uint32_t x = v;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const std::uint32_t y = __shfl_up_sync(kFull, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) warp_sums[w] = x;
+    __syncthreads();
+    if (w == 0) {
+      std::uint32_t s = warp_sums[lane];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const std::uint32_t y = __shfl_up_sync(kFull, s, o);
+        if (lane >= o) s += y;
+      }
+      warp_sums[lane] = s;  // inclusive over warps
+    }
+    __syncthreads();
+    const std::uint32_t excl = carry + (w ? warp_sums[w - 1] : 0u) + x - v;
+    if (i < nb) counts[i] = excl;
+    __syncthreads();
+    if (threadIdx.x == 1023) carry = excl + v;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *d_total = carry;
+}
+
+template <class Pred>
+__global__ void __launch_bounds__(kSelBlock) k_select_write(Pred pred, std::size_t n, const std::uint32_t* chunk_offsets,
+                                                            std::uint32_t* out) {
+  __shared__ std::uint32_t warp_cnt[kSelBlock / 32];
+  const std::size_t b0 = static_cast<std::size_t>(blockIdx.x) * kSelChunk;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  std::uint32_t running = chunk_offsets[blockIdx.x];
+#pragma unroll 1
+  for (int j = 0; j < kSelItems; ++j) {
+    const std::size_t i = b0 + j * kSelBlock + threadIdx.x;
+    const bool p = i < n && pred(i);
+    const unsigned bal = __ballot_sync(kFull, p);
+    if (lane == 0) warp_cnt[w] = __popc(bal);
+    __syncthreads();
+    std::uint32_t before = 0, tot = 0;
+#pragma unroll
+    for (int q = 0; q < kSelBlock / 32; ++q) {
+      const std::uint32_t c = warp_cnt[q];
+      before += q < w ? c : 0u;
+      tot += c;
+    }
+    if (p) out[running + before + __popc(bal & ((1u << lane) - 1u))] = static_cast<std::uint32_t>(i);
+    running += tot;
+    __syncthreads();
+  }
+}
+
+struct PredNonzero {
+  const std::uint32_t* v;
+  __device__ bool operator()(std::size_t i) const { return v[i] != 0u; }
+};
+
+struct PredStraddle {
+  const uint4* tets;
+  const std::uint32_t* masks;
+  std::uint32_t active;
+  __device__ bool operator()(std::size_t i) const {
+    const uint4 t = tets[i];
+    const std::uint32_t a = masks[t.x], b = masks[t.y], c = masks[t.z], d = masks[t.w];
+    return (((a & b & c & d) ^ (a | b | c | d)) & active) != 0u;
+  }
+};
+
+// ---------------------------------------------------------------------------
+// K3: fp64 fix-up. One warp per flagged point; lanes stride the compartment's
+// triangles in file order, fixed xor-butterfly reduction (deterministic).
+// ---------------------------------------------------------------------------
+struct FixupParams {
+  const double* pts;
+  const std::uint32_t* list;    // flagged point ids
+  const std::uint32_t* count;   // device count of list
+  const std::uint32_t* flagmask;
+  const double* xyz;            // original fp64 vertices
+  const std::uint32_t* tri;     // original triangles
+  const std::uint32_t* comp_off;  // K+1
+  int K;
+  double T, tie_eps;
+  std::uint32_t* masks;
+  double* s_out;
+  unsigned long long* counters;  // [2] pairs, [3] ties
+};
+
+__global__ void __launch_bounds__(256) k_fixup(const FixupParams prm) {
+  const int lane = threadIdx.x & 31;
+  const std::uint32_t nwarps = gridDim.x * (blockDim.x / 32);
+  const std::uint32_t cnt = *prm.count;
+  unsigned long long pairs = 0, ties = 0;
+  for (std::uint32_t w = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); w < cnt; w += nwarps) {
+    const std::uint32_t i = prm.list[w];
+    std::uint32_t fm = prm.flagmask[i];
+    std::uint32_t m = prm.masks[i];
+    const double px = prm.pts[3 * static_cast<std::size_t>(i)], py = prm.pts[3 * static_cast<std::size_t>(i) + 1],
+                 pz = prm.pts[3 * static_cast<std::size_t>(i) + 2];
+    while (fm) {
+      const int c = __ffs(fm) - 1;
+      fm &= fm - 1;
+      double sum = 0.0;
+      for (std::uint32_t t = prm.comp_off[c] + lane; t < prm.comp_off[c + 1]; t += 32) {
+        const std::uint32_t* e = prm.tri + 3 * static_cast<std::size_t>(t);
+        sum += vos_half_angle64(prm.xyz + 3 * static_cast<std::size_t>(e[0]), prm.xyz + 3 * static_cast<std::size_t>(e[1]),
+                                prm.xyz + 3 * static_cast<std::size_t>(e[2]), px, py, pz);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(kFull, sum, o);
+      const double s = sum / (2.0 * CUDART_PI);
+      if (s >= prm.T) m |= 1u << c;
+      else m &= ~(1u << c);
+      ++pairs;
+      if (fabs(s - prm.T) < prm.tie_eps) ++ties;
+      if (prm.s_out && lane == 0) prm.s_out[static_cast<std::size_t>(i) * prm.K + c] = s;
+    }
+    if (lane == 0) prm.masks[i] = m;
+  }
+  if (lane == 0 && prm.counters) {
+    atomicAdd(prm.counters + 2, pairs);
+    atomicAdd(prm.counters + 3, ties);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K4: tet labels: highest-priority compartment containing all
+// four nodes, else 0.
+// ---------------------------------------------------------------------------
+__global__ void k_label_tets(const uint4* __restrict__ tets, std::size_t nt, const std::uint32_t* __restrict__ masks,
+                             int* __restrict__ labels, const LabelIds ids) {
+  for (std::size_t i = blockIdx.x * static_cast<std::size_t>(blockDim.x) + threadIdx.x; i < nt;
+       i += static_cast<std::size_t>(gridDim.x) * blockDim.x) {
+    const uint4 t = __ldg(tets + i);
+    const std::uint32_t m = __ldg(masks + t.x) & __ldg(masks + t.y) & __ldg(masks + t.z) & __ldg(masks + t.w);
+    labels[i] = m ? ids.id[__ffs(m) - 1] : 0;
+  }
+}
+
+}  // namespace nm

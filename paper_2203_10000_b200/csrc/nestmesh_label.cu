@@ -1,0 +1,608 @@
+// libnestmesh_label.so — C ABI (include/nestmesh_label.h) over the sm_100a
+// labeling kernels. One context = one device + one stream; host entry points
+// are synchronous, *_device entry points are asynchronous on the caller's
+// stream. There is no CPU fallback: every compute entry point fails without
+// a usable device.
+#include <algorithm>
+#include <array>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <exception>
+#include <numeric>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include <cub/device/device_radix_sort.cuh>
+#include <cuda_runtime.h>
+
+#include "kernels.cuh"
+#include "nestmesh_label.h"
+
+namespace {
+
+thread_local std::string g_err;
+
+struct Error : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+#define NM_CUDA(x)                                                                                    \
+  do {                                                                                                \
+    cudaError_t e_ = (x);                                                                             \
+    if (e_ != cudaSuccess)                                                                            \
+      throw Error(std::string(#x) + ": " + cudaGetErrorName(e_) + " " + cudaGetErrorString(e_));       \
+  } while (0)
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 1;
+  } catch (...) {
+    g_err = "unknown error";
+    return 1;
+  }
+}
+
+// Growable device buffer.
+struct DBuf {
+  void* p = nullptr;
+  std::size_t cap = 0;
+  void* get(std::size_t bytes) {
+    if (bytes > cap) {
+      if (p) cudaFree(p);
+      p = nullptr;
+      cap = 0;
+      const std::size_t want = std::max<std::size_t>(bytes, 256);
+      NM_CUDA(cudaMalloc(&p, want));
+      cap = want;
+    }
+    return p;
+  }
+  template <class T>
+  T* as(std::size_t count) {
+    return static_cast<T*>(get(count * sizeof(T)));
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+  }
+};
+
+// Morton order of triangle centroids (per compartment): compact 256-triangle
+// tiles and 32-triangle subtiles for the near/far split. Order affects only
+// the fp32 summation order, never which triangles are summed.
+std::uint32_t spread10h(std::uint32_t v) {
+  v &= 0x3ffu;
+  v = (v | (v << 16)) & 0x030000ffu;
+  v = (v | (v << 8)) & 0x0300f00fu;
+  v = (v | (v << 4)) & 0x030c30c3u;
+  v = (v | (v << 2)) & 0x09249249u;
+  return v;
+}
+
+}  // namespace
+
+struct nm_ctx {
+  nm_options opt{};
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev[6] = {};
+  int sm_count = 0;
+
+  // surfaces
+  bool has_surfaces = false;
+  int K = 0;
+  std::size_t nt_real = 0, nt_pad = 0, nv = 0;
+  double cx = 0, cy = 0, cz = 0;
+  double lo[3] = {0, 0, 0}, span = 1.0;  // Morton box of the domain
+  nm::LabelIds ids{};
+  DBuf tri, sub, comp_tiles, xyz64, tri_idx, comp_off;
+
+  // scratch
+  DBuf pts, masks, flagmask, order, keys, keys_alt, order_alt, cub_tmp, list, chunk, counters, count, tets, labels,
+      s_out;
+
+  ~nm_ctx() {
+    for (DBuf* b : {&tri, &sub, &comp_tiles, &xyz64, &tri_idx, &comp_off, &pts, &masks, &flagmask, &order, &keys,
+                    &keys_alt, &order_alt, &cub_tmp, &list, &chunk, &counters, &count, &tets, &labels, &s_out})
+      b->release();
+    for (auto& e : ev)
+      if (e) cudaEventDestroy(e);
+    if (stream) cudaStreamDestroy(stream);
+  }
+
+  cudaStream_t pick(void* s) const { return s ? static_cast<cudaStream_t>(s) : stream; }
+};
+
+namespace {
+
+void require_surfaces(const nm_ctx* c) {
+  if (!c) throw Error("null context");
+  if (!c->has_surfaces) throw Error("nm_set_surfaces has not been called");
+}
+
+int grid_for(std::size_t n, int block, int cap) {
+  const std::size_t g = (n + block - 1) / block;
+  return static_cast<int>(std::max<std::size_t>(1, std::min<std::size_t>(g, static_cast<std::size_t>(cap))));
+}
+
+// Ordered compaction of [0,n) under pred into out; count on the device.
+template <class Pred>
+void select(nm_ctx* c, Pred pred, std::size_t n, std::uint32_t* out, std::uint32_t* d_count, cudaStream_t st,
+            std::uint64_t& launches) {
+  const std::size_t nb = std::max<std::size_t>(1, (n + nm::kSelChunk - 1) / nm::kSelChunk);
+  auto* chunk = c->chunk.as<std::uint32_t>(nb);
+  nm::k_select_count<<<static_cast<unsigned>(nb), nm::kSelBlock, 0, st>>>(pred, n, chunk);
+  nm::k_select_scan<<<1, 1024, 0, st>>>(chunk, nb, d_count);
+  nm::k_select_write<<<static_cast<unsigned>(nb), nm::kSelBlock, 0, st>>>(pred, n, chunk, out);
+  NM_CUDA(cudaGetLastError());
+  launches += 3;
+}
+
+constexpr int kPPT = 2;  // points per thread of k_label
+
+// Full node pass on device-resident points: Morton order -> K1 -> compaction
+// of flagged points -> K3. masks/s_out are device pointers.
+void label_nodes_dev(nm_ctx* c, const double* d_pts, std::size_t n, double T, std::uint32_t* d_masks, double* d_s,
+                     cudaStream_t st, nm_stats* stats) {
+  require_surfaces(c);
+  if (!(T > 0.0 && T < 1.0)) throw Error("threshold must lie in (0, 1) (SPEC.md:216)");
+  std::uint64_t launches = 0;
+  auto* counters = c->counters.as<unsigned long long>(8);
+  NM_CUDA(cudaMemsetAsync(counters, 0, 8 * sizeof(unsigned long long), st));
+  if (stats) NM_CUDA(cudaEventRecord(c->ev[0], st));
+  if (n == 0) {
+    if (stats) {
+      std::memset(stats, 0, sizeof *stats);
+      stats->triangles = c->nt_real;
+    }
+    return;
+  }
+  if (n > 0xffffffffull) throw Error("more than 2^32 points in one call");
+  auto* flagmask = c->flagmask.as<std::uint32_t>(n);
+  const std::uint32_t* order = nullptr;
+  if (c->opt.sort_points && n > 1) {
+    auto* keys = c->keys.as<std::uint32_t>(n);
+    auto* keys2 = c->keys_alt.as<std::uint32_t>(n);
+    auto* idx = c->order.as<std::uint32_t>(n);
+    auto* idx2 = c->order_alt.as<std::uint32_t>(n);
+    nm::k_morton_keys<<<grid_for(n, 256, c->sm_count * 16), 256, 0, st>>>(d_pts, n, c->lo[0], c->lo[1], c->lo[2],
+                                                                           1024.0 / c->span, keys, idx);
+    ++launches;
+    cub::DoubleBuffer<std::uint32_t> kb(keys, keys2), vb(idx, idx2);
+    std::size_t tmp = 0;
+    NM_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, kb, vb, static_cast<int>(n), 0, 30, st));
+    void* t = c->cub_tmp.get(tmp);
+    NM_CUDA(cub::DeviceRadixSort::SortPairs(t, tmp, kb, vb, static_cast<int>(n), 0, 30, st));
+    launches += 4;  // CUB onesweep: histogram + 3 passes of 10 bits (library kernels)
+    order = vb.Current();
+  }
+  nm::LabelParams prm{};
+  prm.pts = d_pts;
+  prm.n = n;
+  prm.order = order;
+  prm.tri = static_cast<const float4*>(c->tri.p);
+  prm.sub = static_cast<const float4*>(c->sub.p);
+  prm.comp_tiles = static_cast<const std::uint32_t*>(c->comp_tiles.p);
+  prm.K = c->K;
+  prm.cx = c->cx;
+  prm.cy = c->cy;
+  prm.cz = c->cz;
+  prm.T = T;
+  prm.band = c->opt.band;
+  prm.tau = c->opt.tau;
+  prm.delta = c->opt.delta_mm;
+  prm.masks = d_masks;
+  prm.flagmask = flagmask;
+  prm.s_out = d_s;
+  prm.counters = counters;
+  if (stats) NM_CUDA(cudaEventRecord(c->ev[1], st));
+  const std::size_t per_block = static_cast<std::size_t>(nm::kBlock) * kPPT;
+  nm::k_label<kPPT><<<static_cast<unsigned>((n + per_block - 1) / per_block), nm::kBlock, 0, st>>>(prm);
+  NM_CUDA(cudaGetLastError());
+  ++launches;
+  if (stats) NM_CUDA(cudaEventRecord(c->ev[2], st));
+  // compaction of flagged points + fp64 fix-up
+  auto* list = c->list.as<std::uint32_t>(n);
+  auto* d_count = c->count.as<std::uint32_t>(4);
+  select(c, nm::PredNonzero{flagmask}, n, list, d_count, st, launches);
+  nm::FixupParams fp{};
+  fp.pts = d_pts;
+  fp.list = list;
+  fp.count = d_count;
+  fp.flagmask = flagmask;
+  fp.xyz = static_cast<const double*>(c->xyz64.p);
+  fp.tri = static_cast<const std::uint32_t*>(c->tri_idx.p);
+  fp.comp_off = static_cast<const std::uint32_t*>(c->comp_off.p);
+  fp.K = c->K;
+  fp.T = T;
+  fp.tie_eps = c->opt.tie_eps;
+  fp.masks = d_masks;
+  fp.s_out = d_s;
+  fp.counters = counters;
+  nm::k_fixup<<<c->sm_count * 8, 256, 0, st>>>(fp);
+  NM_CUDA(cudaGetLastError());
+  ++launches;
+  if (stats) {
+    NM_CUDA(cudaEventRecord(c->ev[3], st));
+    unsigned long long h[8];
+    std::uint32_t hc = 0;
+    NM_CUDA(cudaMemcpyAsync(h, counters, sizeof h, cudaMemcpyDeviceToHost, st));
+    NM_CUDA(cudaMemcpyAsync(&hc, d_count, sizeof hc, cudaMemcpyDeviceToHost, st));
+    NM_CUDA(cudaStreamSynchronize(st));
+    std::memset(stats, 0, sizeof *stats);
+    stats->points = n;
+    stats->triangles = c->nt_real;
+    stats->evals = static_cast<std::uint64_t>(n) * c->nt_real;
+    stats->flagged_points = hc;
+    stats->flagged_pairs = h[2];
+    stats->ties = h[3];
+    stats->near_subtiles = h[0];
+    stats->far_subtiles = h[1];
+    stats->launches = launches;
+    NM_CUDA(cudaEventElapsedTime(&stats->ms_label, c->ev[1], c->ev[2]));
+    NM_CUDA(cudaEventElapsedTime(&stats->ms_fixup, c->ev[2], c->ev[3]));
+    NM_CUDA(cudaEventElapsedTime(&stats->ms_total, c->ev[0], c->ev[3]));
+  }
+}
+
+void label_tets_dev(nm_ctx* c, const std::uint32_t* d_tets, std::size_t nt, const std::uint32_t* d_masks, int* d_labels,
+                    cudaStream_t st, nm_stats* stats) {
+  require_surfaces(c);
+  if (nt == 0) return;
+  if (stats) NM_CUDA(cudaEventRecord(c->ev[4], st));
+  nm::k_label_tets<<<grid_for(nt, 256, c->sm_count * 32), 256, 0, st>>>(reinterpret_cast<const uint4*>(d_tets), nt,
+                                                                        d_masks, d_labels, c->ids);
+  NM_CUDA(cudaGetLastError());
+  if (stats) {
+    NM_CUDA(cudaEventRecord(c->ev[5], st));
+    NM_CUDA(cudaEventSynchronize(c->ev[5]));
+    float ms = 0;
+    NM_CUDA(cudaEventElapsedTime(&ms, c->ev[4], c->ev[5]));
+    stats->ms_tets += ms;
+    stats->launches += 1;
+  }
+}
+
+void check_tets(const std::uint32_t* tets, std::size_t nt, std::size_t n_nodes) {
+  for (std::size_t i = 0; i < 4 * nt; ++i)
+    if (tets[i] >= n_nodes) throw Error("tet " + std::to_string(i / 4) + " references node " + std::to_string(tets[i]) +
+                                        " >= node count " + std::to_string(n_nodes));
+}
+
+}  // namespace
+
+extern "C" {
+
+int nm_abi_version(void) { return NM_ABI_VERSION; }
+const char* nm_last_error(void) { return g_err.c_str(); }
+
+void nm_default_options(nm_options* o) {
+  o->device = 0;
+  o->tau = 1e-2f;
+  o->delta_mm = 1e-3f;
+  o->band = 1e-3;
+  o->tie_eps = 1e-9;
+  o->far_ratio = 5.0f;
+  o->far_abs_mm = 0.05f;
+  o->sort_points = 1;
+}
+
+int nm_create(nm_ctx** out, const nm_options* opt) {
+  return guarded([&] {
+    if (!out) throw Error("null output pointer");
+    *out = nullptr;
+    int ndev = 0;
+    const cudaError_t e = cudaGetDeviceCount(&ndev);
+    if (e != cudaSuccess || ndev == 0)
+      throw Error(std::string("no CUDA device available (") + cudaGetErrorString(e) +
+                  "); libnestmesh_label has no CPU fallback");
+    auto* c = new nm_ctx;
+    try {
+      if (opt) c->opt = *opt;
+      else nm_default_options(&c->opt);
+      if (c->opt.device < 0 || c->opt.device >= ndev) throw Error("device ordinal out of range");
+      NM_CUDA(cudaSetDevice(c->opt.device));
+      cudaDeviceProp p;
+      NM_CUDA(cudaGetDeviceProperties(&p, c->opt.device));
+      if (p.major != 10) throw Error(std::string("device ") + p.name + " is not sm_100 (Blackwell B200)");
+      c->sm_count = p.multiProcessorCount;
+      NM_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+      for (auto& ev : c->ev) NM_CUDA(cudaEventCreate(&ev));
+    } catch (...) {
+      delete c;
+      throw;
+    }
+    *out = c;
+  });
+}
+
+int nm_destroy(nm_ctx* c) {
+  return guarded([&] {
+    if (!c) return;
+    cudaSetDevice(c->opt.device);
+    cudaStreamSynchronize(c->stream);
+    delete c;
+  });
+}
+
+int nm_set_surfaces(nm_ctx* c, const double* xyz, std::size_t nv, const std::uint32_t* tri, std::size_t nt,
+                    const std::uint32_t* comp_off, int K, const int* label_ids) {
+  return guarded([&] {
+    if (!c) throw Error("null context");
+    if (K < 1 || K > 32) throw Error("compartment count must be in [1, 32]");
+    if (comp_off[0] != 0 || comp_off[K] != nt) throw Error("comp_tri_off must start at 0 and end at the triangle count");
+    for (int k = 0; k < K; ++k) {
+      if (comp_off[k + 1] < comp_off[k]) throw Error("comp_tri_off must be non-decreasing");
+      if (label_ids[k] <= 0) throw Error("compartment label ids must be > 0 (0 is the bounding box)");
+    }
+    for (std::size_t i = 0; i < 3 * nt; ++i)
+      if (tri[i] >= nv) throw Error("triangle index out of range");
+    NM_CUDA(cudaSetDevice(c->opt.device));
+    // Domain box and centring offset of the fp32 frame.
+    double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
+    for (std::size_t i = 0; i < nv; ++i)
+      for (int a = 0; a < 3; ++a) {
+        lo[a] = std::min(lo[a], xyz[3 * i + a]);
+        hi[a] = std::max(hi[a], xyz[3 * i + a]);
+      }
+    if (nv == 0) lo[0] = lo[1] = lo[2] = hi[0] = hi[1] = hi[2] = 0.0;
+    const double ctr[3] = {0.5 * (lo[0] + hi[0]), 0.5 * (lo[1] + hi[1]), 0.5 * (lo[2] + hi[2])};
+    double span = std::max({hi[0] - lo[0], hi[1] - lo[1], hi[2] - lo[2], 1e-6}) * 1.5;
+    for (int a = 0; a < 3; ++a) c->lo[a] = ctr[a] - 0.5 * span;
+    c->span = span;
+    c->cx = ctr[0];
+    c->cy = ctr[1];
+    c->cz = ctr[2];
+
+    // Per compartment: Morton-sort triangles, pad to whole tiles.
+    std::vector<std::uint32_t> tiles(K + 1, 0);
+    std::vector<std::vector<std::uint32_t>> order(K);
+    for (int k = 0; k < K; ++k) {
+      const std::uint32_t b = comp_off[k], e = comp_off[k + 1];
+      std::vector<std::pair<std::uint32_t, std::uint32_t>> kk;
+      kk.reserve(e - b);
+      for (std::uint32_t t = b; t < e; ++t) {
+        std::uint32_t q[3];
+        for (int a = 0; a < 3; ++a) {
+          const double m = (xyz[3 * tri[3 * t] + a] + xyz[3 * tri[3 * t + 1] + a] + xyz[3 * tri[3 * t + 2] + a]) / 3.0;
+          const double u = (m - c->lo[a]) / span * 1024.0;
+          q[a] = static_cast<std::uint32_t>(std::clamp(u, 0.0, 1023.0));
+        }
+        kk.emplace_back(spread10h(q[0]) | (spread10h(q[1]) << 1) | (spread10h(q[2]) << 2), t);
+      }
+      std::stable_sort(kk.begin(), kk.end(), [](auto& x, auto& y) { return x.first < y.first; });
+      for (auto& p : kk) order[k].push_back(p.second);
+      tiles[k + 1] = tiles[k] + static_cast<std::uint32_t>((e - b + nm::kTile - 1) / nm::kTile);
+    }
+    const std::size_t ntiles = tiles[K];
+    const std::size_t npad = ntiles * nm::kTile;
+    // Tile layout: each 32-triangle subtile carries an fp32
+    // centre c (exactly representable, centred frame) and its triangles'
+    // vertices relative to c, so near-surface geometry keeps ~ulp(radius)
+    // instead of ~ulp(100 mm) precision; the kernel forms p - c in
+    // double-single per subtile.
+    std::vector<float4> htri(3 * npad);
+    std::vector<float4> hsub(ntiles * nm::kSubPerTile);
+    const double far_ratio = c->opt.far_ratio, far_abs = c->opt.far_abs_mm;
+    std::vector<std::array<double, 9>> v64(nm::kSub);
+    std::vector<std::array<double, 3>> n64(nm::kSub);
+    for (int k = 0; k < K; ++k) {
+      const auto& ord = order[k];
+      const std::size_t nreal = ord.size();
+      for (std::uint32_t tl = tiles[k]; tl < tiles[k + 1]; ++tl) {
+        for (int s = 0; s < nm::kSubPerTile; ++s) {
+          const std::size_t r0 = static_cast<std::size_t>(tl - tiles[k]) * nm::kTile + s * nm::kSub;
+          // gather fp64 vertices (centred frame) + normals; pads repeat the
+          // compartment's last real vertex with N = 0 (contributes exactly 0)
+          double blo[3] = {1e300, 1e300, 1e300}, bhi[3] = {-1e300, -1e300, -1e300};
+          for (int j = 0; j < nm::kSub; ++j) {
+            const std::size_t r = r0 + j;
+            if (r < nreal) {
+              const std::uint32_t t = ord[r];
+              const double* A = xyz + 3 * std::size_t(tri[3 * t]);
+              const double* B = xyz + 3 * std::size_t(tri[3 * t + 1]);
+              const double* C = xyz + 3 * std::size_t(tri[3 * t + 2]);
+              const double e1[3] = {B[0] - A[0], B[1] - A[1], B[2] - A[2]};
+              const double e2[3] = {C[0] - A[0], C[1] - A[1], C[2] - A[2]};
+              n64[j] = {e1[1] * e2[2] - e1[2] * e2[1], e1[2] * e2[0] - e1[0] * e2[2], e1[0] * e2[1] - e1[1] * e2[0]};
+              for (int a = 0; a < 3; ++a) {
+                v64[j][a] = A[a] - ctr[a];
+                v64[j][3 + a] = B[a] - ctr[a];
+                v64[j][6 + a] = C[a] - ctr[a];
+              }
+            } else {
+              const std::uint32_t t = nreal ? ord[nreal - 1] : 0u;
+              const double* A = nreal ? xyz + 3 * std::size_t(tri[3 * t]) : ctr;
+              n64[j] = {0.0, 0.0, 0.0};
+              for (int v = 0; v < 3; ++v)
+                for (int a = 0; a < 3; ++a) v64[j][3 * v + a] = A[a] - ctr[a];
+            }
+            for (int v = 0; v < 3; ++v)
+              for (int a = 0; a < 3; ++a) {
+                blo[a] = std::min(blo[a], v64[j][3 * v + a]);
+                bhi[a] = std::max(bhi[a], v64[j][3 * v + a]);
+              }
+          }
+          const float fc[3] = {float(0.5 * (blo[0] + bhi[0])), float(0.5 * (blo[1] + bhi[1])),
+                               float(0.5 * (blo[2] + bhi[2]))};
+          double rho = 0.0;
+          for (int j = 0; j < nm::kSub; ++j) {
+            float q[9];
+            for (int v = 0; v < 3; ++v)
+              for (int a = 0; a < 3; ++a) q[3 * v + a] = float(v64[j][3 * v + a] - double(fc[a]));
+            for (int v = 0; v < 3; ++v)
+              rho = std::max(rho, std::sqrt(double(q[3 * v]) * q[3 * v] + double(q[3 * v + 1]) * q[3 * v + 1] +
+                                            double(q[3 * v + 2]) * q[3 * v + 2]));
+            float4* o = &htri[3 * (static_cast<std::size_t>(tl) * nm::kTile + s * nm::kSub + j)];
+            o[0] = make_float4(q[0], q[1], q[2], float(n64[j][0]));
+            o[1] = make_float4(q[3], q[4], q[5], float(n64[j][1]));
+            o[2] = make_float4(q[6], q[7], q[8], float(n64[j][2]));
+          }
+          const double R = (far_ratio * rho + far_abs) * (1.0 + 1e-5);
+          hsub[static_cast<std::size_t>(tl) * nm::kSubPerTile + s] = make_float4(fc[0], fc[1], fc[2], float(R * R));
+        }
+      }
+    }
+    c->has_surfaces = false;
+    auto up = [&](DBuf& b, const void* src, std::size_t bytes) {
+      void* d = b.get(bytes);
+      if (bytes) NM_CUDA(cudaMemcpyAsync(d, src, bytes, cudaMemcpyHostToDevice, c->stream));
+    };
+    up(c->tri, htri.data(), htri.size() * sizeof(float4));
+    up(c->sub, hsub.data(), hsub.size() * sizeof(float4));
+    up(c->comp_tiles, tiles.data(), tiles.size() * sizeof(std::uint32_t));
+    up(c->xyz64, xyz, nv * 3 * sizeof(double));
+    up(c->tri_idx, tri, nt * 3 * sizeof(std::uint32_t));
+    up(c->comp_off, comp_off, (K + 1) * sizeof(std::uint32_t));
+    NM_CUDA(cudaStreamSynchronize(c->stream));
+    c->K = K;
+    c->nt_real = nt;
+    c->nt_pad = npad;
+    c->nv = nv;
+    for (int k = 0; k < 32; ++k) c->ids.id[k] = k < K ? label_ids[k] : 0;
+    c->has_surfaces = true;
+  });
+}
+
+int nm_surface_info(nm_ctx* c, int* K, std::size_t* triangles, std::size_t* padded) {
+  return guarded([&] {
+    require_surfaces(c);
+    if (K) *K = c->K;
+    if (triangles) *triangles = c->nt_real;
+    if (padded) *padded = c->nt_pad;
+  });
+}
+
+int nm_label_nodes_device(nm_ctx* c, const double* d_pts, std::size_t n, double T, std::uint32_t* d_masks,
+                          double* d_s, void* stream, nm_stats* stats) {
+  return guarded([&] {
+    require_surfaces(c);
+    NM_CUDA(cudaSetDevice(c->opt.device));
+    label_nodes_dev(c, d_pts, n, T, d_masks, d_s, c->pick(stream), stats);
+  });
+}
+
+int nm_label_tets_device(nm_ctx* c, const std::uint32_t* d_tets, std::size_t nt, const std::uint32_t* d_masks,
+                         int* d_labels, void* stream, nm_stats* stats) {
+  return guarded([&] {
+    require_surfaces(c);
+    NM_CUDA(cudaSetDevice(c->opt.device));
+    label_tets_dev(c, d_tets, nt, d_masks, d_labels, c->pick(stream), stats);
+  });
+}
+
+int nm_flag_boundary_device(nm_ctx* c, const std::uint32_t* d_tets, std::size_t nt, const std::uint32_t* d_masks,
+                            std::uint32_t active, std::uint32_t* d_ids, std::uint32_t* d_count, void* stream) {
+  return guarded([&] {
+    require_surfaces(c);
+    NM_CUDA(cudaSetDevice(c->opt.device));
+    std::uint64_t l = 0;
+    select(c, nm::PredStraddle{reinterpret_cast<const uint4*>(d_tets), d_masks, active}, nt, d_ids, d_count,
+           c->pick(stream), l);
+  });
+}
+
+int nm_label_nodes(nm_ctx* c, const double* pts, std::size_t n, double T, std::uint32_t* masks_out, nm_stats* stats) {
+  return guarded([&] {
+    require_surfaces(c);
+    NM_CUDA(cudaSetDevice(c->opt.device));
+    auto* d_pts = c->pts.as<double>(3 * std::max<std::size_t>(n, 1));
+    auto* d_masks = c->masks.as<std::uint32_t>(std::max<std::size_t>(n, 1));
+    if (n) NM_CUDA(cudaMemcpyAsync(d_pts, pts, 3 * n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    label_nodes_dev(c, d_pts, n, T, d_masks, nullptr, c->stream, stats);
+    if (n) NM_CUDA(cudaMemcpyAsync(masks_out, d_masks, n * sizeof(std::uint32_t), cudaMemcpyDeviceToHost, c->stream));
+    NM_CUDA(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int nm_enclosure(nm_ctx* c, const double* pts, std::size_t n, double T, double* s_out, nm_stats* stats) {
+  return guarded([&] {
+    require_surfaces(c);
+    NM_CUDA(cudaSetDevice(c->opt.device));
+    auto* d_pts = c->pts.as<double>(3 * std::max<std::size_t>(n, 1));
+    auto* d_masks = c->masks.as<std::uint32_t>(std::max<std::size_t>(n, 1));
+    auto* d_s = c->s_out.as<double>(std::max<std::size_t>(n * c->K, 1));
+    if (n) NM_CUDA(cudaMemcpyAsync(d_pts, pts, 3 * n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    label_nodes_dev(c, d_pts, n, T, d_masks, d_s, c->stream, stats);
+    if (n) NM_CUDA(cudaMemcpyAsync(s_out, d_s, n * c->K * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    NM_CUDA(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int nm_label_tets(nm_ctx* c, const std::uint32_t* tets, std::size_t nt, const std::uint32_t* masks,
+                  std::size_t n_nodes, int* labels_out, nm_stats* stats) {
+  return guarded([&] {
+    require_surfaces(c);
+    check_tets(tets, nt, n_nodes);
+    NM_CUDA(cudaSetDevice(c->opt.device));
+    if (stats) std::memset(stats, 0, sizeof *stats);
+    auto* d_tets = c->tets.as<std::uint32_t>(4 * std::max<std::size_t>(nt, 1));
+    auto* d_masks = c->masks.as<std::uint32_t>(std::max<std::size_t>(n_nodes, 1));
+    auto* d_labels = c->labels.as<int>(std::max<std::size_t>(nt, 1));
+    if (nt) NM_CUDA(cudaMemcpyAsync(d_tets, tets, 4 * nt * sizeof(std::uint32_t), cudaMemcpyHostToDevice, c->stream));
+    if (n_nodes) NM_CUDA(cudaMemcpyAsync(d_masks, masks, n_nodes * sizeof(std::uint32_t), cudaMemcpyHostToDevice, c->stream));
+    label_tets_dev(c, d_tets, nt, d_masks, d_labels, c->stream, stats);
+    if (nt) NM_CUDA(cudaMemcpyAsync(labels_out, d_labels, nt * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    NM_CUDA(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int nm_label_mesh(nm_ctx* c, const double* nodes, std::size_t n, const std::uint32_t* tets, std::size_t nt, double T,
+                  int* labels_out, std::uint32_t* masks_out, nm_stats* stats) {
+  return guarded([&] {
+    require_surfaces(c);
+    check_tets(tets, nt, n);
+    NM_CUDA(cudaSetDevice(c->opt.device));
+    auto* d_pts = c->pts.as<double>(3 * std::max<std::size_t>(n, 1));
+    auto* d_masks = c->masks.as<std::uint32_t>(std::max<std::size_t>(n, 1));
+    auto* d_tets = c->tets.as<std::uint32_t>(4 * std::max<std::size_t>(nt, 1));
+    auto* d_labels = c->labels.as<int>(std::max<std::size_t>(nt, 1));
+    if (n) NM_CUDA(cudaMemcpyAsync(d_pts, nodes, 3 * n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    if (nt) NM_CUDA(cudaMemcpyAsync(d_tets, tets, 4 * nt * sizeof(std::uint32_t), cudaMemcpyHostToDevice, c->stream));
+    label_nodes_dev(c, d_pts, n, T, d_masks, nullptr, c->stream, stats);
+    label_tets_dev(c, d_tets, nt, d_masks, d_labels, c->stream, stats);
+    if (nt) NM_CUDA(cudaMemcpyAsync(labels_out, d_labels, nt * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    if (masks_out && n)
+      NM_CUDA(cudaMemcpyAsync(masks_out, d_masks, n * sizeof(std::uint32_t), cudaMemcpyDeviceToHost, c->stream));
+    NM_CUDA(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int nm_flag_boundary(nm_ctx* c, const std::uint32_t* tets, std::size_t nt, const std::uint32_t* masks,
+                     std::size_t n_nodes, std::uint32_t active, std::uint32_t* ids_out, std::size_t* count) {
+  return guarded([&] {
+    require_surfaces(c);
+    check_tets(tets, nt, n_nodes);
+    NM_CUDA(cudaSetDevice(c->opt.device));
+    auto* d_tets = c->tets.as<std::uint32_t>(4 * std::max<std::size_t>(nt, 1));
+    auto* d_masks = c->masks.as<std::uint32_t>(std::max<std::size_t>(n_nodes, 1));
+    auto* d_ids = c->list.as<std::uint32_t>(std::max<std::size_t>(nt, 1));
+    auto* d_count = c->count.as<std::uint32_t>(4);
+    if (nt) NM_CUDA(cudaMemcpyAsync(d_tets, tets, 4 * nt * sizeof(std::uint32_t), cudaMemcpyHostToDevice, c->stream));
+    if (n_nodes) NM_CUDA(cudaMemcpyAsync(d_masks, masks, n_nodes * sizeof(std::uint32_t), cudaMemcpyHostToDevice, c->stream));
+    std::uint64_t l = 0;
+    select(c, nm::PredStraddle{reinterpret_cast<const uint4*>(d_tets), d_masks, active}, nt, d_ids, d_count, c->stream, l);
+    std::uint32_t hc = 0;
+    NM_CUDA(cudaMemcpyAsync(&hc, d_count, sizeof hc, cudaMemcpyDeviceToHost, c->stream));
+    NM_CUDA(cudaStreamSynchronize(c->stream));
+    if (hc) NM_CUDA(cudaMemcpy(ids_out, d_ids, hc * sizeof(std::uint32_t), cudaMemcpyDeviceToHost));
+    *count = hc;
+  });
+}
+
+int nm_relabel(nm_ctx* c, const double*, std::size_t, const std::uint32_t*, std::size_t, double, int, int*, int*, int*,
+               std::uint8_t*, nm_stats*) {
+  return guarded([&] {
+    require_surfaces(c);
+    throw Error("nm_relabel: not implemented yet");
+  });
+}
+
+}  // extern "C"
