@@ -1,0 +1,367 @@
+#!/usr/bin/env python
+"""Bench: point-triangle solid-angle evaluations/s and full-mesh labeling time
+on B200 (BASELINE.json `metric`), one process per GPU.
+
+Workload (default `--config 5`, BASELINE.json configs[4], the config the
+metric is quoted on at 1/2/4/8 B200): 12 compartments x icosphere L6
+(983,040 triangles) over a 215^3-cell regular lattice (10,077,696 nodes,
+49,691,875 tets), T = 0.5. One "step" = one full initial_label of that mesh:
+Morton order -> fp32 solid-angle kernel -> flagged-point compaction -> fp64
+fix-up -> NCCL all-gather of node masks (N > 1) -> tet labels.
+
+  value      whole-job evals/s with nodes/tets resident in HBM
+  e2e        same metric through the public host-buffer API (nm_label_mesh at
+             N = 1; pinned host shards + H2D + label + D2H per rank at N > 1)
+  roofline   the solid-angle kernel (k_label) against the FP32-pipe roofline
+             148 SMs x 128 lanes x 1.965 GHz / 57 ops per eval
+  cpu_baseline  the fp64 oracle (oracle/, a port of SPEC.md:225-237) on a
+             seeded node sample with every host thread (rank 0, N = 1 only)
+
+`--impl reference` times that CPU implementation alone (rank 0; other ranks
+exit 0) on the same metric/config, each step a bounded node sample.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "point-triangle solid-angle evals/sec and full-mesh labeling time at 1/2/4/8 B200"
+UNIT = "evals/s"
+OPS_PER_EVAL = 57                      # pinned FP32-pipe cost of one VOS eval
+FP32_LANES_PER_SM = 128
+MY_KERNELS_PER_STEP = 7                # morton keys, k_label, 3x select, k_fixup, k_label_tets
+
+
+def measured_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    try:
+        return json.loads(p.read_text())
+    except Exception:
+        return {}
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+        self.t = threading.Thread(target=self._read, daemon=True)
+        self.t.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 9:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            try:
+                sm.append(float(r[1]))
+                mx.append(float(r[2]))
+            except ValueError:
+                continue
+            for nm_, v in zip(names, r[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm_)
+        loaded = [v for v in sm if v > 500] or sm
+        return {"sm_mhz": statistics.median(loaded) if loaded else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, local, world
+
+
+def cpu_baseline(nodes, surfaces, target_s=15.0, seed=0):
+    """fp64 oracle (port of SPEC.md:225-237) on a seeded node sample, all threads."""
+    import oracle
+    cores = oracle.workers_default()
+    T = surfaces.n_triangles
+    rng = np.random.default_rng(seed)
+    probe = nodes[rng.choice(nodes.shape[0], 16, replace=False)]
+    t0 = time.perf_counter()
+    oracle.label_nodes(probe, surfaces, workers=cores)
+    rate = 16 * T / max(time.perf_counter() - t0, 1e-6)
+    n_s = int(np.clip(rate * target_s / T, cores, 200000))
+    sample = nodes[np.sort(rng.choice(nodes.shape[0], n_s, replace=False))]
+    t0 = time.perf_counter()
+    oracle.label_nodes(sample, surfaces, workers=cores)
+    dt = time.perf_counter() - t0
+    return {"value": n_s * T / dt, "unit": UNIT, "cores": cores, "kind": "port",
+            "sample": f"{n_s} seeded-random lattice nodes x all {T} triangles "
+                      f"({n_s / nodes.shape[0]:.2e} of the node set), fp64 VOS oracle, {dt:.1f} s"}
+
+
+def run_reference(args):
+    rank, local, world = dist_env()
+    if rank != 0:
+        return 0
+    from paper_2203_10000_b200 import synth
+    import oracle
+    cfg = synth.config(args.config)
+    S = cfg.surfaces
+    nodes = cfg.lattice_nodes()
+    cores = oracle.workers_default()
+    T = S.n_triangles
+    rng = np.random.default_rng(1)
+    probe = nodes[rng.choice(nodes.shape[0], 16, replace=False)]
+    t0 = time.perf_counter()
+    oracle.label_nodes(probe, S, workers=cores)
+    rate = 16 * T / max(time.perf_counter() - t0, 1e-6)
+    n_s = int(np.clip(rate * args.ref_step_s / T, cores, 200000))
+    samples = [nodes[np.sort(rng.choice(nodes.shape[0], n_s, replace=False))] for _ in range(args.warmup + args.steps)]
+    for i in range(args.warmup):
+        oracle.label_nodes(samples[i], S, workers=cores)
+    times = []
+    for i in range(args.steps):
+        t0 = time.perf_counter()
+        oracle.label_nodes(samples[args.warmup + i], S, workers=cores)
+        times.append(time.perf_counter() - t0)
+    ms = 1e3 * sum(times) / len(times)
+    value = n_s * T / (ms / 1e3)
+    sample = (f"{n_s} seeded-random lattice nodes x all {T} triangles per step "
+              f"({n_s / nodes.shape[0]:.2e} of the node set), fp64 VOS oracle (port of SPEC.md:225-237), {cores} threads")
+    full_s = nodes.shape[0] * T / value
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic", "config": workload_config(cfg, nodes.shape[0], 5 * int(np.prod(cfg.n)), world),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "full_mesh_labeling_time_s_extrapolated": full_s,
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def workload_config(cfg, n_nodes, n_tets, world):
+    S = cfg.surfaces
+    names = {1: "cfg1 icosphere L3 / 32^3 lattice", 2: "cfg2 4 nested perturbed spheres / 2 mm lattice",
+             3: "cfg3 20-compartment head model / 1 mm lattice", 5: "cfg5 large sweep: 12 x icosphere L6 / 215^3 lattice"}
+    return {"workload": names.get(cfg.id, f"cfg{cfg.id}"), "nodes": n_nodes, "tets": n_tets,
+            "triangles": S.n_triangles, "compartments": S.K, "threshold": 0.5, "cell_mm": cfg.h,
+            "parallelism": f"dp{world} (contiguous node shards, NCCL all-gather of uint32 node masks, tet shards)",
+            "l2": "256 MiB L2 flush between steps; nodes+tets (1.04 GB at cfg5) exceed the 126 MB L2",
+            "evals_per_step": n_nodes * S.n_triangles}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", type=int, default=5, choices=[1, 2, 3, 5])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--ref-step-s", type=float, default=4.0)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    rank, local, world = dist_env()
+    if world != args.gpus and rank == 0:
+        print(f"[bench] note: WORLD_SIZE={world} but --gpus={args.gpus}; using WORLD_SIZE", file=sys.stderr)
+    torch.cuda.set_device(local)
+    group = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2203_10000_b200 import synth
+    from paper_2203_10000_b200._native import Context
+    from paper_2203_10000_b200.distributed import all_gather_masks, shard
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+
+    def allmax(x):
+        if world == 1:
+            return x
+        import torch.distributed as dist
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    cfg = synth.config(args.config)
+    S = cfg.surfaces
+    t0 = time.perf_counter()
+    nodes, tets = cfg.lattice_mesh()
+    gen_s = time.perf_counter() - t0
+    n, nt = nodes.shape[0], tets.shape[0]
+    T = S.n_triangles
+    evals_total = n * T
+    nsh, tsh = shard(n, world, rank), shard(nt, world, rank)
+
+    ctx = Context(local)
+    ctx.set_surfaces(S.xyz, S.tri, S.comp_off, S.label_ids)
+    stream = torch.cuda.current_stream()
+    sptr = stream.cuda_stream
+
+    d_nodes = torch.from_numpy(nodes[nsh.lo:nsh.hi]).cuda()
+    d_tets = torch.from_numpy(np.ascontiguousarray(tets[tsh.lo:tsh.hi]).view(np.int32)).cuda()
+    d_masks = torch.zeros(nsh.per, dtype=torch.int32, device="cuda")
+    d_labels = torch.empty(tsh.size, dtype=torch.int32, device="cuda")
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.int32, device="cuda")  # 256 MiB > 126 MB L2
+
+    last = {}
+
+    def step():
+        st = ctx.label_nodes_device(d_nodes, d_masks[: nsh.size], stream=sptr, stats=True)
+        masks = all_gather_masks(d_masks, nsh, group)
+        ctx.label_tets_device(d_tets, masks, d_labels, stream=sptr, stats=False)
+        last.update(st)
+        return st
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    sampler = ClockSampler(local)
+    sampler.start()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    ms_label = []
+    barrier()
+    torch.cuda.synchronize()
+    w0 = time.perf_counter()
+    for i in range(args.steps):
+        flush.fill_(i)
+        ev[i][0].record(stream)
+        st = step()
+        ev[i][1].record(stream)
+        ms_label.append(st["ms_label"])
+    torch.cuda.synchronize()
+    barrier()
+    wall = time.perf_counter() - w0
+    clocks = sampler.stop()
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    ms_per_step = allmax(sum(step_ms) / len(step_ms))
+    value = evals_total / (ms_per_step / 1e3)
+    k_ms = sum(ms_label) / len(ms_label)
+    achieved = nsh.size * T / (k_ms / 1e3)
+
+    # ---- e2e through the public host-buffer API ------------------------------
+    e2e = None
+    if not args.no_e2e:
+        h_nodes = torch.from_numpy(np.ascontiguousarray(nodes[nsh.lo:nsh.hi])).pin_memory()
+        h_tets = torch.from_numpy(np.ascontiguousarray(tets[tsh.lo:tsh.hi]).view(np.int32)).pin_memory()
+        h_labels = torch.empty(tsh.size, dtype=torch.int32).pin_memory()
+        if world == 1:
+            def e2e_step():
+                labels, _, _ = ctx.label_mesh(h_nodes.numpy(), h_tets.numpy().view(np.uint32))
+                return labels
+        else:
+            def e2e_step():
+                dn = h_nodes.cuda(non_blocking=True)
+                dt = h_tets.cuda(non_blocking=True)
+                dm = torch.zeros(nsh.per, dtype=torch.int32, device="cuda")
+                ctx.label_nodes_device(dn, dm[: nsh.size], stream=sptr, stats=False)
+                masks = all_gather_masks(dm, nsh, group)
+                dl = torch.empty(tsh.size, dtype=torch.int32, device="cuda")
+                ctx.label_tets_device(dt, masks, dl, stream=sptr, stats=False)
+                h_labels.copy_(dl)
+                return h_labels
+        e2e_step()
+        torch.cuda.synchronize()
+        barrier()
+        times = []
+        for i in range(args.steps):
+            flush.fill_(i)
+            torch.cuda.synchronize()
+            barrier()
+            t0 = time.perf_counter()
+            e2e_step()
+            torch.cuda.synchronize()
+            times.append(time.perf_counter() - t0)
+        e_ms = allmax(1e3 * sum(times) / len(times))
+        e2e = {"value": evals_total / (e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": n * 24 + nt * 16,
+               "d2h_bytes_per_step": nt * 4, "ms_per_step": e_ms,
+               "path": "nm_label_mesh (C ABI, host buffers)" if world == 1 else
+                       "pinned host shards -> nm_label_nodes_device -> NCCL all-gather -> nm_label_tets_device -> D2H"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(nodes, S, target_s=args.cpu_seconds)
+
+    if rank == 0:
+        peaks = measured_peaks()
+        sm_max = float(peaks.get("sm_max_mhz", 1965.0))
+        import torch as _t
+        sms = _t.cuda.get_device_properties(local).multi_processor_count
+        peak = sms * FP32_LANES_PER_SM * sm_max * 1e6 / OPS_PER_EVAL
+        roof = {
+            "bound": "fp32", "kernel": "k_label<2> (fp32 VOS tile loop)", "achieved": achieved, "peak": peak,
+            "unit": "evals/s", "frac": achieved / peak, "traffic": None,
+            "peak_basis": f"{sms} SMs x {FP32_LANES_PER_SM} FP32 lanes x {sm_max:.0f} MHz (MEASURED_PEAKS.json sm_max_mhz)"
+                          f" / {OPS_PER_EVAL} FP32-pipe ops per eval (SURVEY.md §8d); per GPU",
+            "kernel_ms_avg": k_ms, "kernel_share_of_step": k_ms / (sum(step_ms) / len(step_ms)),
+        }
+        if clocks.get("sm_mhz"):
+            roof["frac_at_measured_clock"] = achieved / (sms * FP32_LANES_PER_SM * clocks["sm_mhz"] * 1e6 / OPS_PER_EVAL)
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "fp32 (fp64 tile fold + fp64 fix-up)", "data": "synthetic",
+            "config": workload_config(cfg, n, nt, world),
+            "full_mesh_labeling_time_s": ms_per_step / 1e3,
+            "e2e": e2e, "roofline": roof, "cpu_baseline": cpu, "clocks": clocks,
+            "gpu_launches": MY_KERNELS_PER_STEP * args.steps,
+            "labeling_stats_last_step": {k: last[k] for k in ("flagged_points", "flagged_pairs", "ties", "near_subtiles",
+                                                              "far_subtiles", "ms_label", "ms_fixup")},
+            "lattice_generation_s": gen_s, "timed_wall_s": wall,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+    ctx.close()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

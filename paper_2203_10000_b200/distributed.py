@@ -1,0 +1,90 @@
+"""Multi-GPU point partitioner: one process per GPU.
+
+Query points (mesh nodes) are split into equal contiguous shards, one per
+rank; the surface set is replicated on every rank. The single exchange step
+is an all-gather of the per-node uint32 inside masks (NCCL over NVLink on the
+GPU box, gloo in the CPU tests), after which every rank labels its own
+contiguous range of tets. Because each node's result is a pure function of its
+position the gathered masks, and hence the labels, are identical
+for any world size.
+
+The per-rank compute is injected (``node_fn`` / ``tet_fn``) so the CPU tests
+can exercise exactly this sharding + gather logic with the oracle as the
+per-rank checker, while the GPU path plugs in the CUDA entry points.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+
+@dataclass(frozen=True)
+class Shard:
+    rank: int
+    world: int
+    n: int          # global item count
+    per: int        # padded shard length (equal on every rank)
+    lo: int         # first global item of this rank
+    hi: int         # one past the last real item of this rank
+
+    @property
+    def size(self) -> int:
+        return self.hi - self.lo
+
+    @property
+    def padded_total(self) -> int:
+        return self.per * self.world
+
+
+def shard(n: int, world: int, rank: int) -> Shard:
+    """Equal contiguous shards; the tail rank(s) are padded so the all-gather
+    moves equal-sized buffers."""
+    if world < 1 or not (0 <= rank < world):
+        raise ValueError("bad rank/world")
+    per = (n + world - 1) // world if n else 0
+    lo = min(n, rank * per)
+    hi = min(n, lo + per)
+    return Shard(rank, world, n, per, lo, hi)
+
+
+def all_gather_masks(local: "torch.Tensor", sh: Shard, group=None) -> "torch.Tensor":
+    """Gather equal-length (padded) mask shards into one (n,) tensor."""
+    import torch
+    import torch.distributed as dist
+    buf = local
+    if local.shape[0] != sh.per:
+        buf = torch.zeros(sh.per, dtype=local.dtype, device=local.device)
+        buf[: local.shape[0]] = local
+    out = torch.empty(sh.padded_total, dtype=local.dtype, device=local.device)
+    if sh.world == 1:
+        out.copy_(buf)
+    else:
+        dist.all_gather_into_tensor(out, buf, group=group)
+    return out[: sh.n]
+
+
+def label_mesh_sharded(nodes, tets, node_fn, tet_fn, rank: int, world: int, group=None, device="cpu"):
+    """initial_label over `world` ranks.
+
+    nodes: (N,3) float64 (host, every rank may hold the full array or only its
+    shard — only rows [lo, hi) are read); tets: (T,4) uint32.
+    node_fn(points (n,3) f64 torch) -> masks (n,) int32 torch on `device`.
+    tet_fn(tets (t,4) torch, masks (N,) torch) -> labels (t,) int32 torch.
+    Returns (labels of this rank's tet range, tet shard, full masks).
+    """
+    import torch
+    n = nodes.shape[0]
+    nsh = shard(n, world, rank)
+    pts = torch.as_tensor(np.ascontiguousarray(nodes[nsh.lo:nsh.hi]), dtype=torch.float64, device=device)
+    local = node_fn(pts)
+    masks = all_gather_masks(local, nsh, group)
+    tsh = shard(tets.shape[0], world, rank)
+    t = torch.as_tensor(np.ascontiguousarray(tets[tsh.lo:tsh.hi]).view(np.int32), device=device)
+    labels = tet_fn(t, masks)
+    return labels, tsh, masks
+
+
+def gather_labels(labels: "torch.Tensor", sh: Shard, group=None) -> "torch.Tensor":
+    """All-gather per-rank tet label ranges into the full (T,) label vector."""
+    return all_gather_masks(labels, sh, group)
