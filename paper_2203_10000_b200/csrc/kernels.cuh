@@ -46,15 +46,18 @@ struct LabelParams {
   unsigned long long* counters;  // [0] near subtile visits, [1] far subtile visits
 };
 
-template <int P>
+// NP point pairs per thread (2*NP points), packed fp32x2 arithmetic.
+template <int NP>
 __global__ void __launch_bounds__(kBlock) k_label(const LabelParams prm) {
+  constexpr int P = 2 * NP;
   __shared__ float4 s_tri[kTile * 3];
   __shared__ float4 s_sub[kSubPerTile];
 
   const std::size_t base = (static_cast<std::size_t>(blockIdx.x) * kBlock + threadIdx.x) * P;
-  // Point in the centred frame as a double-single (hi + lo); per subtile the
-  // kernel forms p - c = (hi - c) + lo, exact up to one rounding of |p - c|.
-  float hx[P], hy[P], hz[P], lx[P], ly[P], lz[P];
+  // Points in the centred frame as double-singles (hi + lo), packed in pairs;
+  // per subtile the kernel forms p - c = (hi - c) + lo, exact up to one
+  // rounding of |p - c| (near-surface geometry keeps ~ulp(|p - c|)).
+  float2 hx[NP], hy[NP], hz[NP], lx[NP], ly[NP], lz[NP];
   std::size_t pid[P];
   bool valid[P];
 #pragma unroll
@@ -65,12 +68,15 @@ __global__ void __launch_bounds__(kBlock) k_label(const LabelParams prm) {
     const std::size_t j = prm.order ? prm.order[ii] : ii;
     pid[k] = j;
     const double dx = prm.pts[3 * j] - prm.cx, dy = prm.pts[3 * j + 1] - prm.cy, dz = prm.pts[3 * j + 2] - prm.cz;
-    hx[k] = static_cast<float>(dx);
-    hy[k] = static_cast<float>(dy);
-    hz[k] = static_cast<float>(dz);
-    lx[k] = static_cast<float>(dx - hx[k]);
-    ly[k] = static_cast<float>(dy - hy[k]);
-    lz[k] = static_cast<float>(dz - hz[k]);
+    const float fx = static_cast<float>(dx), fy = static_cast<float>(dy), fz = static_cast<float>(dz);
+    const float gx = static_cast<float>(dx - fx), gy = static_cast<float>(dy - fy), gz = static_cast<float>(dz - fz);
+    if (k & 1) {
+      hx[k >> 1].y = fx; hy[k >> 1].y = fy; hz[k >> 1].y = fz;
+      lx[k >> 1].y = gx; ly[k >> 1].y = gy; lz[k >> 1].y = gz;
+    } else {
+      hx[k >> 1].x = fx; hy[k >> 1].x = fy; hz[k >> 1].x = fz;
+      lx[k >> 1].x = gx; ly[k >> 1].x = gy; lz[k >> 1].x = gz;
+    }
   }
   std::uint32_t mask[P], fmask[P];
 #pragma unroll
@@ -92,22 +98,27 @@ __global__ void __launch_bounds__(kBlock) k_label(const LabelParams prm) {
       const float4* gt = prm.tri + static_cast<std::size_t>(tile) * kTile * 3;
 #pragma unroll
       for (int i = threadIdx.x; i < kTile * 3; i += kBlock) s_tri[i] = __ldg(gt + i);
-      if (threadIdx.x < kSubPerTile) s_sub[threadIdx.x] = __ldg(prm.sub + static_cast<std::size_t>(tile) * kSubPerTile + threadIdx.x);
+      if (threadIdx.x < kSubPerTile)
+        s_sub[threadIdx.x] = __ldg(prm.sub + static_cast<std::size_t>(tile) * kSubPerTile + threadIdx.x);
       __syncthreads();
 
-      float acc[P];
+      float2 acc[NP];
 #pragma unroll
-      for (int k = 0; k < P; ++k) acc[k] = 0.0f;
+      for (int q = 0; q < NP; ++q) acc[q] = make_float2(0.0f, 0.0f);
       for (int st = 0; st < kSubPerTile; ++st) {
         const float4 sb = s_sub[st];
-        float px[P], py[P], pz[P];
+        float2 mx[NP], my[NP], mz[NP];  // -(p - c)
         bool far = true;
 #pragma unroll
-        for (int k = 0; k < P; ++k) {
-          px[k] = __fadd_rn(__fsub_rn(hx[k], sb.x), lx[k]);
-          py[k] = __fadd_rn(__fsub_rn(hy[k], sb.y), ly[k]);
-          pz[k] = __fadd_rn(__fsub_rn(hz[k], sb.z), lz[k]);
-          far &= (!valid[k]) || (px[k] * px[k] + py[k] * py[k] + pz[k] * pz[k] > sb.w);
+        for (int q = 0; q < NP; ++q) {
+          const float2 px = add2(add2(hx[q], bc(-sb.x)), lx[q]);
+          const float2 py = add2(add2(hy[q], bc(-sb.y)), ly[q]);
+          const float2 pz = add2(add2(hz[q], bc(-sb.z)), lz[q]);
+          mx[q] = make_float2(-px.x, -px.y);
+          my[q] = make_float2(-py.x, -py.y);
+          mz[q] = make_float2(-pz.x, -pz.y);
+          const float2 d2 = fma2(pz, pz, fma2(py, py, mul2(px, px)));
+          far &= (!valid[2 * q] || d2.x > sb.w) && (!valid[2 * q + 1] || d2.y > sb.w);
         }
         const float4* tt = s_tri + st * kSub * 3;
         if (__all_sync(kFull, far)) {
@@ -116,26 +127,33 @@ __global__ void __launch_bounds__(kBlock) k_label(const LabelParams prm) {
           for (int t = 0; t < kSub; ++t) {
             const float4 A = tt[3 * t], B = tt[3 * t + 1], C = tt[3 * t + 2];
 #pragma unroll
-            for (int k = 0; k < P; ++k) {
-              const VosTerms v = vos_terms(A, B, C, px[k], py[k], pz[k]);
-              acc[k] = acc_far(acc[k], v.num, v.den);
+            for (int q = 0; q < NP; ++q) {
+              const VosTerms2 v = vos_terms2(A, B, C, mx[q], my[q], mz[q]);
+              acc[q] = acc_far2(acc[q], v.num, v.den);
             }
           }
         } else {
           ++n_near;
-#pragma unroll 2
+#pragma unroll 1
           for (int t = 0; t < kSub; ++t) {
             const float4 A = tt[3 * t], B = tt[3 * t + 1], C = tt[3 * t + 2];
 #pragma unroll
-            for (int k = 0; k < P; ++k) {
-              const VosTerms v = vos_terms(A, B, C, px[k], py[k], pz[k]);
-              acc[k] = acc_near(acc[k], v, prm.tau, prm.delta, det[k]);
+            for (int q = 0; q < NP; ++q) {
+              const VosTerms2 v = vos_terms2(A, B, C, mx[q], my[q], mz[q]);
+              const float2 af = acc_far2(acc[q], v.num, v.den);
+              acc[q].x = acc_near_lane(acc[q].x, af.x, v.num.x, v.den.x, v.r1.x, v.r2.x, v.r3.x, prm.tau, prm.delta,
+                                       det[2 * q]);
+              acc[q].y = acc_near_lane(acc[q].y, af.y, v.num.y, v.den.y, v.r1.y, v.r2.y, v.r3.y, prm.tau, prm.delta,
+                                       det[2 * q + 1]);
             }
           }
         }
       }
 #pragma unroll
-      for (int k = 0; k < P; ++k) acc64[k] += static_cast<double>(acc[k]);
+      for (int q = 0; q < NP; ++q) {
+        acc64[2 * q] += static_cast<double>(acc[q].x);
+        acc64[2 * q + 1] += static_cast<double>(acc[q].y);
+      }
     }
 #pragma unroll
     for (int k = 0; k < P; ++k) {

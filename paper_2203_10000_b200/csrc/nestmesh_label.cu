@@ -145,7 +145,8 @@ void select(nm_ctx* c, Pred pred, std::size_t n, std::uint32_t* out, std::uint32
   launches += 3;
 }
 
-constexpr int kPPT = 2;  // points per thread of k_label
+constexpr int kPairs = 1;               // point pairs per thread of k_label
+constexpr int kPPT = 2 * kPairs;        // points per thread
 
 // Full node pass on device-resident points: Morton order -> K1 -> compaction
 // of flagged points -> K3. masks/s_out are device pointers.
@@ -204,7 +205,7 @@ void label_nodes_dev(nm_ctx* c, const double* d_pts, std::size_t n, double T, st
   prm.counters = counters;
   if (stats) NM_CUDA(cudaEventRecord(c->ev[1], st));
   const std::size_t per_block = static_cast<std::size_t>(nm::kBlock) * kPPT;
-  nm::k_label<kPPT><<<static_cast<unsigned>((n + per_block - 1) / per_block), nm::kBlock, 0, st>>>(prm);
+  nm::k_label<kPairs><<<static_cast<unsigned>((n + per_block - 1) / per_block), nm::kBlock, 0, st>>>(prm);
   NM_CUDA(cudaGetLastError());
   ++launches;
   if (stats) NM_CUDA(cudaEventRecord(c->ev[2], st));

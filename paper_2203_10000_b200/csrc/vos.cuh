@@ -18,7 +18,7 @@ namespace nm {
 
 __device__ __forceinline__ float sqrt_approx(float x) {
   float r;
-  asm("sqrt.approx.f32 %0, %1;" : "=f"(r) : "f"(x));
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
   return r;
 }
 __device__ __forceinline__ float rcp_approx(float x) {
@@ -75,6 +75,61 @@ __device__ __forceinline__ float acc_near(float acc, const VosTerms& t, float ta
   const float prod = __fmul_rn(__fmul_rn(t.r1, t.r2), t.r3);
   const float lim = __fmul_rn(tau, prod);
   det |= ((fabsf(t.num) <= lim) && (t.den <= lim)) || (fminf(t.r1, fminf(t.r2, t.r3)) <= delta);
+  return far_range ? a_far : a_full;
+}
+
+// ---------------------------------------------------------------------------
+// Packed form: two points per float2 lane pair, triangle operands broadcast.
+// sm_100a executes FADD2/FMUL2/FFMA2 (fp32x2) with a scalar register
+// broadcast to both lanes (".F32" operand), halving the FP32 issue slots per
+// evaluation. Every lane op is an IEEE fp32 _rn operation, bit-identical to
+// the scalar intrinsics above.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ float2 bc(float a) { return make_float2(a, a); }
+__device__ __forceinline__ float2 add2(float2 a, float2 b) { return __fadd2_rn(a, b); }
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) { return __fmul2_rn(a, b); }
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
+
+struct VosTerms2 {
+  float2 num, den, r1, r2, r3;
+};
+
+// (mx, my, mz) = -(p - c) for two points.
+__device__ __forceinline__ VosTerms2 vos_terms2(const float4& A, const float4& B, const float4& C, float2 mx,
+                                                float2 my, float2 mz) {
+  const float2 x1 = add2(bc(A.x), mx), y1 = add2(bc(A.y), my), z1 = add2(bc(A.z), mz);
+  const float2 x2 = add2(bc(B.x), mx), y2 = add2(bc(B.y), my), z2 = add2(bc(B.z), mz);
+  const float2 x3 = add2(bc(C.x), mx), y3 = add2(bc(C.y), my), z3 = add2(bc(C.z), mz);
+  const float2 q1 = fma2(z1, z1, fma2(y1, y1, mul2(x1, x1)));
+  const float2 q2 = fma2(z2, z2, fma2(y2, y2, mul2(x2, x2)));
+  const float2 q3 = fma2(z3, z3, fma2(y3, y3, mul2(x3, x3)));
+  VosTerms2 t;
+  t.r1 = make_float2(sqrt_approx(q1.x), sqrt_approx(q1.y));
+  t.r2 = make_float2(sqrt_approx(q2.x), sqrt_approx(q2.y));
+  t.r3 = make_float2(sqrt_approx(q3.x), sqrt_approx(q3.y));
+  t.num = fma2(bc(C.w), z1, fma2(bc(B.w), y1, mul2(bc(A.w), x1)));
+  const float2 d12 = fma2(z1, z2, fma2(y1, y2, mul2(x1, x2)));
+  const float2 d13 = fma2(z1, z3, fma2(y1, y3, mul2(x1, x3)));
+  const float2 d23 = fma2(z2, z3, fma2(y2, y3, mul2(x2, x3)));
+  t.den = fma2(fma2(t.r1, t.r2, d12), t.r3, fma2(d13, t.r2, mul2(d23, t.r1)));
+  return t;
+}
+
+__device__ __forceinline__ float2 acc_far2(float2 acc, float2 num, float2 den) {
+  const float2 x = mul2(num, make_float2(rcp_approx(den.x), rcp_approx(den.y)));
+  const float2 y = mul2(x, x);
+  const float2 p = fma2(fma2(fma2(bc(-0.142857142857f), y, bc(0.2f)), y, bc(-0.333333333333f)), y, bc(1.0f));
+  return fma2(x, p, acc);
+}
+
+// Near path for one lane, given the packed far-range value of that lane.
+__device__ __forceinline__ float acc_near_lane(float acc, float a_far, float num, float den, float r1, float r2,
+                                               float r3, float tau, float delta, bool& det) {
+  const bool far_range = (den > 0.0f) && (fabsf(num) <= __fmul_rn(kFarX, den));
+  const float a_full = __fadd_rn(acc, atan2f(num, den));
+  const float prod = __fmul_rn(__fmul_rn(r1, r2), r3);
+  const float lim = __fmul_rn(tau, prod);
+  det |= ((fabsf(num) <= lim) && (den <= lim)) || (fminf(r1, fminf(r2, r3)) <= delta);
   return far_range ? a_far : a_full;
 }
 
