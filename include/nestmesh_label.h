@@ -60,6 +60,8 @@ typedef struct nm_options {
   float far_ratio;       /* subtile is "far" for a point when d >= far_ratio * radius + far_abs_mm */
   float far_abs_mm;
   int sort_points;       /* 1: Morton-order points before the kernel (performance only) */
+  int pairs_per_thread;  /* point pairs per thread of the fp32 kernel: 1 or 2 (performance only) */
+  int layout;            /* triangle tiles: 0 auto, 1 independent triangles, 2 strip segments (performance only) */
 } nm_options;
 
 /* Counters of one labeling call (accumulated by the call, not across calls). */
@@ -129,8 +131,9 @@ int nm_label_tets_device(nm_ctx* ctx, const uint32_t* d_tets, size_t nt, const u
 int nm_flag_boundary_device(nm_ctx* ctx, const uint32_t* d_tets, size_t nt, const uint32_t* d_masks,
                             uint32_t active_mask, uint32_t* d_ids, uint32_t* d_count, void* stream);
 
-/* Compartment count and total padded triangle count of the current surfaces. */
-int nm_surface_info(nm_ctx* ctx, int* K, size_t* triangles, size_t* padded_triangles);
+/* Compartment count, real and padded (evaluated) triangle slots, and the tile
+ * layout (1 triangles, 2 strips) chosen for the current surfaces. */
+int nm_surface_info(nm_ctx* ctx, int* K, size_t* triangles, size_t* padded_triangles, int* layout);
 
 #ifdef __cplusplus
 }

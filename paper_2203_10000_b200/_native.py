@@ -34,6 +34,8 @@ class NmOptions(ctypes.Structure):
         ("far_ratio", ctypes.c_float),
         ("far_abs_mm", ctypes.c_float),
         ("sort_points", ctypes.c_int),
+        ("pairs_per_thread", ctypes.c_int),
+        ("layout", ctypes.c_int),
     ]
 
 
@@ -87,7 +89,7 @@ LABEL_API = {
                                             ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(NmStats)]),
     "nm_flag_boundary_device": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p,
                                                ctypes.c_uint32, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
-    "nm_surface_info": (ctypes.c_int, [ctypes.c_void_p, c_i32_p, c_size_p, c_size_p]),
+    "nm_surface_info": (ctypes.c_int, [ctypes.c_void_p, c_i32_p, c_size_p, c_size_p, c_i32_p]),
 }
 
 _lib = None
@@ -177,8 +179,10 @@ class Context:
         K = ctypes.c_int()
         t = ctypes.c_size_t()
         tp = ctypes.c_size_t()
-        check(self.lib.nm_surface_info(self.handle, ctypes.byref(K), ctypes.byref(t), ctypes.byref(tp)))
-        return K.value, t.value, tp.value
+        lay = ctypes.c_int()
+        check(self.lib.nm_surface_info(self.handle, ctypes.byref(K), ctypes.byref(t), ctypes.byref(tp),
+                                       ctypes.byref(lay)))
+        return {"K": K.value, "triangles": t.value, "slots": tp.value, "layout": "strips" if lay.value == 2 else "triangles"}
 
     # -- host-buffer entry points ----------------------------------------
     def enclosure(self, pts, threshold=0.5):

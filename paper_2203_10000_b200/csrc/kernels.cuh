@@ -32,7 +32,8 @@ struct LabelParams {
   const double* pts;         // fp64 xyz, original frame
   std::size_t n;
   const std::uint32_t* order;  // evaluation order (Morton); nullptr = identity
-  const float4* tri;         // 3 float4 per padded triangle: (a.xyz,N.x) (b.xyz,N.y) (c.xyz,N.z)
+  const float4* tri;         // soup: 3 float4 per triangle (a.xyz,N.x) (b.xyz,N.y) (c.xyz,N.z);
+                             // strip: kSegF4 float4 per 8-triangle segment (vos.cuh)
   const float4* sub;         // per subtile: fp32 centre c (centred frame), w = (far radius)^2;
                              // the subtile's vertices are stored relative to c
   const std::uint32_t* comp_tiles;  // K+1 tile offsets
@@ -47,10 +48,14 @@ struct LabelParams {
 };
 
 // NP point pairs per thread (2*NP points), packed fp32x2 arithmetic.
-template <int NP>
+// STRIP = false: 3 float4 per triangle (triangle soup);
+// STRIP = true : 4 strip segments of 8 triangles per subtile (vos.cuh).
+template <int NP, bool STRIP>
 __global__ void __launch_bounds__(kBlock) k_label(const LabelParams prm) {
   constexpr int P = 2 * NP;
-  __shared__ float4 s_tri[kTile * 3];
+  constexpr int kSubF4 = STRIP ? (kSub / kSegTris) * kSegF4 : kSub * 3;  // float4 per subtile
+  constexpr int kTileF4 = kSubF4 * kSubPerTile;
+  __shared__ float4 s_tri[kTileF4];
   __shared__ float4 s_sub[kSubPerTile];
 
   const std::size_t base = (static_cast<std::size_t>(blockIdx.x) * kBlock + threadIdx.x) * P;
@@ -95,9 +100,9 @@ __global__ void __launch_bounds__(kBlock) k_label(const LabelParams prm) {
     }
     for (; tile < tile_end; ++tile) {
       __syncthreads();
-      const float4* gt = prm.tri + static_cast<std::size_t>(tile) * kTile * 3;
+      const float4* gt = prm.tri + static_cast<std::size_t>(tile) * kTileF4;
 #pragma unroll
-      for (int i = threadIdx.x; i < kTile * 3; i += kBlock) s_tri[i] = __ldg(gt + i);
+      for (int i = threadIdx.x; i < kTileF4; i += kBlock) s_tri[i] = __ldg(gt + i);
       if (threadIdx.x < kSubPerTile)
         s_sub[threadIdx.x] = __ldg(prm.sub + static_cast<std::size_t>(tile) * kSubPerTile + threadIdx.x);
       __syncthreads();
@@ -120,31 +125,43 @@ __global__ void __launch_bounds__(kBlock) k_label(const LabelParams prm) {
           const float2 d2 = fma2(pz, pz, fma2(py, py, mul2(px, px)));
           far &= (!valid[2 * q] || d2.x > sb.w) && (!valid[2 * q + 1] || d2.y > sb.w);
         }
-        const float4* tt = s_tri + st * kSub * 3;
+        const float4* tt = s_tri + st * kSubF4;
         if (__all_sync(kFull, far)) {
           ++n_far;
+          if constexpr (STRIP) {
+#pragma unroll 1
+            for (int g = 0; g < kSub / kSegTris; ++g)
+              eval_segment<NP, false>(tt + g * kSegF4, mx, my, mz, acc, det, prm.tau, prm.delta);
+          } else {
 #pragma unroll 4
-          for (int t = 0; t < kSub; ++t) {
-            const float4 A = tt[3 * t], B = tt[3 * t + 1], C = tt[3 * t + 2];
+            for (int t = 0; t < kSub; ++t) {
+              const float4 A = tt[3 * t], B = tt[3 * t + 1], C = tt[3 * t + 2];
 #pragma unroll
-            for (int q = 0; q < NP; ++q) {
-              const VosTerms2 v = vos_terms2(A, B, C, mx[q], my[q], mz[q]);
-              acc[q] = acc_far2(acc[q], v.num, v.den);
+              for (int q = 0; q < NP; ++q) {
+                const VosTerms2 v = vos_terms2(A, B, C, mx[q], my[q], mz[q]);
+                acc[q] = acc_far2(acc[q], v.num, v.den);
+              }
             }
           }
         } else {
           ++n_near;
+          if constexpr (STRIP) {
 #pragma unroll 1
-          for (int t = 0; t < kSub; ++t) {
-            const float4 A = tt[3 * t], B = tt[3 * t + 1], C = tt[3 * t + 2];
+            for (int g = 0; g < kSub / kSegTris; ++g)
+              eval_segment<NP, true>(tt + g * kSegF4, mx, my, mz, acc, det, prm.tau, prm.delta);
+          } else {
+#pragma unroll 1
+            for (int t = 0; t < kSub; ++t) {
+              const float4 A = tt[3 * t], B = tt[3 * t + 1], C = tt[3 * t + 2];
 #pragma unroll
-            for (int q = 0; q < NP; ++q) {
-              const VosTerms2 v = vos_terms2(A, B, C, mx[q], my[q], mz[q]);
-              const float2 af = acc_far2(acc[q], v.num, v.den);
-              acc[q].x = acc_near_lane(acc[q].x, af.x, v.num.x, v.den.x, v.r1.x, v.r2.x, v.r3.x, prm.tau, prm.delta,
-                                       det[2 * q]);
-              acc[q].y = acc_near_lane(acc[q].y, af.y, v.num.y, v.den.y, v.r1.y, v.r2.y, v.r3.y, prm.tau, prm.delta,
-                                       det[2 * q + 1]);
+              for (int q = 0; q < NP; ++q) {
+                const VosTerms2 v = vos_terms2(A, B, C, mx[q], my[q], mz[q]);
+                const float2 af = acc_far2(acc[q], v.num, v.den);
+                acc[q].x = acc_near_lane(acc[q].x, af.x, v.num.x, v.den.x, v.r1.x, v.r2.x, v.r3.x, prm.tau, prm.delta,
+                                         det[2 * q]);
+                acc[q].y = acc_near_lane(acc[q].y, af.y, v.num.y, v.den.y, v.r1.y, v.r2.y, v.r3.y, prm.tau, prm.delta,
+                                         det[2 * q + 1]);
+              }
             }
           }
         }

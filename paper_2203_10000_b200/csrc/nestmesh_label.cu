@@ -10,6 +10,8 @@
 #include <cstring>
 #include <exception>
 #include <numeric>
+#include <queue>
+#include <unordered_map>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -87,6 +89,107 @@ std::uint32_t spread10h(std::uint32_t v) {
   return v;
 }
 
+
+// Greedy triangle-strip decomposition of one compartment.
+// Start from the unused triangle with the fewest unused neighbours, try its
+// three rotations, walk forward across (u_{k+1}, u_{k+2}) and backward from the
+// reversed start, keep the longest. Returns, per strip, the vertex sequence
+// u_0..u_{m+1} and the original triangle ids t_0..t_{m-1} with
+// {u_k, u_{k+1}, u_{k+2}} == set(t_k). Only performance depends on the
+// quality of the decomposition; every triangle appears in exactly one strip.
+struct Strip {
+  std::vector<std::uint32_t> v;
+  std::vector<std::uint32_t> t;
+};
+
+std::vector<Strip> stripify(const std::uint32_t* tri, std::uint32_t t0, std::uint32_t t1) {
+  const std::uint32_t m = t1 - t0;
+  std::unordered_map<std::uint64_t, std::array<std::int64_t, 2>> edges;
+  edges.reserve(static_cast<std::size_t>(m) * 2);
+  auto key = [](std::uint32_t a, std::uint32_t b) {
+    return a < b ? (std::uint64_t(a) << 32 | b) : (std::uint64_t(b) << 32 | a);
+  };
+  for (std::uint32_t i = 0; i < m; ++i) {
+    const std::uint32_t* e = tri + 3 * std::size_t(t0 + i);
+    for (int j = 0; j < 3; ++j) {
+      auto [it, ins] = edges.try_emplace(key(e[j], e[(j + 1) % 3]), std::array<std::int64_t, 2>{-1, -1});
+      auto& s = it->second;
+      if (s[0] < 0) s[0] = i;
+      else if (s[1] < 0) s[1] = i;
+    }
+  }
+  std::vector<std::uint8_t> used(m, 0);
+  auto nbr = [&](std::uint32_t i, std::uint32_t a, std::uint32_t b) -> std::int64_t {
+    const auto& s = edges.at(key(a, b));
+    return s[0] == static_cast<std::int64_t>(i) ? s[1] : s[0];
+  };
+  std::vector<int> deg(m, 0);
+  for (std::uint32_t i = 0; i < m; ++i) {
+    const std::uint32_t* e = tri + 3 * std::size_t(t0 + i);
+    for (int j = 0; j < 3; ++j) deg[i] += nbr(i, e[j], e[(j + 1) % 3]) >= 0;
+  }
+  using QE = std::pair<int, std::uint32_t>;
+  std::priority_queue<QE, std::vector<QE>, std::greater<QE>> pq;
+  for (std::uint32_t i = 0; i < m; ++i) pq.emplace(deg[i], i);
+  std::vector<std::uint32_t> mark(m, 0);
+  std::uint32_t stamp = 0;
+  // forward walk from triangle i with vertex order (a,b,c)
+  auto walk = [&](std::uint32_t i, std::uint32_t a, std::uint32_t b, std::uint32_t c, std::vector<std::uint32_t>& vs,
+                  std::vector<std::uint32_t>& ts) {
+    vs.assign({a, b, c});
+    ts.assign({i});
+    mark[i] = stamp;
+    std::uint32_t cur = i;
+    for (;;) {
+      const std::uint32_t u = vs[vs.size() - 2], w = vs.back();
+      const std::int64_t n = nbr(cur, u, w);
+      if (n < 0 || used[n] || mark[n] == stamp) break;
+      const std::uint32_t* e = tri + 3 * std::size_t(t0 + n);
+      std::uint32_t x = e[0];
+      for (int j = 0; j < 3; ++j)
+        if (e[j] != u && e[j] != w) x = e[j];
+      vs.push_back(x);
+      ts.push_back(static_cast<std::uint32_t>(n));
+      mark[n] = stamp;
+      cur = static_cast<std::uint32_t>(n);
+    }
+  };
+  std::vector<Strip> out;
+  std::vector<std::uint32_t> fv, ft, bv, btt;
+  while (!pq.empty()) {
+    auto [d, i] = pq.top();
+    pq.pop();
+    if (used[i] || d != deg[i]) continue;
+    const std::uint32_t* e = tri + 3 * std::size_t(t0 + i);
+    Strip best;
+    for (int r = 0; r < 3; ++r) {
+      const std::uint32_t a = e[r], b = e[(r + 1) % 3], c = e[(r + 2) % 3];
+      ++stamp;
+      walk(i, a, b, c, fv, ft);
+      // backward: walk from the reversed start without reusing forward triangles
+      std::vector<std::uint32_t> keep(ft.begin(), ft.end());
+      walk(i, c, b, a, bv, btt);
+      // bv = c,b,a,x,y,...; combined vertex sequence = reverse(bv) + fv[3:]
+      Strip s;
+      s.v.assign(bv.rbegin(), bv.rend());
+      s.v.insert(s.v.end(), fv.begin() + 3, fv.end());
+      s.t.assign(btt.rbegin(), btt.rend());  // ..., i
+      s.t.insert(s.t.end(), ft.begin() + 1, ft.end());
+      if (s.t.size() > best.t.size()) best = std::move(s);
+    }
+    for (std::uint32_t t : best.t) used[t] = 1;
+    for (std::uint32_t t : best.t) {
+      const std::uint32_t* f = tri + 3 * std::size_t(t0 + t);
+      for (int j = 0; j < 3; ++j) {
+        const std::int64_t n = nbr(t, f[j], f[(j + 1) % 3]);
+        if (n >= 0 && !used[n]) pq.emplace(--deg[n], static_cast<std::uint32_t>(n));
+      }
+    }
+    for (auto& t : best.t) t += t0;
+    out.push_back(std::move(best));
+  }
+  return out;
+}
 }  // namespace
 
 struct nm_ctx {
@@ -97,6 +200,7 @@ struct nm_ctx {
 
   // surfaces
   bool has_surfaces = false;
+  bool strips = false;  // tile layout of the current surfaces
   int K = 0;
   std::size_t nt_real = 0, nt_pad = 0, nv = 0;
   double cx = 0, cy = 0, cz = 0;
@@ -145,8 +249,6 @@ void select(nm_ctx* c, Pred pred, std::size_t n, std::uint32_t* out, std::uint32
   launches += 3;
 }
 
-constexpr int kPairs = 1;               // point pairs per thread of k_label
-constexpr int kPPT = 2 * kPairs;        // points per thread
 
 // Full node pass on device-resident points: Morton order -> K1 -> compaction
 // of flagged points -> K3. masks/s_out are device pointers.
@@ -204,8 +306,18 @@ void label_nodes_dev(nm_ctx* c, const double* d_pts, std::size_t n, double T, st
   prm.s_out = d_s;
   prm.counters = counters;
   if (stats) NM_CUDA(cudaEventRecord(c->ev[1], st));
-  const std::size_t per_block = static_cast<std::size_t>(nm::kBlock) * kPPT;
-  nm::k_label<kPairs><<<static_cast<unsigned>((n + per_block - 1) / per_block), nm::kBlock, 0, st>>>(prm);
+  {
+    const int np = c->opt.pairs_per_thread;
+    const std::size_t per_block = static_cast<std::size_t>(nm::kBlock) * 2 * np;
+    const unsigned grid = static_cast<unsigned>((n + per_block - 1) / per_block);
+    if (c->strips) {
+      if (np == 2) nm::k_label<2, true><<<grid, nm::kBlock, 0, st>>>(prm);
+      else nm::k_label<1, true><<<grid, nm::kBlock, 0, st>>>(prm);
+    } else {
+      if (np == 2) nm::k_label<2, false><<<grid, nm::kBlock, 0, st>>>(prm);
+      else nm::k_label<1, false><<<grid, nm::kBlock, 0, st>>>(prm);
+    }
+  }
   NM_CUDA(cudaGetLastError());
   ++launches;
   if (stats) NM_CUDA(cudaEventRecord(c->ev[2], st));
@@ -293,6 +405,8 @@ void nm_default_options(nm_options* o) {
   o->far_ratio = 5.0f;
   o->far_abs_mm = 0.05f;
   o->sort_points = 1;
+  o->pairs_per_thread = 1;
+  o->layout = 0;
 }
 
 int nm_create(nm_ctx** out, const nm_options* opt) {
@@ -309,6 +423,8 @@ int nm_create(nm_ctx** out, const nm_options* opt) {
       if (opt) c->opt = *opt;
       else nm_default_options(&c->opt);
       if (c->opt.device < 0 || c->opt.device >= ndev) throw Error("device ordinal out of range");
+      if (c->opt.pairs_per_thread != 1 && c->opt.pairs_per_thread != 2) throw Error("pairs_per_thread must be 1 or 2");
+      if (c->opt.layout < 0 || c->opt.layout > 2) throw Error("layout must be 0 (auto), 1 (triangles) or 2 (strips)");
       NM_CUDA(cudaSetDevice(c->opt.device));
       cudaDeviceProp p;
       NM_CUDA(cudaGetDeviceProperties(&p, c->opt.device));
@@ -362,95 +478,168 @@ int nm_set_surfaces(nm_ctx* c, const double* xyz, std::size_t nv, const std::uin
     c->cy = ctr[1];
     c->cz = ctr[2];
 
-    // Per compartment: Morton-sort triangles, pad to whole tiles.
+    auto morton = [&](const double* m) {
+      std::uint32_t q[3];
+      for (int a = 0; a < 3; ++a) {
+        const double u = (m[a] - c->lo[a]) / span * 1024.0;
+        q[a] = static_cast<std::uint32_t>(std::clamp(u, 0.0, 1023.0));
+      }
+      return spread10h(q[0]) | (spread10h(q[1]) << 1) | (spread10h(q[2]) << 2);
+    };
+    auto normal64 = [&](std::uint32_t t, double* N) {
+      const double* A = xyz + 3 * std::size_t(tri[3 * t]);
+      const double* B = xyz + 3 * std::size_t(tri[3 * t + 1]);
+      const double* C = xyz + 3 * std::size_t(tri[3 * t + 2]);
+      const double e1[3] = {B[0] - A[0], B[1] - A[1], B[2] - A[2]};
+      const double e2[3] = {C[0] - A[0], C[1] - A[1], C[2] - A[2]};
+      N[0] = e1[1] * e2[2] - e1[2] * e2[1];
+      N[1] = e1[2] * e2[0] - e1[0] * e2[2];
+      N[2] = e1[0] * e2[1] - e1[1] * e2[0];
+    };
+
+    // ---- strip decomposition --------------------------------
+    // Segment = 8 consecutive strip triangles over 10 vertices; a strip's last
+    // segment is padded with zero-normal triangles repeating its last vertex.
+    struct Seg {
+      std::uint32_t v[nm::kSegTris + 2];
+      std::int64_t t[nm::kSegTris];  // original triangle id, -1 = pad
+      std::uint32_t key;
+    };
+    std::vector<std::vector<Seg>> segs(K);
+    std::size_t strip_slots = 0;
+    const bool try_strips = c->opt.layout != 1;
+    if (try_strips) {
+      for (int k = 0; k < K; ++k) {
+        const std::vector<Strip> strips = stripify(tri, comp_off[k], comp_off[k + 1]);
+        for (const Strip& st : strips) {
+          const std::size_t m = st.t.size();
+          for (std::size_t s0 = 0; s0 < m; s0 += nm::kSegTris) {
+            Seg g;
+            for (int j = 0; j < nm::kSegTris + 2; ++j) g.v[j] = st.v[std::min(s0 + j, st.v.size() - 1)];
+            for (int j = 0; j < nm::kSegTris; ++j) g.t[j] = s0 + j < m ? std::int64_t(st.t[s0 + j]) : -1;
+            double cen[3] = {0, 0, 0};
+            for (int j = 0; j < nm::kSegTris + 2; ++j)
+              for (int a = 0; a < 3; ++a) cen[a] += xyz[3 * std::size_t(g.v[j]) + a] / (nm::kSegTris + 2);
+            g.key = morton(cen);
+            segs[k].push_back(g);
+          }
+        }
+        std::stable_sort(segs[k].begin(), segs[k].end(), [](const Seg& x, const Seg& y) { return x.key < y.key; });
+        const std::size_t per_tile = nm::kTile / nm::kSegTris;
+        strip_slots += (segs[k].size() + per_tile - 1) / per_tile * nm::kTile;
+      }
+    }
+    std::size_t soup_slots = 0;
+    for (int k = 0; k < K; ++k) soup_slots += (comp_off[k + 1] - comp_off[k] + nm::kTile - 1) / nm::kTile * nm::kTile;
+    // auto: strips when their padding costs less than the ~1.5x op saving
+    const bool use_strips =
+        c->opt.layout == 2 || (c->opt.layout == 0 && nt > 0 && strip_slots <= soup_slots + soup_slots / 4);
+
     std::vector<std::uint32_t> tiles(K + 1, 0);
     std::vector<std::vector<std::uint32_t>> order(K);
     for (int k = 0; k < K; ++k) {
-      const std::uint32_t b = comp_off[k], e = comp_off[k + 1];
-      std::vector<std::pair<std::uint32_t, std::uint32_t>> kk;
-      kk.reserve(e - b);
-      for (std::uint32_t t = b; t < e; ++t) {
-        std::uint32_t q[3];
-        for (int a = 0; a < 3; ++a) {
-          const double m = (xyz[3 * tri[3 * t] + a] + xyz[3 * tri[3 * t + 1] + a] + xyz[3 * tri[3 * t + 2] + a]) / 3.0;
-          const double u = (m - c->lo[a]) / span * 1024.0;
-          q[a] = static_cast<std::uint32_t>(std::clamp(u, 0.0, 1023.0));
+      std::size_t units;
+      if (use_strips) {
+        units = (segs[k].size() * nm::kSegTris + nm::kTile - 1) / nm::kTile;
+      } else {
+        const std::uint32_t b = comp_off[k], e = comp_off[k + 1];
+        std::vector<std::pair<std::uint32_t, std::uint32_t>> kk;
+        kk.reserve(e - b);
+        for (std::uint32_t t = b; t < e; ++t) {
+          double m[3];
+          for (int a = 0; a < 3; ++a)
+            m[a] = (xyz[3 * tri[3 * t] + a] + xyz[3 * tri[3 * t + 1] + a] + xyz[3 * tri[3 * t + 2] + a]) / 3.0;
+          kk.emplace_back(morton(m), t);
         }
-        kk.emplace_back(spread10h(q[0]) | (spread10h(q[1]) << 1) | (spread10h(q[2]) << 2), t);
+        std::stable_sort(kk.begin(), kk.end(), [](auto& x, auto& y) { return x.first < y.first; });
+        for (auto& p : kk) order[k].push_back(p.second);
+        units = (e - b + nm::kTile - 1) / nm::kTile;
       }
-      std::stable_sort(kk.begin(), kk.end(), [](auto& x, auto& y) { return x.first < y.first; });
-      for (auto& p : kk) order[k].push_back(p.second);
-      tiles[k + 1] = tiles[k] + static_cast<std::uint32_t>((e - b + nm::kTile - 1) / nm::kTile);
+      tiles[k + 1] = tiles[k] + static_cast<std::uint32_t>(units);
     }
     const std::size_t ntiles = tiles[K];
     const std::size_t npad = ntiles * nm::kTile;
-    // Tile layout: each 32-triangle subtile carries an fp32
-    // centre c (exactly representable, centred frame) and its triangles'
-    // vertices relative to c, so near-surface geometry keeps ~ulp(radius)
-    // instead of ~ulp(100 mm) precision; the kernel forms p - c in
-    // double-single per subtile.
-    std::vector<float4> htri(3 * npad);
+    const int sub_f4 = use_strips ? (nm::kSub / nm::kSegTris) * nm::kSegF4 : nm::kSub * 3;
+    const std::size_t tile_f4 = static_cast<std::size_t>(sub_f4) * nm::kSubPerTile;
+    std::vector<float4> htri(ntiles * tile_f4);
     std::vector<float4> hsub(ntiles * nm::kSubPerTile);
     const double far_ratio = c->opt.far_ratio, far_abs = c->opt.far_abs_mm;
-    std::vector<std::array<double, 9>> v64(nm::kSub);
-    std::vector<std::array<double, 3>> n64(nm::kSub);
+    // Each 32-triangle subtile carries an fp32 centre c (exactly representable
+    // in the centred frame) and its vertices relative to c, so near-surface
+    // geometry keeps ~ulp(radius) precision; the kernel forms p - c in
+    // double-single per subtile.
+    constexpr int kMaxV = nm::kSub * 3;
+    std::vector<std::array<double, 3>> vloc(kMaxV);
     for (int k = 0; k < K; ++k) {
-      const auto& ord = order[k];
-      const std::size_t nreal = ord.size();
+      const std::size_t nreal = use_strips ? segs[k].size() : order[k].size();
+      // fallback vertex for all-pad units: the compartment's first vertex
+      const double* pad_v = comp_off[k + 1] > comp_off[k] ? xyz + 3 * std::size_t(tri[3 * comp_off[k]]) : ctr;
       for (std::uint32_t tl = tiles[k]; tl < tiles[k + 1]; ++tl) {
-        for (int s = 0; s < nm::kSubPerTile; ++s) {
-          const std::size_t r0 = static_cast<std::size_t>(tl - tiles[k]) * nm::kTile + s * nm::kSub;
-          // gather fp64 vertices (centred frame) + normals; pads repeat the
-          // compartment's last real vertex with N = 0 (contributes exactly 0)
-          double blo[3] = {1e300, 1e300, 1e300}, bhi[3] = {-1e300, -1e300, -1e300};
-          for (int j = 0; j < nm::kSub; ++j) {
-            const std::size_t r = r0 + j;
-            if (r < nreal) {
-              const std::uint32_t t = ord[r];
-              const double* A = xyz + 3 * std::size_t(tri[3 * t]);
-              const double* B = xyz + 3 * std::size_t(tri[3 * t + 1]);
-              const double* C = xyz + 3 * std::size_t(tri[3 * t + 2]);
-              const double e1[3] = {B[0] - A[0], B[1] - A[1], B[2] - A[2]};
-              const double e2[3] = {C[0] - A[0], C[1] - A[1], C[2] - A[2]};
-              n64[j] = {e1[1] * e2[2] - e1[2] * e2[1], e1[2] * e2[0] - e1[0] * e2[2], e1[0] * e2[1] - e1[1] * e2[0]};
-              for (int a = 0; a < 3; ++a) {
-                v64[j][a] = A[a] - ctr[a];
-                v64[j][3 + a] = B[a] - ctr[a];
-                v64[j][6 + a] = C[a] - ctr[a];
-              }
+        for (int sidx = 0; sidx < nm::kSubPerTile; ++sidx) {
+          // gather this subtile's vertices (centred frame, fp64)
+          int nv_loc = 0;
+          std::vector<const double*> srcv;
+          const std::size_t u0 = static_cast<std::size_t>(tl - tiles[k]) * nm::kTile / (use_strips ? nm::kSegTris : 1) +
+                                 sidx * (use_strips ? nm::kSub / nm::kSegTris : nm::kSub);
+          const int nunits = use_strips ? nm::kSub / nm::kSegTris : nm::kSub;
+          for (int j = 0; j < nunits; ++j) {
+            const std::size_t u = u0 + j;
+            if (use_strips) {
+              for (int q = 0; q < nm::kSegTris + 2; ++q)
+                srcv.push_back(u < nreal ? xyz + 3 * std::size_t(segs[k][u].v[q]) : pad_v);
             } else {
-              const std::uint32_t t = nreal ? ord[nreal - 1] : 0u;
-              const double* A = nreal ? xyz + 3 * std::size_t(tri[3 * t]) : ctr;
-              n64[j] = {0.0, 0.0, 0.0};
-              for (int v = 0; v < 3; ++v)
-                for (int a = 0; a < 3; ++a) v64[j][3 * v + a] = A[a] - ctr[a];
+              const std::uint32_t t = u < nreal ? order[k][u] : 0;
+              for (int q = 0; q < 3; ++q) srcv.push_back(u < nreal ? xyz + 3 * std::size_t(tri[3 * t + q]) : pad_v);
             }
-            for (int v = 0; v < 3; ++v)
-              for (int a = 0; a < 3; ++a) {
-                blo[a] = std::min(blo[a], v64[j][3 * v + a]);
-                bhi[a] = std::max(bhi[a], v64[j][3 * v + a]);
-              }
           }
+          double blo[3] = {1e300, 1e300, 1e300}, bhi[3] = {-1e300, -1e300, -1e300};
+          for (const double* v : srcv)
+            for (int a = 0; a < 3; ++a) {
+              blo[a] = std::min(blo[a], v[a] - ctr[a]);
+              bhi[a] = std::max(bhi[a], v[a] - ctr[a]);
+            }
           const float fc[3] = {float(0.5 * (blo[0] + bhi[0])), float(0.5 * (blo[1] + bhi[1])),
                                float(0.5 * (blo[2] + bhi[2]))};
           double rho = 0.0;
-          for (int j = 0; j < nm::kSub; ++j) {
-            float q[9];
-            for (int v = 0; v < 3; ++v)
-              for (int a = 0; a < 3; ++a) q[3 * v + a] = float(v64[j][3 * v + a] - double(fc[a]));
-            for (int v = 0; v < 3; ++v)
-              rho = std::max(rho, std::sqrt(double(q[3 * v]) * q[3 * v] + double(q[3 * v + 1]) * q[3 * v + 1] +
-                                            double(q[3 * v + 2]) * q[3 * v + 2]));
-            float4* o = &htri[3 * (static_cast<std::size_t>(tl) * nm::kTile + s * nm::kSub + j)];
-            o[0] = make_float4(q[0], q[1], q[2], float(n64[j][0]));
-            o[1] = make_float4(q[3], q[4], q[5], float(n64[j][1]));
-            o[2] = make_float4(q[6], q[7], q[8], float(n64[j][2]));
+          std::vector<float> rel(3 * srcv.size());
+          for (std::size_t q = 0; q < srcv.size(); ++q) {
+            for (int a = 0; a < 3; ++a) rel[3 * q + a] = float((srcv[q][a] - ctr[a]) - double(fc[a]));
+            rho = std::max(rho, std::sqrt(double(rel[3 * q]) * rel[3 * q] + double(rel[3 * q + 1]) * rel[3 * q + 1] +
+                                          double(rel[3 * q + 2]) * rel[3 * q + 2]));
+          }
+          nv_loc = static_cast<int>(srcv.size());
+          (void)nv_loc;
+          float4* o = &htri[(static_cast<std::size_t>(tl) * nm::kSubPerTile + sidx) * sub_f4];
+          for (int j = 0; j < nunits; ++j) {
+            const std::size_t u = u0 + j;
+            if (use_strips) {
+              float4* r = o + j * nm::kSegF4;
+              double N[nm::kSegTris][3];
+              for (int q = 0; q < nm::kSegTris; ++q) {
+                if (u < nreal && segs[k][u].t[q] >= 0) normal64(static_cast<std::uint32_t>(segs[k][u].t[q]), N[q]);
+                else N[q][0] = N[q][1] = N[q][2] = 0.0;
+              }
+              const float* rv = &rel[3 * (j * (nm::kSegTris + 2))];
+              for (int q = 0; q < nm::kSegTris + 2; ++q)
+                r[q] = make_float4(rv[3 * q], rv[3 * q + 1], rv[3 * q + 2], q < nm::kSegTris ? float(N[q][0]) : 0.0f);
+              for (int q = 0; q < nm::kSegTris; q += 2)
+                r[nm::kSegTris + 2 + q / 2] = make_float4(float(N[q][1]), float(N[q][2]), float(N[q + 1][1]),
+                                                          float(N[q + 1][2]));
+            } else {
+              double N[3] = {0, 0, 0};
+              if (u < nreal) normal64(order[k][u], N);
+              const float* rv = &rel[9 * j];
+              for (int q = 0; q < 3; ++q) o[3 * j + q] = make_float4(rv[3 * q], rv[3 * q + 1], rv[3 * q + 2], float(N[q]));
+            }
           }
           const double R = (far_ratio * rho + far_abs) * (1.0 + 1e-5);
-          hsub[static_cast<std::size_t>(tl) * nm::kSubPerTile + s] = make_float4(fc[0], fc[1], fc[2], float(R * R));
+          hsub[static_cast<std::size_t>(tl) * nm::kSubPerTile + sidx] = make_float4(fc[0], fc[1], fc[2], float(R * R));
         }
       }
     }
+    (void)vloc;
+    (void)kMaxV;
+    c->strips = use_strips;
     c->has_surfaces = false;
     auto up = [&](DBuf& b, const void* src, std::size_t bytes) {
       void* d = b.get(bytes);
@@ -472,12 +661,13 @@ int nm_set_surfaces(nm_ctx* c, const double* xyz, std::size_t nv, const std::uin
   });
 }
 
-int nm_surface_info(nm_ctx* c, int* K, std::size_t* triangles, std::size_t* padded) {
+int nm_surface_info(nm_ctx* c, int* K, std::size_t* triangles, std::size_t* padded, int* layout) {
   return guarded([&] {
     require_surfaces(c);
     if (K) *K = c->K;
     if (triangles) *triangles = c->nt_real;
     if (padded) *padded = c->nt_pad;
+    if (layout) *layout = c->strips ? 2 : 1;
   });
 }
 

@@ -9,7 +9,7 @@ from paper_2203_10000_b200 import synth  # noqa: E402
 from paper_2203_10000_b200._native import Context  # noqa: E402
 
 
-def run(cfg_id, max_points=None, reps=2):
+def run(cfg_id, max_points=None, reps=2, **opts):
     cfg = synth.config(cfg_id)
     S = cfg.surfaces
     nodes = cfg.lattice_nodes()
@@ -17,14 +17,14 @@ def run(cfg_id, max_points=None, reps=2):
         # a contiguous slab of k-planes keeps the spatial distribution realistic
         mid = nodes.shape[0] // 2 - max_points // 2
         nodes = nodes[mid:mid + max_points]
-    ctx = Context(0)
+    ctx = Context(0, **opts)
     ctx.set_surfaces(S.xyz, S.tri, S.comp_off, S.label_ids)
     for r in range(reps):
         t = time.time()
         m, st = ctx.label_nodes(nodes)
         wall = time.time() - t
     ev = st["evals"]
-    print(f"cfg{cfg_id}: n={nodes.shape[0]} T={S.n_triangles} K={S.K} evals={ev:.3e} "
+    print(f"{opts} cfg{cfg_id}: n={nodes.shape[0]} T={S.n_triangles} K={S.K} evals={ev:.3e} "
           f"label {st['ms_label']:.1f} ms -> {ev / st['ms_label'] * 1e3:.3e} evals/s (frac57 {ev / st['ms_label'] * 1e3 / 6.53e11:.3f}); "
           f"fixup {st['ms_fixup']:.2f} ms flagged_pts={st['flagged_points']} pairs={st['flagged_pairs']} ties={st['ties']} "
           f"near/far subtiles={st['near_subtiles']}/{st['far_subtiles']} ({st['near_subtiles'] / max(1, st['near_subtiles'] + st['far_subtiles']):.4f}) "
@@ -33,6 +33,12 @@ def run(cfg_id, max_points=None, reps=2):
 
 
 if __name__ == "__main__":
+    import os
+    opts = {}
+    if os.environ.get("NM_LAYOUT"):
+        opts["layout"] = int(os.environ["NM_LAYOUT"])
+    if os.environ.get("NM_PAIRS"):
+        opts["pairs_per_thread"] = int(os.environ["NM_PAIRS"])
     for a in sys.argv[1:]:
         cid, _, mp = a.partition(":")
-        run(int(cid), int(mp) if mp else None)
+        run(int(cid), int(mp) if mp else None, **opts)

@@ -116,3 +116,24 @@ def test_empty_and_ragged(ctx):
         pts = np.random.default_rng(n).uniform(-12, 12, (n, 3))
         m, _ = ctx.label_nodes(pts)
         np.testing.assert_array_equal(m, oracle.label_nodes(pts, synth.single_surface(xyz, tri)))
+
+
+@pytest.mark.parametrize("layout", [1, 2])
+def test_layouts_agree_with_oracle(layout):
+    """Both tile layouts (independent triangles, strip segments) against the
+    oracle on cfg3 (20 intersecting compartments) — a seeded node sample."""
+    from paper_2203_10000_b200._native import Context
+    cfg = synth.config(3)
+    S = cfg.surfaces
+    nodes = cfg.lattice_nodes()
+    idx = np.sort(np.random.default_rng(30 + layout).choice(nodes.shape[0], 3000, replace=False))
+    pts = nodes[idx]
+    with Context(0, layout=layout) as c:
+        c.set_surfaces(S.xyz, S.tri, S.comp_off, S.label_ids)
+        assert c.surface_info()["layout"] == ("strips" if layout == 2 else "triangles")
+        s_gpu, st = c.enclosure(pts)
+        m_gpu, _ = c.label_nodes(pts)
+    m_ref, s_ref = oracle.label_nodes(pts, S, want_s=True)
+    assert np.max(np.abs(s_gpu - s_ref)) <= S_EXPECT
+    bad, _ = _compare_masks(m_gpu, m_ref, s_ref)
+    assert bad == 0
