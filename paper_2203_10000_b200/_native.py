@@ -14,7 +14,7 @@ import numpy as np
 
 PKG_DIR = Path(__file__).resolve().parent
 LIB_DIR = PKG_DIR / "lib"
-LABEL_LIB = LIB_DIR / "libnestmesh_label.so"
+LABEL_LIB = Path(os.environ.get("NM_LABEL_LIB", LIB_DIR / "libnestmesh_label.so"))  # override: experiments only
 SYNTH_LIB = LIB_DIR / "libnestmesh_synth.so"
 
 c_double_p = ctypes.POINTER(ctypes.c_double)

@@ -21,6 +21,12 @@ constexpr int kTile = 256;              // triangles per shared-memory tile (fp6
 constexpr int kSub = 32;                // triangles per subtile (near/far decision unit)
 constexpr int kSubPerTile = kTile / kSub;
 constexpr int kBlock = 256;             // threads per CTA of k_label
+#ifndef NM_DIRECT_LDG
+#define NM_DIRECT_LDG 0
+#endif
+#ifndef NM_MIN_BLOCKS
+#define NM_MIN_BLOCKS 2                 // resident CTAs per SM requested for k_label<1>
+#endif
 constexpr unsigned kFull = 0xffffffffu;
 constexpr double kInv2Pi = 0.15915494309189533576888376337251;
 
@@ -51,12 +57,19 @@ struct LabelParams {
 // STRIP = false: 3 float4 per triangle (triangle soup);
 // STRIP = true : 4 strip segments of 8 triangles per subtile (vos.cuh).
 template <int NP, bool STRIP>
-__global__ void __launch_bounds__(kBlock) k_label(const LabelParams prm) {
+__global__ void __launch_bounds__(kBlock, (NP == 1 ? NM_MIN_BLOCKS : 1)) k_label(const LabelParams prm) {
   constexpr int P = 2 * NP;
   constexpr int kSubF4 = STRIP ? (kSub / kSegTris) * kSegF4 : kSub * 3;  // float4 per subtile
   constexpr int kTileF4 = kSubF4 * kSubPerTile;
+#if NM_DIRECT_LDG
+  // Tiles are read straight from global memory: every lane of a warp loads
+  // the same address (one broadcast transaction, L1-resident across the
+  // CTA's warps), so warps stream through the surface set without
+  // block-wide barriers.
+#else
   __shared__ float4 s_tri[kTileF4];
   __shared__ float4 s_sub[kSubPerTile];
+#endif
 
   const std::size_t base = (static_cast<std::size_t>(blockIdx.x) * kBlock + threadIdx.x) * P;
   // Points in the centred frame as double-singles (hi + lo), packed in pairs;
@@ -99,13 +112,18 @@ __global__ void __launch_bounds__(kBlock) k_label(const LabelParams prm) {
       det[k] = false;
     }
     for (; tile < tile_end; ++tile) {
-      __syncthreads();
       const float4* gt = prm.tri + static_cast<std::size_t>(tile) * kTileF4;
+#if NM_DIRECT_LDG
+      const float4* s_tri = gt;
+      const float4* s_sub = prm.sub + static_cast<std::size_t>(tile) * kSubPerTile;
+#else
+      __syncthreads();
 #pragma unroll
       for (int i = threadIdx.x; i < kTileF4; i += kBlock) s_tri[i] = __ldg(gt + i);
       if (threadIdx.x < kSubPerTile)
         s_sub[threadIdx.x] = __ldg(prm.sub + static_cast<std::size_t>(tile) * kSubPerTile + threadIdx.x);
       __syncthreads();
+#endif
 
       float2 acc[NP];
 #pragma unroll

@@ -35,6 +35,9 @@ def run(cfg_id, max_points=None, reps=2, **opts):
 if __name__ == "__main__":
     import os
     opts = {}
+    if os.environ.get("NM_FAR_RATIO"):
+        opts["far_ratio"] = float(os.environ["NM_FAR_RATIO"])
+        opts["far_abs_mm"] = 0.0
     if os.environ.get("NM_LAYOUT"):
         opts["layout"] = int(os.environ["NM_LAYOUT"])
     if os.environ.get("NM_PAIRS"):

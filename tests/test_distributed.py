@@ -1,0 +1,72 @@
+"""The N>1 path on CPU: the point partitioner + mask all-gather of
+paper_2203_10000_b200.distributed, run with world_size 2 and 3 over gloo, the
+per-rank compute being the oracle (the checker). Labels must equal the
+single-process labels bit for bit (acceptance #8)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import oracle
+from paper_2203_10000_b200 import synth
+from paper_2203_10000_b200.distributed import gather_labels, label_mesh_sharded, shard
+
+
+def test_shard_partition_properties():
+    for n in (0, 1, 7, 35937, 10077696):
+        for world in (1, 2, 3, 4, 8):
+            parts = [shard(n, world, r) for r in range(world)]
+            assert all(p.per == parts[0].per for p in parts)
+            assert parts[0].lo == 0 and parts[-1].hi == n
+            for a, b in zip(parts, parts[1:]):
+                assert a.hi == b.lo
+            assert sum(p.size for p in parts) == n
+            assert parts[0].padded_total >= n and parts[0].padded_total - n < world
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, world, port, out_dir):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        cfg = synth.config(1)
+        S = cfg.surfaces
+        nodes, tets = cfg.lattice_mesh()
+
+        def node_fn(pts):
+            m = oracle.label_nodes(pts.numpy(), S, workers=2)
+            return torch.from_numpy(m.view(np.int32))
+
+        def tet_fn(t, masks):
+            lab = oracle.label_tets(t.numpy().view(np.uint32), masks.numpy().view(np.uint32), S.label_ids)
+            return torch.from_numpy(lab)
+
+        labels, tsh, masks = label_mesh_sharded(nodes, tets, node_fn, tet_fn, rank, world)
+        full = gather_labels(labels, tsh)
+        if rank == 0:
+            np.save(os.path.join(out_dir, f"labels_{world}.npy"), full.numpy())
+            np.save(os.path.join(out_dir, f"masks_{world}.npy"), masks.numpy())
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_labels_equal_single_process(tmp_path, world):
+    mp.spawn(_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    cfg = synth.config(1)
+    nodes, tets = cfg.lattice_mesh()
+    m = oracle.label_nodes(nodes, cfg.surfaces)
+    ref = oracle.label_tets(tets, m, cfg.surfaces.label_ids)
+    np.testing.assert_array_equal(np.load(tmp_path / f"masks_{world}.npy").view(np.uint32), m)
+    np.testing.assert_array_equal(np.load(tmp_path / f"labels_{world}.npy"), ref)
