@@ -240,6 +240,8 @@ def main():
 
     ctx = Context(local)
     ctx.set_surfaces(S.xyz, S.tri, S.comp_off, S.label_ids)
+    sinfo = ctx.surface_info()
+    layout = sinfo["layout"]
     stream = torch.cuda.current_stream()
     sptr = stream.cuda_stream
 
@@ -335,7 +337,7 @@ def main():
         sms = _t.cuda.get_device_properties(local).multi_processor_count
         peak = sms * FP32_LANES_PER_SM * sm_max * 1e6 / OPS_PER_EVAL
         roof = {
-            "bound": "fp32", "kernel": "k_label<2> (fp32 VOS tile loop)", "achieved": achieved, "peak": peak,
+            "bound": "fp32", "kernel": f"k_label<1,{1 if layout == 'strips' else 0}> (fp32x2 VOS tile loop, {layout} layout)", "achieved": achieved, "peak": peak,
             "unit": "evals/s", "frac": achieved / peak, "traffic": None,
             "peak_basis": f"{sms} SMs x {FP32_LANES_PER_SM} FP32 lanes x {sm_max:.0f} MHz (MEASURED_PEAKS.json sm_max_mhz)"
                           f" / {OPS_PER_EVAL} FP32-pipe ops per eval (SURVEY.md §8d); per GPU",
@@ -354,6 +356,7 @@ def main():
             "labeling_stats_last_step": {k: last[k] for k in ("flagged_points", "flagged_pairs", "ties", "near_subtiles",
                                                               "far_subtiles", "ms_label", "ms_fixup")},
             "lattice_generation_s": gen_s, "timed_wall_s": wall,
+            "surface_layout": sinfo,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

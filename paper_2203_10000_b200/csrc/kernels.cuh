@@ -225,17 +225,18 @@ __device__ __forceinline__ std::uint32_t spread10(std::uint32_t v) {
   return v;
 }
 
-__global__ void k_morton_keys(const double* pts, std::size_t n, double lx, double ly, double lz, double inv,
-                              std::uint32_t* keys, std::uint32_t* idx) {
+__global__ void k_morton_keys(const double* pts, std::size_t n, const std::uint32_t* subset, double lx, double ly,
+                              double lz, double inv, std::uint32_t* keys, std::uint32_t* idx) {
   for (std::size_t i = blockIdx.x * static_cast<std::size_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<std::size_t>(gridDim.x) * blockDim.x) {
+    const std::size_t j = subset ? subset[i] : i;
     auto q = [&](double v, double l) {
       const double t = (v - l) * inv;
       return static_cast<std::uint32_t>(t < 0.0 ? 0.0 : (t > 1023.0 ? 1023.0 : t));
     };
-    keys[i] = spread10(q(pts[3 * i], lx)) | (spread10(q(pts[3 * i + 1], ly)) << 1) |
-              (spread10(q(pts[3 * i + 2], lz)) << 2);
-    idx[i] = static_cast<std::uint32_t>(i);
+    keys[i] = spread10(q(pts[3 * j], lx)) | (spread10(q(pts[3 * j + 1], ly)) << 1) |
+              (spread10(q(pts[3 * j + 2], lz)) << 2);
+    idx[i] = static_cast<std::uint32_t>(j);
   }
 }
 
@@ -327,7 +328,8 @@ __global__ void __launch_bounds__(kSelBlock) k_select_write(Pred pred, std::size
 
 struct PredNonzero {
   const std::uint32_t* v;
-  __device__ bool operator()(std::size_t i) const { return v[i] != 0u; }
+  const std::uint32_t* subset;  // nullable: item i is v[subset[i]]
+  __device__ bool operator()(std::size_t i) const { return v[subset ? subset[i] : i] != 0u; }
 };
 
 struct PredStraddle {
@@ -347,7 +349,8 @@ struct PredStraddle {
 // ---------------------------------------------------------------------------
 struct FixupParams {
   const double* pts;
-  const std::uint32_t* list;    // flagged point ids
+  const std::uint32_t* list;    // flagged positions (point ids, or indices into subset)
+  const std::uint32_t* subset;  // nullable
   const std::uint32_t* count;   // device count of list
   const std::uint32_t* flagmask;
   const double* xyz;            // original fp64 vertices
@@ -366,7 +369,7 @@ __global__ void __launch_bounds__(256) k_fixup(const FixupParams prm) {
   const std::uint32_t cnt = *prm.count;
   unsigned long long pairs = 0, ties = 0;
   for (std::uint32_t w = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); w < cnt; w += nwarps) {
-    const std::uint32_t i = prm.list[w];
+    const std::uint32_t i = prm.subset ? prm.subset[prm.list[w]] : prm.list[w];
     std::uint32_t fm = prm.flagmask[i];
     std::uint32_t m = prm.masks[i];
     const double px = prm.pts[3 * static_cast<std::size_t>(i)], py = prm.pts[3 * static_cast<std::size_t>(i) + 1],
@@ -409,6 +412,109 @@ __global__ void k_label_tets(const uint4* __restrict__ tets, std::size_t nt, con
     const std::uint32_t m = __ldg(masks + t.x) & __ldg(masks + t.y) & __ldg(masks + t.z) & __ldg(masks + t.w);
     labels[i] = m ? ids.id[__ffs(m) - 1] : 0;
   }
+}
+
+}  // namespace nm
+
+// ---------------------------------------------------------------------------
+// relabel_recursive support
+// ---------------------------------------------------------------------------
+namespace nm {
+
+// Outward face i of a tet (mesh.hpp:57-64), sorted into (a <= b <= c).
+__device__ __forceinline__ void face_key(const uint4 t, int f, std::uint32_t& a, std::uint32_t& b, std::uint32_t& c) {
+  const std::uint32_t v[4] = {t.x, t.y, t.z, t.w};
+  const int F[4][3] = {{1, 2, 3}, {0, 3, 2}, {0, 1, 3}, {0, 2, 1}};
+  a = v[F[f][0]];
+  b = v[F[f][1]];
+  c = v[F[f][2]];
+  if (a > b) { const std::uint32_t s = a; a = b; b = s; }
+  if (b > c) { const std::uint32_t s = b; b = c; c = s; }
+  if (a > b) { const std::uint32_t s = a; a = b; b = s; }
+}
+
+__global__ void k_face_keys(const uint4* tets, std::size_t nt, std::uint32_t* ka, std::uint32_t* kb, std::uint32_t* kc,
+                            std::uint32_t* fid) {
+  for (std::size_t i = blockIdx.x * static_cast<std::size_t>(blockDim.x) + threadIdx.x; i < 4 * nt;
+       i += static_cast<std::size_t>(gridDim.x) * blockDim.x) {
+    std::uint32_t a, b, c;
+    face_key(tets[i >> 2], static_cast<int>(i & 3), a, b, c);
+    ka[i] = a;
+    kb[i] = b;
+    kc[i] = c;
+    fid[i] = static_cast<std::uint32_t>(i);
+  }
+}
+
+// out[p] = key[fid[p]] (next LSD radix key for the current face order).
+__global__ void k_gather_key(const std::uint32_t* key, const std::uint32_t* fid, std::size_t m, std::uint32_t* out) {
+  for (std::size_t p = blockIdx.x * static_cast<std::size_t>(blockDim.x) + threadIdx.x; p < m;
+       p += static_cast<std::size_t>(gridDim.x) * blockDim.x)
+    out[p] = key[fid[p]];
+}
+
+// Faces sorted by (a,b,c): equal neighbours are the two sides of one face.
+__global__ void k_face_pairs(const std::uint32_t* fid, std::size_t m, const std::uint32_t* ka, const std::uint32_t* kb,
+                             const std::uint32_t* kc, std::int32_t* nbr) {
+  for (std::size_t p = blockIdx.x * static_cast<std::size_t>(blockDim.x) + threadIdx.x; p + 1 < m;
+       p += static_cast<std::size_t>(gridDim.x) * blockDim.x) {
+    const std::uint32_t f = fid[p], g = fid[p + 1];
+    if (ka[f] == ka[g] && kb[f] == kb[g] && kc[f] == kc[g]) {
+      nbr[f] = static_cast<std::int32_t>(g >> 2);
+      nbr[g] = static_cast<std::int32_t>(f >> 2);
+    }
+  }
+}
+
+// Nodes of tets adjacent to a label-change face.
+__global__ void k_frontier(const uint4* tets, std::size_t nt, const std::int32_t* nbr, const int* labels,
+                           std::uint8_t* want) {
+  for (std::size_t t = blockIdx.x * static_cast<std::size_t>(blockDim.x) + threadIdx.x; t < nt;
+       t += static_cast<std::size_t>(gridDim.x) * blockDim.x) {
+    const int l = labels[t];
+    bool adj = false;
+#pragma unroll
+    for (int f = 0; f < 4; ++f) {
+      const std::int32_t o = nbr[4 * t + f];
+      adj |= (o >= 0) && (labels[o] != l);
+    }
+    if (adj) {
+      const uint4 e = tets[t];
+      want[e.x] = 1;
+      want[e.y] = 1;
+      want[e.z] = 1;
+      want[e.w] = 1;
+    }
+  }
+}
+
+struct PredWantNew {
+  const std::uint8_t* want;
+  const std::uint8_t* known;
+  __device__ bool operator()(std::size_t i) const { return want[i] && !known[i]; }
+};
+
+__global__ void k_mark_known(const std::uint32_t* ids, const std::uint32_t* count, std::uint8_t* known) {
+  const std::uint32_t n = *count;
+  for (std::uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) known[ids[i]] = 1;
+}
+
+// Label update barrier: every tet whose four nodes are evaluated.
+__global__ void k_relabel_tets(const uint4* tets, std::size_t nt, const std::uint32_t* masks, const std::uint8_t* known,
+                               int* labels, const LabelIds ids, unsigned long long* changed) {
+  unsigned long long c = 0;
+  for (std::size_t t = blockIdx.x * static_cast<std::size_t>(blockDim.x) + threadIdx.x; t < nt;
+       t += static_cast<std::size_t>(gridDim.x) * blockDim.x) {
+    const uint4 e = tets[t];
+    if (!(known[e.x] && known[e.y] && known[e.z] && known[e.w])) continue;
+    const std::uint32_t m = masks[e.x] & masks[e.y] & masks[e.z] & masks[e.w];
+    const int l = m ? ids.id[__ffs(m) - 1] : 0;
+    if (l != labels[t]) {
+      labels[t] = l;
+      ++c;
+    }
+  }
+  if (c) atomicAdd(changed, c);
 }
 
 }  // namespace nm

@@ -201,6 +201,7 @@ struct nm_ctx {
   // surfaces
   bool has_surfaces = false;
   bool strips = false;  // tile layout of the current surfaces
+  std::size_t flag_cap = 0;  // flagmask length when evaluating a subset (= node count)
   int K = 0;
   std::size_t nt_real = 0, nt_pad = 0, nv = 0;
   double cx = 0, cy = 0, cz = 0;
@@ -209,11 +210,11 @@ struct nm_ctx {
   DBuf tri, sub, comp_tiles, xyz64, tri_idx, comp_off;
 
   // scratch
-  DBuf pts, masks, flagmask, order, keys, keys_alt, order_alt, cub_tmp, list, chunk, counters, count, tets, labels,
+  DBuf pts, masks, flagmask, nbr, known, want, fkeys, frontier, order, keys, keys_alt, order_alt, cub_tmp, list, chunk, counters, count, tets, labels,
       s_out;
 
   ~nm_ctx() {
-    for (DBuf* b : {&tri, &sub, &comp_tiles, &xyz64, &tri_idx, &comp_off, &pts, &masks, &flagmask, &order, &keys,
+    for (DBuf* b : {&tri, &sub, &comp_tiles, &xyz64, &tri_idx, &comp_off, &pts, &masks, &flagmask, &nbr, &known, &want, &fkeys, &frontier, &order, &keys,
                     &keys_alt, &order_alt, &cub_tmp, &list, &chunk, &counters, &count, &tets, &labels, &s_out})
       b->release();
     for (auto& e : ev)
@@ -252,8 +253,10 @@ void select(nm_ctx* c, Pred pred, std::size_t n, std::uint32_t* out, std::uint32
 
 // Full node pass on device-resident points: Morton order -> K1 -> compaction
 // of flagged points -> K3. masks/s_out are device pointers.
+// d_subset (nullable): evaluate only points d_pts[d_subset[i]], i < n; masks
+// (and s) are written at the original point index.
 void label_nodes_dev(nm_ctx* c, const double* d_pts, std::size_t n, double T, std::uint32_t* d_masks, double* d_s,
-                     cudaStream_t st, nm_stats* stats) {
+                     cudaStream_t st, nm_stats* stats, const std::uint32_t* d_subset = nullptr) {
   require_surfaces(c);
   if (!(T > 0.0 && T < 1.0)) throw Error("threshold must lie in (0, 1) (SPEC.md:216)");
   std::uint64_t launches = 0;
@@ -268,14 +271,14 @@ void label_nodes_dev(nm_ctx* c, const double* d_pts, std::size_t n, double T, st
     return;
   }
   if (n > 0xffffffffull) throw Error("more than 2^32 points in one call");
-  auto* flagmask = c->flagmask.as<std::uint32_t>(n);
-  const std::uint32_t* order = nullptr;
+  auto* flagmask = c->flagmask.as<std::uint32_t>(d_subset ? c->flag_cap : n);
+  const std::uint32_t* order = d_subset;
   if (c->opt.sort_points && n > 1) {
     auto* keys = c->keys.as<std::uint32_t>(n);
     auto* keys2 = c->keys_alt.as<std::uint32_t>(n);
     auto* idx = c->order.as<std::uint32_t>(n);
     auto* idx2 = c->order_alt.as<std::uint32_t>(n);
-    nm::k_morton_keys<<<grid_for(n, 256, c->sm_count * 16), 256, 0, st>>>(d_pts, n, c->lo[0], c->lo[1], c->lo[2],
+    nm::k_morton_keys<<<grid_for(n, 256, c->sm_count * 16), 256, 0, st>>>(d_pts, n, d_subset, c->lo[0], c->lo[1], c->lo[2],
                                                                            1024.0 / c->span, keys, idx);
     ++launches;
     cub::DoubleBuffer<std::uint32_t> kb(keys, keys2), vb(idx, idx2);
@@ -324,10 +327,11 @@ void label_nodes_dev(nm_ctx* c, const double* d_pts, std::size_t n, double T, st
   // compaction of flagged points + fp64 fix-up
   auto* list = c->list.as<std::uint32_t>(n);
   auto* d_count = c->count.as<std::uint32_t>(4);
-  select(c, nm::PredNonzero{flagmask}, n, list, d_count, st, launches);
+  select(c, nm::PredNonzero{flagmask, d_subset}, n, list, d_count, st, launches);
   nm::FixupParams fp{};
   fp.pts = d_pts;
   fp.list = list;
+  fp.subset = d_subset;
   fp.count = d_count;
   fp.flagmask = flagmask;
   fp.xyz = static_cast<const double*>(c->xyz64.p);
@@ -788,11 +792,104 @@ int nm_flag_boundary(nm_ctx* c, const std::uint32_t* tets, std::size_t nt, const
   });
 }
 
-int nm_relabel(nm_ctx* c, const double*, std::size_t, const std::uint32_t*, std::size_t, double, int, int*, int*, int*,
-               std::uint8_t*, nm_stats*) {
+int nm_relabel(nm_ctx* c, const double* nodes, std::size_t n, const std::uint32_t* tets, std::size_t nt, double T,
+               int max_iters, int* labels_io, int* passes, int* converged, std::uint8_t* evaluated, nm_stats* stats) {
   return guarded([&] {
     require_surfaces(c);
-    throw Error("nm_relabel: not implemented yet");
+    check_tets(tets, nt, n);
+    if (n > 0xffffffffull || 4 * nt > 0xffffffffull) throw Error("mesh too large for 32-bit face ids");
+    if (max_iters < 1) throw Error("max_iters must be >= 1");
+    NM_CUDA(cudaSetDevice(c->opt.device));
+    cudaStream_t st = c->stream;
+    if (stats) std::memset(stats, 0, sizeof *stats);
+    const std::size_t m = 4 * nt;
+    auto* d_pts = c->pts.as<double>(3 * std::max<std::size_t>(n, 1));
+    auto* d_tets = c->tets.as<std::uint32_t>(4 * std::max<std::size_t>(nt, 1));
+    auto* d_labels = c->labels.as<int>(std::max<std::size_t>(nt, 1));
+    auto* d_masks = c->masks.as<std::uint32_t>(std::max<std::size_t>(n, 1));
+    auto* d_known = c->known.as<std::uint8_t>(std::max<std::size_t>(n, 1));
+    auto* d_want = c->want.as<std::uint8_t>(std::max<std::size_t>(n, 1));
+    auto* d_nbr = c->nbr.as<std::int32_t>(std::max<std::size_t>(m, 1));
+    auto* d_list = c->frontier.as<std::uint32_t>(std::max<std::size_t>(n, 1));  // frontier node ids
+    auto* d_count = c->count.as<std::uint32_t>(4);
+    auto* counters = c->counters.as<unsigned long long>(8);
+    if (n) NM_CUDA(cudaMemcpyAsync(d_pts, nodes, 3 * n * sizeof(double), cudaMemcpyHostToDevice, st));
+    if (nt) NM_CUDA(cudaMemcpyAsync(d_tets, tets, 4 * nt * sizeof(std::uint32_t), cudaMemcpyHostToDevice, st));
+    if (nt) NM_CUDA(cudaMemcpyAsync(d_labels, labels_io, nt * sizeof(int), cudaMemcpyHostToDevice, st));
+    NM_CUDA(cudaMemsetAsync(d_known, 0, std::max<std::size_t>(n, 1), st));
+    NM_CUDA(cudaMemsetAsync(d_masks, 0, std::max<std::size_t>(n, 1) * sizeof(std::uint32_t), st));
+    NM_CUDA(cudaMemsetAsync(d_nbr, 0xff, std::max<std::size_t>(m, 1) * sizeof(std::int32_t), st));
+    const uint4* t4 = reinterpret_cast<const uint4*>(d_tets);
+    // Face adjacency (mesh.hpp:68-88) by an LSD sort of sorted face triples.
+    if (m > 1) {
+      auto* ka = c->fkeys.as<std::uint32_t>(6 * m);
+      std::uint32_t *kb = ka + m, *kc = ka + 2 * m, *fid = ka + 3 * m, *key = ka + 4 * m, *fid2 = ka + 5 * m;
+      auto* key2 = c->keys_alt.as<std::uint32_t>(m);
+      nm::k_face_keys<<<grid_for(m, 256, c->sm_count * 32), 256, 0, st>>>(t4, nt, ka, kb, kc, fid);
+      std::uint32_t* cur = fid;
+      std::uint32_t* alt = fid2;
+      for (std::uint32_t* k : {kc, kb, ka}) {
+        nm::k_gather_key<<<grid_for(m, 256, c->sm_count * 32), 256, 0, st>>>(k, cur, m, key);
+        cub::DoubleBuffer<std::uint32_t> kb2(key, key2), vb(cur, alt);
+        std::size_t tmp = 0;
+        NM_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, kb2, vb, static_cast<int>(m), 0, 32, st));
+        void* tp = c->cub_tmp.get(tmp);
+        NM_CUDA(cub::DeviceRadixSort::SortPairs(tp, tmp, kb2, vb, static_cast<int>(m), 0, 32, st));
+        if (vb.Current() != cur) std::swap(cur, alt);
+      }
+      nm::k_face_pairs<<<grid_for(m, 256, c->sm_count * 32), 256, 0, st>>>(cur, m, ka, kb, kc, d_nbr);
+      NM_CUDA(cudaGetLastError());
+    }
+    c->flag_cap = std::max<std::size_t>(n, 1);
+    int pass = 0;
+    *converged = 0;
+    std::uint64_t evaluated_total = 0;
+    for (pass = 1; pass <= max_iters; ++pass) {
+      NM_CUDA(cudaMemsetAsync(d_want, 0, std::max<std::size_t>(n, 1), st));
+      if (nt) nm::k_frontier<<<grid_for(nt, 256, c->sm_count * 32), 256, 0, st>>>(t4, nt, d_nbr, d_labels, d_want);
+      std::uint64_t l = 0;
+      select(c, nm::PredWantNew{d_want, d_known}, n, d_list, d_count, st, l);
+      std::uint32_t todo = 0;
+      NM_CUDA(cudaMemcpyAsync(&todo, d_count, sizeof todo, cudaMemcpyDeviceToHost, st));
+      NM_CUDA(cudaStreamSynchronize(st));
+      if (todo) {
+        nm_stats s{};
+        label_nodes_dev(c, d_pts, todo, T, d_masks, nullptr, st, stats ? &s : nullptr, d_list);
+        if (stats) {
+          stats->points += s.points;
+          stats->evals += s.evals;
+          stats->flagged_points += s.flagged_points;
+          stats->flagged_pairs += s.flagged_pairs;
+          stats->ties += s.ties;
+          stats->near_subtiles += s.near_subtiles;
+          stats->far_subtiles += s.far_subtiles;
+          stats->ms_label += s.ms_label;
+          stats->ms_fixup += s.ms_fixup;
+        }
+        NM_CUDA(cudaMemcpyAsync(d_count, &todo, sizeof todo, cudaMemcpyHostToDevice, st));
+        nm::k_mark_known<<<grid_for(todo, 256, c->sm_count * 8), 256, 0, st>>>(d_list, d_count, d_known);
+        evaluated_total += todo;
+      }
+      NM_CUDA(cudaMemsetAsync(counters + 7, 0, sizeof(unsigned long long), st));
+      if (nt)
+        nm::k_relabel_tets<<<grid_for(nt, 256, c->sm_count * 32), 256, 0, st>>>(t4, nt, d_masks, d_known, d_labels,
+                                                                               c->ids, counters + 7);
+      unsigned long long changed = 0;
+      NM_CUDA(cudaMemcpyAsync(&changed, counters + 7, sizeof changed, cudaMemcpyDeviceToHost, st));
+      NM_CUDA(cudaStreamSynchronize(st));
+      if (changed == 0) {
+        *converged = 1;
+        break;
+      }
+    }
+    *passes = std::min(pass, max_iters);
+    if (nt) NM_CUDA(cudaMemcpyAsync(labels_io, d_labels, nt * sizeof(int), cudaMemcpyDeviceToHost, st));
+    if (evaluated && n) NM_CUDA(cudaMemcpyAsync(evaluated, d_known, n, cudaMemcpyDeviceToHost, st));
+    NM_CUDA(cudaStreamSynchronize(st));
+    if (stats) {
+      stats->triangles = c->nt_real;
+      stats->points = evaluated_total;
+    }
   });
 }
 

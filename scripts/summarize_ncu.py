@@ -1,0 +1,62 @@
+"""Summarise ncu artefacts (run here, no GPU needed) into profiles/.
+
+    python scripts/summarize_ncu.py launches <launches.csv>      # per-kernel share of a step
+    python scripts/summarize_ncu.py report <prof.ncu-rep>        # key counters of a --set full capture
+"""
+import csv
+import subprocess
+import sys
+from collections import defaultdict
+
+KEYS = [
+    "gpu__time_duration.sum", "sm__cycles_active.avg", "launch__registers_per_thread", "launch__grid_size",
+    "launch__block_size", "sm__warps_active.avg.pct_of_peak_sustained_active",
+    "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active",
+    "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active",
+    "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
+    "smsp__issue_active.avg.pct_of_peak_sustained_active", "smsp__inst_executed.sum",
+    "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", "lts__t_bytes.sum", "dram__bytes_read.sum",
+    "dram__bytes_write.sum", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
+]
+
+
+def launches(path):
+    rows = [r for r in csv.reader(open(path)) if len(r) > 10]
+    h = rows[0]
+    ki, vi = h.index("Kernel Name"), h.index("Metric Value")
+    agg = defaultdict(lambda: [0, 0.0])
+    for r in rows[1:]:
+        try:
+            v = float(r[vi].replace(",", ""))
+        except ValueError:
+            continue
+        agg[r[ki]][0] += 1
+        agg[r[ki]][1] += v
+    tot = sum(v[1] for v in agg.values())
+    print(f"{'launches':>8} {'total ms':>12} {'share':>8}  kernel")
+    for k, (c, v) in sorted(agg.items(), key=lambda x: -x[1][1]):
+        print(f"{c:8d} {v / 1e6:12.3f} {100 * v / tot:7.2f}%  {k[:110]}")
+
+
+def report(path):
+    out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(out.splitlines()))
+    h, units = rows[0], rows[1]
+    for row in rows[2:]:
+        d = dict(zip(h, row))
+        u = dict(zip(h, units))
+        print("kernel:", d.get("Kernel Name", "?")[:100])
+        for k in KEYS:
+            if k in d:
+                print(f"  {k:70s} {d[k]:>20s} {u.get(k, '')}")
+        stalls = {k: d[k] for k in d if k.startswith("smsp__average_warps_issue_stalled") and k.endswith("per_issue_active.ratio")}
+        print("  stall reasons (warps per issued instruction):")
+        for k, v in sorted(stalls.items(), key=lambda kv: -float(kv[1] or 0))[:10]:
+            print(f"    {k.replace('smsp__average_warps_issue_stalled_', '').replace('_per_issue_active.ratio', ''):30s} {v}")
+
+
+if __name__ == "__main__":
+    {"launches": launches, "report": report}[sys.argv[1]](sys.argv[2])

@@ -137,3 +137,29 @@ def test_layouts_agree_with_oracle(layout):
     assert np.max(np.abs(s_gpu - s_ref)) <= S_EXPECT
     bad, _ = _compare_masks(m_gpu, m_ref, s_ref)
     assert bad == 0
+
+
+@pytest.mark.parametrize("div", [6, 10])
+def test_relabel_matches_oracle(ctx, div):
+    """nm_relabel (device frontier + relabel passes) == oracle relabel_recursive
+    == initial labeling on the two-sphere fixture (acceptance #2)."""
+    R = 30.0
+    S = synth.concat_surfaces([synth.icosphere(0.6 * R, 3), synth.icosphere(R, 3)], labels=[1, 2])
+    coarse = synth.concat_surfaces([synth.icosphere(0.6 * R, 1), synth.icosphere(R, 1)], labels=[1, 2])
+    h = R / div
+    n = int(np.ceil(2.6 * R / h))
+    nodes, tets = synth.lattice_mesh((-1.3 * R,) * 3, h, (n, n, n))
+    init = oracle.label_tets(tets, oracle.label_nodes(nodes, S), S.label_ids)
+    prev = oracle.label_tets(tets, oracle.label_nodes(nodes, coarse), coarse.label_ids)
+    lab_o, passes_o, conv_o, ev_o = oracle.relabel_recursive(nodes, tets, S, prev)
+    ctx.set_surfaces(S.xyz, S.tri, S.comp_off, S.label_ids)
+    lab, passes, conv, ev, st = ctx.relabel(nodes, tets, prev, want_evaluated=True)
+    assert conv and conv_o and passes == passes_o
+    np.testing.assert_array_equal(lab, lab_o)
+    np.testing.assert_array_equal(lab, init)
+    np.testing.assert_array_equal(ev, ev_o)
+    assert st["points"] == int(ev.sum()) < nodes.shape[0]
+    # converged input: one pass, nothing changes
+    lab2, passes2, conv2, _, _ = ctx.relabel(nodes, tets, init)
+    assert conv2 and passes2 == 1
+    np.testing.assert_array_equal(lab2, init)
