@@ -131,6 +131,33 @@ int nm_label_tets_device(nm_ctx* ctx, const uint32_t* d_tets, size_t nt, const u
 int nm_flag_boundary_device(nm_ctx* ctx, const uint32_t* d_tets, size_t nt, const uint32_t* d_masks,
                             uint32_t active_mask, uint32_t* d_ids, uint32_t* d_count, void* stream);
 
+/* ---- refinement (host code; the recursive driver's refine step) ----------
+ * refine_volume: selected tets split 1:8
+ * (shortest octahedron diagonal), unselected tets with one split edge, two
+ * split edges of one face or one fully split face get the conforming Fig. 2
+ * templates, any other pattern escalates to 1:8. Old node ids are kept;
+ * midpoints are appended in ascending edge-key order; children inherit the
+ * parent's label; parent[i] = parent tet of child i. */
+typedef struct nm_mesh nm_mesh;
+int nm_refine(const double* nodes, size_t n_nodes, const uint32_t* tets, size_t nt, const int* labels /* nullable */,
+              const uint32_t* selected, size_t n_selected, nm_mesh** out);
+int nm_mesh_sizes(const nm_mesh* m, size_t* n_nodes, size_t* n_tets, size_t* n_old_nodes);
+int nm_mesh_copy(const nm_mesh* m, double* nodes, uint32_t* tets, int* labels, uint32_t* parent);
+void nm_mesh_free(nm_mesh* m);
+const char* nm_refine_last_error(void);
+int nm_mesh_masks(const nm_mesh* m, uint32_t* masks);
+
+/* The recursive boundary driver: `levels`
+ * times { flag the tets whose node masks straddle an active compartment
+ * (device compaction), refine them (nm_refine), evaluate ONLY the new nodes
+ * on the device, relabel the tets on the device }. masks (nullable) are the
+ * input mesh's node masks (computed when NULL). The result, with labels and
+ * final node masks (nm_mesh_masks), is returned in *out (free with
+ * nm_mesh_free). stats accumulates the node passes (evals of new nodes only). */
+int nm_refine_relabel(nm_ctx* ctx, const double* nodes, size_t n_nodes, const uint32_t* tets, size_t nt,
+                      const uint32_t* masks /* nullable */, double threshold, uint32_t active_mask, int levels,
+                      nm_mesh** out, nm_stats* stats);
+
 /* Compartment count, real and padded (evaluated) triangle slots, and the tile
  * layout (1 triangles, 2 strips) chosen for the current surfaces. */
 int nm_surface_info(nm_ctx* ctx, int* K, size_t* triangles, size_t* padded_triangles, int* layout);

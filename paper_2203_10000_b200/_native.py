@@ -89,6 +89,16 @@ LABEL_API = {
                                             ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(NmStats)]),
     "nm_flag_boundary_device": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p,
                                                ctypes.c_uint32, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
+    "nm_refine": (ctypes.c_int, [c_double_p, ctypes.c_size_t, c_u32_p, ctypes.c_size_t, c_i32_p, c_u32_p,
+                                 ctypes.c_size_t, ctypes.POINTER(ctypes.c_void_p)]),
+    "nm_mesh_sizes": (ctypes.c_int, [ctypes.c_void_p, c_size_p, c_size_p, c_size_p]),
+    "nm_mesh_copy": (ctypes.c_int, [ctypes.c_void_p, c_double_p, c_u32_p, c_i32_p, c_u32_p]),
+    "nm_mesh_free": (None, [ctypes.c_void_p]),
+    "nm_refine_last_error": (ctypes.c_char_p, []),
+    "nm_mesh_masks": (ctypes.c_int, [ctypes.c_void_p, c_u32_p]),
+    "nm_refine_relabel": (ctypes.c_int, [ctypes.c_void_p, c_double_p, ctypes.c_size_t, c_u32_p, ctypes.c_size_t,
+                                         c_u32_p, ctypes.c_double, ctypes.c_uint32, ctypes.c_int,
+                                         ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(NmStats)]),
     "nm_surface_info": (ctypes.c_int, [ctypes.c_void_p, c_i32_p, c_size_p, c_size_p, c_i32_p]),
 }
 
@@ -246,6 +256,30 @@ class Context:
                                   ptr(ev, ctypes.c_uint8) if ev is not None else None, ctypes.byref(st)))
         return labels, passes.value, bool(conv.value), ev, st.as_dict()
 
+    def refine_relabel(self, nodes, tets, masks=None, levels=2, active_mask=0xFFFFFFFF, threshold=0.5):
+        """Recursive boundary driver: returns (nodes, tets, labels, masks, stats)."""
+        nodes = np.ascontiguousarray(nodes, dtype=np.float64).reshape(-1, 3)
+        tets = np.ascontiguousarray(tets, dtype=np.uint32).reshape(-1, 4)
+        m = np.ascontiguousarray(masks, dtype=np.uint32) if masks is not None else None
+        h = ctypes.c_void_p()
+        st = NmStats()
+        check(self.lib.nm_refine_relabel(self.handle, ptr(nodes, ctypes.c_double), nodes.shape[0],
+                                         ptr(tets, ctypes.c_uint32), tets.shape[0],
+                                         ptr(m, ctypes.c_uint32) if m is not None else None, threshold, active_mask,
+                                         levels, ctypes.byref(h), ctypes.byref(st)))
+        try:
+            nn, ntt, nold = ctypes.c_size_t(), ctypes.c_size_t(), ctypes.c_size_t()
+            self.lib.nm_mesh_sizes(h, ctypes.byref(nn), ctypes.byref(ntt), ctypes.byref(nold))
+            on = np.empty((nn.value, 3), np.float64)
+            ot = np.empty((ntt.value, 4), np.uint32)
+            ol = np.empty(ntt.value, np.int32)
+            om = np.empty(nn.value, np.uint32)
+            self.lib.nm_mesh_copy(h, ptr(on, ctypes.c_double), ptr(ot, ctypes.c_uint32), ptr(ol, ctypes.c_int), None)
+            self.lib.nm_mesh_masks(h, ptr(om, ctypes.c_uint32))
+        finally:
+            self.lib.nm_mesh_free(h)
+        return on, ot, ol, om, st.as_dict()
+
     # -- device-resident entry points (torch tensors) ---------------------
     def label_nodes_device(self, d_pts, d_masks, threshold=0.5, d_s=None, stream=None, stats=True):
         """d_pts: CUDA float64 tensor (n,3); d_masks: CUDA uint32/int32 tensor (n,)."""
@@ -265,6 +299,34 @@ class Context:
     def flag_boundary_device(self, d_tets, d_masks, d_ids, d_count, active_mask=0xFFFFFFFF, stream=None):
         check(self.lib.nm_flag_boundary_device(self.handle, d_tets.data_ptr(), d_tets.shape[0], d_masks.data_ptr(),
                                                active_mask, d_ids.data_ptr(), d_count.data_ptr(), stream))
+
+
+def refine(nodes, tets, labels, selected):
+    """refine_volume on the host. Returns (nodes, tets,
+    labels, parent, n_old_nodes); new nodes are appended after the old ones."""
+    lib = load_label_lib()
+    nodes = np.ascontiguousarray(nodes, dtype=np.float64).reshape(-1, 3)
+    tets = np.ascontiguousarray(tets, dtype=np.uint32).reshape(-1, 4)
+    labels = np.ascontiguousarray(labels, dtype=np.int32) if labels is not None else None
+    sel = np.ascontiguousarray(selected, dtype=np.uint32)
+    h = ctypes.c_void_p()
+    rc = lib.nm_refine(ptr(nodes, ctypes.c_double), nodes.shape[0], ptr(tets, ctypes.c_uint32), tets.shape[0],
+                       ptr(labels, ctypes.c_int) if labels is not None else None, ptr(sel, ctypes.c_uint32), sel.size,
+                       ctypes.byref(h))
+    if rc != 0:
+        raise NativeError(lib.nm_refine_last_error().decode())
+    try:
+        nn, ntt, nold = ctypes.c_size_t(), ctypes.c_size_t(), ctypes.c_size_t()
+        lib.nm_mesh_sizes(h, ctypes.byref(nn), ctypes.byref(ntt), ctypes.byref(nold))
+        on = np.empty((nn.value, 3), np.float64)
+        ot = np.empty((ntt.value, 4), np.uint32)
+        ol = np.empty(ntt.value, np.int32)
+        op = np.empty(ntt.value, np.uint32)
+        lib.nm_mesh_copy(h, ptr(on, ctypes.c_double), ptr(ot, ctypes.c_uint32), ptr(ol, ctypes.c_int),
+                         ptr(op, ctypes.c_uint32))
+    finally:
+        lib.nm_mesh_free(h)
+    return on, ot, ol, op, nold.value
 
 
 def exported_symbols(path=LABEL_LIB) -> set:

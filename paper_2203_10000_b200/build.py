@@ -22,7 +22,7 @@ NVCC = os.environ.get("NVCC", shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
 CXX = os.environ.get("CXX", shutil.which("g++") or "g++")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "-shared", f"-I{ROOT / 'include'}",
+NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2,-ffp-contract=off", "-shared", f"-I{ROOT / 'include'}",
               "-Xptxas", "-v"]
 
 
@@ -46,9 +46,10 @@ def _stale(out: Path, deps) -> bool:
 def build_label_lib(force=False) -> Path:
     LIB.mkdir(exist_ok=True)
     out = LIB / "libnestmesh_label.so"
-    deps = list(CSRC.glob("*.cu")) + list(CSRC.glob("*.cuh")) + [ROOT / "include" / "nestmesh_label.h"]
+    deps = list(CSRC.glob("*.cu")) + list(CSRC.glob("*.cuh")) + [CSRC / "refine.cpp", ROOT / "include" / "nestmesh_label.h"]
     if force or _stale(out, deps):
-        _run([NVCC, *ARCH, *NVCC_FLAGS, str(CSRC / "nestmesh_label.cu"), "-o", str(out)], log=LIB / "ptxas_label.log")
+        _run([NVCC, *ARCH, *NVCC_FLAGS, str(CSRC / "nestmesh_label.cu"), str(CSRC / "refine.cpp"), "-o", str(out)],
+             log=LIB / "ptxas_label.log")
     return out
 
 

@@ -9,6 +9,7 @@
 #include <cstdio>
 #include <cstring>
 #include <exception>
+#include <memory>
 #include <numeric>
 #include <queue>
 #include <unordered_map>
@@ -21,6 +22,7 @@
 
 #include "kernels.cuh"
 #include "nestmesh_label.h"
+#include "refine.h"
 
 namespace {
 
@@ -890,6 +892,102 @@ int nm_relabel(nm_ctx* c, const double* nodes, std::size_t n, const std::uint32_
       stats->triangles = c->nt_real;
       stats->points = evaluated_total;
     }
+  });
+}
+
+int nm_refine_relabel(nm_ctx* c, const double* nodes, std::size_t n, const std::uint32_t* tets, std::size_t nt,
+                      const std::uint32_t* masks_in, double T, std::uint32_t active, int levels, nm_mesh** out,
+                      nm_stats* stats) {
+  return guarded([&] {
+    if (!out) throw Error("null output pointer");
+    *out = nullptr;
+    require_surfaces(c);
+    check_tets(tets, nt, n);
+    if (levels < 0) throw Error("levels must be >= 0");
+    NM_CUDA(cudaSetDevice(c->opt.device));
+    cudaStream_t st = c->stream;
+    if (stats) std::memset(stats, 0, sizeof *stats);
+    auto acc = [&](const nm_stats& s) {
+      if (!stats) return;
+      stats->points += s.points;
+      stats->evals += s.evals;
+      stats->flagged_points += s.flagged_points;
+      stats->flagged_pairs += s.flagged_pairs;
+      stats->ties += s.ties;
+      stats->near_subtiles += s.near_subtiles;
+      stats->far_subtiles += s.far_subtiles;
+      stats->launches += s.launches;
+      stats->ms_label += s.ms_label;
+      stats->ms_fixup += s.ms_fixup;
+      stats->ms_tets += s.ms_tets;
+    };
+    std::unique_ptr<nm_mesh> cur(new nm_mesh);
+    cur->nodes.assign(nodes, nodes + 3 * n);
+    cur->tets.assign(tets, tets + 4 * nt);
+    cur->masks.resize(n);
+    cur->n_old = n;
+    // device copies of the current mesh
+    auto upload_nodes = [&](const nm_mesh& m, std::size_t from) {
+      const std::size_t nn = m.nodes.size() / 3;
+      auto* d = c->pts.as<double>(3 * std::max<std::size_t>(nn, 1));
+      (void)from;
+      if (nn) NM_CUDA(cudaMemcpyAsync(d, m.nodes.data(), 3 * nn * sizeof(double), cudaMemcpyHostToDevice, st));
+      return d;
+    };
+    double* d_pts = upload_nodes(*cur, 0);
+    auto* d_masks = c->masks.as<std::uint32_t>(std::max<std::size_t>(n, 1));
+    if (masks_in) {
+      if (n) NM_CUDA(cudaMemcpyAsync(d_masks, masks_in, n * sizeof(std::uint32_t), cudaMemcpyHostToDevice, st));
+    } else if (n) {
+      nm_stats s{};
+      label_nodes_dev(c, d_pts, n, T, d_masks, nullptr, st, stats ? &s : nullptr);
+      acc(s);
+    }
+    std::vector<std::uint32_t> sel;
+    for (int lvl = 0; lvl <= levels; ++lvl) {
+      const std::size_t nn = cur->nodes.size() / 3, ntt = cur->tets.size() / 4;
+      auto* d_tets = c->tets.as<std::uint32_t>(4 * std::max<std::size_t>(ntt, 1));
+      auto* d_labels = c->labels.as<int>(std::max<std::size_t>(ntt, 1));
+      if (ntt) NM_CUDA(cudaMemcpyAsync(d_tets, cur->tets.data(), 4 * ntt * sizeof(std::uint32_t), cudaMemcpyHostToDevice, st));
+      // relabel every tet from the (cached + new) node masks
+      nm_stats ts{};
+      label_tets_dev(c, d_tets, ntt, d_masks, d_labels, st, stats ? &ts : nullptr);
+      acc(ts);
+      cur->labels.resize(ntt);
+      if (ntt) NM_CUDA(cudaMemcpyAsync(cur->labels.data(), d_labels, ntt * sizeof(int), cudaMemcpyDeviceToHost, st));
+      if (nn) NM_CUDA(cudaMemcpyAsync(cur->masks.data(), d_masks, nn * sizeof(std::uint32_t), cudaMemcpyDeviceToHost, st));
+      NM_CUDA(cudaStreamSynchronize(st));
+      if (lvl == levels) break;
+      // straddling tets (device compaction)
+      auto* d_ids = c->list.as<std::uint32_t>(std::max<std::size_t>(ntt, 1));
+      auto* d_count = c->count.as<std::uint32_t>(4);
+      std::uint64_t l = 0;
+      select(c, nm::PredStraddle{reinterpret_cast<const uint4*>(d_tets), d_masks, active}, ntt, d_ids, d_count, st, l);
+      std::uint32_t ns = 0;
+      NM_CUDA(cudaMemcpyAsync(&ns, d_count, sizeof ns, cudaMemcpyDeviceToHost, st));
+      NM_CUDA(cudaStreamSynchronize(st));
+      sel.resize(ns);
+      if (ns) NM_CUDA(cudaMemcpy(sel.data(), d_ids, ns * sizeof(std::uint32_t), cudaMemcpyDeviceToHost));
+      // host refinement; old nodes keep ids, so their masks stay valid
+      std::unique_ptr<nm_mesh> next(nmi::refine(cur->nodes.data(), nn, cur->tets.data(), ntt, cur->labels.data(),
+                                                sel.data(), sel.size()));
+      const std::size_t n2 = next->nodes.size() / 3;
+      next->masks.resize(n2);
+      // grow device node/mask buffers preserving the cached masks
+      std::vector<std::uint32_t> keep(cur->masks);
+      d_pts = upload_nodes(*next, nn);
+      d_masks = c->masks.as<std::uint32_t>(std::max<std::size_t>(n2, 1));
+      if (nn) NM_CUDA(cudaMemcpyAsync(d_masks, keep.data(), nn * sizeof(std::uint32_t), cudaMemcpyHostToDevice, st));
+      // evaluate only the new nodes [nn, n2)
+      if (n2 > nn) {
+        nm_stats s{};
+        label_nodes_dev(c, d_pts + 3 * nn, n2 - nn, T, d_masks + nn, nullptr, st, stats ? &s : nullptr);
+        acc(s);
+      }
+      cur = std::move(next);
+    }
+    if (stats) stats->triangles = c->nt_real;
+    *out = cur.release();
   });
 }
 

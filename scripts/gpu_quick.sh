@@ -1,2 +1,1 @@
-python scripts/quick_time.py 5:2000000 3:2000000
-NM_LABEL_LIB=probes/libnl_ldg.so python scripts/quick_time.py 5:2000000 3:2000000
+python -m pytest tests -q -m gpu -x 2>&1 | tail -15

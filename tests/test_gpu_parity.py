@@ -163,3 +163,29 @@ def test_relabel_matches_oracle(ctx, div):
     lab2, passes2, conv2, _, _ = ctx.relabel(nodes, tets, init)
     assert conv2 and passes2 == 1
     np.testing.assert_array_equal(lab2, init)
+
+
+def test_refine_relabel_driver(ctx):
+    """nm_refine_relabel (device straddle compaction + host refine + device
+    evaluation of new nodes only) == oracle initial labeling of the refined
+    mesh, two levels (cfg4 analogue on a nested two-sphere)."""
+    R = 20.0
+    S = synth.concat_surfaces([synth.icosphere(0.6 * R, 3), synth.icosphere(R, 3)], labels=[1, 2])
+    nodes, tets = synth.lattice_mesh((-1.3 * R,) * 3, R / 6, (16, 16, 16))
+    ctx.set_surfaces(S.xyz, S.tri, S.comp_off, S.label_ids)
+    n2, t2, lab, masks, st = ctx.refine_relabel(nodes, tets, levels=2)
+    assert t2.shape[0] > tets.shape[0]
+    m_ref = oracle.label_nodes(n2, S)
+    np.testing.assert_array_equal(masks, m_ref)
+    np.testing.assert_array_equal(lab, oracle.label_tets(t2, m_ref, S.label_ids))
+    # only new nodes were evaluated after the initial pass
+    assert st["points"] == n2.shape[0]
+    # same mesh as the host path driven by the oracle
+    from paper_2203_10000_b200._native import refine
+    m0 = oracle.label_nodes(nodes, S)
+    l0 = oracle.label_tets(tets, m0, S.label_ids)
+    a_n, a_t, a_l, _, _ = refine(nodes, tets, l0, oracle.flag_boundary(tets, m0))
+    a_m = np.concatenate([m0, oracle.label_nodes(a_n[nodes.shape[0]:], S)])
+    b_n, b_t, _, _, _ = refine(a_n, a_t, oracle.label_tets(a_t, a_m, S.label_ids), oracle.flag_boundary(a_t, a_m))
+    np.testing.assert_array_equal(b_n, n2)
+    np.testing.assert_array_equal(b_t, t2)
