@@ -175,6 +175,54 @@ def run_reference(args):
     return 0
 
 
+def run_recursive(args):
+    """cfg4: the 20-compartment model with `levels` rounds of straddle-tet
+    refinement, relabeling only the new nodes (nm_refine_relabel). Single GPU.
+    value = evals of the new-node passes / their device time (CUDA events);
+    the driver's wall time (host refinement included) is reported beside it."""
+    import torch
+    from paper_2203_10000_b200 import synth
+    from paper_2203_10000_b200._native import Context
+    cfg = synth.config(4)
+    S = cfg.surfaces
+    nodes, tets = cfg.lattice_mesh()
+    ctx = Context(0)
+    ctx.set_surfaces(S.xyz, S.tri, S.comp_off, S.label_ids)
+    m0, st0 = ctx.label_nodes(nodes)
+    runs = []
+    for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        n2, t2, lab, masks, st = ctx.refine_relabel(nodes, tets, masks=m0, levels=args.levels)
+        wall = time.perf_counter() - t0
+        if i >= args.warmup:
+            runs.append((wall, st))
+    wall = sum(r[0] for r in runs) / len(runs)
+    st = runs[-1][1]
+    dev_ms = sum(r[1]["ms_label"] + r[1]["ms_fixup"] + r[1]["ms_tets"] for r in runs) / len(runs)
+    host_ms = sum(r[1]["ms_host"] for r in runs) / len(runs)
+    evals = st["evals"]
+    # check: the recursive result equals a full relabel of the refined mesh
+    m_full, _ = ctx.label_nodes(n2)
+    lab_full = ctx.label_tets(t2, m_full)
+    line = {
+        "metric": METRIC, "value": evals / (dev_ms / 1e3), "unit": UNIT, "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": dev_ms, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "fp32 (fp64 tile fold + fp64 fix-up)", "data": "synthetic",
+        "config": {"workload": f"cfg4: cfg3 + {args.levels} levels of straddle-tet refinement, new nodes only",
+                   "initial_nodes": int(nodes.shape[0]), "initial_tets": int(tets.shape[0]),
+                   "refined_nodes": int(n2.shape[0]), "refined_tets": int(t2.shape[0]),
+                   "new_nodes_evaluated": int(st["points"]), "triangles": S.n_triangles, "compartments": S.K},
+        "driver_wall_ms": wall * 1e3, "host_refine_ms": host_ms, "device_ms": dev_ms,
+        "initial_label_ms": st0["ms_total"],
+        "recursive_equals_full_relabel": bool(np.array_equal(lab, lab_full) and np.array_equal(masks, m_full)),
+        "labeling_stats_last_step": {k: st[k] for k in ("flagged_points", "ties", "near_subtiles", "far_subtiles")},
+    }
+    print(json.dumps(line), flush=True)
+    ctx.close()
+    del torch
+    return 0
+
+
 def workload_config(cfg, n_nodes, n_tets, world):
     S = cfg.surfaces
     names = {1: "cfg1 icosphere L3 / 32^3 lattice", 2: "cfg2 4 nested perturbed spheres / 2 mm lattice",
@@ -192,7 +240,8 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", type=int, default=5, choices=[1, 2, 3, 5])
+    ap.add_argument("--config", type=int, default=5, choices=[1, 2, 3, 4, 5])
+    ap.add_argument("--levels", type=int, default=2, help="--config 4: recursive refinement levels")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
@@ -201,6 +250,8 @@ def main():
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
         return run_reference(args)
+    if args.config == 4:
+        return run_recursive(args)
 
     import torch
     rank, local, world = dist_env()
@@ -208,7 +259,8 @@ def main():
         print(f"[bench] note: WORLD_SIZE={world} but --gpus={args.gpus}; using WORLD_SIZE", file=sys.stderr)
     torch.cuda.set_device(local)
     group = None
-    if world > 1:
+    use_dist = world > 1 or os.environ.get("NM_FORCE_DIST") == "1"
+    if use_dist:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2203_10000_b200 import synth
@@ -216,12 +268,12 @@ def main():
     from paper_2203_10000_b200.distributed import all_gather_masks, shard
 
     def barrier():
-        if world > 1:
+        if use_dist:
             import torch.distributed as dist
             dist.barrier()
 
     def allmax(x):
-        if world == 1:
+        if not use_dist:
             return x
         import torch.distributed as dist
         t = torch.tensor([x], dtype=torch.float64, device="cuda")
@@ -293,7 +345,7 @@ def main():
         h_nodes = torch.from_numpy(np.ascontiguousarray(nodes[nsh.lo:nsh.hi])).pin_memory()
         h_tets = torch.from_numpy(np.ascontiguousarray(tets[tsh.lo:tsh.hi]).view(np.int32)).pin_memory()
         h_labels = torch.empty(tsh.size, dtype=torch.int32).pin_memory()
-        if world == 1:
+        if not use_dist:
             def e2e_step():
                 labels, _, _ = ctx.label_mesh(h_nodes.numpy(), h_tets.numpy().view(np.uint32))
                 return labels
@@ -349,7 +401,7 @@ def main():
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "fp32 (fp64 tile fold + fp64 fix-up)", "data": "synthetic",
-            "config": workload_config(cfg, n, nt, world),
+            "config": dict(workload_config(cfg, n, nt, world), distributed=use_dist),
             "full_mesh_labeling_time_s": ms_per_step / 1e3,
             "e2e": e2e, "roofline": roof, "cpu_baseline": cpu, "clocks": clocks,
             "gpu_launches": MY_KERNELS_PER_STEP * args.steps,
@@ -359,7 +411,7 @@ def main():
             "surface_layout": sinfo,
         }
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if use_dist:
         import torch.distributed as dist
         dist.destroy_process_group()
     ctx.close()

@@ -79,6 +79,7 @@ typedef struct nm_stats {
   float ms_fixup;            /* device time of compaction + fp64 fix-up */
   float ms_tets;             /* device time of the tet kernels */
   float ms_total;            /* device time of the whole call */
+  float ms_host;             /* host time of refinement (nm_refine_relabel) */
 } nm_stats;
 
 int nm_abi_version(void);

@@ -54,6 +54,7 @@ class NmStats(ctypes.Structure):
         ("ms_fixup", ctypes.c_float),
         ("ms_tets", ctypes.c_float),
         ("ms_total", ctypes.c_float),
+        ("ms_host", ctypes.c_float),
     ]
 
     def as_dict(self) -> dict:

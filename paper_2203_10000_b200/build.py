@@ -68,10 +68,28 @@ def build_oracle() -> None:
     _run(["make", "-s", "-C", str(ROOT / "oracle")])
 
 
+def build_cpp_dropin_test(force=False):
+    """tests/cpp/dropin_test.cpp against the unmodified reference headers
+    (only where /root/reference exists; the binary travels to the GPU box)."""
+    ref_inc = Path("/root/reference/proj/include")
+    if not ref_inc.exists():
+        return None
+    out = ROOT / "build" / "dropin_test"
+    src = ROOT / "tests" / "cpp" / "dropin_test.cpp"
+    deps = [src, ROOT / "include" / "nestmesh" / "labeling.hpp", ROOT / "include" / "nestmesh_label.h",
+            LIB / "libnestmesh_label.so"]
+    if force or _stale(out, deps):
+        out.parent.mkdir(exist_ok=True)
+        _run([CXX, "-std=c++20", "-O2", "-Wall", "-Wextra", f"-I{ref_inc}", f"-I{ROOT / 'include'}", str(src),
+              "-o", str(out), f"-L{LIB}", "-lnestmesh_label", "-Wl,-rpath,$ORIGIN/../paper_2203_10000_b200/lib"])
+    return out
+
+
 def build_all(force=False) -> None:
     build_synth_lib(force)
     build_label_lib(force)
     build_oracle()
+    build_cpp_dropin_test(force)
 
 
 if __name__ == "__main__":

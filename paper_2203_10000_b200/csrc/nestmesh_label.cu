@@ -4,6 +4,7 @@
 // stream. There is no CPU fallback: every compute entry point fails without
 // a usable device.
 #include <algorithm>
+#include <chrono>
 #include <array>
 #include <cmath>
 #include <cstdio>
@@ -969,8 +970,11 @@ int nm_refine_relabel(nm_ctx* c, const double* nodes, std::size_t n, const std::
       sel.resize(ns);
       if (ns) NM_CUDA(cudaMemcpy(sel.data(), d_ids, ns * sizeof(std::uint32_t), cudaMemcpyDeviceToHost));
       // host refinement; old nodes keep ids, so their masks stay valid
+      const auto h0 = std::chrono::steady_clock::now();
       std::unique_ptr<nm_mesh> next(nmi::refine(cur->nodes.data(), nn, cur->tets.data(), ntt, cur->labels.data(),
                                                 sel.data(), sel.size()));
+      if (stats)
+        stats->ms_host += std::chrono::duration<float, std::milli>(std::chrono::steady_clock::now() - h0).count();
       const std::size_t n2 = next->nodes.size() / 3;
       next->masks.resize(n2);
       // grow device node/mask buffers preserving the cached masks

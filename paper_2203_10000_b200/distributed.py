@@ -57,10 +57,10 @@ def all_gather_masks(local: "torch.Tensor", sh: Shard, group=None) -> "torch.Ten
         buf = torch.zeros(sh.per, dtype=local.dtype, device=local.device)
         buf[: local.shape[0]] = local
     out = torch.empty(sh.padded_total, dtype=local.dtype, device=local.device)
-    if sh.world == 1:
-        out.copy_(buf)
-    else:
+    if dist.is_available() and dist.is_initialized():
         dist.all_gather_into_tensor(out, buf, group=group)
+    else:
+        out.copy_(buf)
     return out[: sh.n]
 
 

@@ -1,1 +1,1 @@
-python -m pytest tests -q -m gpu -x 2>&1 | tail -15
+python -m pytest tests/test_gpu_dropin.py -q -m gpu -x 2>&1 | tail -15

@@ -1,0 +1,55 @@
+// The C++ drop-in (include/nestmesh/labeling.hpp) used exactly as a nestmesh
+// maintainer would: the UNMODIFIED reference headers for the types and the
+// lattice/icosphere generators, the SPEC operations from labeling.hpp.
+// Built by __graft_entry__.build() where /root/reference exists (the binary
+// travels to the GPU box); run by tests/test_gpu_dropin.py, which compares
+// the labels it prints against the oracle.
+#include <cstdio>
+#include <cstdlib>
+
+#include "nestmesh/labeling.hpp"
+#include "nestmesh/lattice.hpp"
+#include "nestmesh/primitives.hpp"
+
+using namespace nestmesh;
+
+int main(int argc, char** argv) {
+  const char* out_path = argc > 1 ? argv[1] : "labels.bin";
+  SurfaceSegmentation seg;
+  seg.compartments.push_back(CompartmentSurface{"inner", 3, icosphere(6.0, 3), 0.33, 1, true});
+  seg.compartments.push_back(CompartmentSurface{"outer", 9, icosphere(10.0, 3), 0.0042, 2, true});
+  LatticeSpec spec;
+  spec.origin = Vec3{-12, -12, -12};
+  spec.cell_size = 0.75;
+  spec.nx = spec.ny = spec.nz = 32;
+  const TetrahedralMesh mesh = generate_lattice_mesh(spec);
+  SolidAngleParams params;
+  nm_stats st{};
+  const std::vector<int> labels = initial_label(mesh, seg, params, GpuOptions{}, &st);
+  // enclosure_ratio KATs
+  const double s_in = enclosure_ratio(Vec3{0, 0, 0}, seg.compartments[0].mesh);
+  const double s_out = enclosure_ratio(Vec3{30, 0, 0}, seg.compartments[0].mesh);
+  if (std::abs(s_in - 1.0) > 1e-6 || std::abs(s_out) > 1e-6) {
+    std::fprintf(stderr, "enclosure KAT failed: %.17g %.17g\n", s_in, s_out);
+    return 2;
+  }
+  // relabel of converged labels: one pass, no change
+  const RelabelResult r = relabel_recursive(mesh, seg, params, labels);
+  if (r.passes != 1 || r.labels != labels) {
+    std::fprintf(stderr, "relabel fixed point failed: passes=%d\n", r.passes);
+    return 3;
+  }
+  // invalid segmentation -> LabelingError (SPEC.md:103 priorities increasing)
+  SurfaceSegmentation bad = seg;
+  bad.compartments[1].priority = 0;
+  try {
+    (void)initial_label(mesh, bad, params);
+    return 4;
+  } catch (const LabelingError&) {
+  }
+  FILE* f = std::fopen(out_path, "wb");
+  std::fwrite(labels.data(), sizeof(int), labels.size(), f);
+  std::fclose(f);
+  std::printf("dropin ok: %zu tets, evals %llu\n", labels.size(), static_cast<unsigned long long>(st.evals));
+  return 0;
+}
