@@ -199,7 +199,7 @@ def run_recursive(args):
     wall = sum(r[0] for r in runs) / len(runs)
     st = runs[-1][1]
     dev_ms = sum(r[1]["ms_label"] + r[1]["ms_fixup"] + r[1]["ms_tets"] for r in runs) / len(runs)
-    host_ms = sum(r[1]["ms_host"] for r in runs) / len(runs)
+    host_ms = sum(r[1]["ms_host"] for r in runs) / len(runs)  # device refinement (CUDA events)
     evals = st["evals"]
     # check: the recursive result equals a full relabel of the refined mesh
     m_full, _ = ctx.label_nodes(n2)
@@ -212,7 +212,7 @@ def run_recursive(args):
                    "initial_nodes": int(nodes.shape[0]), "initial_tets": int(tets.shape[0]),
                    "refined_nodes": int(n2.shape[0]), "refined_tets": int(t2.shape[0]),
                    "new_nodes_evaluated": int(st["points"]), "triangles": S.n_triangles, "compartments": S.K},
-        "driver_wall_ms": wall * 1e3, "host_refine_ms": host_ms, "device_ms": dev_ms,
+        "driver_wall_ms": wall * 1e3, "refine_ms_device": host_ms, "device_ms": dev_ms,
         "initial_label_ms": st0["ms_total"],
         "recursive_equals_full_relabel": bool(np.array_equal(lab, lab_full) and np.array_equal(masks, m_full)),
         "labeling_stats_last_step": {k: st[k] for k in ("flagged_points", "ties", "near_subtiles", "far_subtiles")},

@@ -79,7 +79,7 @@ typedef struct nm_stats {
   float ms_fixup;            /* device time of compaction + fp64 fix-up */
   float ms_tets;             /* device time of the tet kernels */
   float ms_total;            /* device time of the whole call */
-  float ms_host;             /* host time of refinement (nm_refine_relabel) */
+  float ms_host;             /* refinement time inside nm_refine_relabel (device, CUDA events) */
 } nm_stats;
 
 int nm_abi_version(void);
@@ -150,8 +150,8 @@ int nm_mesh_masks(const nm_mesh* m, uint32_t* masks);
 
 /* The recursive boundary driver: `levels`
  * times { flag the tets whose node masks straddle an active compartment
- * (device compaction), refine them (nm_refine), evaluate ONLY the new nodes
- * on the device, relabel the tets on the device }. masks (nullable) are the
+ * (device compaction), refine them on the device (same rules, numbering and
+ * child order as nm_refine), evaluate ONLY the new nodes, relabel the tets }. masks (nullable) are the
  * input mesh's node masks (computed when NULL). The result, with labels and
  * final node masks (nm_mesh_masks), is returned in *out (free with
  * nm_mesh_free). stats accumulates the node passes (evals of new nodes only). */

@@ -21,7 +21,10 @@
 #include <cub/device/device_radix_sort.cuh>
 #include <cuda_runtime.h>
 
+#include <cub/device/device_scan.cuh>
+
 #include "kernels.cuh"
+#include "refine.cuh"
 #include "nestmesh_label.h"
 #include "refine.h"
 
@@ -213,11 +216,15 @@ struct nm_ctx {
   DBuf tri, sub, comp_tiles, xyz64, tri_idx, comp_off;
 
   // scratch
-  DBuf pts, masks, flagmask, nbr, known, want, fkeys, frontier, order, keys, keys_alt, order_alt, cub_tmp, list, chunk, counters, count, tets, labels,
+  DBuf pts, masks, flagmask, nbr, known, want, fkeys, frontier, r_red, r_keys, r_keys2, r_S, r_idx, r_touched,
+      r_mask, r_cnt, r_offs, r_flag, meshA_nodes, meshA_tets, meshA_labels, meshB_nodes, meshB_tets, meshB_labels,
+      meshB_parent, masks2, order, keys, keys_alt, order_alt, cub_tmp, list, chunk, counters, count, tets, labels,
       s_out;
 
   ~nm_ctx() {
-    for (DBuf* b : {&tri, &sub, &comp_tiles, &xyz64, &tri_idx, &comp_off, &pts, &masks, &flagmask, &nbr, &known, &want, &fkeys, &frontier, &order, &keys,
+    for (DBuf* b : {&tri, &sub, &comp_tiles, &xyz64, &tri_idx, &comp_off, &pts, &masks, &flagmask, &nbr, &known, &want, &fkeys, &frontier, &r_red, &r_keys, &r_keys2, &r_S,
+                    &r_idx, &r_touched, &r_mask, &r_cnt, &r_offs, &r_flag, &meshA_nodes, &meshA_tets, &meshA_labels,
+                    &meshB_nodes, &meshB_tets, &meshB_labels, &meshB_parent, &masks2, &order, &keys,
                     &keys_alt, &order_alt, &cub_tmp, &list, &chunk, &counters, &count, &tets, &labels, &s_out})
       b->release();
     for (auto& e : ev)
@@ -394,6 +401,98 @@ void check_tets(const std::uint32_t* tets, std::size_t nt, std::size_t n_nodes) 
   for (std::size_t i = 0; i < 4 * nt; ++i)
     if (tets[i] >= n_nodes) throw Error("tet " + std::to_string(i / 4) + " references node " + std::to_string(tets[i]) +
                                         " >= node count " + std::to_string(n_nodes));
+}
+
+
+struct PredByte {
+  const std::uint8_t* v;
+  __device__ bool operator()(std::size_t i) const { return v[i] != 0; }
+};
+
+// Device refine_volume (refine.cuh): (nodes n, tets nt, labels) + selected
+// tets -> refined mesh in the B buffers. Returns (n2, nt2).
+std::pair<std::size_t, std::size_t> refine_dev(nm_ctx* c, const double* d_nodes, std::size_t n, const std::uint32_t* d_tets,
+                                               std::size_t nt, const int* d_labels, const std::uint32_t* d_sel,
+                                               std::uint32_t nsel, cudaStream_t st, std::uint64_t& launches) {
+  const uint4* t4 = reinterpret_cast<const uint4*>(d_tets);
+  auto* red = c->r_red.as<std::uint8_t>(std::max<std::size_t>(nt, 1));
+  auto* touched = c->r_touched.as<std::uint8_t>(std::max<std::size_t>(n, 1));
+  auto* tmask = c->r_mask.as<std::uint8_t>(std::max<std::size_t>(nt, 1));
+  auto* flag = c->r_flag.as<unsigned>(4);
+  auto* d_count = c->count.as<std::uint32_t>(4);
+  auto* red_list = c->r_idx.as<std::uint32_t>(std::max<std::size_t>(nt, 1));
+  NM_CUDA(cudaMemsetAsync(red, 0, std::max<std::size_t>(nt, 1), st));
+  NM_CUDA(cudaMemcpyAsync(d_count, &nsel, sizeof nsel, cudaMemcpyHostToDevice, st));
+  nm::k_mark_list<<<grid_for(std::max<std::uint32_t>(nsel, 1), 256, c->sm_count * 8), 256, 0, st>>>(d_sel, d_count, red);
+  ++launches;
+  unsigned long long* S = nullptr;
+  std::uint32_t m = 0;
+  for (int it = 0; it < 1000; ++it) {
+    select(c, PredByte{red}, nt, red_list, d_count, st, launches);
+    std::uint32_t r = 0;
+    NM_CUDA(cudaMemcpyAsync(&r, d_count, sizeof r, cudaMemcpyDeviceToHost, st));
+    NM_CUDA(cudaStreamSynchronize(st));
+    const std::size_t nk = 6ull * r;
+    auto* keys = c->r_keys.as<unsigned long long>(std::max<std::size_t>(nk, 1));
+    auto* keys2 = c->r_keys2.as<unsigned long long>(std::max<std::size_t>(nk, 1));
+    nm::k_red_edges<<<grid_for(std::max<std::uint32_t>(r, 1), 256, c->sm_count * 8), 256, 0, st>>>(t4, red_list, d_count, keys);
+    ++launches;
+    const unsigned long long* sorted = keys;
+    if (nk > 1) {
+      cub::DoubleBuffer<unsigned long long> kb(keys, keys2);
+      std::size_t tmp = 0;
+      NM_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tmp, kb, static_cast<int>(nk), 0, 64, st));
+      void* tp = c->cub_tmp.get(tmp);
+      NM_CUDA(cub::DeviceRadixSort::SortKeys(tp, tmp, kb, static_cast<int>(nk), 0, 64, st));
+      sorted = kb.Current();
+    }
+    auto* uidx = c->frontier.as<std::uint32_t>(std::max<std::size_t>(nk, 1));
+    select(c, nm::PredUniqueKey{sorted}, nk, uidx, d_count, st, launches);
+    S = c->r_S.as<unsigned long long>(std::max<std::size_t>(nk, 1));
+    nm::k_gather_keys<<<grid_for(std::max<std::size_t>(nk, 1), 256, c->sm_count * 8), 256, 0, st>>>(sorted, uidx, d_count, S);
+    NM_CUDA(cudaMemsetAsync(touched, 0, std::max<std::size_t>(n, 1), st));
+    nm::k_touch_nodes<<<grid_for(std::max<std::size_t>(nk, 1), 256, c->sm_count * 8), 256, 0, st>>>(S, d_count, touched);
+    NM_CUDA(cudaMemsetAsync(flag, 0, sizeof(unsigned), st));
+    nm::k_classify<<<grid_for(std::max<std::size_t>(nt, 1), 256, c->sm_count * 32), 256, 0, st>>>(t4, nt, red, touched, S,
+                                                                                                 d_count, tmask, flag);
+    launches += 4;
+    unsigned changed = 0;
+    NM_CUDA(cudaMemcpyAsync(&changed, flag, sizeof changed, cudaMemcpyDeviceToHost, st));
+    NM_CUDA(cudaMemcpyAsync(&m, d_count, sizeof m, cudaMemcpyDeviceToHost, st));
+    NM_CUDA(cudaStreamSynchronize(st));
+    if (!changed) break;
+  }
+  // children per tet -> offsets
+  auto* cnt = c->r_cnt.as<std::uint32_t>(std::max<std::size_t>(nt, 1));
+  auto* offs = c->r_offs.as<std::uint32_t>(std::max<std::size_t>(nt, 1));
+  nm::k_child_count<<<grid_for(std::max<std::size_t>(nt, 1), 256, c->sm_count * 32), 256, 0, st>>>(tmask, nt, cnt);
+  std::size_t tmp = 0;
+  NM_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, cnt, offs, static_cast<int>(nt), st));
+  void* tp = c->cub_tmp.get(tmp);
+  NM_CUDA(cub::DeviceScan::ExclusiveSum(tp, tmp, cnt, offs, static_cast<int>(nt), st));
+  std::uint32_t last[2] = {0, 0};
+  if (nt) {
+    NM_CUDA(cudaMemcpyAsync(&last[0], offs + nt - 1, 4, cudaMemcpyDeviceToHost, st));
+    NM_CUDA(cudaMemcpyAsync(&last[1], cnt + nt - 1, 4, cudaMemcpyDeviceToHost, st));
+  }
+  NM_CUDA(cudaStreamSynchronize(st));
+  const std::size_t nt2 = static_cast<std::size_t>(last[0]) + last[1];
+  const std::size_t n2 = n + m;
+  if (n2 > 0xffffffffull || nt2 > 0xffffffffull) throw Error("refined mesh exceeds 32-bit ids");
+  auto* nodes2 = c->meshB_nodes.as<double>(3 * std::max<std::size_t>(n2, 1));
+  auto* tets2 = c->meshB_tets.as<std::uint32_t>(4 * std::max<std::size_t>(nt2, 1));
+  auto* labels2 = c->meshB_labels.as<int>(std::max<std::size_t>(nt2, 1));
+  auto* parent2 = c->meshB_parent.as<std::uint32_t>(std::max<std::size_t>(nt2, 1));
+  if (n) NM_CUDA(cudaMemcpyAsync(nodes2, d_nodes, 3 * n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  NM_CUDA(cudaMemcpyAsync(d_count, &m, sizeof m, cudaMemcpyHostToDevice, st));
+  if (m) nm::k_midpoints<<<grid_for(m, 256, c->sm_count * 8), 256, 0, st>>>(d_nodes, S, d_count, n, nodes2);
+  if (nt)
+    nm::k_emit_children<<<grid_for(nt, 256, c->sm_count * 32), 256, 0, st>>>(t4, nt, tmask, offs, d_labels, S, d_count, n,
+                                                                             nodes2, reinterpret_cast<uint4*>(tets2),
+                                                                             labels2, parent2);
+  NM_CUDA(cudaGetLastError());
+  launches += 3;
+  return {n2, nt2};
 }
 
 }  // namespace
@@ -922,76 +1021,91 @@ int nm_refine_relabel(nm_ctx* c, const double* nodes, std::size_t n, const std::
       stats->ms_fixup += s.ms_fixup;
       stats->ms_tets += s.ms_tets;
     };
-    std::unique_ptr<nm_mesh> cur(new nm_mesh);
-    cur->nodes.assign(nodes, nodes + 3 * n);
-    cur->tets.assign(tets, tets + 4 * nt);
-    cur->masks.resize(n);
-    cur->n_old = n;
-    // device copies of the current mesh
-    auto upload_nodes = [&](const nm_mesh& m, std::size_t from) {
-      const std::size_t nn = m.nodes.size() / 3;
-      auto* d = c->pts.as<double>(3 * std::max<std::size_t>(nn, 1));
-      (void)from;
-      if (nn) NM_CUDA(cudaMemcpyAsync(d, m.nodes.data(), 3 * nn * sizeof(double), cudaMemcpyHostToDevice, st));
-      return d;
-    };
-    double* d_pts = upload_nodes(*cur, 0);
-    auto* d_masks = c->masks.as<std::uint32_t>(std::max<std::size_t>(n, 1));
+    // Device-resident mesh A (current) / B (refined); masks M / M2.
+    DBuf* An = &c->meshA_nodes;
+    DBuf* At = &c->meshA_tets;
+    DBuf* Al = &c->meshA_labels;
+    DBuf* M = &c->masks;
+    DBuf* M2 = &c->masks2;
+    std::size_t cn = n, cnt_t = nt;
+    auto* d_nodes = An->as<double>(3 * std::max<std::size_t>(n, 1));
+    auto* d_tets = At->as<std::uint32_t>(4 * std::max<std::size_t>(nt, 1));
+    if (n) NM_CUDA(cudaMemcpyAsync(d_nodes, nodes, 3 * n * sizeof(double), cudaMemcpyHostToDevice, st));
+    if (nt) NM_CUDA(cudaMemcpyAsync(d_tets, tets, 4 * nt * sizeof(std::uint32_t), cudaMemcpyHostToDevice, st));
+    auto* d_masks = M->as<std::uint32_t>(std::max<std::size_t>(n, 1));
     if (masks_in) {
       if (n) NM_CUDA(cudaMemcpyAsync(d_masks, masks_in, n * sizeof(std::uint32_t), cudaMemcpyHostToDevice, st));
     } else if (n) {
       nm_stats s{};
-      label_nodes_dev(c, d_pts, n, T, d_masks, nullptr, st, stats ? &s : nullptr);
+      label_nodes_dev(c, d_nodes, n, T, d_masks, nullptr, st, stats ? &s : nullptr);
       acc(s);
     }
-    std::vector<std::uint32_t> sel;
+    bool have_parent = false;
     for (int lvl = 0; lvl <= levels; ++lvl) {
-      const std::size_t nn = cur->nodes.size() / 3, ntt = cur->tets.size() / 4;
-      auto* d_tets = c->tets.as<std::uint32_t>(4 * std::max<std::size_t>(ntt, 1));
-      auto* d_labels = c->labels.as<int>(std::max<std::size_t>(ntt, 1));
-      if (ntt) NM_CUDA(cudaMemcpyAsync(d_tets, cur->tets.data(), 4 * ntt * sizeof(std::uint32_t), cudaMemcpyHostToDevice, st));
-      // relabel every tet from the (cached + new) node masks
+      auto* d_labels = Al->as<int>(std::max<std::size_t>(cnt_t, 1));
       nm_stats ts{};
-      label_tets_dev(c, d_tets, ntt, d_masks, d_labels, st, stats ? &ts : nullptr);
+      label_tets_dev(c, reinterpret_cast<const std::uint32_t*>(At->p), cnt_t, static_cast<std::uint32_t*>(M->p), d_labels,
+                     st, stats ? &ts : nullptr);
       acc(ts);
-      cur->labels.resize(ntt);
-      if (ntt) NM_CUDA(cudaMemcpyAsync(cur->labels.data(), d_labels, ntt * sizeof(int), cudaMemcpyDeviceToHost, st));
-      if (nn) NM_CUDA(cudaMemcpyAsync(cur->masks.data(), d_masks, nn * sizeof(std::uint32_t), cudaMemcpyDeviceToHost, st));
-      NM_CUDA(cudaStreamSynchronize(st));
       if (lvl == levels) break;
       // straddling tets (device compaction)
-      auto* d_ids = c->list.as<std::uint32_t>(std::max<std::size_t>(ntt, 1));
+      auto* d_ids = c->list.as<std::uint32_t>(std::max<std::size_t>(cnt_t, 1));
       auto* d_count = c->count.as<std::uint32_t>(4);
       std::uint64_t l = 0;
-      select(c, nm::PredStraddle{reinterpret_cast<const uint4*>(d_tets), d_masks, active}, ntt, d_ids, d_count, st, l);
+      select(c, nm::PredStraddle{reinterpret_cast<const uint4*>(At->p), static_cast<const std::uint32_t*>(M->p), active},
+             cnt_t, d_ids, d_count, st, l);
       std::uint32_t ns = 0;
       NM_CUDA(cudaMemcpyAsync(&ns, d_count, sizeof ns, cudaMemcpyDeviceToHost, st));
       NM_CUDA(cudaStreamSynchronize(st));
-      sel.resize(ns);
-      if (ns) NM_CUDA(cudaMemcpy(sel.data(), d_ids, ns * sizeof(std::uint32_t), cudaMemcpyDeviceToHost));
-      // host refinement; old nodes keep ids, so their masks stay valid
-      const auto h0 = std::chrono::steady_clock::now();
-      std::unique_ptr<nm_mesh> next(nmi::refine(cur->nodes.data(), nn, cur->tets.data(), ntt, cur->labels.data(),
-                                                sel.data(), sel.size()));
-      if (stats)
-        stats->ms_host += std::chrono::duration<float, std::milli>(std::chrono::steady_clock::now() - h0).count();
-      const std::size_t n2 = next->nodes.size() / 3;
-      next->masks.resize(n2);
-      // grow device node/mask buffers preserving the cached masks
-      std::vector<std::uint32_t> keep(cur->masks);
-      d_pts = upload_nodes(*next, nn);
-      d_masks = c->masks.as<std::uint32_t>(std::max<std::size_t>(n2, 1));
-      if (nn) NM_CUDA(cudaMemcpyAsync(d_masks, keep.data(), nn * sizeof(std::uint32_t), cudaMemcpyHostToDevice, st));
-      // evaluate only the new nodes [nn, n2)
-      if (n2 > nn) {
+      // device refinement into the B buffers (refine_dev does not touch c->list)
+      cudaEvent_t h0 = c->ev[4], h1 = c->ev[5];
+      NM_CUDA(cudaEventRecord(h0, st));
+      std::uint64_t rl = 0;
+      const auto [n2, nt2] = refine_dev(c, static_cast<const double*>(An->p), cn, static_cast<const std::uint32_t*>(At->p),
+                                        cnt_t, static_cast<const int*>(Al->p), d_ids, ns, st, rl);
+      NM_CUDA(cudaEventRecord(h1, st));
+      NM_CUDA(cudaEventSynchronize(h1));
+      if (stats) {
+        float ms = 0;
+        NM_CUDA(cudaEventElapsedTime(&ms, h0, h1));
+        stats->ms_host += ms;  // refinement time (device, CUDA events)
+        stats->launches += rl;
+      }
+      // masks of old nodes are kept; only the new nodes are evaluated
+      auto* m2 = M2->as<std::uint32_t>(std::max<std::size_t>(n2, 1));
+      if (cn) NM_CUDA(cudaMemcpyAsync(m2, M->p, cn * sizeof(std::uint32_t), cudaMemcpyDeviceToDevice, st));
+      if (n2 > cn) {
         nm_stats s{};
-        label_nodes_dev(c, d_pts + 3 * nn, n2 - nn, T, d_masks + nn, nullptr, st, stats ? &s : nullptr);
+        label_nodes_dev(c, static_cast<const double*>(c->meshB_nodes.p) + 3 * cn, n2 - cn, T, m2 + cn, nullptr, st,
+                        stats ? &s : nullptr);
         acc(s);
       }
-      cur = std::move(next);
+      std::swap(c->meshA_nodes, c->meshB_nodes);
+      std::swap(c->meshA_tets, c->meshB_tets);
+      std::swap(c->meshA_labels, c->meshB_labels);
+      std::swap(c->masks, c->masks2);
+      have_parent = true;
+      cn = n2;
+      cnt_t = nt2;
     }
+    std::unique_ptr<nm_mesh> res(new nm_mesh);
+    res->nodes.resize(3 * cn);
+    res->tets.resize(4 * cnt_t);
+    res->labels.resize(cnt_t);
+    res->masks.resize(cn);
+    res->parent.resize(cnt_t);
+    res->n_old = n;
+    if (cn) NM_CUDA(cudaMemcpyAsync(res->nodes.data(), An->p, 3 * cn * sizeof(double), cudaMemcpyDeviceToHost, st));
+    if (cnt_t) {
+      NM_CUDA(cudaMemcpyAsync(res->tets.data(), At->p, 4 * cnt_t * sizeof(std::uint32_t), cudaMemcpyDeviceToHost, st));
+      NM_CUDA(cudaMemcpyAsync(res->labels.data(), Al->p, cnt_t * sizeof(int), cudaMemcpyDeviceToHost, st));
+    }
+    if (cn) NM_CUDA(cudaMemcpyAsync(res->masks.data(), M->p, cn * sizeof(std::uint32_t), cudaMemcpyDeviceToHost, st));
+    if (have_parent && cnt_t)
+      NM_CUDA(cudaMemcpyAsync(res->parent.data(), c->meshB_parent.p, cnt_t * sizeof(std::uint32_t), cudaMemcpyDeviceToHost, st));
+    NM_CUDA(cudaStreamSynchronize(st));
     if (stats) stats->triangles = c->nt_real;
-    *out = cur.release();
+    *out = res.release();
   });
 }
 

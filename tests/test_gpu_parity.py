@@ -189,3 +189,23 @@ def test_refine_relabel_driver(ctx):
     b_n, b_t, _, _, _ = refine(a_n, a_t, oracle.label_tets(a_t, a_m, S.label_ids), oracle.flag_boundary(a_t, a_m))
     np.testing.assert_array_equal(b_n, n2)
     np.testing.assert_array_equal(b_t, t2)
+
+
+def test_device_refine_matches_host(ctx):
+    """The device refinement inside nm_refine_relabel produces bit-identical
+    nodes/tets/labels to the host nm_refine on the same selection (one level,
+    random-ish selection through a perturbed surface)."""
+    from paper_2203_10000_b200._native import refine
+    cfg = synth.config(2)
+    S = cfg.surfaces
+    nodes, tets = synth.lattice_mesh((-110.0, -110.0, -110.0), 10.0, (22, 22, 22))
+    ctx.set_surfaces(S.xyz, S.tri, S.comp_off, S.label_ids)
+    n1, t1, l1, m1, st = ctx.refine_relabel(nodes, tets, levels=1)
+    m0 = oracle.label_nodes(nodes, S)
+    l0 = oracle.label_tets(tets, m0, S.label_ids)
+    hn, ht, hl, _, n_old = refine(nodes, tets, l0, oracle.flag_boundary(tets, m0))
+    np.testing.assert_array_equal(n1, hn)
+    np.testing.assert_array_equal(t1, ht)
+    m_ref = oracle.label_nodes(hn, S)
+    np.testing.assert_array_equal(m1, m_ref)
+    np.testing.assert_array_equal(l1, oracle.label_tets(ht, m_ref, S.label_ids))
