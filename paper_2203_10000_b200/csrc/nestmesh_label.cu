@@ -731,6 +731,21 @@ int nm_set_surfaces(nm_ctx* c, const double* xyz, std::size_t nv, const std::uin
               for (int q = 0; q < nm::kSegTris; q += 2)
                 r[nm::kSegTris + 2 + q / 2] = make_float4(float(N[q][1]), float(N[q][2]), float(N[q + 1][1]),
                                                           float(N[q + 1][2]));
+              if (nm::kSegF4 > 14) {
+                // -|e|^2/2 of the consecutive (k,k+1) and skip (k,k+2) edges, from the stored fp32 geometry
+                float E[20] = {0};
+                auto e2 = [&](int i, int j) {
+                  double s2 = 0;
+                  for (int a = 0; a < 3; ++a) {
+                    const double d = double(rv[3 * j + a]) - double(rv[3 * i + a]);
+                    s2 += d * d;
+                  }
+                  return float(-0.5 * s2);
+                };
+                for (int q = 0; q <= nm::kSegTris; ++q) E[q] = e2(q, q + 1);
+                for (int q = 0; q < nm::kSegTris; ++q) E[9 + q] = e2(q, q + 2);
+                for (int q = 0; q < 5; ++q) r[14 + q] = make_float4(E[4 * q], E[4 * q + 1], E[4 * q + 2], E[4 * q + 3]);
+              }
             } else {
               double N[3] = {0, 0, 0};
               if (u < nreal) normal64(order[k][u], N);

@@ -167,11 +167,17 @@ __device__ __forceinline__ float acc_near_lane(float acc, float a_far, float num
 // original triangle's (v2-v1)x(v3-v1), so num_k = N_k . R_k carries the
 // outward orientation whatever the strip's winding parity.
 // ---------------------------------------------------------------------------
+#ifndef NM_EDGE_TRICK
+#define NM_EDGE_TRICK 1
+#endif
 constexpr int kSegTris = 8;
-constexpr int kSegF4 = 14;
+// With NM_EDGE_TRICK the record carries -|e|^2/2 for the 9 consecutive and 8
+// skip edges (5 more float4) and R_a.R_b = (q_a + q_b)/2 - |e_ab|^2/2 costs
+// 2 ops instead of 3.
+constexpr int kSegF4 = NM_EDGE_TRICK ? 19 : 14;
 
 struct Vtx2 {
-  float2 x, y, z, r;
+  float2 x, y, z, r, q;
 };
 
 __device__ __forceinline__ Vtx2 strip_vertex(const float4& V, float2 mx, float2 my, float2 mz) {
@@ -179,9 +185,16 @@ __device__ __forceinline__ Vtx2 strip_vertex(const float4& V, float2 mx, float2 
   v.x = add2(bc(V.x), mx);
   v.y = add2(bc(V.y), my);
   v.z = add2(bc(V.z), mz);
-  const float2 q = fma2(v.z, v.z, fma2(v.y, v.y, mul2(v.x, v.x)));
-  v.r = make_float2(sqrt_approx(q.x), sqrt_approx(q.y));
+  v.q = fma2(v.z, v.z, fma2(v.y, v.y, mul2(v.x, v.x)));
+  v.r = make_float2(sqrt_approx(v.q.x), sqrt_approx(v.q.y));
   return v;
+}
+
+// edge value idx (0..8 consecutive, 9..16 skip) from the 5 trailing float4
+__device__ __forceinline__ float edge_val(const float4 (&E)[5], int idx) {
+  const float4 v = E[idx >> 2];
+  const int c = idx & 3;
+  return c == 0 ? v.x : c == 1 ? v.y : c == 2 ? v.z : v.w;
 }
 
 __device__ __forceinline__ float2 dot2(const Vtx2& a, const Vtx2& b) {
@@ -198,11 +211,23 @@ __device__ __forceinline__ void eval_segment(const float4* __restrict__ rec, con
   float4 V0 = rec[0], V1 = rec[1];
   Vtx2 a[NP], b[NP];
   float2 dab[NP];
+#if NM_EDGE_TRICK
+  float4 EE[5];
+#pragma unroll
+  for (int i = 0; i < 5; ++i) EE[i] = rec[14 + i];
+  auto edot = [&](const Vtx2& u, const Vtx2& w, int idx) {
+    return fma2(add2(u.q, w.q), bc(0.5f), bc(edge_val(EE, idx)));
+  };
+#endif
 #pragma unroll
   for (int q = 0; q < NP; ++q) {
     a[q] = strip_vertex(V0, mx[q], my[q], mz[q]);
     b[q] = strip_vertex(V1, mx[q], my[q], mz[q]);
+#if NM_EDGE_TRICK
+    dab[q] = edot(a[q], b[q], 0);
+#else
     dab[q] = dot2(a[q], b[q]);
+#endif
   }
 #pragma unroll
   for (int k = 0; k < kSegTris; ++k) {
@@ -212,7 +237,11 @@ __device__ __forceinline__ void eval_segment(const float4* __restrict__ rec, con
 #pragma unroll
     for (int q = 0; q < NP; ++q) {
       const Vtx2 c = strip_vertex(V2, mx[q], my[q], mz[q]);
+#if NM_EDGE_TRICK
+      const float2 dbc = edot(b[q], c, k + 1), dac = edot(a[q], c, 9 + k);
+#else
       const float2 dbc = dot2(b[q], c), dac = dot2(a[q], c);
+#endif
       const float2 num = fma2(bc(nz), a[q].z, fma2(bc(ny), a[q].y, mul2(bc(nx), a[q].x)));
       const float2 den = fma2(fma2(a[q].r, b[q].r, dab[q]), c.r, fma2(dac, b[q].r, mul2(dbc, a[q].r)));
       const float2 af = acc_far2(acc[q], num, den);

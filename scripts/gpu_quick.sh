@@ -1,2 +1,3 @@
-python -m pytest tests -q -m gpu -x 2>&1 | tail -15
-python bench.py --config 4 --steps 1 --warmup 3 > gpurun_out/bench_cfg4.json 2> gpurun_out/bench_cfg4.err; cat gpurun_out/bench_cfg4.json; tail -3 gpurun_out/bench_cfg4.err
+NM_LABEL_LIB=probes/libnl_edge.so python -m pytest tests/test_gpu_parity.py -q -m gpu -x 2>&1 | tail -3
+python scripts/quick_time.py 5:2000000 3:2000000 2
+NM_LABEL_LIB=probes/libnl_edge.so python scripts/quick_time.py 5:2000000 3:2000000 2
