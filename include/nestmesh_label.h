@@ -72,7 +72,7 @@ typedef struct nm_stats {
   uint64_t flagged_points;   /* points sent to the fp64 fix-up */
   uint64_t flagged_pairs;    /* (point, compartment) pairs re-evaluated in fp64 */
   uint64_t ties;             /* pairs with |s - T| < tie_eps after fix-up */
-  uint64_t near_subtiles;    /* warp x 32-triangle subtile visits that took the near path */
+  uint64_t near_subtiles;    /* warp x 8-triangle group visits that took the near path */
   uint64_t far_subtiles;     /* ... that took the far path */
   uint64_t launches;         /* kernels launched by this call */
   float ms_label;            /* device time of the fp32 solid-angle kernel (CUDA events) */

@@ -20,6 +20,7 @@ namespace nm {
 constexpr int kTile = 256;              // triangles per shared-memory tile (fp64 fold granularity)
 constexpr int kSub = 32;                // triangles per subtile (near/far decision unit)
 constexpr int kSubPerTile = kTile / kSub;
+constexpr int kSubRec = 5;               // float4 per subtile record: sphere of the subtile + of its 4 groups of 8
 constexpr int kBlock = 256;             // threads per CTA of k_label
 #ifndef NM_DIRECT_LDG
 #define NM_DIRECT_LDG 0
@@ -50,7 +51,7 @@ struct LabelParams {
   std::uint32_t* masks;      // n
   std::uint32_t* flagmask;   // n (bit k: pair (i,k) needs the fp64 fix-up)
   double* s_out;             // n*K or nullptr
-  unsigned long long* counters;  // [0] near subtile visits, [1] far subtile visits
+  unsigned long long* counters;  // [0] near / [1] far visits of (warp, 8-triangle group)
 };
 
 // NP point pairs per thread (2*NP points), packed fp32x2 arithmetic.
@@ -68,7 +69,7 @@ __global__ void __launch_bounds__(kBlock, (NP == 1 ? NM_MIN_BLOCKS : 1)) k_label
   // block-wide barriers.
 #else
   __shared__ float4 s_tri[kTileF4];
-  __shared__ float4 s_sub[kSubPerTile];
+  __shared__ float4 s_sub[kSubPerTile * kSubRec];
 #endif
 
   const std::size_t base = (static_cast<std::size_t>(blockIdx.x) * kBlock + threadIdx.x) * P;
@@ -115,13 +116,13 @@ __global__ void __launch_bounds__(kBlock, (NP == 1 ? NM_MIN_BLOCKS : 1)) k_label
       const float4* gt = prm.tri + static_cast<std::size_t>(tile) * kTileF4;
 #if NM_DIRECT_LDG
       const float4* s_tri = gt;
-      const float4* s_sub = prm.sub + static_cast<std::size_t>(tile) * kSubPerTile;
+      const float4* s_sub = prm.sub + static_cast<std::size_t>(tile) * kSubPerTile * kSubRec;
 #else
       __syncthreads();
 #pragma unroll
       for (int i = threadIdx.x; i < kTileF4; i += kBlock) s_tri[i] = __ldg(gt + i);
-      if (threadIdx.x < kSubPerTile)
-        s_sub[threadIdx.x] = __ldg(prm.sub + static_cast<std::size_t>(tile) * kSubPerTile + threadIdx.x);
+      if (threadIdx.x < kSubPerTile * kSubRec)
+        s_sub[threadIdx.x] = __ldg(prm.sub + static_cast<std::size_t>(tile) * kSubPerTile * kSubRec + threadIdx.x);
       __syncthreads();
 #endif
 
@@ -129,7 +130,7 @@ __global__ void __launch_bounds__(kBlock, (NP == 1 ? NM_MIN_BLOCKS : 1)) k_label
 #pragma unroll
       for (int q = 0; q < NP; ++q) acc[q] = make_float2(0.0f, 0.0f);
       for (int st = 0; st < kSubPerTile; ++st) {
-        const float4 sb = s_sub[st];
+        const float4 sb = s_sub[st * kSubRec];
         float2 mx[NP], my[NP], mz[NP];  // -(p - c)
         bool far = true;
 #pragma unroll
@@ -145,7 +146,7 @@ __global__ void __launch_bounds__(kBlock, (NP == 1 ? NM_MIN_BLOCKS : 1)) k_label
         }
         const float4* tt = s_tri + st * kSubF4;
         if (__all_sync(kFull, far)) {
-          ++n_far;
+          n_far += kSub / 8;
           if constexpr (STRIP) {
 #pragma unroll 1
             for (int g = 0; g < kSub / kSegTris; ++g)
@@ -162,12 +163,29 @@ __global__ void __launch_bounds__(kBlock, (NP == 1 ? NM_MIN_BLOCKS : 1)) k_label
             }
           }
         } else {
-          ++n_near;
           if constexpr (STRIP) {
+            // refine the decision per 8-triangle segment (its own sphere,
+            // centre relative to the subtile centre)
 #pragma unroll 1
-            for (int g = 0; g < kSub / kSegTris; ++g)
-              eval_segment<NP, true>(tt + g * kSegF4, mx, my, mz, acc, det, prm.tau, prm.delta);
+            for (int g = 0; g < kSub / kSegTris; ++g) {
+              const float4 sg = s_sub[st * kSubRec + 1 + g];
+              bool farg = true;
+#pragma unroll
+              for (int q = 0; q < NP; ++q) {
+                const float2 dx = add2(mx[q], bc(sg.x)), dy = add2(my[q], bc(sg.y)), dz = add2(mz[q], bc(sg.z));
+                const float2 d2 = fma2(dz, dz, fma2(dy, dy, mul2(dx, dx)));
+                farg &= (!valid[2 * q] || d2.x > sg.w) && (!valid[2 * q + 1] || d2.y > sg.w);
+              }
+              if (__all_sync(kFull, farg)) {
+                ++n_far;
+                eval_segment<NP, false>(tt + g * kSegF4, mx, my, mz, acc, det, prm.tau, prm.delta);
+              } else {
+                ++n_near;
+                eval_segment<NP, true>(tt + g * kSegF4, mx, my, mz, acc, det, prm.tau, prm.delta);
+              }
+            }
           } else {
+            n_near += kSub / 8;
 #pragma unroll 1
             for (int t = 0; t < kSub; ++t) {
               const float4 A = tt[3 * t], B = tt[3 * t + 1], C = tt[3 * t + 2];

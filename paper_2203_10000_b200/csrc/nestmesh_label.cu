@@ -668,7 +668,7 @@ int nm_set_surfaces(nm_ctx* c, const double* xyz, std::size_t nv, const std::uin
     const int sub_f4 = use_strips ? (nm::kSub / nm::kSegTris) * nm::kSegF4 : nm::kSub * 3;
     const std::size_t tile_f4 = static_cast<std::size_t>(sub_f4) * nm::kSubPerTile;
     std::vector<float4> htri(ntiles * tile_f4);
-    std::vector<float4> hsub(ntiles * nm::kSubPerTile);
+    std::vector<float4> hsub(ntiles * nm::kSubPerTile * nm::kSubRec);
     const double far_ratio = c->opt.far_ratio, far_abs = c->opt.far_abs_mm;
     // Each 32-triangle subtile carries an fp32 centre c (exactly representable
     // in the centred frame) and its vertices relative to c, so near-surface
@@ -754,7 +754,29 @@ int nm_set_surfaces(nm_ctx* c, const double* xyz, std::size_t nv, const std::uin
             }
           }
           const double R = (far_ratio * rho + far_abs) * (1.0 + 1e-5);
-          hsub[static_cast<std::size_t>(tl) * nm::kSubPerTile + sidx] = make_float4(fc[0], fc[1], fc[2], float(R * R));
+          float4* hs = &hsub[(static_cast<std::size_t>(tl) * nm::kSubPerTile + sidx) * nm::kSubRec];
+          hs[0] = make_float4(fc[0], fc[1], fc[2], float(R * R));
+          // spheres of the 4 groups of 8 triangles, centres relative to fc
+          const int per_group = static_cast<int>(srcv.size()) / 4;
+          for (int g = 0; g < 4; ++g) {
+            double glo[3] = {1e300, 1e300, 1e300}, ghi[3] = {-1e300, -1e300, -1e300};
+            for (int q = g * per_group; q < (g + 1) * per_group; ++q)
+              for (int a = 0; a < 3; ++a) {
+                glo[a] = std::min(glo[a], double(rel[3 * q + a]));
+                ghi[a] = std::max(ghi[a], double(rel[3 * q + a]));
+              }
+            const float gc[3] = {float(0.5 * (glo[0] + ghi[0])), float(0.5 * (glo[1] + ghi[1])),
+                                 float(0.5 * (glo[2] + ghi[2]))};
+            double rg = 0.0;
+            for (int q = g * per_group; q < (g + 1) * per_group; ++q) {
+              double d2 = 0.0;
+              for (int a = 0; a < 3; ++a) d2 += (double(rel[3 * q + a]) - gc[a]) * (double(rel[3 * q + a]) - gc[a]);
+              rg = std::max(rg, std::sqrt(d2));
+            }
+            // the kernel forms (p - c) - g in fp32: one more rounding, covered by the 1e-5 margin
+            const double Rg = (far_ratio * rg + far_abs) * (1.0 + 1e-5);
+            hs[1 + g] = make_float4(gc[0], gc[1], gc[2], float(Rg * Rg));
+          }
         }
       }
     }
