@@ -132,6 +132,7 @@ __global__ void __launch_bounds__(kBlock, (NP == 1 ? NM_MIN_BLOCKS : 1)) k_label
       for (int st = 0; st < kSubPerTile; ++st) {
         const float4 sb = s_sub[st * kSubRec];
         float2 mx[NP], my[NP], mz[NP];  // -(p - c)
+        bool lane_far[P];
         bool far = true;
 #pragma unroll
         for (int q = 0; q < NP; ++q) {
@@ -142,16 +143,72 @@ __global__ void __launch_bounds__(kBlock, (NP == 1 ? NM_MIN_BLOCKS : 1)) k_label
           my[q] = make_float2(-py.x, -py.y);
           mz[q] = make_float2(-pz.x, -pz.y);
           const float2 d2 = fma2(pz, pz, fma2(py, py, mul2(px, px)));
-          far &= (!valid[2 * q] || d2.x > sb.w) && (!valid[2 * q + 1] || d2.y > sb.w);
+          lane_far[2 * q] = !valid[2 * q] || d2.x > sb.w;
+          lane_far[2 * q + 1] = !valid[2 * q + 1] || d2.y > sb.w;
+          far &= lane_far[2 * q] && lane_far[2 * q + 1];
         }
         const float4* tt = s_tri + st * kSubF4;
-        if (__all_sync(kFull, far)) {
-          n_far += kSub / 8;
-          if constexpr (STRIP) {
+        if constexpr (STRIP) {
+          PairFrame f[NP];
+#pragma unroll
+          for (int q = 0; q < NP; ++q) f[q] = pair_frame(mx[q], my[q], mz[q]);
+          if (__all_sync(kFull, far)) {
+            n_far += kSub / kSegTris;
 #pragma unroll 1
-            for (int g = 0; g < kSub / kSegTris; ++g)
-              eval_segment<NP, false>(tt + g * kSegF4, mx, my, mz, acc, det, prm.tau, prm.delta);
+            for (int g = 0; g < kSub / kSegTris; ++g) seg_far<NP>(tt + g * kSegF4, f, acc);
           } else {
+            // per-group decision; each lane's evaluator depends only on its
+            // own point (lane_far = far from the subtile or from the group)
+#pragma unroll 1
+            for (int g = 0; g < kSub / kSegTris; ++g) {
+              const float4 sg = s_sub[st * kSubRec + 1 + g];
+              bool gf[P];
+              bool all = true, any = false;
+#pragma unroll
+              for (int q = 0; q < NP; ++q) {
+                const float2 dx = add2(mx[q], bc(sg.x)), dy = add2(my[q], bc(sg.y)), dz = add2(mz[q], bc(sg.z));
+                const float2 d2 = fma2(dz, dz, fma2(dy, dy, mul2(dx, dx)));
+                gf[2 * q] = lane_far[2 * q] || d2.x > sg.w;
+                gf[2 * q + 1] = lane_far[2 * q + 1] || d2.y > sg.w;
+                all &= gf[2 * q] && gf[2 * q + 1];
+                any |= (valid[2 * q] && gf[2 * q]) || (valid[2 * q + 1] && gf[2 * q + 1]);
+              }
+              const float4* rec = tt + g * kSegF4;
+              if (__all_sync(kFull, all)) {
+                ++n_far;
+                seg_far<NP>(rec, f, acc);
+              } else {
+                ++n_near;
+                float2 an[NP];
+                bool dn[P];
+#pragma unroll
+                for (int q = 0; q < NP; ++q) an[q] = acc[q];
+#pragma unroll
+                for (int k = 0; k < P; ++k) dn[k] = false;
+                seg_near<NP>(rec, f, an, dn, prm.tau, prm.delta);
+                if (__any_sync(kFull, any)) {
+                  float2 af[NP];
+#pragma unroll
+                  for (int q = 0; q < NP; ++q) af[q] = acc[q];
+                  seg_far<NP>(rec, f, af);
+#pragma unroll
+                  for (int q = 0; q < NP; ++q) {
+                    an[q].x = gf[2 * q] ? af[q].x : an[q].x;
+                    an[q].y = gf[2 * q + 1] ? af[q].y : an[q].y;
+                  }
+                }
+#pragma unroll
+                for (int q = 0; q < NP; ++q) acc[q] = an[q];
+#pragma unroll
+                for (int k = 0; k < P; ++k) det[k] |= dn[k] && !gf[k];
+              }
+            }
+          }
+        } else {
+          // triangle-soup layout: warp-uniform decision; far and near paths
+          // share vos_terms2, so a pair's value does not depend on the path
+          if (__all_sync(kFull, far)) {
+            n_far += kSub / 8;
 #pragma unroll 4
             for (int t = 0; t < kSub; ++t) {
               const float4 A = tt[3 * t], B = tt[3 * t + 1], C = tt[3 * t + 2];
@@ -159,29 +216,6 @@ __global__ void __launch_bounds__(kBlock, (NP == 1 ? NM_MIN_BLOCKS : 1)) k_label
               for (int q = 0; q < NP; ++q) {
                 const VosTerms2 v = vos_terms2(A, B, C, mx[q], my[q], mz[q]);
                 acc[q] = acc_far2(acc[q], v.num, v.den);
-              }
-            }
-          }
-        } else {
-          if constexpr (STRIP) {
-            // refine the decision per 8-triangle segment (its own sphere,
-            // centre relative to the subtile centre)
-#pragma unroll 1
-            for (int g = 0; g < kSub / kSegTris; ++g) {
-              const float4 sg = s_sub[st * kSubRec + 1 + g];
-              bool farg = true;
-#pragma unroll
-              for (int q = 0; q < NP; ++q) {
-                const float2 dx = add2(mx[q], bc(sg.x)), dy = add2(my[q], bc(sg.y)), dz = add2(mz[q], bc(sg.z));
-                const float2 d2 = fma2(dz, dz, fma2(dy, dy, mul2(dx, dx)));
-                farg &= (!valid[2 * q] || d2.x > sg.w) && (!valid[2 * q + 1] || d2.y > sg.w);
-              }
-              if (__all_sync(kFull, farg)) {
-                ++n_far;
-                eval_segment<NP, false>(tt + g * kSegF4, mx, my, mz, acc, det, prm.tau, prm.delta);
-              } else {
-                ++n_near;
-                eval_segment<NP, true>(tt + g * kSegF4, mx, my, mz, acc, det, prm.tau, prm.delta);
               }
             }
           } else {

@@ -726,26 +726,31 @@ int nm_set_surfaces(nm_ctx* c, const double* xyz, std::size_t nv, const std::uin
                 else N[q][0] = N[q][1] = N[q][2] = 0.0;
               }
               const float* rv = &rel[3 * (j * (nm::kSegTris + 2))];
-              for (int q = 0; q < nm::kSegTris + 2; ++q)
-                r[q] = make_float4(rv[3 * q], rv[3 * q + 1], rv[3 * q + 2], q < nm::kSegTris ? float(N[q][0]) : 0.0f);
-              for (int q = 0; q < nm::kSegTris; q += 2)
-                r[nm::kSegTris + 2 + q / 2] = make_float4(float(N[q][1]), float(N[q][2]), float(N[q + 1][1]),
-                                                          float(N[q + 1][2]));
-              if (nm::kSegF4 > 14) {
-                // -|e|^2/2 of the consecutive (k,k+1) and skip (k,k+2) edges, from the stored fp32 geometry
-                float E[20] = {0};
-                auto e2 = [&](int i, int j) {
-                  double s2 = 0;
-                  for (int a = 0; a < 3; ++a) {
-                    const double d = double(rv[3 * j + a]) - double(rv[3 * i + a]);
-                    s2 += d * d;
-                  }
-                  return float(-0.5 * s2);
-                };
-                for (int q = 0; q <= nm::kSegTris; ++q) E[q] = e2(q, q + 1);
-                for (int q = 0; q < nm::kSegTris; ++q) E[9 + q] = e2(q, q + 2);
-                for (int q = 0; q < 5; ++q) r[14 + q] = make_float4(E[4 * q], E[4 * q + 1], E[4 * q + 2], E[4 * q + 3]);
+              // vertices + |V|^2 (from the stored fp32 coordinates)
+              for (int q = 0; q < nm::kSegTris + 2; ++q) {
+                const double sv = double(rv[3 * q]) * rv[3 * q] + double(rv[3 * q + 1]) * rv[3 * q + 1] +
+                                  double(rv[3 * q + 2]) * rv[3 * q + 2];
+                r[q] = make_float4(rv[3 * q], rv[3 * q + 1], rv[3 * q + 2], float(sv));
               }
+              // (N_k, N_k . V_k) with the fp32 N the kernel multiplies by
+              for (int q = 0; q < nm::kSegTris; ++q) {
+                const float nf[3] = {float(N[q][0]), float(N[q][1]), float(N[q][2])};
+                const double w = double(nf[0]) * rv[3 * q] + double(nf[1]) * rv[3 * q + 1] + double(nf[2]) * rv[3 * q + 2];
+                r[nm::kSegT + q] = make_float4(nf[0], nf[1], nf[2], float(w));
+              }
+              // -|e|^2/2 of the consecutive (k,k+1) and skip (k,k+2) edges
+              float E[20] = {0};
+              auto e2 = [&](int i, int jj) {
+                double s2 = 0;
+                for (int a = 0; a < 3; ++a) {
+                  const double d = double(rv[3 * jj + a]) - double(rv[3 * i + a]);
+                  s2 += d * d;
+                }
+                return float(-0.5 * s2);
+              };
+              for (int q = 0; q <= nm::kSegTris; ++q) E[q] = e2(q, q + 1);
+              for (int q = 0; q < nm::kSegTris; ++q) E[9 + q] = e2(q, q + 2);
+              for (int q = 0; q < 5; ++q) r[nm::kSegE + q] = make_float4(E[4 * q], E[4 * q + 1], E[4 * q + 2], E[4 * q + 3]);
             } else {
               double N[3] = {0, 0, 0};
               if (u < nreal) normal64(order[k][u], N);

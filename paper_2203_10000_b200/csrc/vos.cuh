@@ -160,22 +160,110 @@ __device__ __forceinline__ float acc_near_lane(float acc, float a_far, float num
 // ---------------------------------------------------------------------------
 // Strip segments: 8 triangles t_k = (u_k, u_{k+1}, u_{k+2})
 // of one triangle strip share vertices and edges, so per triangle only one
-// new vertex (R, |R|^2, sqrt) and two new edge dots are computed:
-// ~27 FP32 lane-ops + 2.25 MUFU per evaluation instead of 40 + 4.
-// Record (kSegF4 float4): V[0..9] = (x, y, z, N_k.x for k < 8), then
-// (N_k.y, N_k.z, N_{k+1}.y, N_{k+1}.z) for k = 0, 2, 4, 6. N_k is the
-// original triangle's (v2-v1)x(v3-v1), so num_k = N_k . R_k carries the
-// outward orientation whatever the strip's winding parity.
+// new vertex and two new edge dots are computed. Record (kSegF4 float4):
+//   rec[0..9]   V_i  = (x, y, z, |V_i|^2)            vertices, subtile frame
+//   rec[10..17] T_k  = (N_k.x, N_k.y, N_k.z, N_k.V_k) N_k = (v2-v1)x(v3-v1) of
+//                                                     the original triangle, so
+//                                                     num_k carries the outward
+//                                                     orientation whatever the
+//                                                     strip's winding parity
+//   rec[18..22] -|e|^2/2 of the 9 consecutive (k,k+1) and 8 skip (k,k+2) edges
+// Edge dots use R_a.R_b = (q_a + q_b)/2 - |e_ab|^2/2 (2 ops instead of 3).
+//
+// Two evaluators share the record:
+//   far  (a point at >= 5 rho + 0.05 mm from the group's bounding sphere):
+//        q = |V|^2 + |p|^2 - 2 V.p  (4 ops, no R vector), num = N.V - N.p,
+//        atan(x) = x (1 - x^2/3 + x^4/5) since |x| <= 0.0636 there (cap
+//        bound; truncation < 1e-8 relative): ~21 FP32 lane-ops + 2.25 MUFU;
+//   near R-based terms (exact to ~ulp(|R|)), 3-term series for |x| <= 0.125
+//        else full-range atan2, plus the near-surface detector.
+// Which evaluator a (point, group) pair uses depends only on that point's own
+// distance test, never on its warp mates (mixed warps run both and select per
+// lane), so results are independent of sharding and point order.
 // ---------------------------------------------------------------------------
-#ifndef NM_EDGE_TRICK
-#define NM_EDGE_TRICK 1
-#endif
 constexpr int kSegTris = 8;
-// With NM_EDGE_TRICK the record carries -|e|^2/2 for the 9 consecutive and 8
-// skip edges (5 more float4) and R_a.R_b = (q_a + q_b)/2 - |e_ab|^2/2 costs
-// 2 ops instead of 3.
-constexpr int kSegF4 = NM_EDGE_TRICK ? 19 : 14;
+constexpr int kSegF4 = 23;
+constexpr int kSegT = 10;  // first T_k
+constexpr int kSegE = 18;  // first edge float4
 
+__device__ __forceinline__ float edge_val(const float4* rec, int idx) {
+  const float4 v = rec[kSegE + (idx >> 2)];
+  const int c = idx & 3;
+  return c == 0 ? v.x : c == 1 ? v.y : c == 2 ? v.z : v.w;
+}
+
+// Per point pair, in the subtile frame: m = -(p - c); p2 = -2 (p - c) = 2 m;
+// sp = |p - c|^2.
+struct PairFrame {
+  float2 mx, my, mz, p2x, p2y, p2z, sp;
+};
+
+__device__ __forceinline__ PairFrame pair_frame(float2 mx, float2 my, float2 mz) {
+  PairFrame f;
+  f.mx = mx;
+  f.my = my;
+  f.mz = mz;
+  f.p2x = add2(mx, mx);
+  f.p2y = add2(my, my);
+  f.p2z = add2(mz, mz);
+  f.sp = fma2(mz, mz, fma2(my, my, mul2(mx, mx)));
+  return f;
+}
+
+// ---- far evaluator --------------------------------------------------------
+struct FarV {
+  float2 q, r;
+};
+
+__device__ __forceinline__ FarV far_vertex(const float4& V, const PairFrame& f) {
+  FarV v;
+  v.q = fma2(bc(V.x), f.p2x, fma2(bc(V.y), f.p2y, fma2(bc(V.z), f.p2z, add2(bc(V.w), f.sp))));
+  v.r = make_float2(sqrt_approx(v.q.x), sqrt_approx(v.q.y));
+  return v;
+}
+
+__device__ __forceinline__ float2 atan_far2(float2 acc, float2 num, float2 den) {
+  const float2 x = mul2(num, make_float2(rcp_approx(den.x), rcp_approx(den.y)));
+  const float2 y = mul2(x, x);
+  const float2 p = fma2(fma2(bc(0.2f), y, bc(-0.333333333333f)), y, bc(1.0f));
+  return fma2(x, p, acc);
+}
+
+template <int NP>
+__device__ __forceinline__ void seg_far(const float4* __restrict__ rec, const PairFrame (&f)[NP], float2 (&acc)[NP]) {
+  FarV a[NP], b[NP];
+  float2 dab[NP];
+  {
+    const float4 V0 = rec[0], V1 = rec[1];
+    const float e0 = edge_val(rec, 0);
+#pragma unroll
+    for (int q = 0; q < NP; ++q) {
+      a[q] = far_vertex(V0, f[q]);
+      b[q] = far_vertex(V1, f[q]);
+      dab[q] = fma2(add2(a[q].q, b[q].q), bc(0.5f), bc(e0));
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < kSegTris; ++k) {
+    const float4 V2 = rec[k + 2];
+    const float4 T = rec[kSegT + k];
+    const float ebc = edge_val(rec, k + 1), eac = edge_val(rec, 9 + k);
+#pragma unroll
+    for (int q = 0; q < NP; ++q) {
+      const FarV c = far_vertex(V2, f[q]);
+      const float2 dbc = fma2(add2(b[q].q, c.q), bc(0.5f), bc(ebc));
+      const float2 dac = fma2(add2(a[q].q, c.q), bc(0.5f), bc(eac));
+      const float2 num = fma2(bc(T.x), f[q].mx, fma2(bc(T.y), f[q].my, fma2(bc(T.z), f[q].mz, bc(T.w))));
+      const float2 den = fma2(fma2(a[q].r, b[q].r, dab[q]), c.r, fma2(dac, b[q].r, mul2(dbc, a[q].r)));
+      acc[q] = atan_far2(acc[q], num, den);
+      a[q] = b[q];
+      b[q] = c;
+      dab[q] = dbc;
+    }
+  }
+}
+
+// ---- near evaluator -------------------------------------------------------
 struct Vtx2 {
   float2 x, y, z, r, q;
 };
@@ -190,73 +278,40 @@ __device__ __forceinline__ Vtx2 strip_vertex(const float4& V, float2 mx, float2 
   return v;
 }
 
-// edge value idx (0..8 consecutive, 9..16 skip) from the 5 trailing float4
-__device__ __forceinline__ float edge_val(const float4 (&E)[5], int idx) {
-  const float4 v = E[idx >> 2];
-  const int c = idx & 3;
-  return c == 0 ? v.x : c == 1 ? v.y : c == 2 ? v.z : v.w;
-}
-
-__device__ __forceinline__ float2 dot2(const Vtx2& a, const Vtx2& b) {
-  return fma2(a.z, b.z, fma2(a.y, b.y, mul2(a.x, b.x)));
-}
-
-// Evaluate one segment for NP point pairs. NEAR selects the per-lane
-// full-range path + detector; the shared terms are computed identically in
-// both instantiations, so far-range pairs get the same bits either way.
-template <int NP, bool NEAR>
-__device__ __forceinline__ void eval_segment(const float4* __restrict__ rec, const float2 (&mx)[NP],
-                                             const float2 (&my)[NP], const float2 (&mz)[NP], float2 (&acc)[NP],
-                                             bool (&det)[2 * NP], float tau, float delta) {
-  float4 V0 = rec[0], V1 = rec[1];
+template <int NP>
+__device__ __forceinline__ void seg_near(const float4* __restrict__ rec, const PairFrame (&f)[NP], float2 (&acc)[NP],
+                                         bool (&det)[2 * NP], float tau, float delta) {
   Vtx2 a[NP], b[NP];
   float2 dab[NP];
-#if NM_EDGE_TRICK
-  float4 EE[5];
-#pragma unroll
-  for (int i = 0; i < 5; ++i) EE[i] = rec[14 + i];
-  auto edot = [&](const Vtx2& u, const Vtx2& w, int idx) {
-    return fma2(add2(u.q, w.q), bc(0.5f), bc(edge_val(EE, idx)));
-  };
-#endif
-#pragma unroll
-  for (int q = 0; q < NP; ++q) {
-    a[q] = strip_vertex(V0, mx[q], my[q], mz[q]);
-    b[q] = strip_vertex(V1, mx[q], my[q], mz[q]);
-#if NM_EDGE_TRICK
-    dab[q] = edot(a[q], b[q], 0);
-#else
-    dab[q] = dot2(a[q], b[q]);
-#endif
-  }
-#pragma unroll
-  for (int k = 0; k < kSegTris; ++k) {
-    const float4 V2 = rec[k + 2];
-    const float4 NN = rec[10 + (k >> 1)];
-    const float nx = V0.w, ny = (k & 1) ? NN.z : NN.x, nz = (k & 1) ? NN.w : NN.y;
+  {
+    const float4 V0 = rec[0], V1 = rec[1];
+    const float e0 = edge_val(rec, 0);
 #pragma unroll
     for (int q = 0; q < NP; ++q) {
-      const Vtx2 c = strip_vertex(V2, mx[q], my[q], mz[q]);
-#if NM_EDGE_TRICK
-      const float2 dbc = edot(b[q], c, k + 1), dac = edot(a[q], c, 9 + k);
-#else
-      const float2 dbc = dot2(b[q], c), dac = dot2(a[q], c);
-#endif
-      const float2 num = fma2(bc(nz), a[q].z, fma2(bc(ny), a[q].y, mul2(bc(nx), a[q].x)));
+      a[q] = strip_vertex(V0, f[q].mx, f[q].my, f[q].mz);
+      b[q] = strip_vertex(V1, f[q].mx, f[q].my, f[q].mz);
+      dab[q] = fma2(add2(a[q].q, b[q].q), bc(0.5f), bc(e0));
+    }
+  }
+#pragma unroll 1
+  for (int k = 0; k < kSegTris; ++k) {
+    const float4 V2 = rec[k + 2];
+    const float4 T = rec[kSegT + k];
+    const float ebc = edge_val(rec, k + 1), eac = edge_val(rec, 9 + k);
+#pragma unroll
+    for (int q = 0; q < NP; ++q) {
+      const Vtx2 c = strip_vertex(V2, f[q].mx, f[q].my, f[q].mz);
+      const float2 dbc = fma2(add2(b[q].q, c.q), bc(0.5f), bc(ebc));
+      const float2 dac = fma2(add2(a[q].q, c.q), bc(0.5f), bc(eac));
+      const float2 num = fma2(bc(T.z), a[q].z, fma2(bc(T.y), a[q].y, mul2(bc(T.x), a[q].x)));
       const float2 den = fma2(fma2(a[q].r, b[q].r, dab[q]), c.r, fma2(dac, b[q].r, mul2(dbc, a[q].r)));
       const float2 af = acc_far2(acc[q], num, den);
-      if (NEAR) {
-        acc[q].x = acc_near_lane(acc[q].x, af.x, num.x, den.x, a[q].r.x, b[q].r.x, c.r.x, tau, delta, det[2 * q]);
-        acc[q].y = acc_near_lane(acc[q].y, af.y, num.y, den.y, a[q].r.y, b[q].r.y, c.r.y, tau, delta, det[2 * q + 1]);
-      } else {
-        acc[q] = af;
-      }
+      acc[q].x = acc_near_lane(acc[q].x, af.x, num.x, den.x, a[q].r.x, b[q].r.x, c.r.x, tau, delta, det[2 * q]);
+      acc[q].y = acc_near_lane(acc[q].y, af.y, num.y, den.y, a[q].r.y, b[q].r.y, c.r.y, tau, delta, det[2 * q + 1]);
       a[q] = b[q];
       b[q] = c;
       dab[q] = dbc;
     }
-    V0 = V1;
-    V1 = V2;
   }
 }
 

@@ -209,3 +209,23 @@ def test_device_refine_matches_host(ctx):
     m_ref = oracle.label_nodes(hn, S)
     np.testing.assert_array_equal(m1, m_ref)
     np.testing.assert_array_equal(l1, oracle.label_tets(ht, m_ref, S.label_ids))
+
+
+def test_results_independent_of_point_set(ctx):
+    """s (fp64, bitwise) for a point does not depend on which other points
+    share its warp: a subset evaluated alone equals the same points evaluated
+    inside the full set and inside a shuffled set (the sharding invariance of
+    SPEC.md:265 at the finest level)."""
+    cfg = synth.config(3)
+    S = cfg.surfaces
+    nodes = cfg.lattice_nodes()
+    rng = np.random.default_rng(11)
+    block = nodes[3_000_000:3_040_000]
+    idx = np.sort(rng.choice(block.shape[0], 3000, replace=False))
+    ctx.set_surfaces(S.xyz, S.tri, S.comp_off, S.label_ids)
+    s_block, _ = ctx.enclosure(block)
+    s_sub, _ = ctx.enclosure(block[idx])
+    perm = rng.permutation(block.shape[0])
+    s_perm, _ = ctx.enclosure(block[perm])
+    np.testing.assert_array_equal(s_sub, s_block[idx])
+    np.testing.assert_array_equal(s_perm, s_block[perm])
