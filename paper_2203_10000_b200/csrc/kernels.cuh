@@ -77,16 +77,17 @@ __global__ void __launch_bounds__(kBlock, (NP == 1 ? NM_MIN_BLOCKS : 1)) k_label
   // per subtile the kernel forms p - c = (hi - c) + lo, exact up to one
   // rounding of |p - c| (near-surface geometry keeps ~ulp(|p - c|)).
   float2 hx[NP], hy[NP], hz[NP], lx[NP], ly[NP], lz[NP];
-  std::size_t pid[P];
+  std::uint32_t pid[P];
   bool valid[P];
 #pragma unroll
   for (int k = 0; k < P; ++k) {
     const std::size_t i = base + k;
     valid[k] = i < prm.n;
     const std::size_t ii = valid[k] ? i : prm.n - 1;
-    const std::size_t j = prm.order ? prm.order[ii] : ii;
+    const std::uint32_t j = prm.order ? prm.order[ii] : static_cast<std::uint32_t>(ii);
     pid[k] = j;
-    const double dx = prm.pts[3 * j] - prm.cx, dy = prm.pts[3 * j + 1] - prm.cy, dz = prm.pts[3 * j + 2] - prm.cz;
+    const double dx = prm.pts[3 * static_cast<std::size_t>(j)] - prm.cx, dy = prm.pts[3 * static_cast<std::size_t>(j) + 1] - prm.cy,
+                 dz = prm.pts[3 * static_cast<std::size_t>(j) + 2] - prm.cz;
     const float fx = static_cast<float>(dx), fy = static_cast<float>(dy), fz = static_cast<float>(dz);
     const float gx = static_cast<float>(dx - fx), gy = static_cast<float>(dy - fy), gz = static_cast<float>(dz - fz);
     if (k & 1) {
@@ -248,7 +249,7 @@ __global__ void __launch_bounds__(kBlock, (NP == 1 ? NM_MIN_BLOCKS : 1)) k_label
       if (s >= prm.T) mask[k] |= 1u << c;
       // NaN-safe: anything not provably outside the band is re-evaluated.
       if (det[k] || !(fabs(s - prm.T) >= prm.band)) fmask[k] |= 1u << c;
-      if (prm.s_out && valid[k]) prm.s_out[pid[k] * prm.K + c] = s;
+      if (prm.s_out && valid[k]) prm.s_out[static_cast<std::size_t>(pid[k]) * prm.K + c] = s;
     }
   }
 #pragma unroll

@@ -730,7 +730,7 @@ int nm_set_surfaces(nm_ctx* c, const double* xyz, std::size_t nv, const std::uin
               for (int q = 0; q < nm::kSegTris + 2; ++q) {
                 const double sv = double(rv[3 * q]) * rv[3 * q] + double(rv[3 * q + 1]) * rv[3 * q + 1] +
                                   double(rv[3 * q + 2]) * rv[3 * q + 2];
-                r[q] = make_float4(rv[3 * q], rv[3 * q + 1], rv[3 * q + 2], float(sv));
+                r[q] = make_float4(2.0f * rv[3 * q], 2.0f * rv[3 * q + 1], 2.0f * rv[3 * q + 2], float(sv));
               }
               // (N_k, N_k . V_k) with the fp32 N the kernel multiplies by
               for (int q = 0; q < nm::kSegTris; ++q) {

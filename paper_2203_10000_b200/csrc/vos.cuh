@@ -161,7 +161,7 @@ __device__ __forceinline__ float acc_near_lane(float acc, float a_far, float num
 // Strip segments: 8 triangles t_k = (u_k, u_{k+1}, u_{k+2})
 // of one triangle strip share vertices and edges, so per triangle only one
 // new vertex and two new edge dots are computed. Record (kSegF4 float4):
-//   rec[0..9]   V_i  = (x, y, z, |V_i|^2)            vertices, subtile frame
+//   rec[0..9]   V_i  = (2x, 2y, 2z, |V_i|^2)         vertices (doubled), subtile frame
 //   rec[10..17] T_k  = (N_k.x, N_k.y, N_k.z, N_k.V_k) N_k = (v2-v1)x(v3-v1) of
 //                                                     the original triangle, so
 //                                                     num_k carries the outward
@@ -192,10 +192,9 @@ __device__ __forceinline__ float edge_val(const float4* rec, int idx) {
   return c == 0 ? v.x : c == 1 ? v.y : c == 2 ? v.z : v.w;
 }
 
-// Per point pair, in the subtile frame: m = -(p - c); p2 = -2 (p - c) = 2 m;
-// sp = |p - c|^2.
+// Per point pair, in the subtile frame: m = -(p - c); sp = |p - c|^2.
 struct PairFrame {
-  float2 mx, my, mz, p2x, p2y, p2z, sp;
+  float2 mx, my, mz, sp;
 };
 
 __device__ __forceinline__ PairFrame pair_frame(float2 mx, float2 my, float2 mz) {
@@ -203,9 +202,6 @@ __device__ __forceinline__ PairFrame pair_frame(float2 mx, float2 my, float2 mz)
   f.mx = mx;
   f.my = my;
   f.mz = mz;
-  f.p2x = add2(mx, mx);
-  f.p2y = add2(my, my);
-  f.p2z = add2(mz, mz);
   f.sp = fma2(mz, mz, fma2(my, my, mul2(mx, mx)));
   return f;
 }
@@ -217,7 +213,8 @@ struct FarV {
 
 __device__ __forceinline__ FarV far_vertex(const float4& V, const PairFrame& f) {
   FarV v;
-  v.q = fma2(bc(V.x), f.p2x, fma2(bc(V.y), f.p2y, fma2(bc(V.z), f.p2z, add2(bc(V.w), f.sp))));
+  // |V - p|^2 = |V|^2 + |p|^2 + (2V).(-p)
+  v.q = fma2(bc(V.x), f.mx, fma2(bc(V.y), f.my, fma2(bc(V.z), f.mz, add2(bc(V.w), f.sp))));
   v.r = make_float2(sqrt_approx(v.q.x), sqrt_approx(v.q.y));
   return v;
 }
@@ -229,6 +226,19 @@ __device__ __forceinline__ float2 atan_far2(float2 acc, float2 num, float2 den) 
   return fma2(x, p, acc);
 }
 
+// atan(N/D) for |N/D| <= 0.13: 3-term odd series (truncation x^9/9 < 1e-9 rel).
+__device__ __forceinline__ float2 atan_far3(float2 acc, float2 num, float2 den) {
+  const float2 x = mul2(num, make_float2(rcp_approx(den.x), rcp_approx(den.y)));
+  const float2 y = mul2(x, x);
+  const float2 p = fma2(fma2(fma2(bc(-0.142857142857f), y, bc(0.2f)), y, bc(-0.333333333333f)), y, bc(1.0f));
+  return fma2(x, p, acc);
+}
+
+// Far evaluator. Consecutive triangles are combined pairwise through the
+// complex product (den0 + i num0)(den1 + i num1): its argument is the sum of
+// the two half-angles (each <= 0.0636 rad far away, so the sum stays in the
+// 3-term series' range and the real part stays > 0). Same FP32 work as two
+// separate series, half the MUFU.RCP.
 template <int NP>
 __device__ __forceinline__ void seg_far(const float4* __restrict__ rec, const PairFrame (&f)[NP], float2 (&acc)[NP]) {
   FarV a[NP], b[NP];
@@ -243,6 +253,7 @@ __device__ __forceinline__ void seg_far(const float4* __restrict__ rec, const Pa
       dab[q] = fma2(add2(a[q].q, b[q].q), bc(0.5f), bc(e0));
     }
   }
+  float2 n0[NP], d0[NP];
 #pragma unroll
   for (int k = 0; k < kSegTris; ++k) {
     const float4 V2 = rec[k + 2];
@@ -255,7 +266,14 @@ __device__ __forceinline__ void seg_far(const float4* __restrict__ rec, const Pa
       const float2 dac = fma2(add2(a[q].q, c.q), bc(0.5f), bc(eac));
       const float2 num = fma2(bc(T.x), f[q].mx, fma2(bc(T.y), f[q].my, fma2(bc(T.z), f[q].mz, bc(T.w))));
       const float2 den = fma2(fma2(a[q].r, b[q].r, dab[q]), c.r, fma2(dac, b[q].r, mul2(dbc, a[q].r)));
-      acc[q] = atan_far2(acc[q], num, den);
+      if (k & 1) {
+        const float2 D = fma2(d0[q], den, mul2(make_float2(-n0[q].x, -n0[q].y), num));
+        const float2 N = fma2(n0[q], den, mul2(num, d0[q]));
+        acc[q] = atan_far3(acc[q], N, D);
+      } else {
+        n0[q] = num;
+        d0[q] = den;
+      }
       a[q] = b[q];
       b[q] = c;
       dab[q] = dbc;
@@ -268,11 +286,12 @@ struct Vtx2 {
   float2 x, y, z, r, q;
 };
 
+// V holds 2V: R = 0.5 (2V) - p, exact scaling.
 __device__ __forceinline__ Vtx2 strip_vertex(const float4& V, float2 mx, float2 my, float2 mz) {
   Vtx2 v;
-  v.x = add2(bc(V.x), mx);
-  v.y = add2(bc(V.y), my);
-  v.z = add2(bc(V.z), mz);
+  v.x = fma2(bc(V.x), bc(0.5f), mx);
+  v.y = fma2(bc(V.y), bc(0.5f), my);
+  v.z = fma2(bc(V.z), bc(0.5f), mz);
   v.q = fma2(v.z, v.z, fma2(v.y, v.y, mul2(v.x, v.x)));
   v.r = make_float2(sqrt_approx(v.q.x), sqrt_approx(v.q.y));
   return v;
