@@ -388,9 +388,14 @@ def main():
         import torch as _t
         sms = _t.cuda.get_device_properties(local).multi_processor_count
         peak = sms * FP32_LANES_PER_SM * sm_max * 1e6 / OPS_PER_EVAL
+        traffic = None
+        tf = ROOT / "profiles" / "r01" / "k_label_traffic_cfg5.json"
+        if args.config == 5 and layout == "strips" and tf.exists():
+            traffic = json.loads(tf.read_text())["traffic_bytes"]  # ncu dram bytes of one k_label launch (per launch)
         roof = {
             "bound": "fp32", "kernel": f"k_label<1,{1 if layout == 'strips' else 0}> (fp32x2 VOS tile loop, {layout} layout)", "achieved": achieved, "peak": peak,
-            "unit": "evals/s", "frac": achieved / peak, "traffic": None,
+            "unit": "evals/s", "frac": achieved / peak, "traffic": traffic,
+            "traffic_note": "bytes per k_label launch from profiles/r01/k_label_traffic_cfg5.json (ncu dram__bytes_read+write)",
             "peak_basis": f"{sms} SMs x {FP32_LANES_PER_SM} FP32 lanes x {sm_max:.0f} MHz (MEASURED_PEAKS.json sm_max_mhz)"
                           f" / {OPS_PER_EVAL} FP32-pipe ops per eval (SURVEY.md §8d); per GPU",
             "kernel_ms_avg": k_ms, "kernel_share_of_step": k_ms / (sum(step_ms) / len(step_ms)),
