@@ -78,6 +78,7 @@ struct NonConvergence : std::runtime_error {
 /// Device and numerics options of the B200 path (defaults: nm_default_options).
 struct GpuOptions {
   nm_options opt;
+  bool validate_closed = true;  // check the SPEC.md:227 precondition with validate_closed (surface.hpp:80-104)
   GpuOptions() { nm_default_options(&opt); }
 };
 
@@ -92,7 +93,7 @@ inline void check(int rc) {
 /// RAII owner of one nm_ctx (one device + stream + replicated surfaces).
 class Context {
  public:
-  explicit Context(const GpuOptions& o = {}) { check(nm_create(&ctx_, &o.opt)); }
+  explicit Context(const GpuOptions& o = {}) : validate_(o.validate_closed) { check(nm_create(&ctx_, &o.opt)); }
   ~Context() {
     if (ctx_) nm_destroy(ctx_);
   }
@@ -102,6 +103,15 @@ class Context {
 
   void set_segmentation(const SurfaceSegmentation& seg) {
     validate(seg);
+    if (validate_) {
+      for (const CompartmentSurface& c : seg.compartments) {
+        const ClosednessReport r = validate_closed(c.mesh);
+        if (!r.ok())
+          throw LabelingError("surface '" + c.name + "' is not closed: " + std::to_string(r.open_edges.size()) +
+                              " open edges, " + std::to_string(r.orientation_errors.size()) +
+                              " orientation errors (SPEC.md:227)");
+      }
+    }
     std::vector<double> xyz;
     std::vector<std::uint32_t> tri, off{0};
     std::vector<int> ids;
@@ -131,6 +141,7 @@ class Context {
 
  private:
   nm_ctx* ctx_ = nullptr;
+  bool validate_ = true;
 };
 
 inline const double* xyz_of(const std::vector<Vec3>& v) {

@@ -110,6 +110,12 @@ int nm_label_tets(nm_ctx* ctx, const uint32_t* tets, size_t nt, const uint32_t* 
 int nm_label_mesh(nm_ctx* ctx, const double* nodes, size_t n_nodes, const uint32_t* tets, size_t nt,
                   double threshold, int* labels_out, uint32_t* masks_out /* nullable */, nm_stats* stats);
 
+/* Tet-centroid labeling (query point = (a+b+c+d)*0.25 in fp64): label =
+ * label_ids[lowest k with s_k(centroid) >= T], else 0. The alternative query
+ * point named by the north star ("tet centroids or vertices"). */
+int nm_label_centroids(nm_ctx* ctx, const double* nodes, size_t n_nodes, const uint32_t* tets, size_t nt,
+                       double threshold, int* labels_out, nm_stats* stats);
+
 /* Tets whose node masks disagree on an active compartment (OR != AND on
  * active_mask), ascending; *count receives how many were written. */
 int nm_flag_boundary(nm_ctx* ctx, const uint32_t* tets, size_t nt, const uint32_t* masks, size_t n_nodes,

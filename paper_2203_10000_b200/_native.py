@@ -78,6 +78,8 @@ LABEL_API = {
                                      ctypes.POINTER(NmStats)]),
     "nm_label_mesh": (ctypes.c_int, [ctypes.c_void_p, c_double_p, ctypes.c_size_t, c_u32_p, ctypes.c_size_t,
                                      ctypes.c_double, c_i32_p, c_u32_p, ctypes.POINTER(NmStats)]),
+    "nm_label_centroids": (ctypes.c_int, [ctypes.c_void_p, c_double_p, ctypes.c_size_t, c_u32_p, ctypes.c_size_t,
+                                          ctypes.c_double, c_i32_p, ctypes.POINTER(NmStats)]),
     "nm_flag_boundary": (ctypes.c_int, [ctypes.c_void_p, c_u32_p, ctypes.c_size_t, c_u32_p, ctypes.c_size_t,
                                         ctypes.c_uint32, c_u32_p, c_size_p]),
     "nm_relabel": (ctypes.c_int, [ctypes.c_void_p, c_double_p, ctypes.c_size_t, c_u32_p, ctypes.c_size_t,
@@ -232,6 +234,16 @@ class Context:
                                      ptr(tets, ctypes.c_uint32), tets.shape[0], threshold, ptr(labels, ctypes.c_int),
                                      ptr(masks, ctypes.c_uint32) if masks is not None else None, ctypes.byref(st)))
         return labels, masks, st.as_dict()
+
+    def label_centroids(self, nodes, tets, threshold=0.5):
+        nodes = np.ascontiguousarray(nodes, dtype=np.float64).reshape(-1, 3)
+        tets = np.ascontiguousarray(tets, dtype=np.uint32).reshape(-1, 4)
+        labels = np.empty(tets.shape[0], dtype=np.int32)
+        st = NmStats()
+        check(self.lib.nm_label_centroids(self.handle, ptr(nodes, ctypes.c_double), nodes.shape[0],
+                                          ptr(tets, ctypes.c_uint32), tets.shape[0], threshold,
+                                          ptr(labels, ctypes.c_int), ctypes.byref(st)))
+        return labels, st.as_dict()
 
     def flag_boundary(self, tets, masks, active_mask=0xFFFFFFFF):
         tets = np.ascontiguousarray(tets, dtype=np.uint32).reshape(-1, 4)

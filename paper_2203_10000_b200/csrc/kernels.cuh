@@ -571,3 +571,32 @@ __global__ void k_relabel_tets(const uint4* tets, std::size_t nt, const std::uin
 }
 
 }  // namespace nm
+
+namespace nm {
+
+// Centroid query points (a + b + c + d) * 0.25 in fp64 (the oracle's order).
+__global__ void k_centroids(const double* nodes, const uint4* tets, std::size_t nt, double* out) {
+  for (std::size_t t = blockIdx.x * static_cast<std::size_t>(blockDim.x) + threadIdx.x; t < nt;
+       t += static_cast<std::size_t>(gridDim.x) * blockDim.x) {
+    const uint4 e = tets[t];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      const double s = __dadd_rn(__dadd_rn(__dadd_rn(nodes[3 * static_cast<std::size_t>(e.x) + d],
+                                                     nodes[3 * static_cast<std::size_t>(e.y) + d]),
+                                           nodes[3 * static_cast<std::size_t>(e.z) + d]),
+                                 nodes[3 * static_cast<std::size_t>(e.w) + d]);
+      out[3 * t + d] = __dmul_rn(s, 0.25);
+    }
+  }
+}
+
+// label = id[ffs(mask)] or 0 for point-mode labels (centroids).
+__global__ void k_mask_labels(const std::uint32_t* masks, std::size_t n, int* labels, const LabelIds ids) {
+  for (std::size_t i = blockIdx.x * static_cast<std::size_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<std::size_t>(gridDim.x) * blockDim.x) {
+    const std::uint32_t m = masks[i];
+    labels[i] = m ? ids.id[__ffs(m) - 1] : 0;
+  }
+}
+
+}  // namespace nm

@@ -914,6 +914,33 @@ int nm_label_mesh(nm_ctx* c, const double* nodes, std::size_t n, const std::uint
   });
 }
 
+int nm_label_centroids(nm_ctx* c, const double* nodes, std::size_t n, const std::uint32_t* tets, std::size_t nt,
+                       double T, int* labels_out, nm_stats* stats) {
+  return guarded([&] {
+    require_surfaces(c);
+    check_tets(tets, nt, n);
+    NM_CUDA(cudaSetDevice(c->opt.device));
+    cudaStream_t st = c->stream;
+    auto* d_nodes = c->meshA_nodes.as<double>(3 * std::max<std::size_t>(n, 1));
+    auto* d_tets = c->tets.as<std::uint32_t>(4 * std::max<std::size_t>(nt, 1));
+    auto* d_cen = c->pts.as<double>(3 * std::max<std::size_t>(nt, 1));
+    auto* d_masks = c->masks.as<std::uint32_t>(std::max<std::size_t>(nt, 1));
+    auto* d_labels = c->labels.as<int>(std::max<std::size_t>(nt, 1));
+    if (n) NM_CUDA(cudaMemcpyAsync(d_nodes, nodes, 3 * n * sizeof(double), cudaMemcpyHostToDevice, st));
+    if (nt) NM_CUDA(cudaMemcpyAsync(d_tets, tets, 4 * nt * sizeof(std::uint32_t), cudaMemcpyHostToDevice, st));
+    if (nt)
+      nm::k_centroids<<<grid_for(nt, 256, c->sm_count * 32), 256, 0, st>>>(d_nodes, reinterpret_cast<const uint4*>(d_tets),
+                                                                          nt, d_cen);
+    label_nodes_dev(c, d_cen, nt, T, d_masks, nullptr, st, stats);
+    if (nt) {
+      nm::k_mask_labels<<<grid_for(nt, 256, c->sm_count * 32), 256, 0, st>>>(d_masks, nt, d_labels, c->ids);
+      NM_CUDA(cudaGetLastError());
+      NM_CUDA(cudaMemcpyAsync(labels_out, d_labels, nt * sizeof(int), cudaMemcpyDeviceToHost, st));
+    }
+    NM_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
 int nm_flag_boundary(nm_ctx* c, const std::uint32_t* tets, std::size_t nt, const std::uint32_t* masks,
                      std::size_t n_nodes, std::uint32_t active, std::uint32_t* ids_out, std::size_t* count) {
   return guarded([&] {

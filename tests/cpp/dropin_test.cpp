@@ -47,6 +47,14 @@ int main(int argc, char** argv) {
     return 4;
   } catch (const LabelingError&) {
   }
+  // open surface -> LabelingError (validate_closed)
+  SurfaceSegmentation open_seg = seg;
+  open_seg.compartments[0].mesh.triangles.pop_back();
+  try {
+    (void)initial_label(mesh, open_seg, params);
+    return 5;
+  } catch (const LabelingError&) {
+  }
   FILE* f = std::fopen(out_path, "wb");
   std::fwrite(labels.data(), sizeof(int), labels.size(), f);
   std::fclose(f);

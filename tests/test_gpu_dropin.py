@@ -41,3 +41,55 @@ def test_bench_nccl_path_one_rank(tmp_path):
     assert r.returncode == 0, r.stderr[-3000:]
     line = json.loads([l for l in r.stdout.splitlines() if l.startswith("{")][-1])
     assert line["n_gpus"] == 1 and line["value"] > 0 and line["config"]["distributed"] is True
+
+
+def _gpu_rank(rank, world, port, out_dir):
+    import torch
+    import torch.distributed as dist
+    from paper_2203_10000_b200._native import Context
+    from paper_2203_10000_b200.distributed import gather_labels, label_mesh_sharded
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        cfg = synth.config(2)
+        S = cfg.surfaces
+        nodes, tets = cfg.lattice_mesh()
+        ctx = Context(0)
+        ctx.set_surfaces(S.xyz, S.tri, S.comp_off, S.label_ids)
+
+        def node_fn(pts):
+            m, _ = ctx.label_nodes(pts.numpy())
+            return torch.from_numpy(m.view(np.int32))
+
+        def tet_fn(t, masks):
+            return torch.from_numpy(ctx.label_tets(t.numpy().view(np.uint32), masks.numpy().view(np.uint32)))
+
+        labels, tsh, masks = label_mesh_sharded(nodes, tets, node_fn, tet_fn, rank, world)
+        full = gather_labels(labels, tsh)
+        if rank == 0:
+            np.save(os.path.join(out_dir, "labels.npy"), full.numpy())
+        ctx.close()
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_ranks_sharded_gpu_equals_single(tmp_path):
+    """Two ranks (processes) each label their node shard / tet range with the
+    CUDA path, masks gathered over gloo: labels equal the single-process GPU
+    labels bit for bit (the N>1 path with real kernels; the collective is
+    host-side so the two ranks never wait on each other inside a kernel)."""
+    import socket
+    import torch.multiprocessing as mp
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    mp.spawn(_gpu_rank, args=(2, port, str(tmp_path)), nprocs=2, join=True)
+    from paper_2203_10000_b200._native import Context
+    cfg = synth.config(2)
+    S = cfg.surfaces
+    nodes, tets = cfg.lattice_mesh()
+    with Context(0) as c:
+        c.set_surfaces(S.xyz, S.tri, S.comp_off, S.label_ids)
+        ref, _, _ = c.label_mesh(nodes, tets)
+    np.testing.assert_array_equal(np.load(tmp_path / "labels.npy"), ref)

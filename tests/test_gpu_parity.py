@@ -229,3 +229,58 @@ def test_results_independent_of_point_set(ctx):
     s_perm, _ = ctx.enclosure(block[perm])
     np.testing.assert_array_equal(s_sub, s_block[idx])
     np.testing.assert_array_equal(s_perm, s_block[perm])
+
+
+def test_max_compartments_and_limits():
+    """32 compartments (the uint32 mask width, SPEC.md:96-103 allows many):
+    masks and labels match the oracle; 33 are rejected with an error."""
+    from paper_2203_10000_b200._native import Context, NativeError
+    rng = np.random.default_rng(32)
+    parts = [synth.icosphere(float(rng.uniform(2, 6)), 2, center=tuple(rng.uniform(-10, 10, 3))) for _ in range(32)]
+    S = synth.concat_surfaces(parts, labels=list(range(100, 132)))
+    pts = rng.uniform(-16, 16, (5000, 3))
+    with Context(0) as c:
+        c.set_surfaces(S.xyz, S.tri, S.comp_off, S.label_ids)
+        m, _ = c.label_nodes(pts)
+        np.testing.assert_array_equal(m, oracle.label_nodes(pts, S))
+        assert (m >> 31).any()
+        S33 = synth.concat_surfaces(parts + [synth.icosphere(1.0, 1)])
+        with pytest.raises(NativeError, match="32"):
+            c.set_surfaces(S33.xyz, S33.tri, S33.comp_off, S33.label_ids)
+
+
+def test_on_surface_ties_are_reported():
+    """Lattice nodes lying exactly on a box surface (faces, edges, corners)
+    have s = 1/2, 1/4, 1/8 — implementation-defined ties. The
+    GPU must route them to the fp64 fix-up, agree with the oracle's s to
+    1e-12 and report the tie pairs in nm_stats.ties."""
+    from paper_2203_10000_b200._native import Context
+    bx, bt = synth.box_surface([0, 0, 0], [4, 4, 4])
+    S = synth.single_surface(bx, bt)
+    nodes, _ = synth.lattice_mesh((-1.0, -1.0, -1.0), 1.0, (6, 6, 6))
+    with Context(0) as c:
+        c.set_surfaces(S.xyz, S.tri, S.comp_off, S.label_ids)
+        s, st = c.enclosure(nodes)
+    s_ref = oracle.enclosure(nodes, S)
+    on_surface = (s_ref[:, 0] > 1e-9) & (s_ref[:, 0] < 1 - 1e-9)
+    np.testing.assert_allclose(s[on_surface], s_ref[on_surface], atol=1e-12)   # fp64 fix-up
+    np.testing.assert_allclose(s[~on_surface], s_ref[~on_surface], atol=S_EXPECT)
+    on_face = np.isclose(s_ref[:, 0], 0.5, atol=1e-9)
+    assert on_face.sum() > 0 and st["ties"] == int(on_face.sum())
+    assert st["flagged_points"] >= int(np.count_nonzero((s_ref[:, 0] > 1e-9) & (s_ref[:, 0] < 1 - 1e-9)))
+
+
+def test_centroid_mode(ctx):
+    """nm_label_centroids (query points = tet centroids) == oracle on the
+    centroids; on cfg1 it labels ~the sphere volume (cf. test_sphere_volume_kat)."""
+    cfg = synth.config(1)
+    S = cfg.surfaces
+    nodes, tets = cfg.lattice_mesh()
+    ctx.set_surfaces(S.xyz, S.tri, S.comp_off, S.label_ids)
+    lab, st = ctx.label_centroids(nodes, tets)
+    a, b, c, d = (nodes[tets[:, i]] for i in range(4))
+    cen = (a + b + c + d) * 0.25
+    m = oracle.label_nodes(cen, S)
+    ref = np.where(m != 0, S.label_ids[0], 0).astype(np.int32)
+    np.testing.assert_array_equal(lab, ref)
+    assert st["evals"] == tets.shape[0] * S.n_triangles
