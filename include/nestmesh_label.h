@@ -165,6 +165,19 @@ int nm_refine_relabel(nm_ctx* ctx, const double* nodes, size_t n_nodes, const ui
                       const uint32_t* masks /* nullable */, double threshold, uint32_t active_mask, int levels,
                       nm_mesh** out, nm_stats* stats);
 
+/* ---- compartment boundary extraction on the device ------------------------
+ * extract_compartment_boundary / extract_region_boundary (mesh.hpp:100-155):
+ * faces owned by exactly one tet whose label is in label_set, outward from
+ * that tet (mesh.hpp:57-64), sorted lexicographically, plus the sorted unique
+ * boundary node ids — the reference's output, bit for bit. With a single
+ * label that no tet carries the call fails with "UnknownLabel" (mesh.hpp:21-24). */
+typedef struct nm_boundary nm_boundary;
+int nm_extract_boundary(nm_ctx* ctx, const uint32_t* tets, size_t nt, const int* labels, const int* label_set,
+                        int n_set, nm_boundary** out);
+int nm_boundary_sizes(const nm_boundary* b, size_t* n_triangles, size_t* n_nodes);
+int nm_boundary_copy(const nm_boundary* b, uint32_t* triangles, uint32_t* nodes);
+void nm_boundary_free(nm_boundary* b);
+
 /* Compartment count, real and padded (evaluated) triangle slots, and the tile
  * layout (1 triangles, 2 strips) chosen for the current surfaces. */
 int nm_surface_info(nm_ctx* ctx, int* K, size_t* triangles, size_t* padded_triangles, int* layout);

@@ -70,10 +70,29 @@ def ref():
         R.ref_signed_volume.restype = ctypes.c_double
         R.ref_compartment_boundary_size.argtypes = [_d, _sz, _u32, _sz, _i32, ctypes.c_int]
         R.ref_compartment_boundary_size.restype = ctypes.c_long
+        R.ref_boundary.argtypes = [_u32, _sz, _i32, _i32, ctypes.c_int, _u32, _sz, _u32, _sz, ctypes.POINTER(_sz)]
+        R.ref_boundary.restype = ctypes.c_long
         R.ref_validate_mesh_ok.argtypes = [_d, _sz, _u32, _sz]
         R.ref_validate_mesh_ok.restype = ctypes.c_int
         _ref = R
     return _ref
+
+
+def ref_boundary(tets, labels, label_set):
+    """The UNMODIFIED reference extract_compartment_boundary / extract_region_boundary."""
+    tets = np.ascontiguousarray(tets, np.uint32).reshape(-1, 4)
+    labels = np.ascontiguousarray(labels, np.int32)
+    ls = np.ascontiguousarray(np.atleast_1d(label_set), np.int32)
+    cap = 4 * tets.shape[0]
+    tri = np.empty((max(cap, 1), 3), np.uint32)
+    nodes = np.empty(max(4 * tets.shape[0], 1), np.uint32)
+    nn = ctypes.c_size_t()
+    c = ref().ref_boundary(_p(tets, ctypes.c_uint32), tets.shape[0], _p(labels, ctypes.c_int), _p(ls, ctypes.c_int),
+                           ls.size, _p(tri, ctypes.c_uint32), cap, _p(nodes, ctypes.c_uint32), nodes.size,
+                           ctypes.byref(nn))
+    if c < 0:
+        raise KeyError(f"UnknownLabel {label_set}")
+    return tri[:c].copy(), nodes[:nn.value].copy()
 
 
 def workers_default() -> int:

@@ -109,6 +109,30 @@ long ref_compartment_boundary_size(const double* nodes, std::size_t nn, const st
   }
 }
 
+// mesh.hpp:100-155 — the reference's boundary of one label (n_set == 1,
+// extract_compartment_boundary) or of a label set (extract_region_boundary).
+// Returns the triangle count (-1 on UnknownLabel); copies up to the given
+// capacities.
+long ref_boundary(const std::uint32_t* tets, std::size_t nt, const int* labels, const int* label_set, int n_set,
+                  std::uint32_t* tri_out, std::size_t tri_cap, std::uint32_t* nodes_out, std::size_t nodes_cap,
+                  std::size_t* n_nodes) {
+  TetrahedralMesh m;
+  m.tetrahedra.resize(nt);
+  for (std::size_t i = 0; i < nt; ++i) std::memcpy(m.tetrahedra[i].data(), tets + 4 * i, 16);
+  m.labels.assign(labels, labels + nt);
+  CompartmentBoundary b;
+  try {
+    if (n_set == 1) b = extract_compartment_boundary(m, label_set[0]);
+    else b = extract_region_boundary(m, std::vector<int>(label_set, label_set + n_set));
+  } catch (const UnknownLabel&) {
+    return -1;
+  }
+  for (std::size_t i = 0; i < b.triangles.size() && i < tri_cap; ++i) std::memcpy(tri_out + 3 * i, b.triangles[i].data(), 12);
+  for (std::size_t i = 0; i < b.nodes.size() && i < nodes_cap; ++i) nodes_out[i] = b.nodes[i];
+  *n_nodes = b.nodes.size();
+  return static_cast<long>(b.triangles.size());
+}
+
 // mesh.hpp:194-235 — 1 when validate_mesh reports no findings.
 int ref_validate_mesh_ok(const double* nodes, std::size_t nn, const std::uint32_t* tets, std::size_t nt) {
   TetrahedralMesh m;

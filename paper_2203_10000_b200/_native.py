@@ -102,6 +102,11 @@ LABEL_API = {
     "nm_refine_relabel": (ctypes.c_int, [ctypes.c_void_p, c_double_p, ctypes.c_size_t, c_u32_p, ctypes.c_size_t,
                                          c_u32_p, ctypes.c_double, ctypes.c_uint32, ctypes.c_int,
                                          ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(NmStats)]),
+    "nm_extract_boundary": (ctypes.c_int, [ctypes.c_void_p, c_u32_p, ctypes.c_size_t, c_i32_p, c_i32_p, ctypes.c_int,
+                                           ctypes.POINTER(ctypes.c_void_p)]),
+    "nm_boundary_sizes": (ctypes.c_int, [ctypes.c_void_p, c_size_p, c_size_p]),
+    "nm_boundary_copy": (ctypes.c_int, [ctypes.c_void_p, c_u32_p, c_u32_p]),
+    "nm_boundary_free": (None, [ctypes.c_void_p]),
     "nm_surface_info": (ctypes.c_int, [ctypes.c_void_p, c_i32_p, c_size_p, c_size_p, c_i32_p]),
 }
 
@@ -234,6 +239,25 @@ class Context:
                                      ptr(tets, ctypes.c_uint32), tets.shape[0], threshold, ptr(labels, ctypes.c_int),
                                      ptr(masks, ctypes.c_uint32) if masks is not None else None, ctypes.byref(st)))
         return labels, masks, st.as_dict()
+
+    def extract_boundary(self, tets, labels, label_set):
+        """(triangles (m,3) uint32 outward + sorted, nodes sorted unique) of the
+        region whose labels are in label_set (mesh.hpp:100-155)."""
+        tets = np.ascontiguousarray(tets, dtype=np.uint32).reshape(-1, 4)
+        labels = np.ascontiguousarray(labels, dtype=np.int32)
+        ls = np.ascontiguousarray(np.atleast_1d(label_set), dtype=np.int32)
+        h = ctypes.c_void_p()
+        check(self.lib.nm_extract_boundary(self.handle, ptr(tets, ctypes.c_uint32), tets.shape[0],
+                                           ptr(labels, ctypes.c_int), ptr(ls, ctypes.c_int), ls.size, ctypes.byref(h)))
+        try:
+            nt_, nn_ = ctypes.c_size_t(), ctypes.c_size_t()
+            self.lib.nm_boundary_sizes(h, ctypes.byref(nt_), ctypes.byref(nn_))
+            tri = np.empty((nt_.value, 3), np.uint32)
+            nodes = np.empty(nn_.value, np.uint32)
+            self.lib.nm_boundary_copy(h, ptr(tri, ctypes.c_uint32), ptr(nodes, ctypes.c_uint32))
+        finally:
+            self.lib.nm_boundary_free(h)
+        return tri, nodes
 
     def label_centroids(self, nodes, tets, threshold=0.5):
         nodes = np.ascontiguousarray(nodes, dtype=np.float64).reshape(-1, 3)

@@ -600,3 +600,66 @@ __global__ void k_mask_labels(const std::uint32_t* masks, std::size_t n, int* la
 }
 
 }  // namespace nm
+
+namespace nm {
+
+__global__ void k_iota(std::uint32_t* p, std::size_t m) {
+  for (std::size_t i = blockIdx.x * static_cast<std::size_t>(blockDim.x) + threadIdx.x; i < m;
+       i += static_cast<std::size_t>(gridDim.x) * blockDim.x)
+    p[i] = static_cast<std::uint32_t>(i);
+}
+
+// in_region[t] = labels[t] in set (extract_region_boundary, mesh.hpp:146-155)
+__global__ void k_region(const int* labels, std::size_t nt, const LabelIds set, int n_set, std::uint8_t* in_region) {
+  for (std::size_t t = blockIdx.x * static_cast<std::size_t>(blockDim.x) + threadIdx.x; t < nt;
+       t += static_cast<std::size_t>(gridDim.x) * blockDim.x) {
+    const int l = labels[t];
+    bool in = false;
+    for (int k = 0; k < n_set; ++k) in |= set.id[k] == l;
+    in_region[t] = in ? 1 : 0;
+  }
+}
+
+// A face is on the region boundary when exactly one incident tet is in the
+// region (mesh.hpp:100-128).
+struct PredBoundaryFace {
+  const std::int32_t* nbr;
+  const std::uint8_t* in_region;
+  __device__ bool operator()(std::size_t i) const {
+    if (!in_region[i >> 2]) return false;
+    const std::int32_t o = nbr[i];
+    return o < 0 || !in_region[o];
+  }
+};
+
+struct PredUniqueU32 {
+  const std::uint32_t* k;
+  __device__ bool operator()(std::size_t i) const { return i == 0 || k[i] != k[i - 1]; }
+};
+
+// outward face i of a positively oriented tet (mesh.hpp:57-64)
+__global__ void k_face_tris(const uint4* tets, const std::uint32_t* faces, std::uint32_t nb, std::uint32_t* t0,
+                            std::uint32_t* t1, std::uint32_t* t2) {
+  for (std::uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nb; i += gridDim.x * blockDim.x) {
+    const std::uint32_t f = faces[i];
+    const uint4 e = tets[f >> 2];
+    const std::uint32_t v[4] = {e.x, e.y, e.z, e.w};
+    const int F[4][3] = {{1, 2, 3}, {0, 3, 2}, {0, 1, 3}, {0, 2, 1}};
+    const int k = f & 3;
+    t0[i] = v[F[k][0]];
+    t1[i] = v[F[k][1]];
+    t2[i] = v[F[k][2]];
+  }
+}
+
+__global__ void k_gather_tris(const std::uint32_t* order, std::uint32_t nb, const std::uint32_t* t0,
+                              const std::uint32_t* t1, const std::uint32_t* t2, std::uint32_t* out) {
+  for (std::uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nb; i += gridDim.x * blockDim.x) {
+    const std::uint32_t j = order[i];
+    out[3 * static_cast<std::size_t>(i)] = t0[j];
+    out[3 * static_cast<std::size_t>(i) + 1] = t1[j];
+    out[3 * static_cast<std::size_t>(i) + 2] = t2[j];
+  }
+}
+
+}  // namespace nm

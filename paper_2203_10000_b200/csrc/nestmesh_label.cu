@@ -216,13 +216,13 @@ struct nm_ctx {
   DBuf tri, sub, comp_tiles, xyz64, tri_idx, comp_off;
 
   // scratch
-  DBuf pts, masks, flagmask, nbr, known, want, fkeys, frontier, r_red, r_keys, r_keys2, r_S, r_idx, r_touched,
+  DBuf pts, masks, flagmask, nbr, known, want, fkeys, frontier, lex, region, bfaces, btri, r_red, r_keys, r_keys2, r_S, r_idx, r_touched,
       r_mask, r_cnt, r_offs, r_flag, meshA_nodes, meshA_tets, meshA_labels, meshB_nodes, meshB_tets, meshB_labels,
       meshB_parent, masks2, order, keys, keys_alt, order_alt, cub_tmp, list, chunk, counters, count, tets, labels,
       s_out;
 
   ~nm_ctx() {
-    for (DBuf* b : {&tri, &sub, &comp_tiles, &xyz64, &tri_idx, &comp_off, &pts, &masks, &flagmask, &nbr, &known, &want, &fkeys, &frontier, &r_red, &r_keys, &r_keys2, &r_S,
+    for (DBuf* b : {&tri, &sub, &comp_tiles, &xyz64, &tri_idx, &comp_off, &pts, &masks, &flagmask, &nbr, &known, &want, &fkeys, &frontier, &lex, &region, &bfaces, &btri, &r_red, &r_keys, &r_keys2, &r_S,
                     &r_idx, &r_touched, &r_mask, &r_cnt, &r_offs, &r_flag, &meshA_nodes, &meshA_tets, &meshA_labels,
                     &meshB_nodes, &meshB_tets, &meshB_labels, &meshB_parent, &masks2, &order, &keys,
                     &keys_alt, &order_alt, &cub_tmp, &list, &chunk, &counters, &count, &tets, &labels, &s_out})
@@ -403,6 +403,42 @@ void check_tets(const std::uint32_t* tets, std::size_t nt, std::size_t n_nodes) 
                                         " >= node count " + std::to_string(n_nodes));
 }
 
+
+// Lexicographic order (k0, k1, k2) of m triples by three stable LSD radix
+// passes; returns the device permutation (valid until the next call).
+std::uint32_t* lex_order3(nm_ctx* c, const std::uint32_t* k0, const std::uint32_t* k1, const std::uint32_t* k2,
+                          std::size_t m, cudaStream_t st) {
+  auto* buf = c->lex.as<std::uint32_t>(4 * std::max<std::size_t>(m, 1));
+  std::uint32_t *perm = buf, *perm2 = buf + m, *key = buf + 2 * m, *key2 = buf + 3 * m;
+  nm::k_iota<<<grid_for(std::max<std::size_t>(m, 1), 256, c->sm_count * 32), 256, 0, st>>>(perm, m);
+  if (m <= 1) return perm;
+  std::uint32_t* cur = perm;
+  std::uint32_t* alt = perm2;
+  for (const std::uint32_t* k : {k2, k1, k0}) {
+    nm::k_gather_key<<<grid_for(m, 256, c->sm_count * 32), 256, 0, st>>>(k, cur, m, key);
+    cub::DoubleBuffer<std::uint32_t> kb(key, key2), vb(cur, alt);
+    std::size_t tmp = 0;
+    NM_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, kb, vb, static_cast<int>(m), 0, 32, st));
+    void* tp = c->cub_tmp.get(tmp);
+    NM_CUDA(cub::DeviceRadixSort::SortPairs(tp, tmp, kb, vb, static_cast<int>(m), 0, 32, st));
+    if (vb.Current() != cur) std::swap(cur, alt);
+  }
+  return cur;
+}
+
+// Face adjacency (mesh.hpp:68-88): nbr[4t+f] = tet across local face f, -1 on
+// the mesh boundary. Sorted face triples; equal neighbours share the face.
+void face_adjacency(nm_ctx* c, const uint4* t4, std::size_t nt, std::int32_t* d_nbr, cudaStream_t st) {
+  const std::size_t m = 4 * nt;
+  NM_CUDA(cudaMemsetAsync(d_nbr, 0xff, std::max<std::size_t>(m, 1) * sizeof(std::int32_t), st));
+  if (m <= 1) return;
+  auto* ka = c->fkeys.as<std::uint32_t>(4 * m);
+  std::uint32_t *kb = ka + m, *kc = ka + 2 * m, *fid = ka + 3 * m;
+  nm::k_face_keys<<<grid_for(m, 256, c->sm_count * 32), 256, 0, st>>>(t4, nt, ka, kb, kc, fid);
+  const std::uint32_t* order = lex_order3(c, ka, kb, kc, m, st);
+  nm::k_face_pairs<<<grid_for(m, 256, c->sm_count * 32), 256, 0, st>>>(order, m, ka, kb, kc, d_nbr);
+  NM_CUDA(cudaGetLastError());
+}
 
 struct PredByte {
   const std::uint8_t* v;
@@ -914,6 +950,105 @@ int nm_label_mesh(nm_ctx* c, const double* nodes, std::size_t n, const std::uint
   });
 }
 
+}  // extern "C"
+
+struct nm_boundary {
+  std::vector<std::uint32_t> tri;    // 3 per triangle, outward from the region, lexicographically sorted
+  std::vector<std::uint32_t> nodes;  // sorted, unique
+};
+
+extern "C" {
+
+int nm_extract_boundary(nm_ctx* c, const std::uint32_t* tets, std::size_t nt, const int* labels, const int* label_set,
+                        int n_set, nm_boundary** out) {
+  return guarded([&] {
+    if (!c) throw Error("null context");
+    if (!out) throw Error("null output pointer");
+    *out = nullptr;
+    if (n_set < 1 || n_set > 32) throw Error("label set size must be in [1, 32]");
+    if (4 * nt > 0xffffffffull) throw Error("mesh too large for 32-bit face ids");
+    NM_CUDA(cudaSetDevice(c->opt.device));
+    cudaStream_t st = c->stream;
+    const std::size_t m = 4 * nt;
+    auto* d_tets = c->tets.as<std::uint32_t>(4 * std::max<std::size_t>(nt, 1));
+    auto* d_labels = c->labels.as<int>(std::max<std::size_t>(nt, 1));
+    auto* d_region = c->region.as<std::uint8_t>(std::max<std::size_t>(nt, 1));
+    auto* d_nbr = c->nbr.as<std::int32_t>(std::max<std::size_t>(m, 1));
+    auto* d_count = c->count.as<std::uint32_t>(4);
+    if (nt) NM_CUDA(cudaMemcpyAsync(d_tets, tets, 4 * nt * sizeof(std::uint32_t), cudaMemcpyHostToDevice, st));
+    if (nt) NM_CUDA(cudaMemcpyAsync(d_labels, labels, nt * sizeof(int), cudaMemcpyHostToDevice, st));
+    nm::LabelIds set{};
+    for (int k = 0; k < n_set; ++k) set.id[k] = label_set[k];
+    const uint4* t4 = reinterpret_cast<const uint4*>(d_tets);
+    std::uint32_t in_count = 0;
+    if (nt) {
+      nm::k_region<<<grid_for(nt, 256, c->sm_count * 32), 256, 0, st>>>(d_labels, nt, set, n_set, d_region);
+      std::uint64_t l = 0;
+      select(c, PredByte{d_region}, nt, c->list.as<std::uint32_t>(nt), d_count, st, l);
+      NM_CUDA(cudaMemcpyAsync(&in_count, d_count, sizeof in_count, cudaMemcpyDeviceToHost, st));
+      NM_CUDA(cudaStreamSynchronize(st));
+    }
+    if (n_set == 1 && in_count == 0)
+      throw Error("UnknownLabel: no tetrahedron carries label " + std::to_string(label_set[0]) + " (mesh.hpp:21-24)");
+    face_adjacency(c, t4, nt, d_nbr, st);
+    auto* faces = c->bfaces.as<std::uint32_t>(std::max<std::size_t>(m, 1));
+    std::uint64_t l = 0;
+    select(c, nm::PredBoundaryFace{d_nbr, d_region}, m, faces, d_count, st, l);
+    std::uint32_t nb = 0;
+    NM_CUDA(cudaMemcpyAsync(&nb, d_count, sizeof nb, cudaMemcpyDeviceToHost, st));
+    NM_CUDA(cudaStreamSynchronize(st));
+    auto* tri = c->btri.as<std::uint32_t>(6 * std::max<std::size_t>(nb, 1));
+    std::uint32_t *t0 = tri, *t1 = tri + nb, *t2 = tri + 2 * nb, *sorted = tri + 3 * nb;
+    std::unique_ptr<nm_boundary> res(new nm_boundary);
+    if (nb) {
+      nm::k_face_tris<<<grid_for(nb, 256, c->sm_count * 8), 256, 0, st>>>(t4, faces, nb, t0, t1, t2);
+      const std::uint32_t* order = lex_order3(c, t0, t1, t2, nb, st);
+      nm::k_gather_tris<<<grid_for(nb, 256, c->sm_count * 8), 256, 0, st>>>(order, nb, t0, t1, t2, sorted);
+      NM_CUDA(cudaGetLastError());
+      res->tri.resize(3 * std::size_t(nb));
+      NM_CUDA(cudaMemcpyAsync(res->tri.data(), sorted, 3 * std::size_t(nb) * sizeof(std::uint32_t),
+                              cudaMemcpyDeviceToHost, st));
+      // sorted unique node ids
+      auto* ids = c->keys.as<std::uint32_t>(3 * std::size_t(nb));
+      auto* ids2 = c->keys_alt.as<std::uint32_t>(3 * std::size_t(nb));
+      NM_CUDA(cudaMemcpyAsync(ids, t0, 3 * std::size_t(nb) * sizeof(std::uint32_t), cudaMemcpyDeviceToDevice, st));
+      cub::DoubleBuffer<std::uint32_t> kb(ids, ids2);
+      std::size_t tmp = 0;
+      NM_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tmp, kb, static_cast<int>(3 * nb), 0, 32, st));
+      void* tp = c->cub_tmp.get(tmp);
+      NM_CUDA(cub::DeviceRadixSort::SortKeys(tp, tmp, kb, static_cast<int>(3 * nb), 0, 32, st));
+      const std::uint32_t* sk = kb.Current();
+      auto* uidx = c->frontier.as<std::uint32_t>(3 * std::size_t(nb));
+      select(c, nm::PredUniqueU32{sk}, 3 * std::size_t(nb), uidx, d_count, st, l);
+      std::uint32_t nu = 0;
+      NM_CUDA(cudaMemcpyAsync(&nu, d_count, sizeof nu, cudaMemcpyDeviceToHost, st));
+      NM_CUDA(cudaStreamSynchronize(st));
+      auto* un = c->order_alt.as<std::uint32_t>(std::max<std::uint32_t>(nu, 1));
+      nm::k_gather_key<<<grid_for(std::max<std::uint32_t>(nu, 1), 256, c->sm_count * 8), 256, 0, st>>>(sk, uidx, nu, un);
+      res->nodes.resize(nu);
+      if (nu) NM_CUDA(cudaMemcpyAsync(res->nodes.data(), un, nu * sizeof(std::uint32_t), cudaMemcpyDeviceToHost, st));
+    }
+    NM_CUDA(cudaStreamSynchronize(st));
+    *out = res.release();
+  });
+}
+
+int nm_boundary_sizes(const nm_boundary* b, std::size_t* n_tri, std::size_t* n_nodes) {
+  if (!b) return 1;
+  if (n_tri) *n_tri = b->tri.size() / 3;
+  if (n_nodes) *n_nodes = b->nodes.size();
+  return 0;
+}
+
+int nm_boundary_copy(const nm_boundary* b, std::uint32_t* tri, std::uint32_t* nodes) {
+  if (!b) return 1;
+  if (tri && !b->tri.empty()) std::memcpy(tri, b->tri.data(), b->tri.size() * sizeof(std::uint32_t));
+  if (nodes && !b->nodes.empty()) std::memcpy(nodes, b->nodes.data(), b->nodes.size() * sizeof(std::uint32_t));
+  return 0;
+}
+
+void nm_boundary_free(nm_boundary* b) { delete b; }
+
 int nm_label_centroids(nm_ctx* c, const double* nodes, std::size_t n, const std::uint32_t* tets, std::size_t nt,
                        double T, int* labels_out, nm_stats* stats) {
   return guarded([&] {
@@ -989,28 +1124,8 @@ int nm_relabel(nm_ctx* c, const double* nodes, std::size_t n, const std::uint32_
     if (nt) NM_CUDA(cudaMemcpyAsync(d_labels, labels_io, nt * sizeof(int), cudaMemcpyHostToDevice, st));
     NM_CUDA(cudaMemsetAsync(d_known, 0, std::max<std::size_t>(n, 1), st));
     NM_CUDA(cudaMemsetAsync(d_masks, 0, std::max<std::size_t>(n, 1) * sizeof(std::uint32_t), st));
-    NM_CUDA(cudaMemsetAsync(d_nbr, 0xff, std::max<std::size_t>(m, 1) * sizeof(std::int32_t), st));
     const uint4* t4 = reinterpret_cast<const uint4*>(d_tets);
-    // Face adjacency (mesh.hpp:68-88) by an LSD sort of sorted face triples.
-    if (m > 1) {
-      auto* ka = c->fkeys.as<std::uint32_t>(6 * m);
-      std::uint32_t *kb = ka + m, *kc = ka + 2 * m, *fid = ka + 3 * m, *key = ka + 4 * m, *fid2 = ka + 5 * m;
-      auto* key2 = c->keys_alt.as<std::uint32_t>(m);
-      nm::k_face_keys<<<grid_for(m, 256, c->sm_count * 32), 256, 0, st>>>(t4, nt, ka, kb, kc, fid);
-      std::uint32_t* cur = fid;
-      std::uint32_t* alt = fid2;
-      for (std::uint32_t* k : {kc, kb, ka}) {
-        nm::k_gather_key<<<grid_for(m, 256, c->sm_count * 32), 256, 0, st>>>(k, cur, m, key);
-        cub::DoubleBuffer<std::uint32_t> kb2(key, key2), vb(cur, alt);
-        std::size_t tmp = 0;
-        NM_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, kb2, vb, static_cast<int>(m), 0, 32, st));
-        void* tp = c->cub_tmp.get(tmp);
-        NM_CUDA(cub::DeviceRadixSort::SortPairs(tp, tmp, kb2, vb, static_cast<int>(m), 0, 32, st));
-        if (vb.Current() != cur) std::swap(cur, alt);
-      }
-      nm::k_face_pairs<<<grid_for(m, 256, c->sm_count * 32), 256, 0, st>>>(cur, m, ka, kb, kc, d_nbr);
-      NM_CUDA(cudaGetLastError());
-    }
+    face_adjacency(c, t4, nt, d_nbr, st);
     c->flag_cap = std::max<std::size_t>(n, 1);
     int pass = 0;
     *converged = 0;

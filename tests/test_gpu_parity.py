@@ -284,3 +284,24 @@ def test_centroid_mode(ctx):
     ref = np.where(m != 0, S.label_ids[0], 0).astype(np.int32)
     np.testing.assert_array_equal(lab, ref)
     assert st["evals"] == tets.shape[0] * S.n_triangles
+
+
+def test_extract_boundary_matches_reference(ctx):
+    """Device compartment-boundary extraction == the UNMODIFIED reference
+    extract_compartment_boundary / extract_region_boundary (mesh.hpp:100-155,
+    compiled in oracle/_ref), triangles and nodes bit for bit."""
+    if not oracle.ref_available():
+        pytest.skip("oracle/_ref not built")
+    cfg = synth.config(2)
+    S = cfg.surfaces
+    nodes, tets = synth.lattice_mesh((-110.0, -110.0, -110.0), 5.0, (44, 44, 44))
+    ctx.set_surfaces(S.xyz, S.tri, S.comp_off, S.label_ids)
+    labels, _, _ = ctx.label_mesh(nodes, tets)
+    for ls in ([1], [2], [4], [0], [1, 2], [2, 3, 4]):
+        tri, nb = ctx.extract_boundary(tets, labels, ls)
+        rtri, rnb = oracle.ref_boundary(tets, labels, ls)
+        np.testing.assert_array_equal(tri, rtri)
+        np.testing.assert_array_equal(nb, rnb)
+    from paper_2203_10000_b200._native import NativeError
+    with pytest.raises(NativeError, match="UnknownLabel"):
+        ctx.extract_boundary(tets, labels, [77])
