@@ -110,6 +110,17 @@ int nm_label_tets(nm_ctx* ctx, const uint32_t* tets, size_t nt, const uint32_t* 
 int nm_label_mesh(nm_ctx* ctx, const double* nodes, size_t n_nodes, const uint32_t* tets, size_t nt,
                   double threshold, int* labels_out, uint32_t* masks_out /* nullable */, nm_stats* stats);
 
+/* Regular 5-tet lattice generated on the device, bit-identical to
+ * generate_lattice_mesh (lattice.hpp:40-91): (nx+1)(ny+1)(nz+1) fp64 nodes
+ * and 5 nx ny nz uint32x4 tets into caller device buffers (asynchronous). */
+int nm_lattice_device(nm_ctx* ctx, const double* origin, double h, int nx, int ny, int nz, double* d_nodes,
+                      uint32_t* d_tets, void* stream);
+/* initial_label of a regular lattice without host mesh traffic: the lattice
+ * is generated on the device, labeled, and only the tet labels (and optional
+ * node masks) come back. */
+int nm_label_lattice(nm_ctx* ctx, const double* origin, double h, int nx, int ny, int nz, double threshold,
+                     int* labels_out /* nullable */, uint32_t* masks_out /* nullable */, nm_stats* stats);
+
 /* Tet-centroid labeling (query point = (a+b+c+d)*0.25 in fp64): label =
  * label_ids[lowest k with s_k(centroid) >= T], else 0. The alternative query
  * point named by the north star ("tet centroids or vertices"). */

@@ -78,6 +78,10 @@ LABEL_API = {
                                      ctypes.POINTER(NmStats)]),
     "nm_label_mesh": (ctypes.c_int, [ctypes.c_void_p, c_double_p, ctypes.c_size_t, c_u32_p, ctypes.c_size_t,
                                      ctypes.c_double, c_i32_p, c_u32_p, ctypes.POINTER(NmStats)]),
+    "nm_lattice_device": (ctypes.c_int, [ctypes.c_void_p, c_double_p, ctypes.c_double, ctypes.c_int, ctypes.c_int,
+                                         ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
+    "nm_label_lattice": (ctypes.c_int, [ctypes.c_void_p, c_double_p, ctypes.c_double, ctypes.c_int, ctypes.c_int,
+                                        ctypes.c_int, ctypes.c_double, c_i32_p, c_u32_p, ctypes.POINTER(NmStats)]),
     "nm_label_centroids": (ctypes.c_int, [ctypes.c_void_p, c_double_p, ctypes.c_size_t, c_u32_p, ctypes.c_size_t,
                                           ctypes.c_double, c_i32_p, ctypes.POINTER(NmStats)]),
     "nm_flag_boundary": (ctypes.c_int, [ctypes.c_void_p, c_u32_p, ctypes.c_size_t, c_u32_p, ctypes.c_size_t,
@@ -258,6 +262,23 @@ class Context:
         finally:
             self.lib.nm_boundary_free(h)
         return tri, nodes
+
+    def label_lattice(self, origin, h, n, threshold=0.5, want_masks=False):
+        """initial_label of a lattice generated on the device (no host mesh)."""
+        o = np.ascontiguousarray(origin, dtype=np.float64)
+        nt = 5 * n[0] * n[1] * n[2]
+        labels = np.empty(nt, np.int32)
+        masks = np.empty((n[0] + 1) * (n[1] + 1) * (n[2] + 1), np.uint32) if want_masks else None
+        st = NmStats()
+        check(self.lib.nm_label_lattice(self.handle, ptr(o, ctypes.c_double), h, n[0], n[1], n[2], threshold,
+                                        ptr(labels, ctypes.c_int),
+                                        ptr(masks, ctypes.c_uint32) if masks is not None else None, ctypes.byref(st)))
+        return labels, masks, st.as_dict()
+
+    def lattice_device(self, origin, h, n, d_nodes, d_tets, stream=None):
+        o = np.ascontiguousarray(origin, dtype=np.float64)
+        check(self.lib.nm_lattice_device(self.handle, ptr(o, ctypes.c_double), h, n[0], n[1], n[2],
+                                         d_nodes.data_ptr(), d_tets.data_ptr(), stream))
 
     def label_centroids(self, nodes, tets, threshold=0.5):
         nodes = np.ascontiguousarray(nodes, dtype=np.float64).reshape(-1, 3)

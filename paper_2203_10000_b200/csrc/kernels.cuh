@@ -663,3 +663,74 @@ __global__ void k_gather_tris(const std::uint32_t* order, std::uint32_t nb, cons
 }
 
 }  // namespace nm
+
+namespace nm {
+
+// Regular 5-tet lattice on the device, bit-identical to generate_lattice_mesh
+// (lattice.hpp:40-91): nodes k,j,i-major at origin + (i h, j h, k h); per cell
+// the central + 4 corner tets of the parity pattern; orientation normalised
+// with the fp64 tet_signed_volume of vec3.hpp:79-81 (same operand order).
+__global__ void k_lattice_nodes(double ox, double oy, double oz, double h, int nx, int ny, int nz, double* nodes) {
+  const std::size_t n = static_cast<std::size_t>(nx + 1) * (ny + 1) * (nz + 1);
+  for (std::size_t v = blockIdx.x * static_cast<std::size_t>(blockDim.x) + threadIdx.x; v < n;
+       v += static_cast<std::size_t>(gridDim.x) * blockDim.x) {
+    const int i = static_cast<int>(v % (nx + 1));
+    const int j = static_cast<int>((v / (nx + 1)) % (ny + 1));
+    const int k = static_cast<int>(v / (static_cast<std::size_t>(nx + 1) * (ny + 1)));
+    nodes[3 * v] = __dadd_rn(ox, __dmul_rn(static_cast<double>(i), h));
+    nodes[3 * v + 1] = __dadd_rn(oy, __dmul_rn(static_cast<double>(j), h));
+    nodes[3 * v + 2] = __dadd_rn(oz, __dmul_rn(static_cast<double>(k), h));
+  }
+}
+
+__device__ __forceinline__ double tet_volume64(const double* P, const std::uint32_t* t) {
+  const double* a = P + 3 * static_cast<std::size_t>(t[0]);
+  const double* b = P + 3 * static_cast<std::size_t>(t[1]);
+  const double* c = P + 3 * static_cast<std::size_t>(t[2]);
+  const double* d = P + 3 * static_cast<std::size_t>(t[3]);
+  const double u0 = __dsub_rn(b[0], a[0]), u1 = __dsub_rn(b[1], a[1]), u2 = __dsub_rn(b[2], a[2]);
+  const double v0 = __dsub_rn(c[0], a[0]), v1 = __dsub_rn(c[1], a[1]), v2 = __dsub_rn(c[2], a[2]);
+  const double w0 = __dsub_rn(d[0], a[0]), w1 = __dsub_rn(d[1], a[1]), w2 = __dsub_rn(d[2], a[2]);
+  const double x0 = __dsub_rn(__dmul_rn(v1, w2), __dmul_rn(v2, w1));
+  const double x1 = __dsub_rn(__dmul_rn(v2, w0), __dmul_rn(v0, w2));
+  const double x2 = __dsub_rn(__dmul_rn(v0, w1), __dmul_rn(v1, w0));
+  return __ddiv_rn(__dadd_rn(__dadd_rn(__dmul_rn(u0, x0), __dmul_rn(u1, x1)), __dmul_rn(u2, x2)), 6.0);
+}
+
+__global__ void k_lattice_tets(const double* nodes, int nx, int ny, int nz, uint4* tets) {
+  const std::size_t cells = static_cast<std::size_t>(nx) * ny * nz;
+  for (std::size_t cidx = blockIdx.x * static_cast<std::size_t>(blockDim.x) + threadIdx.x; cidx < cells;
+       cidx += static_cast<std::size_t>(gridDim.x) * blockDim.x) {
+    const int i = static_cast<int>(cidx % nx);
+    const int j = static_cast<int>((cidx / nx) % ny);
+    const int k = static_cast<int>(cidx / (static_cast<std::size_t>(nx) * ny));
+    auto id = [&](int a, int b, int c) {
+      return static_cast<std::uint32_t>((static_cast<std::size_t>(c) * (ny + 1) + b) * (nx + 1) + a);
+    };
+    const std::uint32_t v000 = id(i, j, k), v100 = id(i + 1, j, k), v010 = id(i, j + 1, k), v110 = id(i + 1, j + 1, k),
+                        v001 = id(i, j, k + 1), v101 = id(i + 1, j, k + 1), v011 = id(i, j + 1, k + 1),
+                        v111 = id(i + 1, j + 1, k + 1);
+    std::uint32_t q[5][4];
+    if (((i + j + k) & 1) == 0) {
+      const std::uint32_t e[5][4] = {{v000, v110, v101, v011}, {v100, v000, v110, v101}, {v010, v000, v110, v011},
+                                     {v001, v000, v101, v011}, {v111, v110, v101, v011}};
+      for (int a = 0; a < 5; ++a)
+        for (int b = 0; b < 4; ++b) q[a][b] = e[a][b];
+    } else {
+      const std::uint32_t e[5][4] = {{v100, v010, v001, v111}, {v000, v100, v010, v001}, {v110, v100, v010, v111},
+                                     {v101, v100, v001, v111}, {v011, v010, v001, v111}};
+      for (int a = 0; a < 5; ++a)
+        for (int b = 0; b < 4; ++b) q[a][b] = e[a][b];
+    }
+    for (int a = 0; a < 5; ++a) {
+      if (tet_volume64(nodes, q[a]) < 0.0) {
+        const std::uint32_t s = q[a][2];
+        q[a][2] = q[a][3];
+        q[a][3] = s;
+      }
+      tets[5 * cidx + a] = make_uint4(q[a][0], q[a][1], q[a][2], q[a][3]);
+    }
+  }
+}
+
+}  // namespace nm

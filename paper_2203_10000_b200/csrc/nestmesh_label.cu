@@ -1049,6 +1049,46 @@ int nm_boundary_copy(const nm_boundary* b, std::uint32_t* tri, std::uint32_t* no
 
 void nm_boundary_free(nm_boundary* b) { delete b; }
 
+int nm_lattice_device(nm_ctx* c, const double* origin, double h, int nx, int ny, int nz, double* d_nodes,
+                      std::uint32_t* d_tets, void* stream) {
+  return guarded([&] {
+    if (!c) throw Error("null context");
+    if (!(h > 0.0)) throw Error("lattice cell size must be > 0 (lattice.hpp:19)");
+    if (nx < 1 || ny < 1 || nz < 1) throw Error("lattice cell counts must be >= 1 (lattice.hpp:20)");
+    const std::size_t nn = static_cast<std::size_t>(nx + 1) * (ny + 1) * (nz + 1);
+    const std::size_t cells = static_cast<std::size_t>(nx) * ny * nz;
+    if (nn > 0xffffffffull || 5 * cells > 0xffffffffull) throw Error("lattice exceeds 32-bit ids");
+    NM_CUDA(cudaSetDevice(c->opt.device));
+    cudaStream_t st = c->pick(stream);
+    nm::k_lattice_nodes<<<grid_for(nn, 256, c->sm_count * 32), 256, 0, st>>>(origin[0], origin[1], origin[2], h, nx, ny,
+                                                                            nz, d_nodes);
+    nm::k_lattice_tets<<<grid_for(cells, 128, c->sm_count * 32), 128, 0, st>>>(d_nodes, nx, ny, nz,
+                                                                             reinterpret_cast<uint4*>(d_tets));
+    NM_CUDA(cudaGetLastError());
+  });
+}
+
+int nm_label_lattice(nm_ctx* c, const double* origin, double h, int nx, int ny, int nz, double T, int* labels_out,
+                     std::uint32_t* masks_out, nm_stats* stats) {
+  return guarded([&] {
+    require_surfaces(c);
+    const std::size_t nn = static_cast<std::size_t>(nx + 1) * (ny + 1) * (nz + 1);
+    const std::size_t nt = 5ull * nx * ny * nz;
+    NM_CUDA(cudaSetDevice(c->opt.device));
+    cudaStream_t st = c->stream;
+    auto* d_nodes = c->pts.as<double>(3 * nn);
+    auto* d_tets = c->tets.as<std::uint32_t>(4 * nt);
+    auto* d_masks = c->masks.as<std::uint32_t>(nn);
+    auto* d_labels = c->labels.as<int>(nt);
+    if (nm_lattice_device(c, origin, h, nx, ny, nz, d_nodes, d_tets, st) != 0) throw Error(g_err);
+    label_nodes_dev(c, d_nodes, nn, T, d_masks, nullptr, st, stats);
+    label_tets_dev(c, d_tets, nt, d_masks, d_labels, st, stats);
+    if (labels_out) NM_CUDA(cudaMemcpyAsync(labels_out, d_labels, nt * sizeof(int), cudaMemcpyDeviceToHost, st));
+    if (masks_out) NM_CUDA(cudaMemcpyAsync(masks_out, d_masks, nn * sizeof(std::uint32_t), cudaMemcpyDeviceToHost, st));
+    NM_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
 int nm_label_centroids(nm_ctx* c, const double* nodes, std::size_t n, const std::uint32_t* tets, std::size_t nt,
                        double T, int* labels_out, nm_stats* stats) {
   return guarded([&] {

@@ -305,3 +305,26 @@ def test_extract_boundary_matches_reference(ctx):
     from paper_2203_10000_b200._native import NativeError
     with pytest.raises(NativeError, match="UnknownLabel"):
         ctx.extract_boundary(tets, labels, [77])
+
+
+def test_device_lattice_bitwise(ctx):
+    """nm_lattice_device == generate_lattice_mesh (via the pinned host
+    generator) bit for bit; nm_label_lattice == nm_label_mesh on it."""
+    import torch
+    for (o, h, n) in [((-12.0, -12.0, -12.0), 0.75, (32, 32, 32)), ((-2.0, 1.0, 0.5), 1.25, (3, 4, 2)),
+                      ((-107.5, -107.5, -107.5), 1.0, (60, 17, 33))]:
+        nodes, tets = synth.lattice_mesh(o, h, n)
+        dn = torch.empty(nodes.shape, dtype=torch.float64, device="cuda")
+        dt = torch.empty(tets.shape, dtype=torch.int32, device="cuda")
+        ctx.lattice_device(o, h, n, dn, dt)
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(dn.cpu().numpy(), nodes)
+        np.testing.assert_array_equal(dt.cpu().numpy().view(np.uint32), tets)
+    cfg = synth.config(1)
+    S = cfg.surfaces
+    ctx.set_surfaces(S.xyz, S.tri, S.comp_off, S.label_ids)
+    lab, masks, st = ctx.label_lattice(cfg.origin, cfg.h, cfg.n, want_masks=True)
+    nodes, tets = cfg.lattice_mesh()
+    ref, m_ref, _ = ctx.label_mesh(nodes, tets, want_masks=True)
+    np.testing.assert_array_equal(lab, ref)
+    np.testing.assert_array_equal(masks, m_ref)
