@@ -189,6 +189,16 @@ int nm_boundary_sizes(const nm_boundary* b, size_t* n_triangles, size_t* n_nodes
 int nm_boundary_copy(const nm_boundary* b, uint32_t* triangles, uint32_t* nodes);
 void nm_boundary_free(nm_boundary* b);
 
+/* ---- quality.boundary_distance ---------------------------
+ * Unsigned distance from each point to the closest point of a triangle
+ * surface (exact point-triangle distance; fp32 N-body pass, then fp64 over
+ * the candidates within 1e-3 mm of the fp32 minimum: equal to the fp64
+ * minimum over all triangles). stats->evals counts both passes. */
+int nm_point_surface_distance(nm_ctx* ctx, const double* pts, size_t n, const double* xyz, size_t nv,
+                              const uint32_t* tri, size_t nt, double* dist_out, nm_stats* stats);
+/* Area-uniform samples on a triangle surface with a fixed seed (host code). */
+int nm_sample_surface(const double* xyz, const uint32_t* tri, size_t nt, size_t count, uint64_t seed, double* pts_out);
+
 /* Compartment count, real and padded (evaluated) triangle slots, and the tile
  * layout (1 triangles, 2 strips) chosen for the current surfaces. */
 int nm_surface_info(nm_ctx* ctx, int* K, size_t* triangles, size_t* padded_triangles, int* layout);

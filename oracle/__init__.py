@@ -43,6 +43,7 @@ def lib():
         L.oracle_flag_boundary.restype = _sz
         L.oracle_relabel_recursive.argtypes = [_d, _sz, _u32, _sz, _d, _u32, _u32, _i32, ctypes.c_int, ctypes.c_double,
                                                ctypes.c_int, ctypes.c_int, _i32, _i32, _u8, ctypes.POINTER(_sz)]
+        L.oracle_point_surface_distance.argtypes = [_d, _sz, _d, _u32, _sz, ctypes.c_int, _d]
         L.oracle_lhuilier_solid_angle.argtypes = [_d, _d, _d, _d]
         L.oracle_lhuilier_solid_angle.restype = ctypes.c_double
         _lib = L
@@ -164,6 +165,17 @@ def relabel_recursive(nodes, tets, surfaces, prev_labels, T=0.5, max_iters=64, w
         len(ids), T, max_iters, workers, _p(labels, ctypes.c_int), ctypes.byref(conv), _p(ev, ctypes.c_uint8),
         ctypes.byref(nev))
     return labels, passes, bool(conv.value), ev
+
+
+def point_surface_distance(pts, xyz, tri, workers=0):
+    """quality.boundary_distance restatement, fp64."""
+    pts = np.ascontiguousarray(pts, np.float64).reshape(-1, 3)
+    xyz = np.ascontiguousarray(xyz, np.float64).reshape(-1, 3)
+    tri = np.ascontiguousarray(tri, np.uint32).reshape(-1, 3)
+    out = np.empty(pts.shape[0], np.float64)
+    lib().oracle_point_surface_distance(_p(pts, ctypes.c_double), pts.shape[0], _p(xyz, ctypes.c_double),
+                                        _p(tri, ctypes.c_uint32), tri.shape[0], workers, _p(out, ctypes.c_double))
+    return out
 
 
 def lhuilier(p, a, b, c):

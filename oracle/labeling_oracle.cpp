@@ -268,6 +268,52 @@ int oracle_relabel_recursive(const double* nodes, std::size_t n_nodes, const std
   return passes;
 }
 
+// quality.boundary_distance restatement: unsigned distance
+// to a triangle surface = sqrt(min over triangles of the exact squared
+// point-triangle distance): the plane distance when p projects inside the
+// triangle (all three edge-side tests >= 0), else the nearest edge segment
+// (clamped projection). Operand order of vec3.hpp:32-38, no FMA.
+namespace {
+inline double seg_dist2(const V3& ap, const V3& e) {
+  const double ee = dot(e, e);
+  double t = ee > 0.0 ? dot(ap, e) / ee : 0.0;
+  t = t < 0.0 ? 0.0 : (t > 1.0 ? 1.0 : t);
+  const V3 v{ap.x - t * e.x, ap.y - t * e.y, ap.z - t * e.z};
+  return dot(v, v);
+}
+inline double point_tri_dist2(const V3& p, const V3& a, const V3& b, const V3& c) {
+  const V3 ab = sub(b, a), bc = sub(c, b), ca = sub(a, c);
+  const V3 ap = sub(p, a), bp = sub(p, b), cp = sub(p, c);
+  const V3 n = cross(ab, sub(c, a));
+  const double nn = dot(n, n);
+  const double s0 = dot(cross(ab, ap), n), s1 = dot(cross(bc, bp), n), s2 = dot(cross(ca, cp), n);
+  if (nn > 0.0 && s0 >= 0.0 && s1 >= 0.0 && s2 >= 0.0) {
+    const double h = dot(ap, n);
+    return (h * h) / nn;
+  }
+  double d = seg_dist2(ap, ab);
+  const double d1 = seg_dist2(bp, bc), d2 = seg_dist2(cp, ca);
+  d = d1 < d ? d1 : d;
+  return d2 < d ? d2 : d;
+}
+}  // namespace
+
+int oracle_point_surface_distance(const double* pts, std::size_t n, const double* xyz, const std::uint32_t* tri,
+                                  std::size_t nt, int workers, double* out) {
+  parallel_for(n, workers, [&](std::size_t lo, std::size_t hi) {
+    for (std::size_t i = lo; i < hi; ++i) {
+      const V3 p = load(pts, i);
+      double best = 1e300;
+      for (std::size_t t = 0; t < nt; ++t) {
+        const double q = point_tri_dist2(p, load(xyz, tri[3 * t]), load(xyz, tri[3 * t + 1]), load(xyz, tri[3 * t + 2]));
+        best = q < best ? q : best;
+      }
+      out[i] = std::sqrt(best);
+    }
+  });
+  return 0;
+}
+
 // Independent cross-check formula: L'Huilier's theorem for the solid angle of
 // a spherical triangle, signed by orientation. Used only by tests to pin the
 // VOS restatement (both must agree to ~1e-12 away from the surface).

@@ -111,6 +111,11 @@ LABEL_API = {
     "nm_boundary_sizes": (ctypes.c_int, [ctypes.c_void_p, c_size_p, c_size_p]),
     "nm_boundary_copy": (ctypes.c_int, [ctypes.c_void_p, c_u32_p, c_u32_p]),
     "nm_boundary_free": (None, [ctypes.c_void_p]),
+    "nm_point_surface_distance": (ctypes.c_int, [ctypes.c_void_p, c_double_p, ctypes.c_size_t, c_double_p,
+                                                 ctypes.c_size_t, c_u32_p, ctypes.c_size_t, c_double_p,
+                                                 ctypes.POINTER(NmStats)]),
+    "nm_sample_surface": (ctypes.c_int, [c_double_p, c_u32_p, ctypes.c_size_t, ctypes.c_size_t, ctypes.c_uint64,
+                                         c_double_p]),
     "nm_surface_info": (ctypes.c_int, [ctypes.c_void_p, c_i32_p, c_size_p, c_size_p, c_i32_p]),
 }
 
@@ -263,6 +268,17 @@ class Context:
             self.lib.nm_boundary_free(h)
         return tri, nodes
 
+    def point_surface_distance(self, pts, xyz, tri):
+        pts = np.ascontiguousarray(pts, dtype=np.float64).reshape(-1, 3)
+        xyz = np.ascontiguousarray(xyz, dtype=np.float64).reshape(-1, 3)
+        tri = np.ascontiguousarray(tri, dtype=np.uint32).reshape(-1, 3)
+        out = np.empty(pts.shape[0], np.float64)
+        st = NmStats()
+        check(self.lib.nm_point_surface_distance(self.handle, ptr(pts, ctypes.c_double), pts.shape[0],
+                                                 ptr(xyz, ctypes.c_double), xyz.shape[0], ptr(tri, ctypes.c_uint32),
+                                                 tri.shape[0], ptr(out, ctypes.c_double), ctypes.byref(st)))
+        return out, st.as_dict()
+
     def label_lattice(self, origin, h, n, threshold=0.5, want_masks=False):
         """initial_label of a lattice generated on the device (no host mesh)."""
         o = np.ascontiguousarray(origin, dtype=np.float64)
@@ -385,6 +401,17 @@ def refine(nodes, tets, labels, selected):
     finally:
         lib.nm_mesh_free(h)
     return on, ot, ol, op, nold.value
+
+
+def sample_surface(xyz, tri, count, seed=0):
+    """Area-uniform samples, splitmix64(seed)."""
+    xyz = np.ascontiguousarray(xyz, dtype=np.float64).reshape(-1, 3)
+    tri = np.ascontiguousarray(tri, dtype=np.uint32).reshape(-1, 3)
+    out = np.empty((count, 3), np.float64)
+    if load_label_lib().nm_sample_surface(ptr(xyz, ctypes.c_double), ptr(tri, ctypes.c_uint32), tri.shape[0], count,
+                                          seed, ptr(out, ctypes.c_double)) != 0:
+        raise NativeError("empty surface")
+    return out
 
 
 def exported_symbols(path=LABEL_LIB) -> set:

@@ -25,6 +25,7 @@
 
 #include "kernels.cuh"
 #include "refine.cuh"
+#include "distance.cuh"
 #include "nestmesh_label.h"
 #include "refine.h"
 
@@ -216,13 +217,15 @@ struct nm_ctx {
   DBuf tri, sub, comp_tiles, xyz64, tri_idx, comp_off;
 
   // scratch
-  DBuf pts, masks, flagmask, nbr, known, want, fkeys, frontier, lex, region, bfaces, btri, r_red, r_keys, r_keys2, r_S, r_idx, r_touched,
+  DBuf pts, masks, flagmask, nbr, known, want, fkeys, frontier, lex, region, bfaces, btri, dist_tri, dist_xyz,
+      dist_idx, dist_d32, dist_out, r_red, r_keys, r_keys2, r_S, r_idx, r_touched,
       r_mask, r_cnt, r_offs, r_flag, meshA_nodes, meshA_tets, meshA_labels, meshB_nodes, meshB_tets, meshB_labels,
       meshB_parent, masks2, order, keys, keys_alt, order_alt, cub_tmp, list, chunk, counters, count, tets, labels,
       s_out;
 
   ~nm_ctx() {
-    for (DBuf* b : {&tri, &sub, &comp_tiles, &xyz64, &tri_idx, &comp_off, &pts, &masks, &flagmask, &nbr, &known, &want, &fkeys, &frontier, &lex, &region, &bfaces, &btri, &r_red, &r_keys, &r_keys2, &r_S,
+    for (DBuf* b : {&tri, &sub, &comp_tiles, &xyz64, &tri_idx, &comp_off, &pts, &masks, &flagmask, &nbr, &known, &want, &fkeys, &frontier, &lex, &region, &bfaces, &btri,
+                    &dist_tri, &dist_xyz, &dist_idx, &dist_d32, &dist_out, &r_red, &r_keys, &r_keys2, &r_S,
                     &r_idx, &r_touched, &r_mask, &r_cnt, &r_offs, &r_flag, &meshA_nodes, &meshA_tets, &meshA_labels,
                     &meshB_nodes, &meshB_tets, &meshB_labels, &meshB_parent, &masks2, &order, &keys,
                     &keys_alt, &order_alt, &cub_tmp, &list, &chunk, &counters, &count, &tets, &labels, &s_out})
@@ -1086,6 +1089,66 @@ int nm_label_lattice(nm_ctx* c, const double* origin, double h, int nx, int ny, 
     if (labels_out) NM_CUDA(cudaMemcpyAsync(labels_out, d_labels, nt * sizeof(int), cudaMemcpyDeviceToHost, st));
     if (masks_out) NM_CUDA(cudaMemcpyAsync(masks_out, d_masks, nn * sizeof(std::uint32_t), cudaMemcpyDeviceToHost, st));
     NM_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+int nm_point_surface_distance(nm_ctx* c, const double* pts, std::size_t n, const double* xyz, std::size_t nv,
+                              const std::uint32_t* tri, std::size_t nt, double* dist_out, nm_stats* stats) {
+  return guarded([&] {
+    if (!c) throw Error("null context");
+    if (nt == 0) throw Error("target surface has no triangle (SPEC.md:429 pre: both non-empty)");
+    for (std::size_t i = 0; i < 3 * nt; ++i)
+      if (tri[i] >= nv) throw Error("triangle index out of range");
+    NM_CUDA(cudaSetDevice(c->opt.device));
+    cudaStream_t st = c->stream;
+    if (stats) std::memset(stats, 0, sizeof *stats);
+    double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
+    for (std::size_t v = 0; v < nv; ++v)
+      for (int a = 0; a < 3; ++a) {
+        lo[a] = std::min(lo[a], xyz[3 * v + a]);
+        hi[a] = std::max(hi[a], xyz[3 * v + a]);
+      }
+    const double ctr[3] = {0.5 * (lo[0] + hi[0]), 0.5 * (lo[1] + hi[1]), 0.5 * (lo[2] + hi[2])};
+    std::vector<float4> h32(3 * nt);
+    for (std::size_t t = 0; t < nt; ++t)
+      for (int k = 0; k < 3; ++k) {
+        const double* v = xyz + 3 * std::size_t(tri[3 * t + k]);
+        h32[3 * t + k] = make_float4(float(v[0] - ctr[0]), float(v[1] - ctr[1]), float(v[2] - ctr[2]), 0.0f);
+      }
+    auto* d_t32 = c->dist_tri.as<float4>(3 * nt);
+    auto* d_xyz = c->dist_xyz.as<double>(3 * std::max<std::size_t>(nv, 1));
+    auto* d_idx = c->dist_idx.as<std::uint32_t>(3 * nt);
+    auto* d_pts = c->pts.as<double>(3 * std::max<std::size_t>(n, 1));
+    auto* d_d32 = c->dist_d32.as<float>(std::max<std::size_t>(n, 1));
+    auto* d_out = c->dist_out.as<double>(std::max<std::size_t>(n, 1));
+    auto* counters = c->counters.as<unsigned long long>(8);
+    NM_CUDA(cudaMemsetAsync(counters, 0, 8 * sizeof(unsigned long long), st));
+    NM_CUDA(cudaMemcpyAsync(d_t32, h32.data(), h32.size() * sizeof(float4), cudaMemcpyHostToDevice, st));
+    NM_CUDA(cudaMemcpyAsync(d_xyz, xyz, 3 * nv * sizeof(double), cudaMemcpyHostToDevice, st));
+    NM_CUDA(cudaMemcpyAsync(d_idx, tri, 3 * nt * sizeof(std::uint32_t), cudaMemcpyHostToDevice, st));
+    if (n) NM_CUDA(cudaMemcpyAsync(d_pts, pts, 3 * n * sizeof(double), cudaMemcpyHostToDevice, st));
+    NM_CUDA(cudaStreamSynchronize(st));  // h32 is released at scope exit
+    if (n) {
+      nm::DistParams prm{d_pts, n, d_t32, d_xyz, d_idx, nt, ctr[0], ctr[1], ctr[2], d_d32, d_out, counters};
+      if (stats) NM_CUDA(cudaEventRecord(c->ev[0], st));
+      const unsigned grid = static_cast<unsigned>((n + 255) / 256);
+      nm::k_point_surface_distance<1><<<grid, 256, 0, st>>>(prm);
+      nm::k_point_surface_distance<2><<<grid, 256, 0, st>>>(prm);
+      NM_CUDA(cudaGetLastError());
+      if (stats) NM_CUDA(cudaEventRecord(c->ev[1], st));
+      NM_CUDA(cudaMemcpyAsync(dist_out, d_out, n * sizeof(double), cudaMemcpyDeviceToHost, st));
+    }
+    NM_CUDA(cudaStreamSynchronize(st));
+    if (stats && n) {
+      unsigned long long h[8];
+      NM_CUDA(cudaMemcpy(h, counters, sizeof h, cudaMemcpyDeviceToHost));
+      stats->points = n;
+      stats->triangles = nt;
+      stats->evals = 2ull * n * nt;
+      stats->flagged_pairs = h[4];  // fp64 candidate evaluations
+      stats->launches = 2;
+      NM_CUDA(cudaEventElapsedTime(&stats->ms_label, c->ev[0], c->ev[1]));
+    }
   });
 }
 

@@ -271,6 +271,46 @@ int nm_mesh_copy(const nm_mesh* m, double* nodes, std::uint32_t* tets, int* labe
 
 void nm_mesh_free(nm_mesh* m) { delete m; }
 
+// Area-uniform samples on a triangle surface ("triangle-area-
+// weighted random points with fixed seed"): splitmix64 stream; triangle by
+// binary search on the fp64 cumulative area; barycentric
+// (1 - sqrt(r1), sqrt(r1)(1 - r2), sqrt(r1) r2).
+int nm_sample_surface(const double* xyz, const std::uint32_t* tri, std::size_t nt, std::size_t count,
+                      std::uint64_t seed, double* out) {
+  if (nt == 0) return 1;
+  std::vector<double> cum(nt);
+  double acc = 0.0;
+  for (std::size_t t = 0; t < nt; ++t) {
+    const double* a = xyz + 3 * std::size_t(tri[3 * t]);
+    const double* b = xyz + 3 * std::size_t(tri[3 * t + 1]);
+    const double* c = xyz + 3 * std::size_t(tri[3 * t + 2]);
+    const double u[3] = {b[0] - a[0], b[1] - a[1], b[2] - a[2]}, v[3] = {c[0] - a[0], c[1] - a[1], c[2] - a[2]};
+    const double x = u[1] * v[2] - u[2] * v[1], y = u[2] * v[0] - u[0] * v[2], z = u[0] * v[1] - u[1] * v[0];
+    acc += 0.5 * std::sqrt(x * x + y * y + z * z);
+    cum[t] = acc;
+  }
+  std::uint64_t state = seed;
+  auto next = [&]() {
+    std::uint64_t z = (state += 0x9e3779b97f4a7c15ull);
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+    z ^= z >> 31;
+    return double(z >> 11) * (1.0 / 9007199254740992.0);
+  };
+  for (std::size_t i = 0; i < count; ++i) {
+    const double r0 = next() * acc, r1 = next(), r2 = next();
+    std::size_t t = static_cast<std::size_t>(std::upper_bound(cum.begin(), cum.end(), r0) - cum.begin());
+    if (t >= nt) t = nt - 1;
+    const double* a = xyz + 3 * std::size_t(tri[3 * t]);
+    const double* b = xyz + 3 * std::size_t(tri[3 * t + 1]);
+    const double* c = xyz + 3 * std::size_t(tri[3 * t + 2]);
+    const double s1 = std::sqrt(r1);
+    const double w0 = 1.0 - s1, w1 = s1 * (1.0 - r2), w2 = s1 * r2;
+    for (int d = 0; d < 3; ++d) out[3 * i + d] = w0 * a[d] + w1 * b[d] + w2 * c[d];
+  }
+  return 0;
+}
+
 int nm_mesh_masks(const nm_mesh* m, std::uint32_t* masks) {
   if (!m || m->masks.size() != m->nodes.size() / 3) return 1;
   std::memcpy(masks, m->masks.data(), m->masks.size() * sizeof(std::uint32_t));

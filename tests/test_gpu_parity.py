@@ -328,3 +328,19 @@ def test_device_lattice_bitwise(ctx):
     ref, m_ref, _ = ctx.label_mesh(nodes, tets, want_masks=True)
     np.testing.assert_array_equal(lab, ref)
     np.testing.assert_array_equal(masks, m_ref)
+
+
+def test_point_surface_distance_bitwise_vs_oracle(ctx):
+    """quality.boundary_distance kernel: fp32 pass + fp64 refinement equals the
+    fp64 oracle (min over all triangles) bit for bit; SPEC.md:431-432 KATs."""
+    from paper_2203_10000_b200._native import sample_surface
+    from paper_2203_10000_b200.quality import boundary_distance
+    xyz, tri = synth.icosphere(10.0, 4, center=(30.0, -20.0, 5.0))
+    rng = np.random.default_rng(5)
+    pts = np.concatenate([rng.uniform(10, 50, (3000, 3)) * [1, -1, 0.3], sample_surface(xyz, tri, 2000, seed=3)])
+    d, st = ctx.point_surface_distance(pts, xyz, tri)
+    np.testing.assert_array_equal(d, oracle.point_surface_distance(pts, xyz, tri))
+    assert np.all(d[3000:] < 1e-9)                       # identical surfaces -> < 1e-9 mm
+    outer = synth.icosphere(11.0, 5, center=(30.0, -20.0, 5.0))
+    r = boundary_distance(ctx, xyz, tri, *outer, samples=20000, seed=0)
+    assert abs(r["median"] - 1.0) < 0.05                  # concentric spheres 10 and 11 mm

@@ -97,3 +97,27 @@ def test_two_levels_straddle_refinement_relabels_to_initial():
         nodes, tets = nodes2, tets2
     ok, _ = _faces_conforming(tets)
     assert ok
+
+
+def test_sample_surface_area_uniform_and_deterministic():
+    """area-weighted samples with a fixed seed."""
+    from paper_2203_10000_b200._native import sample_surface
+    xyz = np.array([[0, 0, 0], [4, 0, 0], [0, 1, 0], [0, 0, 1], [1, 0, 1], [0, 1, 1]], np.float64)
+    tri = np.array([[0, 1, 2], [3, 4, 5]], np.uint32)   # areas 2.0 (z=0) and 0.5 (z=1)
+    a = sample_surface(xyz, tri, 20000, seed=7)
+    b = sample_surface(xyz, tri, 20000, seed=7)
+    np.testing.assert_array_equal(a, b)
+    assert np.all(a[:, 0] >= 0) and np.all(a[:, 1] >= 0)
+    on_big = a[:, 2] == 0
+    assert abs(on_big.mean() - 0.8) < 0.015                    # area-weighted triangle choice
+    assert np.all(a[on_big, 0] + 4 * a[on_big, 1] <= 4 + 1e-12)  # inside the big triangle
+    x = a[on_big, 0]
+    assert abs(np.mean(x) - 4 / 3) < 0.03                      # uniform within it (centroid x = 4/3)
+
+
+def test_oracle_point_triangle_distance_kats():
+    tri = np.array([[0, 1, 2]], np.uint32)
+    xyz = np.array([[0, 0, 0], [1, 0, 0], [0, 1, 0]], np.float64)
+    pts = np.array([[0.2, 0.2, 0.5], [2.0, 0.0, 0.0], [-1.0, -1.0, 0.0], [0.5, -2.0, 0.0], [0.6, 0.6, 0.0]])
+    d = oracle.point_surface_distance(pts, xyz, tri)
+    np.testing.assert_allclose(d, [0.5, 1.0, np.sqrt(2.0), 2.0, np.sqrt(2) * 0.1], rtol=1e-12)
