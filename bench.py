@@ -242,6 +242,7 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", type=int, default=5, choices=[1, 2, 3, 4, 5])
     ap.add_argument("--levels", type=int, default=2, help="--config 4: recursive refinement levels")
+    ap.add_argument("--quality", action="store_true", help="also time boundary extraction + boundary_distance")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
@@ -378,6 +379,26 @@ def main():
                "path": "nm_label_mesh (C ABI, host buffers)" if world == 1 else
                        "pinned host shards -> nm_label_nodes_device -> NCCL all-gather -> nm_label_tets_device -> D2H"}
 
+    # §8(f) rows on the labeled mesh (not part of the headline): device
+    # extraction of the region boundary of all compartments (the outer
+    # surface, extract_region_boundary) and its boundary_distance to the
+    # outermost segmentation surface, wall clock.
+    quality = None
+    if rank == 0 and world == 1 and args.quality:
+        from paper_2203_10000_b200.quality import boundary_distance
+        labels_h, _, _ = ctx.label_mesh(nodes, tets)
+        t0 = time.perf_counter()
+        btri, bnodes = ctx.extract_boundary(tets, labels_h, [int(x) for x in S.label_ids])
+        t_ext = time.perf_counter() - t0
+        tx, tt = S.compartment(S.K - 1)
+        t0 = time.perf_counter()
+        r = boundary_distance(ctx, nodes, btri, tx, tt, samples=20000, seed=0)
+        t_dist = time.perf_counter() - t0
+        quality = {"region": "all compartments", "target": S.names[-1], "boundary_triangles": int(btri.shape[0]),
+                   "extract_boundary_s": t_ext, "boundary_distance_s": t_dist,
+                   "distance_evals": r["stats"]["evals"], "median_mm": r["median"], "q25_mm": r["q25"],
+                   "q75_mm": r["q75"], "fp64_candidates": r["stats"]["flagged_pairs"]}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(nodes, S, target_s=args.cpu_seconds)
@@ -414,6 +435,7 @@ def main():
                                                               "far_subtiles", "ms_label", "ms_fixup")},
             "lattice_generation_s": gen_s, "timed_wall_s": wall,
             "surface_layout": sinfo,
+            "quality": quality,
         }
         print(json.dumps(line), flush=True)
     if use_dist:
