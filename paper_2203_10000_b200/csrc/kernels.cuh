@@ -22,8 +22,8 @@ constexpr int kSub = 32;                // triangles per subtile (near/far decis
 constexpr int kSubPerTile = kTile / kSub;
 constexpr int kSubRec = 5;               // float4 per subtile record: sphere of the subtile + of its 4 groups of 8
 constexpr int kBlock = 256;             // threads per CTA of k_label
-#ifndef NM_DIRECT_LDG
-#define NM_DIRECT_LDG 0
+#ifndef NM_WARP_TILES
+#define NM_WARP_TILES 0                 // 1: each warp stages its own tile copy (no CTA barriers; measured 5% slower)
 #endif
 #ifndef NM_MIN_BLOCKS
 #define NM_MIN_BLOCKS 2                 // resident CTAs per SM requested for k_label<1>
@@ -62,11 +62,13 @@ __global__ void __launch_bounds__(kBlock, (NP == 1 ? NM_MIN_BLOCKS : 1)) k_label
   constexpr int P = 2 * NP;
   constexpr int kSubF4 = STRIP ? (kSub / kSegTris) * kSegF4 : kSub * 3;  // float4 per subtile
   constexpr int kTileF4 = kSubF4 * kSubPerTile;
-#if NM_DIRECT_LDG
-  // Tiles are read straight from global memory: every lane of a warp loads
-  // the same address (one broadcast transaction, L1-resident across the
-  // CTA's warps), so warps stream through the surface set without
-  // block-wide barriers.
+#if NM_WARP_TILES
+  // Every warp stages its own copy of the tile in dynamic shared memory
+  // (kLabelSmemPerWarp<STRIP> bytes): warps whose points need the near path
+  // never hold the others up at a CTA barrier.
+  extern __shared__ float4 nm_dyn_smem[];
+  float4* const s_tri = nm_dyn_smem + (threadIdx.x >> 5) * (kTileF4 + kSubPerTile * kSubRec);
+  float4* const s_sub = s_tri + kTileF4;
 #else
   __shared__ float4 s_tri[kTileF4];
   __shared__ float4 s_sub[kSubPerTile * kSubRec];
@@ -115,9 +117,16 @@ __global__ void __launch_bounds__(kBlock, (NP == 1 ? NM_MIN_BLOCKS : 1)) k_label
     }
     for (; tile < tile_end; ++tile) {
       const float4* gt = prm.tri + static_cast<std::size_t>(tile) * kTileF4;
-#if NM_DIRECT_LDG
-      const float4* s_tri = gt;
-      const float4* s_sub = prm.sub + static_cast<std::size_t>(tile) * kSubPerTile * kSubRec;
+#if NM_WARP_TILES
+      {
+        const int lane = threadIdx.x & 31;
+        const float4* gs = prm.sub + static_cast<std::size_t>(tile) * kSubPerTile * kSubRec;
+        __syncwarp();
+#pragma unroll 4
+        for (int i = lane; i < kTileF4; i += 32) s_tri[i] = __ldg(gt + i);
+        for (int i = lane; i < kSubPerTile * kSubRec; i += 32) s_sub[i] = __ldg(gs + i);
+        __syncwarp();
+      }
 #else
       __syncthreads();
 #pragma unroll

@@ -250,6 +250,31 @@ int grid_for(std::size_t n, int block, int cap) {
   return static_cast<int>(std::max<std::size_t>(1, std::min<std::size_t>(g, static_cast<std::size_t>(cap))));
 }
 
+// Dynamic shared memory of k_label: one tile copy per warp (NM_WARP_TILES).
+std::size_t label_smem_bytes(bool strips) {
+#if NM_WARP_TILES
+  const int sub_f4 = strips ? (nm::kSub / nm::kSegTris) * nm::kSegF4 : nm::kSub * 3;
+  return static_cast<std::size_t>(nm::kBlock / 32) * (sub_f4 * nm::kSubPerTile + nm::kSubPerTile * nm::kSubRec) *
+         sizeof(float4);
+#else
+  (void)strips;
+  return 0;
+#endif
+}
+
+void set_label_smem_attributes() {
+#if NM_WARP_TILES
+  NM_CUDA(cudaFuncSetAttribute(nm::k_label<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               static_cast<int>(label_smem_bytes(true))));
+  NM_CUDA(cudaFuncSetAttribute(nm::k_label<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               static_cast<int>(label_smem_bytes(true))));
+  NM_CUDA(cudaFuncSetAttribute(nm::k_label<1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               static_cast<int>(label_smem_bytes(false))));
+  NM_CUDA(cudaFuncSetAttribute(nm::k_label<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               static_cast<int>(label_smem_bytes(false))));
+#endif
+}
+
 // Ordered compaction of [0,n) under pred into out; count on the device.
 template <class Pred>
 void select(nm_ctx* c, Pred pred, std::size_t n, std::uint32_t* out, std::uint32_t* d_count, cudaStream_t st,
@@ -326,12 +351,13 @@ void label_nodes_dev(nm_ctx* c, const double* d_pts, std::size_t n, double T, st
     const int np = c->opt.pairs_per_thread;
     const std::size_t per_block = static_cast<std::size_t>(nm::kBlock) * 2 * np;
     const unsigned grid = static_cast<unsigned>((n + per_block - 1) / per_block);
+    const std::size_t smem = label_smem_bytes(c->strips);
     if (c->strips) {
-      if (np == 2) nm::k_label<2, true><<<grid, nm::kBlock, 0, st>>>(prm);
-      else nm::k_label<1, true><<<grid, nm::kBlock, 0, st>>>(prm);
+      if (np == 2) nm::k_label<2, true><<<grid, nm::kBlock, smem, st>>>(prm);
+      else nm::k_label<1, true><<<grid, nm::kBlock, smem, st>>>(prm);
     } else {
-      if (np == 2) nm::k_label<2, false><<<grid, nm::kBlock, 0, st>>>(prm);
-      else nm::k_label<1, false><<<grid, nm::kBlock, 0, st>>>(prm);
+      if (np == 2) nm::k_label<2, false><<<grid, nm::kBlock, smem, st>>>(prm);
+      else nm::k_label<1, false><<<grid, nm::kBlock, smem, st>>>(prm);
     }
   }
   NM_CUDA(cudaGetLastError());
@@ -575,6 +601,7 @@ int nm_create(nm_ctx** out, const nm_options* opt) {
       NM_CUDA(cudaGetDeviceProperties(&p, c->opt.device));
       if (p.major != 10) throw Error(std::string("device ") + p.name + " is not sm_100 (Blackwell B200)");
       c->sm_count = p.multiProcessorCount;
+      set_label_smem_attributes();
       NM_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
       for (auto& ev : c->ev) NM_CUDA(cudaEventCreate(&ev));
     } catch (...) {

@@ -1,1 +1,3 @@
-python bench.py --config 3 --steps 1 --warmup 3 --no-e2e --no-cpu-baseline --quality > gpurun_out/bench_cfg3_quality.json 2>gpurun_out/q.err; python -c "import json;d=json.load(open('gpurun_out/bench_cfg3_quality.json'));print(d['quality'], d['value'])"; tail -3 gpurun_out/q.err
+python -m pytest tests/test_gpu_parity.py -q -m gpu -x 2>&1 | tail -2
+python scripts/quick_time.py 5:2000000 3:2000000 2
+NM_LABEL_LIB=probes/libnl_cta.so python scripts/quick_time.py 5:2000000 3:2000000 2
