@@ -21,12 +21,15 @@ constexpr int kTile = 256;              // triangles per shared-memory tile (fp6
 constexpr int kSub = 32;                // triangles per subtile (near/far decision unit)
 constexpr int kSubPerTile = kTile / kSub;
 constexpr int kSubRec = 5;               // float4 per subtile record: sphere of the subtile + of its 4 groups of 8
-constexpr int kBlock = 256;             // threads per CTA of k_label
+#ifndef NM_BLOCK
+#define NM_BLOCK 128
+#endif
+constexpr int kBlock = NM_BLOCK;        // threads per CTA of k_label
 #ifndef NM_WARP_TILES
 #define NM_WARP_TILES 0                 // 1: each warp stages its own tile copy (no CTA barriers; measured 5% slower)
 #endif
 #ifndef NM_MIN_BLOCKS
-#define NM_MIN_BLOCKS 2                 // resident CTAs per SM requested for k_label<1>
+#define NM_MIN_BLOCKS 4                 // resident CTAs per SM requested for k_label<1>
 #endif
 constexpr unsigned kFull = 0xffffffffu;
 constexpr double kInv2Pi = 0.15915494309189533576888376337251;
