@@ -79,6 +79,7 @@ struct NonConvergence : std::runtime_error {
 struct GpuOptions {
   nm_options opt;
   bool validate_closed = true;  // check the SPEC.md:227 precondition with validate_closed (surface.hpp:80-104)
+  std::vector<int> devices;     // > 1 entries: initial_label shards over these devices (SPEC.md:267 --label-workers)
   GpuOptions() { nm_default_options(&opt); }
 };
 
@@ -192,6 +193,31 @@ inline NodeEnclosure node_enclosure(const TetrahedralMesh& mesh, const SurfaceSe
 inline std::vector<int> initial_label(const TetrahedralMesh& mesh, const SurfaceSegmentation& seg,
                                       const SolidAngleParams& params, const GpuOptions& o = {},
                                       nm_stats* stats = nullptr) {
+  if (o.devices.size() > 1) {
+    // validate + flatten through a single-device context, then shard over the group
+    detail::Context::validate(seg);
+    nm_group* g = nullptr;
+    detail::check(nm_group_create(&g, static_cast<int>(o.devices.size()), o.devices.data(), &o.opt));
+    std::unique_ptr<nm_group, int (*)(nm_group*)> guard(g, nm_group_destroy);
+    std::vector<double> xyz;
+    std::vector<std::uint32_t> tri, off{0};
+    std::vector<int> ids;
+    for (const CompartmentSurface& c : seg.compartments) {
+      if (o.validate_closed && !validate_closed(c.mesh).ok())
+        throw LabelingError("surface '" + c.name + "' is not closed (SPEC.md:227)");
+      const auto base = static_cast<std::uint32_t>(xyz.size() / 3);
+      for (const Vec3& p : c.mesh.positions) xyz.insert(xyz.end(), {p.x, p.y, p.z});
+      for (const Triangle& t : c.mesh.triangles) tri.insert(tri.end(), {t[0] + base, t[1] + base, t[2] + base});
+      off.push_back(static_cast<std::uint32_t>(tri.size() / 3));
+      ids.push_back(c.label);
+    }
+    detail::check(nm_group_set_surfaces(g, xyz.data(), xyz.size() / 3, tri.data(), tri.size() / 3, off.data(),
+                                        static_cast<int>(ids.size()), ids.data()));
+    std::vector<int> labels(mesh.tet_count());
+    detail::check(nm_group_label_mesh(g, detail::xyz_of(mesh.nodes), mesh.node_count(), detail::idx_of(mesh.tetrahedra),
+                                      mesh.tet_count(), params.threshold, labels.data(), nullptr, stats));
+    return labels;
+  }
   detail::Context ctx(o);
   ctx.set_segmentation(seg);
   std::vector<int> labels(mesh.tet_count());

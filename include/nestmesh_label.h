@@ -141,6 +141,20 @@ int nm_relabel(nm_ctx* ctx, const double* nodes, size_t n_nodes, const uint32_t*
                double threshold, int max_iters, int* labels_io, int* passes, int* converged,
                uint8_t* evaluated /* nullable */, nm_stats* stats);
 
+/* ---- single-process multi-GPU group (C/C++ hosts; SPEC.md:267 --label-workers)
+ * One context per device (devices may repeat), contiguous node and tet
+ * shards, node masks gathered through pinned host memory. Bit-identical to a
+ * single device. (torch hosts use one process per GPU + NCCL instead:
+ * paper_2203_10000_b200/distributed.py.) */
+typedef struct nm_group nm_group;
+int nm_group_create(nm_group** g, int n_devices, const int* devices /* NULL = 0..n-1 */, const nm_options* opt);
+int nm_group_destroy(nm_group* g);
+int nm_group_size(const nm_group* g);
+int nm_group_set_surfaces(nm_group* g, const double* xyz, size_t nv, const uint32_t* tri, size_t nt,
+                          const uint32_t* comp_tri_off, int K, const int* label_ids);
+int nm_group_label_mesh(nm_group* g, const double* nodes, size_t n_nodes, const uint32_t* tets, size_t nt,
+                        double threshold, int* labels_out, uint32_t* masks_out /* nullable */, nm_stats* stats);
+
 /* ---- device-resident entry points (asynchronous on `stream`) -------------- */
 int nm_label_nodes_device(nm_ctx* ctx, const double* d_pts, size_t n, double threshold, uint32_t* d_masks,
                           double* d_s_out /* nullable, n*K */, void* stream, nm_stats* stats);

@@ -116,6 +116,14 @@ LABEL_API = {
                                                  ctypes.POINTER(NmStats)]),
     "nm_sample_surface": (ctypes.c_int, [c_double_p, c_u32_p, ctypes.c_size_t, ctypes.c_size_t, ctypes.c_uint64,
                                          c_double_p]),
+    "nm_group_create": (ctypes.c_int, [ctypes.POINTER(ctypes.c_void_p), ctypes.c_int, c_i32_p,
+                                       ctypes.POINTER(NmOptions)]),
+    "nm_group_destroy": (ctypes.c_int, [ctypes.c_void_p]),
+    "nm_group_size": (ctypes.c_int, [ctypes.c_void_p]),
+    "nm_group_set_surfaces": (ctypes.c_int, [ctypes.c_void_p, c_double_p, ctypes.c_size_t, c_u32_p, ctypes.c_size_t,
+                                             c_u32_p, ctypes.c_int, c_i32_p]),
+    "nm_group_label_mesh": (ctypes.c_int, [ctypes.c_void_p, c_double_p, ctypes.c_size_t, c_u32_p, ctypes.c_size_t,
+                                           ctypes.c_double, c_i32_p, c_u32_p, ctypes.POINTER(NmStats)]),
     "nm_surface_info": (ctypes.c_int, [ctypes.c_void_p, c_i32_p, c_size_p, c_size_p, c_i32_p]),
 }
 
@@ -373,6 +381,48 @@ class Context:
     def flag_boundary_device(self, d_tets, d_masks, d_ids, d_count, active_mask=0xFFFFFFFF, stream=None):
         check(self.lib.nm_flag_boundary_device(self.handle, d_tets.data_ptr(), d_tets.shape[0], d_masks.data_ptr(),
                                                active_mask, d_ids.data_ptr(), d_count.data_ptr(), stream))
+
+
+class Group:
+    """Single-process multi-GPU group (nm_group): devices may repeat."""
+
+    def __init__(self, devices, **options):
+        self.lib = load_label_lib()
+        devs = np.ascontiguousarray(devices, dtype=np.int32)
+        opt = default_options(**options)
+        h = ctypes.c_void_p()
+        check(self.lib.nm_group_create(ctypes.byref(h), devs.size, ptr(devs, ctypes.c_int), ctypes.byref(opt)))
+        self.handle = h
+
+    def close(self):
+        if getattr(self, "handle", None):
+            self.lib.nm_group_destroy(self.handle)
+            self.handle = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def set_surfaces(self, xyz, tri, comp_off, label_ids):
+        xyz = np.ascontiguousarray(xyz, dtype=np.float64).reshape(-1, 3)
+        tri = np.ascontiguousarray(tri, dtype=np.uint32).reshape(-1, 3)
+        comp_off = np.ascontiguousarray(comp_off, dtype=np.uint32)
+        label_ids = np.ascontiguousarray(label_ids, dtype=np.int32)
+        check(self.lib.nm_group_set_surfaces(self.handle, ptr(xyz, ctypes.c_double), xyz.shape[0],
+                                             ptr(tri, ctypes.c_uint32), tri.shape[0], ptr(comp_off, ctypes.c_uint32),
+                                             len(label_ids), ptr(label_ids, ctypes.c_int)))
+
+    def label_mesh(self, nodes, tets, threshold=0.5):
+        nodes = np.ascontiguousarray(nodes, dtype=np.float64).reshape(-1, 3)
+        tets = np.ascontiguousarray(tets, dtype=np.uint32).reshape(-1, 4)
+        labels = np.empty(tets.shape[0], np.int32)
+        masks = np.empty(nodes.shape[0], np.uint32)
+        check(self.lib.nm_group_label_mesh(self.handle, ptr(nodes, ctypes.c_double), nodes.shape[0],
+                                           ptr(tets, ctypes.c_uint32), tets.shape[0], threshold,
+                                           ptr(labels, ctypes.c_int), ptr(masks, ctypes.c_uint32), None))
+        return labels, masks
 
 
 def refine(nodes, tets, labels, selected):

@@ -1,1 +1,1 @@
-python -m pytest tests -q -m gpu 2>&1 | tail -2
+python -m pytest tests/test_gpu_dropin.py -q -m gpu -k cpp 2>&1 | tail -3

@@ -26,6 +26,13 @@ int main(int argc, char** argv) {
   SolidAngleParams params;
   nm_stats st{};
   const std::vector<int> labels = initial_label(mesh, seg, params, GpuOptions{}, &st);
+  // multi-device sharding (two contexts on device 0) is bit-identical
+  GpuOptions multi;
+  multi.devices = {0, 0};
+  if (initial_label(mesh, seg, params, multi) != labels) {
+    std::fprintf(stderr, "group labels differ\n");
+    return 6;
+  }
   // enclosure_ratio KATs
   const double s_in = enclosure_ratio(Vec3{0, 0, 0}, seg.compartments[0].mesh);
   const double s_out = enclosure_ratio(Vec3{30, 0, 0}, seg.compartments[0].mesh);

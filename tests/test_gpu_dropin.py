@@ -93,3 +93,22 @@ def test_two_ranks_sharded_gpu_equals_single(tmp_path):
         c.set_surfaces(S.xyz, S.tri, S.comp_off, S.label_ids)
         ref, _, _ = c.label_mesh(nodes, tets)
     np.testing.assert_array_equal(np.load(tmp_path / "labels.npy"), ref)
+
+
+@pytest.mark.parametrize("devices", [[0], [0, 0], [0, 0, 0]])
+def test_group_multi_context_bitwise(devices):
+    """nm_group (single-process multi-device API for C/C++ hosts): with 1, 2
+    and 3 contexts (on the one GPU available) the labels and masks are
+    bit-identical to a single context (acceptance #8)."""
+    from paper_2203_10000_b200._native import Context, Group
+    cfg = synth.config(2)
+    S = cfg.surfaces
+    nodes, tets = cfg.lattice_mesh()
+    with Context(0) as c:
+        c.set_surfaces(S.xyz, S.tri, S.comp_off, S.label_ids)
+        ref, mref, _ = c.label_mesh(nodes, tets, want_masks=True)
+    with Group(devices) as g:
+        g.set_surfaces(S.xyz, S.tri, S.comp_off, S.label_ids)
+        lab, m = g.label_mesh(nodes, tets)
+    np.testing.assert_array_equal(lab, ref)
+    np.testing.assert_array_equal(m, mref)
