@@ -207,7 +207,7 @@ def run_recursive(args):
     line = {
         "metric": METRIC, "value": evals / (dev_ms / 1e3), "unit": UNIT, "n_gpus": 1, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": dev_ms, "higher_is_better": True, "scaling": "strong",
-        "vs_baseline": None, "dtype": "fp32 (fp64 tile fold + fp64 fix-up)", "data": "synthetic",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": f"cfg4: cfg3 + {args.levels} levels of straddle-tet refinement, new nodes only",
                    "initial_nodes": int(nodes.shape[0]), "initial_tets": int(tets.shape[0]),
                    "refined_nodes": int(n2.shape[0]), "refined_tets": int(t2.shape[0]),
@@ -426,7 +426,8 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "fp32 (fp64 tile fold + fp64 fix-up)", "data": "synthetic",
+            "vs_baseline": None, "dtype": "f32", "dtype_note": "f32 arithmetic, f64 per-tile fold and f64 fix-up of flagged pairs",
+            "data": "synthetic",
             "config": dict(workload_config(cfg, n, nt, world), distributed=use_dist),
             "full_mesh_labeling_time_s": ms_per_step / 1e3,
             "e2e": e2e, "roofline": roof, "cpu_baseline": cpu, "clocks": clocks,
