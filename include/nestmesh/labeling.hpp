@@ -248,6 +248,44 @@ inline RelabelResult relabel_recursive(const TetrahedralMesh& mesh, const Surfac
   return r;
 }
 
+namespace detail {
+inline TetrahedralMesh to_mesh(nm_mesh* m) {
+  std::unique_ptr<nm_mesh, void (*)(nm_mesh*)> guard(m, nm_mesh_free);
+  std::size_t nn = 0, nt = 0, nold = 0;
+  check(nm_mesh_sizes(m, &nn, &nt, &nold));
+  TetrahedralMesh out;
+  out.nodes.resize(nn);
+  out.tetrahedra.resize(nt);
+  out.labels.resize(nt);
+  check(nm_mesh_copy(m, reinterpret_cast<double*>(out.nodes.data()), reinterpret_cast<std::uint32_t*>(out.tetrahedra.data()),
+                     out.labels.data(), nullptr));
+  return out;
+}
+}  // namespace detail
+
+/// refine_volume: 1:8 split of the selected tets plus
+/// conforming transition templates; children inherit labels. Host code.
+inline TetrahedralMesh refine_volume(const TetrahedralMesh& mesh, const std::vector<std::uint32_t>& element_set) {
+  nm_mesh* m = nullptr;
+  if (nm_refine(detail::xyz_of(mesh.nodes), mesh.node_count(), detail::idx_of(mesh.tetrahedra), mesh.tet_count(),
+                mesh.labels.size() == mesh.tet_count() ? mesh.labels.data() : nullptr, element_set.data(),
+                element_set.size(), &m) != 0)
+    throw LabelingError(nm_refine_last_error());
+  return detail::to_mesh(m);
+}
+
+/// refine_boundary on the device: refine the layers on both
+/// sides of the label_a | label_b interface (mesh.labels).
+inline TetrahedralMesh refine_boundary(const TetrahedralMesh& mesh, int label_a, int label_b, const GpuOptions& o = {}) {
+  if (mesh.labels.size() != mesh.tet_count()) throw LabelingError("labels length != tet count");
+  detail::Context ctx(o);
+  nm_mesh* m = nullptr;
+  detail::check(nm_refine_boundary(ctx.get(), detail::xyz_of(mesh.nodes), mesh.node_count(),
+                                   detail::idx_of(mesh.tetrahedra), mesh.tet_count(), mesh.labels.data(), label_a,
+                                   label_b, &m));
+  return detail::to_mesh(m);
+}
+
 /// Tets straddling an active compartment boundary (node masks disagree).
 inline std::vector<std::uint32_t> boundary_tets(const TetrahedralMesh& mesh, const std::vector<std::uint32_t>& masks,
                                                 std::uint32_t active_mask, const SurfaceSegmentation& seg,

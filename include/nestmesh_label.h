@@ -179,6 +179,13 @@ void nm_mesh_free(nm_mesh* m);
 const char* nm_refine_last_error(void);
 int nm_mesh_masks(const nm_mesh* m, uint32_t* masks);
 
+/* refine_boundary on the device: the tets labeled a or b
+ * that share a face with a tet of the other label are refined with
+ * refine_volume (same rules/numbering as nm_refine; children inherit labels).
+ * A pair with no shared face returns the input mesh unchanged. */
+int nm_refine_boundary(nm_ctx* ctx, const double* nodes, size_t n_nodes, const uint32_t* tets, size_t nt,
+                       const int* labels, int label_a, int label_b, nm_mesh** out);
+
 /* The recursive boundary driver: `levels`
  * times { flag the tets whose node masks straddle an active compartment
  * (device compaction), refine them on the device (same rules, numbering and

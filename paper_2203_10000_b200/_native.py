@@ -103,6 +103,8 @@ LABEL_API = {
     "nm_mesh_free": (None, [ctypes.c_void_p]),
     "nm_refine_last_error": (ctypes.c_char_p, []),
     "nm_mesh_masks": (ctypes.c_int, [ctypes.c_void_p, c_u32_p]),
+    "nm_refine_boundary": (ctypes.c_int, [ctypes.c_void_p, c_double_p, ctypes.c_size_t, c_u32_p, ctypes.c_size_t,
+                                          c_i32_p, ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_void_p)]),
     "nm_refine_relabel": (ctypes.c_int, [ctypes.c_void_p, c_double_p, ctypes.c_size_t, c_u32_p, ctypes.c_size_t,
                                          c_u32_p, ctypes.c_double, ctypes.c_uint32, ctypes.c_int,
                                          ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(NmStats)]),
@@ -337,6 +339,28 @@ class Context:
                                   ptr(labels, ctypes.c_int), ctypes.byref(passes), ctypes.byref(conv),
                                   ptr(ev, ctypes.c_uint8) if ev is not None else None, ctypes.byref(st)))
         return labels, passes.value, bool(conv.value), ev, st.as_dict()
+
+    def refine_boundary(self, nodes, tets, labels, label_a, label_b):
+        """refine_boundary on the device: (nodes, tets, labels, parent, n_old)."""
+        nodes = np.ascontiguousarray(nodes, dtype=np.float64).reshape(-1, 3)
+        tets = np.ascontiguousarray(tets, dtype=np.uint32).reshape(-1, 4)
+        labels = np.ascontiguousarray(labels, dtype=np.int32)
+        h = ctypes.c_void_p()
+        check(self.lib.nm_refine_boundary(self.handle, ptr(nodes, ctypes.c_double), nodes.shape[0],
+                                          ptr(tets, ctypes.c_uint32), tets.shape[0], ptr(labels, ctypes.c_int),
+                                          label_a, label_b, ctypes.byref(h)))
+        try:
+            nn, ntt, nold = ctypes.c_size_t(), ctypes.c_size_t(), ctypes.c_size_t()
+            self.lib.nm_mesh_sizes(h, ctypes.byref(nn), ctypes.byref(ntt), ctypes.byref(nold))
+            on = np.empty((nn.value, 3), np.float64)
+            ot = np.empty((ntt.value, 4), np.uint32)
+            ol = np.empty(ntt.value, np.int32)
+            op = np.empty(ntt.value, np.uint32)
+            self.lib.nm_mesh_copy(h, ptr(on, ctypes.c_double), ptr(ot, ctypes.c_uint32), ptr(ol, ctypes.c_int),
+                                  ptr(op, ctypes.c_uint32))
+        finally:
+            self.lib.nm_mesh_free(h)
+        return on, ot, ol, op, nold.value
 
     def refine_relabel(self, nodes, tets, masks=None, levels=2, active_mask=0xFFFFFFFF, threshold=0.5):
         """Recursive boundary driver: returns (nodes, tets, labels, masks, stats)."""

@@ -746,3 +746,27 @@ __global__ void k_lattice_tets(const double* nodes, int nx, int ny, int nz, uint
 }
 
 }  // namespace nm
+
+namespace nm {
+
+// refine_boundary selection: tets labeled a or b that share
+// a face with a tet of the other label (the one-element-thick layers on both
+// sides of the a|b interface).
+struct PredInterface {
+  const std::int32_t* nbr;
+  const int* labels;
+  int a, b;
+  __device__ bool operator()(std::size_t t) const {
+    const int l = labels[t];
+    if (l != a && l != b) return false;
+    const int other = l == a ? b : a;
+#pragma unroll
+    for (int f = 0; f < 4; ++f) {
+      const std::int32_t o = nbr[4 * t + f];
+      if (o >= 0 && labels[o] == other) return true;
+    }
+    return false;
+  }
+};
+
+}  // namespace nm

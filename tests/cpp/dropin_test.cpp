@@ -62,6 +62,20 @@ int main(int argc, char** argv) {
     return 5;
   } catch (const LabelingError&) {
   }
+  // refine_boundary around the inner|outer interface, then relabel: the
+  // recursion premise — relabel == initial labeling of the refined mesh
+  TetrahedralMesh lab_mesh = mesh;
+  lab_mesh.labels = labels;
+  const TetrahedralMesh refined = refine_boundary(lab_mesh, 3, 9);
+  if (refined.tet_count() <= mesh.tet_count() || !validate_mesh(refined).ok()) {
+    std::fprintf(stderr, "refine_boundary failed\n");
+    return 7;
+  }
+  const RelabelResult rr = relabel_recursive(refined, seg, params, refined.labels);
+  if (rr.labels != initial_label(refined, seg, params)) {
+    std::fprintf(stderr, "relabel != initial on the refined mesh\n");
+    return 8;
+  }
   FILE* f = std::fopen(out_path, "wb");
   std::fwrite(labels.data(), sizeof(int), labels.size(), f);
   std::fclose(f);

@@ -408,3 +408,42 @@ def test_poorly_stripifiable_surface(layout):
     assert np.max(np.abs(s - s_ref)) <= S_EXPECT
     bad, _ = _compare_masks(m, m_ref, s_ref)
     assert bad == 0
+
+
+def _interface_tets(tets, labels, a, b):
+    """Host restatement of the refine_boundary selection."""
+    F = np.array([[1, 2, 3], [0, 3, 2], [0, 1, 3], [0, 2, 1]])
+    f = np.sort(tets[:, F].reshape(-1, 3).astype(np.int64), axis=1)
+    key = (f[:, 0] << 42) | (f[:, 1] << 21) | f[:, 2]
+    order = np.argsort(key, kind="stable")
+    k = key[order]
+    same = np.flatnonzero(k[1:] == k[:-1])
+    t1, t2 = order[same] // 4, order[same + 1] // 4
+    sel = np.zeros(tets.shape[0], bool)
+    for x, y in ((t1, t2), (t2, t1)):
+        m = ((labels[x] == a) & (labels[y] == b)) | ((labels[x] == b) & (labels[y] == a))
+        sel[x[m]] = True
+    return np.flatnonzero(sel)
+
+
+def test_refine_boundary_device(ctx):
+    """interface layers of a pair refined on both sides; a
+    pair without a shared face leaves the mesh unchanged; bit-identical to
+    host nm_refine on the same selection."""
+    from paper_2203_10000_b200._native import refine
+    nodes, tets = synth.lattice_mesh((0.0, 0.0, 0.0), 1.0, (6, 6, 6))
+    cen = (nodes[tets].mean(axis=1))
+    labels = np.where(cen[:, 0] < 3.0, 1, 2).astype(np.int32)      # half-and-half cube
+    labels[(cen[:, 0] > 5.5)] = 3
+    n2, t2, l2, par, n_old = ctx.refine_boundary(nodes, tets, labels, 1, 2)
+    sel = _interface_tets(tets, labels, 1, 2)
+    assert sel.size > 0 and np.all(np.isin(labels[sel], [1, 2]))
+    hn, ht, hl, hp, _ = refine(nodes, tets, labels, sel)
+    np.testing.assert_array_equal(n2, hn)
+    np.testing.assert_array_equal(t2, ht)
+    np.testing.assert_array_equal(l2, hl)
+    np.testing.assert_array_equal(par, hp)
+    # 1 and 3 share no face -> identical mesh
+    m2, u2, k2, _, _ = ctx.refine_boundary(nodes, tets, labels, 1, 3)
+    np.testing.assert_array_equal(m2, nodes)
+    np.testing.assert_array_equal(u2, tets)
