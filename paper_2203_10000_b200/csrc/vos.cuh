@@ -181,6 +181,9 @@ __device__ __forceinline__ float acc_near_lane(float acc, float a_far, float num
 // distance test, never on its warp mates (mixed warps run both and select per
 // lane), so results are independent of sharding and point order.
 // ---------------------------------------------------------------------------
+#ifndef NM_PAIR_COMPLEX
+#define NM_PAIR_COMPLEX 1
+#endif
 constexpr int kSegTris = 8;
 constexpr int kSegF4 = 23;
 constexpr int kSegT = 10;  // first T_k
@@ -266,6 +269,7 @@ __device__ __forceinline__ void seg_far(const float4* __restrict__ rec, const Pa
       const float2 dac = fma2(add2(a[q].q, c.q), bc(0.5f), bc(eac));
       const float2 num = fma2(bc(T.x), f[q].mx, fma2(bc(T.y), f[q].my, fma2(bc(T.z), f[q].mz, bc(T.w))));
       const float2 den = fma2(fma2(a[q].r, b[q].r, dab[q]), c.r, fma2(dac, b[q].r, mul2(dbc, a[q].r)));
+#if NM_PAIR_COMPLEX
       if (k & 1) {
         const float2 D = fma2(d0[q], den, mul2(make_float2(-n0[q].x, -n0[q].y), num));
         const float2 N = fma2(n0[q], den, mul2(num, d0[q]));
@@ -274,6 +278,9 @@ __device__ __forceinline__ void seg_far(const float4* __restrict__ rec, const Pa
         n0[q] = num;
         d0[q] = den;
       }
+#else
+      acc[q] = atan_far2(acc[q], num, den);
+#endif
       a[q] = b[q];
       b[q] = c;
       dab[q] = dbc;
