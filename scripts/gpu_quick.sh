@@ -1,3 +1,1 @@
-python scripts/quick_time.py 5:2000000 3:2000000
-NM_LABEL_LIB=probes/libnl_nopair.so python scripts/quick_time.py 5:2000000 3:2000000
-python scripts/quick_time.py 5:2000000 3:2000000
+python -m pytest tests/test_gpu_dropin.py -q -m gpu -k validation 2>&1 | tail -8

@@ -112,3 +112,28 @@ def test_group_multi_context_bitwise(devices):
         lab, m = g.label_mesh(nodes, tets)
     np.testing.assert_array_equal(lab, ref)
     np.testing.assert_array_equal(m, mref)
+
+
+def test_abi_input_validation():
+    """The C ABI rejects malformed inputs with a message instead of faulting."""
+    from paper_2203_10000_b200._native import Context, NativeError
+    xyz, tri = synth.icosphere(5.0, 1)
+    with Context(0) as c:
+        with pytest.raises(NativeError, match="nm_set_surfaces has not been called"):
+            c.label_nodes(np.zeros((4, 3)))
+        with pytest.raises(NativeError, match="out of range"):
+            c.set_surfaces(xyz, tri + 1000, np.array([0, tri.shape[0]], np.uint32), np.array([1], np.int32))
+        with pytest.raises(NativeError, match="comp_tri_off"):
+            c.set_surfaces(xyz, tri, np.array([0, 3], np.uint32), np.array([1], np.int32))
+        with pytest.raises(NativeError, match="label ids must be > 0"):
+            c.set_surfaces(xyz, tri, np.array([0, tri.shape[0]], np.uint32), np.array([0], np.int32))
+        c.set_surfaces(xyz, tri, np.array([0, tri.shape[0]], np.uint32), np.array([1], np.int32))
+        with pytest.raises(NativeError, match="threshold"):
+            c.label_nodes(np.zeros((4, 3)), threshold=1.0)
+        with pytest.raises(NativeError, match="references node"):
+            c.label_mesh(np.zeros((4, 3)), np.array([[0, 1, 2, 9]], np.uint32))
+        with pytest.raises(NativeError, match="references node"):
+            c.refine_boundary(np.zeros((4, 3)), np.array([[0, 1, 2, 7]], np.uint32), np.array([1], np.int32), 1, 2)
+        # still usable after errors
+        m, _ = c.label_nodes(np.zeros((1, 3)))
+        assert m[0] == 1
