@@ -179,6 +179,11 @@ void nm_mesh_free(nm_mesh* m);
 const char* nm_refine_last_error(void);
 int nm_mesh_masks(const nm_mesh* m, uint32_t* masks);
 
+/* refine_volume on the device for a given selection: same rules, numbering
+ * and child order as nm_refine (bit-identical result). */
+int nm_refine_device(nm_ctx* ctx, const double* nodes, size_t n_nodes, const uint32_t* tets, size_t nt,
+                     const int* labels /* nullable */, const uint32_t* selected, size_t n_selected, nm_mesh** out);
+
 /* refine_boundary on the device: the tets labeled a or b
  * that share a face with a tet of the other label are refined with
  * refine_volume (same rules/numbering as nm_refine; children inherit labels).

@@ -103,6 +103,8 @@ LABEL_API = {
     "nm_mesh_free": (None, [ctypes.c_void_p]),
     "nm_refine_last_error": (ctypes.c_char_p, []),
     "nm_mesh_masks": (ctypes.c_int, [ctypes.c_void_p, c_u32_p]),
+    "nm_refine_device": (ctypes.c_int, [ctypes.c_void_p, c_double_p, ctypes.c_size_t, c_u32_p, ctypes.c_size_t,
+                                        c_i32_p, c_u32_p, ctypes.c_size_t, ctypes.POINTER(ctypes.c_void_p)]),
     "nm_refine_boundary": (ctypes.c_int, [ctypes.c_void_p, c_double_p, ctypes.c_size_t, c_u32_p, ctypes.c_size_t,
                                           c_i32_p, ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_void_p)]),
     "nm_refine_relabel": (ctypes.c_int, [ctypes.c_void_p, c_double_p, ctypes.c_size_t, c_u32_p, ctypes.c_size_t,
@@ -340,6 +342,19 @@ class Context:
                                   ptr(ev, ctypes.c_uint8) if ev is not None else None, ctypes.byref(st)))
         return labels, passes.value, bool(conv.value), ev, st.as_dict()
 
+    def refine_device(self, nodes, tets, labels, selected):
+        """refine_volume on the device: (nodes, tets, labels, parent, n_old)."""
+        nodes = np.ascontiguousarray(nodes, dtype=np.float64).reshape(-1, 3)
+        tets = np.ascontiguousarray(tets, dtype=np.uint32).reshape(-1, 4)
+        lab = np.ascontiguousarray(labels, dtype=np.int32) if labels is not None else None
+        sel = np.ascontiguousarray(selected, dtype=np.uint32)
+        h = ctypes.c_void_p()
+        check(self.lib.nm_refine_device(self.handle, ptr(nodes, ctypes.c_double), nodes.shape[0],
+                                        ptr(tets, ctypes.c_uint32), tets.shape[0],
+                                        ptr(lab, ctypes.c_int) if lab is not None else None,
+                                        ptr(sel, ctypes.c_uint32), sel.size, ctypes.byref(h)))
+        return _take_mesh(self.lib, h)
+
     def refine_boundary(self, nodes, tets, labels, label_a, label_b):
         """refine_boundary on the device: (nodes, tets, labels, parent, n_old)."""
         nodes = np.ascontiguousarray(nodes, dtype=np.float64).reshape(-1, 3)
@@ -405,6 +420,21 @@ class Context:
     def flag_boundary_device(self, d_tets, d_masks, d_ids, d_count, active_mask=0xFFFFFFFF, stream=None):
         check(self.lib.nm_flag_boundary_device(self.handle, d_tets.data_ptr(), d_tets.shape[0], d_masks.data_ptr(),
                                                active_mask, d_ids.data_ptr(), d_count.data_ptr(), stream))
+
+
+def _take_mesh(lib, h):
+    try:
+        nn, ntt, nold = ctypes.c_size_t(), ctypes.c_size_t(), ctypes.c_size_t()
+        lib.nm_mesh_sizes(h, ctypes.byref(nn), ctypes.byref(ntt), ctypes.byref(nold))
+        on = np.empty((nn.value, 3), np.float64)
+        ot = np.empty((ntt.value, 4), np.uint32)
+        ol = np.empty(ntt.value, np.int32)
+        op = np.empty(ntt.value, np.uint32)
+        lib.nm_mesh_copy(h, ptr(on, ctypes.c_double), ptr(ot, ctypes.c_uint32), ptr(ol, ctypes.c_int),
+                         ptr(op, ctypes.c_uint32))
+    finally:
+        lib.nm_mesh_free(h)
+    return on, ot, ol, op, nold.value
 
 
 class Group:

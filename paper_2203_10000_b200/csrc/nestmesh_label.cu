@@ -1423,6 +1423,47 @@ int nm_relabel(nm_ctx* c, const double* nodes, std::size_t n, const std::uint32_
   });
 }
 
+int nm_refine_device(nm_ctx* c, const double* nodes, std::size_t n, const std::uint32_t* tets, std::size_t nt,
+                     const int* labels, const std::uint32_t* selected, std::size_t ns, nm_mesh** out) {
+  return guarded([&] {
+    if (!c) throw Error("null context");
+    if (!out) throw Error("null output pointer");
+    *out = nullptr;
+    check_tets(tets, nt, n);
+    for (std::size_t i = 0; i < ns; ++i)
+      if (selected[i] >= nt) throw Error("InvalidSelection: selected tet id out of range (SPEC.md:292)");
+    NM_CUDA(cudaSetDevice(c->opt.device));
+    cudaStream_t st = c->stream;
+    auto* d_nodes = c->meshA_nodes.as<double>(3 * std::max<std::size_t>(n, 1));
+    auto* d_tets = c->meshA_tets.as<std::uint32_t>(4 * std::max<std::size_t>(nt, 1));
+    auto* d_labels = c->meshA_labels.as<int>(std::max<std::size_t>(nt, 1));
+    auto* d_sel = c->list.as<std::uint32_t>(std::max<std::size_t>(ns, 1));
+    if (n) NM_CUDA(cudaMemcpyAsync(d_nodes, nodes, 3 * n * sizeof(double), cudaMemcpyHostToDevice, st));
+    if (nt) NM_CUDA(cudaMemcpyAsync(d_tets, tets, 4 * nt * sizeof(std::uint32_t), cudaMemcpyHostToDevice, st));
+    if (nt) {
+      if (labels) NM_CUDA(cudaMemcpyAsync(d_labels, labels, nt * sizeof(int), cudaMemcpyHostToDevice, st));
+      else NM_CUDA(cudaMemsetAsync(d_labels, 0, nt * sizeof(int), st));
+    }
+    if (ns) NM_CUDA(cudaMemcpyAsync(d_sel, selected, ns * sizeof(std::uint32_t), cudaMemcpyHostToDevice, st));
+    std::uint64_t l = 0;
+    const auto [n2, nt2] = refine_dev(c, d_nodes, n, d_tets, nt, d_labels, d_sel, static_cast<std::uint32_t>(ns), st, l);
+    std::unique_ptr<nm_mesh> res(new nm_mesh);
+    res->n_old = n;
+    res->nodes.resize(3 * n2);
+    res->tets.resize(4 * nt2);
+    res->labels.resize(nt2);
+    res->parent.resize(nt2);
+    if (n2) NM_CUDA(cudaMemcpyAsync(res->nodes.data(), c->meshB_nodes.p, 3 * n2 * sizeof(double), cudaMemcpyDeviceToHost, st));
+    if (nt2) {
+      NM_CUDA(cudaMemcpyAsync(res->tets.data(), c->meshB_tets.p, 4 * nt2 * sizeof(std::uint32_t), cudaMemcpyDeviceToHost, st));
+      NM_CUDA(cudaMemcpyAsync(res->labels.data(), c->meshB_labels.p, nt2 * sizeof(int), cudaMemcpyDeviceToHost, st));
+      NM_CUDA(cudaMemcpyAsync(res->parent.data(), c->meshB_parent.p, nt2 * sizeof(std::uint32_t), cudaMemcpyDeviceToHost, st));
+    }
+    NM_CUDA(cudaStreamSynchronize(st));
+    *out = res.release();
+  });
+}
+
 int nm_refine_boundary(nm_ctx* c, const double* nodes, std::size_t n, const std::uint32_t* tets, std::size_t nt,
                        const int* labels, int label_a, int label_b, nm_mesh** out) {
   return guarded([&] {

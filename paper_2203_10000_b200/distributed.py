@@ -88,3 +88,60 @@ def label_mesh_sharded(nodes, tets, node_fn, tet_fn, rank: int, world: int, grou
 def gather_labels(labels: "torch.Tensor", sh: Shard, group=None) -> "torch.Tensor":
     """All-gather per-rank tet label ranges into the full (T,) label vector."""
     return all_gather_masks(labels, sh, group)
+
+
+def all_gather_varlen(local: "torch.Tensor", group=None) -> "torch.Tensor":
+    """All-gather of variable-length 1-D tensors (rank order preserved):
+    counts first, then equal padded buffers."""
+    import torch
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()):
+        return local.clone()
+    world = dist.get_world_size(group)
+    cnt = torch.tensor([local.shape[0]], dtype=torch.int64, device=local.device)
+    cnts = torch.empty(world, dtype=torch.int64, device=local.device)
+    dist.all_gather_into_tensor(cnts, cnt, group=group)
+    cl = [int(c) for c in cnts.tolist()]
+    mx = max(cl) if cl else 0
+    buf = torch.zeros(max(mx, 1), dtype=local.dtype, device=local.device)
+    buf[: local.shape[0]] = local
+    out = torch.empty(world * max(mx, 1), dtype=local.dtype, device=local.device)
+    dist.all_gather_into_tensor(out, buf, group=group)
+    parts = [out[r * max(mx, 1): r * max(mx, 1) + cl[r]] for r in range(world)]
+    return torch.cat(parts) if parts else local[:0]
+
+
+def refine_relabel_sharded(nodes, tets, masks, levels, node_fn, flag_fn, refine_fn, tet_fn, rank: int, world: int,
+                           group=None, device="cpu"):
+    """The recursive boundary driver over `world` ranks (PAPER.md:151,
+    SPEC.md:294-297): per level, every rank flags the straddling tets of its
+    tet range, the flag lists are all-gathered (refinement flags over NCCL on
+    the GPU box), every rank refines the same mesh with the same selection
+    (deterministic numbering -> identical meshes), evaluates only ITS shard of
+    the new nodes and the new masks are all-gathered. Returns (nodes, tets,
+    labels of this rank's tet range, tet shard, masks).
+
+    node_fn(points (m,3) f64 torch) -> masks (m,) int32 torch
+    flag_fn(tets (t,4) torch, masks (N,) torch) -> ascending local ids (int32 torch)
+    refine_fn(nodes, tets, selected) -> (nodes2, tets2, n_old)   (host numpy)
+    tet_fn(tets (t,4) torch, masks (N,) torch) -> labels (t,) int32 torch
+    """
+    import torch
+    masks = masks.to(device)
+    for _ in range(levels):
+        tsh = shard(tets.shape[0], world, rank)
+        t_local = torch.as_tensor(np.ascontiguousarray(tets[tsh.lo:tsh.hi]).view(np.int32), device=device)
+        ids = flag_fn(t_local, masks).to(torch.int64) + tsh.lo
+        sel = all_gather_varlen(ids, group).cpu().numpy().astype(np.uint32)
+        nodes2, tets2, n_old = refine_fn(nodes, tets, sel)
+        new = nodes2[n_old:]
+        nsh = shard(new.shape[0], world, rank)
+        m_local = node_fn(torch.as_tensor(np.ascontiguousarray(new[nsh.lo:nsh.hi]), dtype=torch.float64,
+                                          device=device))
+        m_new = all_gather_masks(m_local, nsh, group)
+        masks = torch.cat([masks, m_new])
+        nodes, tets = nodes2, tets2
+    tsh = shard(tets.shape[0], world, rank)
+    t_local = torch.as_tensor(np.ascontiguousarray(tets[tsh.lo:tsh.hi]).view(np.int32), device=device)
+    labels = tet_fn(t_local, masks)
+    return nodes, tets, labels, tsh, masks

@@ -70,3 +70,61 @@ def test_sharded_labels_equal_single_process(tmp_path, world):
     ref = oracle.label_tets(tets, m, cfg.surfaces.label_ids)
     np.testing.assert_array_equal(np.load(tmp_path / f"masks_{world}.npy").view(np.uint32), m)
     np.testing.assert_array_equal(np.load(tmp_path / f"labels_{world}.npy"), ref)
+
+
+def _worker_recursive(rank, world, port, out_dir):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2203_10000_b200._native import refine
+        from paper_2203_10000_b200.distributed import refine_relabel_sharded
+        R = 10.0
+        S = synth.concat_surfaces([synth.icosphere(0.6 * R, 2), synth.icosphere(R, 2)], labels=[1, 2])
+        nodes, tets = synth.lattice_mesh((-1.3 * R,) * 3, R / 4, (11, 11, 11))
+        m0 = torch.from_numpy(oracle.label_nodes(nodes, S).view(np.int32))
+
+        def node_fn(pts):
+            return torch.from_numpy(oracle.label_nodes(pts.numpy(), S, workers=1).view(np.int32))
+
+        def flag_fn(t, masks):
+            return torch.from_numpy(oracle.flag_boundary(t.numpy().view(np.uint32), masks.numpy().view(np.uint32))
+                                    .astype(np.int32))
+
+        def refine_fn(nd, tt, sel):
+            n2, t2, _, _, n_old = refine(nd, tt, None, sel)
+            return n2, t2, n_old
+
+        def tet_fn(t, masks):
+            return torch.from_numpy(oracle.label_tets(t.numpy().view(np.uint32), masks.numpy().view(np.uint32),
+                                                      S.label_ids))
+
+        n2, t2, labels, tsh, masks = refine_relabel_sharded(nodes, tets, m0, 2, node_fn, flag_fn, refine_fn, tet_fn,
+                                                            rank, world)
+        from paper_2203_10000_b200.distributed import gather_labels
+        full = gather_labels(labels, tsh)
+        if rank == 0:
+            np.save(os.path.join(out_dir, "rec_labels.npy"), full.numpy())
+            np.save(os.path.join(out_dir, "rec_nodes.npy"), n2)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_recursive_driver(tmp_path, world):
+    """Refinement flags and new-node masks gathered across ranks: the sharded
+    recursive driver equals the single-process driver (and the initial
+    labeling of the refined mesh)."""
+    mp.spawn(_worker_recursive, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    from paper_2203_10000_b200._native import refine
+    R = 10.0
+    S = synth.concat_surfaces([synth.icosphere(0.6 * R, 2), synth.icosphere(R, 2)], labels=[1, 2])
+    nodes, tets = synth.lattice_mesh((-1.3 * R,) * 3, R / 4, (11, 11, 11))
+    m = oracle.label_nodes(nodes, S)
+    for _ in range(2):
+        n2, t2, _, _, n_old = refine(nodes, tets, None, oracle.flag_boundary(tets, m))
+        m = np.concatenate([m, oracle.label_nodes(n2[n_old:], S)])
+        nodes, tets = n2, t2
+    ref = oracle.label_tets(tets, m, S.label_ids)
+    np.testing.assert_array_equal(np.load(tmp_path / "rec_nodes.npy"), nodes)
+    np.testing.assert_array_equal(np.load(tmp_path / "rec_labels.npy"), ref)
+    np.testing.assert_array_equal(ref, oracle.label_tets(tets, oracle.label_nodes(nodes, S), S.label_ids))

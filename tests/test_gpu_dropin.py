@@ -137,3 +137,66 @@ def test_abi_input_validation():
         # still usable after errors
         m, _ = c.label_nodes(np.zeros((1, 3)))
         assert m[0] == 1
+
+
+def _gpu_rank_recursive(rank, world, port, out_dir):
+    import torch
+    import torch.distributed as dist
+    from paper_2203_10000_b200._native import Context
+    from paper_2203_10000_b200.distributed import gather_labels, refine_relabel_sharded
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        cfg = synth.config(2)
+        S = cfg.surfaces
+        nodes, tets = synth.lattice_mesh((-110.0, -110.0, -110.0), 5.0, (44, 44, 44))
+        ctx = Context(0)
+        ctx.set_surfaces(S.xyz, S.tri, S.comp_off, S.label_ids)
+        m0, _ = ctx.label_nodes(nodes)
+
+        def node_fn(pts):
+            m, _ = ctx.label_nodes(pts.numpy())
+            return torch.from_numpy(m.view(np.int32))
+
+        def flag_fn(t, masks):
+            return torch.from_numpy(ctx.flag_boundary(t.numpy().view(np.uint32), masks.numpy().view(np.uint32))
+                                    .astype(np.int32))
+
+        def refine_fn(nd, tt, sel):
+            n2, t2, _, _, n_old = ctx.refine_device(nd, tt, None, sel)
+            return n2, t2, n_old
+
+        def tet_fn(t, masks):
+            return torch.from_numpy(ctx.label_tets(t.numpy().view(np.uint32), masks.numpy().view(np.uint32)))
+
+        n2, t2, labels, tsh, masks = refine_relabel_sharded(nodes, tets, torch.from_numpy(m0.view(np.int32)), 2,
+                                                            node_fn, flag_fn, refine_fn, tet_fn, rank, world)
+        full = gather_labels(labels, tsh)
+        if rank == 0:
+            np.save(os.path.join(out_dir, "labels.npy"), full.numpy())
+            np.save(os.path.join(out_dir, "tets.npy"), t2)
+        ctx.close()
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_ranks_recursive_driver_gpu(tmp_path):
+    """The sharded recursive driver with real kernels on 2 ranks (flags and new
+    masks gathered over a host collective) equals the single-process device
+    driver nm_refine_relabel bit for bit."""
+    import socket
+    import torch.multiprocessing as mp
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    mp.spawn(_gpu_rank_recursive, args=(2, port, str(tmp_path)), nprocs=2, join=True)
+    from paper_2203_10000_b200._native import Context
+    cfg = synth.config(2)
+    S = cfg.surfaces
+    nodes, tets = synth.lattice_mesh((-110.0, -110.0, -110.0), 5.0, (44, 44, 44))
+    with Context(0) as c:
+        c.set_surfaces(S.xyz, S.tri, S.comp_off, S.label_ids)
+        n2, t2, lab, masks, st = c.refine_relabel(nodes, tets, levels=2)
+    np.testing.assert_array_equal(np.load(tmp_path / "tets.npy"), t2)
+    np.testing.assert_array_equal(np.load(tmp_path / "labels.npy"), lab)
