@@ -21,8 +21,9 @@
  *   - Plain pointers and sizes; no torch or STL types cross this boundary.
  *   - Host-buffer entry points borrow caller-owned buffers for the duration
  *     of the call and are synchronous. *_device entry points take device
- *     pointers and a cudaStream_t (passed as void*, NULL = the context's own
- *     stream) and are asynchronous: they never synchronise with the host.
+ *     pointers and a cudaStream_t (passed as void*; NULL = the context's own
+ *     non-blocking stream, cudaStreamLegacy (0x1) = the legacy default
+ *     stream) and are asynchronous unless stats are requested.
  *   - Points are fp64 xyz triples (the layout of std::vector<nestmesh::Vec3>,
  *     vec3.hpp:11-28); triangles are uint32 index triples into one fp64 vertex
  *     array (std::vector<nestmesh::Triangle>, surface.hpp:16); tets are uint32
@@ -62,6 +63,9 @@ typedef struct nm_options {
   int sort_points;       /* 1: Morton-order points before the kernel (performance only) */
   int pairs_per_thread;  /* point pairs per thread of the fp32 kernel: 1 or 2 (performance only) */
   int layout;            /* triangle tiles: 0 auto, 1 independent triangles, 2 strip segments (performance only) */
+  int cull_outside;      /* 1: exact culling — a point outside a closed compartment's bounding box gets s = 0
+                            without evaluating its triangles (the winding number of a closed surface);
+                            0 (default): every point-triangle pair is evaluated */
 } nm_options;
 
 /* Counters of one labeling call (accumulated by the call, not across calls). */

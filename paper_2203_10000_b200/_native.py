@@ -36,6 +36,7 @@ class NmOptions(ctypes.Structure):
         ("sort_points", ctypes.c_int),
         ("pairs_per_thread", ctypes.c_int),
         ("layout", ctypes.c_int),
+        ("cull_outside", ctypes.c_int),
     ]
 
 
@@ -174,6 +175,20 @@ def default_options(**overrides) -> NmOptions:
     return opt
 
 
+CUDA_STREAM_LEGACY = 1  # cudaStreamLegacy: the legacy default stream handle
+
+
+def stream_handle(stream):
+    """Map a caller stream to the ABI's void*: None -> the context's own
+    stream; 0 (torch's default stream) -> cudaStreamLegacy, so the kernels are
+    ordered with torch work on that stream; anything else as is."""
+    if stream is None:
+        return None
+    if hasattr(stream, "cuda_stream"):
+        stream = stream.cuda_stream
+    return CUDA_STREAM_LEGACY if int(stream) == 0 else int(stream)
+
+
 class Context:
     """One device + one stream + the replicated surface set (nm_ctx)."""
 
@@ -306,7 +321,7 @@ class Context:
     def lattice_device(self, origin, h, n, d_nodes, d_tets, stream=None):
         o = np.ascontiguousarray(origin, dtype=np.float64)
         check(self.lib.nm_lattice_device(self.handle, ptr(o, ctypes.c_double), h, n[0], n[1], n[2],
-                                         d_nodes.data_ptr(), d_tets.data_ptr(), stream))
+                                         d_nodes.data_ptr(), d_tets.data_ptr(), stream_handle(stream)))
 
     def label_centroids(self, nodes, tets, threshold=0.5):
         nodes = np.ascontiguousarray(nodes, dtype=np.float64).reshape(-1, 3)
@@ -407,19 +422,20 @@ class Context:
         st = NmStats() if stats else None
         check(self.lib.nm_label_nodes_device(self.handle, d_pts.data_ptr(), d_pts.shape[0], threshold,
                                              d_masks.data_ptr(), d_s.data_ptr() if d_s is not None else None,
-                                             stream, ctypes.byref(st) if st is not None else None))
+                                             stream_handle(stream), ctypes.byref(st) if st is not None else None))
         return st.as_dict() if st is not None else None
 
     def label_tets_device(self, d_tets, d_masks, d_labels, stream=None, stats=True):
         st = NmStats() if stats else None
         check(self.lib.nm_label_tets_device(self.handle, d_tets.data_ptr(), d_tets.shape[0], d_masks.data_ptr(),
-                                            d_labels.data_ptr(), stream,
+                                            d_labels.data_ptr(), stream_handle(stream),
                                             ctypes.byref(st) if st is not None else None))
         return st.as_dict() if st is not None else None
 
     def flag_boundary_device(self, d_tets, d_masks, d_ids, d_count, active_mask=0xFFFFFFFF, stream=None):
         check(self.lib.nm_flag_boundary_device(self.handle, d_tets.data_ptr(), d_tets.shape[0], d_masks.data_ptr(),
-                                               active_mask, d_ids.data_ptr(), d_count.data_ptr(), stream))
+                                               active_mask, d_ids.data_ptr(), d_count.data_ptr(),
+                                               stream_handle(stream)))
 
 
 def _take_mesh(lib, h):

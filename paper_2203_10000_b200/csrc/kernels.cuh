@@ -53,6 +53,7 @@ struct LabelParams {
   float tau, delta;
   std::uint32_t* masks;      // n
   std::uint32_t* flagmask;   // n (bit k: pair (i,k) needs the fp64 fix-up)
+  const float4* comp_box;    // 2 per compartment (lo, hi), centred frame, widened; nullptr = no culling
   double* s_out;             // n*K or nullptr
   unsigned long long* counters;  // [0] near / [1] far visits of (warp, 8-triangle group)
 };
@@ -117,6 +118,25 @@ __global__ void __launch_bounds__(kBlock, (NP == 1 ? NM_MIN_BLOCKS : 1)) k_label
     for (int k = 0; k < P; ++k) {
       acc64[k] = 0.0;
       det[k] = false;
+    }
+    // Exact outside culling (opt-in): a point outside a closed compartment's
+    // bounding box has winding number exactly 0 (SPEC.md:227 closedness), so
+    // its s is set to 0 whatever the CTA does; the CTA skips the
+    // compartment's tiles when every point is outside.
+    bool outside[P];
+#pragma unroll
+    for (int k = 0; k < P; ++k) outside[k] = false;
+    if (prm.comp_box) {
+      const float4 blo = prm.comp_box[2 * c], bhi = prm.comp_box[2 * c + 1];
+      bool all_out = true;
+#pragma unroll
+      for (int k = 0; k < P; ++k) {
+        const float x = (k & 1) ? hx[k >> 1].y : hx[k >> 1].x, y = (k & 1) ? hy[k >> 1].y : hy[k >> 1].x,
+                    z = (k & 1) ? hz[k >> 1].y : hz[k >> 1].x;
+        outside[k] = x < blo.x || x > bhi.x || y < blo.y || y > bhi.y || z < blo.z || z > bhi.z;
+        all_out &= outside[k] || !valid[k];
+      }
+      if (__syncthreads_and(all_out)) tile = tile_end;
     }
     for (; tile < tile_end; ++tile) {
       const float4* gt = prm.tri + static_cast<std::size_t>(tile) * kTileF4;
@@ -257,7 +277,8 @@ __global__ void __launch_bounds__(kBlock, (NP == 1 ? NM_MIN_BLOCKS : 1)) k_label
     }
 #pragma unroll
     for (int k = 0; k < P; ++k) {
-      const double s = acc64[k] * kInv2Pi;
+      const double s = outside[k] ? 0.0 : acc64[k] * kInv2Pi;
+      det[k] &= !outside[k];
       if (s >= prm.T) mask[k] |= 1u << c;
       // NaN-safe: anything not provably outside the band is re-evaluated.
       if (det[k] || !(fabs(s - prm.T) >= prm.band)) fmask[k] |= 1u << c;

@@ -214,7 +214,7 @@ struct nm_ctx {
   double cx = 0, cy = 0, cz = 0;
   double lo[3] = {0, 0, 0}, span = 1.0;  // Morton box of the domain
   nm::LabelIds ids{};
-  DBuf tri, sub, comp_tiles, xyz64, tri_idx, comp_off;
+  DBuf tri, sub, comp_tiles, xyz64, tri_idx, comp_off, comp_box;
 
   // scratch
   DBuf pts, masks, flagmask, nbr, known, want, fkeys, frontier, lex, region, bfaces, btri, dist_tri, dist_xyz,
@@ -224,7 +224,7 @@ struct nm_ctx {
       s_out;
 
   ~nm_ctx() {
-    for (DBuf* b : {&tri, &sub, &comp_tiles, &xyz64, &tri_idx, &comp_off, &pts, &masks, &flagmask, &nbr, &known, &want, &fkeys, &frontier, &lex, &region, &bfaces, &btri,
+    for (DBuf* b : {&tri, &sub, &comp_tiles, &xyz64, &tri_idx, &comp_off, &comp_box, &pts, &masks, &flagmask, &nbr, &known, &want, &fkeys, &frontier, &lex, &region, &bfaces, &btri,
                     &dist_tri, &dist_xyz, &dist_idx, &dist_d32, &dist_out, &r_red, &r_keys, &r_keys2, &r_S,
                     &r_idx, &r_touched, &r_mask, &r_cnt, &r_offs, &r_flag, &meshA_nodes, &meshA_tets, &meshA_labels,
                     &meshB_nodes, &meshB_tets, &meshB_labels, &meshB_parent, &masks2, &order, &keys,
@@ -344,6 +344,7 @@ void label_nodes_dev(nm_ctx* c, const double* d_pts, std::size_t n, double T, st
   prm.delta = c->opt.delta_mm;
   prm.masks = d_masks;
   prm.flagmask = flagmask;
+  prm.comp_box = c->opt.cull_outside ? static_cast<const float4*>(c->comp_box.p) : nullptr;
   prm.s_out = d_s;
   prm.counters = counters;
   if (stats) NM_CUDA(cudaEventRecord(c->ev[1], st));
@@ -578,6 +579,7 @@ void nm_default_options(nm_options* o) {
   o->sort_points = 1;
   o->pairs_per_thread = 1;
   o->layout = 0;
+  o->cull_outside = 0;
 }
 
 int nm_create(nm_ctx** out, const nm_options* opt) {
@@ -865,6 +867,34 @@ int nm_set_surfaces(nm_ctx* c, const double* xyz, std::size_t nv, const std::uin
     up(c->xyz64, xyz, nv * 3 * sizeof(double));
     up(c->tri_idx, tri, nt * 3 * sizeof(std::uint32_t));
     up(c->comp_off, comp_off, (K + 1) * sizeof(std::uint32_t));
+    // compartment boxes for exact outside culling: centred frame, rounded
+    // outward and widened by 1e-3 mm + 1e-6 |x| (covers the fp32 rounding of
+    // the point coordinates the kernel compares)
+    std::vector<float4> hbox(2 * K);
+    for (int k = 0; k < K; ++k) {
+      double blo[3] = {1e300, 1e300, 1e300}, bhi[3] = {-1e300, -1e300, -1e300};
+      for (std::uint32_t t = comp_off[k]; t < comp_off[k + 1]; ++t)
+        for (int v = 0; v < 3; ++v)
+          for (int a = 0; a < 3; ++a) {
+            const double x = xyz[3 * std::size_t(tri[3 * t + v]) + a] - ctr[a];
+            blo[a] = std::min(blo[a], x);
+            bhi[a] = std::max(bhi[a], x);
+          }
+      float lo4[3], hi4[3];
+      for (int a = 0; a < 3; ++a) {
+        if (comp_off[k + 1] == comp_off[k]) {  // empty compartment: s = 0 everywhere
+          lo4[a] = 1e30f;
+          hi4[a] = -1e30f;
+          continue;
+        }
+        const double m = 1e-3 + 1e-6 * std::max(std::fabs(blo[a]), std::fabs(bhi[a]));
+        lo4[a] = std::nextafter(float(blo[a] - m), -INFINITY);
+        hi4[a] = std::nextafter(float(bhi[a] + m), INFINITY);
+      }
+      hbox[2 * k] = make_float4(lo4[0], lo4[1], lo4[2], 0.0f);
+      hbox[2 * k + 1] = make_float4(hi4[0], hi4[1], hi4[2], 0.0f);
+    }
+    up(c->comp_box, hbox.data(), hbox.size() * sizeof(float4));
     NM_CUDA(cudaStreamSynchronize(c->stream));
     c->K = K;
     c->nt_real = nt;

@@ -200,3 +200,25 @@ def test_two_ranks_recursive_driver_gpu(tmp_path):
         n2, t2, lab, masks, st = c.refine_relabel(nodes, tets, levels=2)
     np.testing.assert_array_equal(np.load(tmp_path / "tets.npy"), t2)
     np.testing.assert_array_equal(np.load(tmp_path / "labels.npy"), lab)
+
+
+def test_device_entry_points_follow_torch_stream():
+    """Kernels launched through the *_device entry points with torch's default
+    stream are ordered with torch work on it (cudaStreamLegacy mapping): a
+    torch copy queued right after the node pass sees the finished masks."""
+    import torch
+    from paper_2203_10000_b200._native import Context
+    cfg = synth.config(2)
+    S = cfg.surfaces
+    nodes = torch.from_numpy(cfg.lattice_nodes()).cuda()
+    with Context(0) as c:
+        c.set_surfaces(S.xyz, S.tri, S.comp_off, S.label_ids)
+        ref, _ = c.label_nodes(nodes.cpu().numpy())
+        m = torch.zeros(nodes.shape[0], dtype=torch.int32, device="cuda")
+        stream = torch.cuda.current_stream()
+        for _ in range(3):
+            m.zero_()
+            c.label_nodes_device(nodes, m, stream=stream, stats=False)
+            out = m.clone()                       # queued on the same (default) stream
+            torch.cuda.synchronize()
+            np.testing.assert_array_equal(out.cpu().numpy().view(np.uint32), ref)

@@ -447,3 +447,29 @@ def test_refine_boundary_device(ctx):
     m2, u2, k2, _, _ = ctx.refine_boundary(nodes, tets, labels, 1, 3)
     np.testing.assert_array_equal(m2, nodes)
     np.testing.assert_array_equal(u2, tets)
+
+
+def test_outside_culling_exact():
+    """cull_outside: points outside a closed compartment's bounding box get
+    s = 0 exactly; every other result is bit-identical to the full
+    evaluation, masks/labels are unchanged, and the per-point decision keeps
+    results independent of the point set."""
+    from paper_2203_10000_b200._native import Context
+    cfg = synth.config(3)
+    S = cfg.surfaces
+    nodes = cfg.lattice_nodes()[2_000_000:2_060_000]
+    with Context(0) as full, Context(0, cull_outside=1) as cull:
+        for c in (full, cull):
+            c.set_surfaces(S.xyz, S.tri, S.comp_off, S.label_ids)
+        s_full, _ = full.enclosure(nodes)
+        s_cull, st = cull.enclosure(nodes)
+        m_full, _ = full.label_nodes(nodes)
+        m_cull, _ = cull.label_nodes(nodes)
+        idx = np.arange(0, nodes.shape[0], 7)
+        s_sub, _ = cull.enclosure(nodes[idx])
+    np.testing.assert_array_equal(m_cull, m_full)
+    culled = s_cull == 0.0
+    assert culled.mean() > 0.2                       # nuclei: most points are outside their boxes
+    np.testing.assert_array_equal(s_cull[~culled], s_full[~culled])
+    assert np.max(np.abs(s_full[culled])) < 1e-5
+    np.testing.assert_array_equal(s_sub, s_cull[idx])
