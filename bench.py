@@ -381,9 +381,9 @@ def main():
                        "pinned host shards -> nm_label_nodes_device -> NCCL all-gather -> nm_label_tets_device -> D2H"}
 
     # Exact outside culling (nm_options.cull_outside, opt-in): the same step
-    # with compartments skipped for points outside their bounding boxes
-    # (winding number exactly 0 for a closed surface). Reported beside the
-    # headline, which evaluates every pair.
+    # with compartments skipped for points outside their 13-DOP (winding
+    # number exactly 0 for a closed surface). Reported beside the headline,
+    # which evaluates every pair.
     cull = None
     if rank == 0 and world == 1 and not args.no_cull:
         cctx = Context(local, cull_outside=1)
@@ -403,7 +403,8 @@ def main():
             cms.append(a.elapsed_time(b))
         same = bool(torch.equal(cl, d_labels))
         cull = {"full_mesh_labeling_time_s": sum(cms) / len(cms) / 1e3, "labels_identical": same,
-                "note": "opt-in exact culling of compartments whose bounding box a point lies outside"}
+                "note": "opt-in exact culling (nm_options.cull_outside): a compartment is skipped for points "
+                        "outside its 13-DOP (winding number exactly 0 for a closed surface)"}
         cctx.close()
 
     # §8(f) rows on the labeled mesh (not part of the headline): device

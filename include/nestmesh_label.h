@@ -63,9 +63,9 @@ typedef struct nm_options {
   int sort_points;       /* 1: Morton-order points before the kernel (performance only) */
   int pairs_per_thread;  /* point pairs per thread of the fp32 kernel: 1 or 2 (performance only) */
   int layout;            /* triangle tiles: 0 auto, 1 independent triangles, 2 strip segments (performance only) */
-  int cull_outside;      /* 1: exact culling — a point outside a closed compartment's bounding box gets s = 0
-                            without evaluating its triangles (the winding number of a closed surface);
-                            0 (default): every point-triangle pair is evaluated */
+  int cull_outside;      /* 1: exact culling — a point outside a closed compartment's 13-DOP (slabs on 13
+                            directions around its vertices) gets s = 0 without evaluating its triangles
+                            (winding number of a closed surface); 0 (default): every pair is evaluated */
 } nm_options;
 
 /* Counters of one labeling call (accumulated by the call, not across calls). */

@@ -34,6 +34,27 @@ constexpr int kBlock = NM_BLOCK;        // threads per CTA of k_label
 constexpr unsigned kFull = 0xffffffffu;
 constexpr double kInv2Pi = 0.15915494309189533576888376337251;
 
+// 13-DOP directions (axes, cube diagonals, face diagonals; unnormalised):
+// a point outside any slab [lo_j, hi_j] of p.d_j is outside the convex hull
+// of the compartment's vertices, hence outside the closed surface.
+constexpr int kDopDirs = 13;
+constexpr int kDopF4 = 7;  // 26 floats (lo_j, hi_j) padded to 7 float4
+__host__ __device__ constexpr float dop_dir(int j, int a) {
+  return (j == 0)    ? (a == 0 ? 1.f : 0.f)
+         : (j == 1)  ? (a == 1 ? 1.f : 0.f)
+         : (j == 2)  ? (a == 2 ? 1.f : 0.f)
+         : (j == 3)  ? 1.f
+         : (j == 4)  ? (a == 0 ? -1.f : 1.f)
+         : (j == 5)  ? (a == 1 ? -1.f : 1.f)
+         : (j == 6)  ? (a == 2 ? -1.f : 1.f)
+         : (j == 7)  ? (a == 2 ? 0.f : 1.f)
+         : (j == 8)  ? (a == 2 ? 0.f : (a == 0 ? 1.f : -1.f))
+         : (j == 9)  ? (a == 1 ? 0.f : 1.f)
+         : (j == 10) ? (a == 1 ? 0.f : (a == 0 ? 1.f : -1.f))
+         : (j == 11) ? (a == 0 ? 0.f : 1.f)
+                     : (a == 0 ? 0.f : (a == 1 ? 1.f : -1.f));
+}
+
 struct LabelIds {
   int id[32];
 };
@@ -53,7 +74,8 @@ struct LabelParams {
   float tau, delta;
   std::uint32_t* masks;      // n
   std::uint32_t* flagmask;   // n (bit k: pair (i,k) needs the fp64 fix-up)
-  const float4* comp_box;    // 2 per compartment (lo, hi), centred frame, widened; nullptr = no culling
+  const std::uint32_t* cull;  // per evaluation position: bit k = outside compartment k's 13-DOP
+                              // (k_cull_mask); nullptr = off
   double* s_out;             // n*K or nullptr
   unsigned long long* counters;  // [0] near / [1] far visits of (warp, 8-triangle group)
 };
@@ -61,7 +83,7 @@ struct LabelParams {
 // NP point pairs per thread (2*NP points), packed fp32x2 arithmetic.
 // STRIP = false: 3 float4 per triangle (triangle soup);
 // STRIP = true : 4 strip segments of 8 triangles per subtile (vos.cuh).
-template <int NP, bool STRIP>
+template <int NP, bool STRIP, bool CULL = false>
 __global__ void __launch_bounds__(kBlock, (NP == 1 ? NM_MIN_BLOCKS : 1)) k_label(const LabelParams prm) {
   constexpr int P = 2 * NP;
   constexpr int kSubF4 = STRIP ? (kSub / kSegTris) * kSegF4 : kSub * 3;  // float4 per subtile
@@ -104,9 +126,12 @@ __global__ void __launch_bounds__(kBlock, (NP == 1 ? NM_MIN_BLOCKS : 1)) k_label
       lx[k >> 1].x = gx; ly[k >> 1].x = gy; lz[k >> 1].x = gz;
     }
   }
-  std::uint32_t mask[P], fmask[P];
+  std::uint32_t mask[P], fmask[P], cull[P];
 #pragma unroll
-  for (int k = 0; k < P; ++k) mask[k] = fmask[k] = 0u;
+  for (int k = 0; k < P; ++k) {
+    mask[k] = fmask[k] = 0u;
+    cull[k] = (CULL && valid[k]) ? prm.cull[base + k] : 0u;
+  }
   unsigned n_near = 0, n_far = 0;
 
   int tile = prm.comp_tiles[0];
@@ -126,14 +151,11 @@ __global__ void __launch_bounds__(kBlock, (NP == 1 ? NM_MIN_BLOCKS : 1)) k_label
     bool outside[P];
 #pragma unroll
     for (int k = 0; k < P; ++k) outside[k] = false;
-    if (prm.comp_box) {
-      const float4 blo = prm.comp_box[2 * c], bhi = prm.comp_box[2 * c + 1];
+    if (CULL) {
       bool all_out = true;
 #pragma unroll
       for (int k = 0; k < P; ++k) {
-        const float x = (k & 1) ? hx[k >> 1].y : hx[k >> 1].x, y = (k & 1) ? hy[k >> 1].y : hy[k >> 1].x,
-                    z = (k & 1) ? hz[k >> 1].y : hz[k >> 1].x;
-        outside[k] = x < blo.x || x > bhi.x || y < blo.y || y > bhi.y || z < blo.z || z > bhi.z;
+        outside[k] = (cull[k] >> c) & 1u;
         all_out &= outside[k] || !valid[k];
       }
       if (__syncthreads_and(all_out)) tile = tile_end;
@@ -789,5 +811,34 @@ struct PredInterface {
     return false;
   }
 };
+
+}  // namespace nm
+
+namespace nm {
+
+// Exact outside culling, per point: bit k set when the point (fp32 centred
+// coordinates, as k_label forms them) lies outside a slab of compartment k's
+// 13-DOP — outside the convex hull, so its winding number is exactly 0.
+__global__ void k_cull_mask(const double* pts, const std::uint32_t* order, std::size_t n, double cx, double cy, double cz,
+                            const float4* dop4, int K, std::uint32_t* out) {
+  for (std::size_t i = blockIdx.x * static_cast<std::size_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<std::size_t>(gridDim.x) * blockDim.x) {
+    const std::size_t j = order ? order[i] : i;
+    const float x = static_cast<float>(pts[3 * j] - cx), y = static_cast<float>(pts[3 * j + 1] - cy),
+                z = static_cast<float>(pts[3 * j + 2] - cz);
+    std::uint32_t m = 0;
+    for (int c = 0; c < K; ++c) {
+      const float* dop = reinterpret_cast<const float*>(dop4 + static_cast<std::size_t>(c) * kDopF4);
+      bool o = false;
+#pragma unroll
+      for (int j = 0; j < kDopDirs; ++j) {
+        const float pr = dop_dir(j, 0) * x + dop_dir(j, 1) * y + dop_dir(j, 2) * z;
+        o |= pr < __ldg(dop + 2 * j) || pr > __ldg(dop + 2 * j + 1);
+      }
+      if (o) m |= 1u << c;
+    }
+    out[i] = m;
+  }
+}
 
 }  // namespace nm

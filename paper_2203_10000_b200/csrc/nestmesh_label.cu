@@ -214,7 +214,7 @@ struct nm_ctx {
   double cx = 0, cy = 0, cz = 0;
   double lo[3] = {0, 0, 0}, span = 1.0;  // Morton box of the domain
   nm::LabelIds ids{};
-  DBuf tri, sub, comp_tiles, xyz64, tri_idx, comp_off, comp_box;
+  DBuf tri, sub, comp_tiles, xyz64, tri_idx, comp_off, comp_box, cullmask;
 
   // scratch
   DBuf pts, masks, flagmask, nbr, known, want, fkeys, frontier, lex, region, bfaces, btri, dist_tri, dist_xyz,
@@ -224,7 +224,7 @@ struct nm_ctx {
       s_out;
 
   ~nm_ctx() {
-    for (DBuf* b : {&tri, &sub, &comp_tiles, &xyz64, &tri_idx, &comp_off, &comp_box, &pts, &masks, &flagmask, &nbr, &known, &want, &fkeys, &frontier, &lex, &region, &bfaces, &btri,
+    for (DBuf* b : {&tri, &sub, &comp_tiles, &xyz64, &tri_idx, &comp_off, &comp_box, &cullmask, &pts, &masks, &flagmask, &nbr, &known, &want, &fkeys, &frontier, &lex, &region, &bfaces, &btri,
                     &dist_tri, &dist_xyz, &dist_idx, &dist_d32, &dist_out, &r_red, &r_keys, &r_keys2, &r_S,
                     &r_idx, &r_touched, &r_mask, &r_cnt, &r_offs, &r_flag, &meshA_nodes, &meshA_tets, &meshA_labels,
                     &meshB_nodes, &meshB_tets, &meshB_labels, &meshB_parent, &masks2, &order, &keys,
@@ -271,6 +271,10 @@ void set_label_smem_attributes() {
   NM_CUDA(cudaFuncSetAttribute(nm::k_label<1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                static_cast<int>(label_smem_bytes(false))));
   NM_CUDA(cudaFuncSetAttribute(nm::k_label<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               static_cast<int>(label_smem_bytes(false))));
+  NM_CUDA(cudaFuncSetAttribute(nm::k_label<1, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               static_cast<int>(label_smem_bytes(true))));
+  NM_CUDA(cudaFuncSetAttribute(nm::k_label<1, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                static_cast<int>(label_smem_bytes(false))));
 #endif
 }
@@ -344,18 +348,29 @@ void label_nodes_dev(nm_ctx* c, const double* d_pts, std::size_t n, double T, st
   prm.delta = c->opt.delta_mm;
   prm.masks = d_masks;
   prm.flagmask = flagmask;
-  prm.comp_box = c->opt.cull_outside ? static_cast<const float4*>(c->comp_box.p) : nullptr;
+  prm.cull = nullptr;
+  if (c->opt.cull_outside) {
+    auto* cm = c->cullmask.as<std::uint32_t>(n);
+    nm::k_cull_mask<<<grid_for(n, 256, c->sm_count * 16), 256, 0, st>>>(
+        d_pts, order, n, c->cx, c->cy, c->cz, static_cast<const float4*>(c->comp_box.p), c->K, cm);
+    ++launches;
+    prm.cull = cm;
+  }
   prm.s_out = d_s;
   prm.counters = counters;
   if (stats) NM_CUDA(cudaEventRecord(c->ev[1], st));
   {
-    const int np = c->opt.pairs_per_thread;
+    const int np = prm.cull ? 1 : c->opt.pairs_per_thread;
     const std::size_t per_block = static_cast<std::size_t>(nm::kBlock) * 2 * np;
     const unsigned grid = static_cast<unsigned>((n + per_block - 1) / per_block);
     const std::size_t smem = label_smem_bytes(c->strips);
-    if (c->strips) {
+    if (c->strips && prm.cull) {
+      nm::k_label<1, true, true><<<grid, nm::kBlock, smem, st>>>(prm);  // culling: one pair per thread
+    } else if (c->strips) {
       if (np == 2) nm::k_label<2, true><<<grid, nm::kBlock, smem, st>>>(prm);
       else nm::k_label<1, true><<<grid, nm::kBlock, smem, st>>>(prm);
+    } else if (prm.cull) {
+      nm::k_label<1, false, true><<<grid, nm::kBlock, smem, st>>>(prm);
     } else {
       if (np == 2) nm::k_label<2, false><<<grid, nm::kBlock, smem, st>>>(prm);
       else nm::k_label<1, false><<<grid, nm::kBlock, smem, st>>>(prm);
@@ -867,32 +882,33 @@ int nm_set_surfaces(nm_ctx* c, const double* xyz, std::size_t nv, const std::uin
     up(c->xyz64, xyz, nv * 3 * sizeof(double));
     up(c->tri_idx, tri, nt * 3 * sizeof(std::uint32_t));
     up(c->comp_off, comp_off, (K + 1) * sizeof(std::uint32_t));
-    // compartment boxes for exact outside culling: centred frame, rounded
-    // outward and widened by 1e-3 mm + 1e-6 |x| (covers the fp32 rounding of
-    // the point coordinates the kernel compares)
-    std::vector<float4> hbox(2 * K);
+    // 13-DOP of every compartment for exact outside culling (centred frame):
+    // slab bounds over the vertices, widened by 1e-3 mm + 1e-5 |bound| (covers
+    // the fp32 rounding of the point and of the projection in the kernel) and
+    // rounded outward.
+    std::vector<float4> hbox(static_cast<std::size_t>(K) * nm::kDopF4);
     for (int k = 0; k < K; ++k) {
-      double blo[3] = {1e300, 1e300, 1e300}, bhi[3] = {-1e300, -1e300, -1e300};
-      for (std::uint32_t t = comp_off[k]; t < comp_off[k + 1]; ++t)
-        for (int v = 0; v < 3; ++v)
-          for (int a = 0; a < 3; ++a) {
-            const double x = xyz[3 * std::size_t(tri[3 * t + v]) + a] - ctr[a];
-            blo[a] = std::min(blo[a], x);
-            bhi[a] = std::max(bhi[a], x);
+      float* dst = reinterpret_cast<float*>(&hbox[static_cast<std::size_t>(k) * nm::kDopF4]);
+      for (int q = 0; q < 4 * nm::kDopF4; ++q) dst[q] = 0.0f;
+      for (int j = 0; j < nm::kDopDirs; ++j) {
+        double lo = 1e300, hi = -1e300;
+        for (std::uint32_t t = comp_off[k]; t < comp_off[k + 1]; ++t)
+          for (int v = 0; v < 3; ++v) {
+            const double* X = xyz + 3 * std::size_t(tri[3 * t + v]);
+            double pr = 0.0;
+            for (int a = 0; a < 3; ++a) pr += double(nm::dop_dir(j, a)) * (X[a] - ctr[a]);
+            lo = std::min(lo, pr);
+            hi = std::max(hi, pr);
           }
-      float lo4[3], hi4[3];
-      for (int a = 0; a < 3; ++a) {
-        if (comp_off[k + 1] == comp_off[k]) {  // empty compartment: s = 0 everywhere
-          lo4[a] = 1e30f;
-          hi4[a] = -1e30f;
+        if (comp_off[k + 1] == comp_off[k]) {  // empty compartment: everything outside
+          dst[2 * j] = 1e30f;
+          dst[2 * j + 1] = -1e30f;
           continue;
         }
-        const double m = 1e-3 + 1e-6 * std::max(std::fabs(blo[a]), std::fabs(bhi[a]));
-        lo4[a] = std::nextafter(float(blo[a] - m), -INFINITY);
-        hi4[a] = std::nextafter(float(bhi[a] + m), INFINITY);
+        const double m = 1e-3 + 1e-5 * std::max(std::fabs(lo), std::fabs(hi));
+        dst[2 * j] = std::nextafter(float(lo - m), -INFINITY);
+        dst[2 * j + 1] = std::nextafter(float(hi + m), INFINITY);
       }
-      hbox[2 * k] = make_float4(lo4[0], lo4[1], lo4[2], 0.0f);
-      hbox[2 * k + 1] = make_float4(hi4[0], hi4[1], hi4[2], 0.0f);
     }
     up(c->comp_box, hbox.data(), hbox.size() * sizeof(float4));
     NM_CUDA(cudaStreamSynchronize(c->stream));

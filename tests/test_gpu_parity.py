@@ -450,7 +450,7 @@ def test_refine_boundary_device(ctx):
 
 
 def test_outside_culling_exact():
-    """cull_outside: points outside a closed compartment's bounding box get
+    """cull_outside: points outside a closed compartment's 13-DOP get
     s = 0 exactly; every other result is bit-identical to the full
     evaluation, masks/labels are unchanged, and the per-point decision keeps
     results independent of the point set."""
