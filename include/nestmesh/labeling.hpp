@@ -80,7 +80,10 @@ struct GpuOptions {
   nm_options opt;
   bool validate_closed = true;  // check the SPEC.md:227 precondition with validate_closed (surface.hpp:80-104)
   std::vector<int> devices;     // > 1 entries: initial_label shards over these devices (SPEC.md:267 --label-workers)
-  GpuOptions() { nm_default_options(&opt); }
+  GpuOptions() {
+    nm_default_options(&opt);
+    opt.cull_outside = 1;  // exact for closed surfaces; disabled below whenever closedness is not validated
+  }
 };
 
 inline int labeling_abi_version() { return nm_abi_version(); }
@@ -94,7 +97,11 @@ inline void check(int rc) {
 /// RAII owner of one nm_ctx (one device + stream + replicated surfaces).
 class Context {
  public:
-  explicit Context(const GpuOptions& o = {}) : validate_(o.validate_closed) { check(nm_create(&ctx_, &o.opt)); }
+  explicit Context(const GpuOptions& o = {}) : validate_(o.validate_closed) {
+    nm_options opt = o.opt;
+    if (!o.validate_closed) opt.cull_outside = 0;  // culling relies on closed surfaces
+    check(nm_create(&ctx_, &opt));
+  }
   ~Context() {
     if (ctx_) nm_destroy(ctx_);
   }
@@ -197,7 +204,9 @@ inline std::vector<int> initial_label(const TetrahedralMesh& mesh, const Surface
     // validate + flatten through a single-device context, then shard over the group
     detail::Context::validate(seg);
     nm_group* g = nullptr;
-    detail::check(nm_group_create(&g, static_cast<int>(o.devices.size()), o.devices.data(), &o.opt));
+    nm_options gopt = o.opt;
+    if (!o.validate_closed) gopt.cull_outside = 0;
+    detail::check(nm_group_create(&g, static_cast<int>(o.devices.size()), o.devices.data(), &gopt));
     std::unique_ptr<nm_group, int (*)(nm_group*)> guard(g, nm_group_destroy);
     std::vector<double> xyz;
     std::vector<std::uint32_t> tri, off{0};
