@@ -259,12 +259,22 @@ def main():
     rank, local, world = dist_env()
     if world != args.gpus and rank == 0:
         print(f"[bench] note: WORLD_SIZE={world} but --gpus={args.gpus}; using WORLD_SIZE", file=sys.stderr)
+    # NM_DIST_BACKEND=gloo + NM_SAME_DEVICE=1: every rank on cuda:0 with a
+    # host-side collective — exercises the multi-rank path on a 1-GPU box
+    # (the ranks' kernels never wait on one another). Default: NCCL, one GPU
+    # per rank.
+    backend = os.environ.get("NM_DIST_BACKEND", "nccl")
+    if os.environ.get("NM_SAME_DEVICE") == "1":
+        local = 0
     torch.cuda.set_device(local)
     group = None
     use_dist = world > 1 or os.environ.get("NM_FORCE_DIST") == "1"
     if use_dist:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     from paper_2203_10000_b200 import synth
     from paper_2203_10000_b200._native import Context
     from paper_2203_10000_b200.distributed import all_gather_masks, shard
@@ -278,7 +288,7 @@ def main():
         if not use_dist:
             return x
         import torch.distributed as dist
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        t = torch.tensor([x], dtype=torch.float64, device="cuda" if backend == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 

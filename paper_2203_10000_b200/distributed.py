@@ -58,7 +58,13 @@ def all_gather_masks(local: "torch.Tensor", sh: Shard, group=None) -> "torch.Ten
         buf[: local.shape[0]] = local
     out = torch.empty(sh.padded_total, dtype=local.dtype, device=local.device)
     if dist.is_available() and dist.is_initialized():
-        dist.all_gather_into_tensor(out, buf, group=group)
+        if buf.is_cuda and dist.get_backend(group) == "gloo":
+            # host-side collective (tests / single-GPU multi-rank runs)
+            host = torch.empty(sh.padded_total, dtype=local.dtype)
+            dist.all_gather_into_tensor(host, buf.cpu(), group=group)
+            out.copy_(host)
+        else:
+            dist.all_gather_into_tensor(out, buf, group=group)
     else:
         out.copy_(buf)
     return out[: sh.n]

@@ -222,3 +222,21 @@ def test_device_entry_points_follow_torch_stream():
             out = m.clone()                       # queued on the same (default) stream
             torch.cuda.synchronize()
             np.testing.assert_array_equal(out.cpu().numpy().view(np.uint32), ref)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_bench_multi_rank_on_one_gpu(world):
+    """bench.py under torchrun with `world` ranks sharing cuda:0 and a gloo
+    (host) collective: the sharded step, the e2e leg and max-over-ranks timing
+    run end to end and rank 0 prints one JSON line."""
+    env = dict(os.environ, NM_DIST_BACKEND="gloo", NM_SAME_DEVICE="1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr=127.0.0.1", f"--master-port={29600 + world}", str(ROOT / "bench.py"), "--gpus", str(world),
+           "--config", "2", "--steps", "2", "--warmup", "3"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, env=env, cwd=str(ROOT))
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    line = json.loads(lines[0])
+    assert line["n_gpus"] == world and line["value"] > 0 and line["e2e"]["value"] > 0
+    assert line["cpu_baseline"] is None
