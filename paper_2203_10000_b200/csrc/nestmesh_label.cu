@@ -589,7 +589,7 @@ void nm_default_options(nm_options* o) {
   o->delta_mm = 1e-3f;
   o->band = 1e-3;
   o->tie_eps = 1e-9;
-  o->far_ratio = 5.0f;
+  o->far_ratio = 4.0f;
   o->far_abs_mm = 0.05f;
   o->sort_points = 1;
   o->pairs_per_thread = 1;

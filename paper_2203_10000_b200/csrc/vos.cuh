@@ -171,10 +171,13 @@ __device__ __forceinline__ float acc_near_lane(float acc, float a_far, float num
 // Edge dots use R_a.R_b = (q_a + q_b)/2 - |e_ab|^2/2 (2 ops instead of 3).
 //
 // Two evaluators share the record:
-//   far  (a point at >= 5 rho + 0.05 mm from the group's bounding sphere):
+//   far  (a point at >= 4 rho + 0.05 mm from the centre of the group's
+//        bounding ball of radius rho):
 //        q = |V|^2 + |p|^2 - 2 V.p  (4 ops, no R vector), num = N.V - N.p,
-//        atan(x) = x (1 - x^2/3 + x^4/5) since |x| <= 0.0636 there (cap
-//        bound; truncation < 1e-8 relative): ~21 FP32 lane-ops + 2.25 MUFU;
+//        per triangle |Omega/2| <= pi (1 - sqrt(1 - 1/16)) = 0.1004 rad there
+//        (spherical-cap bound), so a consecutive pair's half-angle sum stays
+//        <= 0.2 rad and its 3-term series (after the complex product below)
+//        truncates at < x^9/9 = 6e-8 rad: ~21 FP32 lane-ops + 1.75 MUFU;
 //   near R-based terms (exact to ~ulp(|R|)), 3-term series for |x| <= 0.125
 //        else full-range atan2, plus the near-surface detector.
 // Which evaluator a (point, group) pair uses depends only on that point's own
@@ -229,7 +232,7 @@ __device__ __forceinline__ float2 atan_far2(float2 acc, float2 num, float2 den) 
   return fma2(x, p, acc);
 }
 
-// atan(N/D) for |N/D| <= 0.13: 3-term odd series (truncation x^9/9 < 1e-9 rel).
+// atan(N/D) for |N/D| <= tan(0.2): 3-term odd series (truncation x^9/9 < 7e-8 rad).
 __device__ __forceinline__ float2 atan_far3(float2 acc, float2 num, float2 den) {
   const float2 x = mul2(num, make_float2(rcp_approx(den.x), rcp_approx(den.y)));
   const float2 y = mul2(x, x);
@@ -239,7 +242,7 @@ __device__ __forceinline__ float2 atan_far3(float2 acc, float2 num, float2 den) 
 
 // Far evaluator. Consecutive triangles are combined pairwise through the
 // complex product (den0 + i num0)(den1 + i num1): its argument is the sum of
-// the two half-angles (each <= 0.0636 rad far away, so the sum stays in the
+// the two half-angles (each <= 0.1004 rad far away, so the sum stays in the
 // 3-term series' range and the real part stays > 0). Same FP32 work as two
 // separate series, half the MUFU.RCP.
 template <int NP>
