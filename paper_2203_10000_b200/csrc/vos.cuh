@@ -7,9 +7,10 @@
 // in fp64 per triangle (det[R1,R2,R3] = det[R1, v2-v1, v3-v1]); this is the
 // same quantity as the cross/dot form with ~1e4x less cancellation for far
 // points, and 6 fewer FP32 ops. Every operation is an explicit _rn intrinsic:
-// no contraction or reassociation is left to the compiler, so the same pair
-// (point, triangle) produces the same bits in the far loop and in the near
-// loop (labels and s are independent of warp composition, hence of sharding).
+// no contraction or reassociation is left to the compiler. Which evaluator
+// (far or near, below) a (point, 8-triangle group) pair uses depends only on
+// that point's own distance test, so a point's s never depends on its warp
+// mates, hence not on sharding or ordering.
 #pragma once
 #include <cuda_runtime.h>
 #include <math_constants.h>
@@ -27,56 +28,10 @@ __device__ __forceinline__ float rcp_approx(float x) {
   return r;
 }
 
-// Far-range arctangent: atan(x) = x (1 + c1 y + c2 y^2 + c3 y^3), y = x^2.
-// Used only for |x| <= kFarX, where the truncation error (x^9/9 < 2e-9
-// relative) is far below fp32 rounding.
+// Far-range arctangent in the near evaluator: atan(x) = x (1 + c1 y + c2 y^2
+// + c3 y^3), y = x^2, used for |x| <= kFarX (truncation x^9/9 < 2e-9
+// relative, far below fp32 rounding); full-range atan2_near otherwise.
 constexpr float kFarX = 0.125f;
-__device__ __forceinline__ float atan_far_poly(float y) {
-  return __fmaf_rn(__fmaf_rn(__fmaf_rn(-0.142857142857f, y, 0.2f), y, -0.333333333333f), y, 1.0f);
-}
-
-struct VosTerms {
-  float num, den, r1, r2, r3;
-};
-
-// One point-triangle evaluation up to (num, den). A/B/C hold the triangle's
-// vertices (xyz, centred frame) and N in .w.
-__device__ __forceinline__ VosTerms vos_terms(const float4& A, const float4& B, const float4& C, float px, float py,
-                                              float pz) {
-  const float x1 = __fsub_rn(A.x, px), y1 = __fsub_rn(A.y, py), z1 = __fsub_rn(A.z, pz);
-  const float x2 = __fsub_rn(B.x, px), y2 = __fsub_rn(B.y, py), z2 = __fsub_rn(B.z, pz);
-  const float x3 = __fsub_rn(C.x, px), y3 = __fsub_rn(C.y, py), z3 = __fsub_rn(C.z, pz);
-  VosTerms t;
-  t.r1 = sqrt_approx(__fmaf_rn(z1, z1, __fmaf_rn(y1, y1, __fmul_rn(x1, x1))));
-  t.r2 = sqrt_approx(__fmaf_rn(z2, z2, __fmaf_rn(y2, y2, __fmul_rn(x2, x2))));
-  t.r3 = sqrt_approx(__fmaf_rn(z3, z3, __fmaf_rn(y3, y3, __fmul_rn(x3, x3))));
-  t.num = __fmaf_rn(C.w, z1, __fmaf_rn(B.w, y1, __fmul_rn(A.w, x1)));
-  const float d12 = __fmaf_rn(z1, z2, __fmaf_rn(y1, y2, __fmul_rn(x1, x2)));
-  const float d13 = __fmaf_rn(z1, z3, __fmaf_rn(y1, y3, __fmul_rn(x1, x3)));
-  const float d23 = __fmaf_rn(z2, z3, __fmaf_rn(y2, y3, __fmul_rn(x2, x3)));
-  t.den = __fmaf_rn(__fmaf_rn(t.r1, t.r2, d12), t.r3, __fmaf_rn(d13, t.r2, __fmul_rn(d23, t.r1)));
-  return t;
-}
-
-// Far-path accumulation: acc += atan(num/den) for |num/den| <= kFarX, den > 0.
-__device__ __forceinline__ float acc_far(float acc, float num, float den) {
-  const float x = __fmul_rn(num, rcp_approx(den));
-  return __fmaf_rn(x, atan_far_poly(__fmul_rn(x, x)), acc);
-}
-
-// Near-path accumulation: identical bits to acc_far when the pair is in the
-// far range; full-range atan2 otherwise. Also updates the near-surface
-// detector: flag when the point is almost coplanar with and
-// projects onto/near the triangle, or is within delta of a vertex.
-__device__ __forceinline__ float acc_near(float acc, const VosTerms& t, float tau, float delta, bool& det) {
-  const bool far_range = (t.den > 0.0f) && (fabsf(t.num) <= __fmul_rn(kFarX, t.den));
-  const float a_far = acc_far(acc, t.num, t.den);
-  const float a_full = __fadd_rn(acc, atan2f(t.num, t.den));
-  const float prod = __fmul_rn(__fmul_rn(t.r1, t.r2), t.r3);
-  const float lim = __fmul_rn(tau, prod);
-  det |= ((fabsf(t.num) <= lim) && (t.den <= lim)) || (fminf(t.r1, fminf(t.r2, t.r3)) <= delta);
-  return far_range ? a_far : a_full;
-}
 
 // ---------------------------------------------------------------------------
 // Packed form: two points per float2 lane pair, triangle operands broadcast.
