@@ -31,8 +31,45 @@ constexpr int kBlock = NM_BLOCK;        // threads per CTA of k_label
 #ifndef NM_MIN_BLOCKS
 #define NM_MIN_BLOCKS 4                 // resident CTAs per SM requested for k_label<1>
 #endif
+#ifndef NM_TMA_PIPE
+#define NM_TMA_PIPE 1                   // double-buffered tiles via cp.async.bulk + mbarrier
+#endif
 constexpr unsigned kFull = 0xffffffffu;
 constexpr double kInv2Pi = 0.15915494309189533576888376337251;
+
+// ---- bulk-copy (TMA engine) staging helpers --------------------------------
+__device__ __forceinline__ unsigned smem_addr(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+// orders this thread's earlier generic-proxy shared accesses (made visible
+// to it by a CTA barrier) before its subsequent async-proxy (bulk copy) writes
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_addr(dst)),
+               "l"(src), "r"(bytes), "r"(smem_addr(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "NM_WAIT:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra NM_WAIT;\n}" ::"r"(smem_addr(bar)),
+      "r"(parity)
+      : "memory");
+}
 
 // 13-DOP directions (axes, cube diagonals, face diagonals; unnormalised):
 // a point outside any slab [lo_j, hi_j] of p.d_j is outside the convex hull
@@ -88,7 +125,16 @@ __global__ void __launch_bounds__(kBlock, (NP == 1 ? NM_MIN_BLOCKS : 1)) k_label
   constexpr int P = 2 * NP;
   constexpr int kSubF4 = STRIP ? (kSub / kSegTris) * kSegF4 : kSub * 3;  // float4 per subtile
   constexpr int kTileF4 = kSubF4 * kSubPerTile;
-#if NM_WARP_TILES
+#if NM_TMA_PIPE
+  // Two tile buffers filled by the bulk-copy engine (cp.async.bulk, one
+  // elected thread), completion signalled on one mbarrier per buffer: tile
+  // t + 1 streams in from L2 while the CTA evaluates tile t.
+  constexpr unsigned kSubF4Tile = kSubPerTile * kSubRec;
+  __shared__ alignas(128) float4 s_tri_buf[2][kTileF4];
+  __shared__ alignas(128) float4 s_sub_buf[2][kSubF4Tile];
+  __shared__ alignas(8) unsigned long long s_bar[2];
+  __shared__ unsigned s_skip;
+#elif NM_WARP_TILES
   // Every warp stages its own copy of the tile in dynamic shared memory
   // (kLabelSmemPerWarp<STRIP> bytes): warps whose points need the near path
   // never hold the others up at a CTA barrier.
@@ -134,6 +180,51 @@ __global__ void __launch_bounds__(kBlock, (NP == 1 ? NM_MIN_BLOCKS : 1)) k_label
   }
   unsigned n_near = 0, n_far = 0;
 
+#if NM_TMA_PIPE
+  // Compartments every point of the CTA is outside of (exact culling) are
+  // skipped by producer and consumers alike; the tile sequence is fixed here.
+  if (threadIdx.x == 0) {
+    mbar_init(&s_bar[0], 1);
+    mbar_init(&s_bar[1], 1);
+    s_skip = ~0u;
+    fence_mbar_init();
+  }
+  __syncthreads();
+  unsigned skip = 0u;
+  if (CULL) {
+    unsigned mine = ~0u;
+#pragma unroll
+    for (int k = 0; k < P; ++k)
+      if (valid[k]) mine &= cull[k];
+    mine = __reduce_and_sync(kFull, mine);
+    if ((threadIdx.x & 31) == 0) atomicAnd(&s_skip, mine);
+    __syncthreads();
+    skip = s_skip;
+  }
+  // producer state (thread 0): next tile to fetch and its compartment
+  int pf_c = 0, pf_t = -1;
+  auto pf_seek = [&](int c) {  // first tile of the first non-skipped, non-empty compartment >= c
+    for (; c < prm.K; ++c)
+      if (!((skip >> c) & 1u) && prm.comp_tiles[c] < prm.comp_tiles[c + 1]) {
+        pf_c = c;
+        pf_t = static_cast<int>(prm.comp_tiles[c]);
+        return;
+      }
+    pf_t = -1;
+  };
+  auto pf_issue = [&](int b) {
+    fence_proxy_async_smem();
+    mbar_expect_tx(&s_bar[b], (kTileF4 + kSubF4Tile) * 16u);
+    bulk_g2s(s_tri_buf[b], prm.tri + static_cast<std::size_t>(pf_t) * kTileF4, kTileF4 * 16u, &s_bar[b]);
+    bulk_g2s(s_sub_buf[b], prm.sub + static_cast<std::size_t>(pf_t) * kSubF4Tile, kSubF4Tile * 16u, &s_bar[b]);
+  };
+  if (threadIdx.x == 0) {
+    pf_seek(0);
+    if (pf_t >= 0) pf_issue(0);
+  }
+  unsigned it = 0;
+#endif
+
   int tile = prm.comp_tiles[0];
   for (int c = 0; c < prm.K; ++c) {
     const int tile_end = prm.comp_tiles[c + 1];
@@ -158,11 +249,27 @@ __global__ void __launch_bounds__(kBlock, (NP == 1 ? NM_MIN_BLOCKS : 1)) k_label
         outside[k] = (cull[k] >> c) & 1u;
         all_out &= outside[k] || !valid[k];
       }
+#if NM_TMA_PIPE
+      (void)all_out;
+      if ((skip >> c) & 1u) tile = tile_end;
+#else
       if (__syncthreads_and(all_out)) tile = tile_end;
+#endif
     }
     for (; tile < tile_end; ++tile) {
+#if NM_TMA_PIPE
+      const int buf = it & 1u;
+      if (threadIdx.x == 0) {
+        // buffer buf ^ 1 was released by the barrier closing the previous tile
+        if (pf_t >= 0 && ++pf_t >= static_cast<int>(prm.comp_tiles[pf_c + 1])) pf_seek(pf_c + 1);
+        if (pf_t >= 0) pf_issue(buf ^ 1);
+      }
+      mbar_wait(&s_bar[buf], (it >> 1) & 1u);
+      ++it;
+      const float4* const s_tri = s_tri_buf[buf];
+      const float4* const s_sub = s_sub_buf[buf];
+#elif NM_WARP_TILES
       const float4* gt = prm.tri + static_cast<std::size_t>(tile) * kTileF4;
-#if NM_WARP_TILES
       {
         const int lane = threadIdx.x & 31;
         const float4* gs = prm.sub + static_cast<std::size_t>(tile) * kSubPerTile * kSubRec;
@@ -173,6 +280,7 @@ __global__ void __launch_bounds__(kBlock, (NP == 1 ? NM_MIN_BLOCKS : 1)) k_label
         __syncwarp();
       }
 #else
+      const float4* gt = prm.tri + static_cast<std::size_t>(tile) * kTileF4;
       __syncthreads();
 #pragma unroll
       for (int i = threadIdx.x; i < kTileF4; i += kBlock) s_tri[i] = __ldg(gt + i);
@@ -296,6 +404,9 @@ __global__ void __launch_bounds__(kBlock, (NP == 1 ? NM_MIN_BLOCKS : 1)) k_label
         acc64[2 * q] += static_cast<double>(acc[q].x);
         acc64[2 * q + 1] += static_cast<double>(acc[q].y);
       }
+#if NM_TMA_PIPE
+      __syncthreads();  // every warp is done with buffer buf: the producer may refill it
+#endif
     }
 #pragma unroll
     for (int k = 0; k < P; ++k) {

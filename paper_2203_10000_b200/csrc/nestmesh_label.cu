@@ -819,9 +819,11 @@ int nm_set_surfaces(nm_ctx* c, const double* xyz, std::size_t nv, const std::uin
               for (int q = 0; q < nm::kSegTris; ++q) {
                 const float nf[3] = {float(N[q][0]), float(N[q][1]), float(N[q][2])};
                 const double w = double(nf[0]) * rv[3 * q] + double(nf[1]) * rv[3 * q + 1] + double(nf[2]) * rv[3 * q + 2];
-                r[nm::kSegT + q] = make_float4(nf[0], nf[1], nf[2], float(w));
+                // kRecScale (N, N.V): exact power-of-two scaling (vos.cuh seg_far)
+                const float sc = nm::kRecScale;
+                r[nm::kSegT + q] = make_float4(sc * nf[0], sc * nf[1], sc * nf[2], sc * float(w));
               }
-              // -|e|^2/2 of the consecutive (k,k+1) and skip (k,k+2) edges
+              // -kRecScale |e|^2/2 = -|e|^2 of the consecutive (k,k+1) and skip (k,k+2) edges
               float E[20] = {0};
               auto e2 = [&](int i, int jj) {
                 double s2 = 0;
@@ -829,7 +831,7 @@ int nm_set_surfaces(nm_ctx* c, const double* xyz, std::size_t nv, const std::uin
                   const double d = double(rv[3 * jj + a]) - double(rv[3 * i + a]);
                   s2 += d * d;
                 }
-                return float(-0.5 * s2);
+                return float(-0.5 * nm::kRecScale * s2);
               };
               for (int q = 0; q <= nm::kSegTris; ++q) E[q] = e2(q, q + 1);
               for (int q = 0; q < nm::kSegTris; ++q) E[9 + q] = e2(q, q + 2);

@@ -115,37 +115,37 @@ __device__ __forceinline__ float acc_near_lane(float acc, float a_far, float num
 // ---------------------------------------------------------------------------
 // Strip segments: 8 triangles t_k = (u_k, u_{k+1}, u_{k+2})
 // of one triangle strip share vertices and edges, so per triangle only one
-// new vertex and two new edge dots are computed. Record (kSegF4 float4):
-//   rec[0..9]   V_i  = (2x, 2y, 2z, |V_i|^2)         vertices (doubled), subtile frame
-//   rec[10..17] T_k  = (N_k.x, N_k.y, N_k.z, N_k.V_k) N_k = (v2-v1)x(v3-v1) of
-//                                                     the original triangle, so
-//                                                     num_k carries the outward
-//                                                     orientation whatever the
-//                                                     strip's winding parity
-//   rec[18..22] -|e|^2/2 of the 9 consecutive (k,k+1) and 8 skip (k,k+2) edges
-// Edge dots use R_a.R_b = (q_a + q_b)/2 - |e_ab|^2/2 (2 ops instead of 3).
+// new vertex and two new edges enter. Record (kSegF4 float4):
+//   rec[0..9]   V_i  = (2x, 2y, 2z, |V_i|^2)             vertices (doubled), subtile frame
+//   rec[10..17] T_k  = 2 (N_k.x, N_k.y, N_k.z, N_k.V_k)  N_k = (v2-v1)x(v3-v1) of the
+//                                                        original triangle, so num_k
+//                                                        carries the outward orientation
+//                                                        whatever the strip's winding parity
+//   rec[18..22] -|e|^2 of the 9 consecutive (k,k+1) and 8 skip (k,k+2) edges
+// The factor 2 on T and on |e|^2 is an exact power-of-two scaling: the far
+// evaluator works with (2 num, 2 den), the near one scales back exactly.
 //
 // Two evaluators share the record:
 //   far  (a point at >= 4 rho + 0.05 mm from the centre of the group's
 //        bounding ball of radius rho):
 //        q = |V|^2 + |p|^2 - 2 V.p  (4 ops, no R vector), num = N.V - N.p,
+//        2 den = (r_a + r_b)(r_b + r_c)(r_c + r_a) - |e_ab|^2 r_c - |e_ac|^2 r_b - |e_bc|^2 r_a,
 //        per triangle |Omega/2| <= pi (1 - sqrt(1 - 1/16)) = 0.1004 rad there
 //        (spherical-cap bound), so a consecutive pair's half-angle sum stays
 //        <= 0.2 rad and its 3-term series (after the complex product below)
-//        truncates at < x^9/9 = 6e-8 rad: ~21 FP32 lane-ops + 1.75 MUFU;
-//   near R-based terms (exact to ~ulp(|R|)), 3-term series for |x| <= 0.125
-//        else full-range atan2, plus the near-surface detector.
+//        truncates at < x^9/9 = 6e-8 rad: 20 FP32 lane-ops + 1.75 MUFU;
+//   near R-based terms, R_a.R_b = (q_a + q_b)/2 - |e_ab|^2/2 (exact to
+//        ~ulp(|R|)), 3-term series for |x| <= 0.125 else full-range atan2,
+//        plus the near-surface detector.
 // Which evaluator a (point, group) pair uses depends only on that point's own
 // distance test, never on its warp mates (mixed warps run both and select per
 // lane), so results are independent of sharding and point order.
 // ---------------------------------------------------------------------------
-#ifndef NM_PAIR_COMPLEX
-#define NM_PAIR_COMPLEX 1
-#endif
 constexpr int kSegTris = 8;
 constexpr int kSegF4 = 23;
 constexpr int kSegT = 10;  // first T_k
 constexpr int kSegE = 18;  // first edge float4
+constexpr float kRecScale = 2.0f;  // T_k and -|e|^2 scaling of the record (host packing)
 
 __device__ __forceinline__ float edge_val(const float4* rec, int idx) {
   const float4 v = rec[kSegE + (idx >> 2)];
@@ -168,23 +168,10 @@ __device__ __forceinline__ PairFrame pair_frame(float2 mx, float2 my, float2 mz)
 }
 
 // ---- far evaluator --------------------------------------------------------
-struct FarV {
-  float2 q, r;
-};
-
-__device__ __forceinline__ FarV far_vertex(const float4& V, const PairFrame& f) {
-  FarV v;
-  // |V - p|^2 = |V|^2 + |p|^2 + (2V).(-p)
-  v.q = fma2(bc(V.x), f.mx, fma2(bc(V.y), f.my, fma2(bc(V.z), f.mz, add2(bc(V.w), f.sp))));
-  v.r = make_float2(sqrt_approx(v.q.x), sqrt_approx(v.q.y));
-  return v;
-}
-
-__device__ __forceinline__ float2 atan_far2(float2 acc, float2 num, float2 den) {
-  const float2 x = mul2(num, make_float2(rcp_approx(den.x), rcp_approx(den.y)));
-  const float2 y = mul2(x, x);
-  const float2 p = fma2(fma2(bc(0.2f), y, bc(-0.333333333333f)), y, bc(1.0f));
-  return fma2(x, p, acc);
+// |V - p| from |V - p|^2 = |V|^2 + |p|^2 + (2V).(-p): 4 ops + MUFU.SQRT
+__device__ __forceinline__ float2 far_dist(const float4& V, const PairFrame& f) {
+  const float2 q = fma2(bc(V.x), f.mx, fma2(bc(V.y), f.my, fma2(bc(V.z), f.mz, add2(bc(V.w), f.sp))));
+  return make_float2(sqrt_approx(q.x), sqrt_approx(q.y));
 }
 
 // atan(N/D) for |N/D| <= tan(0.2): 3-term odd series (truncation x^9/9 < 7e-8 rad).
@@ -195,39 +182,41 @@ __device__ __forceinline__ float2 atan_far3(float2 acc, float2 num, float2 den) 
   return fma2(x, p, acc);
 }
 
-// Far evaluator. Consecutive triangles are combined pairwise through the
-// complex product (den0 + i num0)(den1 + i num1): its argument is the sum of
-// the two half-angles (each <= 0.1004 rad far away, so the sum stays in the
-// 3-term series' range and the real part stays > 0). Same FP32 work as two
-// separate series, half the MUFU.RCP.
+// Far evaluator.
+// Denominator: with 2 R_a.R_b = r_a^2 + r_b^2 - |e_ab|^2 the VOS denominator
+// 2 den = 2 r_a r_b r_c + 2 (R_a.R_b r_c + R_a.R_c r_b + R_b.R_c r_a)
+// regroups through (r_a + r_b)(r_b + r_c)(r_c + r_a) = sum_sym r_a^2 r_b +
+// 2 r_a r_b r_c into the product form above. Far away r ~ d >> |e|, so the
+// product (~8 d^3) dominates without cancellation, and the edge terms are
+// FFMA2s with a broadcast operand: 7 ops per triangle where the edge-dot form
+// takes 8, and no |R|^2 is carried between triangles.
+// Angle: consecutive triangles are combined pairwise through the complex
+// product (den0 + i num0)(den1 + i num1), whose argument is the sum of the two
+// half-angles (each <= 0.1004 rad far away, so the sum stays in the 3-term
+// series' range and the real part stays > 0): half the MUFU.RCP of two series.
 template <int NP>
 __device__ __forceinline__ void seg_far(const float4* __restrict__ rec, const PairFrame (&f)[NP], float2 (&acc)[NP]) {
-  FarV a[NP], b[NP];
-  float2 dab[NP];
-  {
-    const float4 V0 = rec[0], V1 = rec[1];
-    const float e0 = edge_val(rec, 0);
+  float2 ra[NP], rb[NP], sab[NP];
 #pragma unroll
-    for (int q = 0; q < NP; ++q) {
-      a[q] = far_vertex(V0, f[q]);
-      b[q] = far_vertex(V1, f[q]);
-      dab[q] = fma2(add2(a[q].q, b[q].q), bc(0.5f), bc(e0));
-    }
+  for (int q = 0; q < NP; ++q) {
+    ra[q] = far_dist(rec[0], f[q]);
+    rb[q] = far_dist(rec[1], f[q]);
+    sab[q] = add2(ra[q], rb[q]);
   }
   float2 n0[NP], d0[NP];
 #pragma unroll
   for (int k = 0; k < kSegTris; ++k) {
     const float4 V2 = rec[k + 2];
     const float4 T = rec[kSegT + k];
-    const float ebc = edge_val(rec, k + 1), eac = edge_val(rec, 9 + k);
+    const float eab = edge_val(rec, k), ebc = edge_val(rec, k + 1), eac = edge_val(rec, 9 + k);
 #pragma unroll
     for (int q = 0; q < NP; ++q) {
-      const FarV c = far_vertex(V2, f[q]);
-      const float2 dbc = fma2(add2(b[q].q, c.q), bc(0.5f), bc(ebc));
-      const float2 dac = fma2(add2(a[q].q, c.q), bc(0.5f), bc(eac));
-      const float2 num = fma2(bc(T.x), f[q].mx, fma2(bc(T.y), f[q].my, fma2(bc(T.z), f[q].mz, bc(T.w))));
-      const float2 den = fma2(fma2(a[q].r, b[q].r, dab[q]), c.r, fma2(dac, b[q].r, mul2(dbc, a[q].r)));
-#if NM_PAIR_COMPLEX
+      const float2 rc = far_dist(V2, f[q]);
+      const float2 sbc = add2(rb[q], rc);
+      const float2 sac = add2(ra[q], rc);
+      const float2 prod = mul2(mul2(sab[q], sbc), sac);
+      const float2 den = fma2(bc(eab), rc, fma2(bc(eac), rb[q], fma2(bc(ebc), ra[q], prod)));  // 2 den
+      const float2 num = fma2(bc(T.x), f[q].mx, fma2(bc(T.y), f[q].my, fma2(bc(T.z), f[q].mz, bc(T.w))));  // 2 num
       if (k & 1) {
         const float2 D = fma2(d0[q], den, mul2(make_float2(-n0[q].x, -n0[q].y), num));
         const float2 N = fma2(n0[q], den, mul2(num, d0[q]));
@@ -236,12 +225,9 @@ __device__ __forceinline__ void seg_far(const float4* __restrict__ rec, const Pa
         n0[q] = num;
         d0[q] = den;
       }
-#else
-      acc[q] = atan_far2(acc[q], num, den);
-#endif
-      a[q] = b[q];
-      b[q] = c;
-      dab[q] = dbc;
+      ra[q] = rb[q];
+      rb[q] = rc;
+      sab[q] = sbc;
     }
   }
 }
@@ -269,7 +255,7 @@ __device__ __forceinline__ void seg_near(const float4* __restrict__ rec, const P
   float2 dab[NP];
   {
     const float4 V0 = rec[0], V1 = rec[1];
-    const float e0 = edge_val(rec, 0);
+    const float e0 = 0.5f * edge_val(rec, 0);
 #pragma unroll
     for (int q = 0; q < NP; ++q) {
       a[q] = strip_vertex(V0, f[q].mx, f[q].my, f[q].mz);
@@ -281,13 +267,14 @@ __device__ __forceinline__ void seg_near(const float4* __restrict__ rec, const P
   for (int k = 0; k < kSegTris; ++k) {
     const float4 V2 = rec[k + 2];
     const float4 T = rec[kSegT + k];
-    const float ebc = edge_val(rec, k + 1), eac = edge_val(rec, 9 + k);
+    const float ebc = 0.5f * edge_val(rec, k + 1), eac = 0.5f * edge_val(rec, 9 + k);  // -|e|^2/2, exact
 #pragma unroll
     for (int q = 0; q < NP; ++q) {
       const Vtx2 c = strip_vertex(V2, f[q].mx, f[q].my, f[q].mz);
       const float2 dbc = fma2(add2(b[q].q, c.q), bc(0.5f), bc(ebc));
       const float2 dac = fma2(add2(a[q].q, c.q), bc(0.5f), bc(eac));
-      const float2 num = fma2(bc(T.z), a[q].z, fma2(bc(T.y), a[q].y, mul2(bc(T.x), a[q].x)));
+      float2 num = fma2(bc(T.z), a[q].z, fma2(bc(T.y), a[q].y, mul2(bc(T.x), a[q].x)));
+      num = mul2(num, bc(1.0f / kRecScale));  // exact: the record holds 2N
       const float2 den = fma2(fma2(a[q].r, b[q].r, dab[q]), c.r, fma2(dac, b[q].r, mul2(dbc, a[q].r)));
       const float2 af = acc_far2(acc[q], num, den);
       acc[q].x = acc_near_lane(acc[q].x, af.x, num.x, den.x, a[q].r.x, b[q].r.x, c.r.x, tau, delta, det[2 * q]);
