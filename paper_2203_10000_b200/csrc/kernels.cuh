@@ -20,7 +20,8 @@ namespace nm {
 constexpr int kTile = 256;              // triangles per shared-memory tile (fp64 fold granularity)
 constexpr int kSub = 32;                // triangles per subtile (near/far decision unit)
 constexpr int kSubPerTile = kTile / kSub;
-constexpr int kSubRec = 5;               // float4 per subtile record: sphere of the subtile + of its 4 groups of 8
+constexpr int kGroups = kSub / kSegTris;  // near/far groups (= strip segments) per subtile
+constexpr int kSubRec = 1 + kGroups;      // float4 per subtile record: sphere of the subtile + of its groups
 #ifndef NM_BLOCK
 #define NM_BLOCK 128
 #endif
@@ -30,6 +31,9 @@ constexpr int kBlock = NM_BLOCK;        // threads per CTA of k_label
 #endif
 #ifndef NM_MIN_BLOCKS
 #define NM_MIN_BLOCKS 4                 // resident CTAs per SM requested for k_label<1>
+#endif
+#ifndef NM_MIN_BLOCKS_NP2
+#define NM_MIN_BLOCKS_NP2 3             // resident CTAs per SM requested for k_label<2>
 #endif
 #ifndef NM_TMA_PIPE
 #define NM_TMA_PIPE 1                   // double-buffered tiles via cp.async.bulk + mbarrier
@@ -121,7 +125,7 @@ struct LabelParams {
 // STRIP = false: 3 float4 per triangle (triangle soup);
 // STRIP = true : 4 strip segments of 8 triangles per subtile (vos.cuh).
 template <int NP, bool STRIP, bool CULL = false>
-__global__ void __launch_bounds__(kBlock, (NP == 1 ? NM_MIN_BLOCKS : 1)) k_label(const LabelParams prm) {
+__global__ void __launch_bounds__(kBlock, (NP == 1 ? NM_MIN_BLOCKS : NM_MIN_BLOCKS_NP2)) k_label(const LabelParams prm) {
   constexpr int P = 2 * NP;
   constexpr int kSubF4 = STRIP ? (kSub / kSegTris) * kSegF4 : kSub * 3;  // float4 per subtile
   constexpr int kTileF4 = kSubF4 * kSubPerTile;

@@ -824,7 +824,7 @@ int nm_set_surfaces(nm_ctx* c, const double* xyz, std::size_t nv, const std::uin
                 r[nm::kSegT + q] = make_float4(sc * nf[0], sc * nf[1], sc * nf[2], sc * float(w));
               }
               // -kRecScale |e|^2/2 = -|e|^2 of the consecutive (k,k+1) and skip (k,k+2) edges
-              float E[20] = {0};
+              float E[4 * (nm::kSegF4 - nm::kSegE)] = {0};
               auto e2 = [&](int i, int jj) {
                 double s2 = 0;
                 for (int a = 0; a < 3; ++a) {
@@ -834,8 +834,9 @@ int nm_set_surfaces(nm_ctx* c, const double* xyz, std::size_t nv, const std::uin
                 return float(-0.5 * nm::kRecScale * s2);
               };
               for (int q = 0; q <= nm::kSegTris; ++q) E[q] = e2(q, q + 1);
-              for (int q = 0; q < nm::kSegTris; ++q) E[9 + q] = e2(q, q + 2);
-              for (int q = 0; q < 5; ++q) r[nm::kSegE + q] = make_float4(E[4 * q], E[4 * q + 1], E[4 * q + 2], E[4 * q + 3]);
+              for (int q = 0; q < nm::kSegTris; ++q) E[nm::kSegSkip + q] = e2(q, q + 2);
+              for (int q = 0; q < nm::kSegF4 - nm::kSegE; ++q)
+                r[nm::kSegE + q] = make_float4(E[4 * q], E[4 * q + 1], E[4 * q + 2], E[4 * q + 3]);
             } else {
               double N[3] = {0, 0, 0};
               if (u < nreal) normal64(order[k][u], N);
@@ -846,9 +847,9 @@ int nm_set_surfaces(nm_ctx* c, const double* xyz, std::size_t nv, const std::uin
           const double R = (far_ratio * rho + far_abs) * (1.0 + 1e-5);
           float4* hs = &hsub[(static_cast<std::size_t>(tl) * nm::kSubPerTile + sidx) * nm::kSubRec];
           hs[0] = make_float4(fc[0], fc[1], fc[2], float(R * R));
-          // spheres of the 4 groups of 8 triangles, centres relative to fc
-          const int per_group = static_cast<int>(srcv.size()) / 4;
-          for (int g = 0; g < 4; ++g) {
+          // spheres of the kGroups groups of kSegTris triangles, centres relative to fc
+          const int per_group = static_cast<int>(srcv.size()) / nm::kGroups;
+          for (int g = 0; g < nm::kGroups; ++g) {
             double glo[3] = {1e300, 1e300, 1e300}, ghi[3] = {-1e300, -1e300, -1e300};
             for (int q = g * per_group; q < (g + 1) * per_group; ++q)
               for (int a = 0; a < 3; ++a) {

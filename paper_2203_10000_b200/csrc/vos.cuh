@@ -141,10 +141,14 @@ __device__ __forceinline__ float acc_near_lane(float acc, float a_far, float num
 // distance test, never on its warp mates (mixed warps run both and select per
 // lane), so results are independent of sharding and point order.
 // ---------------------------------------------------------------------------
-constexpr int kSegTris = 8;
-constexpr int kSegF4 = 23;
-constexpr int kSegT = 10;  // first T_k
-constexpr int kSegE = 18;  // first edge float4
+#ifndef NM_SEG_TRIS
+#define NM_SEG_TRIS 8
+#endif
+constexpr int kSegTris = NM_SEG_TRIS;               // triangles per segment
+constexpr int kSegT = kSegTris + 2;                 // first T_k (after the vertices)
+constexpr int kSegE = kSegT + kSegTris;             // first edge float4
+constexpr int kSegSkip = kSegTris + 1;              // first skip edge (k, k+2)
+constexpr int kSegF4 = kSegE + (2 * kSegTris + 1 + 3) / 4;  // 23 float4 for 8 triangles
 constexpr float kRecScale = 2.0f;  // T_k and -|e|^2 scaling of the record (host packing)
 
 __device__ __forceinline__ float edge_val(const float4* rec, int idx) {
@@ -208,7 +212,7 @@ __device__ __forceinline__ void seg_far(const float4* __restrict__ rec, const Pa
   for (int k = 0; k < kSegTris; ++k) {
     const float4 V2 = rec[k + 2];
     const float4 T = rec[kSegT + k];
-    const float eab = edge_val(rec, k), ebc = edge_val(rec, k + 1), eac = edge_val(rec, 9 + k);
+    const float eab = edge_val(rec, k), ebc = edge_val(rec, k + 1), eac = edge_val(rec, kSegSkip + k);
 #pragma unroll
     for (int q = 0; q < NP; ++q) {
       const float2 rc = far_dist(V2, f[q]);
@@ -267,7 +271,7 @@ __device__ __forceinline__ void seg_near(const float4* __restrict__ rec, const P
   for (int k = 0; k < kSegTris; ++k) {
     const float4 V2 = rec[k + 2];
     const float4 T = rec[kSegT + k];
-    const float ebc = 0.5f * edge_val(rec, k + 1), eac = 0.5f * edge_val(rec, 9 + k);  // -|e|^2/2, exact
+    const float ebc = 0.5f * edge_val(rec, k + 1), eac = 0.5f * edge_val(rec, kSegSkip + k);  // -|e|^2/2, exact
 #pragma unroll
     for (int q = 0; q < NP; ++q) {
       const Vtx2 c = strip_vertex(V2, f[q].mx, f[q].my, f[q].mz);
