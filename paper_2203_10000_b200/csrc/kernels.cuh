@@ -956,4 +956,17 @@ __global__ void k_cull_mask(const double* pts, const std::uint32_t* order, std::
   }
 }
 
+// Largest node index referenced by the tets (device-side validation of the
+// host mesh, overlapped with the node pass in nm_label_mesh).
+__global__ void k_max_index(const uint4* __restrict__ tets, std::size_t nt, std::uint32_t* __restrict__ out) {
+  std::uint32_t m = 0;
+  for (std::size_t i = blockIdx.x * static_cast<std::size_t>(blockDim.x) + threadIdx.x; i < nt;
+       i += static_cast<std::size_t>(gridDim.x) * blockDim.x) {
+    const uint4 t = __ldg(tets + i);
+    m = max(max(m, max(t.x, t.y)), max(t.z, t.w));
+  }
+  m = __reduce_max_sync(kFull, m);
+  if ((threadIdx.x & 31) == 0) atomicMax(out, m);
+}
+
 }  // namespace nm

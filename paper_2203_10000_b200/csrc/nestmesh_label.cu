@@ -202,7 +202,11 @@ std::vector<Strip> stripify(const std::uint32_t* tri, std::uint32_t t0, std::uin
 struct nm_ctx {
   nm_options opt{};
   cudaStream_t stream = nullptr;
+  cudaStream_t side = nullptr;           // tet upload + validation, overlapped with the node pass
   cudaEvent_t ev[6] = {};
+  cudaEvent_t ev_side = nullptr;
+  std::uint32_t* h_word = nullptr;        // pinned: max tet node index read back from the side stream
+  std::uint64_t node_launches = 0;        // launches of the last label_nodes_dev
   int sm_count = 0;
 
   // surfaces
@@ -221,17 +225,20 @@ struct nm_ctx {
       dist_idx, dist_d32, dist_out, r_red, r_keys, r_keys2, r_S, r_idx, r_touched,
       r_mask, r_cnt, r_offs, r_flag, meshA_nodes, meshA_tets, meshA_labels, meshB_nodes, meshB_tets, meshB_labels,
       meshB_parent, masks2, order, keys, keys_alt, order_alt, cub_tmp, list, chunk, counters, count, tets, labels,
-      s_out;
+      s_out, word;
 
   ~nm_ctx() {
     for (DBuf* b : {&tri, &sub, &comp_tiles, &xyz64, &tri_idx, &comp_off, &comp_box, &cullmask, &pts, &masks, &flagmask, &nbr, &known, &want, &fkeys, &frontier, &lex, &region, &bfaces, &btri,
                     &dist_tri, &dist_xyz, &dist_idx, &dist_d32, &dist_out, &r_red, &r_keys, &r_keys2, &r_S,
                     &r_idx, &r_touched, &r_mask, &r_cnt, &r_offs, &r_flag, &meshA_nodes, &meshA_tets, &meshA_labels,
                     &meshB_nodes, &meshB_tets, &meshB_labels, &meshB_parent, &masks2, &order, &keys,
-                    &keys_alt, &order_alt, &cub_tmp, &list, &chunk, &counters, &count, &tets, &labels, &s_out})
+                    &keys_alt, &order_alt, &cub_tmp, &list, &chunk, &counters, &count, &tets, &labels, &s_out, &word})
       b->release();
     for (auto& e : ev)
       if (e) cudaEventDestroy(e);
+    if (ev_side) cudaEventDestroy(ev_side);
+    if (h_word) cudaFreeHost(h_word);
+    if (side) cudaStreamDestroy(side);
     if (stream) cudaStreamDestroy(stream);
   }
 
@@ -297,8 +304,13 @@ void select(nm_ctx* c, Pred pred, std::size_t n, std::uint32_t* out, std::uint32
 // of flagged points -> K3. masks/s_out are device pointers.
 // d_subset (nullable): evaluate only points d_pts[d_subset[i]], i < n; masks
 // (and s) are written at the original point index.
+void read_node_stats(nm_ctx* c, std::size_t n, cudaStream_t st, nm_stats* stats);
+
+// stats_deferred: the caller collects the stats later with read_node_stats
+// (no host synchronisation inside; nm_label_mesh overlaps the tet upload).
 void label_nodes_dev(nm_ctx* c, const double* d_pts, std::size_t n, double T, std::uint32_t* d_masks, double* d_s,
-                     cudaStream_t st, nm_stats* stats, const std::uint32_t* d_subset = nullptr) {
+                     cudaStream_t st, nm_stats* stats, const std::uint32_t* d_subset = nullptr,
+                     bool stats_deferred = false) {
   require_surfaces(c);
   if (!(T > 0.0 && T < 1.0)) throw Error("threshold must lie in (0, 1) (SPEC.md:216)");
   std::uint64_t launches = 0;
@@ -314,6 +326,11 @@ void label_nodes_dev(nm_ctx* c, const double* d_pts, std::size_t n, double T, st
   }
   if (n > 0xffffffffull) throw Error("more than 2^32 points in one call");
   auto* flagmask = c->flagmask.as<std::uint32_t>(d_subset ? c->flag_cap : n);
+  // every scratch buffer is sized before the first launch: a growing DBuf
+  // frees its old block, and cudaFree would wait for the kernels
+  auto* list = c->list.as<std::uint32_t>(n);
+  auto* d_count = c->count.as<std::uint32_t>(4);
+  (void)c->chunk.as<std::uint32_t>(std::max<std::size_t>(1, (n + nm::kSelChunk - 1) / nm::kSelChunk));
   const std::uint32_t* order = d_subset;
   if (c->opt.sort_points && n > 1) {
     auto* keys = c->keys.as<std::uint32_t>(n);
@@ -380,8 +397,6 @@ void label_nodes_dev(nm_ctx* c, const double* d_pts, std::size_t n, double T, st
   ++launches;
   if (stats) NM_CUDA(cudaEventRecord(c->ev[2], st));
   // compaction of flagged points + fp64 fix-up
-  auto* list = c->list.as<std::uint32_t>(n);
-  auto* d_count = c->count.as<std::uint32_t>(4);
   select(c, nm::PredNonzero{flagmask, d_subset}, n, list, d_count, st, launches);
   nm::FixupParams fp{};
   fp.pts = d_pts;
@@ -401,8 +416,17 @@ void label_nodes_dev(nm_ctx* c, const double* d_pts, std::size_t n, double T, st
   nm::k_fixup<<<c->sm_count * 8, 256, 0, st>>>(fp);
   NM_CUDA(cudaGetLastError());
   ++launches;
+  c->node_launches = launches;
   if (stats) {
     NM_CUDA(cudaEventRecord(c->ev[3], st));
+    if (!stats_deferred) read_node_stats(c, n, st, stats);
+  }
+}
+
+void read_node_stats(nm_ctx* c, std::size_t n, cudaStream_t st, nm_stats* stats) {
+  {
+    auto* counters = static_cast<unsigned long long*>(c->counters.p);
+    auto* d_count = static_cast<std::uint32_t*>(c->count.p);
     unsigned long long h[8];
     std::uint32_t hc = 0;
     NM_CUDA(cudaMemcpyAsync(h, counters, sizeof h, cudaMemcpyDeviceToHost, st));
@@ -417,7 +441,7 @@ void label_nodes_dev(nm_ctx* c, const double* d_pts, std::size_t n, double T, st
     stats->ties = h[3];
     stats->near_subtiles = h[0];
     stats->far_subtiles = h[1];
-    stats->launches = launches;
+    stats->launches = c->node_launches;
     NM_CUDA(cudaEventElapsedTime(&stats->ms_label, c->ev[1], c->ev[2]));
     NM_CUDA(cudaEventElapsedTime(&stats->ms_fixup, c->ev[2], c->ev[3]));
     NM_CUDA(cudaEventElapsedTime(&stats->ms_total, c->ev[0], c->ev[3]));
@@ -620,7 +644,10 @@ int nm_create(nm_ctx** out, const nm_options* opt) {
       c->sm_count = p.multiProcessorCount;
       set_label_smem_attributes();
       NM_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+      NM_CUDA(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
       for (auto& ev : c->ev) NM_CUDA(cudaEventCreate(&ev));
+      NM_CUDA(cudaEventCreateWithFlags(&c->ev_side, cudaEventDisableTiming));
+      NM_CUDA(cudaMallocHost(&c->h_word, sizeof(std::uint32_t)));
     } catch (...) {
       delete c;
       throw;
@@ -1008,19 +1035,40 @@ int nm_label_tets(nm_ctx* c, const std::uint32_t* tets, std::size_t nt, const st
   });
 }
 
+// Full mesh from host buffers. The node pass is enqueued first; the tet
+// upload and its index validation (k_max_index) run on the side stream
+// underneath it, so neither the 16 B/tet copy nor the check sits on the
+// critical path. A bad index is reported with the host scan's message.
 int nm_label_mesh(nm_ctx* c, const double* nodes, std::size_t n, const std::uint32_t* tets, std::size_t nt, double T,
                   int* labels_out, std::uint32_t* masks_out, nm_stats* stats) {
   return guarded([&] {
     require_surfaces(c);
-    check_tets(tets, nt, n);
+    if (nt && !tets) throw Error("null tets");
+    if (nt && n == 0) check_tets(tets, nt, n);
     NM_CUDA(cudaSetDevice(c->opt.device));
     auto* d_pts = c->pts.as<double>(3 * std::max<std::size_t>(n, 1));
     auto* d_masks = c->masks.as<std::uint32_t>(std::max<std::size_t>(n, 1));
     auto* d_tets = c->tets.as<std::uint32_t>(4 * std::max<std::size_t>(nt, 1));
     auto* d_labels = c->labels.as<int>(std::max<std::size_t>(nt, 1));
+    auto* d_word = c->word.as<std::uint32_t>(1);
     if (n) NM_CUDA(cudaMemcpyAsync(d_pts, nodes, 3 * n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
-    if (nt) NM_CUDA(cudaMemcpyAsync(d_tets, tets, 4 * nt * sizeof(std::uint32_t), cudaMemcpyHostToDevice, c->stream));
-    label_nodes_dev(c, d_pts, n, T, d_masks, nullptr, c->stream, stats);
+    label_nodes_dev(c, d_pts, n, T, d_masks, nullptr, c->stream, stats, nullptr, /*stats_deferred=*/true);
+    if (nt) {
+      NM_CUDA(cudaMemcpyAsync(d_tets, tets, 4 * nt * sizeof(std::uint32_t), cudaMemcpyHostToDevice, c->side));
+      NM_CUDA(cudaMemsetAsync(d_word, 0, sizeof(std::uint32_t), c->side));
+      nm::k_max_index<<<grid_for(nt, 256, c->sm_count * 8), 256, 0, c->side>>>(reinterpret_cast<const uint4*>(d_tets),
+                                                                               nt, d_word);
+      NM_CUDA(cudaGetLastError());
+      NM_CUDA(cudaMemcpyAsync(c->h_word, d_word, sizeof(std::uint32_t), cudaMemcpyDeviceToHost, c->side));
+      NM_CUDA(cudaEventRecord(c->ev_side, c->side));
+      NM_CUDA(cudaStreamWaitEvent(c->stream, c->ev_side, 0));
+      NM_CUDA(cudaEventSynchronize(c->ev_side));
+      if (*c->h_word >= n) {
+        NM_CUDA(cudaStreamSynchronize(c->stream));
+        check_tets(tets, nt, n);  // throws with the offending tet
+      }
+    }
+    if (stats && n) read_node_stats(c, n, c->stream, stats);
     label_tets_dev(c, d_tets, nt, d_masks, d_labels, c->stream, stats);
     if (nt) NM_CUDA(cudaMemcpyAsync(labels_out, d_labels, nt * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
     if (masks_out && n)
