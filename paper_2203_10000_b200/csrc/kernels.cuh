@@ -26,17 +26,11 @@ constexpr int kSubRec = 1 + kGroups;      // float4 per subtile record: sphere o
 #define NM_BLOCK 128
 #endif
 constexpr int kBlock = NM_BLOCK;        // threads per CTA of k_label
-#ifndef NM_WARP_TILES
-#define NM_WARP_TILES 0                 // 1: each warp stages its own tile copy (no CTA barriers; measured 5% slower)
-#endif
 #ifndef NM_MIN_BLOCKS
 #define NM_MIN_BLOCKS 4                 // resident CTAs per SM requested for k_label<1>
 #endif
 #ifndef NM_MIN_BLOCKS_NP2
 #define NM_MIN_BLOCKS_NP2 3             // resident CTAs per SM requested for k_label<2>
-#endif
-#ifndef NM_TMA_PIPE
-#define NM_TMA_PIPE 1                   // double-buffered tiles via cp.async.bulk + mbarrier
 #endif
 constexpr unsigned kFull = 0xffffffffu;
 constexpr double kInv2Pi = 0.15915494309189533576888376337251;
@@ -129,7 +123,6 @@ __global__ void __launch_bounds__(kBlock, (NP == 1 ? NM_MIN_BLOCKS : NM_MIN_BLOC
   constexpr int P = 2 * NP;
   constexpr int kSubF4 = STRIP ? (kSub / kSegTris) * kSegF4 : kSub * 3;  // float4 per subtile
   constexpr int kTileF4 = kSubF4 * kSubPerTile;
-#if NM_TMA_PIPE
   // Two tile buffers filled by the bulk-copy engine (cp.async.bulk, one
   // elected thread), completion signalled on one mbarrier per buffer: tile
   // t + 1 streams in from L2 while the CTA evaluates tile t.
@@ -138,17 +131,6 @@ __global__ void __launch_bounds__(kBlock, (NP == 1 ? NM_MIN_BLOCKS : NM_MIN_BLOC
   __shared__ alignas(128) float4 s_sub_buf[2][kSubF4Tile];
   __shared__ alignas(8) unsigned long long s_bar[2];
   __shared__ unsigned s_skip;
-#elif NM_WARP_TILES
-  // Every warp stages its own copy of the tile in dynamic shared memory
-  // (kLabelSmemPerWarp<STRIP> bytes): warps whose points need the near path
-  // never hold the others up at a CTA barrier.
-  extern __shared__ float4 nm_dyn_smem[];
-  float4* const s_tri = nm_dyn_smem + (threadIdx.x >> 5) * (kTileF4 + kSubPerTile * kSubRec);
-  float4* const s_sub = s_tri + kTileF4;
-#else
-  __shared__ float4 s_tri[kTileF4];
-  __shared__ float4 s_sub[kSubPerTile * kSubRec];
-#endif
 
   const std::size_t base = (static_cast<std::size_t>(blockIdx.x) * kBlock + threadIdx.x) * P;
   // Points in the centred frame as double-singles (hi + lo), packed in pairs;
@@ -184,7 +166,6 @@ __global__ void __launch_bounds__(kBlock, (NP == 1 ? NM_MIN_BLOCKS : NM_MIN_BLOC
   }
   unsigned n_near = 0, n_far = 0;
 
-#if NM_TMA_PIPE
   // Compartments every point of the CTA is outside of (exact culling) are
   // skipped by producer and consumers alike; the tile sequence is fixed here.
   if (threadIdx.x == 0) {
@@ -227,7 +208,6 @@ __global__ void __launch_bounds__(kBlock, (NP == 1 ? NM_MIN_BLOCKS : NM_MIN_BLOC
     if (pf_t >= 0) pf_issue(0);
   }
   unsigned it = 0;
-#endif
 
   int tile = prm.comp_tiles[0];
   for (int c = 0; c < prm.K; ++c) {
@@ -242,26 +222,12 @@ __global__ void __launch_bounds__(kBlock, (NP == 1 ? NM_MIN_BLOCKS : NM_MIN_BLOC
     // Exact outside culling (opt-in): a point outside a closed compartment's
     // bounding box has winding number exactly 0 (SPEC.md:227 closedness), so
     // its s is set to 0 whatever the CTA does; the CTA skips the
-    // compartment's tiles when every point is outside.
+    // compartment's tiles when every point is outside (skip bit c).
     bool outside[P];
 #pragma unroll
-    for (int k = 0; k < P; ++k) outside[k] = false;
-    if (CULL) {
-      bool all_out = true;
-#pragma unroll
-      for (int k = 0; k < P; ++k) {
-        outside[k] = (cull[k] >> c) & 1u;
-        all_out &= outside[k] || !valid[k];
-      }
-#if NM_TMA_PIPE
-      (void)all_out;
-      if ((skip >> c) & 1u) tile = tile_end;
-#else
-      if (__syncthreads_and(all_out)) tile = tile_end;
-#endif
-    }
+    for (int k = 0; k < P; ++k) outside[k] = CULL && ((cull[k] >> c) & 1u);
+    if (CULL && ((skip >> c) & 1u)) tile = tile_end;
     for (; tile < tile_end; ++tile) {
-#if NM_TMA_PIPE
       const int buf = it & 1u;
       if (threadIdx.x == 0) {
         // buffer buf ^ 1 was released by the barrier closing the previous tile
@@ -272,26 +238,6 @@ __global__ void __launch_bounds__(kBlock, (NP == 1 ? NM_MIN_BLOCKS : NM_MIN_BLOC
       ++it;
       const float4* const s_tri = s_tri_buf[buf];
       const float4* const s_sub = s_sub_buf[buf];
-#elif NM_WARP_TILES
-      const float4* gt = prm.tri + static_cast<std::size_t>(tile) * kTileF4;
-      {
-        const int lane = threadIdx.x & 31;
-        const float4* gs = prm.sub + static_cast<std::size_t>(tile) * kSubPerTile * kSubRec;
-        __syncwarp();
-#pragma unroll 4
-        for (int i = lane; i < kTileF4; i += 32) s_tri[i] = __ldg(gt + i);
-        for (int i = lane; i < kSubPerTile * kSubRec; i += 32) s_sub[i] = __ldg(gs + i);
-        __syncwarp();
-      }
-#else
-      const float4* gt = prm.tri + static_cast<std::size_t>(tile) * kTileF4;
-      __syncthreads();
-#pragma unroll
-      for (int i = threadIdx.x; i < kTileF4; i += kBlock) s_tri[i] = __ldg(gt + i);
-      if (threadIdx.x < kSubPerTile * kSubRec)
-        s_sub[threadIdx.x] = __ldg(prm.sub + static_cast<std::size_t>(tile) * kSubPerTile * kSubRec + threadIdx.x);
-      __syncthreads();
-#endif
 
       float2 acc[NP];
 #pragma unroll
@@ -347,12 +293,15 @@ __global__ void __launch_bounds__(kBlock, (NP == 1 ? NM_MIN_BLOCKS : NM_MIN_BLOC
               } else {
                 ++n_near;
                 float2 an[NP];
-                bool dn[P];
+                bool dn[P], use[P];
 #pragma unroll
                 for (int q = 0; q < NP; ++q) an[q] = acc[q];
 #pragma unroll
-                for (int k = 0; k < P; ++k) dn[k] = false;
-                seg_near<NP>(rec, f, an, dn, prm.tau, prm.delta);
+                for (int k = 0; k < P; ++k) {
+                  dn[k] = false;
+                  use[k] = valid[k] && !gf[k];
+                }
+                seg_near<NP>(rec, f, an, dn, use, prm.tau, prm.delta);
                 if (__any_sync(kFull, any)) {
                   float2 af[NP];
 #pragma unroll
@@ -408,9 +357,7 @@ __global__ void __launch_bounds__(kBlock, (NP == 1 ? NM_MIN_BLOCKS : NM_MIN_BLOC
         acc64[2 * q] += static_cast<double>(acc[q].x);
         acc64[2 * q + 1] += static_cast<double>(acc[q].y);
       }
-#if NM_TMA_PIPE
       __syncthreads();  // every warp is done with buffer buf: the producer may refill it
-#endif
     }
 #pragma unroll
     for (int k = 0; k < P; ++k) {

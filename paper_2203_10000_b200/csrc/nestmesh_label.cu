@@ -257,35 +257,6 @@ int grid_for(std::size_t n, int block, int cap) {
   return static_cast<int>(std::max<std::size_t>(1, std::min<std::size_t>(g, static_cast<std::size_t>(cap))));
 }
 
-// Dynamic shared memory of k_label: one tile copy per warp (NM_WARP_TILES).
-std::size_t label_smem_bytes(bool strips) {
-#if NM_WARP_TILES
-  const int sub_f4 = strips ? (nm::kSub / nm::kSegTris) * nm::kSegF4 : nm::kSub * 3;
-  return static_cast<std::size_t>(nm::kBlock / 32) * (sub_f4 * nm::kSubPerTile + nm::kSubPerTile * nm::kSubRec) *
-         sizeof(float4);
-#else
-  (void)strips;
-  return 0;
-#endif
-}
-
-void set_label_smem_attributes() {
-#if NM_WARP_TILES
-  NM_CUDA(cudaFuncSetAttribute(nm::k_label<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               static_cast<int>(label_smem_bytes(true))));
-  NM_CUDA(cudaFuncSetAttribute(nm::k_label<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               static_cast<int>(label_smem_bytes(true))));
-  NM_CUDA(cudaFuncSetAttribute(nm::k_label<1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               static_cast<int>(label_smem_bytes(false))));
-  NM_CUDA(cudaFuncSetAttribute(nm::k_label<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               static_cast<int>(label_smem_bytes(false))));
-  NM_CUDA(cudaFuncSetAttribute(nm::k_label<1, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               static_cast<int>(label_smem_bytes(true))));
-  NM_CUDA(cudaFuncSetAttribute(nm::k_label<1, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               static_cast<int>(label_smem_bytes(false))));
-#endif
-}
-
 // Ordered compaction of [0,n) under pred into out; count on the device.
 template <class Pred>
 void select(nm_ctx* c, Pred pred, std::size_t n, std::uint32_t* out, std::uint32_t* d_count, cudaStream_t st,
@@ -380,7 +351,7 @@ void label_nodes_dev(nm_ctx* c, const double* d_pts, std::size_t n, double T, st
     const int np = prm.cull ? 1 : c->opt.pairs_per_thread;
     const std::size_t per_block = static_cast<std::size_t>(nm::kBlock) * 2 * np;
     const unsigned grid = static_cast<unsigned>((n + per_block - 1) / per_block);
-    const std::size_t smem = label_smem_bytes(c->strips);
+    constexpr std::size_t smem = 0;  // k_label's tile buffers are static shared memory
     if (c->strips && prm.cull) {
       nm::k_label<1, true, true><<<grid, nm::kBlock, smem, st>>>(prm);  // culling: one pair per thread
     } else if (c->strips) {
@@ -642,7 +613,6 @@ int nm_create(nm_ctx** out, const nm_options* opt) {
       NM_CUDA(cudaGetDeviceProperties(&p, c->opt.device));
       if (p.major != 10) throw Error(std::string("device ") + p.name + " is not sm_100 (Blackwell B200)");
       c->sm_count = p.multiProcessorCount;
-      set_label_smem_attributes();
       NM_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
       NM_CUDA(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
       for (auto& ev : c->ev) NM_CUDA(cudaEventCreate(&ev));
@@ -793,7 +763,6 @@ int nm_set_surfaces(nm_ctx* c, const double* xyz, std::size_t nv, const std::uin
       for (std::uint32_t tl = tiles[k]; tl < tiles[k + 1]; ++tl) {
         for (int sidx = 0; sidx < nm::kSubPerTile; ++sidx) {
           // gather this subtile's vertices (centred frame, fp64)
-          int nv_loc = 0;
           std::vector<const double*> srcv;
           const std::size_t u0 = static_cast<std::size_t>(tl - tiles[k]) * nm::kTile / (use_strips ? nm::kSegTris : 1) +
                                  sidx * (use_strips ? nm::kSub / nm::kSegTris : nm::kSub);
@@ -823,8 +792,6 @@ int nm_set_surfaces(nm_ctx* c, const double* xyz, std::size_t nv, const std::uin
             rho = std::max(rho, std::sqrt(double(rel[3 * q]) * rel[3 * q] + double(rel[3 * q + 1]) * rel[3 * q + 1] +
                                           double(rel[3 * q + 2]) * rel[3 * q + 2]));
           }
-          nv_loc = static_cast<int>(srcv.size());
-          (void)nv_loc;
           float4* o = &htri[(static_cast<std::size_t>(tl) * nm::kSubPerTile + sidx) * sub_f4];
           for (int j = 0; j < nunits; ++j) {
             const std::size_t u = u0 + j;

@@ -252,9 +252,15 @@ __device__ __forceinline__ Vtx2 strip_vertex(const float4& V, float2 mx, float2 
   return v;
 }
 
+#ifndef NM_NEAR_UNROLL
+#define NM_NEAR_UNROLL 2
+#endif
+constexpr int kNearUnroll = NM_NEAR_UNROLL;
+// use[k]: lane point k takes this group's near result (the caller discards
+// the others), so only those lanes ask for the full-range atan2.
 template <int NP>
 __device__ __forceinline__ void seg_near(const float4* __restrict__ rec, const PairFrame (&f)[NP], float2 (&acc)[NP],
-                                         bool (&det)[2 * NP], float tau, float delta) {
+                                         bool (&det)[2 * NP], const bool (&use)[2 * NP], float tau, float delta) {
   Vtx2 a[NP], b[NP];
   float2 dab[NP];
   {
@@ -267,7 +273,7 @@ __device__ __forceinline__ void seg_near(const float4* __restrict__ rec, const P
       dab[q] = fma2(add2(a[q].q, b[q].q), bc(0.5f), bc(e0));
     }
   }
-#pragma unroll 1
+#pragma unroll kNearUnroll
   for (int k = 0; k < kSegTris; ++k) {
     const float4 V2 = rec[k + 2];
     const float4 T = rec[kSegT + k];
@@ -281,8 +287,23 @@ __device__ __forceinline__ void seg_near(const float4* __restrict__ rec, const P
       num = mul2(num, bc(1.0f / kRecScale));  // exact: the record holds 2N
       const float2 den = fma2(fma2(a[q].r, b[q].r, dab[q]), c.r, fma2(dac, b[q].r, mul2(dbc, a[q].r)));
       const float2 af = acc_far2(acc[q], num, den);
-      acc[q].x = acc_near_lane(acc[q].x, af.x, num.x, den.x, a[q].r.x, b[q].r.x, c.r.x, tau, delta, det[2 * q]);
-      acc[q].y = acc_near_lane(acc[q].y, af.y, num.y, den.y, a[q].r.y, b[q].r.y, c.r.y, tau, delta, det[2 * q + 1]);
+      // |x| <= kFarX with den > 0: the 3-term series (af) is exact to fp32
+      const bool frx = (den.x > 0.0f) && (fabsf(num.x) <= __fmul_rn(kFarX, den.x));
+      const bool fry = (den.y > 0.0f) && (fabsf(num.y) <= __fmul_rn(kFarX, den.y));
+      // near-surface detector
+      const float2 lim = mul2(bc(tau), mul2(mul2(a[q].r, b[q].r), c.r));
+      det[2 * q] |= ((fabsf(num.x) <= lim.x) && (den.x <= lim.x)) || (fminf(a[q].r.x, fminf(b[q].r.x, c.r.x)) <= delta);
+      det[2 * q + 1] |=
+          ((fabsf(num.y) <= lim.y) && (den.y <= lim.y)) || (fminf(a[q].r.y, fminf(b[q].r.y, c.r.y)) <= delta);
+      // full-range atan2 only when some used lane of the warp needs it
+      // (warp-uniform branch; a lane's value never depends on the others)
+      float2 full = acc[q];
+      if (__any_sync(0xffffffffu, (use[2 * q] && !frx) || (use[2 * q + 1] && !fry))) {
+        full.x = __fadd_rn(acc[q].x, atan2_near(num.x, den.x));
+        full.y = __fadd_rn(acc[q].y, atan2_near(num.y, den.y));
+      }
+      acc[q].x = frx ? af.x : full.x;
+      acc[q].y = fry ? af.y : full.y;
       a[q] = b[q];
       b[q] = c;
       dab[q] = dbc;
