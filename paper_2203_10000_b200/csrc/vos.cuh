@@ -253,7 +253,7 @@ __device__ __forceinline__ Vtx2 strip_vertex(const float4& V, float2 mx, float2 
 }
 
 #ifndef NM_NEAR_UNROLL
-#define NM_NEAR_UNROLL 2
+#define NM_NEAR_UNROLL 4
 #endif
 constexpr int kNearUnroll = NM_NEAR_UNROLL;
 // use[k]: lane point k takes this group's near result (the caller discards
