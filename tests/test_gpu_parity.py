@@ -473,3 +473,60 @@ def test_outside_culling_exact():
     np.testing.assert_array_equal(s_cull[~culled], s_full[~culled])
     assert np.max(np.abs(s_full[culled])) < 1e-5
     np.testing.assert_array_equal(s_sub, s_cull[idx])
+
+
+def test_cfg5_full_size_properties():
+    """BASELINE configs[4] at full size (10,077,696 nodes x 983,040 triangles):
+    size-independent properties over every node, the fp64 oracle on a seeded
+    sample.
+      * sample parity: masks bit-exact, |s - s_oracle| <= S_EXPECT;
+      * nesting: the six shells are nested by construction, so shell j's
+        inside bit implies shell j+1's for every node;
+      * determinism: two half-mesh calls reproduce the full call bitwise
+        (results independent of the point set, SPEC.md:265);
+      * exact outside culling (cull_outside=1) changes no bit;
+      * tet labels = id[ffs(AND of the 4 node masks)] on a tet sample."""
+    from paper_2203_10000_b200._native import Context
+    cfg = synth.config(5)
+    S = cfg.surfaces
+    nodes, tets = cfg.lattice_mesh()
+    c = Context(0)
+    c.set_surfaces(S.xyz, S.tri, S.comp_off, S.label_ids)
+    m_all, st = c.label_nodes(nodes)
+    assert st["ties"] == 0
+
+    rng = np.random.default_rng(5)
+    idx = np.sort(rng.choice(nodes.shape[0], 1500, replace=False))
+    m_ref, s_ref = oracle.label_nodes(nodes[idx], S, want_s=True)
+    bad, _ = _compare_masks(m_all[idx], m_ref, s_ref)
+    assert bad == 0
+    s_gpu, _ = c.enclosure(nodes[idx])
+    assert np.max(np.abs(s_gpu - s_ref)) <= S_EXPECT
+
+    shells = [k for k, name in enumerate(S.names) if name.startswith("shell")]
+    assert len(shells) == 6
+    for a, b in zip(shells, shells[1:]):
+        inner = (m_all >> np.uint32(a)) & 1
+        outer = (m_all >> np.uint32(b)) & 1
+        assert np.all(outer >= inner)
+    assert 0 < np.count_nonzero((m_all >> np.uint32(shells[0])) & 1) < nodes.shape[0]
+
+    half = nodes.shape[0] // 2 + 12345
+    m_a, _ = c.label_nodes(nodes[:half])
+    m_b, _ = c.label_nodes(nodes[half:])
+    np.testing.assert_array_equal(np.concatenate([m_a, m_b]), m_all)
+
+    cc = Context(0, cull_outside=1)
+    cc.set_surfaces(S.xyz, S.tri, S.comp_off, S.label_ids)
+    m_cull, _ = cc.label_nodes(nodes)
+    np.testing.assert_array_equal(m_cull, m_all)
+    cc.close()
+
+    labels, _, _ = c.label_mesh(nodes, tets)
+    tidx = rng.choice(tets.shape[0], 200000, replace=False)
+    conj = np.bitwise_and.reduce(m_all[tets[tidx]], axis=1)
+    low = (conj & (~conj + np.uint32(1))).astype(np.float64)  # lowest set bit
+    first = np.where(conj != 0, np.log2(np.maximum(low, 1.0)).astype(np.int64), -1)
+    expect = np.where(first >= 0, S.label_ids[np.maximum(first, 0)], 0)
+    np.testing.assert_array_equal(labels[tidx], expect)
+    c.close()
