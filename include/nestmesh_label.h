@@ -183,6 +183,12 @@ void nm_mesh_free(nm_mesh* m);
 const char* nm_refine_last_error(void);
 int nm_mesh_masks(const nm_mesh* m, uint32_t* masks);
 
+/* Meshes returned by the device entry points below (nm_refine_device,
+ * nm_refine_boundary, nm_refine_relabel) stay in device memory owned by the
+ * handle (stream-ordered pool allocations); nm_mesh_copy / nm_mesh_masks copy
+ * them straight into the caller's buffers and nm_mesh_free releases them.
+ * For nm_refine_relabel with levels = 0, parent is the identity. */
+
 /* refine_volume on the device for a given selection: same rules, numbering
  * and child order as nm_refine (bit-identical result). */
 int nm_refine_device(nm_ctx* ctx, const double* nodes, size_t n_nodes, const uint32_t* tets, size_t nt,

@@ -443,6 +443,21 @@ void check_tets(const std::uint32_t* tets, std::size_t nt, std::size_t n_nodes) 
                                         " >= node count " + std::to_string(n_nodes));
 }
 
+// The same validation on tets already uploaded to d_tets (k_max_index, one
+// word read back); the host scan only runs to name the offending tet.
+void check_tets_device(nm_ctx* c, const std::uint32_t* d_tets, const std::uint32_t* h_tets, std::size_t nt,
+                       std::size_t n_nodes, cudaStream_t st) {
+  if (nt == 0) return;
+  auto* d_word = c->word.as<std::uint32_t>(1);
+  NM_CUDA(cudaMemsetAsync(d_word, 0, sizeof(std::uint32_t), st));
+  nm::k_max_index<<<grid_for(nt, 256, c->sm_count * 8), 256, 0, st>>>(reinterpret_cast<const uint4*>(d_tets), nt,
+                                                                      d_word);
+  NM_CUDA(cudaGetLastError());
+  NM_CUDA(cudaMemcpyAsync(c->h_word, d_word, sizeof(std::uint32_t), cudaMemcpyDeviceToHost, st));
+  NM_CUDA(cudaStreamSynchronize(st));
+  if (*c->h_word >= n_nodes) check_tets(h_tets, nt, n_nodes);
+}
+
 
 // Lexicographic order (k0, k1, k2) of m triples by three stable LSD radix
 // passes; returns the device permutation (valid until the next call).
@@ -618,6 +633,12 @@ int nm_create(nm_ctx** out, const nm_options* opt) {
       for (auto& ev : c->ev) NM_CUDA(cudaEventCreate(&ev));
       NM_CUDA(cudaEventCreateWithFlags(&c->ev_side, cudaEventDisableTiming));
       NM_CUDA(cudaMallocHost(&c->h_word, sizeof(std::uint32_t)));
+      // result meshes are allocated from the device's default pool: keep
+      // freed blocks reserved instead of returning them at every sync
+      cudaMemPool_t pool;
+      NM_CUDA(cudaDeviceGetDefaultMemPool(&pool, c->opt.device));
+      std::uint64_t keep = ~0ull;
+      NM_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
     } catch (...) {
       delete c;
       throw;
@@ -988,13 +1009,14 @@ int nm_label_tets(nm_ctx* c, const std::uint32_t* tets, std::size_t nt, const st
                   std::size_t n_nodes, int* labels_out, nm_stats* stats) {
   return guarded([&] {
     require_surfaces(c);
-    check_tets(tets, nt, n_nodes);
+    if (nt && !tets) throw Error("null tets");
     NM_CUDA(cudaSetDevice(c->opt.device));
     if (stats) std::memset(stats, 0, sizeof *stats);
     auto* d_tets = c->tets.as<std::uint32_t>(4 * std::max<std::size_t>(nt, 1));
     auto* d_masks = c->masks.as<std::uint32_t>(std::max<std::size_t>(n_nodes, 1));
     auto* d_labels = c->labels.as<int>(std::max<std::size_t>(nt, 1));
     if (nt) NM_CUDA(cudaMemcpyAsync(d_tets, tets, 4 * nt * sizeof(std::uint32_t), cudaMemcpyHostToDevice, c->stream));
+    check_tets_device(c, d_tets, tets, nt, n_nodes, c->stream);
     if (n_nodes) NM_CUDA(cudaMemcpyAsync(d_masks, masks, n_nodes * sizeof(std::uint32_t), cudaMemcpyHostToDevice, c->stream));
     label_tets_dev(c, d_tets, nt, d_masks, d_labels, c->stream, stats);
     if (nt) NM_CUDA(cudaMemcpyAsync(labels_out, d_labels, nt * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
@@ -1164,6 +1186,40 @@ struct nm_boundary {
   std::vector<std::uint32_t> tri;    // 3 per triangle, outward from the region, lexicographically sorted
   std::vector<std::uint32_t> nodes;  // sorted, unique
 };
+
+// Device-resident result mesh: fresh device arrays owned by the handle,
+// filled by device-to-device copies (~3 TB/s, so the context keeps its
+// grown scratch buffers for the next call); nm_mesh_copy reads them straight
+// into the caller's arrays. parent == nullptr: identity (no refinement).
+nm_mesh* make_device_mesh(nm_ctx* c, const DBuf& nodes, const DBuf& tets, const DBuf& labels, const DBuf* parent,
+                          const DBuf* masks, std::size_t nn, std::size_t nt, std::size_t n_old, cudaStream_t st) {
+  std::unique_ptr<nm_mesh> m(new nm_mesh);
+  m->n_old = n_old;
+  m->dev.device = c->opt.device;
+  m->dev.nn = nn;
+  m->dev.nt = nt;
+  // stream-ordered pool allocations (nm_create keeps the pool's memory
+  // reserved), so repeated calls do not pay cudaMalloc/cudaFree
+  auto dup = [&](void*& dst, const void* src, std::size_t bytes) {
+    NM_CUDA(cudaMallocAsync(&dst, std::max<std::size_t>(bytes, 256), st));
+    if (bytes) NM_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, st));
+  };
+  dup(m->dev.nodes, nodes.p, 3 * nn * sizeof(double));
+  dup(m->dev.tets, tets.p, 4 * nt * sizeof(std::uint32_t));
+  dup(m->dev.labels, labels.p, nt * sizeof(int));
+  if (parent) {
+    dup(m->dev.parent, parent->p, nt * sizeof(std::uint32_t));
+  } else {
+    NM_CUDA(cudaMallocAsync(&m->dev.parent, std::max<std::size_t>(nt * sizeof(std::uint32_t), 256), st));
+    if (nt) {
+      nm::k_iota<<<grid_for(nt, 256, c->sm_count * 32), 256, 0, st>>>(static_cast<std::uint32_t*>(m->dev.parent), nt);
+      NM_CUDA(cudaGetLastError());
+    }
+  }
+  if (masks) dup(m->dev.masks, masks->p, nn * sizeof(std::uint32_t));
+  NM_CUDA(cudaStreamSynchronize(st));
+  return m.release();
+}
 
 extern "C" {
 
@@ -1511,20 +1567,8 @@ int nm_refine_device(nm_ctx* c, const double* nodes, std::size_t n, const std::u
     if (ns) NM_CUDA(cudaMemcpyAsync(d_sel, selected, ns * sizeof(std::uint32_t), cudaMemcpyHostToDevice, st));
     std::uint64_t l = 0;
     const auto [n2, nt2] = refine_dev(c, d_nodes, n, d_tets, nt, d_labels, d_sel, static_cast<std::uint32_t>(ns), st, l);
-    std::unique_ptr<nm_mesh> res(new nm_mesh);
-    res->n_old = n;
-    res->nodes.resize(3 * n2);
-    res->tets.resize(4 * nt2);
-    res->labels.resize(nt2);
-    res->parent.resize(nt2);
-    if (n2) NM_CUDA(cudaMemcpyAsync(res->nodes.data(), c->meshB_nodes.p, 3 * n2 * sizeof(double), cudaMemcpyDeviceToHost, st));
-    if (nt2) {
-      NM_CUDA(cudaMemcpyAsync(res->tets.data(), c->meshB_tets.p, 4 * nt2 * sizeof(std::uint32_t), cudaMemcpyDeviceToHost, st));
-      NM_CUDA(cudaMemcpyAsync(res->labels.data(), c->meshB_labels.p, nt2 * sizeof(int), cudaMemcpyDeviceToHost, st));
-      NM_CUDA(cudaMemcpyAsync(res->parent.data(), c->meshB_parent.p, nt2 * sizeof(std::uint32_t), cudaMemcpyDeviceToHost, st));
-    }
-    NM_CUDA(cudaStreamSynchronize(st));
-    *out = res.release();
+    *out = make_device_mesh(c, c->meshB_nodes, c->meshB_tets, c->meshB_labels, &c->meshB_parent, nullptr, n2, nt2, n,
+                            st);
   });
 }
 
@@ -1555,20 +1599,8 @@ int nm_refine_boundary(nm_ctx* c, const double* nodes, std::size_t n, const std:
     NM_CUDA(cudaMemcpyAsync(&ns, d_count, sizeof ns, cudaMemcpyDeviceToHost, st));
     NM_CUDA(cudaStreamSynchronize(st));
     const auto [n2, nt2] = refine_dev(c, d_nodes, n, d_tets, nt, d_labels, d_sel, ns, st, l);
-    std::unique_ptr<nm_mesh> res(new nm_mesh);
-    res->n_old = n;
-    res->nodes.resize(3 * n2);
-    res->tets.resize(4 * nt2);
-    res->labels.resize(nt2);
-    res->parent.resize(nt2);
-    if (n2) NM_CUDA(cudaMemcpyAsync(res->nodes.data(), c->meshB_nodes.p, 3 * n2 * sizeof(double), cudaMemcpyDeviceToHost, st));
-    if (nt2) {
-      NM_CUDA(cudaMemcpyAsync(res->tets.data(), c->meshB_tets.p, 4 * nt2 * sizeof(std::uint32_t), cudaMemcpyDeviceToHost, st));
-      NM_CUDA(cudaMemcpyAsync(res->labels.data(), c->meshB_labels.p, nt2 * sizeof(int), cudaMemcpyDeviceToHost, st));
-      NM_CUDA(cudaMemcpyAsync(res->parent.data(), c->meshB_parent.p, nt2 * sizeof(std::uint32_t), cudaMemcpyDeviceToHost, st));
-    }
-    NM_CUDA(cudaStreamSynchronize(st));
-    *out = res.release();
+    *out = make_device_mesh(c, c->meshB_nodes, c->meshB_tets, c->meshB_labels, &c->meshB_parent, nullptr, n2, nt2, n,
+                            st);
   });
 }
 
@@ -1579,7 +1611,7 @@ int nm_refine_relabel(nm_ctx* c, const double* nodes, std::size_t n, const std::
     if (!out) throw Error("null output pointer");
     *out = nullptr;
     require_surfaces(c);
-    check_tets(tets, nt, n);
+    if (nt && !tets) throw Error("null tets");
     if (levels < 0) throw Error("levels must be >= 0");
     NM_CUDA(cudaSetDevice(c->opt.device));
     cudaStream_t st = c->stream;
@@ -1609,6 +1641,7 @@ int nm_refine_relabel(nm_ctx* c, const double* nodes, std::size_t n, const std::
     auto* d_tets = At->as<std::uint32_t>(4 * std::max<std::size_t>(nt, 1));
     if (n) NM_CUDA(cudaMemcpyAsync(d_nodes, nodes, 3 * n * sizeof(double), cudaMemcpyHostToDevice, st));
     if (nt) NM_CUDA(cudaMemcpyAsync(d_tets, tets, 4 * nt * sizeof(std::uint32_t), cudaMemcpyHostToDevice, st));
+    check_tets_device(c, d_tets, tets, nt, n, st);
     auto* d_masks = M->as<std::uint32_t>(std::max<std::size_t>(n, 1));
     if (masks_in) {
       if (n) NM_CUDA(cudaMemcpyAsync(d_masks, masks_in, n * sizeof(std::uint32_t), cudaMemcpyHostToDevice, st));
@@ -1665,24 +1698,8 @@ int nm_refine_relabel(nm_ctx* c, const double* nodes, std::size_t n, const std::
       cn = n2;
       cnt_t = nt2;
     }
-    std::unique_ptr<nm_mesh> res(new nm_mesh);
-    res->nodes.resize(3 * cn);
-    res->tets.resize(4 * cnt_t);
-    res->labels.resize(cnt_t);
-    res->masks.resize(cn);
-    res->parent.resize(cnt_t);
-    res->n_old = n;
-    if (cn) NM_CUDA(cudaMemcpyAsync(res->nodes.data(), An->p, 3 * cn * sizeof(double), cudaMemcpyDeviceToHost, st));
-    if (cnt_t) {
-      NM_CUDA(cudaMemcpyAsync(res->tets.data(), At->p, 4 * cnt_t * sizeof(std::uint32_t), cudaMemcpyDeviceToHost, st));
-      NM_CUDA(cudaMemcpyAsync(res->labels.data(), Al->p, cnt_t * sizeof(int), cudaMemcpyDeviceToHost, st));
-    }
-    if (cn) NM_CUDA(cudaMemcpyAsync(res->masks.data(), M->p, cn * sizeof(std::uint32_t), cudaMemcpyDeviceToHost, st));
-    if (have_parent && cnt_t)
-      NM_CUDA(cudaMemcpyAsync(res->parent.data(), c->meshB_parent.p, cnt_t * sizeof(std::uint32_t), cudaMemcpyDeviceToHost, st));
-    NM_CUDA(cudaStreamSynchronize(st));
     if (stats) stats->triangles = c->nt_real;
-    *out = res.release();
+    *out = make_device_mesh(c, *An, *At, *Al, have_parent ? &c->meshB_parent : nullptr, M, cn, cnt_t, n, st);
   });
 }
 

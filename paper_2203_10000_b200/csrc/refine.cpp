@@ -41,6 +41,8 @@ constexpr int kEdge[6][2] = {{0, 1}, {0, 2}, {0, 3}, {1, 2}, {1, 3}, {2, 3}};
 
 #include "refine.h"
 
+#include <cuda_runtime.h>
+
 namespace {
 thread_local std::string g_refine_err;
 }  // namespace
@@ -254,14 +256,24 @@ int nm_refine(const double* nodes, std::size_t n, const std::uint32_t* tets, std
 
 int nm_mesh_sizes(const nm_mesh* m, std::size_t* n_nodes, std::size_t* n_tets, std::size_t* n_old_nodes) {
   if (!m) return 1;
-  if (n_nodes) *n_nodes = m->nodes.size() / 3;
-  if (n_tets) *n_tets = m->tets.size() / 4;
+  if (n_nodes) *n_nodes = m->node_count();
+  if (n_tets) *n_tets = m->tet_count();
   if (n_old_nodes) *n_old_nodes = m->n_old;
   return 0;
 }
 
 int nm_mesh_copy(const nm_mesh* m, double* nodes, std::uint32_t* tets, int* labels, std::uint32_t* parent) {
   if (!m) return 1;
+  if (m->dev.device >= 0) {
+    const auto& d = m->dev;
+    if (cudaSetDevice(d.device) != cudaSuccess) return 1;
+    auto get = [](void* dst, const void* src, std::size_t bytes) {
+      return !dst || !bytes || (src && cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToHost) == cudaSuccess);
+    };
+    const bool ok = get(nodes, d.nodes, 3 * d.nn * sizeof(double)) && get(tets, d.tets, 4 * d.nt * sizeof(std::uint32_t)) &&
+                    get(labels, d.labels, d.nt * sizeof(int)) && get(parent, d.parent, d.nt * sizeof(std::uint32_t));
+    return ok ? 0 : 1;
+  }
   if (nodes) std::memcpy(nodes, m->nodes.data(), m->nodes.size() * sizeof(double));
   if (tets) std::memcpy(tets, m->tets.data(), m->tets.size() * sizeof(std::uint32_t));
   if (labels) std::memcpy(labels, m->labels.data(), m->labels.size() * sizeof(int));
@@ -312,9 +324,27 @@ int nm_sample_surface(const double* xyz, const std::uint32_t* tri, std::size_t n
 }
 
 int nm_mesh_masks(const nm_mesh* m, std::uint32_t* masks) {
-  if (!m || m->masks.size() != m->nodes.size() / 3) return 1;
+  if (!m) return 1;
+  if (m->dev.device >= 0) {
+    if (!m->dev.masks || cudaSetDevice(m->dev.device) != cudaSuccess) return 1;
+    return m->dev.nn && cudaMemcpy(masks, m->dev.masks, m->dev.nn * sizeof(std::uint32_t), cudaMemcpyDeviceToHost) !=
+                            cudaSuccess
+               ? 1
+               : 0;
+  }
+  if (m->masks.size() != m->nodes.size() / 3) return 1;
   std::memcpy(masks, m->masks.data(), m->masks.size() * sizeof(std::uint32_t));
   return 0;
 }
 
 }  // extern "C"
+
+nm_mesh::~nm_mesh() {
+  if (dev.device < 0) return;
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(dev.device);
+  for (void* p : {dev.nodes, dev.tets, dev.labels, dev.parent, dev.masks})
+    if (p) cudaFreeAsync(p, cudaStreamLegacy);  // pool memory; every use completed before the handle was returned
+  cudaSetDevice(prev);
+}
