@@ -113,6 +113,11 @@ struct LabelParams {
                               // (k_cull_mask); nullptr = off
   double* s_out;             // n*K or nullptr
   unsigned long long* counters;  // [0] near / [1] far visits of (warp, 8-triangle group)
+  // Compartment split (gridDim.y > 1): CTA row y handles compartments
+  // [split[y], split[y+1]) of its points and ORs its bits into masks /
+  // flagmask (zeroed by k_zero_masks). Each (point, compartment) sum is still
+  // one CTA's fixed-order loop, so results do not depend on the split.
+  int split[33];
 };
 
 // NP point pairs per thread (2*NP points), packed fp32x2 arithmetic.
@@ -186,10 +191,11 @@ __global__ void __launch_bounds__(kBlock, (NP == 1 ? NM_MIN_BLOCKS : NM_MIN_BLOC
     __syncthreads();
     skip = s_skip;
   }
+  const int c_lo = prm.split[blockIdx.y], c_hi = prm.split[blockIdx.y + 1];
   // producer state (thread 0): next tile to fetch and its compartment
   int pf_c = 0, pf_t = -1;
-  auto pf_seek = [&](int c) {  // first tile of the first non-skipped, non-empty compartment >= c
-    for (; c < prm.K; ++c)
+  auto pf_seek = [&](int c) {  // first tile of the first non-skipped, non-empty compartment in [c, c_hi)
+    for (; c < c_hi; ++c)
       if (!((skip >> c) & 1u) && prm.comp_tiles[c] < prm.comp_tiles[c + 1]) {
         pf_c = c;
         pf_t = static_cast<int>(prm.comp_tiles[c]);
@@ -204,13 +210,13 @@ __global__ void __launch_bounds__(kBlock, (NP == 1 ? NM_MIN_BLOCKS : NM_MIN_BLOC
     bulk_g2s(s_sub_buf[b], prm.sub + static_cast<std::size_t>(pf_t) * kSubF4Tile, kSubF4Tile * 16u, &s_bar[b]);
   };
   if (threadIdx.x == 0) {
-    pf_seek(0);
+    pf_seek(c_lo);
     if (pf_t >= 0) pf_issue(0);
   }
   unsigned it = 0;
 
-  int tile = prm.comp_tiles[0];
-  for (int c = 0; c < prm.K; ++c) {
+  int tile = prm.comp_tiles[c_lo];
+  for (int c = c_lo; c < c_hi; ++c) {
     const int tile_end = prm.comp_tiles[c + 1];
     double acc64[P];
     bool det[P];
@@ -372,8 +378,13 @@ __global__ void __launch_bounds__(kBlock, (NP == 1 ? NM_MIN_BLOCKS : NM_MIN_BLOC
 #pragma unroll
   for (int k = 0; k < P; ++k) {
     if (valid[k]) {
-      prm.masks[pid[k]] = mask[k];
-      prm.flagmask[pid[k]] = fmask[k];
+      if (gridDim.y == 1) {
+        prm.masks[pid[k]] = mask[k];
+        prm.flagmask[pid[k]] = fmask[k];
+      } else {
+        if (mask[k]) atomicOr(prm.masks + pid[k], mask[k]);
+        if (fmask[k]) atomicOr(prm.flagmask + pid[k], fmask[k]);
+      }
     }
   }
   if ((threadIdx.x & 31) == 0 && prm.counters) {
@@ -900,6 +911,18 @@ __global__ void k_cull_mask(const double* pts, const std::uint32_t* order, std::
       if (o) m |= 1u << c;
     }
     out[i] = m;
+  }
+}
+
+// masks / flagmask of the evaluated points cleared before a compartment-split
+// k_label launch (which ORs its bits in).
+__global__ void k_zero_masks(std::size_t n, const std::uint32_t* subset, std::uint32_t* masks,
+                             std::uint32_t* flagmask) {
+  for (std::size_t i = blockIdx.x * static_cast<std::size_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<std::size_t>(gridDim.x) * blockDim.x) {
+    const std::size_t j = subset ? subset[i] : i;
+    masks[j] = 0u;
+    flagmask[j] = 0u;
   }
 }
 

@@ -218,6 +218,7 @@ struct nm_ctx {
   double cx = 0, cy = 0, cz = 0;
   double lo[3] = {0, 0, 0}, span = 1.0;  // Morton box of the domain
   nm::LabelIds ids{};
+  std::vector<std::uint32_t> comp_tiles_h;  // host copy of the K+1 tile offsets
   DBuf tri, sub, comp_tiles, xyz64, tri_idx, comp_off, comp_box, cullmask;
 
   // scratch
@@ -276,6 +277,33 @@ void select(nm_ctx* c, Pred pred, std::size_t n, std::uint32_t* out, std::uint32
 // d_subset (nullable): evaluate only points d_pts[d_subset[i]], i < n; masks
 // (and s) are written at the original point index.
 void read_node_stats(nm_ctx* c, std::size_t n, cudaStream_t st, nm_stats* stats);
+
+// Compartment split of a k_label launch (LabelParams::split): when the point
+// blocks alone fill fewer than kSplitWaves waves of resident CTAs (few
+// points: small meshes, many GPUs, refinement passes), the compartments are
+// cut into up to K contiguous groups of about equal tile count so the grid
+// has enough CTAs to keep every SM busy to the end. Returns the group count.
+int compartment_split(const nm_ctx* c, std::size_t nblocks, int* split) {
+  constexpr double kSplitWaves = 24.0;
+  const int K = c->K;
+  const double slots = double(c->sm_count) * NM_MIN_BLOCKS;
+  int want = 1;
+  if (K > 1 && nblocks > 0 && double(nblocks) < kSplitWaves * slots)
+    want = static_cast<int>(std::min<double>(K, std::ceil(kSplitWaves * slots / double(nblocks))));
+  const auto& t = c->comp_tiles_h;
+  const double total = double(t[K] - t[0]);
+  int g = 0;
+  split[g++] = 0;
+  for (int j = 1; j < want; ++j) {
+    const double target = total * j / want;
+    int b = split[g - 1] + 1;
+    while (b < K && double(t[b] - t[0]) < target) ++b;
+    if (b >= K) break;
+    split[g++] = b;
+  }
+  split[g] = K;
+  return g;
+}
 
 // stats_deferred: the caller collects the stats later with read_node_stats
 // (no host synchronisation inside; nm_label_mesh overlaps the tet upload).
@@ -346,11 +374,17 @@ void label_nodes_dev(nm_ctx* c, const double* d_pts, std::size_t n, double T, st
   }
   prm.s_out = d_s;
   prm.counters = counters;
+  const int np = prm.cull ? 1 : c->opt.pairs_per_thread;
+  const std::size_t per_block = static_cast<std::size_t>(nm::kBlock) * 2 * np;
+  const std::size_t nblocks = (n + per_block - 1) / per_block;
+  const int csplit = compartment_split(c, nblocks, prm.split);
+  if (csplit > 1) {
+    nm::k_zero_masks<<<grid_for(n, 256, c->sm_count * 16), 256, 0, st>>>(n, d_subset, d_masks, flagmask);
+    ++launches;
+  }
   if (stats) NM_CUDA(cudaEventRecord(c->ev[1], st));
   {
-    const int np = prm.cull ? 1 : c->opt.pairs_per_thread;
-    const std::size_t per_block = static_cast<std::size_t>(nm::kBlock) * 2 * np;
-    const unsigned grid = static_cast<unsigned>((n + per_block - 1) / per_block);
+    const dim3 grid(static_cast<unsigned>(nblocks), static_cast<unsigned>(csplit));
     constexpr std::size_t smem = 0;  // k_label's tile buffers are static shared memory
     if (c->strips && prm.cull) {
       nm::k_label<1, true, true><<<grid, nm::kBlock, smem, st>>>(prm);  // culling: one pair per thread
@@ -931,6 +965,7 @@ int nm_set_surfaces(nm_ctx* c, const double* xyz, std::size_t nv, const std::uin
     up(c->comp_box, hbox.data(), hbox.size() * sizeof(float4));
     NM_CUDA(cudaStreamSynchronize(c->stream));
     c->K = K;
+    c->comp_tiles_h = tiles;
     c->nt_real = nt;
     c->nt_pad = npad;
     c->nv = nv;

@@ -502,6 +502,15 @@ def test_cfg5_full_size_properties():
     assert bad == 0
     s_gpu, _ = c.enclosure(nodes[idx])
     assert np.max(np.abs(s_gpu - s_ref)) <= S_EXPECT
+    # a 1,500-point call runs with the compartments split over 12 CTA rows,
+    # the 10M-point call without: bitwise the same masks and s
+    m_sub, _ = c.label_nodes(nodes[idx])
+    np.testing.assert_array_equal(m_sub, m_all[idx])
+    head = 4_000_000
+    s_head, _ = c.enclosure(nodes[:head])
+    sel = idx < head
+    np.testing.assert_array_equal(s_gpu[sel], s_head[idx[sel]])
+    del s_head
 
     shells = [k for k, name in enumerate(S.names) if name.startswith("shell")]
     assert len(shells) == 6
