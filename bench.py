@@ -43,6 +43,7 @@ OPS_PER_EVAL = 57                      # pinned FP32-pipe cost o
 ISSUED_OPS_PER_EVAL = 20.125           # FP32 lane-ops the strip far evaluator issues per eval (SASS)
 FP32_LANES_PER_SM = 128
 MY_KERNELS_PER_STEP = 7                # morton keys, k_label, 3x select, k_fixup, k_label_tets
+CUB_KERNELS = 4                        # library radix-sort kernels counted in nm_stats.launches
 
 
 def measured_peaks():
@@ -475,7 +476,9 @@ def main():
             "config": dict(workload_config(cfg, n, nt, world), distributed=use_dist),
             "full_mesh_labeling_time_s": ms_per_step / 1e3,
             "e2e": e2e, "roofline": roof, "cpu_baseline": cpu, "clocks": clocks,
-            "gpu_launches": MY_KERNELS_PER_STEP * args.steps,
+            # this repo's kernels per step: the node pass's launches minus the 4
+            # CUB radix-sort kernels, plus k_label_tets
+            "gpu_launches": (int(last.get("launches", MY_KERNELS_PER_STEP + 3)) - CUB_KERNELS + 1) * args.steps,
             "labeling_stats_last_step": {k: last[k] for k in ("flagged_points", "flagged_pairs", "ties", "near_subtiles",
                                                               "far_subtiles", "ms_label", "ms_fixup")},
             "lattice_generation_s": gen_s, "timed_wall_s": wall,
