@@ -100,6 +100,7 @@ struct LabelParams {
   const std::uint32_t* order;  // evaluation order (Morton); nullptr = identity
   const float4* tri;         // soup: 3 float4 per triangle (a.xyz,N.x) (b.xyz,N.y) (c.xyz,N.z);
                              // strip: kSegF4 float4 per 8-triangle segment (vos.cuh)
+  const float4* edges;       // strip layout: kEdgeF4 float4 of -|e|^2 per segment (near evaluator)
   const float4* sub;         // per subtile: fp32 centre c (centred frame), w = (far radius)^2;
                              // the subtile's vertices are stored relative to c
   const std::uint32_t* comp_tiles;  // K+1 tile offsets
@@ -307,7 +308,9 @@ __global__ void __launch_bounds__(kBlock, (NP == 1 ? NM_MIN_BLOCKS : NM_MIN_BLOC
                   dn[k] = false;
                   use[k] = valid[k] && !gf[k];
                 }
-                seg_near<NP>(rec, f, an, dn, use, prm.tau, prm.delta);
+                const float4* erec =
+                    prm.edges + ((static_cast<std::size_t>(tile) * kSubPerTile + st) * kGroups + g) * kEdgeF4;
+                seg_near<NP>(rec, erec, f, an, dn, use, prm.tau, prm.delta);
                 if (__any_sync(kFull, any)) {
                   float2 af[NP];
 #pragma unroll

@@ -219,7 +219,7 @@ struct nm_ctx {
   double lo[3] = {0, 0, 0}, span = 1.0;  // Morton box of the domain
   nm::LabelIds ids{};
   std::vector<std::uint32_t> comp_tiles_h;  // host copy of the K+1 tile offsets
-  DBuf tri, sub, comp_tiles, xyz64, tri_idx, comp_off, comp_box, cullmask;
+  DBuf tri, sub, edges, comp_tiles, xyz64, tri_idx, comp_off, comp_box, cullmask;
 
   // scratch
   DBuf pts, masks, flagmask, nbr, known, want, fkeys, frontier, lex, region, bfaces, btri, dist_tri, dist_xyz,
@@ -229,7 +229,7 @@ struct nm_ctx {
       s_out, word;
 
   ~nm_ctx() {
-    for (DBuf* b : {&tri, &sub, &comp_tiles, &xyz64, &tri_idx, &comp_off, &comp_box, &cullmask, &pts, &masks, &flagmask, &nbr, &known, &want, &fkeys, &frontier, &lex, &region, &bfaces, &btri,
+    for (DBuf* b : {&tri, &sub, &edges, &comp_tiles, &xyz64, &tri_idx, &comp_off, &comp_box, &cullmask, &pts, &masks, &flagmask, &nbr, &known, &want, &fkeys, &frontier, &lex, &region, &bfaces, &btri,
                     &dist_tri, &dist_xyz, &dist_idx, &dist_d32, &dist_out, &r_red, &r_keys, &r_keys2, &r_S,
                     &r_idx, &r_touched, &r_mask, &r_cnt, &r_offs, &r_flag, &meshA_nodes, &meshA_tets, &meshA_labels,
                     &meshB_nodes, &meshB_tets, &meshB_labels, &meshB_parent, &masks2, &order, &keys,
@@ -353,6 +353,7 @@ void label_nodes_dev(nm_ctx* c, const double* d_pts, std::size_t n, double T, st
   prm.order = order;
   prm.tri = static_cast<const float4*>(c->tri.p);
   prm.sub = static_cast<const float4*>(c->sub.p);
+  prm.edges = static_cast<const float4*>(c->edges.p);
   prm.comp_tiles = static_cast<const std::uint32_t*>(c->comp_tiles.p);
   prm.K = c->K;
   prm.cx = c->cx;
@@ -804,6 +805,7 @@ int nm_set_surfaces(nm_ctx* c, const double* xyz, std::size_t nv, const std::uin
     const std::size_t tile_f4 = static_cast<std::size_t>(sub_f4) * nm::kSubPerTile;
     std::vector<float4> htri(ntiles * tile_f4);
     std::vector<float4> hsub(ntiles * nm::kSubPerTile * nm::kSubRec);
+    std::vector<float4> hedge(use_strips ? ntiles * nm::kSubPerTile * nm::kGroups * nm::kEdgeF4 : 1);
     const double far_ratio = c->opt.far_ratio, far_abs = c->opt.far_abs_mm;
     // Each 32-triangle subtile carries an fp32 centre c (exactly representable
     // in the centred frame) and its vertices relative to c, so near-surface
@@ -872,20 +874,36 @@ int nm_set_surfaces(nm_ctx* c, const double* xyz, std::size_t nv, const std::uin
                 const float sc = nm::kRecScale;
                 r[nm::kSegT + q] = make_float4(sc * nf[0], sc * nf[1], sc * nf[2], sc * float(w));
               }
-              // -kRecScale |e|^2/2 = -|e|^2 of the consecutive (k,k+1) and skip (k,k+2) edges
-              float E[4 * (nm::kSegF4 - nm::kSegE)] = {0};
+              // -(vertex dot products) of each triangle (far evaluator, vos.cuh)
+              auto dot3 = [&](int o, int i, int jj) {  // (v_i - v_o).(v_jj - v_o), fp64
+                double acc = 0;
+                for (int a = 0; a < 3; ++a)
+                  acc += (double(rv[3 * i + a]) - double(rv[3 * o + a])) * (double(rv[3 * jj + a]) - double(rv[3 * o + a]));
+                return acc;
+              };
+              float C[4 * (nm::kSegF4 - nm::kSegC)] = {0};
+              for (int q = 0; q < nm::kSegTris; ++q) {
+                const int ia = q, ib = q + 1, ic = q + 2;
+                C[3 * q] = float(-dot3(ic, ia, ib));      // alpha at c
+                C[3 * q + 1] = float(-dot3(ia, ib, ic));  // beta at a
+                C[3 * q + 2] = float(-dot3(ib, ia, ic));  // gamma at b
+              }
+              for (int q = 0; q < nm::kSegF4 - nm::kSegC; ++q)
+                r[nm::kSegC + q] = make_float4(C[4 * q], C[4 * q + 1], C[4 * q + 2], C[4 * q + 3]);
+              // -|e|^2 of the consecutive (k,k+1) and skip (k,k+2) edges (near evaluator)
+              float E[4 * nm::kEdgeF4] = {0};
               auto e2 = [&](int i, int jj) {
                 double s2 = 0;
                 for (int a = 0; a < 3; ++a) {
                   const double d = double(rv[3 * jj + a]) - double(rv[3 * i + a]);
                   s2 += d * d;
                 }
-                return float(-0.5 * nm::kRecScale * s2);
+                return float(-s2);
               };
               for (int q = 0; q <= nm::kSegTris; ++q) E[q] = e2(q, q + 1);
               for (int q = 0; q < nm::kSegTris; ++q) E[nm::kSegSkip + q] = e2(q, q + 2);
-              for (int q = 0; q < nm::kSegF4 - nm::kSegE; ++q)
-                r[nm::kSegE + q] = make_float4(E[4 * q], E[4 * q + 1], E[4 * q + 2], E[4 * q + 3]);
+              float4* er = &hedge[((static_cast<std::size_t>(tl) * nm::kSubPerTile + sidx) * nm::kGroups + j) * nm::kEdgeF4];
+              for (int q = 0; q < nm::kEdgeF4; ++q) er[q] = make_float4(E[4 * q], E[4 * q + 1], E[4 * q + 2], E[4 * q + 3]);
             } else {
               double N[3] = {0, 0, 0};
               if (u < nreal) normal64(order[k][u], N);
@@ -930,6 +948,7 @@ int nm_set_surfaces(nm_ctx* c, const double* xyz, std::size_t nv, const std::uin
     };
     up(c->tri, htri.data(), htri.size() * sizeof(float4));
     up(c->sub, hsub.data(), hsub.size() * sizeof(float4));
+    up(c->edges, hedge.data(), hedge.size() * sizeof(float4));
     up(c->comp_tiles, tiles.data(), tiles.size() * sizeof(std::uint32_t));
     up(c->xyz64, xyz, nv * 3 * sizeof(double));
     up(c->tri_idx, tri, nt * 3 * sizeof(std::uint32_t));

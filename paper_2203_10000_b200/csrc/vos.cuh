@@ -121,19 +121,26 @@ __device__ __forceinline__ float acc_near_lane(float acc, float a_far, float num
 //                                                        original triangle, so num_k
 //                                                        carries the outward orientation
 //                                                        whatever the strip's winding parity
-//   rec[18..22] -|e|^2 of the 9 consecutive (k,k+1) and 8 skip (k,k+2) edges
-// The factor 2 on T and on |e|^2 is an exact power-of-two scaling: the far
-// evaluator works with (2 num, 2 den), the near one scales back exactly.
+//   rec[18..23] C_k  = -(alpha_k, beta_k, gamma_k)       the vertex dot products of
+//                                                        triangle k (a, b, c = u_k,
+//                                                        u_{k+1}, u_{k+2}): alpha =
+//                                                        (a-c).(b-c), beta = (b-a).(c-a),
+//                                                        gamma = (a-b).(c-b)
+// plus, in a separate global array read only by the near evaluator, -|e|^2
+// of the 9 consecutive (k,k+1) and 8 skip (k,k+2) edges (kEdgeF4 float4).
+// The factor 2 on T is an exact power-of-two scaling: the far evaluator
+// works with (2 num, 2 den), the near one scales back exactly.
 //
 // Two evaluators share the record:
 //   far  (a point at >= 4 rho + 0.05 mm from the centre of the group's
 //        bounding ball of radius rho):
 //        q = |V|^2 + |p|^2 - 2 V.p  (4 ops, no R vector), num = N.V - N.p,
-//        2 den = (r_a + r_b)(r_b + r_c)(r_c + r_a) - |e_ab|^2 r_c - |e_ac|^2 r_b - |e_bc|^2 r_a,
+//        2 den = u v w - alpha u - beta v - gamma w  (u = r_a + r_b, v = r_b + r_c,
+//                w = r_a + r_c) = w (u v - gamma) - alpha u - beta v,
 //        per triangle |Omega/2| <= pi (1 - sqrt(1 - 1/16)) = 0.1004 rad there
 //        (spherical-cap bound), so a consecutive pair's half-angle sum stays
 //        <= 0.2 rad and its 3-term series (after the complex product below)
-//        truncates at < x^9/9 = 6e-8 rad: 20 FP32 lane-ops + 1.75 MUFU;
+//        truncates at < x^9/9 = 6e-8 rad: 19 FP32 lane-ops + 1.75 MUFU;
 //   near R-based terms, R_a.R_b = (q_a + q_b)/2 - |e_ab|^2/2 (exact to
 //        ~ulp(|R|)), 3-term series for |x| <= 0.125 else full-range atan2,
 //        plus the near-surface detector.
@@ -146,15 +153,20 @@ __device__ __forceinline__ float acc_near_lane(float acc, float a_far, float num
 #endif
 constexpr int kSegTris = NM_SEG_TRIS;               // triangles per segment
 constexpr int kSegT = kSegTris + 2;                 // first T_k (after the vertices)
-constexpr int kSegE = kSegT + kSegTris;             // first edge float4
-constexpr int kSegSkip = kSegTris + 1;              // first skip edge (k, k+2)
-constexpr int kSegF4 = kSegE + (2 * kSegTris + 1 + 3) / 4;  // 23 float4 for 8 triangles
-constexpr float kRecScale = 2.0f;  // T_k and -|e|^2 scaling of the record (host packing)
+constexpr int kSegC = kSegT + kSegTris;             // first vertex-dot coefficient float4
+constexpr int kSegF4 = kSegC + (3 * kSegTris + 3) / 4;  // 24 float4 for 8 triangles
+constexpr int kSegSkip = kSegTris + 1;              // first skip edge (k, k+2) of the edge record
+constexpr int kEdgeF4 = (2 * kSegTris + 1 + 3) / 4;  // near-evaluator edge record, float4 per segment
+constexpr float kRecScale = 2.0f;  // T_k scaling of the record (host packing)
 
-__device__ __forceinline__ float edge_val(const float4* rec, int idx) {
-  const float4 v = rec[kSegE + (idx >> 2)];
-  const int c = idx & 3;
+__device__ __forceinline__ float f4_at(const float4& v, int c) {
   return c == 0 ? v.x : c == 1 ? v.y : c == 2 ? v.z : v.w;
+}
+// -(vertex dot) coefficient i of the segment (3 per triangle), shared memory
+__device__ __forceinline__ float coef_val(const float4* rec, int idx) { return f4_at(rec[kSegC + (idx >> 2)], idx & 3); }
+// -|e|^2 of edge idx from the segment's edge record in global memory (near path only)
+__device__ __forceinline__ float edge_val(const float4* __restrict__ erec, int idx) {
+  return f4_at(__ldg(erec + (idx >> 2)), idx & 3);
 }
 
 // Per point pair, in the subtile frame: m = -(p - c); sp = |p - c|^2.
@@ -190,10 +202,12 @@ __device__ __forceinline__ float2 atan_far3(float2 acc, float2 num, float2 den) 
 // Denominator: with 2 R_a.R_b = r_a^2 + r_b^2 - |e_ab|^2 the VOS denominator
 // 2 den = 2 r_a r_b r_c + 2 (R_a.R_b r_c + R_a.R_c r_b + R_b.R_c r_a)
 // regroups through (r_a + r_b)(r_b + r_c)(r_c + r_a) = sum_sym r_a^2 r_b +
-// 2 r_a r_b r_c into the product form above. Far away r ~ d >> |e|, so the
-// product (~8 d^3) dominates without cancellation, and the edge terms are
-// FFMA2s with a broadcast operand: 7 ops per triangle where the edge-dot form
-// takes 8, and no |R|^2 is carried between triangles.
+// 2 r_a r_b r_c into u v w - |e_ab|^2 r_c - |e_ac|^2 r_b - |e_bc|^2 r_a, and
+// substituting r_c = (v + w - u)/2 etc. into the edge terms gives
+// u v w - alpha u - beta v - gamma w with the triangle's vertex dot products
+// (host constants). Far away r ~ d >> |e|, so u v w (~8 d^3) dominates without
+// cancellation: v, w, fma(u, v, -gamma), the alpha/beta terms (2, broadcast
+// operands) and one fma = 6 ops per triangle, u carried from the previous one.
 // Angle: consecutive triangles are combined pairwise through the complex
 // product (den0 + i num0)(den1 + i num1), whose argument is the sum of the two
 // half-angles (each <= 0.1004 rad far away, so the sum stays in the 3-term
@@ -212,14 +226,14 @@ __device__ __forceinline__ void seg_far(const float4* __restrict__ rec, const Pa
   for (int k = 0; k < kSegTris; ++k) {
     const float4 V2 = rec[k + 2];
     const float4 T = rec[kSegT + k];
-    const float eab = edge_val(rec, k), ebc = edge_val(rec, k + 1), eac = edge_val(rec, kSegSkip + k);
+    const float ca = coef_val(rec, 3 * k), cb = coef_val(rec, 3 * k + 1), cg = coef_val(rec, 3 * k + 2);
 #pragma unroll
     for (int q = 0; q < NP; ++q) {
       const float2 rc = far_dist(V2, f[q]);
-      const float2 sbc = add2(rb[q], rc);
-      const float2 sac = add2(ra[q], rc);
-      const float2 prod = mul2(mul2(sab[q], sbc), sac);
-      const float2 den = fma2(bc(eab), rc, fma2(bc(eac), rb[q], fma2(bc(ebc), ra[q], prod)));  // 2 den
+      const float2 sbc = add2(rb[q], rc);  // v
+      const float2 sac = add2(ra[q], rc);  // w
+      const float2 x = fma2(sab[q], sbc, bc(cg));  // u v - gamma
+      const float2 den = fma2(x, sac, fma2(bc(ca), sab[q], mul2(bc(cb), sbc)));  // 2 den
       const float2 num = fma2(bc(T.x), f[q].mx, fma2(bc(T.y), f[q].my, fma2(bc(T.z), f[q].mz, bc(T.w))));  // 2 num
       if (k & 1) {
         const float2 D = fma2(d0[q], den, mul2(make_float2(-n0[q].x, -n0[q].y), num));
@@ -259,13 +273,14 @@ constexpr int kNearUnroll = NM_NEAR_UNROLL;
 // use[k]: lane point k takes this group's near result (the caller discards
 // the others), so only those lanes ask for the full-range atan2.
 template <int NP>
-__device__ __forceinline__ void seg_near(const float4* __restrict__ rec, const PairFrame (&f)[NP], float2 (&acc)[NP],
-                                         bool (&det)[2 * NP], const bool (&use)[2 * NP], float tau, float delta) {
+__device__ __forceinline__ void seg_near(const float4* __restrict__ rec, const float4* __restrict__ erec,
+                                         const PairFrame (&f)[NP], float2 (&acc)[NP], bool (&det)[2 * NP],
+                                         const bool (&use)[2 * NP], float tau, float delta) {
   Vtx2 a[NP], b[NP];
   float2 dab[NP];
   {
     const float4 V0 = rec[0], V1 = rec[1];
-    const float e0 = 0.5f * edge_val(rec, 0);
+    const float e0 = 0.5f * edge_val(erec, 0);
 #pragma unroll
     for (int q = 0; q < NP; ++q) {
       a[q] = strip_vertex(V0, f[q].mx, f[q].my, f[q].mz);
@@ -277,7 +292,7 @@ __device__ __forceinline__ void seg_near(const float4* __restrict__ rec, const P
   for (int k = 0; k < kSegTris; ++k) {
     const float4 V2 = rec[k + 2];
     const float4 T = rec[kSegT + k];
-    const float ebc = 0.5f * edge_val(rec, k + 1), eac = 0.5f * edge_val(rec, kSegSkip + k);  // -|e|^2/2, exact
+    const float ebc = 0.5f * edge_val(erec, k + 1), eac = 0.5f * edge_val(erec, kSegSkip + k);  // -|e|^2/2, exact
 #pragma unroll
     for (int q = 0; q < NP; ++q) {
       const Vtx2 c = strip_vertex(V2, f[q].mx, f[q].my, f[q].mz);
