@@ -40,7 +40,7 @@ sys.path.insert(0, str(ROOT))
 METRIC = "point-triangle solid-angle evals/sec and full-mesh labeling time at 1/2/4/8 B200"
 UNIT = "evals/s"
 OPS_PER_EVAL = 57                      # pinned FP32-pipe cost of one VOS eval
-ISSUED_OPS_PER_EVAL = 19.125           # FP32 lane-ops the strip far evaluator issues per eval (SASS)
+ISSUED_OPS_PER_EVAL = 18.625           # FP32 lane-ops the strip far evaluator issues per eval (SASS)
 FP32_LANES_PER_SM = 128
 MY_KERNELS_PER_STEP = 7                # morton keys, k_label, 3x select, k_fixup, k_label_tets
 CUB_KERNELS = 4                        # library radix-sort kernels counted in nm_stats.launches
@@ -461,7 +461,7 @@ def main():
                           f" / {OPS_PER_EVAL} FP32-pipe ops per eval (SURVEY.md §8d); per GPU",
             "kernel_ms_avg": k_ms, "kernel_share_of_step": k_ms / (sum(step_ms) / len(step_ms)),
             # the same kernel against the FP32 ops it actually issues per eval
-            # (far evaluator: 19.125 lane-ops; SASS count in DESIGN.md §3)
+            # (far evaluator: 18.625 lane-ops; SASS count in DESIGN.md §3)
             "issued_fp32_ops_per_eval": ISSUED_OPS_PER_EVAL if layout == "strips" else 40.0,
             "frac_of_issued_fp32_bound": achieved / (sms * FP32_LANES_PER_SM * sm_max * 1e6 /
                                                      (ISSUED_OPS_PER_EVAL if layout == "strips" else 40.0)),

@@ -139,8 +139,9 @@ __device__ __forceinline__ float acc_near_lane(float acc, float a_far, float num
 //                w = r_a + r_c) = w (u v - gamma) - alpha u - beta v,
 //        per triangle |Omega/2| <= pi (1 - sqrt(1 - 1/16)) = 0.1004 rad there
 //        (spherical-cap bound), so a consecutive pair's half-angle sum stays
-//        <= 0.2 rad and its 3-term series (after the complex product below)
-//        truncates at < x^9/9 = 6e-8 rad: 19 FP32 lane-ops + 1.75 MUFU;
+//        <= 0.2 rad, where a 3-coefficient minimax odd polynomial (after the
+//        complex product below) is within 4.9e-8 rad: 18.6 FP32 lane-ops +
+//        1.75 MUFU;
 //   near R-based terms, R_a.R_b = (q_a + q_b)/2 - |e_ab|^2/2 (exact to
 //        ~ulp(|R|)), 3-term series for |x| <= 0.125 else full-range atan2,
 //        plus the near-surface detector.
@@ -190,11 +191,14 @@ __device__ __forceinline__ float2 far_dist(const float4& V, const PairFrame& f) 
   return make_float2(sqrt_approx(q.x), sqrt_approx(q.y));
 }
 
-// atan(N/D) for |N/D| <= tan(0.2): 3-term odd series (truncation x^9/9 < 7e-8 rad).
+// atan(N/D) for |N/D| <= tan(0.2): x (1 + c1 x^2 + c2 x^4), minimax on
+// [0, tan 0.2] with the linear term pinned to 1 (exact for small x): max
+// error 4.9e-8 rad (6.2e-8 evaluated in fp32), below the 4-term Taylor
+// series' 6.2e-8 (7.4e-8) at one FMA less.
 __device__ __forceinline__ float2 atan_far3(float2 acc, float2 num, float2 den) {
   const float2 x = mul2(num, make_float2(rcp_approx(den.x), rcp_approx(den.y)));
   const float2 y = mul2(x, x);
-  const float2 p = fma2(fma2(fma2(bc(-0.142857142857f), y, bc(0.2f)), y, bc(-0.333333333333f)), y, bc(1.0f));
+  const float2 p = fma2(fma2(bc(0.1915847659111023f), y, bc(-0.3332153856754303f)), y, bc(1.0f));
   return fma2(x, p, acc);
 }
 
@@ -210,8 +214,9 @@ __device__ __forceinline__ float2 atan_far3(float2 acc, float2 num, float2 den) 
 // operands) and one fma = 6 ops per triangle, u carried from the previous one.
 // Angle: consecutive triangles are combined pairwise through the complex
 // product (den0 + i num0)(den1 + i num1), whose argument is the sum of the two
-// half-angles (each <= 0.1004 rad far away, so the sum stays in the 3-term
-// series' range and the real part stays > 0): half the MUFU.RCP of two series.
+// half-angles (each <= 0.1004 rad far away, so the sum stays in the minimax
+// polynomial's range and the real part stays > 0): half the MUFU.RCP of two
+// separate arctangents.
 template <int NP>
 __device__ __forceinline__ void seg_far(const float4* __restrict__ rec, const PairFrame (&f)[NP], float2 (&acc)[NP]) {
   float2 ra[NP], rb[NP], sab[NP];
