@@ -27,8 +27,11 @@ def launches(path):
     rows = [r for r in csv.reader(open(path)) if len(r) > 10]
     h = rows[0]
     ki, vi = h.index("Kernel Name"), h.index("Metric Value")
+    mi = h.index("Metric Name") if "Metric Name" in h else None
     agg = defaultdict(lambda: [0, 0.0])
     for r in rows[1:]:
+        if mi is not None and r[mi] != "gpu__time_duration.sum":
+            continue
         try:
             v = float(r[vi].replace(",", ""))
         except ValueError:
@@ -39,6 +42,29 @@ def launches(path):
     print(f"{'launches':>8} {'total ms':>12} {'share':>8}  kernel")
     for k, (c, v) in sorted(agg.items(), key=lambda x: -x[1][1]):
         print(f"{c:8d} {v / 1e6:12.3f} {100 * v / tot:7.2f}%  {k[:110]}")
+
+
+def traffic(path):
+    """k_label DRAM bytes per launch from a launch list taken with
+    --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,lts__t_bytes.sum"""
+    import json
+    rows = [r for r in csv.reader(open(path)) if len(r) > 10]
+    h = rows[0]
+    ki, mi, vi, ii = h.index("Kernel Name"), h.index("Metric Name"), h.index("Metric Value"), h.index("ID")
+    per = defaultdict(dict)
+    for r in rows[1:]:
+        if "k_label<" not in r[ki]:
+            continue
+        unit = r[h.index("Metric Unit")] if "Metric Unit" in h else ""
+        v = float(r[vi].replace(",", ""))
+        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1, "usecond": 1e3, "msecond": 1e6,
+                 "second": 1e9}.get(unit, 1)
+        per[r[ii]][r[mi]] = v * scale
+    last = per[sorted(per, key=int)[-1]]
+    rd, wr = last.get("dram__bytes_read.sum", 0.0), last.get("dram__bytes_write.sum", 0.0)
+    print(json.dumps({"kernel": "k_label<1,1>", "config": 5, "launches_seen": len(per), "dram_bytes_read": rd,
+                      "dram_bytes_write": wr, "traffic_bytes": rd + wr, "lts_bytes": last.get("lts__t_bytes.sum"),
+                      "gpu_time_ns": last.get("gpu__time_duration.sum")}, indent=1))
 
 
 def report(path):
@@ -59,4 +85,4 @@ def report(path):
 
 
 if __name__ == "__main__":
-    {"launches": launches, "report": report}[sys.argv[1]](sys.argv[2])
+    {"launches": launches, "report": report, "traffic": traffic}[sys.argv[1]](sys.argv[2])
