@@ -29,6 +29,14 @@ constexpr int kBlock = NM_BLOCK;        // threads per CTA of k_label
 #ifndef NM_MIN_BLOCKS
 #define NM_MIN_BLOCKS 4                 // resident CTAs per SM requested for k_label<1>
 #endif
+#ifndef NM_FAR_UNROLL
+#define NM_FAR_UNROLL 4                 // strip segments per iteration of the all-far group loop
+#endif
+constexpr int kFarUnroll = NM_FAR_UNROLL;
+#ifndef NM_SUB_UNROLL
+#define NM_SUB_UNROLL 1                 // subtiles per iteration of the tile loop
+#endif
+constexpr int kSubUnroll = NM_SUB_UNROLL;
 #ifndef NM_MIN_BLOCKS_NP2
 #define NM_MIN_BLOCKS_NP2 3             // resident CTAs per SM requested for k_label<2>
 #endif
@@ -249,6 +257,7 @@ __global__ void __launch_bounds__(kBlock, (NP == 1 ? NM_MIN_BLOCKS : NM_MIN_BLOC
       float2 acc[NP];
 #pragma unroll
       for (int q = 0; q < NP; ++q) acc[q] = make_float2(0.0f, 0.0f);
+#pragma unroll kSubUnroll
       for (int st = 0; st < kSubPerTile; ++st) {
         const float4 sb = s_sub[st * kSubRec];
         float2 mx[NP], my[NP], mz[NP];  // -(p - c)
@@ -274,7 +283,7 @@ __global__ void __launch_bounds__(kBlock, (NP == 1 ? NM_MIN_BLOCKS : NM_MIN_BLOC
           for (int q = 0; q < NP; ++q) f[q] = pair_frame(mx[q], my[q], mz[q]);
           if (__all_sync(kFull, far)) {
             n_far += kSub / kSegTris;
-#pragma unroll 1
+#pragma unroll kFarUnroll
             for (int g = 0; g < kSub / kSegTris; ++g) seg_far<NP>(tt + g * kSegF4, f, acc);
           } else {
             // per-group decision; each lane's evaluator depends only on its
