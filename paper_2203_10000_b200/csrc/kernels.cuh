@@ -260,7 +260,7 @@ __global__ void __launch_bounds__(kBlock, (NP == 1 ? NM_MIN_BLOCKS : NM_MIN_BLOC
 #pragma unroll kSubUnroll
       for (int st = 0; st < kSubPerTile; ++st) {
         const float4 sb = s_sub[st * kSubRec];
-        float2 mx[NP], my[NP], mz[NP];  // -(p - c)
+        float2 mx[NP], my[NP], mz[NP], sp[NP];  // -(p - c), |p - c|^2
         bool lane_far[P];
         bool far = true;
 #pragma unroll
@@ -272,6 +272,7 @@ __global__ void __launch_bounds__(kBlock, (NP == 1 ? NM_MIN_BLOCKS : NM_MIN_BLOC
           my[q] = make_float2(-py.x, -py.y);
           mz[q] = make_float2(-pz.x, -pz.y);
           const float2 d2 = fma2(pz, pz, fma2(py, py, mul2(px, px)));
+          sp[q] = d2;
           lane_far[2 * q] = !valid[2 * q] || d2.x > sb.w;
           lane_far[2 * q + 1] = !valid[2 * q + 1] || d2.y > sb.w;
           far &= lane_far[2 * q] && lane_far[2 * q + 1];
@@ -280,7 +281,7 @@ __global__ void __launch_bounds__(kBlock, (NP == 1 ? NM_MIN_BLOCKS : NM_MIN_BLOC
         if constexpr (STRIP) {
           PairFrame f[NP];
 #pragma unroll
-          for (int q = 0; q < NP; ++q) f[q] = pair_frame(mx[q], my[q], mz[q]);
+          for (int q = 0; q < NP; ++q) f[q] = PairFrame{mx[q], my[q], mz[q], sp[q]};
           if (__all_sync(kFull, far)) {
             n_far += kSub / kSegTris;
 #pragma unroll kFarUnroll

@@ -170,19 +170,12 @@ __device__ __forceinline__ float edge_val(const float4* __restrict__ erec, int i
   return f4_at(__ldg(erec + (idx >> 2)), idx & 3);
 }
 
-// Per point pair, in the subtile frame: m = -(p - c); sp = |p - c|^2.
+// Per point pair, in the subtile frame: m = -(p - c); sp = |p - c|^2 (the
+// subtile far test's squared distance, reused).
 struct PairFrame {
   float2 mx, my, mz, sp;
 };
 
-__device__ __forceinline__ PairFrame pair_frame(float2 mx, float2 my, float2 mz) {
-  PairFrame f;
-  f.mx = mx;
-  f.my = my;
-  f.mz = mz;
-  f.sp = fma2(mz, mz, fma2(my, my, mul2(mx, mx)));
-  return f;
-}
 
 // ---- far evaluator --------------------------------------------------------
 // |V - p| from |V - p|^2 = |V|^2 + |p|^2 + (2V).(-p): 4 ops + MUFU.SQRT
