@@ -134,6 +134,17 @@ def test_abi_input_validation():
             c.label_mesh(np.zeros((4, 3)), np.array([[0, 1, 2, 9]], np.uint32))
         with pytest.raises(NativeError, match="references node"):
             c.refine_boundary(np.zeros((4, 3)), np.array([[0, 1, 2, 7]], np.uint32), np.array([1], np.int32), 1, 2)
+        # device-side validation (k_max_index), host scan only for the message
+        with pytest.raises(NativeError, match="tet 1 references node 4"):
+            c.label_tets(np.array([[0, 1, 2, 3], [0, 1, 4, 3]], np.uint32), np.ones(4, np.uint32))
+        with pytest.raises(NativeError, match="references node"):
+            c.refine_relabel(np.zeros((4, 3)), np.array([[0, 1, 2, 5]], np.uint32), levels=1)
+        with pytest.raises(NativeError, match="references node"):
+            c.label_mesh(np.zeros((0, 3)), np.array([[0, 0, 0, 0]], np.uint32))
+        big = np.tile(np.array([[0, 1, 2, 3]], np.uint32), (100000, 1))
+        big[77777, 2] = 4
+        with pytest.raises(NativeError, match="tet 77777 references node 4"):
+            c.label_mesh(np.zeros((4, 3)), big)
         # still usable after errors
         m, _ = c.label_nodes(np.zeros((1, 3)))
         assert m[0] == 1

@@ -121,3 +121,25 @@ def test_oracle_point_triangle_distance_kats():
     pts = np.array([[0.2, 0.2, 0.5], [2.0, 0.0, 0.0], [-1.0, -1.0, 0.0], [0.5, -2.0, 0.0], [0.6, 0.6, 0.0]])
     d = oracle.point_surface_distance(pts, xyz, tri)
     np.testing.assert_allclose(d, [0.5, 1.0, np.sqrt(2.0), 2.0, np.sqrt(2) * 0.1], rtol=1e-12)
+
+
+def test_refine_under_sanitizers(tmp_path):
+    """csrc/refine.cpp (host code of the C ABI) built with AddressSanitizer +
+    UBSan and driven through nm_refine / nm_mesh_* on random selections
+    (tests/cpp/refine_asan.cpp): no memory or UB finding, invariants hold."""
+    import shutil
+    import subprocess
+    from pathlib import Path
+    root = Path(__file__).resolve().parents[1]
+    cuda = Path("/usr/local/cuda")
+    if shutil.which("g++") is None or not (cuda / "include" / "cuda_runtime.h").exists():
+        pytest.skip("g++ or CUDA headers missing")
+    exe = tmp_path / "refine_asan"
+    cmd = ["g++", "-std=c++17", "-O1", "-g", "-fsanitize=address,undefined", "-fno-sanitize-recover=all",
+           "-fno-omit-frame-pointer", f"-I{root / 'include'}", f"-I{cuda / 'include'}",
+           str(root / "tests" / "cpp" / "refine_asan.cpp"), str(root / "paper_2203_10000_b200" / "csrc" / "refine.cpp"),
+           f"-L{cuda / 'lib64'}", "-lcudart", f"-Wl,-rpath,{cuda / 'lib64'}", "-o", str(exe)]
+    subprocess.run(cmd, check=True, capture_output=True, text=True)
+    r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "refine_asan ok" in r.stdout
