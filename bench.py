@@ -40,7 +40,18 @@ sys.path.insert(0, str(ROOT))
 METRIC = "point-triangle solid-angle evals/sec and full-mesh labeling time at 1/2/4/8 B200"
 UNIT = "evals/s"
 OPS_PER_EVAL = 57                      # pinned FP32-pipe cost of one VOS eval
-ISSUED_OPS_PER_EVAL = 18.625           # FP32 lane-ops the strip far evaluator issues per eval (SASS)
+ISSUED_OPS_PER_EVAL = 18.625           # FP32 lane-ops the strip far evaluator issues per eval (SASS),
+SEG_FFMA2, CONT_SAVED_FFMA2 = 149, 9   # per 8-triangle segment and point pair; saved when it continues its strip
+
+
+def issued_ops_per_eval(sinfo):
+    """FP32 lane-ops per eval of the far evaluator on this surface layout:
+    149 packed ops per segment (16 evals), 9 fewer for a segment that
+    continues the previous one of its strip."""
+    if sinfo["layout"] != "strips":
+        return 40.0
+    segs, cont = max(1, sinfo["segments"]), sinfo["continued_segments"]
+    return (SEG_FFMA2 * segs - CONT_SAVED_FFMA2 * cont) * 2.0 / (16.0 * segs)
 FP32_LANES_PER_SM = 128
 MY_KERNELS_PER_STEP = 7                # morton keys, k_label, 3x select, k_fixup, k_label_tets
 CUB_KERNELS = 4                        # library radix-sort kernels counted in nm_stats.launches
@@ -461,10 +472,11 @@ def main():
                           f" / {OPS_PER_EVAL} FP32-pipe ops per eval (SURVEY.md §8d); per GPU",
             "kernel_ms_avg": k_ms, "kernel_share_of_step": k_ms / (sum(step_ms) / len(step_ms)),
             # the same kernel against the FP32 ops it actually issues per eval
-            # (far evaluator: 18.625 lane-ops; SASS count in DESIGN.md §3)
-            "issued_fp32_ops_per_eval": ISSUED_OPS_PER_EVAL if layout == "strips" else 40.0,
+            # (far evaluator: 18.625 lane-ops per eval, less for continued strip segments)
+            "issued_fp32_ops_per_eval": issued_ops_per_eval(sinfo),
+            "continued_segments": f"{sinfo.get('continued_segments', 0)} of {sinfo.get('segments', 0)}",
             "frac_of_issued_fp32_bound": achieved / (sms * FP32_LANES_PER_SM * sm_max * 1e6 /
-                                                     (ISSUED_OPS_PER_EVAL if layout == "strips" else 40.0)),
+                                                     issued_ops_per_eval(sinfo)),
         }
         if clocks.get("sm_mhz"):
             roof["frac_at_measured_clock"] = achieved / (sms * FP32_LANES_PER_SM * clocks["sm_mhz"] * 1e6 / OPS_PER_EVAL)

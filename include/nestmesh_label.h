@@ -239,6 +239,11 @@ int nm_sample_surface(const double* xyz, const uint32_t* tri, size_t nt, size_t 
  * layout (1 triangles, 2 strips) chosen for the current surfaces. */
 int nm_surface_info(nm_ctx* ctx, int* K, size_t* triangles, size_t* padded_triangles, int* layout);
 
+/* Strip layout: 8-triangle segments, and how many of them continue the
+ * previous segment of their strip inside a subtile (the far evaluator
+ * reuses two vertex distances there). Both 0 for the triangle layout. */
+int nm_surface_segments(nm_ctx* ctx, size_t* segments, size_t* continued);
+
 #ifdef __cplusplus
 }
 #endif

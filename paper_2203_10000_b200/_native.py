@@ -130,6 +130,7 @@ LABEL_API = {
     "nm_group_label_mesh": (ctypes.c_int, [ctypes.c_void_p, c_double_p, ctypes.c_size_t, c_u32_p, ctypes.c_size_t,
                                            ctypes.c_double, c_i32_p, c_u32_p, ctypes.POINTER(NmStats)]),
     "nm_surface_info": (ctypes.c_int, [ctypes.c_void_p, c_i32_p, c_size_p, c_size_p, c_i32_p]),
+    "nm_surface_segments": (ctypes.c_int, [ctypes.c_void_p, c_size_p, c_size_p]),
 }
 
 _lib = None
@@ -236,7 +237,10 @@ class Context:
         lay = ctypes.c_int()
         check(self.lib.nm_surface_info(self.handle, ctypes.byref(K), ctypes.byref(t), ctypes.byref(tp),
                                        ctypes.byref(lay)))
-        return {"K": K.value, "triangles": t.value, "slots": tp.value, "layout": "strips" if lay.value == 2 else "triangles"}
+        segs, cont = ctypes.c_size_t(), ctypes.c_size_t()
+        check(self.lib.nm_surface_segments(self.handle, ctypes.byref(segs), ctypes.byref(cont)))
+        return {"K": K.value, "triangles": t.value, "slots": tp.value, "layout": "strips" if lay.value == 2 else "triangles",
+                "segments": segs.value, "continued_segments": cont.value}
 
     # -- host-buffer entry points ----------------------------------------
     def enclosure(self, pts, threshold=0.5):

@@ -109,6 +109,8 @@ struct LabelParams {
   const float4* tri;         // soup: 3 float4 per triangle (a.xyz,N.x) (b.xyz,N.y) (c.xyz,N.z);
                              // strip: kSegF4 float4 per 8-triangle segment (vos.cuh)
   const float4* edges;       // strip layout: kEdgeF4 float4 of -|e|^2 per segment (near evaluator)
+  const std::uint32_t* cont;  // strip layout: per tile, bit sidx * kGroups + j = segment j of subtile
+                              // sidx continues segment j - 1 (same strip)
   const float4* sub;         // per subtile: fp32 centre c (centred frame), w = (far radius)^2;
                              // the subtile's vertices are stored relative to c
   const std::uint32_t* comp_tiles;  // K+1 tile offsets
@@ -253,6 +255,7 @@ __global__ void __launch_bounds__(kBlock, (NP == 1 ? NM_MIN_BLOCKS : NM_MIN_BLOC
       ++it;
       const float4* const s_tri = s_tri_buf[buf];
       const float4* const s_sub = s_sub_buf[buf];
+      const std::uint32_t tcont = STRIP ? __ldg(prm.cont + tile) : 0u;
 
       float2 acc[NP];
 #pragma unroll
@@ -284,8 +287,11 @@ __global__ void __launch_bounds__(kBlock, (NP == 1 ? NM_MIN_BLOCKS : NM_MIN_BLOC
           for (int q = 0; q < NP; ++q) f[q] = PairFrame{mx[q], my[q], mz[q], sp[q]};
           if (__all_sync(kFull, far)) {
             n_far += kSub / kSegTris;
+            float2 ra[NP], rb[NP], sab[NP];  // chain state across continued segments
+            const std::uint32_t cbits = tcont >> (st * kGroups);
 #pragma unroll kFarUnroll
-            for (int g = 0; g < kSub / kSegTris; ++g) seg_far<NP>(tt + g * kSegF4, f, acc);
+            for (int g = 0; g < kSub / kSegTris; ++g)
+              seg_far<NP>(tt + g * kSegF4, f, acc, ra, rb, sab, g > 0 && ((cbits >> g) & 1u));
           } else {
             // per-group decision; each lane's evaluator depends only on its
             // own point (lane_far = far from the subtile or from the group)

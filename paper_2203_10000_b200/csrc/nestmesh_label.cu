@@ -219,7 +219,8 @@ struct nm_ctx {
   double lo[3] = {0, 0, 0}, span = 1.0;  // Morton box of the domain
   nm::LabelIds ids{};
   std::vector<std::uint32_t> comp_tiles_h;  // host copy of the K+1 tile offsets
-  DBuf tri, sub, edges, comp_tiles, xyz64, tri_idx, comp_off, comp_box, cullmask;
+  std::size_t n_continued = 0;              // strip segments continuing the previous one (cont bits set)
+  DBuf tri, sub, edges, cont, comp_tiles, xyz64, tri_idx, comp_off, comp_box, cullmask;
 
   // scratch
   DBuf pts, masks, flagmask, nbr, known, want, fkeys, frontier, lex, region, bfaces, btri, dist_tri, dist_xyz,
@@ -229,7 +230,7 @@ struct nm_ctx {
       s_out, word;
 
   ~nm_ctx() {
-    for (DBuf* b : {&tri, &sub, &edges, &comp_tiles, &xyz64, &tri_idx, &comp_off, &comp_box, &cullmask, &pts, &masks, &flagmask, &nbr, &known, &want, &fkeys, &frontier, &lex, &region, &bfaces, &btri,
+    for (DBuf* b : {&tri, &sub, &edges, &cont, &comp_tiles, &xyz64, &tri_idx, &comp_off, &comp_box, &cullmask, &pts, &masks, &flagmask, &nbr, &known, &want, &fkeys, &frontier, &lex, &region, &bfaces, &btri,
                     &dist_tri, &dist_xyz, &dist_idx, &dist_d32, &dist_out, &r_red, &r_keys, &r_keys2, &r_S,
                     &r_idx, &r_touched, &r_mask, &r_cnt, &r_offs, &r_flag, &meshA_nodes, &meshA_tets, &meshA_labels,
                     &meshB_nodes, &meshB_tets, &meshB_labels, &meshB_parent, &masks2, &order, &keys,
@@ -354,6 +355,7 @@ void label_nodes_dev(nm_ctx* c, const double* d_pts, std::size_t n, double T, st
   prm.tri = static_cast<const float4*>(c->tri.p);
   prm.sub = static_cast<const float4*>(c->sub.p);
   prm.edges = static_cast<const float4*>(c->edges.p);
+  prm.cont = static_cast<const std::uint32_t*>(c->cont.p);
   prm.comp_tiles = static_cast<const std::uint32_t*>(c->comp_tiles.p);
   prm.K = c->K;
   prm.cx = c->cx;
@@ -742,10 +744,18 @@ int nm_set_surfaces(nm_ctx* c, const double* xyz, std::size_t nv, const std::uin
     // ---- strip decomposition --------------------------------
     // Segment = 8 consecutive strip triangles over 10 vertices; a strip's last
     // segment is padded with zero-normal triangles repeating its last vertex.
+    // Segments are laid out in chunks of kGroups consecutive segments of one
+    // strip (one chunk per 32-triangle subtile): full chunks first, in Morton
+    // order of their centroids, then the strips' shorter tail chunks, also in
+    // Morton order. Inside a subtile a segment that continues the previous one
+    // (same strip, next 8 triangles) shares its first two vertices with the
+    // previous segment's last two, so the far evaluator carries their
+    // distances instead of recomputing them (bit-identical: same fp32 vertex,
+    // same frame). cont bit = sidx * kGroups + j per tile.
     struct Seg {
       std::uint32_t v[nm::kSegTris + 2];
       std::int64_t t[nm::kSegTris];  // original triangle id, -1 = pad
-      std::uint32_t key;
+      std::uint32_t strip, pos;      // strip id (within the compartment), segment index in the strip
     };
     std::vector<std::vector<Seg>> segs(K);
     std::size_t strip_slots = 0;
@@ -753,20 +763,43 @@ int nm_set_surfaces(nm_ctx* c, const double* xyz, std::size_t nv, const std::uin
     if (try_strips) {
       for (int k = 0; k < K; ++k) {
         const std::vector<Strip> strips = stripify(tri, comp_off[k], comp_off[k + 1]);
-        for (const Strip& st : strips) {
+        struct Chunk {
+          std::uint32_t key;
+          bool full;
+          std::size_t first, count;  // range in `all`
+        };
+        std::vector<Seg> all;
+        std::vector<Chunk> chunks;
+        for (std::uint32_t si = 0; si < strips.size(); ++si) {
+          const Strip& st = strips[si];
           const std::size_t m = st.t.size();
-          for (std::size_t s0 = 0; s0 < m; s0 += nm::kSegTris) {
+          std::uint32_t pos = 0;
+          for (std::size_t s0 = 0; s0 < m; s0 += nm::kSegTris, ++pos) {
             Seg g;
             for (int j = 0; j < nm::kSegTris + 2; ++j) g.v[j] = st.v[std::min(s0 + j, st.v.size() - 1)];
             for (int j = 0; j < nm::kSegTris; ++j) g.t[j] = s0 + j < m ? std::int64_t(st.t[s0 + j]) : -1;
-            double cen[3] = {0, 0, 0};
-            for (int j = 0; j < nm::kSegTris + 2; ++j)
-              for (int a = 0; a < 3; ++a) cen[a] += xyz[3 * std::size_t(g.v[j]) + a] / (nm::kSegTris + 2);
-            g.key = morton(cen);
-            segs[k].push_back(g);
+            g.strip = si;
+            g.pos = pos;
+            if (pos % nm::kGroups == 0) chunks.push_back({0u, false, all.size(), 0});
+            chunks.back().count++;
+            all.push_back(g);
           }
         }
-        std::stable_sort(segs[k].begin(), segs[k].end(), [](const Seg& x, const Seg& y) { return x.key < y.key; });
+        for (Chunk& ch : chunks) {
+          double cen[3] = {0, 0, 0};
+          double w = 0;
+          for (std::size_t q = ch.first; q < ch.first + ch.count; ++q)
+            for (int j = 0; j < nm::kSegTris + 2; ++j, w += 1)
+              for (int a = 0; a < 3; ++a) cen[a] += xyz[3 * std::size_t(all[q].v[j]) + a];
+          for (double& x : cen) x /= w;
+          ch.key = morton(cen);
+          ch.full = ch.count == static_cast<std::size_t>(nm::kGroups);
+        }
+        std::stable_sort(chunks.begin(), chunks.end(), [](const Chunk& x, const Chunk& y) {
+          return x.full != y.full ? x.full : x.key < y.key;
+        });
+        for (const Chunk& ch : chunks)
+          for (std::size_t q = ch.first; q < ch.first + ch.count; ++q) segs[k].push_back(all[q]);
         const std::size_t per_tile = nm::kTile / nm::kSegTris;
         strip_slots += (segs[k].size() + per_tile - 1) / per_tile * nm::kTile;
       }
@@ -806,6 +839,8 @@ int nm_set_surfaces(nm_ctx* c, const double* xyz, std::size_t nv, const std::uin
     std::vector<float4> htri(ntiles * tile_f4);
     std::vector<float4> hsub(ntiles * nm::kSubPerTile * nm::kSubRec);
     std::vector<float4> hedge(use_strips ? ntiles * nm::kSubPerTile * nm::kGroups * nm::kEdgeF4 : 1);
+    std::vector<std::uint32_t> hcont(std::max<std::size_t>(ntiles, 1), 0u);
+    static_assert(nm::kSubPerTile * nm::kGroups <= 32, "continuation bits of a tile must fit a uint32");
     const double far_ratio = c->opt.far_ratio, far_abs = c->opt.far_abs_mm;
     // Each 32-triangle subtile carries an fp32 centre c (exactly representable
     // in the centred frame) and its vertices relative to c, so near-surface
@@ -853,6 +888,9 @@ int nm_set_surfaces(nm_ctx* c, const double* xyz, std::size_t nv, const std::uin
           for (int j = 0; j < nunits; ++j) {
             const std::size_t u = u0 + j;
             if (use_strips) {
+              if (j > 0 && u < nreal && segs[k][u].strip == segs[k][u - 1].strip &&
+                  segs[k][u].pos == segs[k][u - 1].pos + 1)
+                hcont[tl] |= 1u << (sidx * nm::kGroups + j);
               float4* r = o + j * nm::kSegF4;
               double N[nm::kSegTris][3];
               for (int q = 0; q < nm::kSegTris; ++q) {
@@ -911,7 +949,10 @@ int nm_set_surfaces(nm_ctx* c, const double* xyz, std::size_t nv, const std::uin
               for (int q = 0; q < 3; ++q) o[3 * j + q] = make_float4(rv[3 * q], rv[3 * q + 1], rv[3 * q + 2], float(N[q]));
             }
           }
-          const double R = (far_ratio * rho + far_abs) * (1.0 + 1e-5);
+#ifndef NM_DIAG_SUBR
+#define NM_DIAG_SUBR 1.0
+#endif
+          const double R = (far_ratio * rho * NM_DIAG_SUBR + far_abs) * (1.0 + 1e-5);
           float4* hs = &hsub[(static_cast<std::size_t>(tl) * nm::kSubPerTile + sidx) * nm::kSubRec];
           hs[0] = make_float4(fc[0], fc[1], fc[2], float(R * R));
           // spheres of the kGroups groups of kSegTris triangles, centres relative to fc
@@ -949,6 +990,7 @@ int nm_set_surfaces(nm_ctx* c, const double* xyz, std::size_t nv, const std::uin
     up(c->tri, htri.data(), htri.size() * sizeof(float4));
     up(c->sub, hsub.data(), hsub.size() * sizeof(float4));
     up(c->edges, hedge.data(), hedge.size() * sizeof(float4));
+    up(c->cont, hcont.data(), hcont.size() * sizeof(std::uint32_t));
     up(c->comp_tiles, tiles.data(), tiles.size() * sizeof(std::uint32_t));
     up(c->xyz64, xyz, nv * 3 * sizeof(double));
     up(c->tri_idx, tri, nt * 3 * sizeof(std::uint32_t));
@@ -985,11 +1027,21 @@ int nm_set_surfaces(nm_ctx* c, const double* xyz, std::size_t nv, const std::uin
     NM_CUDA(cudaStreamSynchronize(c->stream));
     c->K = K;
     c->comp_tiles_h = tiles;
+    c->n_continued = 0;
+    for (std::uint32_t w : hcont) c->n_continued += static_cast<std::size_t>(__builtin_popcount(w));
     c->nt_real = nt;
     c->nt_pad = npad;
     c->nv = nv;
     for (int k = 0; k < 32; ++k) c->ids.id[k] = k < K ? label_ids[k] : 0;
     c->has_surfaces = true;
+  });
+}
+
+int nm_surface_segments(nm_ctx* c, std::size_t* segments, std::size_t* continued) {
+  return guarded([&] {
+    require_surfaces(c);
+    if (segments) *segments = c->strips ? c->nt_pad / nm::kSegTris : 0;
+    if (continued) *continued = c->strips ? c->n_continued : 0;
   });
 }
 

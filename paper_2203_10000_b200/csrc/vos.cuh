@@ -210,14 +210,19 @@ __device__ __forceinline__ float2 atan_far3(float2 acc, float2 num, float2 den) 
 // half-angles (each <= 0.1004 rad far away, so the sum stays in the minimax
 // polynomial's range and the real part stays > 0): half the MUFU.RCP of two
 // separate arctangents.
+// Chain state (ra, rb, sab): the distances of the segment's first two
+// vertices and their sum. cont: this segment continues the previous one of
+// the same strip in the same subtile, whose final state is already there.
 template <int NP>
-__device__ __forceinline__ void seg_far(const float4* __restrict__ rec, const PairFrame (&f)[NP], float2 (&acc)[NP]) {
-  float2 ra[NP], rb[NP], sab[NP];
+__device__ __forceinline__ void seg_far(const float4* __restrict__ rec, const PairFrame (&f)[NP], float2 (&acc)[NP],
+                                        float2 (&ra)[NP], float2 (&rb)[NP], float2 (&sab)[NP], bool cont) {
+  if (!cont) {
 #pragma unroll
-  for (int q = 0; q < NP; ++q) {
-    ra[q] = far_dist(rec[0], f[q]);
-    rb[q] = far_dist(rec[1], f[q]);
-    sab[q] = add2(ra[q], rb[q]);
+    for (int q = 0; q < NP; ++q) {
+      ra[q] = far_dist(rec[0], f[q]);
+      rb[q] = far_dist(rec[1], f[q]);
+      sab[q] = add2(ra[q], rb[q]);
+    }
   }
   float2 n0[NP], d0[NP];
 #pragma unroll
@@ -270,6 +275,12 @@ __device__ __forceinline__ Vtx2 strip_vertex(const float4& V, float2 mx, float2 
 constexpr int kNearUnroll = NM_NEAR_UNROLL;
 // use[k]: lane point k takes this group's near result (the caller discards
 // the others), so only those lanes ask for the full-range atan2.
+template <int NP>
+__device__ __forceinline__ void seg_far(const float4* __restrict__ rec, const PairFrame (&f)[NP], float2 (&acc)[NP]) {
+  float2 ra[NP], rb[NP], sab[NP];
+  seg_far<NP>(rec, f, acc, ra, rb, sab, false);
+}
+
 template <int NP>
 __device__ __forceinline__ void seg_near(const float4* __restrict__ rec, const float4* __restrict__ erec,
                                          const PairFrame (&f)[NP], float2 (&acc)[NP], bool (&det)[2 * NP],
