@@ -285,18 +285,21 @@ __global__ void __launch_bounds__(kBlock, (NP == 1 ? NM_MIN_BLOCKS : NM_MIN_BLOC
           PairFrame f[NP];
 #pragma unroll
           for (int q = 0; q < NP; ++q) f[q] = PairFrame{mx[q], my[q], mz[q], sp[q]};
+          float2 ra[NP], rb[NP], sab[NP];  // chain state across continued segments
+          const std::uint32_t cbits = tcont >> (st * kGroups);
           if (__all_sync(kFull, far)) {
             n_far += kSub / kSegTris;
-            float2 ra[NP], rb[NP], sab[NP];  // chain state across continued segments
-            const std::uint32_t cbits = tcont >> (st * kGroups);
 #pragma unroll kFarUnroll
             for (int g = 0; g < kSub / kSegTris; ++g)
               seg_far<NP>(tt + g * kSegF4, f, acc, ra, rb, sab, g > 0 && ((cbits >> g) & 1u));
           } else {
             // per-group decision; each lane's evaluator depends only on its
-            // own point (lane_far = far from the subtile or from the group)
+            // own point (lane_far = far from the subtile or from the group).
+            // The chain state is valid when the previous group ran seg_far.
+            bool chain = false;
 #pragma unroll 1
             for (int g = 0; g < kSub / kSegTris; ++g) {
+              const bool cont = chain && ((cbits >> g) & 1u);
               const float4 sg = s_sub[st * kSubRec + 1 + g];
               bool gf[P];
               bool all = true, any = false;
@@ -312,7 +315,8 @@ __global__ void __launch_bounds__(kBlock, (NP == 1 ? NM_MIN_BLOCKS : NM_MIN_BLOC
               const float4* rec = tt + g * kSegF4;
               if (__all_sync(kFull, all)) {
                 ++n_far;
-                seg_far<NP>(rec, f, acc);
+                seg_far<NP>(rec, f, acc, ra, rb, sab, cont);
+                chain = true;
               } else {
                 ++n_near;
                 float2 an[NP];
@@ -327,11 +331,13 @@ __global__ void __launch_bounds__(kBlock, (NP == 1 ? NM_MIN_BLOCKS : NM_MIN_BLOC
                 const float4* erec =
                     prm.edges + ((static_cast<std::size_t>(tile) * kSubPerTile + st) * kGroups + g) * kEdgeF4;
                 seg_near<NP>(rec, erec, f, an, dn, use, prm.tau, prm.delta);
+                chain = false;
                 if (__any_sync(kFull, any)) {
                   float2 af[NP];
 #pragma unroll
                   for (int q = 0; q < NP; ++q) af[q] = acc[q];
-                  seg_far<NP>(rec, f, af);
+                  seg_far<NP>(rec, f, af, ra, rb, sab, cont);
+                  chain = true;
 #pragma unroll
                   for (int q = 0; q < NP; ++q) {
                     an[q].x = gf[2 * q] ? af[q].x : an[q].x;
