@@ -409,26 +409,43 @@ def main():
     # which evaluates every pair.
     cull = None
     if rank == 0 and world == 1 and not args.no_cull:
-        cctx = Context(local, cull_outside=1)
-        cctx.set_surfaces(S.xyz, S.tri, S.comp_off, S.label_ids)
-        cm = torch.zeros(nsh.per, dtype=torch.int32, device="cuda")
-        cctx.label_nodes_device(d_nodes, cm[: nsh.size], stream=sptr, stats=True)
-        cl = torch.empty(tsh.size, dtype=torch.int32, device="cuda")
-        cms = []
-        for i in range(args.steps):
-            flush.fill_(i)
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record(stream)
-            cctx.label_nodes_device(d_nodes, cm[: nsh.size], stream=sptr, stats=False)
-            cctx.label_tets_device(d_tets, cm, cl, stream=sptr, stats=False)
-            b.record(stream)
-            torch.cuda.synchronize()
-            cms.append(a.elapsed_time(b))
-        same = bool(torch.equal(cl, d_labels))
-        cull = {"full_mesh_labeling_time_s": sum(cms) / len(cms) / 1e3, "labels_identical": same,
-                "note": "opt-in exact culling (nm_options.cull_outside): a compartment is skipped for points "
-                        "outside its 13-DOP (winding number exactly 0 for a closed surface)"}
-        cctx.close()
+        cull = {}
+        notes = {1: "opt-in exact culling (nm_options.cull_outside=1): a compartment is skipped for points "
+                    "outside its 13-DOP (winding number exactly 0 for a closed surface)",
+                 2: "cull_outside=2: 13-DOP plus certified cells (per-compartment grid cells whose ball meets no "
+                    "triangle carry their exact winding number 0/1; only the remaining (point, compartment) "
+                    "pairs are evaluated, by the same k_label loop in sparse mode)"}
+        for mode in (1, 2):
+            cctx = Context(local, cull_outside=mode)
+            t_set = time.perf_counter()
+            cctx.set_surfaces(S.xyz, S.tri, S.comp_off, S.label_ids)
+            t_set = time.perf_counter() - t_set
+            cm = torch.zeros(nsh.per, dtype=torch.int32, device="cuda")
+            cctx.label_nodes_device(d_nodes, cm[: nsh.size], stream=sptr, stats=True)
+            cl = torch.empty(tsh.size, dtype=torch.int32, device="cuda")
+            cms = []
+            for i in range(args.steps):
+                flush.fill_(i)
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                cctx.label_nodes_device(d_nodes, cm[: nsh.size], stream=sptr, stats=False)
+                cctx.label_tets_device(d_tets, cm, cl, stream=sptr, stats=False)
+                b.record(stream)
+                torch.cuda.synchronize()
+                cms.append(a.elapsed_time(b))
+            same = bool(torch.equal(cl, d_labels))
+            entry = {"full_mesh_labeling_time_s": sum(cms) / len(cms) / 1e3, "labels_identical": same,
+                     "set_surfaces_s": t_set, "note": notes[mode]}
+            if mode == 2:
+                ci = cctx.cell_info()
+                entry.update({"cells": ci["cells"], "certified_cells": ci["certified"],
+                              "representatives": ci["reps"], "cell_build_ms": ci["ms_build"],
+                              "pairs_evaluated": ci["last_pairs"], "pairs_total": nsh.size * S.K,
+                              "evals_performed": ci["last_evals"]})
+            cull["mode%d" % mode] = entry
+            cctx.close()
+        cull["full_mesh_labeling_time_s"] = cull["mode2"]["full_mesh_labeling_time_s"]
+        cull["labels_identical"] = cull["mode1"]["labels_identical"] and cull["mode2"]["labels_identical"]
 
     # §8(f) rows on the labeled mesh (not part of the headline): device
     # extraction of the region boundary of all compartments (the outer

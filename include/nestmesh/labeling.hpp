@@ -82,7 +82,8 @@ struct GpuOptions {
   std::vector<int> devices;     // > 1 entries: initial_label shards over these devices (SPEC.md:267 --label-workers)
   GpuOptions() {
     nm_default_options(&opt);
-    opt.cull_outside = 1;  // exact for closed surfaces; disabled below whenever closedness is not validated
+    opt.cull_outside = 2;  // exact for closed surfaces (13-DOP + certified cells); disabled below whenever
+                           // closedness is not validated
   }
 };
 

@@ -65,7 +65,10 @@ typedef struct nm_options {
   int layout;            /* triangle tiles: 0 auto, 1 independent triangles, 2 strip segments (performance only) */
   int cull_outside;      /* 1: exact culling — a point outside a closed compartment's 13-DOP (slabs on 13
                             directions around its vertices) gets s = 0 without evaluating its triangles
-                            (winding number of a closed surface); 0 (default): every pair is evaluated */
+                            (winding number of a closed surface); 2: additionally, a point inside a
+                            certified cell of the compartment's grid (a cell whose ball meets no
+                            triangle; grid built by nm_set_surfaces from the surfaces alone) gets the
+                            cell's exact winding number (0 or 1); 0 (default): every pair is evaluated */
 } nm_options;
 
 /* Counters of one labeling call (accumulated by the call, not across calls). */
@@ -243,6 +246,13 @@ int nm_surface_info(nm_ctx* ctx, int* K, size_t* triangles, size_t* padded_trian
  * previous segment of their strip inside a subtile (the far evaluator
  * reuses two vertex distances there). Both 0 for the triangle layout. */
 int nm_surface_segments(nm_ctx* ctx, size_t* segments, size_t* continued);
+
+/* Certified cells (cull_outside = 2): grid cells over all compartments, how
+ * many are certified, representative evaluations and host wall time of the
+ * build (nm_set_surfaces); (point, compartment) pairs and point-triangle
+ * evaluations of the last node pass that were not resolved by culling. */
+int nm_cell_info(nm_ctx* ctx, uint64_t* cells, uint64_t* certified, uint64_t* reps, double* ms_build,
+                 uint64_t* last_pairs, uint64_t* last_evals);
 
 #ifdef __cplusplus
 }

@@ -131,6 +131,8 @@ LABEL_API = {
                                            ctypes.c_double, c_i32_p, c_u32_p, ctypes.POINTER(NmStats)]),
     "nm_surface_info": (ctypes.c_int, [ctypes.c_void_p, c_i32_p, c_size_p, c_size_p, c_i32_p]),
     "nm_surface_segments": (ctypes.c_int, [ctypes.c_void_p, c_size_p, c_size_p]),
+    "nm_cell_info": (ctypes.c_int, [ctypes.c_void_p] + [ctypes.POINTER(ctypes.c_uint64)] * 3
+                     + [c_double_p] + [ctypes.POINTER(ctypes.c_uint64)] * 2),
 }
 
 _lib = None
@@ -241,6 +243,17 @@ class Context:
         check(self.lib.nm_surface_segments(self.handle, ctypes.byref(segs), ctypes.byref(cont)))
         return {"K": K.value, "triangles": t.value, "slots": tp.value, "layout": "strips" if lay.value == 2 else "triangles",
                 "segments": segs.value, "continued_segments": cont.value}
+
+    def cell_info(self):
+        """Certified-cell culling (cull_outside=2): grid size, certified cells,
+        representative evaluations, build time, and the pairs / evaluations
+        of the last node pass left to the sparse kernel."""
+        v = [ctypes.c_uint64() for _ in range(5)]
+        ms = ctypes.c_double()
+        check(self.lib.nm_cell_info(self.handle, ctypes.byref(v[0]), ctypes.byref(v[1]), ctypes.byref(v[2]),
+                                    ctypes.byref(ms), ctypes.byref(v[3]), ctypes.byref(v[4])))
+        return {"cells": v[0].value, "certified": v[1].value, "reps": v[2].value, "ms_build": ms.value,
+                "last_pairs": v[3].value, "last_evals": v[4].value}
 
     # -- host-buffer entry points ----------------------------------------
     def enclosure(self, pts, threshold=0.5):

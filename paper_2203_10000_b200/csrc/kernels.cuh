@@ -129,14 +129,27 @@ struct LabelParams {
   // flagmask (zeroed by k_zero_masks). Each (point, compartment) sum is still
   // one CTA's fixed-order loop, so results do not depend on the split.
   int split[33];
+  // Sparse mode (k_label MODE 2, cell culling): CTA b of the 1-D grid takes
+  // compartment c with sp_blk[c] <= b < sp_blk[c + 1] and evaluates the
+  // positions sp_list[sp_off[c] .. sp_off[c + 1]) (indices into `order`)
+  // against that compartment only, ORing its bits in (masks pre-set by
+  // k_cell_classify).
+  const std::uint32_t* sp_list;
+  std::uint32_t sp_off[33];
+  std::uint32_t sp_blk[33];
 };
 
 // NP point pairs per thread (2*NP points), packed fp32x2 arithmetic.
 // STRIP = false: 3 float4 per triangle (triangle soup);
 // STRIP = true : 4 strip segments of 8 triangles per subtile (vos.cuh).
-template <int NP, bool STRIP, bool CULL = false>
+// MODE 0: every point x every compartment; 1: exact 13-DOP outside culling
+// (prm.cull); 2: sparse (prm.sp_*): (point, compartment) pairs left unknown
+// by the certified-cell classification (k_cell_classify).
+template <int NP, bool STRIP, int MODE = 0>
 __global__ void __launch_bounds__(kBlock, (NP == 1 ? NM_MIN_BLOCKS : NM_MIN_BLOCKS_NP2)) k_label(const LabelParams prm) {
   constexpr int P = 2 * NP;
+  constexpr bool CULL = MODE == 1;
+  constexpr bool SPARSE = MODE == 2;
   constexpr int kSubF4 = STRIP ? (kSub / kSegTris) * kSegF4 : kSub * 3;  // float4 per subtile
   constexpr int kTileF4 = kSubF4 * kSubPerTile;
   // Two tile buffers filled by the bulk-copy engine (cp.async.bulk, one
@@ -148,7 +161,14 @@ __global__ void __launch_bounds__(kBlock, (NP == 1 ? NM_MIN_BLOCKS : NM_MIN_BLOC
   __shared__ alignas(8) unsigned long long s_bar[2];
   __shared__ unsigned s_skip;
 
-  const std::size_t base = (static_cast<std::size_t>(blockIdx.x) * kBlock + threadIdx.x) * P;
+  std::size_t base = (static_cast<std::size_t>(blockIdx.x) * kBlock + threadIdx.x) * P;
+  std::size_t n_end = prm.n;
+  int c_sp = 0;
+  if (SPARSE) {
+    while (c_sp + 1 < prm.K && blockIdx.x >= prm.sp_blk[c_sp + 1]) ++c_sp;
+    base = prm.sp_off[c_sp] + (static_cast<std::size_t>(blockIdx.x - prm.sp_blk[c_sp]) * kBlock + threadIdx.x) * P;
+    n_end = prm.sp_off[c_sp + 1];
+  }
   // Points in the centred frame as double-singles (hi + lo), packed in pairs;
   // per subtile the kernel forms p - c = (hi - c) + lo, exact up to one
   // rounding of |p - c| (near-surface geometry keeps ~ulp(|p - c|)).
@@ -158,8 +178,9 @@ __global__ void __launch_bounds__(kBlock, (NP == 1 ? NM_MIN_BLOCKS : NM_MIN_BLOC
 #pragma unroll
   for (int k = 0; k < P; ++k) {
     const std::size_t i = base + k;
-    valid[k] = i < prm.n;
-    const std::size_t ii = valid[k] ? i : prm.n - 1;
+    valid[k] = i < n_end;
+    std::size_t ii = valid[k] ? i : n_end - 1;
+    if (SPARSE) ii = prm.sp_list[ii];
     const std::uint32_t j = prm.order ? prm.order[ii] : static_cast<std::uint32_t>(ii);
     pid[k] = j;
     const double dx = prm.pts[3 * static_cast<std::size_t>(j)] - prm.cx, dy = prm.pts[3 * static_cast<std::size_t>(j) + 1] - prm.cy,
@@ -202,7 +223,7 @@ __global__ void __launch_bounds__(kBlock, (NP == 1 ? NM_MIN_BLOCKS : NM_MIN_BLOC
     __syncthreads();
     skip = s_skip;
   }
-  const int c_lo = prm.split[blockIdx.y], c_hi = prm.split[blockIdx.y + 1];
+  const int c_lo = SPARSE ? c_sp : prm.split[blockIdx.y], c_hi = SPARSE ? c_sp + 1 : prm.split[blockIdx.y + 1];
   // producer state (thread 0): next tile to fetch and its compartment
   int pf_c = 0, pf_t = -1;
   auto pf_seek = [&](int c) {  // first tile of the first non-skipped, non-empty compartment in [c, c_hi)
@@ -403,7 +424,7 @@ __global__ void __launch_bounds__(kBlock, (NP == 1 ? NM_MIN_BLOCKS : NM_MIN_BLOC
 #pragma unroll
   for (int k = 0; k < P; ++k) {
     if (valid[k]) {
-      if (gridDim.y == 1) {
+      if (gridDim.y == 1 && !SPARSE) {
         prm.masks[pid[k]] = mask[k];
         prm.flagmask[pid[k]] = fmask[k];
       } else {

@@ -26,6 +26,7 @@
 #include "kernels.cuh"
 #include "refine.cuh"
 #include "distance.cuh"
+#include "cells.cuh"
 #include "nestmesh_label.h"
 #include "refine.h"
 
@@ -221,6 +222,12 @@ struct nm_ctx {
   std::vector<std::uint32_t> comp_tiles_h;  // host copy of the K+1 tile offsets
   std::size_t n_continued = 0;              // strip segments continuing the previous one (cont bits set)
   DBuf tri, sub, edges, cont, comp_tiles, xyz64, tri_idx, comp_off, comp_box, cullmask;
+  // certified cells (cull_outside = 2, cells.cuh)
+  bool cells = false;
+  DBuf cell_state, cell_grids, clus, clus_tri, unk, sp_list, sp_chunk, sp_cnt, rep_pts, rep_s, rep_m, rep_f;
+  std::uint64_t cells_total = 0, cells_certified = 0, cell_reps = 0, sparse_pairs = 0, sparse_evals = 0;
+  double ms_cells = 0.0;  // host wall time of the certification (nm_set_surfaces)
+  std::vector<std::uint32_t> comp_off_h;
 
   // scratch
   DBuf pts, masks, flagmask, nbr, known, want, fkeys, frontier, lex, region, bfaces, btri, dist_tri, dist_xyz,
@@ -230,6 +237,9 @@ struct nm_ctx {
       s_out, word;
 
   ~nm_ctx() {
+    for (DBuf* b : {&cell_state, &cell_grids, &clus, &clus_tri, &unk, &sp_list, &sp_chunk, &sp_cnt, &rep_pts, &rep_s,
+                    &rep_m, &rep_f})
+      b->release();
     for (DBuf* b : {&tri, &sub, &edges, &cont, &comp_tiles, &xyz64, &tri_idx, &comp_off, &comp_box, &cullmask, &pts, &masks, &flagmask, &nbr, &known, &want, &fkeys, &frontier, &lex, &region, &bfaces, &btri,
                     &dist_tri, &dist_xyz, &dist_idx, &dist_d32, &dist_out, &r_red, &r_keys, &r_keys2, &r_S,
                     &r_idx, &r_touched, &r_mask, &r_cnt, &r_offs, &r_flag, &meshA_nodes, &meshA_tets, &meshA_labels,
@@ -306,6 +316,87 @@ int compartment_split(const nm_ctx* c, std::size_t nblocks, int* split) {
   return g;
 }
 
+
+// Sparse k_label (MODE 2) over per-compartment lists of evaluation positions
+// (prm.sp_list, cnt[k] entries for compartment k, concatenated). Returns the
+// number of launches (0 when every list is empty).
+int launch_sparse(nm_ctx* c, nm::LabelParams& prm, const std::vector<std::uint32_t>& cnt, cudaStream_t st) {
+  const std::uint32_t per_block = nm::kBlock * 2;
+  std::uint32_t off = 0, blk = 0;
+  for (int k = 0; k <= 32; ++k) {
+    prm.sp_off[k] = off;
+    prm.sp_blk[k] = blk;
+    if (k < c->K) {
+      off += cnt[k];
+      blk += (cnt[k] + per_block - 1) / per_block;
+    }
+  }
+  if (blk == 0) return 0;
+  prm.split[0] = 0;
+  prm.split[1] = c->K;
+  if (c->strips) nm::k_label<1, true, 2><<<blk, nm::kBlock, 0, st>>>(prm);
+  else nm::k_label<1, false, 2><<<blk, nm::kBlock, 0, st>>>(prm);
+  NM_CUDA(cudaGetLastError());
+  return 1;
+}
+
+// Certified-cell classification of the n evaluation positions (order[i]) and
+// per-compartment compaction of the pairs left to evaluate. Presets masks,
+// flagmask and the known s entries; returns the per-compartment counts (one
+// host synchronisation, for the grid size) with the lists in c->sp_list.
+std::vector<std::uint32_t> classify_cells(nm_ctx* c, const double* d_pts, std::size_t n, const std::uint32_t* order,
+                                          std::uint32_t* d_masks, std::uint32_t* flagmask, double* d_s, cudaStream_t st,
+                                          std::uint64_t& launches) {
+  const int K = c->K;
+  auto* unk = c->unk.as<std::uint32_t>(n);
+  const std::size_t nb = std::max<std::size_t>(1, (n + nm::kSelChunk - 1) / nm::kSelChunk);
+  auto* chunk = c->sp_chunk.as<std::uint32_t>(nb * K);
+  auto* dcnt = c->sp_cnt.as<std::uint32_t>(K);
+  (void)c->sp_list.as<std::uint32_t>(n);  // grown below if needed (after the sync)
+  nm::ClassifyParams cp{};
+  cp.pts = d_pts;
+  cp.n = n;
+  cp.order = order;
+  cp.cx = c->cx;
+  cp.cy = c->cy;
+  cp.cz = c->cz;
+  cp.dop4 = static_cast<const float4*>(c->comp_box.p);
+  cp.grids = static_cast<const nm::CellGrid*>(c->cell_grids.p);
+  cp.state = static_cast<const std::uint8_t*>(c->cell_state.p);
+  cp.K = K;
+  cp.unk = unk;
+  cp.masks = d_masks;
+  cp.flagmask = flagmask;
+  cp.s_out = d_s;
+  nm::k_cell_classify<<<grid_for(n, 256, c->sm_count * 16), 256, 0, st>>>(cp);
+  ++launches;
+  for (int k = 0; k < K; ++k) {
+    nm::k_select_count<<<static_cast<unsigned>(nb), nm::kSelBlock, 0, st>>>(nm::PredBit{unk, k}, n, chunk + k * nb);
+    nm::k_select_scan<<<1, 1024, 0, st>>>(chunk + k * nb, nb, dcnt + k);
+    launches += 2;
+  }
+  std::vector<std::uint32_t> cnt(K);
+  NM_CUDA(cudaMemcpyAsync(cnt.data(), dcnt, K * sizeof(std::uint32_t), cudaMemcpyDeviceToHost, st));
+  NM_CUDA(cudaStreamSynchronize(st));
+  std::size_t total = 0;
+  for (int k = 0; k < K; ++k) total += cnt[k];
+  auto* list = c->sp_list.as<std::uint32_t>(std::max<std::size_t>(total, 1));
+  std::size_t off = 0;
+  c->sparse_pairs = total;
+  c->sparse_evals = 0;
+  for (int k = 0; k < K; ++k) {
+    if (cnt[k]) {
+      nm::k_select_write<<<static_cast<unsigned>(nb), nm::kSelBlock, 0, st>>>(nm::PredBit{unk, k}, n, chunk + k * nb,
+                                                                              list + off);
+      ++launches;
+    }
+    off += cnt[k];
+    c->sparse_evals += std::uint64_t(cnt[k]) * (c->comp_off_h[k + 1] - c->comp_off_h[k]);
+  }
+  NM_CUDA(cudaGetLastError());
+  return cnt;
+}
+
 // stats_deferred: the caller collects the stats later with read_node_stats
 // (no host synchronisation inside; nm_label_mesh overlaps the tet upload).
 void label_nodes_dev(nm_ctx* c, const double* d_pts, std::size_t n, double T, std::uint32_t* d_masks, double* d_s,
@@ -368,6 +459,16 @@ void label_nodes_dev(nm_ctx* c, const double* d_pts, std::size_t n, double T, st
   prm.masks = d_masks;
   prm.flagmask = flagmask;
   prm.cull = nullptr;
+  if (c->opt.cull_outside == 2 && c->cells) {
+    // certified-cell culling: classification presets every known pair, the
+    // sparse pass evaluates the rest (one host synchronisation for its grid)
+    prm.s_out = d_s;
+    prm.counters = counters;
+    const std::vector<std::uint32_t> cnt = classify_cells(c, d_pts, n, order, d_masks, flagmask, d_s, st, launches);
+    prm.sp_list = static_cast<const std::uint32_t*>(c->sp_list.p);
+    if (stats) NM_CUDA(cudaEventRecord(c->ev[1], st));
+    launches += launch_sparse(c, prm, cnt, st);
+  } else {
   if (c->opt.cull_outside) {
     auto* cm = c->cullmask.as<std::uint32_t>(n);
     nm::k_cull_mask<<<grid_for(n, 256, c->sm_count * 16), 256, 0, st>>>(
@@ -390,12 +491,12 @@ void label_nodes_dev(nm_ctx* c, const double* d_pts, std::size_t n, double T, st
     const dim3 grid(static_cast<unsigned>(nblocks), static_cast<unsigned>(csplit));
     constexpr std::size_t smem = 0;  // k_label's tile buffers are static shared memory
     if (c->strips && prm.cull) {
-      nm::k_label<1, true, true><<<grid, nm::kBlock, smem, st>>>(prm);  // culling: one pair per thread
+      nm::k_label<1, true, 1><<<grid, nm::kBlock, smem, st>>>(prm);  // culling: one pair per thread
     } else if (c->strips) {
       if (np == 2) nm::k_label<2, true><<<grid, nm::kBlock, smem, st>>>(prm);
       else nm::k_label<1, true><<<grid, nm::kBlock, smem, st>>>(prm);
     } else if (prm.cull) {
-      nm::k_label<1, false, true><<<grid, nm::kBlock, smem, st>>>(prm);
+      nm::k_label<1, false, 1><<<grid, nm::kBlock, smem, st>>>(prm);
     } else {
       if (np == 2) nm::k_label<2, false><<<grid, nm::kBlock, smem, st>>>(prm);
       else nm::k_label<1, false><<<grid, nm::kBlock, smem, st>>>(prm);
@@ -403,6 +504,7 @@ void label_nodes_dev(nm_ctx* c, const double* d_pts, std::size_t n, double T, st
   }
   NM_CUDA(cudaGetLastError());
   ++launches;
+  }
   if (stats) NM_CUDA(cudaEventRecord(c->ev[2], st));
   // compaction of flagged points + fp64 fix-up
   select(c, nm::PredNonzero{flagmask, d_subset}, n, list, d_count, st, launches);
@@ -621,6 +723,215 @@ std::pair<std::size_t, std::size_t> refine_dev(nm_ctx* c, const double* d_nodes,
   NM_CUDA(cudaGetLastError());
   launches += 3;
   return {n2, nt2};
+}
+
+
+#ifndef NM_CELL_AXIS
+#define NM_CELL_AXIS 120
+#endif
+// Certified cells of every compartment (cells.cuh), built once per surface
+// set from the surfaces alone. hbox: the 13-DOP slabs (centred frame).
+void build_cells(nm_ctx* c, const double* xyz, const std::uint32_t* tri, const std::uint32_t* comp_off,
+                 const std::vector<float4>& hbox) {
+  const auto t0 = std::chrono::steady_clock::now();
+  const int K = c->K;
+  const double ctr[3] = {c->cx, c->cy, c->cz};
+  std::vector<nm::CellGrid> G(K);
+  std::vector<float4> clus;
+  std::vector<std::uint32_t> ctri;
+  std::vector<std::size_t> coff(K + 1, 0);
+  std::size_t total = 0;
+  for (int k = 0; k < K; ++k) {
+    coff[k] = clus.size();
+    const std::uint32_t b = comp_off[k], e = comp_off[k + 1];
+    nm::CellGrid g{0.0, 0.0, 0.0, 1.0, 0, 0, 0, static_cast<std::uint32_t>(total)};
+    if (e > b) {
+      double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
+      std::vector<std::pair<std::uint32_t, std::uint32_t>> kk;
+      kk.reserve(e - b);
+      for (std::uint32_t t = b; t < e; ++t) {
+        double m[3] = {0, 0, 0};
+        for (int v = 0; v < 3; ++v)
+          for (int a = 0; a < 3; ++a) {
+            const double x = xyz[3 * std::size_t(tri[3 * t + v]) + a] - ctr[a];
+            lo[a] = std::min(lo[a], x);
+            hi[a] = std::max(hi[a], x);
+            m[a] += x / 3.0;
+          }
+        std::uint32_t q[3];
+        for (int a = 0; a < 3; ++a)
+          q[a] = static_cast<std::uint32_t>(std::clamp((m[a] + ctr[a] - c->lo[a]) / c->span * 1024.0, 0.0, 1023.0));
+        kk.emplace_back(spread10h(q[0]) | (spread10h(q[1]) << 1) | (spread10h(q[2]) << 2), t);
+      }
+      std::stable_sort(kk.begin(), kk.end(), [](auto& x, auto& y) { return x.first < y.first; });
+      for (std::size_t i0 = 0; i0 < kk.size(); i0 += nm::kCluster) {
+        const std::size_t i1 = std::min(kk.size(), i0 + nm::kCluster);
+        double blo[3] = {1e300, 1e300, 1e300}, bhi[3] = {-1e300, -1e300, -1e300};
+        for (std::size_t i = i0; i < i1; ++i)
+          for (int v = 0; v < 3; ++v)
+            for (int a = 0; a < 3; ++a) {
+              const double x = xyz[3 * std::size_t(tri[3 * kk[i].second + v]) + a] - ctr[a];
+              blo[a] = std::min(blo[a], x);
+              bhi[a] = std::max(bhi[a], x);
+            }
+        const float fc[3] = {float(0.5 * (blo[0] + bhi[0])), float(0.5 * (blo[1] + bhi[1])), float(0.5 * (blo[2] + bhi[2]))};
+        double rho = 0.0;
+        for (std::size_t i = i0; i < i1; ++i)
+          for (int v = 0; v < 3; ++v) {
+            double d2 = 0.0;
+            for (int a = 0; a < 3; ++a) {
+              const double d = xyz[3 * std::size_t(tri[3 * kk[i].second + v]) + a] - ctr[a] - double(fc[a]);
+              d2 += d * d;
+            }
+            rho = std::max(rho, std::sqrt(d2));
+          }
+        clus.push_back(make_float4(fc[0], fc[1], fc[2], std::nextafter(float(rho * (1.0 + 1e-6) + 1e-5), INFINITY)));
+        for (std::size_t i = i0; i < i0 + nm::kCluster; ++i) ctri.push_back(i < i1 ? kk[i].second : 0xffffffffu);
+      }
+      const double ext = std::max({hi[0] - lo[0], hi[1] - lo[1], hi[2] - lo[2]});
+      g.B = std::max(ext / NM_CELL_AXIS, 1e-3);
+      int n3[3];
+      for (int a = 0; a < 3; ++a) n3[a] = static_cast<int>(std::ceil((hi[a] - lo[a]) / g.B)) + 2;
+      g.ox = lo[0] - g.B;
+      g.oy = lo[1] - g.B;
+      g.oz = lo[2] - g.B;
+      g.nx = n3[0];
+      g.ny = n3[1];
+      g.nz = n3[2];
+      total += static_cast<std::size_t>(g.nx) * g.ny * g.nz;
+      if (total > 0xffffffffull) throw Error("certified-cell grids exceed 2^32 cells");
+    }
+    G[k] = g;
+  }
+  coff[K] = clus.size();
+  cudaStream_t st = c->stream;
+  auto up = [&](DBuf& b, const void* src, std::size_t bytes) {
+    void* d = b.get(std::max<std::size_t>(bytes, 1));
+    if (bytes) NM_CUDA(cudaMemcpyAsync(d, src, bytes, cudaMemcpyHostToDevice, st));
+  };
+  up(c->clus, clus.data(), clus.size() * sizeof(float4));
+  up(c->clus_tri, ctri.data(), ctri.size() * sizeof(std::uint32_t));
+  auto* cert = c->cell_state.as<std::uint8_t>(std::max<std::size_t>(total, 1));
+  for (int k = 0; k < K; ++k) {
+    const std::size_t nc = static_cast<std::size_t>(G[k].nx) * G[k].ny * G[k].nz;
+    if (!nc) continue;
+    nm::k_cell_certify<<<static_cast<unsigned>((nc + 255) / 256), 256, 0, st>>>(
+        G[k], static_cast<const float4*>(c->clus.p) + coff[k], static_cast<int>(coff[k + 1] - coff[k]),
+        static_cast<const std::uint32_t*>(c->clus_tri.p) + coff[k] * nm::kCluster, static_cast<const double*>(c->xyz64.p),
+        static_cast<const std::uint32_t*>(c->tri_idx.p), c->cx, c->cy, c->cz, cert);
+  }
+  NM_CUDA(cudaGetLastError());
+  std::vector<std::uint8_t> state(total);
+  if (total) NM_CUDA(cudaMemcpyAsync(state.data(), cert, total, cudaMemcpyDeviceToHost, st));
+  NM_CUDA(cudaStreamSynchronize(st));
+
+  // x-runs of certified cells: 13-DOP-outside end -> w = 0, else one
+  // representative evaluation per run
+  auto outside_dop = [&](int k, double x, double y, double z) {
+    const float* dop = reinterpret_cast<const float*>(&hbox[static_cast<std::size_t>(k) * nm::kDopF4]);
+    const float xf = float(x), yf = float(y), zf = float(z);
+    for (int d = 0; d < nm::kDopDirs; ++d) {
+      const float pr = nm::dop_dir(d, 0) * xf + nm::dop_dir(d, 1) * yf + nm::dop_dir(d, 2) * zf;
+      if (pr < dop[2 * d] || pr > dop[2 * d + 1]) return true;
+    }
+    return false;
+  };
+  struct Run {
+    std::size_t first;
+    int len;
+  };
+  std::vector<Run> runs;
+  std::vector<double> reps;
+  std::vector<std::uint32_t> rep_cnt(K, 0);
+  std::uint64_t ncert = 0;
+  for (int k = 0; k < K; ++k) {
+    const nm::CellGrid& g = G[k];
+    for (int iz = 0; iz < g.nz; ++iz)
+      for (int iy = 0; iy < g.ny; ++iy) {
+        const std::size_t row = g.off + (static_cast<std::size_t>(iz) * g.ny + iy) * g.nx;
+        int ix = 0;
+        while (ix < g.nx) {
+          if (!state[row + ix]) {
+            ++ix;
+            continue;
+          }
+          int jx = ix;
+          while (jx + 1 < g.nx && state[row + jx + 1]) ++jx;
+          ncert += jx - ix + 1;
+          const double y = g.oy + (iy + 0.5) * g.B, z = g.oz + (iz + 0.5) * g.B;
+          const bool zero = ix == 0 || jx == g.nx - 1 || outside_dop(k, g.ox + (ix + 0.5) * g.B, y, z) ||
+                            outside_dop(k, g.ox + (jx + 0.5) * g.B, y, z);
+          if (zero) {
+            for (int q = ix; q <= jx; ++q) state[row + q] = 1;
+          } else {
+            const int mid = (ix + jx) / 2;
+            reps.push_back(g.ox + (mid + 0.5) * g.B + ctr[0]);
+            reps.push_back(y + ctr[1]);
+            reps.push_back(z + ctr[2]);
+            runs.push_back({row + ix, jx - ix + 1});
+            ++rep_cnt[k];
+            for (int q = ix; q <= jx; ++q) state[row + q] = 0;  // until its representative is known
+          }
+          ix = jx + 1;
+        }
+      }
+  }
+  const std::size_t R = runs.size();
+  if (R) {
+    // representatives: compartment k's reps are contiguous (k ascending)
+    up(c->rep_pts, reps.data(), reps.size() * sizeof(double));
+    auto* s_dev = c->rep_s.as<double>(R * K);
+    auto* m_dev = c->rep_m.as<std::uint32_t>(R);
+    auto* f_dev = c->rep_f.as<std::uint32_t>(R);
+    std::vector<std::uint32_t> iota(R);
+    std::iota(iota.begin(), iota.end(), 0u);
+    up(c->sp_list, iota.data(), R * sizeof(std::uint32_t));
+    NM_CUDA(cudaMemsetAsync(m_dev, 0, R * sizeof(std::uint32_t), st));
+    NM_CUDA(cudaMemsetAsync(f_dev, 0, R * sizeof(std::uint32_t), st));
+    nm::LabelParams prm{};
+    prm.pts = static_cast<const double*>(c->rep_pts.p);
+    prm.n = R;
+    prm.order = nullptr;
+    prm.tri = static_cast<const float4*>(c->tri.p);
+    prm.sub = static_cast<const float4*>(c->sub.p);
+    prm.edges = static_cast<const float4*>(c->edges.p);
+    prm.cont = static_cast<const std::uint32_t*>(c->cont.p);
+    prm.comp_tiles = static_cast<const std::uint32_t*>(c->comp_tiles.p);
+    prm.K = K;
+    prm.cx = c->cx;
+    prm.cy = c->cy;
+    prm.cz = c->cz;
+    prm.T = 0.5;
+    prm.band = c->opt.band;
+    prm.tau = c->opt.tau;
+    prm.delta = c->opt.delta_mm;
+    prm.masks = m_dev;
+    prm.flagmask = f_dev;
+    prm.s_out = s_dev;
+    prm.sp_list = static_cast<const std::uint32_t*>(c->sp_list.p);
+    launch_sparse(c, prm, rep_cnt, st);
+    std::vector<double> s(R * K);
+    NM_CUDA(cudaMemcpyAsync(s.data(), s_dev, R * K * sizeof(double), cudaMemcpyDeviceToHost, st));
+    NM_CUDA(cudaStreamSynchronize(st));
+    std::size_t r = 0;
+    for (int k = 0; k < K; ++k)
+      for (std::uint32_t q = 0; q < rep_cnt[k]; ++q, ++r) {
+        const double v = s[r * K + k];
+        const double w = std::round(v);
+        if (std::fabs(v - w) < 1e-3 && (w == 0.0 || w == 1.0))
+          std::memset(&state[runs[r].first], w == 1.0 ? 2 : 1, runs[r].len);
+      }
+  }
+  up(c->cell_state, state.data(), total);
+  up(c->cell_grids, G.data(), G.size() * sizeof(nm::CellGrid));
+  NM_CUDA(cudaStreamSynchronize(st));
+  c->cells_total = total;
+  c->cells_certified = 0;
+  for (std::uint8_t v : state) c->cells_certified += v != 0;
+  (void)ncert;
+  c->cell_reps = R;
+  c->cells = true;
+  c->ms_cells = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
 }
 
 }  // namespace
@@ -1033,7 +1344,23 @@ int nm_set_surfaces(nm_ctx* c, const double* xyz, std::size_t nv, const std::uin
     c->nt_pad = npad;
     c->nv = nv;
     for (int k = 0; k < 32; ++k) c->ids.id[k] = k < K ? label_ids[k] : 0;
+    c->comp_off_h.assign(comp_off, comp_off + K + 1);
+    c->cells = false;
     c->has_surfaces = true;
+    if (c->opt.cull_outside == 2) build_cells(c, xyz, tri, comp_off, hbox);
+  });
+}
+
+int nm_cell_info(nm_ctx* c, uint64_t* cells, uint64_t* certified, uint64_t* reps, double* ms_build,
+                 uint64_t* last_pairs, uint64_t* last_evals) {
+  return guarded([&] {
+    require_surfaces(c);
+    if (cells) *cells = c->cells_total;
+    if (certified) *certified = c->cells_certified;
+    if (reps) *reps = c->cell_reps;
+    if (ms_build) *ms_build = c->ms_cells;
+    if (last_pairs) *last_pairs = c->sparse_pairs;
+    if (last_evals) *last_evals = c->sparse_evals;
   });
 }
 

@@ -475,6 +475,46 @@ def test_outside_culling_exact():
     np.testing.assert_array_equal(s_sub, s_cull[idx])
 
 
+@pytest.mark.parametrize("cfg_id,lo,hi", [(3, 2_000_000, 2_200_000), (2, 0, 1_300_000)])
+def test_cell_culling_exact(cfg_id, lo, hi):
+    """cull_outside=2 (certified cells): a pair resolved by a certified cell
+    gets its exact winding number (0 or 1), every evaluated pair is
+    bit-identical to the full evaluation, masks are unchanged, the fp64
+    oracle agrees on a sample of resolved points, and results do not depend
+    on the point set (a strided subset reproduces its rows bitwise)."""
+    from paper_2203_10000_b200._native import Context
+    cfg = synth.config(cfg_id)
+    S = cfg.surfaces
+    nodes = cfg.lattice_nodes()[lo:hi]
+    with Context(0) as full, Context(0, cull_outside=2) as cell:
+        for c in (full, cell):
+            c.set_surfaces(S.xyz, S.tri, S.comp_off, S.label_ids)
+        info0 = cell.cell_info()
+        assert 0 < info0["certified"] <= info0["cells"]
+        s_full, _ = full.enclosure(nodes)
+        s_cell, _ = cell.enclosure(nodes)
+        info = cell.cell_info()
+        m_full, _ = full.label_nodes(nodes)
+        m_cell, _ = cell.label_nodes(nodes)
+        idx = np.arange(3, nodes.shape[0], 11)
+        s_sub, _ = cell.enclosure(nodes[idx])
+        m_sub, _ = cell.label_nodes(nodes[idx])
+    np.testing.assert_array_equal(m_cell, m_full)
+    np.testing.assert_array_equal(m_sub, m_full[idx])
+    np.testing.assert_array_equal(s_sub, s_cell[idx])
+    resolved = (s_cell == 0.0) | (s_cell == 1.0)
+    assert info["last_pairs"] < 0.6 * s_full.size    # most pairs are resolved without evaluation
+    diff = s_cell != s_full
+    assert np.all(resolved[diff])                     # only resolved pairs may differ ...
+    assert np.max(np.abs(s_full[diff] - s_cell[diff])) < 1e-5   # ... and only by fp32 rounding
+    rng = np.random.default_rng(cfg_id)
+    rows = np.unique(np.nonzero(diff)[0])
+    pick = np.sort(rng.choice(rows, min(300, rows.size), replace=False))
+    _, s_ref = oracle.label_nodes(nodes[pick], S, want_s=True)
+    sel = diff[pick]
+    np.testing.assert_allclose(s_cell[pick][sel], s_ref[sel], rtol=0, atol=1e-9)
+
+
 def test_cfg5_full_size_properties():
     """BASELINE configs[4] at full size (10,077,696 nodes x 983,040 triangles):
     size-independent properties over every node, the fp64 oracle on a seeded
@@ -525,11 +565,12 @@ def test_cfg5_full_size_properties():
     m_b, _ = c.label_nodes(nodes[half:])
     np.testing.assert_array_equal(np.concatenate([m_a, m_b]), m_all)
 
-    cc = Context(0, cull_outside=1)
-    cc.set_surfaces(S.xyz, S.tri, S.comp_off, S.label_ids)
-    m_cull, _ = cc.label_nodes(nodes)
-    np.testing.assert_array_equal(m_cull, m_all)
-    cc.close()
+    for mode in (1, 2):
+        cc = Context(0, cull_outside=mode)
+        cc.set_surfaces(S.xyz, S.tri, S.comp_off, S.label_ids)
+        m_cull, _ = cc.label_nodes(nodes)
+        np.testing.assert_array_equal(m_cull, m_all)
+        cc.close()
 
     labels, _, _ = c.label_mesh(nodes, tets)
     tidx = rng.choice(tets.shape[0], 200000, replace=False)
