@@ -9,6 +9,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <exception>
 #include <memory>
 #include <numeric>
@@ -16,6 +17,8 @@
 #include <unordered_map>
 #include <stdexcept>
 #include <string>
+#include <thread>
+#include <atomic>
 #include <vector>
 
 #include <cub/device/device_radix_sort.cuh>
@@ -224,7 +227,7 @@ struct nm_ctx {
   DBuf tri, sub, edges, cont, comp_tiles, xyz64, tri_idx, comp_off, comp_box, cullmask;
   // certified cells (cull_outside = 2, cells.cuh)
   bool cells = false;
-  DBuf cell_state, cell_grids, clus, clus_tri, unk, sp_list, sp_chunk, sp_cnt, rep_pts, rep_s, rep_m, rep_f;
+  DBuf cell_state, cell_child, cell_grids, clus, clus_tri, clus_tsph, unk, sp_list, sp_chunk, sp_cnt, rep_pts, rep_s, rep_m, rep_f;
   std::uint64_t cells_total = 0, cells_certified = 0, cell_reps = 0, sparse_pairs = 0, sparse_evals = 0;
   double ms_cells = 0.0;  // host wall time of the certification (nm_set_surfaces)
   std::vector<std::uint32_t> comp_off_h;
@@ -237,7 +240,7 @@ struct nm_ctx {
       s_out, word;
 
   ~nm_ctx() {
-    for (DBuf* b : {&cell_state, &cell_grids, &clus, &clus_tri, &unk, &sp_list, &sp_chunk, &sp_cnt, &rep_pts, &rep_s,
+    for (DBuf* b : {&cell_state, &cell_child, &cell_grids, &clus, &clus_tri, &clus_tsph, &unk, &sp_list, &sp_chunk, &sp_cnt, &rep_pts, &rep_s,
                     &rep_m, &rep_f})
       b->release();
     for (DBuf* b : {&tri, &sub, &edges, &cont, &comp_tiles, &xyz64, &tri_idx, &comp_off, &comp_box, &cullmask, &pts, &masks, &flagmask, &nbr, &known, &want, &fkeys, &frontier, &lex, &region, &bfaces, &btri,
@@ -362,7 +365,8 @@ std::vector<std::uint32_t> classify_cells(nm_ctx* c, const double* d_pts, std::s
   cp.cz = c->cz;
   cp.dop4 = static_cast<const float4*>(c->comp_box.p);
   cp.grids = static_cast<const nm::CellGrid*>(c->cell_grids.p);
-  cp.state = static_cast<const std::uint8_t*>(c->cell_state.p);
+  cp.code = static_cast<const std::uint32_t*>(c->cell_state.p);
+  cp.child = static_cast<const std::uint8_t*>(c->cell_child.p);
   cp.K = K;
   cp.unk = unk;
   cp.masks = d_masks;
@@ -734,11 +738,20 @@ std::pair<std::size_t, std::size_t> refine_dev(nm_ctx* c, const double* d_nodes,
 void build_cells(nm_ctx* c, const double* xyz, const std::uint32_t* tri, const std::uint32_t* comp_off,
                  const std::vector<float4>& hbox) {
   const auto t0 = std::chrono::steady_clock::now();
+  const bool verbose = std::getenv("NM_CELL_VERBOSE") != nullptr;
+  auto tl = t0;
+  auto lap = [&](const char* what) {
+    if (!verbose) return;
+    const auto t = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[cells] %-6s %8.1f ms\n", what, std::chrono::duration<double, std::milli>(t - tl).count());
+    tl = t;
+  };
   const int K = c->K;
   const double ctr[3] = {c->cx, c->cy, c->cz};
   std::vector<nm::CellGrid> G(K);
   std::vector<float4> clus;
   std::vector<std::uint32_t> ctri;
+  std::vector<float4> tsph;
   std::vector<std::size_t> coff(K + 1, 0);
   std::size_t total = 0;
   for (int k = 0; k < K; ++k) {
@@ -785,8 +798,36 @@ void build_cells(nm_ctx* c, const double* xyz, const std::uint32_t* tri, const s
             }
             rho = std::max(rho, std::sqrt(d2));
           }
-        clus.push_back(make_float4(fc[0], fc[1], fc[2], std::nextafter(float(rho * (1.0 + 1e-6) + 1e-5), INFINITY)));
-        for (std::size_t i = i0; i < i0 + nm::kCluster; ++i) ctri.push_back(i < i1 ? kk[i].second : 0xffffffffu);
+        const double rel = 4e-6 * (std::fabs(fc[0]) + std::fabs(fc[1]) + std::fabs(fc[2]));
+        clus.push_back(make_float4(fc[0], fc[1], fc[2], std::nextafter(float(rho * (1.0 + 1e-6) + 1e-5 + rel), INFINITY)));
+        for (std::size_t i = i0; i < i0 + nm::kCluster; ++i) {
+          ctri.push_back(i < i1 ? kk[i].second : 0xffffffffu);
+          // the triangle's bounding sphere (vertex-box centre), same rounding margins as the cluster's
+          float4 ts = make_float4(0.f, 0.f, 0.f, -1e30f);
+          if (i < i1) {
+            double tlo[3] = {1e300, 1e300, 1e300}, thi[3] = {-1e300, -1e300, -1e300};
+            for (int v = 0; v < 3; ++v)
+              for (int a = 0; a < 3; ++a) {
+                const double x = xyz[3 * std::size_t(tri[3 * kk[i].second + v]) + a] - ctr[a];
+                tlo[a] = std::min(tlo[a], x);
+                thi[a] = std::max(thi[a], x);
+              }
+            const float tc[3] = {float(0.5 * (tlo[0] + thi[0])), float(0.5 * (tlo[1] + thi[1])),
+                                 float(0.5 * (tlo[2] + thi[2]))};
+            double tr = 0.0;
+            for (int v = 0; v < 3; ++v) {
+              double d2 = 0.0;
+              for (int a = 0; a < 3; ++a) {
+                const double d = xyz[3 * std::size_t(tri[3 * kk[i].second + v]) + a] - ctr[a] - double(tc[a]);
+                d2 += d * d;
+              }
+              tr = std::max(tr, std::sqrt(d2));
+            }
+            const double trel = 4e-6 * (std::fabs(tc[0]) + std::fabs(tc[1]) + std::fabs(tc[2]));
+            ts = make_float4(tc[0], tc[1], tc[2], std::nextafter(float(tr * (1.0 + 1e-6) + 1e-5 + trel), INFINITY));
+          }
+          tsph.push_back(ts);
+        }
       }
       const double ext = std::max({hi[0] - lo[0], hi[1] - lo[1], hi[2] - lo[2]});
       g.B = std::max(ext / NM_CELL_AXIS, 1e-3);
@@ -804,6 +845,7 @@ void build_cells(nm_ctx* c, const double* xyz, const std::uint32_t* tri, const s
     G[k] = g;
   }
   coff[K] = clus.size();
+  lap("setup");
   cudaStream_t st = c->stream;
   auto up = [&](DBuf& b, const void* src, std::size_t bytes) {
     void* d = b.get(std::max<std::size_t>(bytes, 1));
@@ -811,22 +853,81 @@ void build_cells(nm_ctx* c, const double* xyz, const std::uint32_t* tri, const s
   };
   up(c->clus, clus.data(), clus.size() * sizeof(float4));
   up(c->clus_tri, ctri.data(), ctri.size() * sizeof(std::uint32_t));
-  auto* cert = c->cell_state.as<std::uint8_t>(std::max<std::size_t>(total, 1));
+  up(c->clus_tsph, tsph.data(), tsph.size() * sizeof(float4));
+  auto clus_k = [&](int k) { return static_cast<const float4*>(c->clus.p) + coff[k]; };
+  auto ctri_k = [&](int k) { return static_cast<const std::uint32_t*>(c->clus_tri.p) + coff[k] * nm::kCluster; };
+  auto tsph_k = [&](int k) { return static_cast<const float4*>(c->clus_tsph.p) + coff[k] * nm::kCluster; };
+  const int ncl_max = 0;
+  (void)ncl_max;
+
+  // ---- level 1 ----
+  auto* cert_d = c->rep_m.as<std::uint8_t>(std::max<std::size_t>(total, 1));
   for (int k = 0; k < K; ++k) {
     const std::size_t nc = static_cast<std::size_t>(G[k].nx) * G[k].ny * G[k].nz;
     if (!nc) continue;
-    nm::k_cell_certify<<<static_cast<unsigned>((nc + 255) / 256), 256, 0, st>>>(
-        G[k], static_cast<const float4*>(c->clus.p) + coff[k], static_cast<int>(coff[k + 1] - coff[k]),
-        static_cast<const std::uint32_t*>(c->clus_tri.p) + coff[k] * nm::kCluster, static_cast<const double*>(c->xyz64.p),
-        static_cast<const std::uint32_t*>(c->tri_idx.p), c->cx, c->cy, c->cz, cert);
+    const std::size_t nbrick = static_cast<std::size_t>((G[k].nx + 3) / 4) * ((G[k].ny + 3) / 4) * ((G[k].nz + 1) / 2);
+    nm::k_cell_certify<<<static_cast<unsigned>((nbrick * 32 + 255) / 256), 256, 0, st>>>(
+        G[k], clus_k(k), static_cast<int>(coff[k + 1] - coff[k]), ctri_k(k), tsph_k(k), static_cast<const double*>(c->xyz64.p),
+        static_cast<const std::uint32_t*>(c->tri_idx.p), c->cx, c->cy, c->cz, cert_d);
   }
   NM_CUDA(cudaGetLastError());
-  std::vector<std::uint8_t> state(total);
-  if (total) NM_CUDA(cudaMemcpyAsync(state.data(), cert, total, cudaMemcpyDeviceToHost, st));
+  std::vector<std::uint8_t> cert1(total);
+  if (total) NM_CUDA(cudaMemcpyAsync(cert1.data(), cert_d, total, cudaMemcpyDeviceToHost, st));
   NM_CUDA(cudaStreamSynchronize(st));
+  lap("l1");
 
-  // x-runs of certified cells: 13-DOP-outside end -> w = 0, else one
-  // representative evaluation per run
+  // ---- level 2: children of every uncertified cell ----
+  // (host loops run one compartment per thread; every compartment's grid,
+  // blocks, runs and representatives are independent)
+  auto parallel_k = [&](auto&& f) {
+    const int nth = std::max(1, std::min<int>(K, static_cast<int>(std::thread::hardware_concurrency())));
+    std::atomic<int> next{0};
+    std::vector<std::thread> th;
+    for (int t = 0; t < nth; ++t)
+      th.emplace_back([&] {
+        for (int k; (k = next++) < K;) f(k);
+      });
+    for (auto& x : th) x.join();
+  };
+  std::vector<std::uint32_t> block_of(total, 0xffffffffu);  // local block index within the compartment
+  std::vector<std::vector<std::uint32_t>> blk_k(K);          // local cell index per local block
+  parallel_k([&](int k) {
+    const std::size_t nc = static_cast<std::size_t>(G[k].nx) * G[k].ny * G[k].nz;
+    for (std::size_t q = 0; q < nc; ++q)
+      if (!cert1[G[k].off + q]) {
+        block_of[G[k].off + q] = static_cast<std::uint32_t>(blk_k[k].size());
+        blk_k[k].push_back(static_cast<std::uint32_t>(q));
+      }
+  });
+  std::vector<std::size_t> boff(K + 1, 0);
+  for (int k = 0; k < K; ++k) boff[k + 1] = boff[k] + blk_k[k].size();
+  lap("blocks");
+  const std::size_t nblk = boff[K];
+  std::vector<std::uint8_t> child(nblk * nm::kChildren);
+  if (nblk) {
+    std::vector<std::uint32_t> blk_cells(nblk);
+    for (int k = 0; k < K; ++k) std::copy(blk_k[k].begin(), blk_k[k].end(), blk_cells.begin() + boff[k]);
+    up(c->sp_chunk, blk_cells.data(), nblk * sizeof(std::uint32_t));
+    auto* ch_d = c->cell_state.as<std::uint8_t>(nblk * nm::kChildren);
+    for (int k = 0; k < K; ++k) {
+      const std::size_t nb = boff[k + 1] - boff[k];
+      if (!nb) continue;
+      nm::k_child_certify<<<static_cast<unsigned>((nb * 64 + 255) / 256), 256, 0, st>>>(
+          G[k], static_cast<const std::uint32_t*>(c->sp_chunk.p) + boff[k], nb, clus_k(k),
+          static_cast<int>(coff[k + 1] - coff[k]), ctri_k(k), tsph_k(k), static_cast<const double*>(c->xyz64.p),
+          static_cast<const std::uint32_t*>(c->tri_idx.p), c->cx, c->cy, c->cz, ch_d + boff[k] * nm::kChildren);
+    }
+    NM_CUDA(cudaGetLastError());
+    if (verbose) {
+      NM_CUDA(cudaStreamSynchronize(st));
+      lap("l2kern");
+    }
+    NM_CUDA(cudaMemcpyAsync(child.data(), ch_d, child.size(), cudaMemcpyDeviceToHost, st));
+    NM_CUDA(cudaStreamSynchronize(st));
+  }
+  lap("l2");
+
+  // ---- winding numbers of runs ----
   auto outside_dop = [&](int k, double x, double y, double z) {
     const float* dop = reinterpret_cast<const float*>(&hbox[static_cast<std::size_t>(k) * nm::kDopF4]);
     const float xf = float(x), yf = float(y), zf = float(z);
@@ -836,50 +937,102 @@ void build_cells(nm_ctx* c, const double* xyz, const std::uint32_t* tri, const s
     }
     return false;
   };
-  struct Run {
-    std::size_t first;
-    int len;
+  // run value: 0 / 1 known; kRep + r: local representative r of the
+  // compartment; kRun + q: the value of the compartment's level-1 run q
+  constexpr std::int64_t kUnknown = -1, kRep = 1ll << 40, kRun = 1ll << 41;
+  constexpr int S = nm::kSubCells;
+  struct FineRun {
+    std::size_t row;  // level-1 row base (global cell index of ix = 0)
+    int fx0, fx1;     // fine x range (fine index = 4 ix + sx)
+    int sy, sz;
+    std::int64_t v;
   };
-  std::vector<Run> runs;
-  std::vector<double> reps;
-  std::vector<std::uint32_t> rep_cnt(K, 0);
-  std::uint64_t ncert = 0;
-  for (int k = 0; k < K; ++k) {
+  std::vector<std::vector<double>> reps(K);
+  std::vector<std::vector<std::int64_t>> run_val(K);   // level-1 runs per compartment
+  std::vector<std::int32_t> run_of(total, -1);         // level-1 cell -> its local run
+  std::vector<std::vector<FineRun>> fine(K);
+  auto child_at = [&](int k, std::size_t row, int fx, int sy, int sz) -> std::uint8_t& {
+    const std::size_t b = boff[k] + block_of[row + fx / S];
+    return child[b * nm::kChildren + (sz * S + sy) * S + fx % S];
+  };
+  parallel_k([&](int k) {
     const nm::CellGrid& g = G[k];
+    auto new_rep = [&](double x, double y, double z) {
+      const std::int64_t v = kRep + static_cast<std::int64_t>(reps[k].size() / 3);
+      reps[k].insert(reps[k].end(), {x + ctr[0], y + ctr[1], z + ctr[2]});
+      return v;
+    };
     for (int iz = 0; iz < g.nz; ++iz)
       for (int iy = 0; iy < g.ny; ++iy) {
         const std::size_t row = g.off + (static_cast<std::size_t>(iz) * g.ny + iy) * g.nx;
-        int ix = 0;
-        while (ix < g.nx) {
-          if (!state[row + ix]) {
-            ++ix;
-            continue;
-          }
+        const double y = g.oy + (iy + 0.5) * g.B, z = g.oz + (iz + 0.5) * g.B;
+        for (int ix = 0; ix < g.nx;) {
+          const bool c1 = cert1[row + ix];
           int jx = ix;
-          while (jx + 1 < g.nx && state[row + jx + 1]) ++jx;
-          ncert += jx - ix + 1;
-          const double y = g.oy + (iy + 0.5) * g.B, z = g.oz + (iz + 0.5) * g.B;
-          const bool zero = ix == 0 || jx == g.nx - 1 || outside_dop(k, g.ox + (ix + 0.5) * g.B, y, z) ||
-                            outside_dop(k, g.ox + (jx + 0.5) * g.B, y, z);
-          if (zero) {
-            for (int q = ix; q <= jx; ++q) state[row + q] = 1;
+          while (jx + 1 < g.nx && bool(cert1[row + jx + 1]) == c1) ++jx;
+          if (c1) {
+            // level-1 run [ix, jx]
+            std::int64_t v;
+            if (ix == 0 || jx == g.nx - 1 || outside_dop(k, g.ox + (ix + 0.5) * g.B, y, z) ||
+                outside_dop(k, g.ox + (jx + 0.5) * g.B, y, z))
+              v = 0;
+            else
+              v = new_rep(g.ox + ((ix + jx) / 2 + 0.5) * g.B, y, z);
+            for (int q = ix; q <= jx; ++q) run_of[row + q] = static_cast<std::int32_t>(run_val[k].size());
+            run_val[k].push_back(v);
           } else {
-            const int mid = (ix + jx) / 2;
-            reps.push_back(g.ox + (mid + 0.5) * g.B + ctr[0]);
-            reps.push_back(y + ctr[1]);
-            reps.push_back(z + ctr[2]);
-            runs.push_back({row + ix, jx - ix + 1});
-            ++rep_cnt[k];
-            for (int q = ix; q <= jx; ++q) state[row + q] = 0;  // until its representative is known
+            // segment [ix, jx] of uncertified cells: runs of certified children per (sy, sz) sub-row
+            const double b = g.B / S;
+            const int f_lo = S * ix, f_hi = S * jx + S - 1;
+            for (int sz = 0; sz < S; ++sz)
+              for (int sy = 0; sy < S; ++sy)
+                for (int f = f_lo; f <= f_hi;) {
+                  if (!child_at(k, row, f, sy, sz)) {
+                    ++f;
+                    continue;
+                  }
+                  int e = f;
+                  while (e + 1 <= f_hi && child_at(k, row, e + 1, sy, sz)) ++e;
+                  std::int64_t v;
+                  if (f == f_lo) {
+                    v = ix == 0 ? 0 : -2;  // left neighbour's run, resolved below (its run id may not exist yet)
+                  } else if (e == f_hi) {
+                    v = jx == g.nx - 1 ? 0 : -3;  // right neighbour's run
+                  } else {
+                    const double yy = g.oy + iy * g.B + (sy + 0.5) * b, zz = g.oz + iz * g.B + (sz + 0.5) * b;
+                    if (outside_dop(k, g.ox + (f + 0.5) * b, yy, zz) || outside_dop(k, g.ox + (e + 0.5) * b, yy, zz))
+                      v = 0;
+                    else
+                      v = new_rep(g.ox + ((f + e) / 2 + 0.5) * b, yy, zz);
+                  }
+                  fine[k].push_back({row, f, e, sy, sz, v});
+                  f = e + 1;
+                }
           }
           ix = jx + 1;
         }
       }
+    // neighbour references: the level-1 runs of the whole row exist now
+    for (FineRun& fr : fine[k]) {
+      if (fr.v == -2) fr.v = kRun + run_of[fr.row + fr.fx0 / S - 1];
+      else if (fr.v == -3) fr.v = kRun + run_of[fr.row + fr.fx1 / S + 1];
+    }
+  });
+  lap("runs");
+
+  // ---- representatives (compartment k's are contiguous) ----
+  std::vector<std::uint32_t> rep_cnt(K, 0), rep_first(K + 1, 0);
+  std::vector<double> rep_all;
+  for (int k = 0; k < K; ++k) {
+    rep_first[k] = static_cast<std::uint32_t>(rep_all.size() / 3);
+    rep_cnt[k] = static_cast<std::uint32_t>(reps[k].size() / 3);
+    rep_all.insert(rep_all.end(), reps[k].begin(), reps[k].end());
   }
-  const std::size_t R = runs.size();
+  const std::size_t R = rep_all.size() / 3;
+  rep_first[K] = static_cast<std::uint32_t>(R);
+  std::vector<double> rep_w(R, -1.0);
   if (R) {
-    // representatives: compartment k's reps are contiguous (k ascending)
-    up(c->rep_pts, reps.data(), reps.size() * sizeof(double));
+    up(c->rep_pts, rep_all.data(), rep_all.size() * sizeof(double));
     auto* s_dev = c->rep_s.as<double>(R * K);
     auto* m_dev = c->rep_m.as<std::uint32_t>(R);
     auto* f_dev = c->rep_f.as<std::uint32_t>(R);
@@ -913,22 +1066,52 @@ void build_cells(nm_ctx* c, const double* xyz, const std::uint32_t* tri, const s
     std::vector<double> s(R * K);
     NM_CUDA(cudaMemcpyAsync(s.data(), s_dev, R * K * sizeof(double), cudaMemcpyDeviceToHost, st));
     NM_CUDA(cudaStreamSynchronize(st));
-    std::size_t r = 0;
     for (int k = 0; k < K; ++k)
-      for (std::uint32_t q = 0; q < rep_cnt[k]; ++q, ++r) {
-        const double v = s[r * K + k];
+      for (std::uint32_t r = rep_first[k]; r < rep_first[k + 1]; ++r) {
+        const double v = s[static_cast<std::size_t>(r) * K + k];
         const double w = std::round(v);
-        if (std::fabs(v - w) < 1e-3 && (w == 0.0 || w == 1.0))
-          std::memset(&state[runs[r].first], w == 1.0 ? 2 : 1, runs[r].len);
+        if (std::fabs(v - w) < 1e-3 && (w == 0.0 || w == 1.0)) rep_w[r] = w;
       }
   }
-  up(c->cell_state, state.data(), total);
+  lap("reps");
+  std::vector<std::uint32_t> code(total, 0);
+  lap("alloc");
+  parallel_k([&](int k) {
+    auto resolve = [&](std::int64_t v) -> std::int64_t {  // -> 0, 1 or kUnknown
+      if (v >= kRun) v = run_val[k][static_cast<std::size_t>(v - kRun)];
+      if (v >= kRep) {
+        const double w = rep_w[rep_first[k] + static_cast<std::size_t>(v - kRep)];
+        return w < 0.0 ? kUnknown : static_cast<std::int64_t>(w);
+      }
+      return v;
+    };
+    const nm::CellGrid& g = G[k];
+    const std::size_t nc = static_cast<std::size_t>(g.nx) * g.ny * g.nz;
+    for (std::size_t q = g.off; q < g.off + nc; ++q) {
+      if (!cert1[q]) {
+        code[q] = 3u + static_cast<std::uint32_t>(boff[k] + block_of[q]);
+      } else {
+        const std::int64_t w = resolve(run_val[k][run_of[q]]);
+        code[q] = w == kUnknown ? 0u : static_cast<std::uint32_t>(1 + w);
+      }
+    }
+    std::fill(child.begin() + boff[k] * nm::kChildren, child.begin() + boff[k + 1] * nm::kChildren, 0);
+    for (const FineRun& fr : fine[k]) {
+      const std::int64_t w = resolve(fr.v);
+      if (w == kUnknown) continue;
+      for (int f = fr.fx0; f <= fr.fx1; ++f) child_at(k, fr.row, f, fr.sy, fr.sz) = static_cast<std::uint8_t>(1 + w);
+    }
+  });
+  lap("codes");
+  up(c->cell_state, code.data(), total * sizeof(std::uint32_t));
+  up(c->cell_child, child.data(), child.size());
   up(c->cell_grids, G.data(), G.size() * sizeof(nm::CellGrid));
   NM_CUDA(cudaStreamSynchronize(st));
-  c->cells_total = total;
+  lap("final");
+  c->cells_total = total + child.size();
   c->cells_certified = 0;
-  for (std::uint8_t v : state) c->cells_certified += v != 0;
-  (void)ncert;
+  for (std::size_t q = 0; q < total; ++q) c->cells_certified += code[q] == 1 || code[q] == 2;
+  for (std::uint8_t v : child) c->cells_certified += v != 0;
   c->cell_reps = R;
   c->cells = true;
   c->ms_cells = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();

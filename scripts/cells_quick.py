@@ -11,7 +11,7 @@ cfg = synth.config(cfg_id)
 S = cfg.surfaces
 nodes = cfg.lattice_nodes()
 res = {}
-for mode in (1, 2):
+for mode in (1, 2, 2):
     ctx = Context(0, cull_outside=mode)
     t0 = time.perf_counter()
     ctx.set_surfaces(S.xyz, S.tri, S.comp_off, S.label_ids)
