@@ -230,6 +230,24 @@ def run_recursive(args):
         "recursive_equals_full_relabel": bool(np.array_equal(lab, lab_full) and np.array_equal(masks, m_full)),
         "labeling_stats_last_step": {k: st[k] for k in ("flagged_points", "ties", "near_subtiles", "far_subtiles")},
     }
+    # the same driver with certified-cell culling (cull_outside=2, the C++
+    # drop-in's default): initial labels + both refinement levels
+    cc = Context(0, cull_outside=2)
+    t0 = time.perf_counter()
+    cc.set_surfaces(S.xyz, S.tri, S.comp_off, S.label_ids)
+    t_set = time.perf_counter() - t0
+    cw = []
+    for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        mc, stc0 = cc.label_nodes(nodes)
+        n2c, t2c, labc, masksc, stc = cc.refine_relabel(nodes, tets, masks=mc, levels=args.levels)
+        if i >= args.warmup:
+            cw.append(time.perf_counter() - t0)
+    line["cull_outside_mode2"] = {
+        "driver_wall_ms_incl_initial_label": sum(cw) / len(cw) * 1e3, "set_surfaces_s": t_set,
+        "labels_identical": bool(np.array_equal(labc, lab) and np.array_equal(n2c, n2) and np.array_equal(t2c, t2)),
+        "initial_label_ms": stc0["ms_total"]}
+    cc.close()
     print(json.dumps(line), flush=True)
     ctx.close()
     del torch
@@ -436,6 +454,18 @@ def main():
             same = bool(torch.equal(cl, d_labels))
             entry = {"full_mesh_labeling_time_s": sum(cms) / len(cms) / 1e3, "labels_identical": same,
                      "set_surfaces_s": t_set, "note": notes[mode]}
+            if e2e is not None and not use_dist:
+                # the same through the host-buffer C ABI (nm_label_mesh: H2D nodes + tets, D2H labels), wall clock
+                hl, _, _ = cctx.label_mesh(h_nodes.numpy(), h_tets.numpy().view(np.uint32))
+                wt = []
+                for i in range(args.steps):
+                    flush.fill_(i)
+                    torch.cuda.synchronize()
+                    t0 = time.perf_counter()
+                    hl, _, _ = cctx.label_mesh(h_nodes.numpy(), h_tets.numpy().view(np.uint32))
+                    wt.append(time.perf_counter() - t0)
+                entry["e2e_full_mesh_labeling_time_s"] = sum(wt) / len(wt)
+                entry["e2e_labels_identical"] = bool(np.array_equal(hl, cl.cpu().numpy()))
             if mode == 2:
                 ci = cctx.cell_info()
                 entry.update({"cells": ci["cells"], "certified_cells": ci["certified"],
