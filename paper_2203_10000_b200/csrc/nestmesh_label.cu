@@ -88,6 +88,24 @@ struct DBuf {
   }
 };
 
+// Run f(0..n-1) on up to hardware_concurrency host threads (independent
+// per-compartment host work of nm_set_surfaces; f must not throw).
+template <class F>
+void parallel_for(int n, F&& f) {
+  const int nth = std::max(1, std::min<int>(n, static_cast<int>(std::thread::hardware_concurrency())));
+  if (nth <= 1) {
+    for (int k = 0; k < n; ++k) f(k);
+    return;
+  }
+  std::atomic<int> next{0};
+  std::vector<std::thread> th;
+  for (int t = 0; t < nth; ++t)
+    th.emplace_back([&] {
+      for (int k; (k = next++) < n;) f(k);
+    });
+  for (auto& x : th) x.join();
+}
+
 // Morton order of triangle centroids (per compartment): compact 256-triangle
 // tiles and 32-triangle subtiles for the near/far split. Order affects only
 // the fp32 summation order, never which triangles are summed.
@@ -227,7 +245,7 @@ struct nm_ctx {
   DBuf tri, sub, edges, cont, comp_tiles, xyz64, tri_idx, comp_off, comp_box, cullmask;
   // certified cells (cull_outside = 2, cells.cuh)
   bool cells = false;
-  DBuf cell_state, cell_child, cell_grids, clus, clus_tri, clus_tsph, unk, sp_list, sp_chunk, sp_cnt, rep_pts, rep_s, rep_m, rep_f;
+  DBuf cell_state, cell_child, cell_cert, cell_blk, cell_grids, clus, clus_tri, clus_tsph, unk, sp_list, sp_chunk, sp_cnt, rep_pts, rep_s, rep_m, rep_f;
   std::uint64_t cells_total = 0, cells_certified = 0, cell_reps = 0, sparse_pairs = 0, sparse_evals = 0;
   double ms_cells = 0.0;  // host wall time of the certification (nm_set_surfaces)
   std::vector<std::uint32_t> comp_off_h;
@@ -240,7 +258,7 @@ struct nm_ctx {
       s_out, word;
 
   ~nm_ctx() {
-    for (DBuf* b : {&cell_state, &cell_child, &cell_grids, &clus, &clus_tri, &clus_tsph, &unk, &sp_list, &sp_chunk, &sp_cnt, &rep_pts, &rep_s,
+    for (DBuf* b : {&cell_state, &cell_child, &cell_cert, &cell_blk, &cell_grids, &clus, &clus_tri, &clus_tsph, &unk, &sp_list, &sp_chunk, &sp_cnt, &rep_pts, &rep_s,
                     &rep_m, &rep_f})
       b->release();
     for (DBuf* b : {&tri, &sub, &edges, &cont, &comp_tiles, &xyz64, &tri_idx, &comp_off, &comp_box, &cullmask, &pts, &masks, &flagmask, &nbr, &known, &want, &fkeys, &frontier, &lex, &region, &bfaces, &btri,
@@ -754,10 +772,14 @@ void build_cells(nm_ctx* c, const double* xyz, const std::uint32_t* tri, const s
   std::vector<float4> tsph;
   std::vector<std::size_t> coff(K + 1, 0);
   std::size_t total = 0;
-  for (int k = 0; k < K; ++k) {
-    coff[k] = clus.size();
+  std::vector<std::vector<float4>> clus_kv(K), tsph_kv(K);
+  std::vector<std::vector<std::uint32_t>> ctri_kv(K);
+  parallel_for(K, [&](int k) {
+    auto& clus = clus_kv[k];
+    auto& ctri = ctri_kv[k];
+    auto& tsph = tsph_kv[k];
     const std::uint32_t b = comp_off[k], e = comp_off[k + 1];
-    nm::CellGrid g{0.0, 0.0, 0.0, 1.0, 0, 0, 0, static_cast<std::uint32_t>(total)};
+    nm::CellGrid g{0.0, 0.0, 0.0, 1.0, 0, 0, 0, 0u};
     if (e > b) {
       double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
       std::vector<std::pair<std::uint32_t, std::uint32_t>> kk;
@@ -839,10 +861,17 @@ void build_cells(nm_ctx* c, const double* xyz, const std::uint32_t* tri, const s
       g.nx = n3[0];
       g.ny = n3[1];
       g.nz = n3[2];
-      total += static_cast<std::size_t>(g.nx) * g.ny * g.nz;
-      if (total > 0xffffffffull) throw Error("certified-cell grids exceed 2^32 cells");
     }
     G[k] = g;
+  });
+  for (int k = 0; k < K; ++k) {
+    G[k].off = static_cast<std::uint32_t>(total);
+    total += static_cast<std::size_t>(G[k].nx) * G[k].ny * G[k].nz;
+    if (total > 0xffffffffull) throw Error("certified-cell grids exceed 2^32 cells");
+    coff[k] = clus.size();
+    clus.insert(clus.end(), clus_kv[k].begin(), clus_kv[k].end());
+    ctri.insert(ctri.end(), ctri_kv[k].begin(), ctri_kv[k].end());
+    tsph.insert(tsph.end(), tsph_kv[k].begin(), tsph_kv[k].end());
   }
   coff[K] = clus.size();
   lap("setup");
@@ -861,7 +890,7 @@ void build_cells(nm_ctx* c, const double* xyz, const std::uint32_t* tri, const s
   (void)ncl_max;
 
   // ---- level 1 ----
-  auto* cert_d = c->rep_m.as<std::uint8_t>(std::max<std::size_t>(total, 1));
+  auto* cert_d = c->cell_cert.as<std::uint8_t>(std::max<std::size_t>(total, 1));
   for (int k = 0; k < K; ++k) {
     const std::size_t nc = static_cast<std::size_t>(G[k].nx) * G[k].ny * G[k].nz;
     if (!nc) continue;
@@ -879,16 +908,7 @@ void build_cells(nm_ctx* c, const double* xyz, const std::uint32_t* tri, const s
   // ---- level 2: children of every uncertified cell ----
   // (host loops run one compartment per thread; every compartment's grid,
   // blocks, runs and representatives are independent)
-  auto parallel_k = [&](auto&& f) {
-    const int nth = std::max(1, std::min<int>(K, static_cast<int>(std::thread::hardware_concurrency())));
-    std::atomic<int> next{0};
-    std::vector<std::thread> th;
-    for (int t = 0; t < nth; ++t)
-      th.emplace_back([&] {
-        for (int k; (k = next++) < K;) f(k);
-      });
-    for (auto& x : th) x.join();
-  };
+  auto parallel_k = [&](auto&& f) { parallel_for(K, f); };
   std::vector<std::uint32_t> block_of(total, 0xffffffffu);  // local block index within the compartment
   std::vector<std::vector<std::uint32_t>> blk_k(K);          // local cell index per local block
   parallel_k([&](int k) {
@@ -907,13 +927,13 @@ void build_cells(nm_ctx* c, const double* xyz, const std::uint32_t* tri, const s
   if (nblk) {
     std::vector<std::uint32_t> blk_cells(nblk);
     for (int k = 0; k < K; ++k) std::copy(blk_k[k].begin(), blk_k[k].end(), blk_cells.begin() + boff[k]);
-    up(c->sp_chunk, blk_cells.data(), nblk * sizeof(std::uint32_t));
-    auto* ch_d = c->cell_state.as<std::uint8_t>(nblk * nm::kChildren);
+    up(c->cell_blk, blk_cells.data(), nblk * sizeof(std::uint32_t));
+    auto* ch_d = c->cell_child.as<std::uint8_t>(nblk * nm::kChildren);
     for (int k = 0; k < K; ++k) {
       const std::size_t nb = boff[k + 1] - boff[k];
       if (!nb) continue;
       nm::k_child_certify<<<static_cast<unsigned>((nb * 64 + 255) / 256), 256, 0, st>>>(
-          G[k], static_cast<const std::uint32_t*>(c->sp_chunk.p) + boff[k], nb, clus_k(k),
+          G[k], static_cast<const std::uint32_t*>(c->cell_blk.p) + boff[k], nb, clus_k(k),
           static_cast<int>(coff[k + 1] - coff[k]), ctri_k(k), tsph_k(k), static_cast<const double*>(c->xyz64.p),
           static_cast<const std::uint32_t*>(c->tri_idx.p), c->cx, c->cy, c->cz, ch_d + boff[k] * nm::kChildren);
     }
@@ -1255,7 +1275,7 @@ int nm_set_surfaces(nm_ctx* c, const double* xyz, std::size_t nv, const std::uin
     std::size_t strip_slots = 0;
     const bool try_strips = c->opt.layout != 1;
     if (try_strips) {
-      for (int k = 0; k < K; ++k) {
+      parallel_for(K, [&](int k) {
         const std::vector<Strip> strips = stripify(tri, comp_off[k], comp_off[k + 1]);
         struct Chunk {
           std::uint32_t key;
@@ -1294,9 +1314,9 @@ int nm_set_surfaces(nm_ctx* c, const double* xyz, std::size_t nv, const std::uin
         });
         for (const Chunk& ch : chunks)
           for (std::size_t q = ch.first; q < ch.first + ch.count; ++q) segs[k].push_back(all[q]);
-        const std::size_t per_tile = nm::kTile / nm::kSegTris;
-        strip_slots += (segs[k].size() + per_tile - 1) / per_tile * nm::kTile;
-      }
+      });
+      const std::size_t per_tile = nm::kTile / nm::kSegTris;
+      for (int k = 0; k < K; ++k) strip_slots += (segs[k].size() + per_tile - 1) / per_tile * nm::kTile;
     }
     std::size_t soup_slots = 0;
     for (int k = 0; k < K; ++k) soup_slots += (comp_off[k + 1] - comp_off[k] + nm::kTile - 1) / nm::kTile * nm::kTile;
@@ -1342,7 +1362,7 @@ int nm_set_surfaces(nm_ctx* c, const double* xyz, std::size_t nv, const std::uin
     // double-single per subtile.
     constexpr int kMaxV = nm::kSub * 3;
     std::vector<std::array<double, 3>> vloc(kMaxV);
-    for (int k = 0; k < K; ++k) {
+    parallel_for(K, [&](int k) {  // compartments own disjoint tile ranges
       const std::size_t nreal = use_strips ? segs[k].size() : order[k].size();
       // fallback vertex for all-pad units: the compartment's first vertex
       const double* pad_v = comp_off[k + 1] > comp_off[k] ? xyz + 3 * std::size_t(tri[3 * comp_off[k]]) : ctr;
@@ -1472,7 +1492,7 @@ int nm_set_surfaces(nm_ctx* c, const double* xyz, std::size_t nv, const std::uin
           }
         }
       }
-    }
+    });
     (void)vloc;
     (void)kMaxV;
     c->strips = use_strips;
@@ -1494,7 +1514,7 @@ int nm_set_surfaces(nm_ctx* c, const double* xyz, std::size_t nv, const std::uin
     // the fp32 rounding of the point and of the projection in the kernel) and
     // rounded outward.
     std::vector<float4> hbox(static_cast<std::size_t>(K) * nm::kDopF4);
-    for (int k = 0; k < K; ++k) {
+    parallel_for(K, [&](int k) {
       float* dst = reinterpret_cast<float*>(&hbox[static_cast<std::size_t>(k) * nm::kDopF4]);
       for (int q = 0; q < 4 * nm::kDopF4; ++q) dst[q] = 0.0f;
       for (int j = 0; j < nm::kDopDirs; ++j) {
@@ -1516,7 +1536,7 @@ int nm_set_surfaces(nm_ctx* c, const double* xyz, std::size_t nv, const std::uin
         dst[2 * j] = std::nextafter(float(lo - m), -INFINITY);
         dst[2 * j + 1] = std::nextafter(float(hi + m), INFINITY);
       }
-    }
+    });
     up(c->comp_box, hbox.data(), hbox.size() * sizeof(float4));
     NM_CUDA(cudaStreamSynchronize(c->stream));
     c->K = K;
