@@ -580,3 +580,55 @@ def test_cfg5_full_size_properties():
     expect = np.where(first >= 0, S.label_ids[np.maximum(first, 0)], 0)
     np.testing.assert_array_equal(labels[tidx], expect)
     c.close()
+
+
+def _torus(R, r, nu, nv, center=(0.0, 0.0, 0.0)):
+    """Closed, outward torus (hole along z): nu x nv quads split in two."""
+    u = np.arange(nu) * 2 * np.pi / nu
+    v = np.arange(nv) * 2 * np.pi / nv
+    U, V = np.meshgrid(u, v, indexing="ij")
+    xyz = np.stack([(R + r * np.cos(V)) * np.cos(U), (R + r * np.cos(V)) * np.sin(U), r * np.sin(V)], -1)
+    xyz = xyz.reshape(-1, 3) + np.asarray(center)
+    idx = lambda i, j: (i % nu) * nv + (j % nv)
+    tri = []
+    for i in range(nu):
+        for j in range(nv):
+            a, b, c, d = idx(i, j), idx(i + 1, j), idx(i + 1, j + 1), idx(i, j + 1)
+            tri += [(a, b, c), (a, c, d)]
+    return xyz, np.array(tri, np.uint32)
+
+
+def test_cell_culling_topology_and_thin_gaps():
+    """cull_outside=2 on shapes that stress the run logic: a torus (the hole
+    is inside the 13-DOP but outside the surface: runs through it need their
+    own representative), two concentric spheres 0.2 mm apart (cells between
+    them stay uncertified), a 1 mm sphere (tiny cells) and a sphere touching
+    the lattice edge. Masks equal the brute-force pass; s of resolved pairs
+    equals the fp64 oracle."""
+    from paper_2203_10000_b200._native import Context
+    tx, tt = _torus(20.0, 6.0, 96, 48)
+    # sphere orientation from the synth generator (outward)
+    s1 = synth.icosphere(15.0, 4, center=(0.0, 0.0, 30.0))
+    s2 = synth.icosphere(15.2, 4, center=(0.0, 0.0, 30.0))
+    s3 = synth.icosphere(1.0, 3, center=(0.3, -0.2, 0.1))
+    s4 = synth.icosphere(8.0, 3, center=(-24.0, 24.0, -16.0))
+    S = synth.concat_surfaces([(tx, tt), s1, s2, s3, s4])
+    nodes = synth.lattice_nodes((-32.0, -32.0, -16.0), 0.37, (174, 174, 174))
+    with Context(0) as full, Context(0, cull_outside=2) as cell:
+        for c in (full, cell):
+            c.set_surfaces(S.xyz, S.tri, S.comp_off, S.label_ids)
+        m_full, _ = full.label_nodes(nodes)
+        m_cell, _ = cell.label_nodes(nodes)
+        info = cell.cell_info()
+        rng = np.random.default_rng(11)
+        idx = np.sort(rng.choice(nodes.shape[0], 4000, replace=False))
+        s_cell, _ = cell.enclosure(nodes[idx])
+    np.testing.assert_array_equal(m_cell, m_full)
+    assert info["last_pairs"] < 0.25 * nodes.shape[0] * 5
+    hole = (np.abs(nodes[:, 2]) < 2.0) & (np.hypot(nodes[:, 0], nodes[:, 1]) < 10.0)
+    assert hole.any() and not np.any(m_full[hole] & 1)          # the hole is outside the torus
+    _, s_ref = oracle.label_nodes(nodes[idx], S, want_s=True)
+    resolved = (s_cell == 0.0) | (s_cell == 1.0)
+    assert resolved.mean() > 0.5
+    np.testing.assert_allclose(s_cell[resolved], s_ref[resolved], rtol=0, atol=1e-9)
+    np.testing.assert_allclose(s_cell, s_ref, rtol=0, atol=S_EXPECT)
