@@ -80,6 +80,10 @@ struct GpuOptions {
   nm_options opt;
   bool validate_closed = true;  // check the SPEC.md:227 precondition with validate_closed (surface.hpp:80-104)
   std::vector<int> devices;     // > 1 entries: initial_label shards over these devices (SPEC.md:267 --label-workers)
+  // Certified cells (cull_outside = 2) cost a one-off grid build per call
+  // (~0.3-0.5 s at 1e6 triangles); calls with fewer point-triangle pairs
+  // than this use 13-DOP culling alone. Labels are identical either way.
+  double cell_min_evals = 2e12;
   GpuOptions() {
     nm_default_options(&opt);
     opt.cull_outside = 2;  // exact for closed surfaces (13-DOP + certified cells); disabled below whenever
@@ -98,10 +102,16 @@ inline void check(int rc) {
 /// RAII owner of one nm_ctx (one device + stream + replicated surfaces).
 class Context {
  public:
-  explicit Context(const GpuOptions& o = {}) : validate_(o.validate_closed) {
+  explicit Context(const GpuOptions& o = {}, double work_evals = 0.0) : validate_(o.validate_closed) {
     nm_options opt = o.opt;
-    if (!o.validate_closed) opt.cull_outside = 0;  // culling relies on closed surfaces
+    opt.cull_outside = cull_mode(o, work_evals);
     check(nm_create(&ctx_, &opt));
+  }
+  // culling relies on closed surfaces; certified cells only pay off on large calls
+  static int cull_mode(const GpuOptions& o, double work_evals) {
+    if (!o.validate_closed) return 0;
+    if (o.opt.cull_outside == 2 && work_evals < o.cell_min_evals) return 1;
+    return o.opt.cull_outside;
   }
   ~Context() {
     if (ctx_) nm_destroy(ctx_);
@@ -153,6 +163,12 @@ class Context {
   bool validate_ = true;
 };
 
+inline double triangles(const SurfaceSegmentation& seg) {
+  double t = 0.0;
+  for (const CompartmentSurface& c : seg.compartments) t += static_cast<double>(c.mesh.triangles.size());
+  return t;
+}
+
 inline const double* xyz_of(const std::vector<Vec3>& v) {
   static_assert(sizeof(Vec3) == 3 * sizeof(double), "Vec3 must be three packed doubles");
   return reinterpret_cast<const double*>(v.data());
@@ -179,7 +195,7 @@ inline double enclosure_ratio(const Vec3& point, const TriangleSurface& surface,
 /// Per-node ratios and inside masks for every compartment.
 inline NodeEnclosure node_enclosure(const TetrahedralMesh& mesh, const SurfaceSegmentation& seg,
                                     const SolidAngleParams& params, const GpuOptions& o = {}) {
-  detail::Context ctx(o);
+  detail::Context ctx(o, double(mesh.node_count()) * detail::triangles(seg));
   ctx.set_segmentation(seg);
   NodeEnclosure e;
   e.compartments = seg.compartments.size();
@@ -206,7 +222,7 @@ inline std::vector<int> initial_label(const TetrahedralMesh& mesh, const Surface
     detail::Context::validate(seg);
     nm_group* g = nullptr;
     nm_options gopt = o.opt;
-    if (!o.validate_closed) gopt.cull_outside = 0;
+    gopt.cull_outside = detail::Context::cull_mode(o, double(mesh.node_count()) * detail::triangles(seg));
     detail::check(nm_group_create(&g, static_cast<int>(o.devices.size()), o.devices.data(), &gopt));
     std::unique_ptr<nm_group, int (*)(nm_group*)> guard(g, nm_group_destroy);
     std::vector<double> xyz;
@@ -228,7 +244,7 @@ inline std::vector<int> initial_label(const TetrahedralMesh& mesh, const Surface
                                       mesh.tet_count(), params.threshold, labels.data(), nullptr, stats));
     return labels;
   }
-  detail::Context ctx(o);
+  detail::Context ctx(o, double(mesh.node_count()) * detail::triangles(seg));
   ctx.set_segmentation(seg);
   std::vector<int> labels(mesh.tet_count());
   detail::check(nm_label_mesh(ctx.get(), detail::xyz_of(mesh.nodes), mesh.node_count(), detail::idx_of(mesh.tetrahedra),
@@ -242,7 +258,7 @@ inline RelabelResult relabel_recursive(const TetrahedralMesh& mesh, const Surfac
                                        const SolidAngleParams& params, const std::vector<int>& prev_labels,
                                        const GpuOptions& o = {}) {
   if (prev_labels.size() != mesh.tet_count()) throw LabelingError("prev_labels length != tet count");
-  detail::Context ctx(o);
+  detail::Context ctx(o, double(mesh.node_count()) * detail::triangles(seg));
   ctx.set_segmentation(seg);
   RelabelResult r;
   r.labels = prev_labels;

@@ -33,6 +33,26 @@ int main(int argc, char** argv) {
     std::fprintf(stderr, "group labels differ\n");
     return 6;
   }
+  // certified cells forced on (cell_min_evals = 0), and every culling mode
+  // off / 13-DOP only: the same labels
+  for (int mode : {0, 1, 2}) {
+    GpuOptions o;
+    o.opt.cull_outside = mode;
+    o.cell_min_evals = 0.0;
+    if (initial_label(mesh, seg, params, o) != labels) {
+      std::fprintf(stderr, "labels differ with cull_outside=%d\n", mode);
+      return 9;
+    }
+  }
+  {
+    GpuOptions o;
+    o.cell_min_evals = 0.0;
+    const RelabelResult rc = relabel_recursive(mesh, seg, params, labels, o);
+    if (rc.passes != 1 || rc.labels != labels) {
+      std::fprintf(stderr, "relabel with certified cells failed\n");
+      return 10;
+    }
+  }
   // enclosure_ratio KATs
   const double s_in = enclosure_ratio(Vec3{0, 0, 0}, seg.compartments[0].mesh);
   const double s_out = enclosure_ratio(Vec3{30, 0, 0}, seg.compartments[0].mesh);
