@@ -282,10 +282,13 @@ class Context:
                                      ctypes.byref(st)))
         return out
 
-    def label_mesh(self, nodes, tets, threshold=0.5, want_masks=False):
+    def label_mesh(self, nodes, tets, threshold=0.5, want_masks=False, out=None):
+        """out: optional int32 array of the tet count (e.g. a pinned buffer) for the labels."""
         nodes = np.ascontiguousarray(nodes, dtype=np.float64).reshape(-1, 3)
         tets = np.ascontiguousarray(tets, dtype=np.uint32).reshape(-1, 4)
-        labels = np.empty(tets.shape[0], dtype=np.int32)
+        labels = np.empty(tets.shape[0], dtype=np.int32) if out is None else out
+        if labels.dtype != np.int32 or labels.shape != (tets.shape[0],) or not labels.flags.c_contiguous:
+            raise ValueError("out must be a contiguous int32 array with one entry per tet")
         masks = np.empty(nodes.shape[0], dtype=np.uint32) if want_masks else None
         st = NmStats()
         check(self.lib.nm_label_mesh(self.handle, ptr(nodes, ctypes.c_double), nodes.shape[0],

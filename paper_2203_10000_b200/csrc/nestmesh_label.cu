@@ -799,8 +799,10 @@ void build_cells(nm_ctx* c, const double* xyz, const std::uint32_t* tri, const s
         kk.emplace_back(spread10h(q[0]) | (spread10h(q[1]) << 1) | (spread10h(q[2]) << 2), t);
       }
       std::stable_sort(kk.begin(), kk.end(), [](auto& x, auto& y) { return x.first < y.first; });
-      for (std::size_t i0 = 0; i0 < kk.size(); i0 += nm::kCluster) {
-        const std::size_t i1 = std::min(kk.size(), i0 + nm::kCluster);
+      // bounding sphere of triangles kk[i0, i1) in the centred frame: fp32
+      // centre of the vertex box, radius rounded up with the kernel's
+      // margins (1e-6 relative + 1e-5 mm + 4e-6 |centre|)
+      auto sphere = [&](std::size_t i0, std::size_t i1) {
         double blo[3] = {1e300, 1e300, 1e300}, bhi[3] = {-1e300, -1e300, -1e300};
         for (std::size_t i = i0; i < i1; ++i)
           for (int v = 0; v < 3; ++v)
@@ -809,7 +811,8 @@ void build_cells(nm_ctx* c, const double* xyz, const std::uint32_t* tri, const s
               blo[a] = std::min(blo[a], x);
               bhi[a] = std::max(bhi[a], x);
             }
-        const float fc[3] = {float(0.5 * (blo[0] + bhi[0])), float(0.5 * (blo[1] + bhi[1])), float(0.5 * (blo[2] + bhi[2]))};
+        const float fc[3] = {float(0.5 * (blo[0] + bhi[0])), float(0.5 * (blo[1] + bhi[1])),
+                             float(0.5 * (blo[2] + bhi[2]))};
         double rho = 0.0;
         for (std::size_t i = i0; i < i1; ++i)
           for (int v = 0; v < 3; ++v) {
@@ -821,34 +824,14 @@ void build_cells(nm_ctx* c, const double* xyz, const std::uint32_t* tri, const s
             rho = std::max(rho, std::sqrt(d2));
           }
         const double rel = 4e-6 * (std::fabs(fc[0]) + std::fabs(fc[1]) + std::fabs(fc[2]));
-        clus.push_back(make_float4(fc[0], fc[1], fc[2], std::nextafter(float(rho * (1.0 + 1e-6) + 1e-5 + rel), INFINITY)));
+        return make_float4(fc[0], fc[1], fc[2], std::nextafter(float(rho * (1.0 + 1e-6) + 1e-5 + rel), INFINITY));
+      };
+      for (std::size_t i0 = 0; i0 < kk.size(); i0 += nm::kCluster) {
+        const std::size_t i1 = std::min(kk.size(), i0 + nm::kCluster);
+        clus.push_back(sphere(i0, i1));
         for (std::size_t i = i0; i < i0 + nm::kCluster; ++i) {
           ctri.push_back(i < i1 ? kk[i].second : 0xffffffffu);
-          // the triangle's bounding sphere (vertex-box centre), same rounding margins as the cluster's
-          float4 ts = make_float4(0.f, 0.f, 0.f, -1e30f);
-          if (i < i1) {
-            double tlo[3] = {1e300, 1e300, 1e300}, thi[3] = {-1e300, -1e300, -1e300};
-            for (int v = 0; v < 3; ++v)
-              for (int a = 0; a < 3; ++a) {
-                const double x = xyz[3 * std::size_t(tri[3 * kk[i].second + v]) + a] - ctr[a];
-                tlo[a] = std::min(tlo[a], x);
-                thi[a] = std::max(thi[a], x);
-              }
-            const float tc[3] = {float(0.5 * (tlo[0] + thi[0])), float(0.5 * (tlo[1] + thi[1])),
-                                 float(0.5 * (tlo[2] + thi[2]))};
-            double tr = 0.0;
-            for (int v = 0; v < 3; ++v) {
-              double d2 = 0.0;
-              for (int a = 0; a < 3; ++a) {
-                const double d = xyz[3 * std::size_t(tri[3 * kk[i].second + v]) + a] - ctr[a] - double(tc[a]);
-                d2 += d * d;
-              }
-              tr = std::max(tr, std::sqrt(d2));
-            }
-            const double trel = 4e-6 * (std::fabs(tc[0]) + std::fabs(tc[1]) + std::fabs(tc[2]));
-            ts = make_float4(tc[0], tc[1], tc[2], std::nextafter(float(tr * (1.0 + 1e-6) + 1e-5 + trel), INFINITY));
-          }
-          tsph.push_back(ts);
+          tsph.push_back(i < i1 ? sphere(i, i + 1) : make_float4(0.f, 0.f, 0.f, -1e30f));
         }
       }
       const double ext = std::max({hi[0] - lo[0], hi[1] - lo[1], hi[2] - lo[2]});
@@ -886,8 +869,6 @@ void build_cells(nm_ctx* c, const double* xyz, const std::uint32_t* tri, const s
   auto clus_k = [&](int k) { return static_cast<const float4*>(c->clus.p) + coff[k]; };
   auto ctri_k = [&](int k) { return static_cast<const std::uint32_t*>(c->clus_tri.p) + coff[k] * nm::kCluster; };
   auto tsph_k = [&](int k) { return static_cast<const float4*>(c->clus_tsph.p) + coff[k] * nm::kCluster; };
-  const int ncl_max = 0;
-  (void)ncl_max;
 
   // ---- level 1 ----
   auto* cert_d = c->cell_cert.as<std::uint8_t>(std::max<std::size_t>(total, 1));
@@ -1360,8 +1341,6 @@ int nm_set_surfaces(nm_ctx* c, const double* xyz, std::size_t nv, const std::uin
     // in the centred frame) and its vertices relative to c, so near-surface
     // geometry keeps ~ulp(radius) precision; the kernel forms p - c in
     // double-single per subtile.
-    constexpr int kMaxV = nm::kSub * 3;
-    std::vector<std::array<double, 3>> vloc(kMaxV);
     parallel_for(K, [&](int k) {  // compartments own disjoint tile ranges
       const std::size_t nreal = use_strips ? segs[k].size() : order[k].size();
       // fallback vertex for all-pad units: the compartment's first vertex
@@ -1493,8 +1472,6 @@ int nm_set_surfaces(nm_ctx* c, const double* xyz, std::size_t nv, const std::uin
         }
       }
     });
-    (void)vloc;
-    (void)kMaxV;
     c->strips = use_strips;
     c->has_surfaces = false;
     auto up = [&](DBuf& b, const void* src, std::size_t bytes) {
@@ -1677,7 +1654,9 @@ int nm_label_mesh(nm_ctx* c, const double* nodes, std::size_t n, const std::uint
     auto* d_labels = c->labels.as<int>(std::max<std::size_t>(nt, 1));
     auto* d_word = c->word.as<std::uint32_t>(1);
     if (n) NM_CUDA(cudaMemcpyAsync(d_pts, nodes, 3 * n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
-    label_nodes_dev(c, d_pts, n, T, d_masks, nullptr, c->stream, stats, nullptr, /*stats_deferred=*/true);
+    // tet upload + index validation on the side stream, enqueued first so it
+    // runs under the whole node pass (which may synchronise the host once,
+    // for the sparse grid of certified-cell culling)
     if (nt) {
       NM_CUDA(cudaMemcpyAsync(d_tets, tets, 4 * nt * sizeof(std::uint32_t), cudaMemcpyHostToDevice, c->side));
       NM_CUDA(cudaMemsetAsync(d_word, 0, sizeof(std::uint32_t), c->side));
@@ -1686,6 +1665,9 @@ int nm_label_mesh(nm_ctx* c, const double* nodes, std::size_t n, const std::uint
       NM_CUDA(cudaGetLastError());
       NM_CUDA(cudaMemcpyAsync(c->h_word, d_word, sizeof(std::uint32_t), cudaMemcpyDeviceToHost, c->side));
       NM_CUDA(cudaEventRecord(c->ev_side, c->side));
+    }
+    label_nodes_dev(c, d_pts, n, T, d_masks, nullptr, c->stream, stats, nullptr, /*stats_deferred=*/true);
+    if (nt) {
       NM_CUDA(cudaStreamWaitEvent(c->stream, c->ev_side, 0));
       NM_CUDA(cudaEventSynchronize(c->ev_side));
       if (*c->h_word >= n) {
