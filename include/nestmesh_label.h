@@ -165,6 +165,17 @@ int nm_group_label_mesh(nm_group* g, const double* nodes, size_t n_nodes, const 
 /* ---- device-resident entry points (asynchronous on `stream`) -------------- */
 int nm_label_nodes_device(nm_ctx* ctx, const double* d_pts, size_t n, double threshold, uint32_t* d_masks,
                           double* d_s_out /* nullable, n*K */, void* stream, nm_stats* stats);
+/* Cost-balanced multi-GPU node pass: shard `shard` of `nshards` evaluates its
+ * share of the (point, compartment) pairs of ALL n points that culling does
+ * not resolve (pair i of compartment k weighs k's tile count; equal-weight
+ * contiguous slices of the per-compartment lists). d_masks (n entries) gets
+ * the bits this shard owns: the known bits on shard 0, the evaluated bits on
+ * their owner; the shards' masks are disjoint, so their bitwise OR — or their
+ * integer sum, e.g. an NCCL all-reduce — is the full result, bit-identical
+ * to nm_label_nodes_device. Every shard needs all n points. */
+int nm_label_nodes_shard_device(nm_ctx* ctx, const double* d_pts, size_t n, double threshold, uint32_t* d_masks,
+                                int shard, int nshards, void* stream, nm_stats* stats);
+
 int nm_label_tets_device(nm_ctx* ctx, const uint32_t* d_tets, size_t nt, const uint32_t* d_masks,
                          int* d_labels, void* stream, nm_stats* stats);
 int nm_flag_boundary_device(nm_ctx* ctx, const uint32_t* d_tets, size_t nt, const uint32_t* d_masks,

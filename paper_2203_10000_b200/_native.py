@@ -90,6 +90,9 @@ LABEL_API = {
     "nm_relabel": (ctypes.c_int, [ctypes.c_void_p, c_double_p, ctypes.c_size_t, c_u32_p, ctypes.c_size_t,
                                   ctypes.c_double, ctypes.c_int, c_i32_p, c_i32_p, c_i32_p, c_u8_p,
                                   ctypes.POINTER(NmStats)]),
+    "nm_label_nodes_shard_device": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_double,
+                                                   ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_void_p,
+                                                   ctypes.POINTER(NmStats)]),
     "nm_label_nodes_device": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_double,
                                              ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                                              ctypes.POINTER(NmStats)]),
@@ -443,6 +446,15 @@ class Context:
         check(self.lib.nm_label_nodes_device(self.handle, d_pts.data_ptr(), d_pts.shape[0], threshold,
                                              d_masks.data_ptr(), d_s.data_ptr() if d_s is not None else None,
                                              stream_handle(stream), ctypes.byref(st) if st is not None else None))
+        return st.as_dict() if st is not None else None
+
+    def label_nodes_shard_device(self, d_pts, d_masks, shard, nshards, threshold=0.5, stream=None, stats=True):
+        """Cost-balanced share `shard` of `nshards` of the node pass over ALL points
+        d_pts; the shards' d_masks OR (or add) to the full masks."""
+        st = NmStats() if stats else None
+        check(self.lib.nm_label_nodes_shard_device(self.handle, d_pts.data_ptr(), d_pts.shape[0], threshold,
+                                                   d_masks.data_ptr(), shard, nshards, stream_handle(stream),
+                                                   ctypes.byref(st) if st is not None else None))
         return st.as_dict() if st is not None else None
 
     def label_tets_device(self, d_tets, d_masks, d_labels, stream=None, stats=True):

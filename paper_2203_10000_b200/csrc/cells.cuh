@@ -160,12 +160,13 @@ struct ClassifyParams {
   std::size_t n;
   const std::uint32_t* order;
   double cx, cy, cz;
-  const float4* dop4;  // 13-DOP slabs per compartment (k_cull_mask)
-  const CellGrid* grids;
+  const float4* dop4;  // 13-DOP slabs per compartment (k_cull_mask); nullptr: no outside culling
+  const CellGrid* grids;  // nullptr: no certified cells
   const std::uint32_t* code;  // per level-1 cell: 0 unknown, 1 certified w = 0, 2 certified w = 1,
                               // 3 + b: uncertified, children in child block b
   const std::uint8_t* child;  // per child: 0 unknown, 1 w = 0, 2 w = 1
   int K;
+  bool preset;  // write the known inside bits into masks (false: masks = 0; sharded passes, shard > 0)
   std::uint32_t* unk;
   std::uint32_t* masks;
   std::uint32_t* flagmask;
@@ -180,14 +181,20 @@ __global__ void k_cell_classify(const ClassifyParams prm) {
     const float xf = static_cast<float>(x), yf = static_cast<float>(y), zf = static_cast<float>(z);
     std::uint32_t unk = 0, ins = 0;
     for (int c = 0; c < prm.K; ++c) {
-      const float* dop = reinterpret_cast<const float*>(prm.dop4 + static_cast<std::size_t>(c) * kDopF4);
-      bool o = false;
+      if (prm.dop4) {
+        const float* dop = reinterpret_cast<const float*>(prm.dop4 + static_cast<std::size_t>(c) * kDopF4);
+        bool o = false;
 #pragma unroll
-      for (int d = 0; d < kDopDirs; ++d) {
-        const float pr = dop_dir(d, 0) * xf + dop_dir(d, 1) * yf + dop_dir(d, 2) * zf;
-        o |= pr < __ldg(dop + 2 * d) || pr > __ldg(dop + 2 * d + 1);
+        for (int d = 0; d < kDopDirs; ++d) {
+          const float pr = dop_dir(d, 0) * xf + dop_dir(d, 1) * yf + dop_dir(d, 2) * zf;
+          o |= pr < __ldg(dop + 2 * d) || pr > __ldg(dop + 2 * d + 1);
+        }
+        if (o) continue;  // outside the convex hull: w = 0
       }
-      if (o) continue;  // outside the convex hull: w = 0
+      if (!prm.grids) {
+        unk |= 1u << c;
+        continue;
+      }
       const CellGrid g = prm.grids[c];
       const double u = (x - g.ox) / g.B, v = (y - g.oy) / g.B, w = (z - g.oz) / g.B;
       std::uint32_t st = 0;
@@ -206,7 +213,7 @@ __global__ void k_cell_classify(const ClassifyParams prm) {
       else if (st != 1) unk |= 1u << c;
     }
     prm.unk[i] = unk;
-    prm.masks[j] = ins;
+    prm.masks[j] = prm.preset ? ins : 0u;
     prm.flagmask[j] = 0u;
     if (prm.s_out)
       for (int c = 0; c < prm.K; ++c)

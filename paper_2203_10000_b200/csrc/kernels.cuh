@@ -131,11 +131,12 @@ struct LabelParams {
   int split[33];
   // Sparse mode (k_label MODE 2, cell culling): CTA b of the 1-D grid takes
   // compartment c with sp_blk[c] <= b < sp_blk[c + 1] and evaluates the
-  // positions sp_list[sp_off[c] .. sp_off[c + 1]) (indices into `order`)
+  // positions sp_list[sp_off[c] .. sp_end[c]) (indices into `order`)
   // against that compartment only, ORing its bits in (masks pre-set by
   // k_cell_classify).
   const std::uint32_t* sp_list;
   std::uint32_t sp_off[33];
+  std::uint32_t sp_end[32];  // end of compartment c's slice (= sp_off[c + 1] when the slices are packed)
   std::uint32_t sp_blk[33];
 };
 
@@ -167,7 +168,7 @@ __global__ void __launch_bounds__(kBlock, (NP == 1 ? NM_MIN_BLOCKS : NM_MIN_BLOC
   if (SPARSE) {
     while (c_sp + 1 < prm.K && blockIdx.x >= prm.sp_blk[c_sp + 1]) ++c_sp;
     base = prm.sp_off[c_sp] + (static_cast<std::size_t>(blockIdx.x - prm.sp_blk[c_sp]) * kBlock + threadIdx.x) * P;
-    n_end = prm.sp_off[c_sp + 1];
+    n_end = prm.sp_end[c_sp];
   }
   // Points in the centred frame as double-singles (hi + lo), packed in pairs;
   // per subtile the kernel forms p - c = (hi - c) + lo, exact up to one

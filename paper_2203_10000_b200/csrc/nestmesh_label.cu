@@ -341,17 +341,22 @@ int compartment_split(const nm_ctx* c, std::size_t nblocks, int* split) {
 // Sparse k_label (MODE 2) over per-compartment lists of evaluation positions
 // (prm.sp_list, cnt[k] entries for compartment k, concatenated). Returns the
 // number of launches (0 when every list is empty).
-int launch_sparse(nm_ctx* c, nm::LabelParams& prm, const std::vector<std::uint32_t>& cnt, cudaStream_t st) {
+// first (optional): start of compartment k's slice in sp_list (default: the
+// prefix sum of cnt, i.e. the slices are packed).
+int launch_sparse(nm_ctx* c, nm::LabelParams& prm, const std::vector<std::uint32_t>& cnt, cudaStream_t st,
+                  const std::vector<std::uint32_t>* first = nullptr) {
   const std::uint32_t per_block = nm::kBlock * 2;
   std::uint32_t off = 0, blk = 0;
   for (int k = 0; k <= 32; ++k) {
-    prm.sp_off[k] = off;
     prm.sp_blk[k] = blk;
     if (k < c->K) {
+      prm.sp_off[k] = first ? (*first)[k] : off;
       off += cnt[k];
       blk += (cnt[k] + per_block - 1) / per_block;
     }
   }
+  // the kernel reads sp_list[sp_off[k], sp_end[k])
+  for (int k = 0; k < c->K; ++k) prm.sp_end[k] = prm.sp_off[k] + cnt[k];
   if (blk == 0) return 0;
   prm.split[0] = 0;
   prm.split[1] = c->K;
@@ -367,7 +372,7 @@ int launch_sparse(nm_ctx* c, nm::LabelParams& prm, const std::vector<std::uint32
 // host synchronisation, for the grid size) with the lists in c->sp_list.
 std::vector<std::uint32_t> classify_cells(nm_ctx* c, const double* d_pts, std::size_t n, const std::uint32_t* order,
                                           std::uint32_t* d_masks, std::uint32_t* flagmask, double* d_s, cudaStream_t st,
-                                          std::uint64_t& launches) {
+                                          std::uint64_t& launches, bool preset_known = true) {
   const int K = c->K;
   auto* unk = c->unk.as<std::uint32_t>(n);
   const std::size_t nb = std::max<std::size_t>(1, (n + nm::kSelChunk - 1) / nm::kSelChunk);
@@ -381,8 +386,9 @@ std::vector<std::uint32_t> classify_cells(nm_ctx* c, const double* d_pts, std::s
   cp.cx = c->cx;
   cp.cy = c->cy;
   cp.cz = c->cz;
-  cp.dop4 = static_cast<const float4*>(c->comp_box.p);
-  cp.grids = static_cast<const nm::CellGrid*>(c->cell_grids.p);
+  cp.dop4 = c->opt.cull_outside ? static_cast<const float4*>(c->comp_box.p) : nullptr;
+  cp.grids = c->cells ? static_cast<const nm::CellGrid*>(c->cell_grids.p) : nullptr;
+  cp.preset = preset_known;
   cp.code = static_cast<const std::uint32_t*>(c->cell_state.p);
   cp.child = static_cast<const std::uint8_t*>(c->cell_child.p);
   cp.K = K;
@@ -421,9 +427,49 @@ std::vector<std::uint32_t> classify_cells(nm_ctx* c, const double* d_pts, std::s
 
 // stats_deferred: the caller collects the stats later with read_node_stats
 // (no host synchronisation inside; nm_label_mesh overlaps the tet upload).
+// Cost-balanced split of the per-compartment pair lists over nshards: pair i
+// of compartment k costs w_k = its tile count and starts at cost P_k + i w_k
+// (P_k = cost of the lists before k); shard r takes the pairs starting in
+// [floor(C r / N), floor(C (r + 1) / N)). The same integer formula on every
+// shard, so the slices partition every list exactly. In: cnt = list lengths;
+// out: first[k] = start of this shard's slice in the packed lists, cnt[k] =
+// its length.
+void shard_slices(const nm_ctx* c, std::vector<std::uint32_t>& cnt, int shard, int nshards,
+                  std::vector<std::uint32_t>& first) {
+  const int K = c->K;
+  std::vector<std::uint64_t> w(K), P(K + 1, 0);
+  std::uint32_t off = 0;
+  for (int k = 0; k < K; ++k) {
+    w[k] = std::max<std::uint64_t>(1, c->comp_tiles_h[k + 1] - c->comp_tiles_h[k]);
+    P[k + 1] = P[k] + w[k] * cnt[k];
+    first[k] = off;
+    off += cnt[k];
+  }
+  if (nshards <= 1) return;
+  if (shard < 0 || shard >= nshards) throw Error("shard index out of range");
+  const unsigned __int128 C = P[K];
+  const std::uint64_t t0 = static_cast<std::uint64_t>(C * static_cast<unsigned>(shard) / static_cast<unsigned>(nshards));
+  const std::uint64_t t1 =
+      static_cast<std::uint64_t>(C * static_cast<unsigned>(shard + 1) / static_cast<unsigned>(nshards));
+  auto bound = [&](int k, std::uint64_t t) -> std::uint32_t {  // first pair of k starting at cost >= t
+    if (t <= P[k]) return 0;
+    const std::uint64_t i = (t - P[k] + w[k] - 1) / w[k];
+    return static_cast<std::uint32_t>(std::min<std::uint64_t>(i, cnt[k]));
+  };
+  for (int k = 0; k < K; ++k) {
+    const std::uint32_t a = bound(k, t0), b = bound(k, t1);
+    first[k] += a;
+    cnt[k] = b - a;
+  }
+}
+
+// nshards >= 1: a sharded pass (nm_label_nodes_shard_device) — evaluate only
+// shard's cost-balanced share of the (point, compartment) pair lists of all
+// n points; masks hold the known bits on shard 0 only, so the shards' masks
+// OR (or add: the bits are disjoint) to the full result.
 void label_nodes_dev(nm_ctx* c, const double* d_pts, std::size_t n, double T, std::uint32_t* d_masks, double* d_s,
                      cudaStream_t st, nm_stats* stats, const std::uint32_t* d_subset = nullptr,
-                     bool stats_deferred = false) {
+                     bool stats_deferred = false, int shard = 0, int nshards = 0) {
   require_surfaces(c);
   if (!(T > 0.0 && T < 1.0)) throw Error("threshold must lie in (0, 1) (SPEC.md:216)");
   std::uint64_t launches = 0;
@@ -481,15 +527,25 @@ void label_nodes_dev(nm_ctx* c, const double* d_pts, std::size_t n, double T, st
   prm.masks = d_masks;
   prm.flagmask = flagmask;
   prm.cull = nullptr;
-  if (c->opt.cull_outside == 2 && c->cells) {
-    // certified-cell culling: classification presets every known pair, the
-    // sparse pass evaluates the rest (one host synchronisation for its grid)
+  if ((c->opt.cull_outside == 2 && c->cells) || nshards >= 1) {
+    // pair lists: classification presets every known pair (certified cells,
+    // 13-DOP), the sparse pass evaluates the rest (one host synchronisation
+    // for its grid); a sharded pass takes only its share of the lists
+    if (nshards >= 1 && d_s) throw Error("sharded node passes do not return s");
     prm.s_out = d_s;
     prm.counters = counters;
-    const std::vector<std::uint32_t> cnt = classify_cells(c, d_pts, n, order, d_masks, flagmask, d_s, st, launches);
+    std::vector<std::uint32_t> cnt =
+        classify_cells(c, d_pts, n, order, d_masks, flagmask, d_s, st, launches, /*preset_known=*/shard == 0);
     prm.sp_list = static_cast<const std::uint32_t*>(c->sp_list.p);
+    std::vector<std::uint32_t> first(c->K);
+    shard_slices(c, cnt, shard, nshards, first);
+    c->sparse_pairs = c->sparse_evals = 0;  // this pass's share (nm_cell_info)
+    for (int k = 0; k < c->K; ++k) {
+      c->sparse_pairs += cnt[k];
+      c->sparse_evals += std::uint64_t(cnt[k]) * (c->comp_off_h[k + 1] - c->comp_off_h[k]);
+    }
     if (stats) NM_CUDA(cudaEventRecord(c->ev[1], st));
-    launches += launch_sparse(c, prm, cnt, st);
+    launches += launch_sparse(c, prm, cnt, st, &first);
   } else {
   if (c->opt.cull_outside) {
     auto* cm = c->cullmask.as<std::uint32_t>(n);
@@ -1562,6 +1618,16 @@ int nm_surface_info(nm_ctx* c, int* K, std::size_t* triangles, std::size_t* padd
   });
 }
 
+int nm_label_nodes_shard_device(nm_ctx* c, const double* d_pts, std::size_t n, double T, std::uint32_t* d_masks,
+                                int shard, int nshards, void* stream, nm_stats* stats) {
+  return guarded([&] {
+    require_surfaces(c);
+    if (nshards < 1 || shard < 0 || shard >= nshards) throw Error("shard must lie in [0, nshards)");
+    NM_CUDA(cudaSetDevice(c->opt.device));
+    label_nodes_dev(c, d_pts, n, T, d_masks, nullptr, c->pick(stream), stats, nullptr, false, shard, nshards);
+  });
+}
+
 int nm_label_nodes_device(nm_ctx* c, const double* d_pts, std::size_t n, double T, std::uint32_t* d_masks,
                           double* d_s, void* stream, nm_stats* stats) {
   return guarded([&] {
@@ -1694,9 +1760,12 @@ struct nm_group {
   std::vector<nm_ctx*> ctx;
   std::uint32_t* h_masks = nullptr;  // pinned gather buffer
   std::size_t h_cap = 0;
+  std::uint32_t* h_part = nullptr;   // pinned per-device partial masks (certified-cell sharding)
+  std::size_t part_cap = 0;
   ~nm_group() {
     for (nm_ctx* c : ctx) nm_destroy(c);
     if (h_masks) cudaFreeHost(h_masks);
+    if (h_part) cudaFreeHost(h_part);
   }
 };
 
@@ -1751,8 +1820,33 @@ int nm_group_label_mesh(nm_group* g, const double* nodes, std::size_t n, const s
       NM_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&g->h_masks), std::max<std::size_t>(n, 1) * 4, cudaHostAllocPortable));
       g->h_cap = n;
     }
-    // 1) node shards, asynchronously on every device
-    for (std::size_t r = 0; r < R; ++r) {
+    // 1) node pass. With certified cells the work per point is far from
+    // uniform (only pairs near a surface are evaluated), so every device
+    // takes a cost-balanced share of the pair lists of ALL points and the
+    // disjoint partial masks are OR-ed; otherwise contiguous node shards.
+    const bool by_pairs = R > 1 && g->ctx[0]->opt.cull_outside == 2 && g->ctx[0]->cells;
+    if (by_pairs && g->part_cap < R * n) {
+      if (g->h_part) cudaFreeHost(g->h_part);
+      g->h_part = nullptr;
+      g->part_cap = 0;
+      NM_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&g->h_part), std::max<std::size_t>(R * n, 1) * 4,
+                            cudaHostAllocPortable));
+      g->part_cap = R * n;
+    }
+    for (std::size_t r = 0; by_pairs && r < R; ++r) {
+      nm_ctx* c = g->ctx[r];
+      require_surfaces(c);
+      NM_CUDA(cudaSetDevice(c->opt.device));
+      auto* d_pts = c->pts.as<double>(3 * std::max<std::size_t>(n, 1));
+      auto* d_m = c->masks2.as<std::uint32_t>(std::max<std::size_t>(n, 1));
+      if (n) {
+        NM_CUDA(cudaMemcpyAsync(d_pts, nodes, 3 * n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+        label_nodes_dev(c, d_pts, n, T, d_m, nullptr, c->stream, nullptr, nullptr, false, static_cast<int>(r),
+                        static_cast<int>(R));
+        NM_CUDA(cudaMemcpyAsync(g->h_part + r * n, d_m, n * 4, cudaMemcpyDeviceToHost, c->stream));
+      }
+    }
+    for (std::size_t r = 0; !by_pairs && r < R; ++r) {
       nm_ctx* c = g->ctx[r];
       require_surfaces(c);
       NM_CUDA(cudaSetDevice(c->opt.device));
@@ -1768,6 +1862,17 @@ int nm_group_label_mesh(nm_group* g, const double* nodes, std::size_t n, const s
     for (nm_ctx* c : g->ctx) {
       NM_CUDA(cudaSetDevice(c->opt.device));
       NM_CUDA(cudaStreamSynchronize(c->stream));
+    }
+    if (by_pairs) {
+      const int nchunk = 64;
+      parallel_for(nchunk, [&](int q) {
+        const std::size_t lo = n * q / nchunk, hi = n * (q + 1) / nchunk;
+        for (std::size_t i = lo; i < hi; ++i) {
+          std::uint32_t m = 0;
+          for (std::size_t r = 0; r < R; ++r) m |= g->h_part[r * n + i];
+          g->h_masks[i] = m;
+        }
+      });
     }
     // 2) gathered masks to every device, tet shards
     for (std::size_t r = 0; r < R; ++r) {

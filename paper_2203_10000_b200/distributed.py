@@ -8,6 +8,11 @@ contiguous range of tets. Because each node's result is a pure function of its
 position the gathered masks, and hence the labels, are identical
 for any world size.
 
+With certified-cell culling the per-point work is far from uniform, so
+``label_mesh_balanced`` instead gives every rank a cost-balanced share of the
+(point, compartment) pairs of all nodes and merges the disjoint partial masks
+with one all-reduce.
+
 The per-rank compute is injected (``node_fn`` / ``tet_fn``) so the CPU tests
 can exercise exactly this sharding + gather logic with the oracle as the
 per-rank checker, while the GPU path plugs in the CUDA entry points.
@@ -89,6 +94,41 @@ def label_mesh_sharded(nodes, tets, node_fn, tet_fn, rank: int, world: int, grou
     t = torch.as_tensor(np.ascontiguousarray(tets[tsh.lo:tsh.hi]).view(np.int32), device=device)
     labels = tet_fn(t, masks)
     return labels, tsh, masks
+
+
+def merge_partial_masks(local: "torch.Tensor", group=None) -> "torch.Tensor":
+    """Per-rank partial masks with pairwise DISJOINT bits (the cost-balanced
+    pair-list shards of nm_label_nodes_shard_device) -> the full masks on
+    every rank: one all-reduce SUM — disjoint bits add without carries, so
+    the sum is the bitwise OR (NCCL has no OR reduction)."""
+    import torch
+    import torch.distributed as dist
+    out = local.clone()
+    if dist.is_available() and dist.is_initialized():
+        if out.is_cuda and dist.get_backend(group) == "gloo":
+            host = out.cpu()
+            dist.all_reduce(host, op=dist.ReduceOp.SUM, group=group)
+            out.copy_(host)
+        else:
+            dist.all_reduce(out, op=dist.ReduceOp.SUM, group=group)
+    return out
+
+
+def label_mesh_balanced(nodes, tets, shard_fn, tet_fn, rank: int, world: int, group=None, device="cpu"):
+    """initial_label with the node pass split by COST rather than by points
+    (certified-cell culling leaves only the pairs near a surface, so equal
+    point ranges would not be equal work). Every rank holds all nodes.
+
+    shard_fn(points (N,3) f64 torch, rank, world) -> (N,) int32 partial masks
+    whose bits are disjoint across ranks (nm_label_nodes_shard_device on the
+    GPU); tet_fn as in label_mesh_sharded. Returns (labels of this rank's tet
+    range, tet shard, full masks)."""
+    import torch
+    pts = torch.as_tensor(np.ascontiguousarray(nodes), dtype=torch.float64, device=device)
+    masks = merge_partial_masks(shard_fn(pts, rank, world), group)
+    tsh = shard(tets.shape[0], world, rank)
+    t = torch.as_tensor(np.ascontiguousarray(tets[tsh.lo:tsh.hi]).view(np.int32), device=device)
+    return tet_fn(t, masks), tsh, masks
 
 
 def gather_labels(labels: "torch.Tensor", sh: Shard, group=None) -> "torch.Tensor":

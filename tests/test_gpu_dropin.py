@@ -73,6 +73,61 @@ def _gpu_rank(rank, world, port, out_dir):
         dist.destroy_process_group()
 
 
+def _gpu_rank_balanced(rank, world, port, out_dir):
+    import torch
+    import torch.distributed as dist
+    from paper_2203_10000_b200._native import Context
+    from paper_2203_10000_b200.distributed import gather_labels, label_mesh_balanced
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        cfg = synth.config(2)
+        S = cfg.surfaces
+        nodes, tets = cfg.lattice_mesh()
+        ctx = Context(0, cull_outside=2)
+        ctx.set_surfaces(S.xyz, S.tri, S.comp_off, S.label_ids)
+
+        def shard_fn(pts, r, w):
+            d_pts = pts.cuda()
+            d_m = torch.zeros(pts.shape[0], dtype=torch.int32, device="cuda")
+            ctx.label_nodes_shard_device(d_pts, d_m, r, w)
+            torch.cuda.synchronize()
+            return d_m.cpu()
+
+        def tet_fn(t, masks):
+            return torch.from_numpy(ctx.label_tets(t.numpy().view(np.uint32), masks.numpy().view(np.uint32)))
+
+        labels, tsh, masks = label_mesh_balanced(nodes, tets, shard_fn, tet_fn, rank, world)
+        full = gather_labels(labels, tsh)
+        if rank == 0:
+            np.save(os.path.join(out_dir, "labels.npy"), full.numpy())
+        ctx.close()
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_ranks_balanced_cells_gpu_equals_single(tmp_path):
+    """Certified-cell culling over two ranks: each evaluates its cost-balanced
+    share of the pair lists (nm_label_nodes_shard_device), the disjoint partial
+    masks merge with one all-reduce: labels equal the single-process
+    brute-force labels bit for bit."""
+    import socket
+    import torch.multiprocessing as mp
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    mp.spawn(_gpu_rank_balanced, args=(2, port, str(tmp_path)), nprocs=2, join=True)
+    from paper_2203_10000_b200._native import Context
+    cfg = synth.config(2)
+    S = cfg.surfaces
+    nodes, tets = cfg.lattice_mesh()
+    with Context(0) as c:
+        c.set_surfaces(S.xyz, S.tri, S.comp_off, S.label_ids)
+        ref, _, _ = c.label_mesh(nodes, tets)
+    np.testing.assert_array_equal(np.load(tmp_path / "labels.npy"), ref)
+
+
 def test_two_ranks_sharded_gpu_equals_single(tmp_path):
     """Two ranks (processes) each label their node shard / tet range with the
     CUDA path, masks gathered over gloo: labels equal the single-process GPU
@@ -95,11 +150,14 @@ def test_two_ranks_sharded_gpu_equals_single(tmp_path):
     np.testing.assert_array_equal(np.load(tmp_path / "labels.npy"), ref)
 
 
+@pytest.mark.parametrize("cull", [0, 2])
 @pytest.mark.parametrize("devices", [[0], [0, 0], [0, 0, 0]])
-def test_group_multi_context_bitwise(devices):
+def test_group_multi_context_bitwise(devices, cull):
     """nm_group (single-process multi-device API for C/C++ hosts): with 1, 2
     and 3 contexts (on the one GPU available) the labels and masks are
-    bit-identical to a single context (acceptance #8)."""
+    bit-identical to a single context (acceptance #8) — with
+    contiguous node shards (cull 0) and with the cost-balanced pair-list
+    shards of certified-cell culling (cull 2)."""
     from paper_2203_10000_b200._native import Context, Group
     cfg = synth.config(2)
     S = cfg.surfaces
@@ -107,7 +165,7 @@ def test_group_multi_context_bitwise(devices):
     with Context(0) as c:
         c.set_surfaces(S.xyz, S.tri, S.comp_off, S.label_ids)
         ref, mref, _ = c.label_mesh(nodes, tets, want_masks=True)
-    with Group(devices) as g:
+    with Group(devices, cull_outside=cull) as g:
         g.set_surfaces(S.xyz, S.tri, S.comp_off, S.label_ids)
         lab, m = g.label_mesh(nodes, tets)
     np.testing.assert_array_equal(lab, ref)
@@ -251,3 +309,38 @@ def test_bench_multi_rank_on_one_gpu(world):
     line = json.loads(lines[0])
     assert line["n_gpus"] == world and line["value"] > 0 and line["e2e"]["value"] > 0
     assert line["cpu_baseline"] is None
+
+
+@pytest.mark.parametrize("cull", [0, 1, 2])
+def test_shard_device_partials_are_disjoint_and_balanced(cull):
+    """nm_label_nodes_shard_device: for 1, 2, 3 and 5 shards the partial masks
+    are pairwise disjoint and OR to the single-pass masks (bit-identical), and
+    the evaluated work is split evenly (pairs weighted by their compartment's
+    tile count)."""
+    import torch
+    from paper_2203_10000_b200._native import Context
+    cfg = synth.config(3)
+    S = cfg.surfaces
+    nodes = cfg.lattice_nodes()[1_500_000:1_800_000]
+    with Context(0, cull_outside=cull) as c:
+        c.set_surfaces(S.xyz, S.tri, S.comp_off, S.label_ids)
+        ref, _ = c.label_nodes(nodes)
+        d_pts = torch.from_numpy(nodes).cuda()
+        for R in (1, 2, 3, 5):
+            parts, evals = [], []
+            for r in range(R):
+                d_m = torch.zeros(nodes.shape[0], dtype=torch.int32, device="cuda")
+                c.label_nodes_shard_device(d_pts, d_m, r, R)
+                torch.cuda.synchronize()
+                parts.append(d_m.cpu().numpy().view(np.uint32))
+                evals.append(c.cell_info()["last_evals"])
+            acc = np.zeros_like(ref)
+            for p in parts:
+                assert not np.any(acc & p)        # disjoint
+                acc |= p
+            np.testing.assert_array_equal(acc, ref)
+            total = sum(np.uint64(p.astype(np.uint64)) for p in parts)
+            np.testing.assert_array_equal(total.astype(np.uint32), ref)  # integer sum = OR (disjoint bits)
+            assert max(evals) <= 1.01 * sum(evals) / R + 400_000     # balanced to one pair's weight
+        with pytest.raises(RuntimeError):
+            c.label_nodes_shard_device(d_pts, torch.zeros(nodes.shape[0], dtype=torch.int32, device="cuda"), 2, 2)
