@@ -572,8 +572,10 @@ struct PredStraddle {
 };
 
 // ---------------------------------------------------------------------------
-// K3: fp64 fix-up. One warp per flagged point; lanes stride the compartment's
-// triangles in file order, fixed xor-butterfly reduction (deterministic).
+// K3: fp64 fix-up. One CTA of kFixWarps warps per flagged point: each warp
+// takes a fixed contiguous quarter of the compartment's triangles (file
+// order), lanes strided, fixed xor-butterfly; the quarters are added in fixed
+// order (deterministic).
 // ---------------------------------------------------------------------------
 struct FixupParams {
   const double* pts;
@@ -591,12 +593,13 @@ struct FixupParams {
   unsigned long long* counters;  // [2] pairs, [3] ties
 };
 
-__global__ void __launch_bounds__(256) k_fixup(const FixupParams prm) {
-  const int lane = threadIdx.x & 31;
-  const std::uint32_t nwarps = gridDim.x * (blockDim.x / 32);
+constexpr int kFixWarps = 4;  // warps per flagged point (one CTA)
+__global__ void __launch_bounds__(32 * kFixWarps) k_fixup(const FixupParams prm) {
+  __shared__ double part[kFixWarps];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const std::uint32_t cnt = *prm.count;
   unsigned long long pairs = 0, ties = 0;
-  for (std::uint32_t w = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); w < cnt; w += nwarps) {
+  for (std::uint32_t w = blockIdx.x; w < cnt; w += gridDim.x) {  // CTA-uniform loop
     const std::uint32_t i = prm.subset ? prm.subset[prm.list[w]] : prm.list[w];
     std::uint32_t fm = prm.flagmask[i];
     std::uint32_t m = prm.masks[i];
@@ -605,24 +608,35 @@ __global__ void __launch_bounds__(256) k_fixup(const FixupParams prm) {
     while (fm) {
       const int c = __ffs(fm) - 1;
       fm &= fm - 1;
+      // warp wid sums a fixed quarter of the compartment's triangles (lanes
+      // strided, fixed butterfly); the quarters are added in fixed order
+      const std::uint32_t lo = prm.comp_off[c], len = prm.comp_off[c + 1] - lo;
+      const std::uint32_t t0 = lo + static_cast<std::uint32_t>(std::uint64_t(len) * wid / kFixWarps);
+      const std::uint32_t t1 = lo + static_cast<std::uint32_t>(std::uint64_t(len) * (wid + 1) / kFixWarps);
       double sum = 0.0;
-      for (std::uint32_t t = prm.comp_off[c] + lane; t < prm.comp_off[c + 1]; t += 32) {
+      for (std::uint32_t t = t0 + lane; t < t1; t += 32) {
         const std::uint32_t* e = prm.tri + 3 * static_cast<std::size_t>(t);
         sum += vos_half_angle64(prm.xyz + 3 * static_cast<std::size_t>(e[0]), prm.xyz + 3 * static_cast<std::size_t>(e[1]),
                                 prm.xyz + 3 * static_cast<std::size_t>(e[2]), px, py, pz);
       }
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(kFull, sum, o);
-      const double s = sum / (2.0 * CUDART_PI);
+      if (lane == 0) part[wid] = sum;
+      __syncthreads();
+      double tot = part[0];
+#pragma unroll
+      for (int q = 1; q < kFixWarps; ++q) tot += part[q];
+      __syncthreads();  // part is rewritten by the next compartment
+      const double s = tot / (2.0 * CUDART_PI);
       if (s >= prm.T) m |= 1u << c;
       else m &= ~(1u << c);
       ++pairs;
       if (fabs(s - prm.T) < prm.tie_eps) ++ties;
-      if (prm.s_out && lane == 0) prm.s_out[static_cast<std::size_t>(i) * prm.K + c] = s;
+      if (prm.s_out && threadIdx.x == 0) prm.s_out[static_cast<std::size_t>(i) * prm.K + c] = s;
     }
-    if (lane == 0) prm.masks[i] = m;
+    if (threadIdx.x == 0) prm.masks[i] = m;
   }
-  if (lane == 0 && prm.counters) {
+  if (threadIdx.x == 0 && prm.counters) {
     atomicAdd(prm.counters + 2, pairs);
     atomicAdd(prm.counters + 3, ties);
   }

@@ -601,7 +601,7 @@ void label_nodes_dev(nm_ctx* c, const double* d_pts, std::size_t n, double T, st
   fp.masks = d_masks;
   fp.s_out = d_s;
   fp.counters = counters;
-  nm::k_fixup<<<c->sm_count * 8, 256, 0, st>>>(fp);
+  nm::k_fixup<<<c->sm_count * 16, 32 * nm::kFixWarps, 0, st>>>(fp);
   NM_CUDA(cudaGetLastError());
   ++launches;
   c->node_launches = launches;
