@@ -97,6 +97,12 @@ class ClockSampler:
     def stop(self):
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        # a timed region shorter than nvidia-smi's start-up sees no sample:
+        # then keep the first one taken right after it (flagged)
+        in_region = len(self.rows)
+        deadline = time.time() + 3.0
+        while not self.rows and time.time() < deadline:
+            time.sleep(0.05)
         self.proc.terminate()
         try:
             self.proc.wait(timeout=5)
@@ -115,8 +121,11 @@ class ClockSampler:
                 if v.lower() == "active":
                     reasons.add(nm_)
         loaded = [v for v in sm if v > 500] or sm
-        return {"sm_mhz": statistics.median(loaded) if loaded else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+        out = {"sm_mhz": statistics.median(loaded) if loaded else None, "sm_max_mhz": max(mx) if mx else None,
+               "reasons": sorted(reasons), "samples": len(sm)}
+        if in_region == 0 and sm:
+            out["note"] = "timed region shorter than the first nvidia-smi sample; sampled right after it"
+        return out
 
 
 def dist_env():

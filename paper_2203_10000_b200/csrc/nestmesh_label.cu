@@ -18,6 +18,7 @@
 #include <stdexcept>
 #include <string>
 #include <thread>
+#include <type_traits>
 #include <atomic>
 #include <vector>
 
@@ -937,8 +938,14 @@ void build_cells(nm_ctx* c, const double* xyz, const std::uint32_t* tri, const s
         static_cast<const std::uint32_t*>(c->tri_idx.p), c->cx, c->cy, c->cz, cert_d);
   }
   NM_CUDA(cudaGetLastError());
-  std::vector<std::uint8_t> cert1(total);
-  if (total) NM_CUDA(cudaMemcpyAsync(cert1.data(), cert_d, total, cudaMemcpyDeviceToHost, st));
+  // host arrays below are allocated uninitialised: every entry is written
+  // (by a copy or by its compartment's thread) before it is read
+  auto uninit = [](auto* tag, std::size_t m) {
+    using T = std::remove_pointer_t<decltype(tag)>;
+    return std::unique_ptr<T[]>(new T[std::max<std::size_t>(m, 1)]);
+  };
+  auto cert1 = uninit(static_cast<std::uint8_t*>(nullptr), total);
+  if (total) NM_CUDA(cudaMemcpyAsync(cert1.get(), cert_d, total, cudaMemcpyDeviceToHost, st));
   NM_CUDA(cudaStreamSynchronize(st));
   lap("l1");
 
@@ -946,7 +953,7 @@ void build_cells(nm_ctx* c, const double* xyz, const std::uint32_t* tri, const s
   // (host loops run one compartment per thread; every compartment's grid,
   // blocks, runs and representatives are independent)
   auto parallel_k = [&](auto&& f) { parallel_for(K, f); };
-  std::vector<std::uint32_t> block_of(total, 0xffffffffu);  // local block index within the compartment
+  auto block_of = uninit(static_cast<std::uint32_t*>(nullptr), total);  // local block index (uncertified cells)
   std::vector<std::vector<std::uint32_t>> blk_k(K);          // local cell index per local block
   parallel_k([&](int k) {
     const std::size_t nc = static_cast<std::size_t>(G[k].nx) * G[k].ny * G[k].nz;
@@ -960,7 +967,8 @@ void build_cells(nm_ctx* c, const double* xyz, const std::uint32_t* tri, const s
   for (int k = 0; k < K; ++k) boff[k + 1] = boff[k] + blk_k[k].size();
   lap("blocks");
   const std::size_t nblk = boff[K];
-  std::vector<std::uint8_t> child(nblk * nm::kChildren);
+  const std::size_t nchild = nblk * nm::kChildren;
+  auto child = uninit(static_cast<std::uint8_t*>(nullptr), nchild);
   if (nblk) {
     std::vector<std::uint32_t> blk_cells(nblk);
     for (int k = 0; k < K; ++k) std::copy(blk_k[k].begin(), blk_k[k].end(), blk_cells.begin() + boff[k]);
@@ -979,7 +987,7 @@ void build_cells(nm_ctx* c, const double* xyz, const std::uint32_t* tri, const s
       NM_CUDA(cudaStreamSynchronize(st));
       lap("l2kern");
     }
-    NM_CUDA(cudaMemcpyAsync(child.data(), ch_d, child.size(), cudaMemcpyDeviceToHost, st));
+    NM_CUDA(cudaMemcpyAsync(child.get(), ch_d, nchild, cudaMemcpyDeviceToHost, st));
     NM_CUDA(cudaStreamSynchronize(st));
   }
   lap("l2");
@@ -1006,7 +1014,7 @@ void build_cells(nm_ctx* c, const double* xyz, const std::uint32_t* tri, const s
   };
   std::vector<std::vector<double>> reps(K);
   std::vector<std::vector<std::int64_t>> run_val(K);   // level-1 runs per compartment
-  std::vector<std::int32_t> run_of(total, -1);         // level-1 cell -> its local run
+  auto run_of = uninit(static_cast<std::int32_t*>(nullptr), total);  // certified level-1 cell -> its local run
   std::vector<std::vector<FineRun>> fine(K);
   auto child_at = [&](int k, std::size_t row, int fx, int sy, int sz) -> std::uint8_t& {
     const std::size_t b = boff[k] + block_of[row + fx / S];
@@ -1131,7 +1139,7 @@ void build_cells(nm_ctx* c, const double* xyz, const std::uint32_t* tri, const s
       }
   }
   lap("reps");
-  std::vector<std::uint32_t> code(total, 0);
+  auto code = uninit(static_cast<std::uint32_t*>(nullptr), total);
   lap("alloc");
   parallel_k([&](int k) {
     auto resolve = [&](std::int64_t v) -> std::int64_t {  // -> 0, 1 or kUnknown
@@ -1152,7 +1160,7 @@ void build_cells(nm_ctx* c, const double* xyz, const std::uint32_t* tri, const s
         code[q] = w == kUnknown ? 0u : static_cast<std::uint32_t>(1 + w);
       }
     }
-    std::fill(child.begin() + boff[k] * nm::kChildren, child.begin() + boff[k + 1] * nm::kChildren, 0);
+    std::fill(child.get() + boff[k] * nm::kChildren, child.get() + boff[k + 1] * nm::kChildren, 0);
     for (const FineRun& fr : fine[k]) {
       const std::int64_t w = resolve(fr.v);
       if (w == kUnknown) continue;
@@ -1160,15 +1168,15 @@ void build_cells(nm_ctx* c, const double* xyz, const std::uint32_t* tri, const s
     }
   });
   lap("codes");
-  up(c->cell_state, code.data(), total * sizeof(std::uint32_t));
-  up(c->cell_child, child.data(), child.size());
+  up(c->cell_state, code.get(), total * sizeof(std::uint32_t));
+  up(c->cell_child, child.get(), nchild);
   up(c->cell_grids, G.data(), G.size() * sizeof(nm::CellGrid));
   NM_CUDA(cudaStreamSynchronize(st));
   lap("final");
-  c->cells_total = total + child.size();
+  c->cells_total = total + nchild;
   c->cells_certified = 0;
   for (std::size_t q = 0; q < total; ++q) c->cells_certified += code[q] == 1 || code[q] == 2;
-  for (std::uint8_t v : child) c->cells_certified += v != 0;
+  for (std::size_t q = 0; q < nchild; ++q) c->cells_certified += child[q] != 0;
   c->cell_reps = R;
   c->cells = true;
   c->ms_cells = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
