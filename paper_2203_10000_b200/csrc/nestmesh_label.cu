@@ -409,6 +409,7 @@ std::vector<std::uint32_t> classify_cells(nm_ctx* c, const double* d_pts, std::s
   NM_CUDA(cudaStreamSynchronize(st));
   std::size_t total = 0;
   for (int k = 0; k < K; ++k) total += cnt[k];
+  if (total > 0xffffffffull) throw Error("more than 2^32 (point, compartment) pairs to evaluate in one call");
   auto* list = c->sp_list.as<std::uint32_t>(std::max<std::size_t>(total, 1));
   std::size_t off = 0;
   c->sparse_pairs = total;
