@@ -632,3 +632,33 @@ def test_cell_culling_topology_and_thin_gaps():
     assert resolved.mean() > 0.5
     np.testing.assert_allclose(s_cell[resolved], s_ref[resolved], rtol=0, atol=1e-9)
     np.testing.assert_allclose(s_cell, s_ref, rtol=0, atol=S_EXPECT)
+
+
+def test_cell_culling_small_and_empty_compartments():
+    """cull_outside=2 with a 4-triangle tetrahedron surface (one cluster,
+    fewer triangles than a cluster), an EMPTY compartment between two
+    spheres, and points far outside every grid: masks equal the brute-force
+    pass and s of resolved pairs equals the fp64 oracle."""
+    from paper_2203_10000_b200._native import Context
+    tet_xyz = np.array([[0, 0, 0], [4, 0, 0], [0, 4, 0], [0, 0, 4]], np.float64) + 1.0
+    tet_tri = np.array([[0, 2, 1], [0, 1, 3], [0, 3, 2], [1, 2, 3]], np.uint32)  # outward
+    a = synth.icosphere(3.0, 2, center=(-6.0, 0.0, 0.0))
+    b = synth.icosphere(9.0, 3)
+    S = synth.concat_surfaces([(tet_xyz, tet_tri), a, (np.zeros((0, 3)), np.zeros((0, 3), np.uint32)), b])
+    assert S.comp_off[2] == S.comp_off[3]
+    rng = np.random.default_rng(3)
+    pts = np.concatenate([rng.uniform(-12, 12, (200_000, 3)), rng.uniform(-1e3, 1e3, (2000, 3))])
+    with Context(0) as full, Context(0, cull_outside=2) as cell:
+        for c in (full, cell):
+            c.set_surfaces(S.xyz, S.tri, S.comp_off, S.label_ids)
+        m_full, _ = full.label_nodes(pts)
+        m_cell, _ = cell.label_nodes(pts)
+        s_cell, _ = cell.enclosure(pts[:3000])
+    np.testing.assert_array_equal(m_cell, m_full)
+    assert not np.any(m_full & np.uint32(1 << 2))                 # nothing is inside the empty compartment
+    inside_tet = (pts[:, 0] > 1) & (pts[:, 1] > 1) & (pts[:, 2] > 1) & (pts.sum(axis=1) - 3 < 4)
+    np.testing.assert_array_equal((m_full & 1).astype(bool), inside_tet)
+    _, s_ref = oracle.label_nodes(pts[:3000], S, want_s=True)
+    resolved = (s_cell == 0.0) | (s_cell == 1.0)
+    np.testing.assert_allclose(s_cell[resolved], s_ref[resolved], rtol=0, atol=1e-9)
+    np.testing.assert_allclose(s_cell, s_ref, rtol=0, atol=S_EXPECT)
