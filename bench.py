@@ -486,6 +486,51 @@ def main():
         cull["full_mesh_labeling_time_s"] = cull["mode2"]["full_mesh_labeling_time_s"]
         cull["labels_identical"] = cull["mode1"]["labels_identical"] and cull["mode2"]["labels_identical"]
 
+    # N > 1: the certified-cell pass split by COST over the ranks (every rank
+    # holds all nodes, evaluates its share of the pair lists; the disjoint
+    # partial masks merge in one all-reduce), then each rank's tet range.
+    if use_dist and not args.no_cull:
+        from paper_2203_10000_b200.distributed import merge_partial_masks
+        cctx = Context(local, cull_outside=2)
+        t_set = time.perf_counter()
+        cctx.set_surfaces(S.xyz, S.tri, S.comp_off, S.label_ids)
+        t_set = time.perf_counter() - t_set
+        d_all = torch.from_numpy(nodes).cuda()
+        part = torch.zeros(n, dtype=torch.int32, device="cuda")
+        cl = torch.empty(tsh.size, dtype=torch.int32, device="cuda")
+
+        def cstep():
+            cctx.label_nodes_shard_device(d_all, part, rank, world, stream=sptr, stats=False)
+            full = merge_partial_masks(part, group)
+            cctx.label_tets_device(d_tets, full, cl, stream=sptr, stats=False)
+
+        cstep()
+        torch.cuda.synchronize()
+        cms = []
+        for i in range(args.steps):
+            flush.fill_(i)
+            barrier()
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            cstep()
+            b.record(stream)
+            torch.cuda.synchronize()
+            cms.append(a.elapsed_time(b))
+        ci = cctx.cell_info()
+        my_evals = float(ci["last_evals"])
+        c_ms = allmax(sum(cms) / len(cms))
+        max_evals = allmax(my_evals)
+        same = allmax(0.0 if torch.equal(cl, d_labels) else 1.0) == 0.0
+        cull = {"mode2_balanced": {
+            "full_mesh_labeling_time_s": c_ms / 1e3, "labels_identical": same, "set_surfaces_s": t_set,
+            "max_rank_evals_performed": max_evals, "ranks": world,
+            "note": "cull_outside=2 over N ranks: each evaluates its cost-balanced share of the (point, compartment) "
+                    "pair lists of all nodes (nm_label_nodes_shard_device); partial masks merged by one all-reduce"}}
+        cull["full_mesh_labeling_time_s"] = c_ms / 1e3
+        cull["labels_identical"] = same
+        cctx.close()
+
     # §8(f) rows on the labeled mesh (not part of the headline): device
     # extraction of the region boundary of all compartments (the outer
     # surface, extract_region_boundary) and its boundary_distance to the

@@ -309,6 +309,8 @@ def test_bench_multi_rank_on_one_gpu(world):
     line = json.loads(lines[0])
     assert line["n_gpus"] == world and line["value"] > 0 and line["e2e"]["value"] > 0
     assert line["cpu_baseline"] is None
+    bal = line["cull_outside"]["mode2_balanced"]      # cost-balanced certified-cell pass over the ranks
+    assert bal["ranks"] == world and bal["labels_identical"] and bal["full_mesh_labeling_time_s"] > 0
 
 
 @pytest.mark.parametrize("cull", [0, 1, 2])
