@@ -138,7 +138,23 @@ struct LabelParams {
   std::uint32_t sp_off[33];
   std::uint32_t sp_end[32];  // end of compartment c's slice (= sp_off[c + 1] when the slices are packed)
   std::uint32_t sp_blk[33];
+  // Split sparse mode (sp_part != nullptr): compartment c's CTAs are
+  // (point chunk, fold block) pairs, sp_fb[c] fold blocks per chunk; each
+  // writes its points' fold-block partial sums to sp_part[sp_po[c] + i *
+  // sp_fb[c] + b] (i = position in c's slice) and its detector bits to
+  // sp_det; k_sparse_finalize adds the partials in block order.
+  double* sp_part;
+  std::uint8_t* sp_det;
+  std::uint32_t sp_po[32];
+  std::uint32_t sp_fb[32];
 };
+
+// fp64 fold structure of every (point, compartment) sum: per 256-triangle
+// tile an fp32 sum, added in fp64 into a fold-block sum over kFoldTiles
+// consecutive tiles of the compartment, the block sums added in block order.
+// The split sparse pass evaluates fold blocks in separate CTAs and adds them
+// in the same order, so every pass gives the same bits.
+constexpr int kFoldTiles = 32;
 
 // NP point pairs per thread (2*NP points), packed fp32x2 arithmetic.
 // STRIP = false: 3 float4 per triangle (triangle soup);
@@ -165,10 +181,20 @@ __global__ void __launch_bounds__(kBlock, (NP == 1 ? NM_MIN_BLOCKS : NM_MIN_BLOC
   std::size_t base = (static_cast<std::size_t>(blockIdx.x) * kBlock + threadIdx.x) * P;
   std::size_t n_end = prm.n;
   int c_sp = 0;
+  int fb = 0, t_lo = 0, t_hi = 0;  // split sparse mode: this CTA's fold block and tile range
   if (SPARSE) {
     while (c_sp + 1 < prm.K && blockIdx.x >= prm.sp_blk[c_sp + 1]) ++c_sp;
-    base = prm.sp_off[c_sp] + (static_cast<std::size_t>(blockIdx.x - prm.sp_blk[c_sp]) * kBlock + threadIdx.x) * P;
+    const unsigned nfb = prm.sp_part ? prm.sp_fb[c_sp] : 1u;
+    const unsigned l = blockIdx.x - prm.sp_blk[c_sp];
+    fb = static_cast<int>(l % nfb);
+    base = prm.sp_off[c_sp] + (static_cast<std::size_t>(l / nfb) * kBlock + threadIdx.x) * P;
     n_end = prm.sp_end[c_sp];
+    t_lo = static_cast<int>(prm.comp_tiles[c_sp]);
+    t_hi = static_cast<int>(prm.comp_tiles[c_sp + 1]);
+    if (prm.sp_part) {
+      t_lo += fb * kFoldTiles;
+      t_hi = min(t_hi, t_lo + kFoldTiles);
+    }
   }
   // Points in the centred frame as double-singles (hi + lo), packed in pairs;
   // per subtile the kernel forms p - c = (hi - c) + lo, exact up to one
@@ -227,11 +253,14 @@ __global__ void __launch_bounds__(kBlock, (NP == 1 ? NM_MIN_BLOCKS : NM_MIN_BLOC
   const int c_lo = SPARSE ? c_sp : prm.split[blockIdx.y], c_hi = SPARSE ? c_sp + 1 : prm.split[blockIdx.y + 1];
   // producer state (thread 0): next tile to fetch and its compartment
   int pf_c = 0, pf_t = -1;
+  // tile range of compartment c for this CTA (split sparse: one fold block)
+  auto t_first = [&](int c) { return SPARSE ? t_lo : static_cast<int>(prm.comp_tiles[c]); };
+  auto t_last = [&](int c) { return SPARSE ? t_hi : static_cast<int>(prm.comp_tiles[c + 1]); };
   auto pf_seek = [&](int c) {  // first tile of the first non-skipped, non-empty compartment in [c, c_hi)
     for (; c < c_hi; ++c)
-      if (!((skip >> c) & 1u) && prm.comp_tiles[c] < prm.comp_tiles[c + 1]) {
+      if (!((skip >> c) & 1u) && t_first(c) < t_last(c)) {
         pf_c = c;
-        pf_t = static_cast<int>(prm.comp_tiles[c]);
+        pf_t = t_first(c);
         return;
       }
     pf_t = -1;
@@ -248,14 +277,15 @@ __global__ void __launch_bounds__(kBlock, (NP == 1 ? NM_MIN_BLOCKS : NM_MIN_BLOC
   }
   unsigned it = 0;
 
-  int tile = prm.comp_tiles[c_lo];
+  int tile = t_first(c_lo);
   for (int c = c_lo; c < c_hi; ++c) {
-    const int tile_end = prm.comp_tiles[c + 1];
-    double acc64[P];
+    const int tile_end = t_last(c);
+    const int tile_c0 = static_cast<int>(prm.comp_tiles[c]);  // fold blocks count from the compartment's first tile
+    double acc64[P], blk64[P];
     bool det[P];
 #pragma unroll
     for (int k = 0; k < P; ++k) {
-      acc64[k] = 0.0;
+      acc64[k] = blk64[k] = 0.0;
       det[k] = false;
     }
     // Exact outside culling (opt-in): a point outside a closed compartment's
@@ -270,7 +300,7 @@ __global__ void __launch_bounds__(kBlock, (NP == 1 ? NM_MIN_BLOCKS : NM_MIN_BLOC
       const int buf = it & 1u;
       if (threadIdx.x == 0) {
         // buffer buf ^ 1 was released by the barrier closing the previous tile
-        if (pf_t >= 0 && ++pf_t >= static_cast<int>(prm.comp_tiles[pf_c + 1])) pf_seek(pf_c + 1);
+        if (pf_t >= 0 && ++pf_t >= t_last(pf_c)) pf_seek(pf_c + 1);
         if (pf_t >= 0) pf_issue(buf ^ 1);
       }
       mbar_wait(&s_bar[buf], (it >> 1) & 1u);
@@ -407,10 +437,28 @@ __global__ void __launch_bounds__(kBlock, (NP == 1 ? NM_MIN_BLOCKS : NM_MIN_BLOC
       }
 #pragma unroll
       for (int q = 0; q < NP; ++q) {
-        acc64[2 * q] += static_cast<double>(acc[q].x);
-        acc64[2 * q + 1] += static_cast<double>(acc[q].y);
+        blk64[2 * q] += static_cast<double>(acc[q].x);
+        blk64[2 * q + 1] += static_cast<double>(acc[q].y);
+      }
+      if ((tile - tile_c0) % kFoldTiles == kFoldTiles - 1 || tile + 1 == tile_end) {  // fold block complete
+#pragma unroll
+        for (int k = 0; k < P; ++k) {
+          acc64[k] += blk64[k];
+          blk64[k] = 0.0;
+        }
       }
       __syncthreads();  // every warp is done with buffer buf: the producer may refill it
+    }
+    if (SPARSE && prm.sp_part) {  // split: this CTA's fold-block partials, added by k_sparse_finalize
+      const unsigned nfb = prm.sp_fb[c];
+#pragma unroll
+      for (int k = 0; k < P; ++k)
+        if (valid[k]) {
+          const std::size_t slot = prm.sp_po[c] + (base + k - prm.sp_off[c]) * nfb + fb;
+          prm.sp_part[slot] = acc64[k];
+          prm.sp_det[slot] = det[k];
+        }
+      continue;
     }
 #pragma unroll
     for (int k = 0; k < P; ++k) {
@@ -424,7 +472,7 @@ __global__ void __launch_bounds__(kBlock, (NP == 1 ? NM_MIN_BLOCKS : NM_MIN_BLOC
   }
 #pragma unroll
   for (int k = 0; k < P; ++k) {
-    if (valid[k]) {
+    if (valid[k] && !(SPARSE && prm.sp_part)) {
       if (gridDim.y == 1 && !SPARSE) {
         prm.masks[pid[k]] = mask[k];
         prm.flagmask[pid[k]] = fmask[k];
@@ -452,6 +500,48 @@ __device__ __forceinline__ std::uint32_t spread10(std::uint32_t v) {
   v = (v | (v << 2)) & 0x09249249u;
   return v;
 }
+
+// Split sparse pass, second half: per (point, compartment) pair the fold-block
+// partials added in block order (the dense pass's order), then the same
+// threshold / detector / band logic as k_label's epilogue.
+struct FinalizeParams {
+  const std::uint32_t* list;   // pair positions (indices into order)
+  const std::uint32_t* order;  // evaluation order -> point id (nullable)
+  const double* part;
+  const std::uint8_t* det;
+  std::uint32_t sp_off[32];    // compartment c's slice in list
+  std::uint32_t qo[33];        // prefix of the slice lengths (pair index space)
+  std::uint32_t po[32], fb[32];
+  int K;
+  double T, band;
+  std::uint32_t* masks;
+  std::uint32_t* flagmask;
+  double* s_out;
+};
+
+__global__ void k_sparse_finalize(const FinalizeParams prm) {
+  const std::size_t total = prm.qo[prm.K];
+  for (std::size_t q = blockIdx.x * static_cast<std::size_t>(blockDim.x) + threadIdx.x; q < total;
+       q += static_cast<std::size_t>(gridDim.x) * blockDim.x) {
+    int c = 0;
+    while (c + 1 < prm.K && q >= prm.qo[c + 1]) ++c;
+    const std::size_t i = q - prm.qo[c];
+    const std::size_t slot = prm.po[c] + i * prm.fb[c];
+    double acc = 0.0;
+    bool det = false;
+    for (std::uint32_t b = 0; b < prm.fb[c]; ++b) {
+      acc += prm.part[slot + b];
+      det |= prm.det[slot + b] != 0;
+    }
+    const std::uint32_t pos = prm.list[prm.sp_off[c] + i];
+    const std::uint32_t j = prm.order ? prm.order[pos] : pos;
+    const double s = acc * kInv2Pi;
+    if (s >= prm.T) atomicOr(prm.masks + j, 1u << c);
+    if (det || !(fabs(s - prm.T) >= prm.band)) atomicOr(prm.flagmask + j, 1u << c);
+    if (prm.s_out) prm.s_out[static_cast<std::size_t>(j) * prm.K + c] = s;
+  }
+}
+
 
 __global__ void k_morton_keys(const double* pts, std::size_t n, const std::uint32_t* subset, double lx, double ly,
                               double lz, double inv, std::uint32_t* keys, std::uint32_t* idx) {

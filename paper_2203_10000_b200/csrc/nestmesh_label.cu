@@ -246,7 +246,7 @@ struct nm_ctx {
   DBuf tri, sub, edges, cont, comp_tiles, xyz64, tri_idx, comp_off, comp_box, cullmask;
   // certified cells (cull_outside = 2, cells.cuh)
   bool cells = false;
-  DBuf cell_state, cell_child, cell_cert, cell_blk, cell_grids, clus, clus_tri, clus_tsph, unk, sp_list, sp_chunk, sp_cnt, rep_pts, rep_s, rep_m, rep_f;
+  DBuf sp_part, sp_det, cell_state, cell_child, cell_cert, cell_blk, cell_grids, clus, clus_tri, clus_tsph, unk, sp_list, sp_chunk, sp_cnt, rep_pts, rep_s, rep_m, rep_f;
   std::uint64_t cells_total = 0, cells_certified = 0, cell_reps = 0, sparse_pairs = 0, sparse_evals = 0;
   double ms_cells = 0.0;  // host wall time of the certification (nm_set_surfaces)
   std::vector<std::uint32_t> comp_off_h;
@@ -259,7 +259,7 @@ struct nm_ctx {
       s_out, word;
 
   ~nm_ctx() {
-    for (DBuf* b : {&cell_state, &cell_child, &cell_cert, &cell_blk, &cell_grids, &clus, &clus_tri, &clus_tsph, &unk, &sp_list, &sp_chunk, &sp_cnt, &rep_pts, &rep_s,
+    for (DBuf* b : {&sp_part, &sp_det, &cell_state, &cell_child, &cell_cert, &cell_blk, &cell_grids, &clus, &clus_tri, &clus_tsph, &unk, &sp_list, &sp_chunk, &sp_cnt, &rep_pts, &rep_s,
                     &rep_m, &rep_f})
       b->release();
     for (DBuf* b : {&tri, &sub, &edges, &cont, &comp_tiles, &xyz64, &tri_idx, &comp_off, &comp_box, &cullmask, &pts, &masks, &flagmask, &nbr, &known, &want, &fkeys, &frontier, &lex, &region, &bfaces, &btri,
@@ -347,24 +347,65 @@ int compartment_split(const nm_ctx* c, std::size_t nblocks, int* split) {
 int launch_sparse(nm_ctx* c, nm::LabelParams& prm, const std::vector<std::uint32_t>& cnt, cudaStream_t st,
                   const std::vector<std::uint32_t>* first = nullptr) {
   const std::uint32_t per_block = nm::kBlock * 2;
+  const int K = c->K;
+  // Few point chunks (a thin shell of pairs) would leave SMs idle in the last
+  // wave: then each chunk's tiles are split into fold blocks evaluated by
+  // separate CTAs (same fp64 fold order, see kFoldTiles), and
+  // k_sparse_finalize adds the block partials.
+  std::uint64_t chunks = 0;
+  for (int k = 0; k < K; ++k) chunks += (cnt[k] + per_block - 1) / per_block;
+  constexpr double kSplitWaves = 8.0;
+  const bool split = chunks > 0 && double(chunks) < kSplitWaves * c->sm_count * NM_MIN_BLOCKS;
   std::uint32_t off = 0, blk = 0;
+  std::uint64_t po = 0;
   for (int k = 0; k <= 32; ++k) {
     prm.sp_blk[k] = blk;
-    if (k < c->K) {
+    if (k < K) {
+      const std::uint32_t tiles = c->comp_tiles_h[k + 1] - c->comp_tiles_h[k];
+      const std::uint32_t nfb = split ? std::max<std::uint32_t>(1, (tiles + nm::kFoldTiles - 1) / nm::kFoldTiles) : 1;
       prm.sp_off[k] = first ? (*first)[k] : off;
+      prm.sp_fb[k] = nfb;
+      prm.sp_po[k] = static_cast<std::uint32_t>(po);
       off += cnt[k];
-      blk += (cnt[k] + per_block - 1) / per_block;
+      blk += (cnt[k] + per_block - 1) / per_block * nfb;
+      po += std::uint64_t(cnt[k]) * nfb;
     }
   }
   // the kernel reads sp_list[sp_off[k], sp_end[k])
-  for (int k = 0; k < c->K; ++k) prm.sp_end[k] = prm.sp_off[k] + cnt[k];
+  for (int k = 0; k < K; ++k) prm.sp_end[k] = prm.sp_off[k] + cnt[k];
   if (blk == 0) return 0;
+  if (po > 0xffffffffull) throw Error("too many fold-block partials in one call");
   prm.split[0] = 0;
-  prm.split[1] = c->K;
+  prm.split[1] = K;
+  prm.sp_part = split ? c->sp_part.as<double>(po) : nullptr;
+  prm.sp_det = split ? c->sp_det.as<std::uint8_t>(po) : nullptr;
   if (c->strips) nm::k_label<1, true, 2><<<blk, nm::kBlock, 0, st>>>(prm);
   else nm::k_label<1, false, 2><<<blk, nm::kBlock, 0, st>>>(prm);
   NM_CUDA(cudaGetLastError());
-  return 1;
+  if (!split) return 1;
+  nm::FinalizeParams fp{};
+  fp.list = prm.sp_list;
+  fp.order = prm.order;
+  fp.part = prm.sp_part;
+  fp.det = prm.sp_det;
+  std::uint32_t q = 0;
+  for (int k = 0; k < K; ++k) {
+    fp.sp_off[k] = prm.sp_off[k];
+    fp.qo[k] = q;
+    fp.po[k] = prm.sp_po[k];
+    fp.fb[k] = prm.sp_fb[k];
+    q += cnt[k];
+  }
+  fp.qo[K] = q;
+  fp.K = K;
+  fp.T = prm.T;
+  fp.band = prm.band;
+  fp.masks = prm.masks;
+  fp.flagmask = prm.flagmask;
+  fp.s_out = prm.s_out;
+  nm::k_sparse_finalize<<<grid_for(q, 256, c->sm_count * 8), 256, 0, st>>>(fp);
+  NM_CUDA(cudaGetLastError());
+  return 2;
 }
 
 // Certified-cell classification of the n evaluation positions (order[i]) and
