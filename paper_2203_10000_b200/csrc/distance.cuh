@@ -3,6 +3,8 @@
 // distance. Same N-body tile loop as the labeling kernel with a min-reduction
 // instead of a sum.
 //
+//   (triangles are grouped in Morton-ordered clusters of 32 with bounding
+//   spheres; both passes skip clusters that provably cannot matter)
 //   pass 1 (fp32): d1 = min over triangles of the fp32 distance;
 //   pass 2 (fp32 + fp64): every triangle whose fp32 distance is within
 //     tol = 1e-3 mm + 1e-5 d1 of d1 (fp32 error at ~100 mm coordinates is
@@ -85,65 +87,82 @@ __device__ __forceinline__ T point_tri_dist2(V3t<T> p, V3t<T> a, V3t<T> b, V3t<T
   return d2 < d ? d2 : d;
 }
 
-constexpr int kDistTile = 256;
+constexpr int kDistCluster = 32;  // triangles per cluster (Morton order of centroids)
 
 struct DistParams {
   const double* pts;     // n fp64 points (original frame)
   std::size_t n;
-  const float4* tri32;   // 3 float4 per triangle (a, b, c relative to (cx, cy, cz))
+  const std::uint32_t* order;  // evaluation order of the points (Morton); results scattered back
+  const float4* tri32;   // 3 float4 per triangle slot (a, b, c relative to (cx, cy, cz)), cluster order
+  const std::uint32_t* slot_tri;  // original triangle of each slot (padding repeats a triangle)
+  const float4* clus;    // per cluster: fp32 centre (centred frame), w = radius (rounded up)
+  int nclus;
   const double* xyz;     // fp64 vertices (original frame)
   const std::uint32_t* tri;  // original triangles
-  std::size_t nt;
   double cx, cy, cz;
   float* d32;            // pass-1 fp32 minimum distance per point
   double* out;           // fp64 distances
-  unsigned long long* counters;  // [4] fp64 candidate evaluations
+  unsigned long long* counters;  // [4] fp64 candidate evaluations, [5] fp32 cluster visits
 };
 
 // PASS 1: fp32 minimum; PASS 2: fp64 refinement over the candidates.
+// Exact cluster culling: a cluster is skipped when the lower bound of its
+// triangles' distance, |p - c| - rho, exceeds the bound (pass 1: the least
+// upper bound min |p - c| + rho and the running minimum; pass 2: the
+// candidate limit) by more than the fp32 error margin. A skipped cluster
+// holds no triangle that could change the pass's result, so d32 and the
+// candidate set — hence the fp64 minimum — are those of the full scan.
 template <int PASS>
 __global__ void __launch_bounds__(256) k_point_surface_distance(const DistParams prm) {
-  __shared__ float4 s_tri[kDistTile * 3];
   const std::size_t i = blockIdx.x * static_cast<std::size_t>(blockDim.x) + threadIdx.x;
-  const bool valid = i < prm.n;
-  const std::size_t ii = valid ? i : (prm.n ? prm.n - 1 : 0);
-  const double px = prm.pts[3 * ii], py = prm.pts[3 * ii + 1], pz = prm.pts[3 * ii + 2];
+  if (i >= prm.n) return;
+  const std::size_t j = prm.order ? prm.order[i] : i;
+  const double px = prm.pts[3 * j], py = prm.pts[3 * j + 1], pz = prm.pts[3 * j + 2];
   const V3t<float> p{static_cast<float>(px - prm.cx), static_cast<float>(py - prm.cy), static_cast<float>(pz - prm.cz)};
+  const float margin = 1e-3f + 4e-6f * (fabsf(p.x) + fabsf(p.y) + fabsf(p.z));
   float best = 3.4e38f;
   double best64 = 1e300;
-  float lim = 0.0f;
-  if (PASS == 2) {
-    const float d1 = prm.d32[ii];
-    lim = d1 + 1e-3f + 1e-5f * d1;
+  float bound = 3.4e38f;
+  if (PASS == 1) {
+    for (int q = 0; q < prm.nclus; ++q) {  // least upper bound of the minimum distance
+      const float4 s = __ldg(prm.clus + q);
+      const float dx = p.x - s.x, dy = p.y - s.y, dz = p.z - s.z;
+      bound = fminf(bound, sqrtf(dx * dx + dy * dy + dz * dz) + s.w);
+    }
+  } else {
+    const float d1 = prm.d32[j];
+    bound = d1 + 1e-3f + 1e-5f * d1;  // candidate limit (as the full scan)
   }
-  unsigned long long cand = 0;
-  for (std::size_t t0 = 0; t0 < prm.nt; t0 += kDistTile) {
-    const int cnt = static_cast<int>(prm.nt - t0 < static_cast<std::size_t>(kDistTile) ? prm.nt - t0 : kDistTile);
-    __syncthreads();
-    for (int k = threadIdx.x; k < cnt * 3; k += blockDim.x) s_tri[k] = prm.tri32[3 * t0 + k];
-    __syncthreads();
-    for (int k = 0; k < cnt; ++k) {
-      const float4 A = s_tri[3 * k], B = s_tri[3 * k + 1], C = s_tri[3 * k + 2];
-      const float d2 = point_tri_dist2<float>(p, {A.x, A.y, A.z}, {B.x, B.y, B.z}, {C.x, C.y, C.z});
-      const float d = sqrtf(d2);
+  unsigned long long cand = 0, visits = 0;
+  for (int q = 0; q < prm.nclus; ++q) {
+    const float4 s = __ldg(prm.clus + q);
+    const float dx = p.x - s.x, dy = p.y - s.y, dz = p.z - s.z;
+    const float lb = sqrtf(dx * dx + dy * dy + dz * dz) - s.w;
+    if (lb > (PASS == 1 ? fminf(bound, best) : bound) + margin) continue;
+    ++visits;
+    for (int k = 0; k < kDistCluster; ++k) {
+      const std::size_t t = static_cast<std::size_t>(q) * kDistCluster + k;
+      const float4 A = __ldg(prm.tri32 + 3 * t), B = __ldg(prm.tri32 + 3 * t + 1), C = __ldg(prm.tri32 + 3 * t + 2);
+      const float d = sqrtf(point_tri_dist2<float>(p, {A.x, A.y, A.z}, {B.x, B.y, B.z}, {C.x, C.y, C.z}));
       if (PASS == 1) {
         best = fminf(best, d);
-      } else if (d <= lim) {
-        const std::uint32_t* e = prm.tri + 3 * (t0 + k);
+      } else if (d <= bound) {
+        const std::uint32_t* e = prm.tri + 3 * static_cast<std::size_t>(prm.slot_tri[t]);
         const double* a = prm.xyz + 3 * static_cast<std::size_t>(e[0]);
         const double* b = prm.xyz + 3 * static_cast<std::size_t>(e[1]);
         const double* c = prm.xyz + 3 * static_cast<std::size_t>(e[2]);
-        const double q = point_tri_dist2<double>({px, py, pz}, {a[0], a[1], a[2]}, {b[0], b[1], b[2]},
-                                                 {c[0], c[1], c[2]});
-        best64 = q < best64 ? q : best64;
+        const double q2 = point_tri_dist2<double>({px, py, pz}, {a[0], a[1], a[2]}, {b[0], b[1], b[2]},
+                                                  {c[0], c[1], c[2]});
+        best64 = q2 < best64 ? q2 : best64;
         ++cand;
       }
     }
   }
-  if (!valid) return;
-  if (PASS == 1) prm.d32[i] = best;
-  else {
-    prm.out[i] = __dsqrt_rn(best64);
+  if (PASS == 1) {
+    prm.d32[j] = best;
+    if (prm.counters) atomicAdd(prm.counters + 5, visits);
+  } else {
+    prm.out[j] = __dsqrt_rn(best64);
     if (prm.counters) atomicAdd(prm.counters + 4, cand);
   }
 }

@@ -246,7 +246,7 @@ struct nm_ctx {
   DBuf tri, sub, edges, cont, comp_tiles, xyz64, tri_idx, comp_off, comp_box, cullmask;
   // certified cells (cull_outside = 2, cells.cuh)
   bool cells = false;
-  DBuf sp_part, sp_det, cell_state, cell_child, cell_cert, cell_blk, cell_grids, clus, clus_tri, clus_tsph, unk, sp_list, sp_chunk, sp_cnt, rep_pts, rep_s, rep_m, rep_f;
+  DBuf dist_clus, dist_slot, dist_ord, sp_part, sp_det, cell_state, cell_child, cell_cert, cell_blk, cell_grids, clus, clus_tri, clus_tsph, unk, sp_list, sp_chunk, sp_cnt, rep_pts, rep_s, rep_m, rep_f;
   std::uint64_t cells_total = 0, cells_certified = 0, cell_reps = 0, sparse_pairs = 0, sparse_evals = 0;
   double ms_cells = 0.0;  // host wall time of the certification (nm_set_surfaces)
   std::vector<std::uint32_t> comp_off_h;
@@ -259,7 +259,7 @@ struct nm_ctx {
       s_out, word;
 
   ~nm_ctx() {
-    for (DBuf* b : {&sp_part, &sp_det, &cell_state, &cell_child, &cell_cert, &cell_blk, &cell_grids, &clus, &clus_tri, &clus_tsph, &unk, &sp_list, &sp_chunk, &sp_cnt, &rep_pts, &rep_s,
+    for (DBuf* b : {&dist_clus, &dist_slot, &dist_ord, &sp_part, &sp_det, &cell_state, &cell_child, &cell_cert, &cell_blk, &cell_grids, &clus, &clus_tri, &clus_tsph, &unk, &sp_list, &sp_chunk, &sp_cnt, &rep_pts, &rep_s,
                     &rep_m, &rep_f})
       b->release();
     for (DBuf* b : {&tri, &sub, &edges, &cont, &comp_tiles, &xyz64, &tri_idx, &comp_off, &comp_box, &cullmask, &pts, &masks, &flagmask, &nbr, &known, &want, &fkeys, &frontier, &lex, &region, &bfaces, &btri,
@@ -2143,13 +2143,63 @@ int nm_point_surface_distance(nm_ctx* c, const double* pts, std::size_t n, const
         hi[a] = std::max(hi[a], xyz[3 * v + a]);
       }
     const double ctr[3] = {0.5 * (lo[0] + hi[0]), 0.5 * (lo[1] + hi[1]), 0.5 * (lo[2] + hi[2])};
-    std::vector<float4> h32(3 * nt);
-    for (std::size_t t = 0; t < nt; ++t)
-      for (int k = 0; k < 3; ++k) {
-        const double* v = xyz + 3 * std::size_t(tri[3 * t + k]);
-        h32[3 * t + k] = make_float4(float(v[0] - ctr[0]), float(v[1] - ctr[1]), float(v[2] - ctr[2]), 0.0f);
+    const double span = std::max({hi[0] - lo[0], hi[1] - lo[1], hi[2] - lo[2], 1e-6}) * 1.5;
+    auto morton = [&](const double* m) {  // 30-bit key in the centred frame (spread10h)
+      std::uint32_t q[3];
+      for (int a = 0; a < 3; ++a)
+        q[a] = static_cast<std::uint32_t>(std::clamp((m[a] - ctr[a]) / span * 1024.0 + 512.0, 0.0, 1023.0));
+      return spread10h(q[0]) | (spread10h(q[1]) << 1) | (spread10h(q[2]) << 2);
+    };
+    // clusters of kDistCluster triangles in Morton order of their centroids,
+    // each with a bounding sphere (the last cluster padded by repeating a
+    // triangle, which cannot change a minimum)
+    std::vector<std::pair<std::uint32_t, std::uint32_t>> kk(nt);
+    for (std::size_t t = 0; t < nt; ++t) {
+      double m[3] = {0, 0, 0};
+      for (int k = 0; k < 3; ++k)
+        for (int a = 0; a < 3; ++a) m[a] += xyz[3 * std::size_t(tri[3 * t + k]) + a] / 3.0;
+      kk[t] = {morton(m), static_cast<std::uint32_t>(t)};
+    }
+    std::stable_sort(kk.begin(), kk.end(), [](auto& x, auto& y) { return x.first < y.first; });
+    const std::size_t nclus = (nt + nm::kDistCluster - 1) / nm::kDistCluster;
+    std::vector<float4> h32(3 * nclus * nm::kDistCluster), hclus(nclus);
+    std::vector<std::uint32_t> hslot(nclus * nm::kDistCluster);
+    for (std::size_t q = 0; q < nclus; ++q) {
+      double blo[3] = {1e300, 1e300, 1e300}, bhi[3] = {-1e300, -1e300, -1e300};
+      for (int k = 0; k < nm::kDistCluster; ++k) {
+        const std::size_t slot = q * nm::kDistCluster + k;
+        const std::uint32_t t = kk[std::min(slot, nt - 1)].second;
+        hslot[slot] = t;
+        for (int v = 0; v < 3; ++v) {
+          const double* X = xyz + 3 * std::size_t(tri[3 * t + v]);
+          h32[3 * slot + v] = make_float4(float(X[0] - ctr[0]), float(X[1] - ctr[1]), float(X[2] - ctr[2]), 0.0f);
+          for (int a = 0; a < 3; ++a) {
+            blo[a] = std::min(blo[a], X[a] - ctr[a]);
+            bhi[a] = std::max(bhi[a], X[a] - ctr[a]);
+          }
+        }
       }
-    auto* d_t32 = c->dist_tri.as<float4>(3 * nt);
+      const float fc[3] = {float(0.5 * (blo[0] + bhi[0])), float(0.5 * (blo[1] + bhi[1])), float(0.5 * (blo[2] + bhi[2]))};
+      double rho = 0.0;
+      for (int k = 0; k < nm::kDistCluster; ++k)
+        for (int v = 0; v < 3; ++v) {
+          const double* X = xyz + 3 * std::size_t(tri[3 * hslot[q * nm::kDistCluster + k] + v]);
+          double d2 = 0.0;
+          for (int a = 0; a < 3; ++a) d2 += (X[a] - ctr[a] - fc[a]) * (X[a] - ctr[a] - fc[a]);
+          rho = std::max(rho, std::sqrt(d2));
+        }
+      hclus[q] = make_float4(fc[0], fc[1], fc[2], std::nextafter(float(rho * (1.0 + 1e-6) + 1e-5), INFINITY));
+    }
+    // evaluation order of the points: Morton (coherent warps), results by index
+    std::vector<std::pair<std::uint32_t, std::uint32_t>> pk(n);
+    for (std::size_t i = 0; i < n; ++i) pk[i] = {morton(pts + 3 * i), static_cast<std::uint32_t>(i)};
+    std::stable_sort(pk.begin(), pk.end(), [](auto& x, auto& y) { return x.first < y.first; });
+    std::vector<std::uint32_t> hord(std::max<std::size_t>(n, 1));
+    for (std::size_t i = 0; i < n; ++i) hord[i] = pk[i].second;
+    auto* d_t32 = c->dist_tri.as<float4>(h32.size());
+    auto* d_clus = c->dist_clus.as<float4>(nclus);
+    auto* d_slot = c->dist_slot.as<std::uint32_t>(hslot.size());
+    auto* d_ord = c->dist_ord.as<std::uint32_t>(hord.size());
     auto* d_xyz = c->dist_xyz.as<double>(3 * std::max<std::size_t>(nv, 1));
     auto* d_idx = c->dist_idx.as<std::uint32_t>(3 * nt);
     auto* d_pts = c->pts.as<double>(3 * std::max<std::size_t>(n, 1));
@@ -2160,10 +2210,14 @@ int nm_point_surface_distance(nm_ctx* c, const double* pts, std::size_t n, const
     NM_CUDA(cudaMemcpyAsync(d_t32, h32.data(), h32.size() * sizeof(float4), cudaMemcpyHostToDevice, st));
     NM_CUDA(cudaMemcpyAsync(d_xyz, xyz, 3 * nv * sizeof(double), cudaMemcpyHostToDevice, st));
     NM_CUDA(cudaMemcpyAsync(d_idx, tri, 3 * nt * sizeof(std::uint32_t), cudaMemcpyHostToDevice, st));
+    NM_CUDA(cudaMemcpyAsync(d_clus, hclus.data(), nclus * sizeof(float4), cudaMemcpyHostToDevice, st));
+    NM_CUDA(cudaMemcpyAsync(d_slot, hslot.data(), hslot.size() * sizeof(std::uint32_t), cudaMemcpyHostToDevice, st));
+    NM_CUDA(cudaMemcpyAsync(d_ord, hord.data(), hord.size() * sizeof(std::uint32_t), cudaMemcpyHostToDevice, st));
     if (n) NM_CUDA(cudaMemcpyAsync(d_pts, pts, 3 * n * sizeof(double), cudaMemcpyHostToDevice, st));
     NM_CUDA(cudaStreamSynchronize(st));  // h32 is released at scope exit
     if (n) {
-      nm::DistParams prm{d_pts, n, d_t32, d_xyz, d_idx, nt, ctr[0], ctr[1], ctr[2], d_d32, d_out, counters};
+      nm::DistParams prm{d_pts, n,      d_ord,  d_t32,  d_slot, d_clus, static_cast<int>(nclus), d_xyz,
+                         d_idx, ctr[0], ctr[1], ctr[2], d_d32,  d_out,  counters};
       if (stats) NM_CUDA(cudaEventRecord(c->ev[0], st));
       const unsigned grid = static_cast<unsigned>((n + 255) / 256);
       nm::k_point_surface_distance<1><<<grid, 256, 0, st>>>(prm);
@@ -2180,6 +2234,7 @@ int nm_point_surface_distance(nm_ctx* c, const double* pts, std::size_t n, const
       stats->triangles = nt;
       stats->evals = 2ull * n * nt;
       stats->flagged_pairs = h[4];  // fp64 candidate evaluations
+      stats->far_subtiles = h[5];   // pass-1 cluster visits (of n x clusters)
       stats->launches = 2;
       NM_CUDA(cudaEventElapsedTime(&stats->ms_label, c->ev[0], c->ev[1]));
     }
