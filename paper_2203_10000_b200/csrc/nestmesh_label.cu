@@ -851,33 +851,135 @@ std::pair<std::size_t, std::size_t> refine_dev(nm_ctx* c, const double* d_nodes,
 #define NM_CELL_AXIS 120
 #endif
 // Certified cells of every compartment (cells.cuh), built once per surface
-// set from the surfaces alone. hbox: the 13-DOP slabs (centred frame).
-void build_cells(nm_ctx* c, const double* xyz, const std::uint32_t* tri, const std::uint32_t* comp_off,
-                 const std::vector<float4>& hbox) {
-  const auto t0 = std::chrono::steady_clock::now();
-  const bool verbose = std::getenv("NM_CELL_VERBOSE") != nullptr;
-  auto tl = t0;
-  auto lap = [&](const char* what) {
-    if (!verbose) return;
-    const auto t = std::chrono::steady_clock::now();
-    std::fprintf(stderr, "[cells] %-6s %8.1f ms\n", what, std::chrono::duration<double, std::milli>(t - tl).count());
-    tl = t;
+// set from the surfaces alone, in four phases: geometry (grids + clusters),
+// certification (level-1 cells and children, on the device), runs (x-runs of
+// certified cells -> winding number, neighbour run or representative) and
+// resolve (representatives evaluated by the sparse k_label, final codes).
+// Host loops run one compartment per thread: every compartment's grid,
+// blocks, runs and representatives are independent.
+class CellBuild {
+ public:
+  CellBuild(nm_ctx* c, const double* xyz, const std::uint32_t* tri, const std::uint32_t* comp_off,
+            const std::vector<float4>& hbox)
+      : c_(c), xyz_(xyz), tri_(tri), comp_off_(comp_off), hbox_(hbox), K_(c->K), ctr_{c->cx, c->cy, c->cz},
+        st_(c->stream), t0_(std::chrono::steady_clock::now()), tl_(t0_),
+        verbose_(std::getenv("NM_CELL_VERBOSE") != nullptr) {}
+
+  void run() {
+    geometry();
+    certify();
+    runs();
+    resolve();
+  }
+
+ private:
+  // run value of a level-1 or child run: 0 / 1 known; kRep + r: the
+  // compartment's local representative r; kRun + q: the value of the
+  // compartment's level-1 run q; kLeft / kRight: the neighbour parent's run
+  // (resolved once the row is scanned)
+  static constexpr std::int64_t kUnknown = -1, kLeft = -2, kRight = -3, kRep = 1ll << 40, kRun = 1ll << 41;
+  static constexpr int S = nm::kSubCells;
+  struct FineRun {
+    std::size_t row;  // level-1 row base (global cell index of ix = 0)
+    int fx0, fx1;     // fine x range (fine index = 4 ix + sx)
+    int sy, sz;
+    std::int64_t v;
   };
-  const int K = c->K;
-  const double ctr[3] = {c->cx, c->cy, c->cz};
-  std::vector<nm::CellGrid> G(K);
-  std::vector<float4> clus;
-  std::vector<std::uint32_t> ctri;
-  std::vector<float4> tsph;
-  std::vector<std::size_t> coff(K + 1, 0);
-  std::size_t total = 0;
-  std::vector<std::vector<float4>> clus_kv(K), tsph_kv(K);
-  std::vector<std::vector<std::uint32_t>> ctri_kv(K);
-  parallel_for(K, [&](int k) {
-    auto& clus = clus_kv[k];
-    auto& ctri = ctri_kv[k];
-    auto& tsph = tsph_kv[k];
-    const std::uint32_t b = comp_off[k], e = comp_off[k + 1];
+
+  nm_ctx* c_;
+  const double* xyz_;
+  const std::uint32_t* tri_;
+  const std::uint32_t* comp_off_;
+  const std::vector<float4>& hbox_;
+  const int K_;
+  const double ctr_[3];
+  cudaStream_t st_;
+  std::chrono::steady_clock::time_point t0_, tl_;
+  bool verbose_;
+
+  std::vector<nm::CellGrid> G_;
+  std::vector<std::size_t> coff_;       // first cluster of each compartment
+  std::size_t total_ = 0;               // level-1 cells
+  std::unique_ptr<std::uint8_t[]> cert1_;
+  std::unique_ptr<std::uint32_t[]> block_of_;  // local child block of each uncertified cell
+  std::vector<std::size_t> boff_;       // first child block of each compartment
+  std::size_t nchild_ = 0;
+  std::unique_ptr<std::uint8_t[]> child_;
+  std::vector<std::vector<double>> reps_;
+  std::vector<std::vector<std::int64_t>> run_val_;
+  std::unique_ptr<std::int32_t[]> run_of_;
+  std::vector<std::vector<FineRun>> fine_;
+  std::size_t nreps_ = 0;
+
+  void lap(const char* what) {
+    if (!verbose_) return;
+    const auto t = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[cells] %-6s %8.1f ms\n", what, std::chrono::duration<double, std::milli>(t - tl_).count());
+    tl_ = t;
+  }
+  // host arrays allocated uninitialised: every entry is written (by a copy or
+  // by its compartment's thread) before it is read
+  template <class T>
+  static std::unique_ptr<T[]> uninit(std::size_t m) {
+    return std::unique_ptr<T[]>(new T[std::max<std::size_t>(m, 1)]);
+  }
+  void up(DBuf& b, const void* src, std::size_t bytes) {
+    void* d = b.get(std::max<std::size_t>(bytes, 1));
+    if (bytes) NM_CUDA(cudaMemcpyAsync(d, src, bytes, cudaMemcpyHostToDevice, st_));
+  }
+  std::size_t cells(int k) const { return static_cast<std::size_t>(G_[k].nx) * G_[k].ny * G_[k].nz; }
+  const float4* clus_k(int k) const { return static_cast<const float4*>(c_->clus.p) + coff_[k]; }
+  const std::uint32_t* ctri_k(int k) const {
+    return static_cast<const std::uint32_t*>(c_->clus_tri.p) + coff_[k] * nm::kCluster;
+  }
+  const float4* tsph_k(int k) const { return static_cast<const float4*>(c_->clus_tsph.p) + coff_[k] * nm::kCluster; }
+  int nclus(int k) const { return static_cast<int>(coff_[k + 1] - coff_[k]); }
+  bool outside_dop(int k, double x, double y, double z) const {
+    const float* dop = reinterpret_cast<const float*>(&hbox_[static_cast<std::size_t>(k) * nm::kDopF4]);
+    const float xf = float(x), yf = float(y), zf = float(z);
+    for (int d = 0; d < nm::kDopDirs; ++d) {
+      const float pr = nm::dop_dir(d, 0) * xf + nm::dop_dir(d, 1) * yf + nm::dop_dir(d, 2) * zf;
+      if (pr < dop[2 * d] || pr > dop[2 * d + 1]) return true;
+    }
+    return false;
+  }
+  std::uint8_t& child_at(int k, std::size_t row, int fx, int sy, int sz) {
+    const std::size_t b = boff_[k] + block_of_[row + fx / S];
+    return child_[b * nm::kChildren + (sz * S + sy) * S + fx % S];
+  }
+
+  // ---- geometry: per compartment its grid and Morton-ordered clusters ----
+  void geometry() {
+    const int K = K_;
+    G_.assign(K, nm::CellGrid{});
+    coff_.assign(K + 1, 0);
+    std::vector<std::vector<float4>> clus_kv(K), tsph_kv(K);
+    std::vector<std::vector<std::uint32_t>> ctri_kv(K);
+    parallel_for(K, [&](int k) { compartment_geometry(k, clus_kv[k], ctri_kv[k], tsph_kv[k]); });
+    std::vector<float4> clus, tsph;
+    std::vector<std::uint32_t> ctri;
+    for (int k = 0; k < K; ++k) {
+      G_[k].off = static_cast<std::uint32_t>(total_);
+      total_ += cells(k);
+      if (total_ > 0xffffffffull) throw Error("certified-cell grids exceed 2^32 cells");
+      coff_[k] = clus.size();
+      clus.insert(clus.end(), clus_kv[k].begin(), clus_kv[k].end());
+      ctri.insert(ctri.end(), ctri_kv[k].begin(), ctri_kv[k].end());
+      tsph.insert(tsph.end(), tsph_kv[k].begin(), tsph_kv[k].end());
+    }
+    coff_[K] = clus.size();
+    lap("setup");
+    up(c_->clus, clus.data(), clus.size() * sizeof(float4));
+    up(c_->clus_tri, ctri.data(), ctri.size() * sizeof(std::uint32_t));
+    up(c_->clus_tsph, tsph.data(), tsph.size() * sizeof(float4));
+  }
+
+  void compartment_geometry(int k, std::vector<float4>& clus, std::vector<std::uint32_t>& ctri,
+                            std::vector<float4>& tsph) {
+    const double* ctr = ctr_;
+    const double* xyz = xyz_;
+    const std::uint32_t* tri = tri_;
+    const std::uint32_t b = comp_off_[k], e = comp_off_[k + 1];
     nm::CellGrid g{0.0, 0.0, 0.0, 1.0, 0, 0, 0, 0u};
     if (e > b) {
       double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
@@ -894,7 +996,7 @@ void build_cells(nm_ctx* c, const double* xyz, const std::uint32_t* tri, const s
           }
         std::uint32_t q[3];
         for (int a = 0; a < 3; ++a)
-          q[a] = static_cast<std::uint32_t>(std::clamp((m[a] + ctr[a] - c->lo[a]) / c->span * 1024.0, 0.0, 1023.0));
+          q[a] = static_cast<std::uint32_t>(std::clamp((m[a] + ctr[a] - c_->lo[a]) / c_->span * 1024.0, 0.0, 1023.0));
         kk.emplace_back(spread10h(q[0]) | (spread10h(q[1]) << 1) | (spread10h(q[2]) << 2), t);
       }
       std::stable_sort(kk.begin(), kk.end(), [](auto& x, auto& y) { return x.first < y.first; });
@@ -944,284 +1046,256 @@ void build_cells(nm_ctx* c, const double* xyz, const std::uint32_t* tri, const s
       g.ny = n3[1];
       g.nz = n3[2];
     }
-    G[k] = g;
-  });
-  for (int k = 0; k < K; ++k) {
-    G[k].off = static_cast<std::uint32_t>(total);
-    total += static_cast<std::size_t>(G[k].nx) * G[k].ny * G[k].nz;
-    if (total > 0xffffffffull) throw Error("certified-cell grids exceed 2^32 cells");
-    coff[k] = clus.size();
-    clus.insert(clus.end(), clus_kv[k].begin(), clus_kv[k].end());
-    ctri.insert(ctri.end(), ctri_kv[k].begin(), ctri_kv[k].end());
-    tsph.insert(tsph.end(), tsph_kv[k].begin(), tsph_kv[k].end());
+    G_[k] = g;
   }
-  coff[K] = clus.size();
-  lap("setup");
-  cudaStream_t st = c->stream;
-  auto up = [&](DBuf& b, const void* src, std::size_t bytes) {
-    void* d = b.get(std::max<std::size_t>(bytes, 1));
-    if (bytes) NM_CUDA(cudaMemcpyAsync(d, src, bytes, cudaMemcpyHostToDevice, st));
-  };
-  up(c->clus, clus.data(), clus.size() * sizeof(float4));
-  up(c->clus_tri, ctri.data(), ctri.size() * sizeof(std::uint32_t));
-  up(c->clus_tsph, tsph.data(), tsph.size() * sizeof(float4));
-  auto clus_k = [&](int k) { return static_cast<const float4*>(c->clus.p) + coff[k]; };
-  auto ctri_k = [&](int k) { return static_cast<const std::uint32_t*>(c->clus_tri.p) + coff[k] * nm::kCluster; };
-  auto tsph_k = [&](int k) { return static_cast<const float4*>(c->clus_tsph.p) + coff[k] * nm::kCluster; };
 
-  // ---- level 1 ----
-  auto* cert_d = c->cell_cert.as<std::uint8_t>(std::max<std::size_t>(total, 1));
-  for (int k = 0; k < K; ++k) {
-    const std::size_t nc = static_cast<std::size_t>(G[k].nx) * G[k].ny * G[k].nz;
-    if (!nc) continue;
-    const std::size_t nbrick = static_cast<std::size_t>((G[k].nx + 3) / 4) * ((G[k].ny + 3) / 4) * ((G[k].nz + 1) / 2);
-    nm::k_cell_certify<<<static_cast<unsigned>((nbrick * 32 + 255) / 256), 256, 0, st>>>(
-        G[k], clus_k(k), static_cast<int>(coff[k + 1] - coff[k]), ctri_k(k), tsph_k(k), static_cast<const double*>(c->xyz64.p),
-        static_cast<const std::uint32_t*>(c->tri_idx.p), c->cx, c->cy, c->cz, cert_d);
-  }
-  NM_CUDA(cudaGetLastError());
-  // host arrays below are allocated uninitialised: every entry is written
-  // (by a copy or by its compartment's thread) before it is read
-  auto uninit = [](auto* tag, std::size_t m) {
-    using T = std::remove_pointer_t<decltype(tag)>;
-    return std::unique_ptr<T[]>(new T[std::max<std::size_t>(m, 1)]);
-  };
-  auto cert1 = uninit(static_cast<std::uint8_t*>(nullptr), total);
-  if (total) NM_CUDA(cudaMemcpyAsync(cert1.get(), cert_d, total, cudaMemcpyDeviceToHost, st));
-  NM_CUDA(cudaStreamSynchronize(st));
-  lap("l1");
-
-  // ---- level 2: children of every uncertified cell ----
-  // (host loops run one compartment per thread; every compartment's grid,
-  // blocks, runs and representatives are independent)
-  auto parallel_k = [&](auto&& f) { parallel_for(K, f); };
-  auto block_of = uninit(static_cast<std::uint32_t*>(nullptr), total);  // local block index (uncertified cells)
-  std::vector<std::vector<std::uint32_t>> blk_k(K);          // local cell index per local block
-  parallel_k([&](int k) {
-    const std::size_t nc = static_cast<std::size_t>(G[k].nx) * G[k].ny * G[k].nz;
-    for (std::size_t q = 0; q < nc; ++q)
-      if (!cert1[G[k].off + q]) {
-        block_of[G[k].off + q] = static_cast<std::uint32_t>(blk_k[k].size());
-        blk_k[k].push_back(static_cast<std::uint32_t>(q));
-      }
-  });
-  std::vector<std::size_t> boff(K + 1, 0);
-  for (int k = 0; k < K; ++k) boff[k + 1] = boff[k] + blk_k[k].size();
-  lap("blocks");
-  const std::size_t nblk = boff[K];
-  const std::size_t nchild = nblk * nm::kChildren;
-  auto child = uninit(static_cast<std::uint8_t*>(nullptr), nchild);
-  if (nblk) {
-    std::vector<std::uint32_t> blk_cells(nblk);
-    for (int k = 0; k < K; ++k) std::copy(blk_k[k].begin(), blk_k[k].end(), blk_cells.begin() + boff[k]);
-    up(c->cell_blk, blk_cells.data(), nblk * sizeof(std::uint32_t));
-    auto* ch_d = c->cell_child.as<std::uint8_t>(nblk * nm::kChildren);
+  // ---- certification: level-1 cells, then the children of uncertified cells ----
+  void certify() {
+    const int K = K_;
+    auto* cert_d = c_->cell_cert.as<std::uint8_t>(std::max<std::size_t>(total_, 1));
     for (int k = 0; k < K; ++k) {
-      const std::size_t nb = boff[k + 1] - boff[k];
-      if (!nb) continue;
-      nm::k_child_certify<<<static_cast<unsigned>((nb * 64 + 255) / 256), 256, 0, st>>>(
-          G[k], static_cast<const std::uint32_t*>(c->cell_blk.p) + boff[k], nb, clus_k(k),
-          static_cast<int>(coff[k + 1] - coff[k]), ctri_k(k), tsph_k(k), static_cast<const double*>(c->xyz64.p),
-          static_cast<const std::uint32_t*>(c->tri_idx.p), c->cx, c->cy, c->cz, ch_d + boff[k] * nm::kChildren);
+      if (!cells(k)) continue;
+      const std::size_t nbrick =
+          static_cast<std::size_t>((G_[k].nx + 3) / 4) * ((G_[k].ny + 3) / 4) * ((G_[k].nz + 1) / 2);
+      nm::k_cell_certify<<<static_cast<unsigned>((nbrick * 32 + 255) / 256), 256, 0, st_>>>(
+          G_[k], clus_k(k), nclus(k), ctri_k(k), tsph_k(k), static_cast<const double*>(c_->xyz64.p),
+          static_cast<const std::uint32_t*>(c_->tri_idx.p), c_->cx, c_->cy, c_->cz, cert_d);
     }
     NM_CUDA(cudaGetLastError());
-    if (verbose) {
-      NM_CUDA(cudaStreamSynchronize(st));
+    cert1_ = uninit<std::uint8_t>(total_);
+    if (total_) NM_CUDA(cudaMemcpyAsync(cert1_.get(), cert_d, total_, cudaMemcpyDeviceToHost, st_));
+    NM_CUDA(cudaStreamSynchronize(st_));
+    lap("l1");
+
+    block_of_ = uninit<std::uint32_t>(total_);
+    std::vector<std::vector<std::uint32_t>> blk_k(K);  // local cell index per local block
+    parallel_for(K, [&](int k) {
+      for (std::size_t q = 0; q < cells(k); ++q)
+        if (!cert1_[G_[k].off + q]) {
+          block_of_[G_[k].off + q] = static_cast<std::uint32_t>(blk_k[k].size());
+          blk_k[k].push_back(static_cast<std::uint32_t>(q));
+        }
+    });
+    boff_.assign(K + 1, 0);
+    for (int k = 0; k < K; ++k) boff_[k + 1] = boff_[k] + blk_k[k].size();
+    lap("blocks");
+    const std::size_t nblk = boff_[K];
+    nchild_ = nblk * nm::kChildren;
+    child_ = uninit<std::uint8_t>(nchild_);
+    if (!nblk) return;
+    std::vector<std::uint32_t> blk_cells(nblk);
+    for (int k = 0; k < K; ++k) std::copy(blk_k[k].begin(), blk_k[k].end(), blk_cells.begin() + boff_[k]);
+    up(c_->cell_blk, blk_cells.data(), nblk * sizeof(std::uint32_t));
+    auto* ch_d = c_->cell_child.as<std::uint8_t>(nchild_);
+    for (int k = 0; k < K; ++k) {
+      const std::size_t nb = boff_[k + 1] - boff_[k];
+      if (!nb) continue;
+      nm::k_child_certify<<<static_cast<unsigned>((nb * 64 + 255) / 256), 256, 0, st_>>>(
+          G_[k], static_cast<const std::uint32_t*>(c_->cell_blk.p) + boff_[k], nb, clus_k(k), nclus(k), ctri_k(k),
+          tsph_k(k), static_cast<const double*>(c_->xyz64.p), static_cast<const std::uint32_t*>(c_->tri_idx.p), c_->cx,
+          c_->cy, c_->cz, ch_d + boff_[k] * nm::kChildren);
+    }
+    NM_CUDA(cudaGetLastError());
+    if (verbose_) {
+      NM_CUDA(cudaStreamSynchronize(st_));
       lap("l2kern");
     }
-    NM_CUDA(cudaMemcpyAsync(child.get(), ch_d, nchild, cudaMemcpyDeviceToHost, st));
-    NM_CUDA(cudaStreamSynchronize(st));
+    NM_CUDA(cudaMemcpyAsync(child_.get(), ch_d, nchild_, cudaMemcpyDeviceToHost, st_));
+    NM_CUDA(cudaStreamSynchronize(st_));
+    lap("l2");
   }
-  lap("l2");
 
-  // ---- winding numbers of runs ----
-  auto outside_dop = [&](int k, double x, double y, double z) {
-    const float* dop = reinterpret_cast<const float*>(&hbox[static_cast<std::size_t>(k) * nm::kDopF4]);
-    const float xf = float(x), yf = float(y), zf = float(z);
-    for (int d = 0; d < nm::kDopDirs; ++d) {
-      const float pr = nm::dop_dir(d, 0) * xf + nm::dop_dir(d, 1) * yf + nm::dop_dir(d, 2) * zf;
-      if (pr < dop[2 * d] || pr > dop[2 * d + 1]) return true;
-    }
-    return false;
-  };
-  // run value: 0 / 1 known; kRep + r: local representative r of the
-  // compartment; kRun + q: the value of the compartment's level-1 run q
-  constexpr std::int64_t kUnknown = -1, kRep = 1ll << 40, kRun = 1ll << 41;
-  constexpr int S = nm::kSubCells;
-  struct FineRun {
-    std::size_t row;  // level-1 row base (global cell index of ix = 0)
-    int fx0, fx1;     // fine x range (fine index = 4 ix + sx)
-    int sy, sz;
-    std::int64_t v;
-  };
-  std::vector<std::vector<double>> reps(K);
-  std::vector<std::vector<std::int64_t>> run_val(K);   // level-1 runs per compartment
-  auto run_of = uninit(static_cast<std::int32_t*>(nullptr), total);  // certified level-1 cell -> its local run
-  std::vector<std::vector<FineRun>> fine(K);
-  auto child_at = [&](int k, std::size_t row, int fx, int sy, int sz) -> std::uint8_t& {
-    const std::size_t b = boff[k] + block_of[row + fx / S];
-    return child[b * nm::kChildren + (sz * S + sy) * S + fx % S];
-  };
-  parallel_k([&](int k) {
-    const nm::CellGrid& g = G[k];
-    auto new_rep = [&](double x, double y, double z) {
-      const std::int64_t v = kRep + static_cast<std::int64_t>(reps[k].size() / 3);
-      reps[k].insert(reps[k].end(), {x + ctr[0], y + ctr[1], z + ctr[2]});
-      return v;
-    };
+  // ---- runs: every maximal x-run of certified cells gets one winding number ----
+  void runs() {
+    reps_.assign(K_, {});
+    run_val_.assign(K_, {});
+    fine_.assign(K_, {});
+    run_of_ = uninit<std::int32_t>(total_);
+    parallel_for(K_, [&](int k) { compartment_runs(k); });
+    lap("runs");
+  }
+
+  std::int64_t new_rep(int k, double x, double y, double z) {
+    const std::int64_t v = kRep + static_cast<std::int64_t>(reps_[k].size() / 3);
+    reps_[k].insert(reps_[k].end(), {x + ctr_[0], y + ctr_[1], z + ctr_[2]});
+    return v;
+  }
+
+  void compartment_runs(int k) {
+    const nm::CellGrid& g = G_[k];
     for (int iz = 0; iz < g.nz; ++iz)
       for (int iy = 0; iy < g.ny; ++iy) {
         const std::size_t row = g.off + (static_cast<std::size_t>(iz) * g.ny + iy) * g.nx;
         const double y = g.oy + (iy + 0.5) * g.B, z = g.oz + (iz + 0.5) * g.B;
         for (int ix = 0; ix < g.nx;) {
-          const bool c1 = cert1[row + ix];
+          const bool c1 = cert1_[row + ix];
           int jx = ix;
-          while (jx + 1 < g.nx && bool(cert1[row + jx + 1]) == c1) ++jx;
+          while (jx + 1 < g.nx && bool(cert1_[row + jx + 1]) == c1) ++jx;
           if (c1) {
-            // level-1 run [ix, jx]
+            // level-1 run [ix, jx]: grid edge or an end outside the 13-DOP -> 0
             std::int64_t v;
             if (ix == 0 || jx == g.nx - 1 || outside_dop(k, g.ox + (ix + 0.5) * g.B, y, z) ||
                 outside_dop(k, g.ox + (jx + 0.5) * g.B, y, z))
               v = 0;
             else
-              v = new_rep(g.ox + ((ix + jx) / 2 + 0.5) * g.B, y, z);
-            for (int q = ix; q <= jx; ++q) run_of[row + q] = static_cast<std::int32_t>(run_val[k].size());
-            run_val[k].push_back(v);
+              v = new_rep(k, g.ox + ((ix + jx) / 2 + 0.5) * g.B, y, z);
+            for (int q = ix; q <= jx; ++q) run_of_[row + q] = static_cast<std::int32_t>(run_val_[k].size());
+            run_val_[k].push_back(v);
           } else {
-            // segment [ix, jx] of uncertified cells: runs of certified children per (sy, sz) sub-row
-            const double b = g.B / S;
-            const int f_lo = S * ix, f_hi = S * jx + S - 1;
-            for (int sz = 0; sz < S; ++sz)
-              for (int sy = 0; sy < S; ++sy)
-                for (int f = f_lo; f <= f_hi;) {
-                  if (!child_at(k, row, f, sy, sz)) {
-                    ++f;
-                    continue;
-                  }
-                  int e = f;
-                  while (e + 1 <= f_hi && child_at(k, row, e + 1, sy, sz)) ++e;
-                  std::int64_t v;
-                  if (f == f_lo) {
-                    v = ix == 0 ? 0 : -2;  // left neighbour's run, resolved below (its run id may not exist yet)
-                  } else if (e == f_hi) {
-                    v = jx == g.nx - 1 ? 0 : -3;  // right neighbour's run
-                  } else {
-                    const double yy = g.oy + iy * g.B + (sy + 0.5) * b, zz = g.oz + iz * g.B + (sz + 0.5) * b;
-                    if (outside_dop(k, g.ox + (f + 0.5) * b, yy, zz) || outside_dop(k, g.ox + (e + 0.5) * b, yy, zz))
-                      v = 0;
-                    else
-                      v = new_rep(g.ox + ((f + e) / 2 + 0.5) * b, yy, zz);
-                  }
-                  fine[k].push_back({row, f, e, sy, sz, v});
-                  f = e + 1;
-                }
+            segment_runs(k, g, row, ix, jx, iy, iz);
           }
           ix = jx + 1;
         }
       }
-    // neighbour references: the level-1 runs of the whole row exist now
-    for (FineRun& fr : fine[k]) {
-      if (fr.v == -2) fr.v = kRun + run_of[fr.row + fr.fx0 / S - 1];
-      else if (fr.v == -3) fr.v = kRun + run_of[fr.row + fr.fx1 / S + 1];
+    // neighbour references: the level-1 runs of every row exist now
+    for (FineRun& fr : fine_[k]) {
+      if (fr.v == kLeft) fr.v = kRun + run_of_[fr.row + fr.fx0 / S - 1];
+      else if (fr.v == kRight) fr.v = kRun + run_of_[fr.row + fr.fx1 / S + 1];
     }
-  });
-  lap("runs");
-
-  // ---- representatives (compartment k's are contiguous) ----
-  std::vector<std::uint32_t> rep_cnt(K, 0), rep_first(K + 1, 0);
-  std::vector<double> rep_all;
-  for (int k = 0; k < K; ++k) {
-    rep_first[k] = static_cast<std::uint32_t>(rep_all.size() / 3);
-    rep_cnt[k] = static_cast<std::uint32_t>(reps[k].size() / 3);
-    rep_all.insert(rep_all.end(), reps[k].begin(), reps[k].end());
   }
-  const std::size_t R = rep_all.size() / 3;
-  rep_first[K] = static_cast<std::uint32_t>(R);
-  std::vector<double> rep_w(R, -1.0);
-  if (R) {
-    up(c->rep_pts, rep_all.data(), rep_all.size() * sizeof(double));
-    auto* s_dev = c->rep_s.as<double>(R * K);
-    auto* m_dev = c->rep_m.as<std::uint32_t>(R);
-    auto* f_dev = c->rep_f.as<std::uint32_t>(R);
+
+  // segment [ix, jx] of uncertified level-1 cells: runs of certified children
+  // per (sy, sz) sub-row; a run reaching the segment's end continues into the
+  // certified neighbour parent (or the grid edge)
+  void segment_runs(int k, const nm::CellGrid& g, std::size_t row, int ix, int jx, int iy, int iz) {
+    const double b = g.B / S;
+    const int f_lo = S * ix, f_hi = S * jx + S - 1;
+    for (int sz = 0; sz < S; ++sz)
+      for (int sy = 0; sy < S; ++sy)
+        for (int f = f_lo; f <= f_hi;) {
+          if (!child_at(k, row, f, sy, sz)) {
+            ++f;
+            continue;
+          }
+          int e = f;
+          while (e + 1 <= f_hi && child_at(k, row, e + 1, sy, sz)) ++e;
+          std::int64_t v;
+          if (f == f_lo) {
+            v = ix == 0 ? 0 : kLeft;
+          } else if (e == f_hi) {
+            v = jx == g.nx - 1 ? 0 : kRight;
+          } else {
+            const double yy = g.oy + iy * g.B + (sy + 0.5) * b, zz = g.oz + iz * g.B + (sz + 0.5) * b;
+            if (outside_dop(k, g.ox + (f + 0.5) * b, yy, zz) || outside_dop(k, g.ox + (e + 0.5) * b, yy, zz))
+              v = 0;
+            else
+              v = new_rep(k, g.ox + ((f + e) / 2 + 0.5) * b, yy, zz);
+          }
+          fine_[k].push_back({row, f, e, sy, sz, v});
+          f = e + 1;
+        }
+  }
+
+  // ---- resolve: representatives evaluated, final codes uploaded ----
+  void resolve() {
+    const int K = K_;
+    std::vector<std::uint32_t> rep_cnt(K, 0), rep_first(K + 1, 0);
+    std::vector<double> rep_all;
+    for (int k = 0; k < K; ++k) {  // compartment k's representatives are contiguous
+      rep_first[k] = static_cast<std::uint32_t>(rep_all.size() / 3);
+      rep_cnt[k] = static_cast<std::uint32_t>(reps_[k].size() / 3);
+      rep_all.insert(rep_all.end(), reps_[k].begin(), reps_[k].end());
+    }
+    nreps_ = rep_all.size() / 3;
+    rep_first[K] = static_cast<std::uint32_t>(nreps_);
+    const std::vector<double> rep_w = evaluate_reps(rep_all, rep_cnt, rep_first);
+    lap("reps");
+    auto code = uninit<std::uint32_t>(total_);
+    parallel_for(K, [&](int k) {
+      auto value = [&](std::int64_t v) -> std::int64_t {  // -> 0, 1 or kUnknown
+        if (v >= kRun) v = run_val_[k][static_cast<std::size_t>(v - kRun)];
+        if (v >= kRep) {
+          const double w = rep_w[rep_first[k] + static_cast<std::size_t>(v - kRep)];
+          return w < 0.0 ? kUnknown : static_cast<std::int64_t>(w);
+        }
+        return v;
+      };
+      const nm::CellGrid& g = G_[k];
+      for (std::size_t q = g.off; q < g.off + cells(k); ++q) {
+        if (!cert1_[q]) {
+          code[q] = 3u + static_cast<std::uint32_t>(boff_[k] + block_of_[q]);
+        } else {
+          const std::int64_t w = value(run_val_[k][run_of_[q]]);
+          code[q] = w == kUnknown ? 0u : static_cast<std::uint32_t>(1 + w);
+        }
+      }
+      std::fill(child_.get() + boff_[k] * nm::kChildren, child_.get() + boff_[k + 1] * nm::kChildren, 0);
+      for (const FineRun& fr : fine_[k]) {
+        const std::int64_t w = value(fr.v);
+        if (w == kUnknown) continue;
+        for (int f = fr.fx0; f <= fr.fx1; ++f) child_at(k, fr.row, f, fr.sy, fr.sz) = static_cast<std::uint8_t>(1 + w);
+      }
+    });
+    lap("codes");
+    up(c_->cell_state, code.get(), total_ * sizeof(std::uint32_t));
+    up(c_->cell_child, child_.get(), nchild_);
+    up(c_->cell_grids, G_.data(), G_.size() * sizeof(nm::CellGrid));
+    NM_CUDA(cudaStreamSynchronize(st_));
+    lap("final");
+    c_->cells_total = total_ + nchild_;
+    c_->cells_certified = 0;
+    for (std::size_t q = 0; q < total_; ++q) c_->cells_certified += code[q] == 1 || code[q] == 2;
+    for (std::size_t q = 0; q < nchild_; ++q) c_->cells_certified += child_[q] != 0;
+    c_->cell_reps = nreps_;
+    c_->cells = true;
+    c_->ms_cells = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0_).count();
+  }
+
+  // s at every representative (sparse k_label against its own compartment);
+  // w = round(s) when within 1e-3 of 0 or 1, else -1 (the run stays unresolved)
+  std::vector<double> evaluate_reps(const std::vector<double>& rep_all, const std::vector<std::uint32_t>& rep_cnt,
+                                    const std::vector<std::uint32_t>& rep_first) {
+    const int K = K_;
+    const std::size_t R = nreps_;
+    std::vector<double> rep_w(R, -1.0);
+    if (!R) return rep_w;
+    up(c_->rep_pts, rep_all.data(), rep_all.size() * sizeof(double));
+    auto* s_dev = c_->rep_s.as<double>(R * K);
+    auto* m_dev = c_->rep_m.as<std::uint32_t>(R);
+    auto* f_dev = c_->rep_f.as<std::uint32_t>(R);
     std::vector<std::uint32_t> iota(R);
     std::iota(iota.begin(), iota.end(), 0u);
-    up(c->sp_list, iota.data(), R * sizeof(std::uint32_t));
-    NM_CUDA(cudaMemsetAsync(m_dev, 0, R * sizeof(std::uint32_t), st));
-    NM_CUDA(cudaMemsetAsync(f_dev, 0, R * sizeof(std::uint32_t), st));
+    up(c_->sp_list, iota.data(), R * sizeof(std::uint32_t));
+    NM_CUDA(cudaMemsetAsync(m_dev, 0, R * sizeof(std::uint32_t), st_));
+    NM_CUDA(cudaMemsetAsync(f_dev, 0, R * sizeof(std::uint32_t), st_));
     nm::LabelParams prm{};
-    prm.pts = static_cast<const double*>(c->rep_pts.p);
+    prm.pts = static_cast<const double*>(c_->rep_pts.p);
     prm.n = R;
     prm.order = nullptr;
-    prm.tri = static_cast<const float4*>(c->tri.p);
-    prm.sub = static_cast<const float4*>(c->sub.p);
-    prm.edges = static_cast<const float4*>(c->edges.p);
-    prm.cont = static_cast<const std::uint32_t*>(c->cont.p);
-    prm.comp_tiles = static_cast<const std::uint32_t*>(c->comp_tiles.p);
+    prm.tri = static_cast<const float4*>(c_->tri.p);
+    prm.sub = static_cast<const float4*>(c_->sub.p);
+    prm.edges = static_cast<const float4*>(c_->edges.p);
+    prm.cont = static_cast<const std::uint32_t*>(c_->cont.p);
+    prm.comp_tiles = static_cast<const std::uint32_t*>(c_->comp_tiles.p);
     prm.K = K;
-    prm.cx = c->cx;
-    prm.cy = c->cy;
-    prm.cz = c->cz;
+    prm.cx = c_->cx;
+    prm.cy = c_->cy;
+    prm.cz = c_->cz;
     prm.T = 0.5;
-    prm.band = c->opt.band;
-    prm.tau = c->opt.tau;
-    prm.delta = c->opt.delta_mm;
+    prm.band = c_->opt.band;
+    prm.tau = c_->opt.tau;
+    prm.delta = c_->opt.delta_mm;
     prm.masks = m_dev;
     prm.flagmask = f_dev;
     prm.s_out = s_dev;
-    prm.sp_list = static_cast<const std::uint32_t*>(c->sp_list.p);
-    launch_sparse(c, prm, rep_cnt, st);
+    prm.sp_list = static_cast<const std::uint32_t*>(c_->sp_list.p);
+    launch_sparse(c_, prm, rep_cnt, st_);
     std::vector<double> s(R * K);
-    NM_CUDA(cudaMemcpyAsync(s.data(), s_dev, R * K * sizeof(double), cudaMemcpyDeviceToHost, st));
-    NM_CUDA(cudaStreamSynchronize(st));
+    NM_CUDA(cudaMemcpyAsync(s.data(), s_dev, R * K * sizeof(double), cudaMemcpyDeviceToHost, st_));
+    NM_CUDA(cudaStreamSynchronize(st_));
     for (int k = 0; k < K; ++k)
       for (std::uint32_t r = rep_first[k]; r < rep_first[k + 1]; ++r) {
         const double v = s[static_cast<std::size_t>(r) * K + k];
         const double w = std::round(v);
         if (std::fabs(v - w) < 1e-3 && (w == 0.0 || w == 1.0)) rep_w[r] = w;
       }
+    return rep_w;
   }
-  lap("reps");
-  auto code = uninit(static_cast<std::uint32_t*>(nullptr), total);
-  lap("alloc");
-  parallel_k([&](int k) {
-    auto resolve = [&](std::int64_t v) -> std::int64_t {  // -> 0, 1 or kUnknown
-      if (v >= kRun) v = run_val[k][static_cast<std::size_t>(v - kRun)];
-      if (v >= kRep) {
-        const double w = rep_w[rep_first[k] + static_cast<std::size_t>(v - kRep)];
-        return w < 0.0 ? kUnknown : static_cast<std::int64_t>(w);
-      }
-      return v;
-    };
-    const nm::CellGrid& g = G[k];
-    const std::size_t nc = static_cast<std::size_t>(g.nx) * g.ny * g.nz;
-    for (std::size_t q = g.off; q < g.off + nc; ++q) {
-      if (!cert1[q]) {
-        code[q] = 3u + static_cast<std::uint32_t>(boff[k] + block_of[q]);
-      } else {
-        const std::int64_t w = resolve(run_val[k][run_of[q]]);
-        code[q] = w == kUnknown ? 0u : static_cast<std::uint32_t>(1 + w);
-      }
-    }
-    std::fill(child.get() + boff[k] * nm::kChildren, child.get() + boff[k + 1] * nm::kChildren, 0);
-    for (const FineRun& fr : fine[k]) {
-      const std::int64_t w = resolve(fr.v);
-      if (w == kUnknown) continue;
-      for (int f = fr.fx0; f <= fr.fx1; ++f) child_at(k, fr.row, f, fr.sy, fr.sz) = static_cast<std::uint8_t>(1 + w);
-    }
-  });
-  lap("codes");
-  up(c->cell_state, code.get(), total * sizeof(std::uint32_t));
-  up(c->cell_child, child.get(), nchild);
-  up(c->cell_grids, G.data(), G.size() * sizeof(nm::CellGrid));
-  NM_CUDA(cudaStreamSynchronize(st));
-  lap("final");
-  c->cells_total = total + nchild;
-  c->cells_certified = 0;
-  for (std::size_t q = 0; q < total; ++q) c->cells_certified += code[q] == 1 || code[q] == 2;
-  for (std::size_t q = 0; q < nchild; ++q) c->cells_certified += child[q] != 0;
-  c->cell_reps = R;
-  c->cells = true;
-  c->ms_cells = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+};
+
+void build_cells(nm_ctx* c, const double* xyz, const std::uint32_t* tri, const std::uint32_t* comp_off,
+                 const std::vector<float4>& hbox) {
+  CellBuild(c, xyz, tri, comp_off, hbox).run();
 }
 
 }  // namespace
