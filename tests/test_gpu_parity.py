@@ -662,3 +662,28 @@ def test_cell_culling_small_and_empty_compartments():
     resolved = (s_cell == 0.0) | (s_cell == 1.0)
     np.testing.assert_allclose(s_cell[resolved], s_ref[resolved], rtol=0, atol=1e-9)
     np.testing.assert_allclose(s_cell, s_ref, rtol=0, atol=S_EXPECT)
+
+
+def test_cell_culling_winding_number_two():
+    """A compartment made of two overlapping closed spheres: the winding
+    number is 2 in the overlap. Certified cells only accept winding numbers 0
+    and 1, so the overlap stays evaluated: masks equal the brute-force pass
+    and the oracle, s = 2 there."""
+    from paper_2203_10000_b200._native import Context
+    a = synth.icosphere(8.0, 3, center=(-3.0, 0.0, 0.0))
+    b = synth.icosphere(8.0, 3, center=(3.0, 0.0, 0.0))
+    two = (np.concatenate([a[0], b[0]]), np.concatenate([a[1], b[1] + np.uint32(a[0].shape[0])]))
+    S = synth.concat_surfaces([two, synth.icosphere(14.0, 3)])
+    rng = np.random.default_rng(9)
+    pts = rng.uniform(-15, 15, (150_000, 3))
+    with Context(0) as full, Context(0, cull_outside=2) as cell:
+        for c in (full, cell):
+            c.set_surfaces(S.xyz, S.tri, S.comp_off, S.label_ids)
+        m_full, _ = full.label_nodes(pts)
+        m_cell, _ = cell.label_nodes(pts)
+        probe = np.array([[0.0, 0.0, 0.0], [-9.0, 0.0, 0.0], [0.0, 0.0, 12.0]])
+        s_cell, _ = cell.enclosure(probe)
+    np.testing.assert_array_equal(m_cell, m_full)
+    _, s_ref = oracle.label_nodes(probe, S, want_s=True)
+    np.testing.assert_allclose(s_cell, s_ref, rtol=0, atol=S_EXPECT)
+    assert abs(s_cell[0, 0] - 2.0) < 1e-5 and abs(s_cell[1, 0] - 1.0) < 1e-5 and s_cell[2, 0] == 0.0
