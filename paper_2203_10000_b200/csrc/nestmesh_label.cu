@@ -910,6 +910,15 @@ class CellBuild {
   std::unique_ptr<std::int32_t[]> run_of_;
   std::vector<std::vector<FineRun>> fine_;
   std::size_t nreps_ = 0;
+  // host work items: z-slabs of kSlab planes of one compartment's grid (in
+  // compartment, then z order); every phase's results are merged in item
+  // order, so the numbering does not depend on the thread count
+  static constexpr int kSlab = 8;
+  struct Slab {
+    int k, z0, z1;
+  };
+  std::vector<Slab> slabs_;
+  std::vector<std::size_t> slab_first_;  // first slab of each compartment (K + 1)
 
   void lap(const char* what) {
     if (!verbose_) return;
@@ -1049,9 +1058,26 @@ class CellBuild {
     G_[k] = g;
   }
 
+  void make_slabs() {
+    slabs_.clear();
+    slab_first_.assign(K_ + 1, 0);
+    for (int k = 0; k < K_; ++k) {
+      slab_first_[k] = slabs_.size();
+      for (int z = 0; z < G_[k].nz; z += kSlab) slabs_.push_back({k, z, std::min(G_[k].nz, z + kSlab)});
+    }
+    slab_first_[K_] = slabs_.size();
+  }
+  std::size_t slab_begin(const Slab& sl) const {
+    return G_[sl.k].off + static_cast<std::size_t>(sl.z0) * G_[sl.k].ny * G_[sl.k].nx;
+  }
+  std::size_t slab_end(const Slab& sl) const {
+    return G_[sl.k].off + static_cast<std::size_t>(sl.z1) * G_[sl.k].ny * G_[sl.k].nx;
+  }
+
   // ---- certification: level-1 cells, then the children of uncertified cells ----
   void certify() {
     const int K = K_;
+    make_slabs();
     auto* cert_d = c_->cell_cert.as<std::uint8_t>(std::max<std::size_t>(total_, 1));
     for (int k = 0; k < K; ++k) {
       if (!cells(k)) continue;
@@ -1067,24 +1093,35 @@ class CellBuild {
     NM_CUDA(cudaStreamSynchronize(st_));
     lap("l1");
 
+    // child blocks: the uncertified cells in cell order (count per slab,
+    // prefix, fill per slab)
+    const std::size_t ns = slabs_.size();
+    std::vector<std::size_t> sl_cnt(ns + 1, 0);
+    parallel_for(static_cast<int>(ns), [&](int i) {
+      std::size_t m = 0;
+      for (std::size_t q = slab_begin(slabs_[i]); q < slab_end(slabs_[i]); ++q) m += !cert1_[q];
+      sl_cnt[i] = m;
+    });
+    std::vector<std::size_t> sl_off(ns + 1, 0);  // global first block of each slab
+    for (std::size_t i = 0; i < ns; ++i) sl_off[i + 1] = sl_off[i] + sl_cnt[i];
+    boff_.assign(K + 1, 0);
+    for (int k = 0; k <= K; ++k) boff_[k] = sl_off[slab_first_[k]];
+    const std::size_t nblk = boff_[K];
     block_of_ = uninit<std::uint32_t>(total_);
-    std::vector<std::vector<std::uint32_t>> blk_k(K);  // local cell index per local block
-    parallel_for(K, [&](int k) {
-      for (std::size_t q = 0; q < cells(k); ++q)
-        if (!cert1_[G_[k].off + q]) {
-          block_of_[G_[k].off + q] = static_cast<std::uint32_t>(blk_k[k].size());
-          blk_k[k].push_back(static_cast<std::uint32_t>(q));
+    std::vector<std::uint32_t> blk_cells(std::max<std::size_t>(nblk, 1));
+    parallel_for(static_cast<int>(ns), [&](int i) {
+      const Slab& sl = slabs_[i];
+      std::size_t b = sl_off[i];
+      for (std::size_t q = slab_begin(sl); q < slab_end(sl); ++q)
+        if (!cert1_[q]) {
+          block_of_[q] = static_cast<std::uint32_t>(b - boff_[sl.k]);  // local to the compartment
+          blk_cells[b++] = static_cast<std::uint32_t>(q - G_[sl.k].off);
         }
     });
-    boff_.assign(K + 1, 0);
-    for (int k = 0; k < K; ++k) boff_[k + 1] = boff_[k] + blk_k[k].size();
     lap("blocks");
-    const std::size_t nblk = boff_[K];
     nchild_ = nblk * nm::kChildren;
     child_ = uninit<std::uint8_t>(nchild_);
     if (!nblk) return;
-    std::vector<std::uint32_t> blk_cells(nblk);
-    for (int k = 0; k < K; ++k) std::copy(blk_k[k].begin(), blk_k[k].end(), blk_cells.begin() + boff_[k]);
     up(c_->cell_blk, blk_cells.data(), nblk * sizeof(std::uint32_t));
     auto* ch_d = c_->cell_child.as<std::uint8_t>(nchild_);
     for (int k = 0; k < K; ++k) {
@@ -1106,24 +1143,64 @@ class CellBuild {
   }
 
   // ---- runs: every maximal x-run of certified cells gets one winding number ----
+  // per-slab results, merged per compartment in slab order
+  struct SlabRuns {
+    std::vector<double> reps;
+    std::vector<std::int64_t> run_val;
+    std::vector<FineRun> fine;
+  };
+
   void runs() {
+    const std::size_t ns = slabs_.size();
+    std::vector<SlabRuns> part(ns);
+    run_of_ = uninit<std::int32_t>(total_);
+    parallel_for(static_cast<int>(ns), [&](int i) { slab_runs(slabs_[i], part[i]); });
+    // merge: slab-local run / representative indices -> compartment-local
+    std::vector<std::size_t> run_base(ns), rep_base(ns);
+    for (int k = 0; k < K_; ++k) {
+      std::size_t nr = 0, np = 0;
+      for (std::size_t i = slab_first_[k]; i < slab_first_[k + 1]; ++i) {
+        run_base[i] = nr;
+        rep_base[i] = np;
+        nr += part[i].run_val.size();
+        np += part[i].reps.size() / 3;
+      }
+    }
+    auto rebase = [&](std::int64_t v, std::size_t i) -> std::int64_t {
+      if (v >= kRun) return v + static_cast<std::int64_t>(run_base[i]);
+      if (v >= kRep) return v + static_cast<std::int64_t>(rep_base[i]);
+      return v;
+    };
+    parallel_for(static_cast<int>(ns), [&](int i) {
+      const Slab& sl = slabs_[i];
+      for (std::size_t q = slab_begin(sl); q < slab_end(sl); ++q)
+        if (cert1_[q]) run_of_[q] += static_cast<std::int32_t>(run_base[i]);
+      for (std::int64_t& v : part[i].run_val) v = rebase(v, i);
+      for (FineRun& fr : part[i].fine) fr.v = rebase(fr.v, i);
+    });
     reps_.assign(K_, {});
     run_val_.assign(K_, {});
     fine_.assign(K_, {});
-    run_of_ = uninit<std::int32_t>(total_);
-    parallel_for(K_, [&](int k) { compartment_runs(k); });
+    parallel_for(K_, [&](int k) {
+      for (std::size_t i = slab_first_[k]; i < slab_first_[k + 1]; ++i) {
+        reps_[k].insert(reps_[k].end(), part[i].reps.begin(), part[i].reps.end());
+        run_val_[k].insert(run_val_[k].end(), part[i].run_val.begin(), part[i].run_val.end());
+        fine_[k].insert(fine_[k].end(), part[i].fine.begin(), part[i].fine.end());
+      }
+    });
     lap("runs");
   }
 
-  std::int64_t new_rep(int k, double x, double y, double z) {
-    const std::int64_t v = kRep + static_cast<std::int64_t>(reps_[k].size() / 3);
-    reps_[k].insert(reps_[k].end(), {x + ctr_[0], y + ctr_[1], z + ctr_[2]});
+  std::int64_t new_rep(SlabRuns& out, double x, double y, double z) {
+    const std::int64_t v = kRep + static_cast<std::int64_t>(out.reps.size() / 3);
+    out.reps.insert(out.reps.end(), {x + ctr_[0], y + ctr_[1], z + ctr_[2]});
     return v;
   }
 
-  void compartment_runs(int k) {
+  void slab_runs(const Slab& sl, SlabRuns& out) {
+    const int k = sl.k;
     const nm::CellGrid& g = G_[k];
-    for (int iz = 0; iz < g.nz; ++iz)
+    for (int iz = sl.z0; iz < sl.z1; ++iz)
       for (int iy = 0; iy < g.ny; ++iy) {
         const std::size_t row = g.off + (static_cast<std::size_t>(iz) * g.ny + iy) * g.nx;
         const double y = g.oy + (iy + 0.5) * g.B, z = g.oz + (iz + 0.5) * g.B;
@@ -1138,17 +1215,18 @@ class CellBuild {
                 outside_dop(k, g.ox + (jx + 0.5) * g.B, y, z))
               v = 0;
             else
-              v = new_rep(k, g.ox + ((ix + jx) / 2 + 0.5) * g.B, y, z);
-            for (int q = ix; q <= jx; ++q) run_of_[row + q] = static_cast<std::int32_t>(run_val_[k].size());
-            run_val_[k].push_back(v);
+              v = new_rep(out, g.ox + ((ix + jx) / 2 + 0.5) * g.B, y, z);
+            for (int q = ix; q <= jx; ++q) run_of_[row + q] = static_cast<std::int32_t>(out.run_val.size());
+            out.run_val.push_back(v);
           } else {
-            segment_runs(k, g, row, ix, jx, iy, iz);
+            segment_runs(out, k, g, row, ix, jx, iy, iz);
           }
           ix = jx + 1;
         }
       }
-    // neighbour references: the level-1 runs of every row exist now
-    for (FineRun& fr : fine_[k]) {
+    // neighbour references: the level-1 runs of the slab's rows exist now
+    // (slab-local indices, rebased with the slab's runs)
+    for (FineRun& fr : out.fine) {
       if (fr.v == kLeft) fr.v = kRun + run_of_[fr.row + fr.fx0 / S - 1];
       else if (fr.v == kRight) fr.v = kRun + run_of_[fr.row + fr.fx1 / S + 1];
     }
@@ -1157,7 +1235,7 @@ class CellBuild {
   // segment [ix, jx] of uncertified level-1 cells: runs of certified children
   // per (sy, sz) sub-row; a run reaching the segment's end continues into the
   // certified neighbour parent (or the grid edge)
-  void segment_runs(int k, const nm::CellGrid& g, std::size_t row, int ix, int jx, int iy, int iz) {
+  void segment_runs(SlabRuns& out, int k, const nm::CellGrid& g, std::size_t row, int ix, int jx, int iy, int iz) {
     const double b = g.B / S;
     const int f_lo = S * ix, f_hi = S * jx + S - 1;
     for (int sz = 0; sz < S; ++sz)
@@ -1179,9 +1257,9 @@ class CellBuild {
             if (outside_dop(k, g.ox + (f + 0.5) * b, yy, zz) || outside_dop(k, g.ox + (e + 0.5) * b, yy, zz))
               v = 0;
             else
-              v = new_rep(k, g.ox + ((f + e) / 2 + 0.5) * b, yy, zz);
+              v = new_rep(out, g.ox + ((f + e) / 2 + 0.5) * b, yy, zz);
           }
-          fine_[k].push_back({row, f, e, sy, sz, v});
+          out.fine.push_back({row, f, e, sy, sz, v});
           f = e + 1;
         }
   }
@@ -1201,27 +1279,31 @@ class CellBuild {
     const std::vector<double> rep_w = evaluate_reps(rep_all, rep_cnt, rep_first);
     lap("reps");
     auto code = uninit<std::uint32_t>(total_);
-    parallel_for(K, [&](int k) {
-      auto value = [&](std::int64_t v) -> std::int64_t {  // -> 0, 1 or kUnknown
-        if (v >= kRun) v = run_val_[k][static_cast<std::size_t>(v - kRun)];
-        if (v >= kRep) {
-          const double w = rep_w[rep_first[k] + static_cast<std::size_t>(v - kRep)];
-          return w < 0.0 ? kUnknown : static_cast<std::int64_t>(w);
-        }
-        return v;
-      };
-      const nm::CellGrid& g = G_[k];
-      for (std::size_t q = g.off; q < g.off + cells(k); ++q) {
+    auto value = [&](int k, std::int64_t v) -> std::int64_t {  // -> 0, 1 or kUnknown
+      if (v >= kRun) v = run_val_[k][static_cast<std::size_t>(v - kRun)];
+      if (v >= kRep) {
+        const double w = rep_w[rep_first[k] + static_cast<std::size_t>(v - kRep)];
+        return w < 0.0 ? kUnknown : static_cast<std::int64_t>(w);
+      }
+      return v;
+    };
+    parallel_for(static_cast<int>(slabs_.size()), [&](int i) {
+      const Slab& sl = slabs_[i];
+      const int k = sl.k;
+      for (std::size_t q = slab_begin(sl); q < slab_end(sl); ++q) {
         if (!cert1_[q]) {
           code[q] = 3u + static_cast<std::uint32_t>(boff_[k] + block_of_[q]);
+          std::fill(child_.get() + (boff_[k] + block_of_[q]) * nm::kChildren,
+                    child_.get() + (boff_[k] + block_of_[q] + 1) * nm::kChildren, 0);
         } else {
-          const std::int64_t w = value(run_val_[k][run_of_[q]]);
+          const std::int64_t w = value(k, run_val_[k][run_of_[q]]);
           code[q] = w == kUnknown ? 0u : static_cast<std::uint32_t>(1 + w);
         }
       }
-      std::fill(child_.get() + boff_[k] * nm::kChildren, child_.get() + boff_[k + 1] * nm::kChildren, 0);
+    });
+    parallel_for(K, [&](int k) {  // fine runs write children of their own compartment only
       for (const FineRun& fr : fine_[k]) {
-        const std::int64_t w = value(fr.v);
+        const std::int64_t w = value(k, fr.v);
         if (w == kUnknown) continue;
         for (int f = fr.fx0; f <= fr.fx1; ++f) child_at(k, fr.row, f, fr.sy, fr.sz) = static_cast<std::uint8_t>(1 + w);
       }
