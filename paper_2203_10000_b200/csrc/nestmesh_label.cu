@@ -859,18 +859,22 @@ std::pair<std::size_t, std::size_t> refine_dev(nm_ctx* c, const double* d_nodes,
 // blocks, runs and representatives are independent.
 class CellBuild {
  public:
+  // c->K, the centring frame, xyz64 / tri_idx on the device and hbox must be
+  // set; prepare() may run on a host thread beside the tile packing (it uses
+  // its own stream); finish() needs the tiles (representatives run k_label).
   CellBuild(nm_ctx* c, const double* xyz, const std::uint32_t* tri, const std::uint32_t* comp_off,
-            const std::vector<float4>& hbox)
+            const std::vector<float4>& hbox, cudaStream_t st)
       : c_(c), xyz_(xyz), tri_(tri), comp_off_(comp_off), hbox_(hbox), K_(c->K), ctr_{c->cx, c->cy, c->cz},
-        st_(c->stream), t0_(std::chrono::steady_clock::now()), tl_(t0_),
+        st_(st), t0_(std::chrono::steady_clock::now()), tl_(t0_),
         verbose_(std::getenv("NM_CELL_VERBOSE") != nullptr) {}
 
-  void run() {
+  void prepare() {
+    NM_CUDA(cudaSetDevice(c_->opt.device));
     geometry();
     certify();
     runs();
-    resolve();
   }
+  void finish() { resolve(); }
 
  private:
   // run value of a level-1 or child run: 0 / 1 known; kRep + r: the
@@ -1375,10 +1379,6 @@ class CellBuild {
   }
 };
 
-void build_cells(nm_ctx* c, const double* xyz, const std::uint32_t* tri, const std::uint32_t* comp_off,
-                 const std::vector<float4>& hbox) {
-  CellBuild(c, xyz, tri, comp_off, hbox).run();
-}
 
 }  // namespace
 
@@ -1478,6 +1478,65 @@ int nm_set_surfaces(nm_ctx* c, const double* xyz, std::size_t nv, const std::uin
     c->cx = ctr[0];
     c->cy = ctr[1];
     c->cz = ctr[2];
+
+    c->has_surfaces = false;
+    c->cells = false;
+    c->K = K;
+    // fp64 originals (fix-up, cell certification) and the 13-DOP of every
+    // compartment first: the certified-cell build (cull_outside = 2) starts on
+    // its own host thread and stream while the tiles are packed below.
+    auto up_on = [&](DBuf& b, const void* src, std::size_t bytes, cudaStream_t st) {
+      void* d = b.get(bytes);
+      if (bytes) NM_CUDA(cudaMemcpyAsync(d, src, bytes, cudaMemcpyHostToDevice, st));
+    };
+    up_on(c->xyz64, xyz, nv * 3 * sizeof(double), c->side);
+    up_on(c->tri_idx, tri, nt * 3 * sizeof(std::uint32_t), c->side);
+    up_on(c->comp_off, comp_off, (K + 1) * sizeof(std::uint32_t), c->side);
+    // 13-DOP: slab bounds over the vertices (centred frame), widened by 1e-3 mm
+    // + 1e-5 |bound| (covers the fp32 rounding of the point and of the
+    // projection in the kernel) and rounded outward.
+    std::vector<float4> hbox(static_cast<std::size_t>(K) * nm::kDopF4);
+    parallel_for(K, [&](int k) {
+      float* dst = reinterpret_cast<float*>(&hbox[static_cast<std::size_t>(k) * nm::kDopF4]);
+      for (int q = 0; q < 4 * nm::kDopF4; ++q) dst[q] = 0.0f;
+      for (int j = 0; j < nm::kDopDirs; ++j) {
+        double lo = 1e300, hi = -1e300;
+        for (std::uint32_t t = comp_off[k]; t < comp_off[k + 1]; ++t)
+          for (int v = 0; v < 3; ++v) {
+            const double* X = xyz + 3 * std::size_t(tri[3 * t + v]);
+            double pr = 0.0;
+            for (int a = 0; a < 3; ++a) pr += double(nm::dop_dir(j, a)) * (X[a] - ctr[a]);
+            lo = std::min(lo, pr);
+            hi = std::max(hi, pr);
+          }
+        if (comp_off[k + 1] == comp_off[k]) {  // empty compartment: everything outside
+          dst[2 * j] = 1e30f;
+          dst[2 * j + 1] = -1e30f;
+          continue;
+        }
+        const double m = 1e-3 + 1e-5 * std::max(std::fabs(lo), std::fabs(hi));
+        dst[2 * j] = std::nextafter(float(lo - m), -INFINITY);
+        dst[2 * j + 1] = std::nextafter(float(hi + m), INFINITY);
+      }
+    });
+    std::unique_ptr<CellBuild> cells;
+    std::exception_ptr cells_err;
+    struct Joiner {
+      std::thread t;
+      ~Joiner() {
+        if (t.joinable()) t.join();
+      }
+    } cells_thread;
+    if (c->opt.cull_outside == 2) {
+      cells = std::make_unique<CellBuild>(c, xyz, tri, comp_off, hbox, c->side);
+      cells_thread.t = std::thread([&] {
+        try {
+          cells->prepare();
+        } catch (...) {
+          cells_err = std::current_exception();
+        }
+      });
+    }
 
     auto morton = [&](const double* m) {
       std::uint32_t q[3];
@@ -1735,50 +1794,17 @@ int nm_set_surfaces(nm_ctx* c, const double* xyz, std::size_t nv, const std::uin
       }
     });
     c->strips = use_strips;
-    c->has_surfaces = false;
-    auto up = [&](DBuf& b, const void* src, std::size_t bytes) {
-      void* d = b.get(bytes);
-      if (bytes) NM_CUDA(cudaMemcpyAsync(d, src, bytes, cudaMemcpyHostToDevice, c->stream));
-    };
+    auto up = [&](DBuf& b, const void* src, std::size_t bytes) { up_on(b, src, bytes, c->stream); };
     up(c->tri, htri.data(), htri.size() * sizeof(float4));
     up(c->sub, hsub.data(), hsub.size() * sizeof(float4));
     up(c->edges, hedge.data(), hedge.size() * sizeof(float4));
     up(c->cont, hcont.data(), hcont.size() * sizeof(std::uint32_t));
     up(c->comp_tiles, tiles.data(), tiles.size() * sizeof(std::uint32_t));
-    up(c->xyz64, xyz, nv * 3 * sizeof(double));
-    up(c->tri_idx, tri, nt * 3 * sizeof(std::uint32_t));
-    up(c->comp_off, comp_off, (K + 1) * sizeof(std::uint32_t));
-    // 13-DOP of every compartment for exact outside culling (centred frame):
-    // slab bounds over the vertices, widened by 1e-3 mm + 1e-5 |bound| (covers
-    // the fp32 rounding of the point and of the projection in the kernel) and
-    // rounded outward.
-    std::vector<float4> hbox(static_cast<std::size_t>(K) * nm::kDopF4);
-    parallel_for(K, [&](int k) {
-      float* dst = reinterpret_cast<float*>(&hbox[static_cast<std::size_t>(k) * nm::kDopF4]);
-      for (int q = 0; q < 4 * nm::kDopF4; ++q) dst[q] = 0.0f;
-      for (int j = 0; j < nm::kDopDirs; ++j) {
-        double lo = 1e300, hi = -1e300;
-        for (std::uint32_t t = comp_off[k]; t < comp_off[k + 1]; ++t)
-          for (int v = 0; v < 3; ++v) {
-            const double* X = xyz + 3 * std::size_t(tri[3 * t + v]);
-            double pr = 0.0;
-            for (int a = 0; a < 3; ++a) pr += double(nm::dop_dir(j, a)) * (X[a] - ctr[a]);
-            lo = std::min(lo, pr);
-            hi = std::max(hi, pr);
-          }
-        if (comp_off[k + 1] == comp_off[k]) {  // empty compartment: everything outside
-          dst[2 * j] = 1e30f;
-          dst[2 * j + 1] = -1e30f;
-          continue;
-        }
-        const double m = 1e-3 + 1e-5 * std::max(std::fabs(lo), std::fabs(hi));
-        dst[2 * j] = std::nextafter(float(lo - m), -INFINITY);
-        dst[2 * j + 1] = std::nextafter(float(hi + m), INFINITY);
-      }
-    });
     up(c->comp_box, hbox.data(), hbox.size() * sizeof(float4));
     NM_CUDA(cudaStreamSynchronize(c->stream));
-    c->K = K;
+    if (cells_thread.t.joinable()) cells_thread.t.join();
+    if (cells_err) std::rethrow_exception(cells_err);
+    NM_CUDA(cudaStreamSynchronize(c->side));
     c->comp_tiles_h = tiles;
     c->n_continued = 0;
     for (std::uint32_t w : hcont) c->n_continued += static_cast<std::size_t>(__builtin_popcount(w));
@@ -1787,9 +1813,8 @@ int nm_set_surfaces(nm_ctx* c, const double* xyz, std::size_t nv, const std::uin
     c->nv = nv;
     for (int k = 0; k < 32; ++k) c->ids.id[k] = k < K ? label_ids[k] : 0;
     c->comp_off_h.assign(comp_off, comp_off + K + 1);
-    c->cells = false;
     c->has_surfaces = true;
-    if (c->opt.cull_outside == 2) build_cells(c, xyz, tri, comp_off, hbox);
+    if (cells) cells->finish();  // representatives need the tiles: after the packing
   });
 }
 
