@@ -43,13 +43,35 @@ def _stale(out: Path, deps) -> bool:
     return any(Path(d).stat().st_mtime > t for d in deps)
 
 
+def LABEL_SOURCES():
+    """CUDA translation units of libnestmesh_label.so (context.cuh is shared)."""
+    return [str(CSRC / f) for f in ("nestmesh_label.cu", "cell_build.cu", "group.cu", "mesh_ops.cu")]
+
+
+def compile_label_lib(out: Path, defs=(), log=None):
+    """Compile the translation units in parallel (one nvcc per source), then link."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    objdir = out.parent / f".obj_{out.stem}"
+    objdir.mkdir(parents=True, exist_ok=True)
+    cflags = [f for f in NVCC_FLAGS if f != "-shared"] + [f"-D{d}" for d in defs]
+    srcs = LABEL_SOURCES() + [str(CSRC / "refine.cpp")]
+    objs = [objdir / (Path(s).stem + ".o") for s in srcs]
+    with ThreadPoolExecutor(len(srcs)) as ex:
+        rs = list(ex.map(lambda so: _run([NVCC, *ARCH, *cflags, "-c", so[0], "-o", str(so[1])]), zip(srcs, objs)))
+    _run([NVCC, *ARCH, "-shared", *map(str, objs), "-o", str(out)])
+    text = "".join(r.stdout + r.stderr for r in rs)
+    if log is not None:
+        log.write_text(text)
+    return text
+
+
 def build_label_lib(force=False) -> Path:
     LIB.mkdir(exist_ok=True)
     out = LIB / "libnestmesh_label.so"
     deps = list(CSRC.glob("*.cu")) + list(CSRC.glob("*.cuh")) + [CSRC / "refine.cpp", ROOT / "include" / "nestmesh_label.h"]
     if force or _stale(out, deps):
-        _run([NVCC, *ARCH, *NVCC_FLAGS, str(CSRC / "nestmesh_label.cu"), str(CSRC / "refine.cpp"), "-o", str(out)],
-             log=LIB / "ptxas_label.log")
+        compile_label_lib(out, log=LIB / "ptxas_label.log")
     return out
 
 

@@ -1,0 +1,545 @@
+// Certified cells (cells.cuh): the per-surface-set build
+// behind nm_options.cull_outside = 2.
+#include "context.cuh"
+
+namespace nmh {
+
+#ifndef NM_CELL_AXIS
+#define NM_CELL_AXIS 120
+#endif
+// Certified cells of every compartment (cells.cuh), built once per surface
+// set from the surfaces alone, in four phases: geometry (grids + clusters),
+// certification (level-1 cells and children, on the device), runs (x-runs of
+// certified cells -> winding number, neighbour run or representative) and
+// resolve (representatives evaluated by the sparse k_label, final codes).
+// Host loops run one compartment per thread: every compartment's grid,
+// blocks, runs and representatives are independent.
+class CellBuild : public CellBuilder {
+ public:
+  // c->K, the centring frame, xyz64 / tri_idx on the device and hbox must be
+  // set; prepare() may run on a host thread beside the tile packing (it uses
+  // its own stream); finish() needs the tiles (representatives run k_label).
+  CellBuild(nm_ctx* c, const double* xyz, const std::uint32_t* tri, const std::uint32_t* comp_off,
+            const std::vector<float4>& hbox, cudaStream_t st)
+      : c_(c), xyz_(xyz), tri_(tri), comp_off_(comp_off), hbox_(hbox), K_(c->K), ctr_{c->cx, c->cy, c->cz},
+        st_(st), t0_(std::chrono::steady_clock::now()), tl_(t0_),
+        verbose_(std::getenv("NM_CELL_VERBOSE") != nullptr) {}
+
+  void prepare() override {
+    NM_CUDA(cudaSetDevice(c_->opt.device));
+    geometry();
+    certify();
+    runs();
+  }
+  void finish() override { resolve(); }
+
+ private:
+  // run value of a level-1 or child run: 0 / 1 known; kRep + r: the
+  // compartment's local representative r; kRun + q: the value of the
+  // compartment's level-1 run q; kLeft / kRight: the neighbour parent's run
+  // (resolved once the row is scanned)
+  static constexpr std::int64_t kUnknown = -1, kLeft = -2, kRight = -3, kRep = 1ll << 40, kRun = 1ll << 41;
+  static constexpr int S = nm::kSubCells;
+  struct FineRun {
+    std::size_t row;  // level-1 row base (global cell index of ix = 0)
+    int fx0, fx1;     // fine x range (fine index = 4 ix + sx)
+    int sy, sz;
+    std::int64_t v;
+  };
+
+  nm_ctx* c_;
+  const double* xyz_;
+  const std::uint32_t* tri_;
+  const std::uint32_t* comp_off_;
+  const std::vector<float4>& hbox_;
+  const int K_;
+  const double ctr_[3];
+  cudaStream_t st_;
+  std::chrono::steady_clock::time_point t0_, tl_;
+  bool verbose_;
+
+  std::vector<nm::CellGrid> G_;
+  std::vector<std::size_t> coff_;       // first cluster of each compartment
+  std::size_t total_ = 0;               // level-1 cells
+  std::unique_ptr<std::uint8_t[]> cert1_;
+  std::unique_ptr<std::uint32_t[]> block_of_;  // local child block of each uncertified cell
+  std::vector<std::size_t> boff_;       // first child block of each compartment
+  std::size_t nchild_ = 0;
+  std::unique_ptr<std::uint8_t[]> child_;
+  std::vector<std::vector<double>> reps_;
+  std::vector<std::vector<std::int64_t>> run_val_;
+  std::unique_ptr<std::int32_t[]> run_of_;
+  std::vector<std::vector<FineRun>> fine_;
+  std::size_t nreps_ = 0;
+  // host work items: z-slabs of kSlab planes of one compartment's grid (in
+  // compartment, then z order); every phase's results are merged in item
+  // order, so the numbering does not depend on the thread count
+  static constexpr int kSlab = 8;
+  struct Slab {
+    int k, z0, z1;
+  };
+  std::vector<Slab> slabs_;
+  std::vector<std::size_t> slab_first_;  // first slab of each compartment (K + 1)
+
+  void lap(const char* what) {
+    if (!verbose_) return;
+    const auto t = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[cells] %-6s %8.1f ms\n", what, std::chrono::duration<double, std::milli>(t - tl_).count());
+    tl_ = t;
+  }
+  // host arrays allocated uninitialised: every entry is written (by a copy or
+  // by its compartment's thread) before it is read
+  template <class T>
+  static std::unique_ptr<T[]> uninit(std::size_t m) {
+    return std::unique_ptr<T[]>(new T[std::max<std::size_t>(m, 1)]);
+  }
+  void up(DBuf& b, const void* src, std::size_t bytes) {
+    void* d = b.get(std::max<std::size_t>(bytes, 1));
+    if (bytes) NM_CUDA(cudaMemcpyAsync(d, src, bytes, cudaMemcpyHostToDevice, st_));
+  }
+  std::size_t cells(int k) const { return static_cast<std::size_t>(G_[k].nx) * G_[k].ny * G_[k].nz; }
+  const float4* clus_k(int k) const { return static_cast<const float4*>(c_->clus.p) + coff_[k]; }
+  const std::uint32_t* ctri_k(int k) const {
+    return static_cast<const std::uint32_t*>(c_->clus_tri.p) + coff_[k] * nm::kCluster;
+  }
+  const float4* tsph_k(int k) const { return static_cast<const float4*>(c_->clus_tsph.p) + coff_[k] * nm::kCluster; }
+  int nclus(int k) const { return static_cast<int>(coff_[k + 1] - coff_[k]); }
+  bool outside_dop(int k, double x, double y, double z) const {
+    const float* dop = reinterpret_cast<const float*>(&hbox_[static_cast<std::size_t>(k) * nm::kDopF4]);
+    const float xf = float(x), yf = float(y), zf = float(z);
+    for (int d = 0; d < nm::kDopDirs; ++d) {
+      const float pr = nm::dop_dir(d, 0) * xf + nm::dop_dir(d, 1) * yf + nm::dop_dir(d, 2) * zf;
+      if (pr < dop[2 * d] || pr > dop[2 * d + 1]) return true;
+    }
+    return false;
+  }
+  std::uint8_t& child_at(int k, std::size_t row, int fx, int sy, int sz) {
+    const std::size_t b = boff_[k] + block_of_[row + fx / S];
+    return child_[b * nm::kChildren + (sz * S + sy) * S + fx % S];
+  }
+
+  // ---- geometry: per compartment its grid and Morton-ordered clusters ----
+  void geometry() {
+    const int K = K_;
+    G_.assign(K, nm::CellGrid{});
+    coff_.assign(K + 1, 0);
+    std::vector<std::vector<float4>> clus_kv(K), tsph_kv(K);
+    std::vector<std::vector<std::uint32_t>> ctri_kv(K);
+    parallel_for(K, [&](int k) { compartment_geometry(k, clus_kv[k], ctri_kv[k], tsph_kv[k]); });
+    std::vector<float4> clus, tsph;
+    std::vector<std::uint32_t> ctri;
+    for (int k = 0; k < K; ++k) {
+      G_[k].off = static_cast<std::uint32_t>(total_);
+      total_ += cells(k);
+      if (total_ > 0xffffffffull) throw Error("certified-cell grids exceed 2^32 cells");
+      coff_[k] = clus.size();
+      clus.insert(clus.end(), clus_kv[k].begin(), clus_kv[k].end());
+      ctri.insert(ctri.end(), ctri_kv[k].begin(), ctri_kv[k].end());
+      tsph.insert(tsph.end(), tsph_kv[k].begin(), tsph_kv[k].end());
+    }
+    coff_[K] = clus.size();
+    lap("setup");
+    up(c_->clus, clus.data(), clus.size() * sizeof(float4));
+    up(c_->clus_tri, ctri.data(), ctri.size() * sizeof(std::uint32_t));
+    up(c_->clus_tsph, tsph.data(), tsph.size() * sizeof(float4));
+  }
+
+  void compartment_geometry(int k, std::vector<float4>& clus, std::vector<std::uint32_t>& ctri,
+                            std::vector<float4>& tsph) {
+    const double* ctr = ctr_;
+    const double* xyz = xyz_;
+    const std::uint32_t* tri = tri_;
+    const std::uint32_t b = comp_off_[k], e = comp_off_[k + 1];
+    nm::CellGrid g{0.0, 0.0, 0.0, 1.0, 0, 0, 0, 0u};
+    if (e > b) {
+      double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
+      std::vector<std::pair<std::uint32_t, std::uint32_t>> kk;
+      kk.reserve(e - b);
+      for (std::uint32_t t = b; t < e; ++t) {
+        double m[3] = {0, 0, 0};
+        for (int v = 0; v < 3; ++v)
+          for (int a = 0; a < 3; ++a) {
+            const double x = xyz[3 * std::size_t(tri[3 * t + v]) + a] - ctr[a];
+            lo[a] = std::min(lo[a], x);
+            hi[a] = std::max(hi[a], x);
+            m[a] += x / 3.0;
+          }
+        std::uint32_t q[3];
+        for (int a = 0; a < 3; ++a)
+          q[a] = static_cast<std::uint32_t>(std::clamp((m[a] + ctr[a] - c_->lo[a]) / c_->span * 1024.0, 0.0, 1023.0));
+        kk.emplace_back(spread10h(q[0]) | (spread10h(q[1]) << 1) | (spread10h(q[2]) << 2), t);
+      }
+      std::stable_sort(kk.begin(), kk.end(), [](auto& x, auto& y) { return x.first < y.first; });
+      // bounding sphere of triangles kk[i0, i1) in the centred frame: fp32
+      // centre of the vertex box, radius rounded up with the kernel's
+      // margins (1e-6 relative + 1e-5 mm + 4e-6 |centre|)
+      auto sphere = [&](std::size_t i0, std::size_t i1) {
+        double blo[3] = {1e300, 1e300, 1e300}, bhi[3] = {-1e300, -1e300, -1e300};
+        for (std::size_t i = i0; i < i1; ++i)
+          for (int v = 0; v < 3; ++v)
+            for (int a = 0; a < 3; ++a) {
+              const double x = xyz[3 * std::size_t(tri[3 * kk[i].second + v]) + a] - ctr[a];
+              blo[a] = std::min(blo[a], x);
+              bhi[a] = std::max(bhi[a], x);
+            }
+        const float fc[3] = {float(0.5 * (blo[0] + bhi[0])), float(0.5 * (blo[1] + bhi[1])),
+                             float(0.5 * (blo[2] + bhi[2]))};
+        double rho = 0.0;
+        for (std::size_t i = i0; i < i1; ++i)
+          for (int v = 0; v < 3; ++v) {
+            double d2 = 0.0;
+            for (int a = 0; a < 3; ++a) {
+              const double d = xyz[3 * std::size_t(tri[3 * kk[i].second + v]) + a] - ctr[a] - double(fc[a]);
+              d2 += d * d;
+            }
+            rho = std::max(rho, std::sqrt(d2));
+          }
+        const double rel = 4e-6 * (std::fabs(fc[0]) + std::fabs(fc[1]) + std::fabs(fc[2]));
+        return make_float4(fc[0], fc[1], fc[2], std::nextafter(float(rho * (1.0 + 1e-6) + 1e-5 + rel), INFINITY));
+      };
+      for (std::size_t i0 = 0; i0 < kk.size(); i0 += nm::kCluster) {
+        const std::size_t i1 = std::min(kk.size(), i0 + nm::kCluster);
+        clus.push_back(sphere(i0, i1));
+        for (std::size_t i = i0; i < i0 + nm::kCluster; ++i) {
+          ctri.push_back(i < i1 ? kk[i].second : 0xffffffffu);
+          tsph.push_back(i < i1 ? sphere(i, i + 1) : make_float4(0.f, 0.f, 0.f, -1e30f));
+        }
+      }
+      const double ext = std::max({hi[0] - lo[0], hi[1] - lo[1], hi[2] - lo[2]});
+      g.B = std::max(ext / NM_CELL_AXIS, 1e-3);
+      int n3[3];
+      for (int a = 0; a < 3; ++a) n3[a] = static_cast<int>(std::ceil((hi[a] - lo[a]) / g.B)) + 2;
+      g.ox = lo[0] - g.B;
+      g.oy = lo[1] - g.B;
+      g.oz = lo[2] - g.B;
+      g.nx = n3[0];
+      g.ny = n3[1];
+      g.nz = n3[2];
+    }
+    G_[k] = g;
+  }
+
+  void make_slabs() {
+    slabs_.clear();
+    slab_first_.assign(K_ + 1, 0);
+    for (int k = 0; k < K_; ++k) {
+      slab_first_[k] = slabs_.size();
+      for (int z = 0; z < G_[k].nz; z += kSlab) slabs_.push_back({k, z, std::min(G_[k].nz, z + kSlab)});
+    }
+    slab_first_[K_] = slabs_.size();
+  }
+  std::size_t slab_begin(const Slab& sl) const {
+    return G_[sl.k].off + static_cast<std::size_t>(sl.z0) * G_[sl.k].ny * G_[sl.k].nx;
+  }
+  std::size_t slab_end(const Slab& sl) const {
+    return G_[sl.k].off + static_cast<std::size_t>(sl.z1) * G_[sl.k].ny * G_[sl.k].nx;
+  }
+
+  // ---- certification: level-1 cells, then the children of uncertified cells ----
+  void certify() {
+    const int K = K_;
+    make_slabs();
+    auto* cert_d = c_->cell_cert.as<std::uint8_t>(std::max<std::size_t>(total_, 1));
+    for (int k = 0; k < K; ++k) {
+      if (!cells(k)) continue;
+      const std::size_t nbrick =
+          static_cast<std::size_t>((G_[k].nx + 3) / 4) * ((G_[k].ny + 3) / 4) * ((G_[k].nz + 1) / 2);
+      nm::k_cell_certify<<<static_cast<unsigned>((nbrick * 32 + 255) / 256), 256, 0, st_>>>(
+          G_[k], clus_k(k), nclus(k), ctri_k(k), tsph_k(k), static_cast<const double*>(c_->xyz64.p),
+          static_cast<const std::uint32_t*>(c_->tri_idx.p), c_->cx, c_->cy, c_->cz, cert_d);
+    }
+    NM_CUDA(cudaGetLastError());
+    cert1_ = uninit<std::uint8_t>(total_);
+    if (total_) NM_CUDA(cudaMemcpyAsync(cert1_.get(), cert_d, total_, cudaMemcpyDeviceToHost, st_));
+    NM_CUDA(cudaStreamSynchronize(st_));
+    lap("l1");
+
+    // child blocks: the uncertified cells in cell order (count per slab,
+    // prefix, fill per slab)
+    const std::size_t ns = slabs_.size();
+    std::vector<std::size_t> sl_cnt(ns + 1, 0);
+    parallel_for(static_cast<int>(ns), [&](int i) {
+      std::size_t m = 0;
+      for (std::size_t q = slab_begin(slabs_[i]); q < slab_end(slabs_[i]); ++q) m += !cert1_[q];
+      sl_cnt[i] = m;
+    });
+    std::vector<std::size_t> sl_off(ns + 1, 0);  // global first block of each slab
+    for (std::size_t i = 0; i < ns; ++i) sl_off[i + 1] = sl_off[i] + sl_cnt[i];
+    boff_.assign(K + 1, 0);
+    for (int k = 0; k <= K; ++k) boff_[k] = sl_off[slab_first_[k]];
+    const std::size_t nblk = boff_[K];
+    block_of_ = uninit<std::uint32_t>(total_);
+    std::vector<std::uint32_t> blk_cells(std::max<std::size_t>(nblk, 1));
+    parallel_for(static_cast<int>(ns), [&](int i) {
+      const Slab& sl = slabs_[i];
+      std::size_t b = sl_off[i];
+      for (std::size_t q = slab_begin(sl); q < slab_end(sl); ++q)
+        if (!cert1_[q]) {
+          block_of_[q] = static_cast<std::uint32_t>(b - boff_[sl.k]);  // local to the compartment
+          blk_cells[b++] = static_cast<std::uint32_t>(q - G_[sl.k].off);
+        }
+    });
+    lap("blocks");
+    nchild_ = nblk * nm::kChildren;
+    child_ = uninit<std::uint8_t>(nchild_);
+    if (!nblk) return;
+    up(c_->cell_blk, blk_cells.data(), nblk * sizeof(std::uint32_t));
+    auto* ch_d = c_->cell_child.as<std::uint8_t>(nchild_);
+    for (int k = 0; k < K; ++k) {
+      const std::size_t nb = boff_[k + 1] - boff_[k];
+      if (!nb) continue;
+      nm::k_child_certify<<<static_cast<unsigned>((nb * 64 + 255) / 256), 256, 0, st_>>>(
+          G_[k], static_cast<const std::uint32_t*>(c_->cell_blk.p) + boff_[k], nb, clus_k(k), nclus(k), ctri_k(k),
+          tsph_k(k), static_cast<const double*>(c_->xyz64.p), static_cast<const std::uint32_t*>(c_->tri_idx.p), c_->cx,
+          c_->cy, c_->cz, ch_d + boff_[k] * nm::kChildren);
+    }
+    NM_CUDA(cudaGetLastError());
+    if (verbose_) {
+      NM_CUDA(cudaStreamSynchronize(st_));
+      lap("l2kern");
+    }
+    NM_CUDA(cudaMemcpyAsync(child_.get(), ch_d, nchild_, cudaMemcpyDeviceToHost, st_));
+    NM_CUDA(cudaStreamSynchronize(st_));
+    lap("l2");
+  }
+
+  // ---- runs: every maximal x-run of certified cells gets one winding number ----
+  // per-slab results, merged per compartment in slab order
+  struct SlabRuns {
+    std::vector<double> reps;
+    std::vector<std::int64_t> run_val;
+    std::vector<FineRun> fine;
+  };
+
+  void runs() {
+    const std::size_t ns = slabs_.size();
+    std::vector<SlabRuns> part(ns);
+    run_of_ = uninit<std::int32_t>(total_);
+    parallel_for(static_cast<int>(ns), [&](int i) { slab_runs(slabs_[i], part[i]); });
+    // merge: slab-local run / representative indices -> compartment-local
+    std::vector<std::size_t> run_base(ns), rep_base(ns);
+    for (int k = 0; k < K_; ++k) {
+      std::size_t nr = 0, np = 0;
+      for (std::size_t i = slab_first_[k]; i < slab_first_[k + 1]; ++i) {
+        run_base[i] = nr;
+        rep_base[i] = np;
+        nr += part[i].run_val.size();
+        np += part[i].reps.size() / 3;
+      }
+    }
+    auto rebase = [&](std::int64_t v, std::size_t i) -> std::int64_t {
+      if (v >= kRun) return v + static_cast<std::int64_t>(run_base[i]);
+      if (v >= kRep) return v + static_cast<std::int64_t>(rep_base[i]);
+      return v;
+    };
+    parallel_for(static_cast<int>(ns), [&](int i) {
+      const Slab& sl = slabs_[i];
+      for (std::size_t q = slab_begin(sl); q < slab_end(sl); ++q)
+        if (cert1_[q]) run_of_[q] += static_cast<std::int32_t>(run_base[i]);
+      for (std::int64_t& v : part[i].run_val) v = rebase(v, i);
+      for (FineRun& fr : part[i].fine) fr.v = rebase(fr.v, i);
+    });
+    reps_.assign(K_, {});
+    run_val_.assign(K_, {});
+    fine_.assign(K_, {});
+    parallel_for(K_, [&](int k) {
+      for (std::size_t i = slab_first_[k]; i < slab_first_[k + 1]; ++i) {
+        reps_[k].insert(reps_[k].end(), part[i].reps.begin(), part[i].reps.end());
+        run_val_[k].insert(run_val_[k].end(), part[i].run_val.begin(), part[i].run_val.end());
+        fine_[k].insert(fine_[k].end(), part[i].fine.begin(), part[i].fine.end());
+      }
+    });
+    lap("runs");
+  }
+
+  std::int64_t new_rep(SlabRuns& out, double x, double y, double z) {
+    const std::int64_t v = kRep + static_cast<std::int64_t>(out.reps.size() / 3);
+    out.reps.insert(out.reps.end(), {x + ctr_[0], y + ctr_[1], z + ctr_[2]});
+    return v;
+  }
+
+  void slab_runs(const Slab& sl, SlabRuns& out) {
+    const int k = sl.k;
+    const nm::CellGrid& g = G_[k];
+    for (int iz = sl.z0; iz < sl.z1; ++iz)
+      for (int iy = 0; iy < g.ny; ++iy) {
+        const std::size_t row = g.off + (static_cast<std::size_t>(iz) * g.ny + iy) * g.nx;
+        const double y = g.oy + (iy + 0.5) * g.B, z = g.oz + (iz + 0.5) * g.B;
+        for (int ix = 0; ix < g.nx;) {
+          const bool c1 = cert1_[row + ix];
+          int jx = ix;
+          while (jx + 1 < g.nx && bool(cert1_[row + jx + 1]) == c1) ++jx;
+          if (c1) {
+            // level-1 run [ix, jx]: grid edge or an end outside the 13-DOP -> 0
+            std::int64_t v;
+            if (ix == 0 || jx == g.nx - 1 || outside_dop(k, g.ox + (ix + 0.5) * g.B, y, z) ||
+                outside_dop(k, g.ox + (jx + 0.5) * g.B, y, z))
+              v = 0;
+            else
+              v = new_rep(out, g.ox + ((ix + jx) / 2 + 0.5) * g.B, y, z);
+            for (int q = ix; q <= jx; ++q) run_of_[row + q] = static_cast<std::int32_t>(out.run_val.size());
+            out.run_val.push_back(v);
+          } else {
+            segment_runs(out, k, g, row, ix, jx, iy, iz);
+          }
+          ix = jx + 1;
+        }
+      }
+    // neighbour references: the level-1 runs of the slab's rows exist now
+    // (slab-local indices, rebased with the slab's runs)
+    for (FineRun& fr : out.fine) {
+      if (fr.v == kLeft) fr.v = kRun + run_of_[fr.row + fr.fx0 / S - 1];
+      else if (fr.v == kRight) fr.v = kRun + run_of_[fr.row + fr.fx1 / S + 1];
+    }
+  }
+
+  // segment [ix, jx] of uncertified level-1 cells: runs of certified children
+  // per (sy, sz) sub-row; a run reaching the segment's end continues into the
+  // certified neighbour parent (or the grid edge)
+  void segment_runs(SlabRuns& out, int k, const nm::CellGrid& g, std::size_t row, int ix, int jx, int iy, int iz) {
+    const double b = g.B / S;
+    const int f_lo = S * ix, f_hi = S * jx + S - 1;
+    for (int sz = 0; sz < S; ++sz)
+      for (int sy = 0; sy < S; ++sy)
+        for (int f = f_lo; f <= f_hi;) {
+          if (!child_at(k, row, f, sy, sz)) {
+            ++f;
+            continue;
+          }
+          int e = f;
+          while (e + 1 <= f_hi && child_at(k, row, e + 1, sy, sz)) ++e;
+          std::int64_t v;
+          if (f == f_lo) {
+            v = ix == 0 ? 0 : kLeft;
+          } else if (e == f_hi) {
+            v = jx == g.nx - 1 ? 0 : kRight;
+          } else {
+            const double yy = g.oy + iy * g.B + (sy + 0.5) * b, zz = g.oz + iz * g.B + (sz + 0.5) * b;
+            if (outside_dop(k, g.ox + (f + 0.5) * b, yy, zz) || outside_dop(k, g.ox + (e + 0.5) * b, yy, zz))
+              v = 0;
+            else
+              v = new_rep(out, g.ox + ((f + e) / 2 + 0.5) * b, yy, zz);
+          }
+          out.fine.push_back({row, f, e, sy, sz, v});
+          f = e + 1;
+        }
+  }
+
+  // ---- resolve: representatives evaluated, final codes uploaded ----
+  void resolve() {
+    const int K = K_;
+    std::vector<std::uint32_t> rep_cnt(K, 0), rep_first(K + 1, 0);
+    std::vector<double> rep_all;
+    for (int k = 0; k < K; ++k) {  // compartment k's representatives are contiguous
+      rep_first[k] = static_cast<std::uint32_t>(rep_all.size() / 3);
+      rep_cnt[k] = static_cast<std::uint32_t>(reps_[k].size() / 3);
+      rep_all.insert(rep_all.end(), reps_[k].begin(), reps_[k].end());
+    }
+    nreps_ = rep_all.size() / 3;
+    rep_first[K] = static_cast<std::uint32_t>(nreps_);
+    const std::vector<double> rep_w = evaluate_reps(rep_all, rep_cnt, rep_first);
+    lap("reps");
+    auto code = uninit<std::uint32_t>(total_);
+    auto value = [&](int k, std::int64_t v) -> std::int64_t {  // -> 0, 1 or kUnknown
+      if (v >= kRun) v = run_val_[k][static_cast<std::size_t>(v - kRun)];
+      if (v >= kRep) {
+        const double w = rep_w[rep_first[k] + static_cast<std::size_t>(v - kRep)];
+        return w < 0.0 ? kUnknown : static_cast<std::int64_t>(w);
+      }
+      return v;
+    };
+    parallel_for(static_cast<int>(slabs_.size()), [&](int i) {
+      const Slab& sl = slabs_[i];
+      const int k = sl.k;
+      for (std::size_t q = slab_begin(sl); q < slab_end(sl); ++q) {
+        if (!cert1_[q]) {
+          code[q] = 3u + static_cast<std::uint32_t>(boff_[k] + block_of_[q]);
+          std::fill(child_.get() + (boff_[k] + block_of_[q]) * nm::kChildren,
+                    child_.get() + (boff_[k] + block_of_[q] + 1) * nm::kChildren, 0);
+        } else {
+          const std::int64_t w = value(k, run_val_[k][run_of_[q]]);
+          code[q] = w == kUnknown ? 0u : static_cast<std::uint32_t>(1 + w);
+        }
+      }
+    });
+    parallel_for(K, [&](int k) {  // fine runs write children of their own compartment only
+      for (const FineRun& fr : fine_[k]) {
+        const std::int64_t w = value(k, fr.v);
+        if (w == kUnknown) continue;
+        for (int f = fr.fx0; f <= fr.fx1; ++f) child_at(k, fr.row, f, fr.sy, fr.sz) = static_cast<std::uint8_t>(1 + w);
+      }
+    });
+    lap("codes");
+    up(c_->cell_state, code.get(), total_ * sizeof(std::uint32_t));
+    up(c_->cell_child, child_.get(), nchild_);
+    up(c_->cell_grids, G_.data(), G_.size() * sizeof(nm::CellGrid));
+    NM_CUDA(cudaStreamSynchronize(st_));
+    lap("final");
+    c_->cells_total = total_ + nchild_;
+    c_->cells_certified = 0;
+    for (std::size_t q = 0; q < total_; ++q) c_->cells_certified += code[q] == 1 || code[q] == 2;
+    for (std::size_t q = 0; q < nchild_; ++q) c_->cells_certified += child_[q] != 0;
+    c_->cell_reps = nreps_;
+    c_->cells = true;
+    c_->ms_cells = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0_).count();
+  }
+
+  // s at every representative (sparse k_label against its own compartment);
+  // w = round(s) when within 1e-3 of 0 or 1, else -1 (the run stays unresolved)
+  std::vector<double> evaluate_reps(const std::vector<double>& rep_all, const std::vector<std::uint32_t>& rep_cnt,
+                                    const std::vector<std::uint32_t>& rep_first) {
+    const int K = K_;
+    const std::size_t R = nreps_;
+    std::vector<double> rep_w(R, -1.0);
+    if (!R) return rep_w;
+    up(c_->rep_pts, rep_all.data(), rep_all.size() * sizeof(double));
+    auto* s_dev = c_->rep_s.as<double>(R * K);
+    auto* m_dev = c_->rep_m.as<std::uint32_t>(R);
+    auto* f_dev = c_->rep_f.as<std::uint32_t>(R);
+    std::vector<std::uint32_t> iota(R);
+    std::iota(iota.begin(), iota.end(), 0u);
+    up(c_->sp_list, iota.data(), R * sizeof(std::uint32_t));
+    NM_CUDA(cudaMemsetAsync(m_dev, 0, R * sizeof(std::uint32_t), st_));
+    NM_CUDA(cudaMemsetAsync(f_dev, 0, R * sizeof(std::uint32_t), st_));
+    nm::LabelParams prm{};
+    prm.pts = static_cast<const double*>(c_->rep_pts.p);
+    prm.n = R;
+    prm.order = nullptr;
+    prm.tri = static_cast<const float4*>(c_->tri.p);
+    prm.sub = static_cast<const float4*>(c_->sub.p);
+    prm.edges = static_cast<const float4*>(c_->edges.p);
+    prm.cont = static_cast<const std::uint32_t*>(c_->cont.p);
+    prm.comp_tiles = static_cast<const std::uint32_t*>(c_->comp_tiles.p);
+    prm.K = K;
+    prm.cx = c_->cx;
+    prm.cy = c_->cy;
+    prm.cz = c_->cz;
+    prm.T = 0.5;
+    prm.band = c_->opt.band;
+    prm.tau = c_->opt.tau;
+    prm.delta = c_->opt.delta_mm;
+    prm.masks = m_dev;
+    prm.flagmask = f_dev;
+    prm.s_out = s_dev;
+    prm.sp_list = static_cast<const std::uint32_t*>(c_->sp_list.p);
+    launch_sparse(c_, prm, rep_cnt, st_);
+    std::vector<double> s(R * K);
+    NM_CUDA(cudaMemcpyAsync(s.data(), s_dev, R * K * sizeof(double), cudaMemcpyDeviceToHost, st_));
+    NM_CUDA(cudaStreamSynchronize(st_));
+    for (int k = 0; k < K; ++k)
+      for (std::uint32_t r = rep_first[k]; r < rep_first[k + 1]; ++r) {
+        const double v = s[static_cast<std::size_t>(r) * K + k];
+        const double w = std::round(v);
+        if (std::fabs(v - w) < 1e-3 && (w == 0.0 || w == 1.0)) rep_w[r] = w;
+      }
+    return rep_w;
+  }
+};
+
+std::unique_ptr<CellBuilder> make_cell_builder(nm_ctx* c, const double* xyz, const std::uint32_t* tri,
+                                               const std::uint32_t* comp_off, const std::vector<float4>& hbox,
+                                               cudaStream_t st) {
+  return std::make_unique<CellBuild>(c, xyz, tri, comp_off, hbox, st);
+}
+
+}  // namespace nmh

@@ -54,7 +54,7 @@ constexpr int kChildren = kSubCells * kSubCells * kSubCells;
 // cube ball), then each lane tests the surviving clusters against its own
 // ball (ball_hits_surface's tests). Returns this lane's "ball meets the
 // surface"; inactive lanes return true.
-__device__ bool warp_certify(double Ox, double Oy, double Oz, double e, bool active, const float4* __restrict__ clus,
+static __device__ bool warp_certify(double Ox, double Oy, double Oz, double e, bool active, const float4* __restrict__ clus,
                              int nclus, const std::uint32_t* __restrict__ clus_tri, const float4* __restrict__ tsph,
                              const double* __restrict__ xyz, const std::uint32_t* __restrict__ tri, double cx,
                              double cy, double cz) {
@@ -108,7 +108,7 @@ __device__ bool warp_certify(double Ox, double Oy, double Oz, double e, bool act
 
 // Level 1: one warp per 4 x 4 x 2 brick of cells of one compartment;
 // cert = 1 when no triangle of the compartment meets the cell's ball.
-__global__ void __launch_bounds__(256) k_cell_certify(const CellGrid g, const float4* __restrict__ clus, int nclus,
+static __global__ void __launch_bounds__(256) k_cell_certify(const CellGrid g, const float4* __restrict__ clus, int nclus,
                                                       const std::uint32_t* __restrict__ clus_tri,
                                                       const float4* __restrict__ tsph, const double* __restrict__ xyz,
                                                       const std::uint32_t* __restrict__ tri, double cx, double cy,
@@ -130,7 +130,7 @@ __global__ void __launch_bounds__(256) k_cell_certify(const CellGrid g, const fl
 // uncertified level-1 cell, one warp per half (4 x 4 x 2 children). cells[b]
 // = level-1 cell (local index) of child block b; out[b * kChildren + child]
 // = 1 when certified, child = (sz * 4 + sy) * 4 + sx.
-__global__ void __launch_bounds__(256) k_child_certify(const CellGrid g, const std::uint32_t* __restrict__ cells,
+static __global__ void __launch_bounds__(256) k_child_certify(const CellGrid g, const std::uint32_t* __restrict__ cells,
                                                        std::size_t nblocks, const float4* __restrict__ clus, int nclus,
                                                        const std::uint32_t* __restrict__ clus_tri,
                                                        const float4* __restrict__ tsph, const double* __restrict__ xyz,
@@ -173,7 +173,7 @@ struct ClassifyParams {
   double* s_out;
 };
 
-__global__ void k_cell_classify(const ClassifyParams prm) {
+static __global__ void k_cell_classify(const ClassifyParams prm) {
   for (std::size_t i = blockIdx.x * static_cast<std::size_t>(blockDim.x) + threadIdx.x; i < prm.n;
        i += static_cast<std::size_t>(gridDim.x) * blockDim.x) {
     const std::size_t j = prm.order ? prm.order[i] : i;

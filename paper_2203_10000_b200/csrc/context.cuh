@@ -1,0 +1,256 @@
+// Host-side internals shared by the translation units of libnestmesh_label.so
+// (nestmesh_label.cu: context, surfaces, node pass, labeling ABI;
+// cell_build.cu: certified cells; group.cu: nm_group; mesh_ops.cu: relabel,
+// refinement, boundary extraction, lattice, distance). Not part of the ABI.
+#pragma once
+#include <algorithm>
+#include <chrono>
+#include <array>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <cstdlib>
+#include <exception>
+#include <memory>
+#include <numeric>
+#include <queue>
+#include <unordered_map>
+#include <stdexcept>
+#include <string>
+#include <thread>
+#include <type_traits>
+#include <atomic>
+#include <vector>
+#include <cub/device/device_radix_sort.cuh>
+#include <cuda_runtime.h>
+#include <cub/device/device_scan.cuh>
+#include "kernels.cuh"
+#include "refine.cuh"
+#include "distance.cuh"
+#include "cells.cuh"
+#include "nestmesh_label.h"
+#include "refine.h"
+
+namespace nmh {
+
+
+// thread-local message of the last failed C ABI call (nm_last_error)
+inline std::string& last_error() {
+  thread_local std::string e;
+  return e;
+}
+
+struct Error : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+#define NM_CUDA(x)                                                                                    \
+  do {                                                                                                \
+    cudaError_t e_ = (x);                                                                             \
+    if (e_ != cudaSuccess)                                                                            \
+      throw Error(std::string(#x) + ": " + cudaGetErrorName(e_) + " " + cudaGetErrorString(e_));       \
+  } while (0)
+
+template <class F>
+inline int guarded(F&& f) {
+  try {
+    f();
+    return 0;
+  } catch (const std::exception& e) {
+    last_error() = e.what();
+    return 1;
+  } catch (...) {
+    last_error() = "unknown error";
+    return 1;
+  }
+}
+
+// Growable device buffer.
+struct DBuf {
+  void* p = nullptr;
+  std::size_t cap = 0;
+  void* get(std::size_t bytes) {
+    if (bytes > cap) {
+      if (p) cudaFree(p);
+      p = nullptr;
+      cap = 0;
+      const std::size_t want = std::max<std::size_t>(bytes, 256);
+      NM_CUDA(cudaMalloc(&p, want));
+      cap = want;
+    }
+    return p;
+  }
+  template <class T>
+  T* as(std::size_t count) {
+    return static_cast<T*>(get(count * sizeof(T)));
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+  }
+};
+
+// Run f(0..n-1) on up to hardware_concurrency host threads (independent
+// per-compartment host work of nm_set_surfaces; f must not throw).
+template <class F>
+inline void parallel_for(int n, F&& f) {
+  const int nth = std::max(1, std::min<int>(n, static_cast<int>(std::thread::hardware_concurrency())));
+  if (nth <= 1) {
+    for (int k = 0; k < n; ++k) f(k);
+    return;
+  }
+  std::atomic<int> next{0};
+  std::vector<std::thread> th;
+  for (int t = 0; t < nth; ++t)
+    th.emplace_back([&] {
+      for (int k; (k = next++) < n;) f(k);
+    });
+  for (auto& x : th) x.join();
+}
+
+// Morton order of triangle centroids (per compartment): compact 256-triangle
+// tiles and 32-triangle subtiles for the near/far split. Order affects only
+// the fp32 summation order, never which triangles are summed.
+inline std::uint32_t spread10h(std::uint32_t v) {
+  v &= 0x3ffu;
+  v = (v | (v << 16)) & 0x030000ffu;
+  v = (v | (v << 8)) & 0x0300f00fu;
+  v = (v | (v << 4)) & 0x030c30c3u;
+  v = (v | (v << 2)) & 0x09249249u;
+  return v;
+}
+
+
+// Greedy triangle-strip decomposition of one compartment.
+// Start from the unused triangle with the fewest unused neighbours, try its
+// three rotations, walk forward across (u_{k+1}, u_{k+2}) and backward from the
+// reversed start, keep the longest. Returns, per strip, the vertex sequence
+// u_0..u_{m+1} and the original triangle ids t_0..t_{m-1} with
+// {u_k, u_{k+1}, u_{k+2}} == set(t_k). Only performance depends on the
+// quality of the decomposition; every triangle appears in exactly one strip.
+
+}  // namespace nmh
+
+struct nm_ctx {
+  nm_options opt{};
+  cudaStream_t stream = nullptr;
+  cudaStream_t side = nullptr;           // tet upload + validation, overlapped with the node pass
+  cudaEvent_t ev[6] = {};
+  cudaEvent_t ev_side = nullptr;
+  std::uint32_t* h_word = nullptr;        // pinned: max tet node index read back from the side stream
+  std::uint64_t node_launches = 0;        // launches of the last label_nodes_dev
+  int sm_count = 0;
+
+  // surfaces
+  bool has_surfaces = false;
+  bool strips = false;  // tile layout of the current surfaces
+  std::size_t flag_cap = 0;  // flagmask length when evaluating a subset (= node count)
+  int K = 0;
+  std::size_t nt_real = 0, nt_pad = 0, nv = 0;
+  double cx = 0, cy = 0, cz = 0;
+  double lo[3] = {0, 0, 0}, span = 1.0;  // Morton box of the domain
+  nm::LabelIds ids{};
+  std::vector<std::uint32_t> comp_tiles_h;  // host copy of the K+1 tile offsets
+  std::size_t n_continued = 0;              // strip segments continuing the previous one (cont bits set)
+  nmh::DBuf tri, sub, edges, cont, comp_tiles, xyz64, tri_idx, comp_off, comp_box, cullmask;
+  // certified cells (cull_outside = 2, cells.cuh)
+  bool cells = false;
+  nmh::DBuf dist_clus, dist_slot, dist_ord, sp_part, sp_det, cell_state, cell_child, cell_cert, cell_blk, cell_grids, clus, clus_tri, clus_tsph, unk, sp_list, sp_chunk, sp_cnt, rep_pts, rep_s, rep_m, rep_f;
+  std::uint64_t cells_total = 0, cells_certified = 0, cell_reps = 0, sparse_pairs = 0, sparse_evals = 0;
+  double ms_cells = 0.0;  // host wall time of the certification (nm_set_surfaces)
+  std::vector<std::uint32_t> comp_off_h;
+
+  // scratch
+  nmh::DBuf pts, masks, flagmask, nbr, known, want, fkeys, frontier, lex, region, bfaces, btri, dist_tri, dist_xyz,
+      dist_idx, dist_d32, dist_out, r_red, r_keys, r_keys2, r_S, r_idx, r_touched,
+      r_mask, r_cnt, r_offs, r_flag, meshA_nodes, meshA_tets, meshA_labels, meshB_nodes, meshB_tets, meshB_labels,
+      meshB_parent, masks2, order, keys, keys_alt, order_alt, cub_tmp, list, chunk, counters, count, tets, labels,
+      s_out, word;
+
+  ~nm_ctx() {
+    for (nmh::DBuf* b : {&dist_clus, &dist_slot, &dist_ord, &sp_part, &sp_det, &cell_state, &cell_child, &cell_cert, &cell_blk, &cell_grids, &clus, &clus_tri, &clus_tsph, &unk, &sp_list, &sp_chunk, &sp_cnt, &rep_pts, &rep_s,
+                    &rep_m, &rep_f})
+      b->release();
+    for (nmh::DBuf* b : {&tri, &sub, &edges, &cont, &comp_tiles, &xyz64, &tri_idx, &comp_off, &comp_box, &cullmask, &pts, &masks, &flagmask, &nbr, &known, &want, &fkeys, &frontier, &lex, &region, &bfaces, &btri,
+                    &dist_tri, &dist_xyz, &dist_idx, &dist_d32, &dist_out, &r_red, &r_keys, &r_keys2, &r_S,
+                    &r_idx, &r_touched, &r_mask, &r_cnt, &r_offs, &r_flag, &meshA_nodes, &meshA_tets, &meshA_labels,
+                    &meshB_nodes, &meshB_tets, &meshB_labels, &meshB_parent, &masks2, &order, &keys,
+                    &keys_alt, &order_alt, &cub_tmp, &list, &chunk, &counters, &count, &tets, &labels, &s_out, &word})
+      b->release();
+    for (auto& e : ev)
+      if (e) cudaEventDestroy(e);
+    if (ev_side) cudaEventDestroy(ev_side);
+    if (h_word) cudaFreeHost(h_word);
+    if (side) cudaStreamDestroy(side);
+    if (stream) cudaStreamDestroy(stream);
+  }
+
+  cudaStream_t pick(void* s) const { return s ? static_cast<cudaStream_t>(s) : stream; }
+};
+
+namespace nmh {
+
+inline void require_surfaces(const nm_ctx* c) {
+  if (!c) throw Error("null context");
+  if (!c->has_surfaces) throw Error("nm_set_surfaces has not been called");
+}
+
+inline int grid_for(std::size_t n, int block, int cap) {
+  const std::size_t g = (n + block - 1) / block;
+  return static_cast<int>(std::max<std::size_t>(1, std::min<std::size_t>(g, static_cast<std::size_t>(cap))));
+}
+
+// Ordered compaction of [0,n) under pred into out; count on the device.
+template <class Pred>
+void select(nm_ctx* c, Pred pred, std::size_t n, std::uint32_t* out, std::uint32_t* d_count, cudaStream_t st,
+            std::uint64_t& launches) {
+  const std::size_t nb = std::max<std::size_t>(1, (n + nm::kSelChunk - 1) / nm::kSelChunk);
+  auto* chunk = c->chunk.as<std::uint32_t>(nb);
+  nm::k_select_count<<<static_cast<unsigned>(nb), nm::kSelBlock, 0, st>>>(pred, n, chunk);
+  nm::k_select_scan<<<1, 1024, 0, st>>>(chunk, nb, d_count);
+  nm::k_select_write<<<static_cast<unsigned>(nb), nm::kSelBlock, 0, st>>>(pred, n, chunk, out);
+  NM_CUDA(cudaGetLastError());
+  launches += 3;
+}
+
+// ---- node pass and tet labels (nestmesh_label.cu) ----
+// Full node pass on device-resident points: Morton order -> K1 -> compaction
+// of flagged points -> K3. masks/s_out are device pointers. d_subset
+// (nullable): evaluate only points d_pts[d_subset[i]], i < n (masks and s at
+// the original index). stats_deferred: the caller collects the stats later
+// with read_node_stats. nshards >= 1: a sharded pass
+// (nm_label_nodes_shard_device).
+void label_nodes_dev(nm_ctx* c, const double* d_pts, std::size_t n, double T, std::uint32_t* d_masks, double* d_s,
+                     cudaStream_t st, nm_stats* stats, const std::uint32_t* d_subset = nullptr,
+                     bool stats_deferred = false, int shard = 0, int nshards = 0);
+void read_node_stats(nm_ctx* c, std::size_t n, cudaStream_t st, nm_stats* stats);
+void label_tets_dev(nm_ctx* c, const std::uint32_t* d_tets, std::size_t nt, const std::uint32_t* d_masks, int* d_labels,
+                    cudaStream_t st, nm_stats* stats);
+void check_tets(const std::uint32_t* tets, std::size_t nt, std::size_t n_nodes);
+void check_tets_device(nm_ctx* c, const std::uint32_t* d_tets, const std::uint32_t* h_tets, std::size_t nt,
+                       std::size_t n_nodes, cudaStream_t st);
+// sparse k_label over per-compartment pair lists (first: slice starts; default packed)
+int launch_sparse(nm_ctx* c, nm::LabelParams& prm, const std::vector<std::uint32_t>& cnt, cudaStream_t st,
+                  const std::vector<std::uint32_t>* first = nullptr);
+
+// ---- certified cells (cell_build.cu) ----
+// prepare(): grids, certification, runs (may run on a host thread beside the
+// tile packing, on its own stream); finish(): representatives + codes (needs
+// the tiles).
+class CellBuilder {
+ public:
+  virtual ~CellBuilder() = default;
+  virtual void prepare() = 0;
+  virtual void finish() = 0;
+};
+std::unique_ptr<CellBuilder> make_cell_builder(nm_ctx* c, const double* xyz, const std::uint32_t* tri,
+                                               const std::uint32_t* comp_off, const std::vector<float4>& hbox,
+                                               cudaStream_t st);
+
+// ---- mesh operations (mesh_ops.cu) ----
+std::uint32_t* lex_order3(nm_ctx* c, const std::uint32_t* k0, const std::uint32_t* k1, const std::uint32_t* k2,
+                          std::size_t m, cudaStream_t st);
+void face_adjacency(nm_ctx* c, const uint4* t4, std::size_t nt, std::int32_t* d_nbr, cudaStream_t st);
+
+}  // namespace nmh

@@ -113,7 +113,7 @@ struct DistParams {
 // holds no triangle that could change the pass's result, so d32 and the
 // candidate set — hence the fp64 minimum — are those of the full scan.
 template <int PASS>
-__global__ void __launch_bounds__(256) k_point_surface_distance(const DistParams prm) {
+static __global__ void __launch_bounds__(256) k_point_surface_distance(const DistParams prm) {
   const std::size_t i = blockIdx.x * static_cast<std::size_t>(blockDim.x) + threadIdx.x;
   if (i >= prm.n) return;
   const std::size_t j = prm.order ? prm.order[i] : i;

@@ -163,7 +163,7 @@ constexpr int kFoldTiles = 32;
 // (prm.cull); 2: sparse (prm.sp_*): (point, compartment) pairs left unknown
 // by the certified-cell classification (k_cell_classify).
 template <int NP, bool STRIP, int MODE = 0>
-__global__ void __launch_bounds__(kBlock, (NP == 1 ? NM_MIN_BLOCKS : NM_MIN_BLOCKS_NP2)) k_label(const LabelParams prm) {
+static __global__ void __launch_bounds__(kBlock, (NP == 1 ? NM_MIN_BLOCKS : NM_MIN_BLOCKS_NP2)) k_label(const LabelParams prm) {
   constexpr int P = 2 * NP;
   constexpr bool CULL = MODE == 1;
   constexpr bool SPARSE = MODE == 2;
@@ -519,7 +519,7 @@ struct FinalizeParams {
   double* s_out;
 };
 
-__global__ void k_sparse_finalize(const FinalizeParams prm) {
+static __global__ void k_sparse_finalize(const FinalizeParams prm) {
   const std::size_t total = prm.qo[prm.K];
   for (std::size_t q = blockIdx.x * static_cast<std::size_t>(blockDim.x) + threadIdx.x; q < total;
        q += static_cast<std::size_t>(gridDim.x) * blockDim.x) {
@@ -543,7 +543,7 @@ __global__ void k_sparse_finalize(const FinalizeParams prm) {
 }
 
 
-__global__ void k_morton_keys(const double* pts, std::size_t n, const std::uint32_t* subset, double lx, double ly,
+static __global__ void k_morton_keys(const double* pts, std::size_t n, const std::uint32_t* subset, double lx, double ly,
                               double lz, double inv, std::uint32_t* keys, std::uint32_t* idx) {
   for (std::size_t i = blockIdx.x * static_cast<std::size_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<std::size_t>(gridDim.x) * blockDim.x) {
@@ -568,7 +568,7 @@ constexpr int kSelItems = 8;  // per thread
 constexpr int kSelChunk = kSelBlock * kSelItems;
 
 template <class Pred>
-__global__ void __launch_bounds__(kSelBlock) k_select_count(Pred pred, std::size_t n, std::uint32_t* chunk_counts) {
+static __global__ void __launch_bounds__(kSelBlock) k_select_count(Pred pred, std::size_t n, std::uint32_t* chunk_counts) {
   const std::size_t b0 = static_cast<std::size_t>(blockIdx.x) * kSelChunk;
   int total = 0;
 #pragma unroll
@@ -580,7 +580,7 @@ __global__ void __launch_bounds__(kSelBlock) k_select_count(Pred pred, std::size
 }
 
 // Single-CTA exclusive scan of chunk counts; writes the grand total.
-__global__ void __launch_bounds__(1024) k_select_scan(std::uint32_t* counts, std::size_t nb, std::uint32_t* d_total) {
+static __global__ void __launch_bounds__(1024) k_select_scan(std::uint32_t* counts, std::size_t nb, std::uint32_t* d_total) {
   __shared__ std::uint32_t warp_sums[32];
   __shared__ std::uint32_t carry;
   if (threadIdx.x == 0) carry = 0;
@@ -618,7 +618,7 @@ __global__ void __launch_bounds__(1024) k_select_scan(std::uint32_t* counts, std
 }
 
 template <class Pred>
-__global__ void __launch_bounds__(kSelBlock) k_select_write(Pred pred, std::size_t n, const std::uint32_t* chunk_offsets,
+static __global__ void __launch_bounds__(kSelBlock) k_select_write(Pred pred, std::size_t n, const std::uint32_t* chunk_offsets,
                                                             std::uint32_t* out) {
   __shared__ std::uint32_t warp_cnt[kSelBlock / 32];
   const std::size_t b0 = static_cast<std::size_t>(blockIdx.x) * kSelChunk;
@@ -684,7 +684,7 @@ struct FixupParams {
 };
 
 constexpr int kFixWarps = 4;  // warps per flagged point (one CTA)
-__global__ void __launch_bounds__(32 * kFixWarps) k_fixup(const FixupParams prm) {
+static __global__ void __launch_bounds__(32 * kFixWarps) k_fixup(const FixupParams prm) {
   __shared__ double part[kFixWarps];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const std::uint32_t cnt = *prm.count;
@@ -736,7 +736,7 @@ __global__ void __launch_bounds__(32 * kFixWarps) k_fixup(const FixupParams prm)
 // K4: tet labels: highest-priority compartment containing all
 // four nodes, else 0.
 // ---------------------------------------------------------------------------
-__global__ void k_label_tets(const uint4* __restrict__ tets, std::size_t nt, const std::uint32_t* __restrict__ masks,
+static __global__ void k_label_tets(const uint4* __restrict__ tets, std::size_t nt, const std::uint32_t* __restrict__ masks,
                              int* __restrict__ labels, const LabelIds ids) {
   for (std::size_t i = blockIdx.x * static_cast<std::size_t>(blockDim.x) + threadIdx.x; i < nt;
        i += static_cast<std::size_t>(gridDim.x) * blockDim.x) {
@@ -765,7 +765,7 @@ __device__ __forceinline__ void face_key(const uint4 t, int f, std::uint32_t& a,
   if (a > b) { const std::uint32_t s = a; a = b; b = s; }
 }
 
-__global__ void k_face_keys(const uint4* tets, std::size_t nt, std::uint32_t* ka, std::uint32_t* kb, std::uint32_t* kc,
+static __global__ void k_face_keys(const uint4* tets, std::size_t nt, std::uint32_t* ka, std::uint32_t* kb, std::uint32_t* kc,
                             std::uint32_t* fid) {
   for (std::size_t i = blockIdx.x * static_cast<std::size_t>(blockDim.x) + threadIdx.x; i < 4 * nt;
        i += static_cast<std::size_t>(gridDim.x) * blockDim.x) {
@@ -779,14 +779,14 @@ __global__ void k_face_keys(const uint4* tets, std::size_t nt, std::uint32_t* ka
 }
 
 // out[p] = key[fid[p]] (next LSD radix key for the current face order).
-__global__ void k_gather_key(const std::uint32_t* key, const std::uint32_t* fid, std::size_t m, std::uint32_t* out) {
+static __global__ void k_gather_key(const std::uint32_t* key, const std::uint32_t* fid, std::size_t m, std::uint32_t* out) {
   for (std::size_t p = blockIdx.x * static_cast<std::size_t>(blockDim.x) + threadIdx.x; p < m;
        p += static_cast<std::size_t>(gridDim.x) * blockDim.x)
     out[p] = key[fid[p]];
 }
 
 // Faces sorted by (a,b,c): equal neighbours are the two sides of one face.
-__global__ void k_face_pairs(const std::uint32_t* fid, std::size_t m, const std::uint32_t* ka, const std::uint32_t* kb,
+static __global__ void k_face_pairs(const std::uint32_t* fid, std::size_t m, const std::uint32_t* ka, const std::uint32_t* kb,
                              const std::uint32_t* kc, std::int32_t* nbr) {
   for (std::size_t p = blockIdx.x * static_cast<std::size_t>(blockDim.x) + threadIdx.x; p + 1 < m;
        p += static_cast<std::size_t>(gridDim.x) * blockDim.x) {
@@ -799,7 +799,7 @@ __global__ void k_face_pairs(const std::uint32_t* fid, std::size_t m, const std:
 }
 
 // Nodes of tets adjacent to a label-change face.
-__global__ void k_frontier(const uint4* tets, std::size_t nt, const std::int32_t* nbr, const int* labels,
+static __global__ void k_frontier(const uint4* tets, std::size_t nt, const std::int32_t* nbr, const int* labels,
                            std::uint8_t* want) {
   for (std::size_t t = blockIdx.x * static_cast<std::size_t>(blockDim.x) + threadIdx.x; t < nt;
        t += static_cast<std::size_t>(gridDim.x) * blockDim.x) {
@@ -826,13 +826,13 @@ struct PredWantNew {
   __device__ bool operator()(std::size_t i) const { return want[i] && !known[i]; }
 };
 
-__global__ void k_mark_known(const std::uint32_t* ids, const std::uint32_t* count, std::uint8_t* known) {
+static __global__ void k_mark_known(const std::uint32_t* ids, const std::uint32_t* count, std::uint8_t* known) {
   const std::uint32_t n = *count;
   for (std::uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) known[ids[i]] = 1;
 }
 
 // Label update barrier: every tet whose four nodes are evaluated.
-__global__ void k_relabel_tets(const uint4* tets, std::size_t nt, const std::uint32_t* masks, const std::uint8_t* known,
+static __global__ void k_relabel_tets(const uint4* tets, std::size_t nt, const std::uint32_t* masks, const std::uint8_t* known,
                                int* labels, const LabelIds ids, unsigned long long* changed) {
   unsigned long long c = 0;
   for (std::size_t t = blockIdx.x * static_cast<std::size_t>(blockDim.x) + threadIdx.x; t < nt;
@@ -854,7 +854,7 @@ __global__ void k_relabel_tets(const uint4* tets, std::size_t nt, const std::uin
 namespace nm {
 
 // Centroid query points (a + b + c + d) * 0.25 in fp64 (the oracle's order).
-__global__ void k_centroids(const double* nodes, const uint4* tets, std::size_t nt, double* out) {
+static __global__ void k_centroids(const double* nodes, const uint4* tets, std::size_t nt, double* out) {
   for (std::size_t t = blockIdx.x * static_cast<std::size_t>(blockDim.x) + threadIdx.x; t < nt;
        t += static_cast<std::size_t>(gridDim.x) * blockDim.x) {
     const uint4 e = tets[t];
@@ -870,7 +870,7 @@ __global__ void k_centroids(const double* nodes, const uint4* tets, std::size_t 
 }
 
 // label = id[ffs(mask)] or 0 for point-mode labels (centroids).
-__global__ void k_mask_labels(const std::uint32_t* masks, std::size_t n, int* labels, const LabelIds ids) {
+static __global__ void k_mask_labels(const std::uint32_t* masks, std::size_t n, int* labels, const LabelIds ids) {
   for (std::size_t i = blockIdx.x * static_cast<std::size_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<std::size_t>(gridDim.x) * blockDim.x) {
     const std::uint32_t m = masks[i];
@@ -882,14 +882,14 @@ __global__ void k_mask_labels(const std::uint32_t* masks, std::size_t n, int* la
 
 namespace nm {
 
-__global__ void k_iota(std::uint32_t* p, std::size_t m) {
+static __global__ void k_iota(std::uint32_t* p, std::size_t m) {
   for (std::size_t i = blockIdx.x * static_cast<std::size_t>(blockDim.x) + threadIdx.x; i < m;
        i += static_cast<std::size_t>(gridDim.x) * blockDim.x)
     p[i] = static_cast<std::uint32_t>(i);
 }
 
 // in_region[t] = labels[t] in set (extract_region_boundary, mesh.hpp:146-155)
-__global__ void k_region(const int* labels, std::size_t nt, const LabelIds set, int n_set, std::uint8_t* in_region) {
+static __global__ void k_region(const int* labels, std::size_t nt, const LabelIds set, int n_set, std::uint8_t* in_region) {
   for (std::size_t t = blockIdx.x * static_cast<std::size_t>(blockDim.x) + threadIdx.x; t < nt;
        t += static_cast<std::size_t>(gridDim.x) * blockDim.x) {
     const int l = labels[t];
@@ -917,7 +917,7 @@ struct PredUniqueU32 {
 };
 
 // outward face i of a positively oriented tet (mesh.hpp:57-64)
-__global__ void k_face_tris(const uint4* tets, const std::uint32_t* faces, std::uint32_t nb, std::uint32_t* t0,
+static __global__ void k_face_tris(const uint4* tets, const std::uint32_t* faces, std::uint32_t nb, std::uint32_t* t0,
                             std::uint32_t* t1, std::uint32_t* t2) {
   for (std::uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nb; i += gridDim.x * blockDim.x) {
     const std::uint32_t f = faces[i];
@@ -931,7 +931,7 @@ __global__ void k_face_tris(const uint4* tets, const std::uint32_t* faces, std::
   }
 }
 
-__global__ void k_gather_tris(const std::uint32_t* order, std::uint32_t nb, const std::uint32_t* t0,
+static __global__ void k_gather_tris(const std::uint32_t* order, std::uint32_t nb, const std::uint32_t* t0,
                               const std::uint32_t* t1, const std::uint32_t* t2, std::uint32_t* out) {
   for (std::uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nb; i += gridDim.x * blockDim.x) {
     const std::uint32_t j = order[i];
@@ -949,7 +949,7 @@ namespace nm {
 // (lattice.hpp:40-91): nodes k,j,i-major at origin + (i h, j h, k h); per cell
 // the central + 4 corner tets of the parity pattern; orientation normalised
 // with the fp64 tet_signed_volume of vec3.hpp:79-81 (same operand order).
-__global__ void k_lattice_nodes(double ox, double oy, double oz, double h, int nx, int ny, int nz, double* nodes) {
+static __global__ void k_lattice_nodes(double ox, double oy, double oz, double h, int nx, int ny, int nz, double* nodes) {
   const std::size_t n = static_cast<std::size_t>(nx + 1) * (ny + 1) * (nz + 1);
   for (std::size_t v = blockIdx.x * static_cast<std::size_t>(blockDim.x) + threadIdx.x; v < n;
        v += static_cast<std::size_t>(gridDim.x) * blockDim.x) {
@@ -976,7 +976,7 @@ __device__ __forceinline__ double tet_volume64(const double* P, const std::uint3
   return __ddiv_rn(__dadd_rn(__dadd_rn(__dmul_rn(u0, x0), __dmul_rn(u1, x1)), __dmul_rn(u2, x2)), 6.0);
 }
 
-__global__ void k_lattice_tets(const double* nodes, int nx, int ny, int nz, uint4* tets) {
+static __global__ void k_lattice_tets(const double* nodes, int nx, int ny, int nz, uint4* tets) {
   const std::size_t cells = static_cast<std::size_t>(nx) * ny * nz;
   for (std::size_t cidx = blockIdx.x * static_cast<std::size_t>(blockDim.x) + threadIdx.x; cidx < cells;
        cidx += static_cast<std::size_t>(gridDim.x) * blockDim.x) {
@@ -1043,7 +1043,7 @@ namespace nm {
 // Exact outside culling, per point: bit k set when the point (fp32 centred
 // coordinates, as k_label forms them) lies outside a slab of compartment k's
 // 13-DOP — outside the convex hull, so its winding number is exactly 0.
-__global__ void k_cull_mask(const double* pts, const std::uint32_t* order, std::size_t n, double cx, double cy, double cz,
+static __global__ void k_cull_mask(const double* pts, const std::uint32_t* order, std::size_t n, double cx, double cy, double cz,
                             const float4* dop4, int K, std::uint32_t* out) {
   for (std::size_t i = blockIdx.x * static_cast<std::size_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<std::size_t>(gridDim.x) * blockDim.x) {
@@ -1067,7 +1067,7 @@ __global__ void k_cull_mask(const double* pts, const std::uint32_t* order, std::
 
 // masks / flagmask of the evaluated points cleared before a compartment-split
 // k_label launch (which ORs its bits in).
-__global__ void k_zero_masks(std::size_t n, const std::uint32_t* subset, std::uint32_t* masks,
+static __global__ void k_zero_masks(std::size_t n, const std::uint32_t* subset, std::uint32_t* masks,
                              std::uint32_t* flagmask) {
   for (std::size_t i = blockIdx.x * static_cast<std::size_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<std::size_t>(gridDim.x) * blockDim.x) {
@@ -1079,7 +1079,7 @@ __global__ void k_zero_masks(std::size_t n, const std::uint32_t* subset, std::ui
 
 // Largest node index referenced by the tets (device-side validation of the
 // host mesh, overlapped with the node pass in nm_label_mesh).
-__global__ void k_max_index(const uint4* __restrict__ tets, std::size_t nt, std::uint32_t* __restrict__ out) {
+static __global__ void k_max_index(const uint4* __restrict__ tets, std::size_t nt, std::uint32_t* __restrict__ out) {
   std::uint32_t m = 0;
   for (std::size_t i = blockIdx.x * static_cast<std::size_t>(blockDim.x) + threadIdx.x; i < nt;
        i += static_cast<std::size_t>(gridDim.x) * blockDim.x) {

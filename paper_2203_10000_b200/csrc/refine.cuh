@@ -32,7 +32,7 @@ __device__ __forceinline__ bool has_key(const unsigned long long* S, int m, unsi
   return i < m && S[i] == k;
 }
 
-__constant__ int kEdgeD[6][2] = {{0, 1}, {0, 2}, {0, 3}, {1, 2}, {1, 3}, {2, 3}};
+static __constant__ int kEdgeD[6][2] = {{0, 1}, {0, 2}, {0, 3}, {1, 2}, {1, 3}, {2, 3}};
 
 // 6-bit split-edge mask -> pattern: 0 none, 1 one edge, 2 two edges of one
 // face, 3 one full face, -1 escalate (the host classify()).
@@ -50,12 +50,12 @@ __device__ __forceinline__ int pattern_of(unsigned mask) {
   return -1;
 }
 
-__global__ void k_mark_list(const std::uint32_t* ids, const std::uint32_t* count, std::uint8_t* flag) {
+static __global__ void k_mark_list(const std::uint32_t* ids, const std::uint32_t* count, std::uint8_t* flag) {
   const std::uint32_t n = *count;
   for (std::uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) flag[ids[i]] = 1;
 }
 
-__global__ void k_red_edges(const uint4* tets, const std::uint32_t* red_list, const std::uint32_t* count,
+static __global__ void k_red_edges(const uint4* tets, const std::uint32_t* red_list, const std::uint32_t* count,
                             unsigned long long* keys) {
   const std::uint32_t n = *count;
   for (std::uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
@@ -71,13 +71,13 @@ struct PredUniqueKey {
   __device__ bool operator()(std::size_t i) const { return i == 0 || k[i] != k[i - 1]; }
 };
 
-__global__ void k_gather_keys(const unsigned long long* src, const std::uint32_t* idx, const std::uint32_t* count,
+static __global__ void k_gather_keys(const unsigned long long* src, const std::uint32_t* idx, const std::uint32_t* count,
                               unsigned long long* dst) {
   const std::uint32_t n = *count;
   for (std::uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) dst[i] = src[idx[i]];
 }
 
-__global__ void k_touch_nodes(const unsigned long long* S, const std::uint32_t* count, std::uint8_t* touched) {
+static __global__ void k_touch_nodes(const unsigned long long* S, const std::uint32_t* count, std::uint8_t* touched) {
   const std::uint32_t n = *count;
   for (std::uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     touched[static_cast<std::uint32_t>(S[i] >> 32)] = 1;
@@ -86,7 +86,7 @@ __global__ void k_touch_nodes(const unsigned long long* S, const std::uint32_t* 
 }
 
 // Split masks of every tet; non-red tets with an escalating pattern turn red.
-__global__ void k_classify(const uint4* tets, std::size_t nt, std::uint8_t* red, const std::uint8_t* touched,
+static __global__ void k_classify(const uint4* tets, std::size_t nt, std::uint8_t* red, const std::uint8_t* touched,
                            const unsigned long long* S, const std::uint32_t* count, std::uint8_t* mask_out,
                            unsigned* changed) {
   const int m = static_cast<int>(*count);
@@ -114,7 +114,7 @@ __global__ void k_classify(const uint4* tets, std::size_t nt, std::uint8_t* red,
   }
 }
 
-__global__ void k_child_count(const std::uint8_t* mask, std::size_t nt, std::uint32_t* cnt) {
+static __global__ void k_child_count(const std::uint8_t* mask, std::size_t nt, std::uint32_t* cnt) {
   for (std::size_t t = blockIdx.x * static_cast<std::size_t>(blockDim.x) + threadIdx.x; t < nt;
        t += static_cast<std::size_t>(gridDim.x) * blockDim.x) {
     const unsigned m = mask[t];
@@ -123,7 +123,7 @@ __global__ void k_child_count(const std::uint8_t* mask, std::size_t nt, std::uin
   }
 }
 
-__global__ void k_midpoints(const double* nodes, const unsigned long long* S, const std::uint32_t* count,
+static __global__ void k_midpoints(const double* nodes, const unsigned long long* S, const std::uint32_t* count,
                             std::size_t n_old, double* out) {
   const std::uint32_t m = *count;
   for (std::uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
@@ -172,7 +172,7 @@ __device__ __forceinline__ double dist2_d(const double* P, std::uint32_t a, std:
   return s;
 }
 
-__global__ void k_emit_children(const uint4* tets, std::size_t nt, const std::uint8_t* mask, const std::uint32_t* offs,
+static __global__ void k_emit_children(const uint4* tets, std::size_t nt, const std::uint8_t* mask, const std::uint32_t* offs,
                                 const int* labels_in, const unsigned long long* S, const std::uint32_t* count,
                                 std::size_t n_old, const double* P, uint4* out, int* labels_out,
                                 std::uint32_t* parent_out) {

@@ -8,9 +8,7 @@ from paper_2203_10000_b200 import build as b  # noqa: E402
 name, defs = sys.argv[1], sys.argv[2:]
 out = b.LIB / "variants" / f"{name}.so"
 out.parent.mkdir(parents=True, exist_ok=True)
-r = b._run([b.NVCC, *b.ARCH, *b.NVCC_FLAGS, *[f"-D{d}" for d in defs], str(b.CSRC / "nestmesh_label.cu"),
-            str(b.CSRC / "refine.cpp"), "-o", str(out)])
-lines = (r.stdout + r.stderr).splitlines()
+lines = b.compile_label_lib(out, defs).splitlines()
 for i, l in enumerate(lines):
     if "k_labelILi1ELb1ELb0" in l and "Compiling" in l:
         print(name, lines[i + 2].strip(), "|", lines[i + 3].strip())
