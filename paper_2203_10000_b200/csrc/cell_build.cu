@@ -25,6 +25,11 @@ class CellBuild : public CellBuilder {
         st_(st), t0_(std::chrono::steady_clock::now()), tl_(t0_),
         verbose_(std::getenv("NM_CELL_VERBOSE") != nullptr) {}
 
+  ~CellBuild() override {
+    for (cudaEvent_t e : child_ev_)
+      if (e) cudaEventDestroy(e);
+  }
+
   void prepare() override {
     NM_CUDA(cudaSetDevice(c_->opt.device));
     geometry();
@@ -70,6 +75,7 @@ class CellBuild : public CellBuilder {
   std::vector<std::vector<std::int64_t>> run_val_;
   std::unique_ptr<std::int32_t[]> run_of_;
   std::vector<std::vector<FineRun>> fine_;
+  std::vector<cudaEvent_t> child_ev_;  // end of compartment k's child kernel
   std::size_t nreps_ = 0;
   // host work items: z-slabs of kSlab planes of one compartment's grid (in
   // compartment, then z order); every phase's results are merged in item
@@ -250,6 +256,7 @@ class CellBuild : public CellBuilder {
     }
     NM_CUDA(cudaGetLastError());
     cert1_ = uninit<std::uint8_t>(total_);
+    prefault(cert1_.get(), total_);  // page faults on all threads while the kernels run
     if (total_) NM_CUDA(cudaMemcpyAsync(cert1_.get(), cert_d, total_, cudaMemcpyDeviceToHost, st_));
     NM_CUDA(cudaStreamSynchronize(st_));
     lap("l1");
@@ -285,6 +292,7 @@ class CellBuild : public CellBuilder {
     if (!nblk) return;
     up(c_->cell_blk, blk_cells.data(), nblk * sizeof(std::uint32_t));
     auto* ch_d = c_->cell_child.as<std::uint8_t>(nchild_);
+    child_ev_.assign(K, nullptr);
     for (int k = 0; k < K; ++k) {
       const std::size_t nb = boff_[k + 1] - boff_[k];
       if (!nb) continue;
@@ -292,15 +300,44 @@ class CellBuild : public CellBuilder {
           G_[k], static_cast<const std::uint32_t*>(c_->cell_blk.p) + boff_[k], nb, clus_k(k), nclus(k), ctri_k(k),
           tsph_k(k), static_cast<const double*>(c_->xyz64.p), static_cast<const std::uint32_t*>(c_->tri_idx.p), c_->cx,
           c_->cy, c_->cz, ch_d + boff_[k] * nm::kChildren);
+      NM_CUDA(cudaEventCreateWithFlags(&child_ev_[k], cudaEventDisableTiming));
+      NM_CUDA(cudaEventRecord(child_ev_[k], st_));
     }
     NM_CUDA(cudaGetLastError());
-    if (verbose_) {
-      NM_CUDA(cudaStreamSynchronize(st_));
-      lap("l2kern");
-    }
-    NM_CUDA(cudaMemcpyAsync(child_.get(), ch_d, nchild_, cudaMemcpyDeviceToHost, st_));
-    NM_CUDA(cudaStreamSynchronize(st_));
+    prefault(child_.get(), nchild_);
     lap("l2");
+  }
+
+  // children of compartment k, device -> host on a copy stream once its
+  // kernel is done (the later compartments' kernels keep running); ready
+  // counts the compartments whose children are in
+  void copy_children(std::atomic<int>& ready) {
+    NM_CUDA(cudaSetDevice(c_->opt.device));
+    cudaStream_t cp = nullptr;
+    NM_CUDA(cudaStreamCreateWithFlags(&cp, cudaStreamNonBlocking));
+    struct Guard {
+      cudaStream_t s;
+      ~Guard() { cudaStreamDestroy(s); }
+    } guard{cp};
+    const auto* ch_d = static_cast<const std::uint8_t*>(c_->cell_child.p);
+    for (int k = 0; k < K_; ++k) {
+      const std::size_t b0 = boff_[k] * nm::kChildren, bytes = (boff_[k + 1] - boff_[k]) * nm::kChildren;
+      if (bytes) {
+        NM_CUDA(cudaStreamWaitEvent(cp, child_ev_[k], 0));
+        NM_CUDA(cudaMemcpyAsync(child_.get() + b0, ch_d + b0, bytes, cudaMemcpyDeviceToHost, cp));
+        NM_CUDA(cudaStreamSynchronize(cp));
+      }
+      ready.store(k + 1, std::memory_order_release);
+    }
+  }
+
+  // touch every page of a fresh host array on all threads
+  static void prefault(std::uint8_t* p, std::size_t bytes) {
+    constexpr std::size_t kChunk = std::size_t(1) << 22;
+    parallel_for(static_cast<int>((bytes + kChunk - 1) / kChunk), [&](int i) {
+      const std::size_t b = static_cast<std::size_t>(i) * kChunk;
+      std::memset(p + b, 0, std::min(kChunk, bytes - b));
+    });
   }
 
   // ---- runs: every maximal x-run of certified cells gets one winding number ----
@@ -315,7 +352,29 @@ class CellBuild : public CellBuilder {
     const std::size_t ns = slabs_.size();
     std::vector<SlabRuns> part(ns);
     run_of_ = uninit<std::int32_t>(total_);
-    parallel_for(static_cast<int>(ns), [&](int i) { slab_runs(slabs_[i], part[i]); });
+    // slabs are handed out in compartment order: each waits only for its own
+    // compartment's children
+    std::atomic<int> ready{nchild_ ? 0 : K_};
+    std::exception_ptr copy_err;
+    std::thread copier;
+    if (nchild_)
+      copier = std::thread([&] {
+        try {
+          copy_children(ready);
+        } catch (...) {
+          copy_err = std::current_exception();
+          ready.store(K_, std::memory_order_release);
+        }
+      });
+    parallel_for(static_cast<int>(ns), [&](int i) {
+      while (ready.load(std::memory_order_acquire) <= slabs_[i].k) std::this_thread::yield();
+      slab_runs(slabs_[i], part[i]);
+    });
+    if (copier.joinable()) copier.join();
+    for (cudaEvent_t e : child_ev_)
+      if (e) cudaEventDestroy(e);
+    child_ev_.clear();
+    if (copy_err) std::rethrow_exception(copy_err);
     // merge: slab-local run / representative indices -> compartment-local
     std::vector<std::size_t> run_base(ns), rep_base(ns);
     for (int k = 0; k < K_; ++k) {
