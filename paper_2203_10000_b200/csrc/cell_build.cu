@@ -125,33 +125,77 @@ class CellBuild : public CellBuilder {
   }
 
   // ---- geometry: per compartment its grid and Morton-ordered clusters ----
+  // (per compartment: bounds, grid and Morton order; then the cluster and
+  // triangle spheres in chunks of clusters over all threads, written in place)
   void geometry() {
     const int K = K_;
     G_.assign(K, nm::CellGrid{});
     coff_.assign(K + 1, 0);
-    std::vector<std::vector<float4>> clus_kv(K), tsph_kv(K);
-    std::vector<std::vector<std::uint32_t>> ctri_kv(K);
-    parallel_for(K, [&](int k) { compartment_geometry(k, clus_kv[k], ctri_kv[k], tsph_kv[k]); });
-    std::vector<float4> clus, tsph;
-    std::vector<std::uint32_t> ctri;
+    std::vector<std::vector<std::uint32_t>> order(K);
+    parallel_for(K, [&](int k) { compartment_grid(k, order[k]); });
     for (int k = 0; k < K; ++k) {
       G_[k].off = static_cast<std::uint32_t>(total_);
       total_ += cells(k);
       if (total_ > 0xffffffffull) throw Error("certified-cell grids exceed 2^32 cells");
-      coff_[k] = clus.size();
-      clus.insert(clus.end(), clus_kv[k].begin(), clus_kv[k].end());
-      ctri.insert(ctri.end(), ctri_kv[k].begin(), ctri_kv[k].end());
-      tsph.insert(tsph.end(), tsph_kv[k].begin(), tsph_kv[k].end());
+      coff_[k + 1] = coff_[k] + (order[k].size() + nm::kCluster - 1) / nm::kCluster;
     }
-    coff_[K] = clus.size();
+    const std::size_t ncl = coff_[K];
+    std::vector<float4> clus(ncl), tsph(ncl * nm::kCluster);
+    std::vector<std::uint32_t> ctri(ncl * nm::kCluster);
+    constexpr std::size_t kChunk = 256;  // clusters per work item
+    parallel_for(static_cast<int>((ncl + kChunk - 1) / kChunk), [&](int i) {
+      const std::size_t q0 = i * kChunk, q1 = std::min(ncl, q0 + kChunk);
+      int k = static_cast<int>(std::upper_bound(coff_.begin(), coff_.end(), q0) - coff_.begin()) - 1;
+      for (std::size_t q = q0; q < q1; ++q) {
+        while (q >= coff_[k + 1]) ++k;
+        const std::vector<std::uint32_t>& ord = order[k];
+        const std::size_t i0 = (q - coff_[k]) * nm::kCluster, i1 = std::min(ord.size(), i0 + nm::kCluster);
+        clus[q] = sphere(ord.data() + i0, ord.data() + i1);
+        for (std::size_t j = 0; j < nm::kCluster; ++j) {
+          const std::size_t t = i0 + j;
+          ctri[q * nm::kCluster + j] = t < i1 ? ord[t] : 0xffffffffu;
+          tsph[q * nm::kCluster + j] = t < i1 ? sphere(ord.data() + t, ord.data() + t + 1)
+                                             : make_float4(0.f, 0.f, 0.f, -1e30f);
+        }
+      }
+    });
     lap("setup");
     up(c_->clus, clus.data(), clus.size() * sizeof(float4));
     up(c_->clus_tri, ctri.data(), ctri.size() * sizeof(std::uint32_t));
     up(c_->clus_tsph, tsph.data(), tsph.size() * sizeof(float4));
   }
 
-  void compartment_geometry(int k, std::vector<float4>& clus, std::vector<std::uint32_t>& ctri,
-                            std::vector<float4>& tsph) {
+  // bounding sphere of triangles [b, e) in the centred frame: fp32 centre of
+  // the vertex box, radius rounded up with the kernel's margins (1e-6
+  // relative + 1e-5 mm + 4e-6 |centre|)
+  float4 sphere(const std::uint32_t* b, const std::uint32_t* e) const {
+    const double* ctr = ctr_;
+    double blo[3] = {1e300, 1e300, 1e300}, bhi[3] = {-1e300, -1e300, -1e300};
+    for (const std::uint32_t* t = b; t < e; ++t)
+      for (int v = 0; v < 3; ++v)
+        for (int a = 0; a < 3; ++a) {
+          const double x = xyz_[3 * std::size_t(tri_[3 * *t + v]) + a] - ctr[a];
+          blo[a] = std::min(blo[a], x);
+          bhi[a] = std::max(bhi[a], x);
+        }
+    const float fc[3] = {float(0.5 * (blo[0] + bhi[0])), float(0.5 * (blo[1] + bhi[1])),
+                         float(0.5 * (blo[2] + bhi[2]))};
+    double rho = 0.0;
+    for (const std::uint32_t* t = b; t < e; ++t)
+      for (int v = 0; v < 3; ++v) {
+        double d2 = 0.0;
+        for (int a = 0; a < 3; ++a) {
+          const double d = xyz_[3 * std::size_t(tri_[3 * *t + v]) + a] - ctr[a] - double(fc[a]);
+          d2 += d * d;
+        }
+        rho = std::max(rho, std::sqrt(d2));
+      }
+    const double rel = 4e-6 * (std::fabs(fc[0]) + std::fabs(fc[1]) + std::fabs(fc[2]));
+    return make_float4(fc[0], fc[1], fc[2], std::nextafter(float(rho * (1.0 + 1e-6) + 1e-5 + rel), INFINITY));
+  }
+
+  // compartment k: its triangles in Morton order of their centroids and its grid
+  void compartment_grid(int k, std::vector<std::uint32_t>& order) {
     const double* ctr = ctr_;
     const double* xyz = xyz_;
     const std::uint32_t* tri = tri_;
@@ -176,41 +220,8 @@ class CellBuild : public CellBuilder {
         kk.emplace_back(spread10h(q[0]) | (spread10h(q[1]) << 1) | (spread10h(q[2]) << 2), t);
       }
       std::stable_sort(kk.begin(), kk.end(), [](auto& x, auto& y) { return x.first < y.first; });
-      // bounding sphere of triangles kk[i0, i1) in the centred frame: fp32
-      // centre of the vertex box, radius rounded up with the kernel's
-      // margins (1e-6 relative + 1e-5 mm + 4e-6 |centre|)
-      auto sphere = [&](std::size_t i0, std::size_t i1) {
-        double blo[3] = {1e300, 1e300, 1e300}, bhi[3] = {-1e300, -1e300, -1e300};
-        for (std::size_t i = i0; i < i1; ++i)
-          for (int v = 0; v < 3; ++v)
-            for (int a = 0; a < 3; ++a) {
-              const double x = xyz[3 * std::size_t(tri[3 * kk[i].second + v]) + a] - ctr[a];
-              blo[a] = std::min(blo[a], x);
-              bhi[a] = std::max(bhi[a], x);
-            }
-        const float fc[3] = {float(0.5 * (blo[0] + bhi[0])), float(0.5 * (blo[1] + bhi[1])),
-                             float(0.5 * (blo[2] + bhi[2]))};
-        double rho = 0.0;
-        for (std::size_t i = i0; i < i1; ++i)
-          for (int v = 0; v < 3; ++v) {
-            double d2 = 0.0;
-            for (int a = 0; a < 3; ++a) {
-              const double d = xyz[3 * std::size_t(tri[3 * kk[i].second + v]) + a] - ctr[a] - double(fc[a]);
-              d2 += d * d;
-            }
-            rho = std::max(rho, std::sqrt(d2));
-          }
-        const double rel = 4e-6 * (std::fabs(fc[0]) + std::fabs(fc[1]) + std::fabs(fc[2]));
-        return make_float4(fc[0], fc[1], fc[2], std::nextafter(float(rho * (1.0 + 1e-6) + 1e-5 + rel), INFINITY));
-      };
-      for (std::size_t i0 = 0; i0 < kk.size(); i0 += nm::kCluster) {
-        const std::size_t i1 = std::min(kk.size(), i0 + nm::kCluster);
-        clus.push_back(sphere(i0, i1));
-        for (std::size_t i = i0; i < i0 + nm::kCluster; ++i) {
-          ctri.push_back(i < i1 ? kk[i].second : 0xffffffffu);
-          tsph.push_back(i < i1 ? sphere(i, i + 1) : make_float4(0.f, 0.f, 0.f, -1e30f));
-        }
-      }
+      order.resize(kk.size());
+      for (std::size_t i = 0; i < kk.size(); ++i) order[i] = kk[i].second;
       const double ext = std::max({hi[0] - lo[0], hi[1] - lo[1], hi[2] - lo[2]});
       g.B = std::max(ext / NM_CELL_AXIS, 1e-3);
       int n3[3];
