@@ -1,8 +1,16 @@
 // Certified cells (cells.cuh): the per-surface-set build
 // behind nm_options.cull_outside = 2.
+#include <sys/mman.h>
+
 #include "context.cuh"
 
 namespace nmh {
+
+struct FreeDel {
+  void operator()(void* p) const { std::free(p); }
+};
+template <class T>
+using HostArr = std::unique_ptr<T[], FreeDel>;
 
 #ifndef NM_CELL_AXIS
 #define NM_CELL_AXIS 120
@@ -66,14 +74,14 @@ class CellBuild : public CellBuilder {
   std::vector<nm::CellGrid> G_;
   std::vector<std::size_t> coff_;       // first cluster of each compartment
   std::size_t total_ = 0;               // level-1 cells
-  std::unique_ptr<std::uint8_t[]> cert1_;
-  std::unique_ptr<std::uint32_t[]> block_of_;  // local child block of each uncertified cell
+  HostArr<std::uint8_t> cert1_;
+  HostArr<std::uint32_t> block_of_;  // local child block of each uncertified cell
   std::vector<std::size_t> boff_;       // first child block of each compartment
   std::size_t nchild_ = 0;
-  std::unique_ptr<std::uint8_t[]> child_;
+  HostArr<std::uint8_t> child_;
   std::vector<std::vector<double>> reps_;
   std::vector<std::vector<std::int64_t>> run_val_;
-  std::unique_ptr<std::int32_t[]> run_of_;
+  HostArr<std::int32_t> run_of_;
   std::vector<std::vector<FineRun>> fine_;
   std::vector<cudaEvent_t> child_ev_;  // end of compartment k's child kernel
   std::size_t nreps_ = 0;
@@ -94,10 +102,17 @@ class CellBuild : public CellBuilder {
     tl_ = t;
   }
   // host arrays allocated uninitialised: every entry is written (by a copy or
-  // by its compartment's thread) before it is read
+  // by its compartment's thread) before it is read. 2 MiB-aligned and marked
+  // for transparent huge pages: the cfg5 build touches ~300 MB of fresh host
+  // memory, and 4 KiB page faults were a visible share of it
   template <class T>
-  static std::unique_ptr<T[]> uninit(std::size_t m) {
-    return std::unique_ptr<T[]>(new T[std::max<std::size_t>(m, 1)]);
+  static HostArr<T> uninit(std::size_t m) {
+    constexpr std::size_t kHuge = std::size_t(1) << 21;
+    const std::size_t bytes = (std::max<std::size_t>(m, 1) * sizeof(T) + kHuge - 1) / kHuge * kHuge;
+    void* p = std::aligned_alloc(kHuge, bytes);
+    if (!p) throw Error("host allocation failed");
+    madvise(p, bytes, MADV_HUGEPAGE);  // advisory: ignored where THP is off
+    return HostArr<T>(static_cast<T*>(p));
   }
   void up(DBuf& b, const void* src, std::size_t bytes) {
     void* d = b.get(std::max<std::size_t>(bytes, 1));
@@ -268,6 +283,8 @@ class CellBuild : public CellBuilder {
     NM_CUDA(cudaGetLastError());
     cert1_ = uninit<std::uint8_t>(total_);
     prefault(cert1_.get(), total_);  // page faults on all threads while the kernels run
+    block_of_ = uninit<std::uint32_t>(total_);
+    prefault(reinterpret_cast<std::uint8_t*>(block_of_.get()), total_ * sizeof(std::uint32_t));
     if (total_) NM_CUDA(cudaMemcpyAsync(cert1_.get(), cert_d, total_, cudaMemcpyDeviceToHost, st_));
     NM_CUDA(cudaStreamSynchronize(st_));
     lap("l1");
@@ -286,7 +303,6 @@ class CellBuild : public CellBuilder {
     boff_.assign(K + 1, 0);
     for (int k = 0; k <= K; ++k) boff_[k] = sl_off[slab_first_[k]];
     const std::size_t nblk = boff_[K];
-    block_of_ = uninit<std::uint32_t>(total_);
     std::vector<std::uint32_t> blk_cells(std::max<std::size_t>(nblk, 1));
     parallel_for(static_cast<int>(ns), [&](int i) {
       const Slab& sl = slabs_[i];
@@ -316,6 +332,8 @@ class CellBuild : public CellBuilder {
     }
     NM_CUDA(cudaGetLastError());
     prefault(child_.get(), nchild_);
+    run_of_ = uninit<std::int32_t>(total_);
+    prefault(reinterpret_cast<std::uint8_t*>(run_of_.get()), total_ * sizeof(std::int32_t));
     lap("l2");
   }
 
@@ -362,7 +380,7 @@ class CellBuild : public CellBuilder {
   void runs() {
     const std::size_t ns = slabs_.size();
     std::vector<SlabRuns> part(ns);
-    run_of_ = uninit<std::int32_t>(total_);
+    if (!run_of_) run_of_ = uninit<std::int32_t>(total_);
     // slabs are handed out in compartment order: each waits only for its own
     // compartment's children
     std::atomic<int> ready{nchild_ ? 0 : K_};
