@@ -82,7 +82,7 @@ class CellBuild : public CellBuilder {
   std::vector<std::vector<double>> reps_;
   std::vector<std::vector<std::int64_t>> run_val_;
   HostArr<std::int32_t> run_of_;
-  std::vector<std::vector<FineRun>> fine_;
+  std::vector<std::vector<FineRun>> fine_;  // per slab
   std::vector<cudaEvent_t> child_ev_;  // end of compartment k's child kernel
   std::size_t nreps_ = 0;
   // host work items: z-slabs of kSlab planes of one compartment's grid (in
@@ -404,8 +404,10 @@ class CellBuild : public CellBuilder {
       if (e) cudaEventDestroy(e);
     child_ev_.clear();
     if (copy_err) std::rethrow_exception(copy_err);
+    lap("slabs");
     // merge: slab-local run / representative indices -> compartment-local
     std::vector<std::size_t> run_base(ns), rep_base(ns);
+    fine_.assign(ns, {});
     for (int k = 0; k < K_; ++k) {
       std::size_t nr = 0, np = 0;
       for (std::size_t i = slab_first_[k]; i < slab_first_[k + 1]; ++i) {
@@ -426,18 +428,17 @@ class CellBuild : public CellBuilder {
         if (cert1_[q]) run_of_[q] += static_cast<std::int32_t>(run_base[i]);
       for (std::int64_t& v : part[i].run_val) v = rebase(v, i);
       for (FineRun& fr : part[i].fine) fr.v = rebase(fr.v, i);
+      fine_[i] = std::move(part[i].fine);  // fine runs stay per slab (no copy)
     });
     reps_.assign(K_, {});
     run_val_.assign(K_, {});
-    fine_.assign(K_, {});
     parallel_for(K_, [&](int k) {
       for (std::size_t i = slab_first_[k]; i < slab_first_[k + 1]; ++i) {
         reps_[k].insert(reps_[k].end(), part[i].reps.begin(), part[i].reps.end());
         run_val_[k].insert(run_val_[k].end(), part[i].run_val.begin(), part[i].run_val.end());
-        fine_[k].insert(fine_[k].end(), part[i].fine.begin(), part[i].fine.end());
       }
     });
-    lap("runs");
+    lap("merge");
   }
 
   std::int64_t new_rep(SlabRuns& out, double x, double y, double z) {
@@ -549,9 +550,8 @@ class CellBuild : public CellBuilder {
           code[q] = w == kUnknown ? 0u : static_cast<std::uint32_t>(1 + w);
         }
       }
-    });
-    parallel_for(K, [&](int k) {  // fine runs write children of their own compartment only
-      for (const FineRun& fr : fine_[k]) {
+      // the slab's fine runs write children of the slab's own cells
+      for (const FineRun& fr : fine_[i]) {
         const std::int64_t w = value(k, fr.v);
         if (w == kUnknown) continue;
         for (int f = fr.fx0; f <= fr.fx1; ++f) child_at(k, fr.row, f, fr.sy, fr.sz) = static_cast<std::uint8_t>(1 + w);
