@@ -94,6 +94,7 @@ class CellBuild : public CellBuilder {
   };
   std::vector<Slab> slabs_;
   std::vector<std::size_t> slab_first_;  // first slab of each compartment (K + 1)
+  std::vector<std::size_t> slab_blk_;    // first child block of each slab (ns + 1)
 
   void lap(const char* what) {
     if (!verbose_) return;
@@ -298,7 +299,8 @@ class CellBuild : public CellBuilder {
       for (std::size_t q = slab_begin(slabs_[i]); q < slab_end(slabs_[i]); ++q) m += !cert1_[q];
       sl_cnt[i] = m;
     });
-    std::vector<std::size_t> sl_off(ns + 1, 0);  // global first block of each slab
+    slab_blk_.assign(ns + 1, 0);  // global first block of each slab
+    std::vector<std::size_t>& sl_off = slab_blk_;
     for (std::size_t i = 0; i < ns; ++i) sl_off[i + 1] = sl_off[i] + sl_cnt[i];
     boff_.assign(K + 1, 0);
     for (int k = 0; k <= K; ++k) boff_[k] = sl_off[slab_first_[k]];
@@ -537,7 +539,15 @@ class CellBuild : public CellBuilder {
       }
       return v;
     };
+    // per slab: level-1 codes, its child blocks zeroed and written by its fine
+    // runs, both uploaded right away (other slabs are still being coded) and
+    // the certified cells counted
+    auto* state_d = c_->cell_state.as<std::uint32_t>(std::max<std::size_t>(total_, 1));
+    auto* child_d = static_cast<std::uint8_t*>(c_->cell_child.get(std::max<std::size_t>(nchild_, 1)));
+    std::vector<std::size_t> ncert(slabs_.size(), 0);
+    std::vector<cudaError_t> cp_err(slabs_.size(), cudaSuccess);
     parallel_for(static_cast<int>(slabs_.size()), [&](int i) {
+      cp_err[i] = cudaSetDevice(c_->opt.device);  // (f must not throw: errors are collected)
       const Slab& sl = slabs_[i];
       const int k = sl.k;
       for (std::size_t q = slab_begin(sl); q < slab_end(sl); ++q) {
@@ -556,17 +566,25 @@ class CellBuild : public CellBuilder {
         if (w == kUnknown) continue;
         for (int f = fr.fx0; f <= fr.fx1; ++f) child_at(k, fr.row, f, fr.sy, fr.sz) = static_cast<std::uint8_t>(1 + w);
       }
+      const std::size_t q0 = slab_begin(sl), q1 = slab_end(sl);
+      const std::size_t c0 = nchild_ ? slab_blk_[i] * nm::kChildren : 0, c1 = nchild_ ? slab_blk_[i + 1] * nm::kChildren : 0;
+      if (q1 > q0 && cp_err[i] == cudaSuccess)
+        cp_err[i] = cudaMemcpyAsync(state_d + q0, code.get() + q0, (q1 - q0) * sizeof(std::uint32_t),
+                                    cudaMemcpyHostToDevice, st_);
+      if (c1 > c0 && cp_err[i] == cudaSuccess)
+        cp_err[i] = cudaMemcpyAsync(child_d + c0, child_.get() + c0, c1 - c0, cudaMemcpyHostToDevice, st_);
+      std::size_t m = 0;
+      for (std::size_t q = q0; q < q1; ++q) m += code[q] == 1 || code[q] == 2;
+      for (std::size_t q = c0; q < c1; ++q) m += child_[q] != 0;
+      ncert[i] = m;
     });
+    for (cudaError_t e : cp_err) NM_CUDA(e);
     lap("codes");
-    up(c_->cell_state, code.get(), total_ * sizeof(std::uint32_t));
-    up(c_->cell_child, child_.get(), nchild_);
     up(c_->cell_grids, G_.data(), G_.size() * sizeof(nm::CellGrid));
     NM_CUDA(cudaStreamSynchronize(st_));
     lap("final");
     c_->cells_total = total_ + nchild_;
-    c_->cells_certified = 0;
-    for (std::size_t q = 0; q < total_; ++q) c_->cells_certified += code[q] == 1 || code[q] == 2;
-    for (std::size_t q = 0; q < nchild_; ++q) c_->cells_certified += child_[q] != 0;
+    c_->cells_certified = std::accumulate(ncert.begin(), ncert.end(), std::size_t(0));
     c_->cell_reps = nreps_;
     c_->cells = true;
     c_->ms_cells = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0_).count();
