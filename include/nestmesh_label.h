@@ -47,7 +47,7 @@
 extern "C" {
 #endif
 
-#define NM_ABI_VERSION 1
+#define NM_ABI_VERSION 2
 
 typedef struct nm_ctx nm_ctx;
 
@@ -69,6 +69,10 @@ typedef struct nm_options {
                             certified cell of the compartment's grid (a cell whose ball meets no
                             triangle; grid built by nm_set_surfaces from the surfaces alone) gets the
                             cell's exact winding number (0 or 1); 0 (default): every pair is evaluated */
+  int cell_axis;         /* certified-cell grid resolution: cells along each compartment's longest bounding-box
+                            side, in [8, 1024]; 0 = default (120). A finer grid takes longer to build in
+                            nm_set_surfaces and leaves fewer pairs to evaluate per pass (performance only:
+                            results are identical) */
 } nm_options;
 
 /* Counters of one labeling call (accumulated by the call, not across calls). */

@@ -37,6 +37,7 @@ class NmOptions(ctypes.Structure):
         ("pairs_per_thread", ctypes.c_int),
         ("layout", ctypes.c_int),
         ("cull_outside", ctypes.c_int),
+        ("cell_axis", ctypes.c_int),
     ]
 
 

@@ -12,9 +12,6 @@ struct FreeDel {
 template <class T>
 using HostArr = std::unique_ptr<T[], FreeDel>;
 
-#ifndef NM_CELL_AXIS
-#define NM_CELL_AXIS 120
-#endif
 // Certified cells of every compartment (cells.cuh), built once per surface
 // set from the surfaces alone, in four phases: geometry (grids + clusters),
 // certification (level-1 cells and children, on the device), runs (x-runs of
@@ -239,7 +236,7 @@ class CellBuild : public CellBuilder {
       order.resize(kk.size());
       for (std::size_t i = 0; i < kk.size(); ++i) order[i] = kk[i].second;
       const double ext = std::max({hi[0] - lo[0], hi[1] - lo[1], hi[2] - lo[2]});
-      g.B = std::max(ext / NM_CELL_AXIS, 1e-3);
+      g.B = std::max(ext / c_->opt.cell_axis, 1e-3);
       int n3[3];
       for (int a = 0; a < 3; ++a) n3[a] = static_cast<int>(std::ceil((hi[a] - lo[a]) / g.B)) + 2;
       g.ox = lo[0] - g.B;

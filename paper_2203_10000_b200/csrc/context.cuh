@@ -33,6 +33,9 @@
 
 namespace nmh {
 
+// certified-cell grid: cells along each compartment's longest side (nm_options.cell_axis = 0)
+constexpr int kDefaultCellAxis = 120;
+
 
 // thread-local message of the last failed C ABI call (nm_last_error)
 inline std::string& last_error() {

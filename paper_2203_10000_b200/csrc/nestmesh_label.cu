@@ -537,6 +537,7 @@ void nm_default_options(nm_options* o) {
   o->pairs_per_thread = 1;
   o->layout = 0;
   o->cull_outside = 0;
+  o->cell_axis = kDefaultCellAxis;
 }
 
 int nm_create(nm_ctx** out, const nm_options* opt) {
@@ -555,6 +556,8 @@ int nm_create(nm_ctx** out, const nm_options* opt) {
       if (c->opt.device < 0 || c->opt.device >= ndev) throw Error("device ordinal out of range");
       if (c->opt.pairs_per_thread != 1 && c->opt.pairs_per_thread != 2) throw Error("pairs_per_thread must be 1 or 2");
       if (c->opt.layout < 0 || c->opt.layout > 2) throw Error("layout must be 0 (auto), 1 (triangles) or 2 (strips)");
+      if (c->opt.cell_axis == 0) c->opt.cell_axis = kDefaultCellAxis;
+      if (c->opt.cell_axis < 8 || c->opt.cell_axis > 1024) throw Error("cell_axis must be 0 (default) or in [8, 1024]");
       NM_CUDA(cudaSetDevice(c->opt.device));
       cudaDeviceProp p;
       NM_CUDA(cudaGetDeviceProperties(&p, c->opt.device));

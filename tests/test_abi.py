@@ -32,7 +32,7 @@ def test_header_symbols_exported():
 def test_python_binding_mirrors_header():
     assert set(_native.LABEL_API) == header_functions()
     lib = _native.load_label_lib()
-    assert lib.nm_abi_version() == 1
+    assert lib.nm_abi_version() == 2
 
 
 def test_sm100a_code_present():
@@ -45,6 +45,7 @@ def test_sm100a_code_present():
 def test_default_options():
     o = _native.default_options()
     assert o.device == 0 and abs(o.tau - 1e-2) < 1e-9 and abs(o.band - 1e-3) < 1e-15 and o.sort_points == 1
+    assert o.cull_outside == 0 and o.cell_axis == 120
 
 
 def test_no_cpu_fallback_without_device(has_gpu):
@@ -72,7 +73,7 @@ def test_cpp_dropin_header_compiles(tmp_path):
     if not ref_inc.exists():
         pytest.skip("reference headers not present on this machine")
     src = tmp_path / "t.cpp"
-    src.write_text('#include "nestmesh/labeling.hpp"\nint main() { return nestmesh::labeling_abi_version() == 1 ? 0 : 1; }\n')
+    src.write_text('#include "nestmesh/labeling.hpp"\nint main() { return nestmesh::labeling_abi_version() == 2 ? 0 : 1; }\n')
     r = subprocess.run(["g++", "-std=c++20", "-Wall", "-Wextra", "-Werror", f"-I{ref_inc}", f"-I{ROOT / 'include'}",
                         str(src), "-o", str(tmp_path / "t"), f"-L{_native.LIB_DIR}", "-lnestmesh_label",
                         f"-Wl,-rpath,{_native.LIB_DIR}"], capture_output=True, text=True)

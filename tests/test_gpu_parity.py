@@ -515,6 +515,36 @@ def test_cell_culling_exact(cfg_id, lo, hi):
     np.testing.assert_allclose(s_cell[pick][sel], s_ref[sel], rtol=0, atol=1e-9)
 
 
+def test_cell_axis_changes_cost_not_results():
+    """nm_options.cell_axis (certified-cell grid resolution) is performance
+    only: coarser and finer grids certify different cells but give the same
+    masks and the same s on every evaluated pair; out-of-range values fail."""
+    from paper_2203_10000_b200._native import Context, NativeError
+    cfg = synth.config(2)
+    S = cfg.surfaces
+    nodes = cfg.lattice_nodes()[::3]
+    with Context(0) as full:
+        full.set_surfaces(S.xyz, S.tri, S.comp_off, S.label_ids)
+        m_full, _ = full.label_nodes(nodes)
+        s_full, _ = full.enclosure(nodes)
+    infos = {}
+    for axis in (48, 200):
+        with Context(0, cull_outside=2, cell_axis=axis) as c:
+            c.set_surfaces(S.xyz, S.tri, S.comp_off, S.label_ids)
+            m, _ = c.label_nodes(nodes)
+            s, _ = c.enclosure(nodes)
+            infos[axis] = c.cell_info()
+        np.testing.assert_array_equal(m, m_full)
+        diff = s != s_full
+        assert np.all((s[diff] == 0.0) | (s[diff] == 1.0))
+        assert np.max(np.abs(s_full[diff] - s[diff]), initial=0.0) < 1e-5
+    assert infos[200]["cells"] > infos[48]["cells"]
+    assert infos[200]["last_pairs"] < infos[48]["last_pairs"]
+    for bad in (4, 5000):
+        with pytest.raises(NativeError, match="cell_axis"):
+            Context(0, cull_outside=2, cell_axis=bad)
+
+
 def test_cfg5_full_size_properties():
     """BASELINE configs[4] at full size (10,077,696 nodes x 983,040 triangles):
     size-independent properties over every node, the fp64 oracle on a seeded
