@@ -236,7 +236,11 @@ __device__ __forceinline__ void seg_far(const float4* __restrict__ rec, const Pa
       const float2 sbc = add2(rb[q], rc);  // v
       const float2 sac = add2(ra[q], rc);  // w
       const float2 x = fma2(sab[q], sbc, bc(cg));  // u v - gamma
-      const float2 den = fma2(x, sac, fma2(bc(ca), sab[q], mul2(bc(cb), sbc)));  // 2 den
+      // x w first, then the two broadcast terms: no FFMA2 here reads three
+      // register pairs (those issue at ~65 % of the pipe rate against ~90 %
+      // with a broadcast operand, profiles/r01/probe_ffma2_banks.txt);
+      // +1.0 % cfg5, +1.2 % cfg3 (profiles/r01/den_bcast_ab.txt)
+      const float2 den = fma2(bc(cb), sbc, fma2(bc(ca), sab[q], mul2(x, sac)));  // 2 den
       const float2 num = fma2(bc(T.x), f[q].mx, fma2(bc(T.y), f[q].my, fma2(bc(T.z), f[q].mz, bc(T.w))));  // 2 num
       if (k & 1) {
         const float2 D = fma2(d0[q], den, mul2(make_float2(-n0[q].x, -n0[q].y), num));
