@@ -243,8 +243,10 @@ __device__ __forceinline__ void seg_far(const float4* __restrict__ rec, const Pa
       const float2 den = fma2(bc(cb), sbc, fma2(bc(ca), sab[q], mul2(x, sac)));  // 2 den
       const float2 num = fma2(bc(T.x), f[q].mx, fma2(bc(T.y), f[q].my, fma2(bc(T.z), f[q].mz, bc(T.w))));  // 2 num
       if (k & 1) {
+        // den and num sit in the same operand slot of both products, so the
+        // operand reuse cache can serve them (+0.5 %, profiles/r01/cprod_order_ab.txt)
         const float2 D = fma2(d0[q], den, mul2(make_float2(-n0[q].x, -n0[q].y), num));
-        const float2 N = fma2(n0[q], den, mul2(num, d0[q]));
+        const float2 N = fma2(n0[q], den, mul2(d0[q], num));
         acc[q] = atan_far3(acc[q], N, D);
       } else {
         n0[q] = num;
