@@ -13,7 +13,8 @@ fix-up -> NCCL all-gather of node masks (N > 1) -> tet labels.
   e2e        same metric through the public host-buffer API (nm_label_mesh at
              N = 1; pinned host shards + H2D + label + D2H per rank at N > 1)
   roofline   the solid-angle kernel (k_label) against the FP32-pipe roofline
-             148 SMs x 128 lanes x 1.965 GHz / 57 ops per eval
+             148 SMs x 128 lanes x 1.965 GHz: achieved = evals/s x the FP32
+             lane-ops per eval ncu counted on this build (stamped capture)
   cpu_baseline  the fp64 oracle (oracle/, a port of SPEC.md:225-237) on a
              seeded node sample with every host thread (rank 0, N = 1 only)
 
@@ -39,19 +40,26 @@ sys.path.insert(0, str(ROOT))
 
 METRIC = "point-triangle solid-angle evals/sec and full-mesh labeling time at 1/2/4/8 B200"
 UNIT = "evals/s"
-OPS_PER_EVAL = 57                      # pinned FP32-pipe cost of one VOS eval
-ISSUED_OPS_PER_EVAL = 18.625           # FP32 lane-ops the strip far evaluator issues per eval (SASS),
-SEG_FFMA2, CONT_SAVED_FFMA2 = 149, 9   # per 8-triangle segment and point pair; saved when it continues its strip
+OPS_PER_EVAL = 57                      # canonical VOS cost (FP32-pipe ops per eval), for canonical_speedup
+# FP32-pipe lane-ops the headline kernel issues per evaluation, MEASURED: ncu
+# per-opcode thread-instruction counts of one k_label launch of the same build
+# (scripts/ncu_opcounts.sh -> scripts/summarize_ncu.py opcounts), stamped with
+# the SASS hash of k_label<1,true,0>; a capture of another build is refused.
+OPCOUNT_FILE = ROOT / "profiles" / "r02" / "k_label_opcounts_cfg5.json"
+TRAFFIC_FILE = ROOT / "profiles" / "r02" / "k_label_traffic_cfg5.json"
 
 
-def issued_ops_per_eval(sinfo):
-    """FP32 lane-ops per eval of the far evaluator on this surface layout:
-    149 packed ops per segment (16 evals), 9 fewer for a segment that
-    continues the previous one of its strip."""
-    if sinfo["layout"] != "strips":
-        return 40.0
-    segs, cont = max(1, sinfo["segments"]), sinfo["continued_segments"]
-    return (SEG_FFMA2 * segs - CONT_SAVED_FFMA2 * cont) * 2.0 / (16.0 * segs)
+def stamped(path, sass):
+    """A committed ncu summary, only when it was captured on this build."""
+    try:
+        d = json.loads(path.read_text())
+    except Exception:
+        return None, f"{path.name} missing"
+    if sass is None:
+        return None, "cuobjdump unavailable: build hash unknown"
+    if d.get("sass_sha16") != sass:
+        return None, f"{path.name} was captured on build {d.get('sass_sha16')}, this build is {sass}"
+    return d, None
 FP32_LANES_PER_SM = 128
 MY_KERNELS_PER_STEP = 7                # morton keys, k_label, 3x select, k_fixup, k_label_tets
 CUB_KERNELS = 4                        # library radix-sort kernels counted in nm_stats.launches
@@ -565,27 +573,38 @@ def main():
         sm_max = float(peaks.get("sm_max_mhz", 1965.0))
         import torch as _t
         sms = _t.cuda.get_device_properties(local).multi_processor_count
-        peak = sms * FP32_LANES_PER_SM * sm_max * 1e6 / OPS_PER_EVAL
-        traffic = None
-        tf = ROOT / "profiles" / "r01" / "k_label_traffic_cfg5.json"
-        if args.config == 5 and layout == "strips" and tf.exists():
-            traffic = json.loads(tf.read_text())["traffic_bytes"]  # ncu dram bytes of one k_label launch (per launch)
+        lane_peak = sms * FP32_LANES_PER_SM * sm_max * 1e6          # FP32 lane-ops/s of the whole GPU
+        sys.path.insert(0, str(ROOT / "scripts"))
+        from kernel_hash import sass_hash
+        sass = sass_hash()
+        ops, ops_why = stamped(OPCOUNT_FILE, sass)
+        tr, tr_why = stamped(TRAFFIC_FILE, sass)
+        strips = layout == "strips"
+        ops_pe = ops["fp32_lane_ops_per_eval"] if (ops and strips and args.config == 5) else None
+        traffic = tr["traffic_bytes"] * (nsh.size / tr["points"]) if (tr and strips and args.config == 5) else None
         roof = {
-            "bound": "fp32", "kernel": f"k_label<1,{1 if layout == 'strips' else 0}> (fp32x2 VOS tile loop, {layout} layout)", "achieved": achieved, "peak": peak,
-            "unit": "evals/s", "frac": achieved / peak, "traffic": traffic,
-            "traffic_note": "bytes per k_label launch from profiles/r01/k_label_traffic_cfg5.json (ncu dram__bytes_read+write)",
-            "peak_basis": f"{sms} SMs x {FP32_LANES_PER_SM} FP32 lanes x {sm_max:.0f} MHz (MEASURED_PEAKS.json sm_max_mhz)"
-                          f" / {OPS_PER_EVAL} FP32-pipe ops per eval (SURVEY.md §8d); per GPU",
+            "bound": "fp32", "kernel": f"k_label<1,{1 if strips else 0},0> (fp32x2 VOS tile loop, {layout} layout)",
+            "achieved": achieved * ops_pe if ops_pe else None,
+            "peak": lane_peak, "unit": "FP32 lane-ops/s",
+            "frac": achieved * ops_pe / lane_peak if ops_pe else None,
+            "traffic": traffic,
+            "algorithmic_bytes": nsh.size * (24 + 8),
+            "peak_basis": f"{sms} SMs x {FP32_LANES_PER_SM} FP32 lanes x {sm_max:.0f} MHz (MEASURED_PEAKS.json sm_max_mhz)",
+            "evals_per_s": achieved,
+            "fp32_lane_ops_per_eval": ops_pe,
+            "ops_source": (f"{OPCOUNT_FILE.relative_to(ROOT)}: ncu sass__thread_inst_executed_true_per_opcode of one "
+                           f"k_label launch on this build (sass {sass}), 2 x FFMA2/FADD2/FMUL2 + FFMA/FADD/FMUL"
+                           if ops_pe else f"unavailable ({ops_why})"),
+            "traffic_source": (f"{TRAFFIC_FILE.relative_to(ROOT)}: ncu dram__bytes_read.sum + dram__bytes_write.sum of "
+                               f"one full-mesh k_label launch on this build" if traffic else f"unavailable ({tr_why})"),
             "kernel_ms_avg": k_ms, "kernel_share_of_step": k_ms / (sum(step_ms) / len(step_ms)),
-            # the same kernel against the FP32 ops it actually issues per eval
-            # (far evaluator: 18.625 lane-ops per eval, less for continued strip segments)
-            "issued_fp32_ops_per_eval": issued_ops_per_eval(sinfo),
+            # the canonical formula's throughput (57 FP32 ops + 5 MUFU per eval), for
+            # comparison with the paper-style count; NOT a roofline fraction
+            "canonical_speedup": achieved / (lane_peak / OPS_PER_EVAL),
             "continued_segments": f"{sinfo.get('continued_segments', 0)} of {sinfo.get('segments', 0)}",
-            "frac_of_issued_fp32_bound": achieved / (sms * FP32_LANES_PER_SM * sm_max * 1e6 /
-                                                     issued_ops_per_eval(sinfo)),
         }
-        if clocks.get("sm_mhz"):
-            roof["frac_at_measured_clock"] = achieved / (sms * FP32_LANES_PER_SM * clocks["sm_mhz"] * 1e6 / OPS_PER_EVAL)
+        if clocks.get("sm_mhz") and ops_pe:
+            roof["frac_at_measured_clock"] = achieved * ops_pe / (sms * FP32_LANES_PER_SM * clocks["sm_mhz"] * 1e6)
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",

@@ -181,3 +181,56 @@ def point_surface_distance(pts, xyz, tri, workers=0):
 def lhuilier(p, a, b, c):
     arr = [np.ascontiguousarray(x, np.float64) for x in (p, a, b, c)]
     return lib().oracle_lhuilier_solid_angle(*[_p(x, ctypes.c_double) for x in arr])
+
+
+REFINE_LIB = HERE / "build" / "librefine_oracle.so"
+_rlib = None
+
+
+def _refine_lib():
+    global _rlib
+    if _rlib is None:
+        if not REFINE_LIB.exists():
+            raise ImportError(f"{REFINE_LIB} missing: run `make -C oracle`")
+        L = ctypes.CDLL(str(REFINE_LIB))
+        L.oracle_refine.argtypes = [_d, _sz, _u32, _sz, _i32, _u32, _sz]
+        L.oracle_refine.restype = ctypes.c_void_p
+        L.oracle_refine_sizes.argtypes = [ctypes.c_void_p, ctypes.POINTER(_sz), ctypes.POINTER(_sz)]
+        L.oracle_refine_copy.argtypes = [ctypes.c_void_p, _d, _u32, _i32, _u32]
+        L.oracle_refine_free.argtypes = [ctypes.c_void_p]
+        L.oracle_refine_last_error.restype = ctypes.c_char_p
+        _rlib = L
+    return _rlib
+
+
+def refine_volume(nodes, tets, labels, selected):
+    """refine_volume restatement (oracle/refine_oracle.cpp, SPEC.md:285-293,
+    311-312, 321): returns nodes, tets, labels, parent (children in an
+    oracle-chosen order inside each parent; compare with canonical_children)."""
+    L = _refine_lib()
+    nodes = np.ascontiguousarray(nodes, np.float64).reshape(-1, 3)
+    tets = np.ascontiguousarray(tets, np.uint32).reshape(-1, 4)
+    lab = None if labels is None else np.ascontiguousarray(labels, np.int32)
+    sel = np.ascontiguousarray(np.asarray(selected, np.uint32).reshape(-1))
+    h = L.oracle_refine(_p(nodes, ctypes.c_double), nodes.shape[0], _p(tets, ctypes.c_uint32), tets.shape[0],
+                        _p(lab, ctypes.c_int), _p(sel, ctypes.c_uint32), sel.size)
+    if not h:
+        raise ValueError(L.oracle_refine_last_error().decode())
+    nn, nt = _sz(), _sz()
+    L.oracle_refine_sizes(h, ctypes.byref(nn), ctypes.byref(nt))
+    on = np.empty((nn.value, 3), np.float64)
+    ot = np.empty((nt.value, 4), np.uint32)
+    ol = np.empty(nt.value, np.int32)
+    op = np.empty(nt.value, np.uint32)
+    L.oracle_refine_copy(h, _p(on, ctypes.c_double), _p(ot, ctypes.c_uint32), _p(ol, ctypes.c_int),
+                         _p(op, ctypes.c_uint32))
+    L.oracle_refine_free(h)
+    return on, ot, ol, op
+
+
+def canonical_children(tets, labels, parent):
+    """Children as a sorted table of (parent, sorted node ids, label): the
+    comparison key for refinements whose within-parent child order differs."""
+    t = np.sort(np.asarray(tets, np.int64).reshape(-1, 4), axis=1)
+    rows = np.column_stack([np.asarray(parent, np.int64), t, np.asarray(labels, np.int64)])
+    return rows[np.lexsort(rows.T[::-1])]

@@ -610,7 +610,6 @@ class CellBuild : public CellBuilder {
     prm.order = nullptr;
     prm.tri = static_cast<const float4*>(c_->tri.p);
     prm.sub = static_cast<const float4*>(c_->sub.p);
-    prm.edges = static_cast<const float4*>(c_->edges.p);
     prm.cont = static_cast<const std::uint32_t*>(c_->cont.p);
     prm.comp_tiles = static_cast<const std::uint32_t*>(c_->comp_tiles.p);
     prm.K = K;

@@ -142,6 +142,7 @@ struct nm_ctx {
   cudaEvent_t ev[6] = {};
   cudaEvent_t ev_side = nullptr;
   std::uint32_t* h_word = nullptr;        // pinned: max tet node index read back from the side stream
+  std::uint32_t* h_pcnt = nullptr;        // pinned: per-compartment flagged-pair counts of the fix-up (32)
   std::uint64_t node_launches = 0;        // launches of the last label_nodes_dev
   int sm_count = 0;
 
@@ -156,7 +157,8 @@ struct nm_ctx {
   nm::LabelIds ids{};
   std::vector<std::uint32_t> comp_tiles_h;  // host copy of the K+1 tile offsets
   std::size_t n_continued = 0;              // strip segments continuing the previous one (cont bits set)
-  nmh::DBuf tri, sub, edges, cont, comp_tiles, xyz64, tri_idx, comp_off, comp_box, cullmask;
+  double snap_grid = 0.0;                   // vertex snapping grid of the fp32 subtile frames (mm, power of two)
+  nmh::DBuf tri, sub, cont, comp_tiles, xyz64, tri_idx, tri64, comp_off, comp_box, cullmask;
   // certified cells (cull_outside = 2, cells.cuh)
   bool cells = false;
   nmh::DBuf dist_clus, dist_slot, dist_ord, sp_part, sp_det, cell_state, cell_child, cell_cert, cell_blk, cell_grids, clus, clus_tri, clus_tsph, unk, sp_list, sp_chunk, sp_cnt, rep_pts, rep_s, rep_m, rep_f;
@@ -169,22 +171,23 @@ struct nm_ctx {
       dist_idx, dist_d32, dist_out, r_red, r_keys, r_keys2, r_S, r_idx, r_touched,
       r_mask, r_cnt, r_offs, r_flag, meshA_nodes, meshA_tets, meshA_labels, meshB_nodes, meshB_tets, meshB_labels,
       meshB_parent, masks2, order, keys, keys_alt, order_alt, cub_tmp, list, chunk, counters, count, tets, labels,
-      s_out, word;
+      s_out, word, pair_cnt, pairs;
 
   ~nm_ctx() {
     for (nmh::DBuf* b : {&dist_clus, &dist_slot, &dist_ord, &sp_part, &sp_det, &cell_state, &cell_child, &cell_cert, &cell_blk, &cell_grids, &clus, &clus_tri, &clus_tsph, &unk, &sp_list, &sp_chunk, &sp_cnt, &rep_pts, &rep_s,
                     &rep_m, &rep_f})
       b->release();
-    for (nmh::DBuf* b : {&tri, &sub, &edges, &cont, &comp_tiles, &xyz64, &tri_idx, &comp_off, &comp_box, &cullmask, &pts, &masks, &flagmask, &nbr, &known, &want, &fkeys, &frontier, &lex, &region, &bfaces, &btri,
+    for (nmh::DBuf* b : {&tri, &sub, &cont, &comp_tiles, &xyz64, &tri_idx, &tri64, &comp_off, &comp_box, &cullmask, &pts, &masks, &flagmask, &nbr, &known, &want, &fkeys, &frontier, &lex, &region, &bfaces, &btri,
                     &dist_tri, &dist_xyz, &dist_idx, &dist_d32, &dist_out, &r_red, &r_keys, &r_keys2, &r_S,
                     &r_idx, &r_touched, &r_mask, &r_cnt, &r_offs, &r_flag, &meshA_nodes, &meshA_tets, &meshA_labels,
                     &meshB_nodes, &meshB_tets, &meshB_labels, &meshB_parent, &masks2, &order, &keys,
-                    &keys_alt, &order_alt, &cub_tmp, &list, &chunk, &counters, &count, &tets, &labels, &s_out, &word})
+                    &keys_alt, &order_alt, &cub_tmp, &list, &chunk, &counters, &count, &tets, &labels, &s_out, &word, &pair_cnt, &pairs})
       b->release();
     for (auto& e : ev)
       if (e) cudaEventDestroy(e);
     if (ev_side) cudaEventDestroy(ev_side);
     if (h_word) cudaFreeHost(h_word);
+    if (h_pcnt) cudaFreeHost(h_pcnt);
     if (side) cudaStreamDestroy(side);
     if (stream) cudaStreamDestroy(stream);
   }

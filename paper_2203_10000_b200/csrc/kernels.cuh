@@ -102,13 +102,23 @@ struct LabelIds {
   int id[32];
 };
 
+// Label ids staged in shared memory: a dynamically indexed kernel-parameter
+// array would be copied to every thread's local stack (128 B per thread).
+__device__ __forceinline__ const int* stage_ids(const LabelIds& ids, int* s_ids) {
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < 32; ++k) s_ids[k] = ids.id[k];  // constant indices: read straight from the parameter bank
+  }
+  __syncthreads();
+  return s_ids;
+}
+
 struct LabelParams {
   const double* pts;         // fp64 xyz, original frame
   std::size_t n;
   const std::uint32_t* order;  // evaluation order (Morton); nullptr = identity
   const float4* tri;         // soup: 3 float4 per triangle (a.xyz,N.x) (b.xyz,N.y) (c.xyz,N.z);
                              // strip: kSegF4 float4 per 8-triangle segment (vos.cuh)
-  const float4* edges;       // strip layout: kEdgeF4 float4 of -|e|^2 per segment (near evaluator)
   const std::uint32_t* cont;  // strip layout: per tile, bit sidx * kGroups + j = segment j of subtile
                               // sidx continues segment j - 1 (same strip)
   const float4* sub;         // per subtile: fp32 centre c (centred frame), w = (far radius)^2;
@@ -380,9 +390,13 @@ static __global__ void __launch_bounds__(kBlock, (NP == 1 ? NM_MIN_BLOCKS : NM_M
                   dn[k] = false;
                   use[k] = valid[k] && !gf[k];
                 }
-                const float4* erec =
-                    prm.edges + ((static_cast<std::size_t>(tile) * kSubPerTile + st) * kGroups + g) * kEdgeF4;
-                seg_near<NP>(rec, erec, f, an, dn, use, prm.tau, prm.delta);
+                NearFrame nf[NP];
+                {
+                  const float4 sc = s_sub[st * kSubRec];
+#pragma unroll
+                  for (int q = 0; q < NP; ++q) nf[q] = near_frame(hx[q], hy[q], hz[q], lx[q], ly[q], lz[q], sc);
+                }
+                seg_near<NP>(rec, nf, an, dn, use, prm.tau, prm.delta);
                 chain = false;
                 if (__any_sync(kFull, any)) {
                   float2 af[NP];
@@ -404,8 +418,9 @@ static __global__ void __launch_bounds__(kBlock, (NP == 1 ? NM_MIN_BLOCKS : NM_M
             }
           }
         } else {
-          // triangle-soup layout: warp-uniform decision; far and near paths
-          // share vos_terms2, so a pair's value does not depend on the path
+          // triangle-soup layout: warp-uniform loop choice, per-lane
+          // evaluator (the lane's own subtile test), so a pair's value does
+          // not depend on its warp mates
           if (__all_sync(kFull, far)) {
             n_far += kSub / 8;
 #pragma unroll 4
@@ -419,6 +434,11 @@ static __global__ void __launch_bounds__(kBlock, (NP == 1 ? NM_MIN_BLOCKS : NM_M
             }
           } else {
             n_near += kSub / 8;
+            // far lanes keep the far-form terms (bit-identical to an all-far
+            // warp); near lanes use the exact double-single frame
+            NearFrame nf[NP];
+#pragma unroll
+            for (int q = 0; q < NP; ++q) nf[q] = near_frame(hx[q], hy[q], hz[q], lx[q], ly[q], lz[q], sb);
 #pragma unroll 1
             for (int t = 0; t < kSub; ++t) {
               const float4 A = tt[3 * t], B = tt[3 * t + 1], C = tt[3 * t + 2];
@@ -426,10 +446,18 @@ static __global__ void __launch_bounds__(kBlock, (NP == 1 ? NM_MIN_BLOCKS : NM_M
               for (int q = 0; q < NP; ++q) {
                 const VosTerms2 v = vos_terms2(A, B, C, mx[q], my[q], mz[q]);
                 const float2 af = acc_far2(acc[q], v.num, v.den);
-                acc[q].x = acc_near_lane(acc[q].x, af.x, v.num.x, v.den.x, v.r1.x, v.r2.x, v.r3.x, prm.tau, prm.delta,
-                                         det[2 * q]);
-                acc[q].y = acc_near_lane(acc[q].y, af.y, v.num.y, v.den.y, v.r1.y, v.r2.y, v.r3.y, prm.tau, prm.delta,
-                                         det[2 * q + 1]);
+                const float2 m3[3] = {nf[q].mx, nf[q].my, nf[q].mz}, l3[3] = {nf[q].lx, nf[q].ly, nf[q].lz};
+                const VosTerms2 w = vos_terms2x(A, B, C, m3, l3);
+                const float2 aw = acc_far2(acc[q], w.num, w.den);
+                bool dx = false, dy = false;
+                const float nx = acc_near_lane(acc[q].x, aw.x, w.num.x, w.den.x, w.r1.x, w.r2.x, w.r3.x, prm.tau,
+                                               prm.delta, dx);
+                const float ny = acc_near_lane(acc[q].y, aw.y, w.num.y, w.den.y, w.r1.y, w.r2.y, w.r3.y, prm.tau,
+                                               prm.delta, dy);
+                acc[q].x = lane_far[2 * q] ? af.x : nx;
+                acc[q].y = lane_far[2 * q + 1] ? af.y : ny;
+                det[2 * q] |= dx && !lane_far[2 * q];
+                det[2 * q + 1] |= dy && !lane_far[2 * q + 1];
               }
             }
           }
@@ -662,10 +690,18 @@ struct PredStraddle {
 };
 
 // ---------------------------------------------------------------------------
-// K3: fp64 fix-up. One CTA of kFixWarps warps per flagged point: each warp
-// takes a fixed contiguous quarter of the compartment's triangles (file
-// order), lanes strided, fixed xor-butterfly; the quarters are added in fixed
-// order (deterministic).
+// K3: fp64 fix-up of flagged (point, compartment) pairs.
+//
+// Pairs are grouped by compartment (k_fix_count / k_fix_fill: per-compartment
+// counts and lists of positions in the flagged-point list; the order inside a
+// list is irrelevant, see below). k_fixup: a CTA takes a batch of kFixPairs
+// pairs of ONE compartment and streams that compartment's de-indexed fp64
+// triangles (72 B each, file order) through shared memory in tiles of
+// kFixTile, so every triangle load feeds kFixPairs points. Each pair is
+// owned by kFixLanes threads: lane l sums triangles t = l, l + kFixLanes, ...
+// in increasing t, then a fixed xor-butterfly adds the lanes. That order
+// depends only on the compartment's triangle count, never on which pairs
+// share the batch, so s is a pure function of (point, compartment).
 // ---------------------------------------------------------------------------
 struct FixupParams {
   const double* pts;
@@ -673,9 +709,10 @@ struct FixupParams {
   const std::uint32_t* subset;  // nullable
   const std::uint32_t* count;   // device count of list
   const std::uint32_t* flagmask;
-  const double* xyz;            // original fp64 vertices
-  const std::uint32_t* tri;     // original triangles
+  const double* tri64;          // de-indexed fp64 triangles: 9 doubles per triangle, compartment ranges of comp_off
   const std::uint32_t* comp_off;  // K+1
+  const std::uint32_t* pair_cnt;  // K: flagged pairs per compartment
+  const std::uint32_t* pairs;     // per compartment (prefix of pair_cnt): positions into list
   int K;
   double T, tie_eps;
   std::uint32_t* masks;
@@ -683,52 +720,117 @@ struct FixupParams {
   unsigned long long* counters;  // [2] pairs, [3] ties
 };
 
-constexpr int kFixWarps = 4;  // warps per flagged point (one CTA)
-static __global__ void __launch_bounds__(32 * kFixWarps) k_fixup(const FixupParams prm) {
-  __shared__ double part[kFixWarps];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const std::uint32_t cnt = *prm.count;
-  unsigned long long pairs = 0, ties = 0;
-  for (std::uint32_t w = blockIdx.x; w < cnt; w += gridDim.x) {  // CTA-uniform loop
-    const std::uint32_t i = prm.subset ? prm.subset[prm.list[w]] : prm.list[w];
-    std::uint32_t fm = prm.flagmask[i];
-    std::uint32_t m = prm.masks[i];
-    const double px = prm.pts[3 * static_cast<std::size_t>(i)], py = prm.pts[3 * static_cast<std::size_t>(i) + 1],
-                 pz = prm.pts[3 * static_cast<std::size_t>(i) + 2];
-    while (fm) {
+constexpr int kFixThreads = 128;
+constexpr int kFixLanes = 8;                          // threads per pair
+constexpr int kFixPairs = kFixThreads / kFixLanes;    // pairs per batch
+constexpr int kFixTile = 128;                         // triangles per shared-memory tile
+
+static __global__ void k_fix_count(const std::uint32_t* list, const std::uint32_t* subset, const std::uint32_t* count,
+                                   const std::uint32_t* flagmask, std::uint32_t* pair_cnt) {
+  const std::uint32_t n = *count;
+  for (std::uint32_t w = blockIdx.x * blockDim.x + threadIdx.x; w < n; w += gridDim.x * blockDim.x) {
+    const std::uint32_t i = subset ? subset[list[w]] : list[w];
+    for (std::uint32_t fm = flagmask[i]; fm; fm &= fm - 1) atomicAdd(pair_cnt + (__ffs(fm) - 1), 1u);
+  }
+}
+
+// pair_fill: per-compartment cursors (zeroed); lists at the prefix of pair_cnt
+static __global__ void k_fix_fill(const std::uint32_t* list, const std::uint32_t* subset, const std::uint32_t* count,
+                                  const std::uint32_t* flagmask, const std::uint32_t* pair_cnt, int K,
+                                  std::uint32_t* pair_fill, std::uint32_t* pairs) {
+  __shared__ std::uint32_t off[33];
+  if (threadIdx.x == 0) {
+    std::uint32_t o = 0;
+    for (int c = 0; c < K; ++c) {
+      off[c] = o;
+      o += pair_cnt[c];
+    }
+  }
+  __syncthreads();
+  const std::uint32_t n = *count;
+  for (std::uint32_t w = blockIdx.x * blockDim.x + threadIdx.x; w < n; w += gridDim.x * blockDim.x) {
+    const std::uint32_t i = subset ? subset[list[w]] : list[w];
+    for (std::uint32_t fm = flagmask[i]; fm; fm &= fm - 1) {
       const int c = __ffs(fm) - 1;
-      fm &= fm - 1;
-      // warp wid sums a fixed quarter of the compartment's triangles (lanes
-      // strided, fixed butterfly); the quarters are added in fixed order
-      const std::uint32_t lo = prm.comp_off[c], len = prm.comp_off[c + 1] - lo;
-      const std::uint32_t t0 = lo + static_cast<std::uint32_t>(std::uint64_t(len) * wid / kFixWarps);
-      const std::uint32_t t1 = lo + static_cast<std::uint32_t>(std::uint64_t(len) * (wid + 1) / kFixWarps);
-      double sum = 0.0;
-      for (std::uint32_t t = t0 + lane; t < t1; t += 32) {
-        const std::uint32_t* e = prm.tri + 3 * static_cast<std::size_t>(t);
-        sum += vos_half_angle64(prm.xyz + 3 * static_cast<std::size_t>(e[0]), prm.xyz + 3 * static_cast<std::size_t>(e[1]),
-                                prm.xyz + 3 * static_cast<std::size_t>(e[2]), px, py, pz);
-      }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(kFull, sum, o);
-      if (lane == 0) part[wid] = sum;
+      pairs[off[c] + atomicAdd(pair_fill + c, 1u)] = w;
+    }
+  }
+}
+
+// de-indexed fp64 triangles for the fix-up (built once by nm_set_surfaces)
+static __global__ void k_deindex64(const double* xyz, const std::uint32_t* tri, std::size_t nt, double* tri64) {
+  for (std::size_t q = blockIdx.x * static_cast<std::size_t>(blockDim.x) + threadIdx.x; q < 9 * nt;
+       q += static_cast<std::size_t>(gridDim.x) * blockDim.x) {
+    const std::size_t t = q / 9, r = q % 9;
+    tri64[q] = xyz[3 * static_cast<std::size_t>(tri[3 * t + r / 3]) + r % 3];
+  }
+}
+
+static __global__ void __launch_bounds__(kFixThreads) k_fixup(const FixupParams prm) {
+  __shared__ double s_tri[kFixTile * 9];
+  __shared__ std::uint32_t s_off[33], s_bo[33];
+  const int K = prm.K;
+  if (threadIdx.x == 0) {
+    std::uint32_t o = 0, b = 0;
+    for (int c = 0; c < K; ++c) {
+      s_off[c] = o;
+      s_bo[c] = b;
+      o += prm.pair_cnt[c];
+      b += (prm.pair_cnt[c] + kFixPairs - 1) / kFixPairs;
+    }
+    s_bo[K] = b;
+  }
+  __syncthreads();
+  const std::uint32_t nbatch = s_bo[K];
+  const int slot = threadIdx.x / kFixLanes, lane = threadIdx.x % kFixLanes;
+  unsigned long long pairs = 0, ties = 0;
+  for (std::uint32_t bt = blockIdx.x; bt < nbatch; bt += gridDim.x) {  // CTA-uniform loop
+    int c = 0;
+    while (c + 1 < K && bt >= s_bo[c + 1]) ++c;
+    const std::uint32_t j = (bt - s_bo[c]) * kFixPairs + slot;
+    const bool has = j < prm.pair_cnt[c];
+    std::uint32_t i = 0;
+    double px = 0.0, py = 0.0, pz = 0.0;
+    if (has) {
+      const std::uint32_t w = prm.pairs[s_off[c] + j];
+      i = prm.subset ? prm.subset[prm.list[w]] : prm.list[w];
+      px = prm.pts[3 * static_cast<std::size_t>(i)];
+      py = prm.pts[3 * static_cast<std::size_t>(i) + 1];
+      pz = prm.pts[3 * static_cast<std::size_t>(i) + 2];
+    }
+    const std::uint32_t lo = prm.comp_off[c], hi = prm.comp_off[c + 1];
+    double sum = 0.0;
+    for (std::uint32_t t0 = lo; t0 < hi; t0 += kFixTile) {
+      const std::uint32_t m = min(static_cast<std::uint32_t>(kFixTile), hi - t0);
+      __syncthreads();  // the previous tile is consumed
+      const double* src = prm.tri64 + 9 * static_cast<std::size_t>(t0);
+      for (std::uint32_t q = threadIdx.x; q < 9 * m; q += kFixThreads) s_tri[q] = __ldg(src + q);
       __syncthreads();
-      double tot = part[0];
+      if (has) {
+        for (std::uint32_t u = lane; u < m; u += kFixLanes) {
+          const double* e = s_tri + 9 * u;
+          sum += vos_half_angle64(e, e + 3, e + 6, px, py, pz);
+        }
+      }
+    }
 #pragma unroll
-      for (int q = 1; q < kFixWarps; ++q) tot += part[q];
-      __syncthreads();  // part is rewritten by the next compartment
-      const double s = tot / (2.0 * CUDART_PI);
-      if (s >= prm.T) m |= 1u << c;
-      else m &= ~(1u << c);
+    for (int o = kFixLanes / 2; o > 0; o >>= 1) sum += __shfl_xor_sync(kFull, sum, o, kFixLanes);
+    if (has && lane == 0) {
+      const double s = sum / (2.0 * CUDART_PI);
+      if (s >= prm.T) atomicOr(prm.masks + i, 1u << c);
+      else atomicAnd(prm.masks + i, ~(1u << c));
       ++pairs;
       if (fabs(s - prm.T) < prm.tie_eps) ++ties;
-      if (prm.s_out && threadIdx.x == 0) prm.s_out[static_cast<std::size_t>(i) * prm.K + c] = s;
+      if (prm.s_out) prm.s_out[static_cast<std::size_t>(i) * prm.K + c] = s;
     }
-    if (threadIdx.x == 0) prm.masks[i] = m;
   }
-  if (threadIdx.x == 0 && prm.counters) {
-    atomicAdd(prm.counters + 2, pairs);
-    atomicAdd(prm.counters + 3, ties);
+  if (prm.counters) {
+    pairs = __reduce_add_sync(kFull, static_cast<unsigned>(pairs));
+    ties = __reduce_add_sync(kFull, static_cast<unsigned>(ties));
+    if ((threadIdx.x & 31) == 0 && (pairs || ties)) {
+      atomicAdd(prm.counters + 2, pairs);
+      atomicAdd(prm.counters + 3, ties);
+    }
   }
 }
 
@@ -738,11 +840,13 @@ static __global__ void __launch_bounds__(32 * kFixWarps) k_fixup(const FixupPara
 // ---------------------------------------------------------------------------
 static __global__ void k_label_tets(const uint4* __restrict__ tets, std::size_t nt, const std::uint32_t* __restrict__ masks,
                              int* __restrict__ labels, const LabelIds ids) {
+  __shared__ int s_ids[32];
+  const int* id = stage_ids(ids, s_ids);
   for (std::size_t i = blockIdx.x * static_cast<std::size_t>(blockDim.x) + threadIdx.x; i < nt;
        i += static_cast<std::size_t>(gridDim.x) * blockDim.x) {
     const uint4 t = __ldg(tets + i);
     const std::uint32_t m = __ldg(masks + t.x) & __ldg(masks + t.y) & __ldg(masks + t.z) & __ldg(masks + t.w);
-    labels[i] = m ? ids.id[__ffs(m) - 1] : 0;
+    labels[i] = m ? id[__ffs(m) - 1] : 0;
   }
 }
 
@@ -834,13 +938,15 @@ static __global__ void k_mark_known(const std::uint32_t* ids, const std::uint32_
 // Label update barrier: every tet whose four nodes are evaluated.
 static __global__ void k_relabel_tets(const uint4* tets, std::size_t nt, const std::uint32_t* masks, const std::uint8_t* known,
                                int* labels, const LabelIds ids, unsigned long long* changed) {
+  __shared__ int s_ids[32];
+  const int* id = stage_ids(ids, s_ids);
   unsigned long long c = 0;
   for (std::size_t t = blockIdx.x * static_cast<std::size_t>(blockDim.x) + threadIdx.x; t < nt;
        t += static_cast<std::size_t>(gridDim.x) * blockDim.x) {
     const uint4 e = tets[t];
     if (!(known[e.x] && known[e.y] && known[e.z] && known[e.w])) continue;
     const std::uint32_t m = masks[e.x] & masks[e.y] & masks[e.z] & masks[e.w];
-    const int l = m ? ids.id[__ffs(m) - 1] : 0;
+    const int l = m ? id[__ffs(m) - 1] : 0;
     if (l != labels[t]) {
       labels[t] = l;
       ++c;
@@ -871,10 +977,12 @@ static __global__ void k_centroids(const double* nodes, const uint4* tets, std::
 
 // label = id[ffs(mask)] or 0 for point-mode labels (centroids).
 static __global__ void k_mask_labels(const std::uint32_t* masks, std::size_t n, int* labels, const LabelIds ids) {
+  __shared__ int s_ids[32];
+  const int* id = stage_ids(ids, s_ids);
   for (std::size_t i = blockIdx.x * static_cast<std::size_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<std::size_t>(gridDim.x) * blockDim.x) {
     const std::uint32_t m = masks[i];
-    labels[i] = m ? ids.id[__ffs(m) - 1] : 0;
+    labels[i] = m ? id[__ffs(m) - 1] : 0;
   }
 }
 

@@ -356,7 +356,6 @@ void label_nodes_dev(nm_ctx* c, const double* d_pts, std::size_t n, double T, st
   prm.order = order;
   prm.tri = static_cast<const float4*>(c->tri.p);
   prm.sub = static_cast<const float4*>(c->sub.p);
-  prm.edges = static_cast<const float4*>(c->edges.p);
   prm.cont = static_cast<const std::uint32_t*>(c->cont.p);
   prm.comp_tiles = static_cast<const std::uint32_t*>(c->comp_tiles.p);
   prm.K = c->K;
@@ -427,26 +426,46 @@ void label_nodes_dev(nm_ctx* c, const double* d_pts, std::size_t n, double T, st
   ++launches;
   }
   if (stats) NM_CUDA(cudaEventRecord(c->ev[2], st));
-  // compaction of flagged points + fp64 fix-up
+  // compaction of flagged points, per-compartment pair lists, fp64 fix-up
   select(c, nm::PredNonzero{flagmask, d_subset}, n, list, d_count, st, launches);
-  nm::FixupParams fp{};
-  fp.pts = d_pts;
-  fp.list = list;
-  fp.subset = d_subset;
-  fp.count = d_count;
-  fp.flagmask = flagmask;
-  fp.xyz = static_cast<const double*>(c->xyz64.p);
-  fp.tri = static_cast<const std::uint32_t*>(c->tri_idx.p);
-  fp.comp_off = static_cast<const std::uint32_t*>(c->comp_off.p);
-  fp.K = c->K;
-  fp.T = T;
-  fp.tie_eps = c->opt.tie_eps;
-  fp.masks = d_masks;
-  fp.s_out = d_s;
-  fp.counters = counters;
-  nm::k_fixup<<<c->sm_count * 16, 32 * nm::kFixWarps, 0, st>>>(fp);
+  const int K = c->K;
+  auto* pair_cnt = c->pair_cnt.as<std::uint32_t>(2 * 32);
+  NM_CUDA(cudaMemsetAsync(pair_cnt, 0, 2 * 32 * sizeof(std::uint32_t), st));
+  nm::k_fix_count<<<grid_for(n, 256, c->sm_count * 4), 256, 0, st>>>(list, d_subset, d_count, flagmask, pair_cnt);
   NM_CUDA(cudaGetLastError());
-  ++launches;
+  // one host synchronisation: the pair lists' size (the fix-up is the only
+  // consumer, and its batch grid runs from the device-side counts)
+  NM_CUDA(cudaMemcpyAsync(c->h_pcnt, pair_cnt, K * sizeof(std::uint32_t), cudaMemcpyDeviceToHost, st));
+  NM_CUDA(cudaStreamSynchronize(st));
+  std::size_t total = 0;
+  for (int k = 0; k < K; ++k) total += c->h_pcnt[k];
+  auto* pairs = c->pairs.as<std::uint32_t>(std::max<std::size_t>(total, 1));
+  launches += 1;
+  if (total) {
+    nm::k_fix_fill<<<grid_for(n, 256, c->sm_count * 4), 256, 0, st>>>(list, d_subset, d_count, flagmask, pair_cnt, K,
+                                                                       pair_cnt + 32, pairs);
+    nm::FixupParams fp{};
+    fp.pts = d_pts;
+    fp.list = list;
+    fp.subset = d_subset;
+    fp.count = d_count;
+    fp.flagmask = flagmask;
+    fp.tri64 = static_cast<const double*>(c->tri64.p);
+    fp.comp_off = static_cast<const std::uint32_t*>(c->comp_off.p);
+    fp.pair_cnt = pair_cnt;
+    fp.pairs = pairs;
+    fp.K = K;
+    fp.T = T;
+    fp.tie_eps = c->opt.tie_eps;
+    fp.masks = d_masks;
+    fp.s_out = d_s;
+    fp.counters = counters;
+    std::size_t nbatch = 0;
+    for (int k = 0; k < K; ++k) nbatch += (c->h_pcnt[k] + nm::kFixPairs - 1) / nm::kFixPairs;
+    nm::k_fixup<<<grid_for(nbatch, 1, c->sm_count * 8), nm::kFixThreads, 0, st>>>(fp);
+    NM_CUDA(cudaGetLastError());
+    launches += 2;
+  }
   c->node_launches = launches;
   if (stats) {
     NM_CUDA(cudaEventRecord(c->ev[3], st));
@@ -568,6 +587,7 @@ int nm_create(nm_ctx** out, const nm_options* opt) {
       for (auto& ev : c->ev) NM_CUDA(cudaEventCreate(&ev));
       NM_CUDA(cudaEventCreateWithFlags(&c->ev_side, cudaEventDisableTiming));
       NM_CUDA(cudaMallocHost(&c->h_word, sizeof(std::uint32_t)));
+      NM_CUDA(cudaMallocHost(&c->h_pcnt, 32 * sizeof(std::uint32_t)));
       // result meshes are allocated from the device's default pool: keep
       // freed blocks reserved instead of returning them at every sync
       cudaMemPool_t pool;
@@ -633,6 +653,14 @@ int nm_set_surfaces(nm_ctx* c, const double* xyz, std::size_t nv, const std::uin
     up_on(c->xyz64, xyz, nv * 3 * sizeof(double), c->side);
     up_on(c->tri_idx, tri, nt * 3 * sizeof(std::uint32_t), c->side);
     up_on(c->comp_off, comp_off, (K + 1) * sizeof(std::uint32_t), c->side);
+    // de-indexed fp64 triangles (72 B each, file order) for the fix-up
+    {
+      auto* t64 = c->tri64.as<double>(std::max<std::size_t>(9 * nt, 1));
+      if (nt)
+        nm::k_deindex64<<<grid_for(9 * nt, 256, c->sm_count * 16), 256, 0, c->side>>>(
+            static_cast<const double*>(c->xyz64.p), static_cast<const std::uint32_t*>(c->tri_idx.p), nt, t64);
+      NM_CUDA(cudaGetLastError());
+    }
     // 13-DOP: slab bounds over the vertices (centred frame), widened by 1e-3 mm
     // + 1e-5 |bound| (covers the fp32 rounding of the point and of the
     // projection in the kernel) and rounded outward.
@@ -795,50 +823,122 @@ int nm_set_surfaces(nm_ctx* c, const double* xyz, std::size_t nv, const std::uin
     const std::size_t tile_f4 = static_cast<std::size_t>(sub_f4) * nm::kSubPerTile;
     std::vector<float4> htri(ntiles * tile_f4);
     std::vector<float4> hsub(ntiles * nm::kSubPerTile * nm::kSubRec);
-    std::vector<float4> hedge(use_strips ? ntiles * nm::kSubPerTile * nm::kGroups * nm::kEdgeF4 : 1);
     std::vector<std::uint32_t> hcont(std::max<std::size_t>(ntiles, 1), 0u);
     static_assert(nm::kSubPerTile * nm::kGroups <= 32, "continuation bits of a tile must fit a uint32");
     const double far_ratio = c->opt.far_ratio, far_abs = c->opt.far_abs_mm;
-    // Each 32-triangle subtile carries an fp32 centre c (exactly representable
-    // in the centred frame) and its vertices relative to c, so near-surface
-    // geometry keeps ~ulp(radius) precision; the kernel forms p - c in
-    // double-single per subtile.
-    parallel_for(K, [&](int k) {  // compartments own disjoint tile ranges
+    // Watertight subtile frames. Each 32-triangle subtile
+    // carries an fp32 centre c and its vertices relative to c, so the kernel
+    // forms R = (v - c) - (p - c) with ~ulp(|R|) error. For the sum over a
+    // closed surface to stay a winding number in fp32, every vertex must have
+    // the SAME position in every subtile it appears in: vertices are snapped
+    // (centred frame, fp64) to a global power-of-two grid G fine enough that
+    // v - c is exactly representable in fp32 for every subtile (c on a
+    // coarser power-of-two grid Gc, exact in fp32). Snapping moves a vertex by
+    // <= G/2 (a few nm) consistently in every triangle, so the snapped
+    // surfaces are still closed and their winding numbers are the oracle's
+    // for every point not within G of a surface (such points are caught by
+    // the near-face / near-vertex detector and re-evaluated in fp64 on the
+    // original vertices).
+    auto gather = [&](int k, std::uint32_t tl, int sidx, std::vector<const double*>& srcv) {
       const std::size_t nreal = use_strips ? segs[k].size() : order[k].size();
       // fallback vertex for all-pad units: the compartment's first vertex
       const double* pad_v = comp_off[k + 1] > comp_off[k] ? xyz + 3 * std::size_t(tri[3 * comp_off[k]]) : ctr;
-      for (std::uint32_t tl = tiles[k]; tl < tiles[k + 1]; ++tl) {
-        for (int sidx = 0; sidx < nm::kSubPerTile; ++sidx) {
-          // gather this subtile's vertices (centred frame, fp64)
-          std::vector<const double*> srcv;
-          const std::size_t u0 = static_cast<std::size_t>(tl - tiles[k]) * nm::kTile / (use_strips ? nm::kSegTris : 1) +
-                                 sidx * (use_strips ? nm::kSub / nm::kSegTris : nm::kSub);
-          const int nunits = use_strips ? nm::kSub / nm::kSegTris : nm::kSub;
-          for (int j = 0; j < nunits; ++j) {
-            const std::size_t u = u0 + j;
-            if (use_strips) {
-              for (int q = 0; q < nm::kSegTris + 2; ++q)
-                srcv.push_back(u < nreal ? xyz + 3 * std::size_t(segs[k][u].v[q]) : pad_v);
-            } else {
-              const std::uint32_t t = u < nreal ? order[k][u] : 0;
-              for (int q = 0; q < 3; ++q) srcv.push_back(u < nreal ? xyz + 3 * std::size_t(tri[3 * t + q]) : pad_v);
+      srcv.clear();
+      const std::size_t u0 = static_cast<std::size_t>(tl - tiles[k]) * nm::kTile / (use_strips ? nm::kSegTris : 1) +
+                             sidx * (use_strips ? nm::kSub / nm::kSegTris : nm::kSub);
+      const int nunits = use_strips ? nm::kSub / nm::kSegTris : nm::kSub;
+      for (int j = 0; j < nunits; ++j) {
+        const std::size_t u = u0 + j;
+        if (use_strips) {
+          for (int q = 0; q < nm::kSegTris + 2; ++q) srcv.push_back(u < nreal ? xyz + 3 * std::size_t(segs[k][u].v[q]) : pad_v);
+        } else {
+          const std::uint32_t t = u < nreal ? order[k][u] : 0;
+          for (int q = 0; q < 3; ++q) srcv.push_back(u < nreal ? xyz + 3 * std::size_t(tri[3 * t + q]) : pad_v);
+        }
+      }
+      return u0;
+    };
+    auto mid_of = [&](const std::vector<const double*>& srcv, double* mid, double* half) {
+      double blo[3] = {1e300, 1e300, 1e300}, bhi[3] = {-1e300, -1e300, -1e300};
+      for (const double* v : srcv)
+        for (int a = 0; a < 3; ++a) {
+          blo[a] = std::min(blo[a], v[a] - ctr[a]);
+          bhi[a] = std::max(bhi[a], v[a] - ctr[a]);
+        }
+      for (int a = 0; a < 3; ++a) {
+        mid[a] = 0.5 * (blo[a] + bhi[a]);
+        half[a] = 0.5 * (bhi[a] - blo[a]);
+      }
+    };
+    // grids: Gc for the centres (|c| / Gc < 2^23), G for the vertices
+    // (|v - c| / G < 2^23 with c rounded to Gc)
+    double cmax = 0.0, emax = 0.0;
+    {
+      std::vector<double> cm(K, 0.0), em(K, 0.0);
+      parallel_for(K, [&](int k) {
+        std::vector<const double*> srcv;
+        for (std::uint32_t tl = tiles[k]; tl < tiles[k + 1]; ++tl)
+          for (int sidx = 0; sidx < nm::kSubPerTile; ++sidx) {
+            gather(k, tl, sidx, srcv);
+            double mid[3], half[3];
+            mid_of(srcv, mid, half);
+            for (int a = 0; a < 3; ++a) {
+              cm[k] = std::max(cm[k], std::fabs(mid[a]));
+              em[k] = std::max(em[k], half[a]);
             }
           }
-          double blo[3] = {1e300, 1e300, 1e300}, bhi[3] = {-1e300, -1e300, -1e300};
-          for (const double* v : srcv)
+      });
+      for (int k = 0; k < K; ++k) {
+        cmax = std::max(cmax, cm[k]);
+        emax = std::max(emax, em[k]);
+      }
+    }
+    // (factor-2 margins: |v - c| <= emax + G/2 + Gc/2 < 2^24 G)
+    double Gc = std::ldexp(1.0, std::max(-120, std::ilogb(std::max(cmax, 1e-30)) + 1 - 23));
+    const double G = std::ldexp(1.0, std::max(-120, std::ilogb(std::max(emax + Gc, 1e-30)) + 1 - 22));
+    Gc = std::max(Gc, G);  // centres on the vertex grid too
+    c->snap_grid = G;
+    std::atomic<bool> inexact{false};
+    auto snap = [&](double x, double g) { return std::nearbyint(x / g) * g; };
+    parallel_for(K, [&](int k) {  // compartments own disjoint tile ranges
+      const std::size_t nreal = use_strips ? segs[k].size() : order[k].size();
+      std::vector<const double*> srcv;
+      for (std::uint32_t tl = tiles[k]; tl < tiles[k + 1]; ++tl) {
+        for (int sidx = 0; sidx < nm::kSubPerTile; ++sidx) {
+          const std::size_t u0 = gather(k, tl, sidx, srcv);
+          const int nunits = use_strips ? nm::kSub / nm::kSegTris : nm::kSub;
+          double mid[3], half[3];
+          mid_of(srcv, mid, half);
+          const float fc[3] = {float(snap(mid[0], Gc)), float(snap(mid[1], Gc)), float(snap(mid[2], Gc))};
+          // snapped vertex relative to the centre: exact in fp32 (checked)
+          auto relv = [&](const double* v, float* out) {
             for (int a = 0; a < 3; ++a) {
-              blo[a] = std::min(blo[a], v[a] - ctr[a]);
-              bhi[a] = std::max(bhi[a], v[a] - ctr[a]);
+              const double r = snap(v[a] - ctr[a], G) - double(fc[a]);
+              out[a] = float(r);
+              if (double(out[a]) != r) inexact = true;
             }
-          const float fc[3] = {float(0.5 * (blo[0] + bhi[0])), float(0.5 * (blo[1] + bhi[1])),
-                               float(0.5 * (blo[2] + bhi[2]))};
+          };
           double rho = 0.0;
           std::vector<float> rel(3 * srcv.size());
           for (std::size_t q = 0; q < srcv.size(); ++q) {
-            for (int a = 0; a < 3; ++a) rel[3 * q + a] = float((srcv[q][a] - ctr[a]) - double(fc[a]));
+            relv(srcv[q], &rel[3 * q]);
             rho = std::max(rho, std::sqrt(double(rel[3 * q]) * rel[3 * q] + double(rel[3 * q + 1]) * rel[3 * q + 1] +
                                           double(rel[3 * q + 2]) * rel[3 * q + 2]));
           }
+          // N = (v2 - v1) x (v3 - v1) of the snapped ORIGINAL triangle (its own
+          // vertex order: outward whatever the strip parity), fp64 from the
+          // exact fp32 coordinates
+          auto normal_rel = [&](std::uint32_t t, double* N) {
+            float A[3], B[3], C[3];
+            relv(xyz + 3 * std::size_t(tri[3 * t]), A);
+            relv(xyz + 3 * std::size_t(tri[3 * t + 1]), B);
+            relv(xyz + 3 * std::size_t(tri[3 * t + 2]), C);
+            const double e1[3] = {double(B[0]) - A[0], double(B[1]) - A[1], double(B[2]) - A[2]};
+            const double e2[3] = {double(C[0]) - A[0], double(C[1]) - A[1], double(C[2]) - A[2]};
+            N[0] = e1[1] * e2[2] - e1[2] * e2[1];
+            N[1] = e1[2] * e2[0] - e1[0] * e2[2];
+            N[2] = e1[0] * e2[1] - e1[1] * e2[0];
+          };
           float4* o = &htri[(static_cast<std::size_t>(tl) * nm::kSubPerTile + sidx) * sub_f4];
           for (int j = 0; j < nunits; ++j) {
             const std::size_t u = u0 + j;
@@ -849,7 +949,7 @@ int nm_set_surfaces(nm_ctx* c, const double* xyz, std::size_t nv, const std::uin
               float4* r = o + j * nm::kSegF4;
               double N[nm::kSegTris][3];
               for (int q = 0; q < nm::kSegTris; ++q) {
-                if (u < nreal && segs[k][u].t[q] >= 0) normal64(static_cast<std::uint32_t>(segs[k][u].t[q]), N[q]);
+                if (u < nreal && segs[k][u].t[q] >= 0) normal_rel(static_cast<std::uint32_t>(segs[k][u].t[q]), N[q]);
                 else N[q][0] = N[q][1] = N[q][2] = 0.0;
               }
               const float* rv = &rel[3 * (j * (nm::kSegTris + 2))];
@@ -883,23 +983,9 @@ int nm_set_surfaces(nm_ctx* c, const double* xyz, std::size_t nv, const std::uin
               }
               for (int q = 0; q < nm::kSegF4 - nm::kSegC; ++q)
                 r[nm::kSegC + q] = make_float4(C[4 * q], C[4 * q + 1], C[4 * q + 2], C[4 * q + 3]);
-              // -|e|^2 of the consecutive (k,k+1) and skip (k,k+2) edges (near evaluator)
-              float E[4 * nm::kEdgeF4] = {0};
-              auto e2 = [&](int i, int jj) {
-                double s2 = 0;
-                for (int a = 0; a < 3; ++a) {
-                  const double d = double(rv[3 * jj + a]) - double(rv[3 * i + a]);
-                  s2 += d * d;
-                }
-                return float(-s2);
-              };
-              for (int q = 0; q <= nm::kSegTris; ++q) E[q] = e2(q, q + 1);
-              for (int q = 0; q < nm::kSegTris; ++q) E[nm::kSegSkip + q] = e2(q, q + 2);
-              float4* er = &hedge[((static_cast<std::size_t>(tl) * nm::kSubPerTile + sidx) * nm::kGroups + j) * nm::kEdgeF4];
-              for (int q = 0; q < nm::kEdgeF4; ++q) er[q] = make_float4(E[4 * q], E[4 * q + 1], E[4 * q + 2], E[4 * q + 3]);
             } else {
               double N[3] = {0, 0, 0};
-              if (u < nreal) normal64(order[k][u], N);
+              if (u < nreal) normal_rel(order[k][u], N);
               const float* rv = &rel[9 * j];
               for (int q = 0; q < 3; ++q) o[3 * j + q] = make_float4(rv[3 * q], rv[3 * q + 1], rv[3 * q + 2], float(N[q]));
             }
@@ -934,11 +1020,11 @@ int nm_set_surfaces(nm_ctx* c, const double* xyz, std::size_t nv, const std::uin
         }
       }
     });
+    if (inexact) throw Error("internal: a snapped subtile coordinate is not exact in fp32");
     c->strips = use_strips;
     auto up = [&](DBuf& b, const void* src, std::size_t bytes) { up_on(b, src, bytes, c->stream); };
     up(c->tri, htri.data(), htri.size() * sizeof(float4));
     up(c->sub, hsub.data(), hsub.size() * sizeof(float4));
-    up(c->edges, hedge.data(), hedge.size() * sizeof(float4));
     up(c->cont, hcont.data(), hcont.size() * sizeof(std::uint32_t));
     up(c->comp_tiles, tiles.data(), tiles.size() * sizeof(std::uint32_t));
     up(c->comp_box, hbox.data(), hbox.size() * sizeof(float4));

@@ -70,6 +70,31 @@ __device__ __forceinline__ VosTerms2 vos_terms2(const float4& A, const float4& B
   return t;
 }
 
+// The same terms in the exact double-single frame (near path of the
+// triangle layout): R = (v - c) + m + l.
+__device__ __forceinline__ VosTerms2 vos_terms2x(const float4& A, const float4& B, const float4& C, const float2 (&m)[3],
+                                                 const float2 (&l)[3]) {
+  const float2 x1 = add2(add2(bc(A.x), m[0]), l[0]), y1 = add2(add2(bc(A.y), m[1]), l[1]),
+               z1 = add2(add2(bc(A.z), m[2]), l[2]);
+  const float2 x2 = add2(add2(bc(B.x), m[0]), l[0]), y2 = add2(add2(bc(B.y), m[1]), l[1]),
+               z2 = add2(add2(bc(B.z), m[2]), l[2]);
+  const float2 x3 = add2(add2(bc(C.x), m[0]), l[0]), y3 = add2(add2(bc(C.y), m[1]), l[1]),
+               z3 = add2(add2(bc(C.z), m[2]), l[2]);
+  const float2 q1 = fma2(z1, z1, fma2(y1, y1, mul2(x1, x1)));
+  const float2 q2 = fma2(z2, z2, fma2(y2, y2, mul2(x2, x2)));
+  const float2 q3 = fma2(z3, z3, fma2(y3, y3, mul2(x3, x3)));
+  VosTerms2 t;
+  t.r1 = make_float2(sqrt_approx(q1.x), sqrt_approx(q1.y));
+  t.r2 = make_float2(sqrt_approx(q2.x), sqrt_approx(q2.y));
+  t.r3 = make_float2(sqrt_approx(q3.x), sqrt_approx(q3.y));
+  t.num = fma2(bc(C.w), z1, fma2(bc(B.w), y1, mul2(bc(A.w), x1)));
+  const float2 d12 = fma2(z1, z2, fma2(y1, y2, mul2(x1, x2)));
+  const float2 d13 = fma2(z1, z3, fma2(y1, y3, mul2(x1, x3)));
+  const float2 d23 = fma2(z2, z3, fma2(y2, y3, mul2(x2, x3)));
+  t.den = fma2(fma2(t.r1, t.r2, d12), t.r3, fma2(d13, t.r2, mul2(d23, t.r1)));
+  return t;
+}
+
 __device__ __forceinline__ float2 acc_far2(float2 acc, float2 num, float2 den) {
   const float2 x = mul2(num, make_float2(rcp_approx(den.x), rcp_approx(den.y)));
   const float2 y = mul2(x, x);
@@ -126,8 +151,6 @@ __device__ __forceinline__ float acc_near_lane(float acc, float a_far, float num
 //                                                        u_{k+1}, u_{k+2}): alpha =
 //                                                        (a-c).(b-c), beta = (b-a).(c-a),
 //                                                        gamma = (a-b).(c-b)
-// plus, in a separate global array read only by the near evaluator, -|e|^2
-// of the 9 consecutive (k,k+1) and 8 skip (k,k+2) edges (kEdgeF4 float4).
 // The factor 2 on T is an exact power-of-two scaling: the far evaluator
 // works with (2 num, 2 den), the near one scales back exactly.
 //
@@ -142,8 +165,8 @@ __device__ __forceinline__ float acc_near_lane(float acc, float a_far, float num
 //        <= 0.2 rad, where a 3-coefficient minimax odd polynomial (after the
 //        complex product below) is within 4.9e-8 rad: 18.6 FP32 lane-ops +
 //        1.75 MUFU;
-//   near R-based terms, R_a.R_b = (q_a + q_b)/2 - |e_ab|^2/2 (exact to
-//        ~ulp(|R|)), 3-term series for |x| <= 0.125 else full-range atan2,
+//   near R-based terms in the exact double-single subtile frame, direct dot
+//        products, 3-term series for |x| <= 0.125 else full-range atan2,
 //        plus the near-surface detector.
 // Which evaluator a (point, group) pair uses depends only on that point's own
 // distance test, never on its warp mates (mixed warps run both and select per
@@ -156,8 +179,6 @@ constexpr int kSegTris = NM_SEG_TRIS;               // triangles per segment
 constexpr int kSegT = kSegTris + 2;                 // first T_k (after the vertices)
 constexpr int kSegC = kSegT + kSegTris;             // first vertex-dot coefficient float4
 constexpr int kSegF4 = kSegC + (3 * kSegTris + 3) / 4;  // 24 float4 for 8 triangles
-constexpr int kSegSkip = kSegTris + 1;              // first skip edge (k, k+2) of the edge record
-constexpr int kEdgeF4 = (2 * kSegTris + 1 + 3) / 4;  // near-evaluator edge record, float4 per segment
 constexpr float kRecScale = 2.0f;  // T_k scaling of the record (host packing)
 
 __device__ __forceinline__ float f4_at(const float4& v, int c) {
@@ -165,10 +186,6 @@ __device__ __forceinline__ float f4_at(const float4& v, int c) {
 }
 // -(vertex dot) coefficient i of the segment (3 per triangle), shared memory
 __device__ __forceinline__ float coef_val(const float4* rec, int idx) { return f4_at(rec[kSegC + (idx >> 2)], idx & 3); }
-// -|e|^2 of edge idx from the segment's edge record in global memory (near path only)
-__device__ __forceinline__ float edge_val(const float4* __restrict__ erec, int idx) {
-  return f4_at(__ldg(erec + (idx >> 2)), idx & 3);
-}
 
 // Per point pair, in the subtile frame: m = -(p - c); sp = |p - c|^2 (the
 // subtile far test's squared distance, reused).
@@ -260,59 +277,94 @@ __device__ __forceinline__ void seg_far(const float4* __restrict__ rec, const Pa
 }
 
 // ---- near evaluator -------------------------------------------------------
-struct Vtx2 {
-  float2 x, y, z, r, q;
+// Exact subtile frame of a point pair: -(p - c) = m + l as a double-single
+// (m = -fl(hx - c), l = -(TwoSum error + lx)); R = (v - c) + m + l then has
+// one rounding relative to |R| (not to |p - c|), so near a surface every
+// term is accurate to ~ulp of its own geometry. Together with the snapped,
+// watertight subtile vertices (nm_set_surfaces) this keeps the fp32 sum over
+// a closed surface at its winding number for points close to vertices and
+// edges.
+struct NearFrame {
+  float2 mx, my, mz, lx, ly, lz;
 };
 
-// V holds 2V: R = 0.5 (2V) - p, exact scaling.
-__device__ __forceinline__ Vtx2 strip_vertex(const float4& V, float2 mx, float2 my, float2 mz) {
+__device__ __forceinline__ void two_sum_neg(float2 a, float b, float2 lo_in, float2& m, float2& l) {
+  const float2 s = add2(a, bc(b));
+  const float2 bp = add2(s, make_float2(-a.x, -a.y));
+  const float2 ap = add2(s, make_float2(-bp.x, -bp.y));
+  const float2 err = add2(add2(a, make_float2(-ap.x, -ap.y)), add2(bc(b), make_float2(-bp.x, -bp.y)));
+  const float2 lo = add2(err, lo_in);
+  m = make_float2(-s.x, -s.y);
+  l = make_float2(-lo.x, -lo.y);
+}
+
+// hi/lo of the centred point pair and the subtile centre c -> exact frame
+__device__ __forceinline__ NearFrame near_frame(float2 hx, float2 hy, float2 hz, float2 lx, float2 ly, float2 lz,
+                                                const float4& c) {
+  NearFrame f;
+  two_sum_neg(hx, -c.x, lx, f.mx, f.lx);
+  two_sum_neg(hy, -c.y, ly, f.my, f.ly);
+  two_sum_neg(hz, -c.z, lz, f.mz, f.lz);
+  return f;
+}
+
+struct Vtx2 {
+  float2 x, y, z, r;
+};
+
+// V holds 2V: R = (0.5 (2V) + m) + l, exact scaling, two roundings relative to |R|.
+__device__ __forceinline__ Vtx2 strip_vertex(const float4& V, const NearFrame& f) {
   Vtx2 v;
-  v.x = fma2(bc(V.x), bc(0.5f), mx);
-  v.y = fma2(bc(V.y), bc(0.5f), my);
-  v.z = fma2(bc(V.z), bc(0.5f), mz);
-  v.q = fma2(v.z, v.z, fma2(v.y, v.y, mul2(v.x, v.x)));
-  v.r = make_float2(sqrt_approx(v.q.x), sqrt_approx(v.q.y));
+  v.x = add2(fma2(bc(V.x), bc(0.5f), f.mx), f.lx);
+  v.y = add2(fma2(bc(V.y), bc(0.5f), f.my), f.ly);
+  v.z = add2(fma2(bc(V.z), bc(0.5f), f.mz), f.lz);
+  const float2 q = fma2(v.z, v.z, fma2(v.y, v.y, mul2(v.x, v.x)));
+  v.r = make_float2(sqrt_approx(q.x), sqrt_approx(q.y));
   return v;
+}
+__device__ __forceinline__ float2 dot2(const Vtx2& a, const Vtx2& b) {
+  return fma2(a.z, b.z, fma2(a.y, b.y, mul2(a.x, b.x)));
 }
 
 #ifndef NM_NEAR_UNROLL
 #define NM_NEAR_UNROLL 4
 #endif
 constexpr int kNearUnroll = NM_NEAR_UNROLL;
-// use[k]: lane point k takes this group's near result (the caller discards
-// the others), so only those lanes ask for the full-range atan2.
 template <int NP>
 __device__ __forceinline__ void seg_far(const float4* __restrict__ rec, const PairFrame (&f)[NP], float2 (&acc)[NP]) {
   float2 ra[NP], rb[NP], sab[NP];
   seg_far<NP>(rec, f, acc, ra, rb, sab, false);
 }
 
+// Near evaluator: R-based VOS terms with direct dot products (no
+// |R_a|^2 + |R_b|^2 - |e|^2 identity, whose O(|e|^2) cancellation would cost
+// ~eps |e| / r relative near a vertex), 3-term series for |x| <= kFarX, else
+// the full-range atan2, plus the near-surface detector.
+// use[k]: lane point k takes this group's near result (the caller discards
+// the others), so only those lanes ask for the full-range atan2.
 template <int NP>
-__device__ __forceinline__ void seg_near(const float4* __restrict__ rec, const float4* __restrict__ erec,
-                                         const PairFrame (&f)[NP], float2 (&acc)[NP], bool (&det)[2 * NP],
-                                         const bool (&use)[2 * NP], float tau, float delta) {
+__device__ __forceinline__ void seg_near(const float4* __restrict__ rec, const NearFrame (&f)[NP], float2 (&acc)[NP],
+                                         bool (&det)[2 * NP], const bool (&use)[2 * NP], float tau, float delta) {
   Vtx2 a[NP], b[NP];
   float2 dab[NP];
   {
     const float4 V0 = rec[0], V1 = rec[1];
-    const float e0 = 0.5f * edge_val(erec, 0);
 #pragma unroll
     for (int q = 0; q < NP; ++q) {
-      a[q] = strip_vertex(V0, f[q].mx, f[q].my, f[q].mz);
-      b[q] = strip_vertex(V1, f[q].mx, f[q].my, f[q].mz);
-      dab[q] = fma2(add2(a[q].q, b[q].q), bc(0.5f), bc(e0));
+      a[q] = strip_vertex(V0, f[q]);
+      b[q] = strip_vertex(V1, f[q]);
+      dab[q] = dot2(a[q], b[q]);
     }
   }
 #pragma unroll kNearUnroll
   for (int k = 0; k < kSegTris; ++k) {
     const float4 V2 = rec[k + 2];
     const float4 T = rec[kSegT + k];
-    const float ebc = 0.5f * edge_val(erec, k + 1), eac = 0.5f * edge_val(erec, kSegSkip + k);  // -|e|^2/2, exact
 #pragma unroll
     for (int q = 0; q < NP; ++q) {
-      const Vtx2 c = strip_vertex(V2, f[q].mx, f[q].my, f[q].mz);
-      const float2 dbc = fma2(add2(b[q].q, c.q), bc(0.5f), bc(ebc));
-      const float2 dac = fma2(add2(a[q].q, c.q), bc(0.5f), bc(eac));
+      const Vtx2 c = strip_vertex(V2, f[q]);
+      const float2 dbc = dot2(b[q], c);
+      const float2 dac = dot2(a[q], c);
       float2 num = fma2(bc(T.z), a[q].z, fma2(bc(T.y), a[q].y, mul2(bc(T.x), a[q].x)));
       num = mul2(num, bc(1.0f / kRecScale));  // exact: the record holds 2N
       const float2 den = fma2(fma2(a[q].r, b[q].r, dab[q]), c.r, fma2(dac, b[q].r, mul2(dbc, a[q].r)));

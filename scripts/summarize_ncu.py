@@ -69,6 +69,45 @@ def traffic(path):
                       "gpu_time_ns": last.get("gpu__time_duration.sum")}, indent=1))
 
 
+FP32_PIPE = {"FFMA2": 2, "FADD2": 2, "FMUL2": 2, "FFMA": 1, "FADD": 1, "FMUL": 1}
+
+
+def _opcode_counts(cell):
+    """'235128 (FFMA2: 109; FADD2: 30; ...)' -> {'FFMA2': 109, ...}"""
+    inner = cell[cell.index("(") + 1: cell.rindex(")")]
+    out = {}
+    for part in inner.split(";"):
+        k, v = part.split(":")
+        out[k.strip()] = int(v.strip())
+    return out
+
+
+def opcounts(path, sass_hash, evals, config, points, note=""):
+    """FP32-pipe lane-ops per point-triangle evaluation of one k_label launch,
+    from ncu --metrics sass__thread_inst_executed_true_per_opcode
+    --print-metric-instances details (csv): 2 x packed (FFMA2/FADD2/FMUL2) +
+    scalar FFMA/FADD/FMUL thread instructions with a true predicate."""
+    import json
+    rows = [r for r in csv.reader(open(path)) if len(r) > 10]
+    h = rows[0]
+    col = h.index("sass__thread_inst_executed_true_per_opcode")
+    kcol = h.index("Kernel Name")
+    cands = [r for r in rows[1:] if "k_label<" in r[kcol] and "(" in r[col]]
+    r = cands[-1]
+    thr = _opcode_counts(r[col])
+    warp = _opcode_counts(r[h.index("sass__inst_executed_per_opcode")]) if "sass__inst_executed_per_opcode" in h else {}
+    lane_ops = sum(thr.get(k, 0) * w for k, w in FP32_PIPE.items())
+    evals = int(evals)
+    out = {"kernel": r[kcol], "sass_sha16": sass_hash, "config": config, "points": int(points), "evals": evals,
+           "fp32_lane_ops": lane_ops, "fp32_lane_ops_per_eval": lane_ops / evals,
+           "mufu_per_eval": thr.get("MUFU", 0) / evals,
+           "thread_inst_per_eval": {k: v / evals for k, v in sorted(thr.items(), key=lambda kv: -kv[1])[:16]},
+           "warp_inst_total": sum(warp.values()) if warp else None,
+           "source": "ncu --metrics sass__thread_inst_executed_true_per_opcode (thread instructions, predicate true)",
+           "note": note}
+    print(json.dumps(out, indent=1))
+
+
 def report(path):
     out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(out.splitlines()))
@@ -87,4 +126,4 @@ def report(path):
 
 
 if __name__ == "__main__":
-    {"launches": launches, "report": report, "traffic": traffic}[sys.argv[1]](sys.argv[2])
+    {"launches": launches, "report": report, "traffic": traffic, "opcounts": opcounts}[sys.argv[1]](*sys.argv[2:])

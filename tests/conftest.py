@@ -14,8 +14,8 @@ def pytest_configure(config):
 
 def _ensure_built():
     from paper_2203_10000_b200 import _native, build
-    oracle_lib = ROOT / "oracle" / "build" / "liblabel_oracle.so"
-    if not (_native.LABEL_LIB.exists() and _native.SYNTH_LIB.exists() and oracle_lib.exists()):
+    oracle_libs = [ROOT / "oracle" / "build" / f for f in ("liblabel_oracle.so", "librefine_oracle.so")]
+    if not (_native.LABEL_LIB.exists() and _native.SYNTH_LIB.exists() and all(p.exists() for p in oracle_libs)):
         build.build_all()
 
 
