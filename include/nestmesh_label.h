@@ -269,6 +269,43 @@ int nm_surface_segments(nm_ctx* ctx, size_t* segments, size_t* continued);
 int nm_cell_info(nm_ctx* ctx, uint64_t* cells, uint64_t* certified, uint64_t* reps, double* ms_build,
                  uint64_t* last_pairs, uint64_t* last_evals);
 
+/* ---- binary label / node-mask sidecar next to tetmesh v1 -----------------
+ * The reference writes meshes as %.17g text (write_tetmesh, mesh.hpp:238-289).
+ * A labeling result is kept beside it, bit for bit, in <mesh>.tetmesh.nmlabels:
+ * int32 labels per tet, optional uint32 node masks, and what ties them to the
+ * mesh — its fingerprint (explicit meshes) or its LatticeSpec (lattices:
+ * generate_lattice_mesh, lattice.hpp:40-91, regenerates the mesh bit for bit).
+ * Little-endian; the payload carries a hash checked on read. */
+typedef struct nm_sidecar_info {
+  uint64_t n_nodes, n_tets;
+  uint64_t mesh_fingerprint; /* nm_mesh_fingerprint of the labeled mesh */
+  int K;                     /* compartments (label_ids[0..K)) */
+  int has_masks;             /* node masks follow the labels */
+  int is_lattice;            /* origin/h/n describe the mesh (generate_lattice_mesh) */
+  int reserved;
+  int label_ids[32];
+  double threshold;          /* T of the labeling */
+  double origin[3];
+  double h;
+  int n[3];
+  int reserved2;
+} nm_sidecar_info;
+
+/* Order-independent 64-bit fingerprint of a mesh (fp64 node bits + tet
+ * indices); host and device versions give the same value. */
+int nm_mesh_fingerprint(const double* nodes, size_t n_nodes, const uint32_t* tets, size_t nt, uint64_t* fp);
+int nm_mesh_fingerprint_device(nm_ctx* ctx, const double* d_nodes, size_t n_nodes, const uint32_t* d_tets, size_t nt,
+                               uint64_t* fp, void* stream);
+int nm_sidecar_write(const char* path, const nm_sidecar_info* info, const int* labels, const uint32_t* masks /* nullable */);
+int nm_sidecar_read_info(const char* path, nm_sidecar_info* info);
+/* labels: n_tets entries; masks: n_nodes entries when has_masks (nullable: skipped) */
+int nm_sidecar_read(const char* path, nm_sidecar_info* info, int* labels, uint32_t* masks);
+/* initial_label of a regular lattice straight to a sidecar: the lattice is
+ * generated, labeled and fingerprinted on the device; only labels (+ masks)
+ * cross to the host, into the file. info_out (nullable) receives the header. */
+int nm_label_lattice_sidecar(nm_ctx* ctx, const double* origin, double h, int nx, int ny, int nz, double threshold,
+                             const char* path, int with_masks, nm_sidecar_info* info_out, nm_stats* stats);
+
 #ifdef __cplusplus
 }
 #endif

@@ -75,6 +75,8 @@ def ref():
         R.ref_boundary.restype = ctypes.c_long
         R.ref_validate_mesh_ok.argtypes = [_d, _sz, _u32, _sz]
         R.ref_validate_mesh_ok.restype = ctypes.c_int
+        R.ref_save_tetmesh.argtypes = [ctypes.c_char_p, _d, _sz, _u32, _i32, _sz]
+        R.ref_load_tetmesh.argtypes = [ctypes.c_char_p, ctypes.POINTER(_sz), ctypes.POINTER(_sz), _d, _u32, _i32]
         _ref = R
     return _ref
 
@@ -94,6 +96,27 @@ def ref_boundary(tets, labels, label_set):
     if c < 0:
         raise KeyError(f"UnknownLabel {label_set}")
     return tri[:c].copy(), nodes[:nn.value].copy()
+
+
+def ref_save_tetmesh(path, nodes, tets, labels):
+    """The UNMODIFIED reference save_tetmesh (tetmesh v1 text, mesh.hpp:238-289)."""
+    nodes = np.ascontiguousarray(nodes, np.float64).reshape(-1, 3)
+    tets = np.ascontiguousarray(tets, np.uint32).reshape(-1, 4)
+    labels = np.ascontiguousarray(labels, np.int32)
+    assert ref().ref_save_tetmesh(str(path).encode(), _p(nodes, ctypes.c_double), nodes.shape[0],
+                                  _p(tets, ctypes.c_uint32), _p(labels, ctypes.c_int), tets.shape[0]) == 0
+
+
+def ref_load_tetmesh(path):
+    R = ref()
+    nn, nt = _sz(), _sz()
+    assert R.ref_load_tetmesh(str(path).encode(), ctypes.byref(nn), ctypes.byref(nt), None, None, None) == 0
+    nodes = np.empty((nn.value, 3), np.float64)
+    tets = np.empty((nt.value, 4), np.uint32)
+    labels = np.empty(nt.value, np.int32)
+    assert R.ref_load_tetmesh(str(path).encode(), ctypes.byref(nn), ctypes.byref(nt), _p(nodes, ctypes.c_double),
+                              _p(tets, ctypes.c_uint32), _p(labels, ctypes.c_int)) == 0
+    return nodes, tets, labels
 
 
 def workers_default() -> int:

@@ -144,4 +144,44 @@ int ref_validate_mesh_ok(const double* nodes, std::size_t nn, const std::uint32_
   return validate_mesh(m).ok() ? 1 : 0;
 }
 
+// mesh.hpp:238-289 tetmesh v1 text export / import (the format the label
+// sidecar sits next to)
+int ref_save_tetmesh(const char* path, const double* nodes, std::size_t nn, const std::uint32_t* tets,
+                     const int* labels, std::size_t nt) {
+  try {
+    TetrahedralMesh m;
+    m.nodes.resize(nn);
+    for (std::size_t i = 0; i < nn; ++i) m.nodes[i] = Vec3{nodes[3 * i], nodes[3 * i + 1], nodes[3 * i + 2]};
+    m.tetrahedra.resize(nt);
+    m.labels.assign(labels, labels + nt);
+    for (std::size_t t = 0; t < nt; ++t) std::memcpy(m.tetrahedra[t].data(), tets + 4 * t, 16);
+    save_tetmesh(path, m);
+    return 0;
+  } catch (...) {
+    return 1;
+  }
+}
+
+// sizes first (nodes/tets/labels null), then the arrays
+int ref_load_tetmesh(const char* path, std::size_t* nn, std::size_t* nt, double* nodes, std::uint32_t* tets,
+                     int* labels) {
+  try {
+    const TetrahedralMesh m = load_tetmesh(path);
+    *nn = m.node_count();
+    *nt = m.tet_count();
+    if (nodes)
+      for (std::size_t i = 0; i < m.node_count(); ++i) {
+        nodes[3 * i] = m.nodes[i].x;
+        nodes[3 * i + 1] = m.nodes[i].y;
+        nodes[3 * i + 2] = m.nodes[i].z;
+      }
+    if (tets)
+      for (std::size_t t = 0; t < m.tet_count(); ++t) std::memcpy(tets + 4 * t, m.tetrahedra[t].data(), 16);
+    if (labels) std::memcpy(labels, m.labels.data(), m.tet_count() * sizeof(int));
+    return 0;
+  } catch (...) {
+    return 1;
+  }
+}
+
 }  // extern "C"

@@ -63,6 +63,31 @@ class NmStats(ctypes.Structure):
         return {name: getattr(self, name) for name, _ in self._fields_}
 
 
+class NmSidecarInfo(ctypes.Structure):
+    _fields_ = [
+        ("n_nodes", ctypes.c_uint64),
+        ("n_tets", ctypes.c_uint64),
+        ("mesh_fingerprint", ctypes.c_uint64),
+        ("K", ctypes.c_int),
+        ("has_masks", ctypes.c_int),
+        ("is_lattice", ctypes.c_int),
+        ("reserved", ctypes.c_int),
+        ("label_ids", ctypes.c_int * 32),
+        ("threshold", ctypes.c_double),
+        ("origin", ctypes.c_double * 3),
+        ("h", ctypes.c_double),
+        ("n", ctypes.c_int * 3),
+        ("reserved2", ctypes.c_int),
+    ]
+
+    def as_dict(self) -> dict:
+        d = {name: getattr(self, name) for name, _ in self._fields_ if not name.startswith("reserved")}
+        d["label_ids"] = list(self.label_ids)[: self.K]
+        d["origin"] = tuple(self.origin)
+        d["n"] = tuple(self.n)
+        return d
+
+
 # name -> (restype, argtypes); mirrors include/nestmesh_label.h exactly.
 LABEL_API = {
     "nm_abi_version": (ctypes.c_int, []),
@@ -137,6 +162,16 @@ LABEL_API = {
     "nm_surface_segments": (ctypes.c_int, [ctypes.c_void_p, c_size_p, c_size_p]),
     "nm_cell_info": (ctypes.c_int, [ctypes.c_void_p] + [ctypes.POINTER(ctypes.c_uint64)] * 3
                      + [c_double_p] + [ctypes.POINTER(ctypes.c_uint64)] * 2),
+    "nm_mesh_fingerprint": (ctypes.c_int, [c_double_p, ctypes.c_size_t, c_u32_p, ctypes.c_size_t,
+                                           ctypes.POINTER(ctypes.c_uint64)]),
+    "nm_mesh_fingerprint_device": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p,
+                                                  ctypes.c_size_t, ctypes.POINTER(ctypes.c_uint64), ctypes.c_void_p]),
+    "nm_sidecar_write": (ctypes.c_int, [ctypes.c_char_p, ctypes.POINTER(NmSidecarInfo), c_i32_p, c_u32_p]),
+    "nm_sidecar_read_info": (ctypes.c_int, [ctypes.c_char_p, ctypes.POINTER(NmSidecarInfo)]),
+    "nm_sidecar_read": (ctypes.c_int, [ctypes.c_char_p, ctypes.POINTER(NmSidecarInfo), c_i32_p, c_u32_p]),
+    "nm_label_lattice_sidecar": (ctypes.c_int, [ctypes.c_void_p, c_double_p, ctypes.c_double, ctypes.c_int,
+                                                ctypes.c_int, ctypes.c_int, ctypes.c_double, ctypes.c_char_p,
+                                                ctypes.c_int, ctypes.POINTER(NmSidecarInfo), ctypes.POINTER(NmStats)]),
 }
 
 _lib = None
@@ -341,6 +376,24 @@ class Context:
                                         ptr(labels, ctypes.c_int),
                                         ptr(masks, ctypes.c_uint32) if masks is not None else None, ctypes.byref(st)))
         return labels, masks, st.as_dict()
+
+    def label_lattice_sidecar(self, origin, h, n, path, threshold=0.5, with_masks=True):
+        """initial_label of a regular lattice written straight to a label
+        sidecar (nm_label_lattice_sidecar): returns (info dict, stats)."""
+        o = np.ascontiguousarray(origin, dtype=np.float64)
+        info = NmSidecarInfo()
+        st = NmStats()
+        check(self.lib.nm_label_lattice_sidecar(self.handle, ptr(o, ctypes.c_double), float(h), int(n[0]), int(n[1]),
+                                                int(n[2]), threshold, str(path).encode(), int(bool(with_masks)),
+                                                ctypes.byref(info), ctypes.byref(st)))
+        return info.as_dict(), st.as_dict()
+
+    def mesh_fingerprint_device(self, d_nodes, d_tets, stream=None):
+        fp = ctypes.c_uint64()
+        check(self.lib.nm_mesh_fingerprint_device(self.handle, ctypes.c_void_p(d_nodes.data_ptr()), d_nodes.shape[0],
+                                                  ctypes.c_void_p(d_tets.data_ptr()), d_tets.shape[0],
+                                                  ctypes.byref(fp), stream_handle(stream)))
+        return fp.value
 
     def lattice_device(self, origin, h, n, d_nodes, d_tets, stream=None):
         o = np.ascontiguousarray(origin, dtype=np.float64)
@@ -565,6 +618,58 @@ def sample_surface(xyz, tri, count, seed=0):
                                           seed, ptr(out, ctypes.c_double)) != 0:
         raise NativeError("empty surface")
     return out
+
+
+def mesh_fingerprint(nodes, tets) -> int:
+    """nm_mesh_fingerprint (host): order-independent 64-bit mesh fingerprint."""
+    nodes = np.ascontiguousarray(nodes, dtype=np.float64).reshape(-1, 3)
+    tets = np.ascontiguousarray(tets, dtype=np.uint32).reshape(-1, 4)
+    fp = ctypes.c_uint64()
+    check(load_label_lib().nm_mesh_fingerprint(ptr(nodes, ctypes.c_double), nodes.shape[0],
+                                               ptr(tets, ctypes.c_uint32), tets.shape[0], ctypes.byref(fp)))
+    return fp.value
+
+
+def sidecar_write(path, labels, masks=None, *, n_nodes=None, mesh_fingerprint=0, label_ids=(), threshold=0.5,
+                  lattice=None):
+    """Write a label sidecar. lattice = (origin, h, (nx, ny, nz)) marks a
+    generate_lattice_mesh mesh."""
+    labels = np.ascontiguousarray(labels, dtype=np.int32)
+    info = NmSidecarInfo()
+    info.n_tets = labels.shape[0]
+    info.n_nodes = n_nodes if n_nodes is not None else (0 if masks is None else len(masks))
+    info.mesh_fingerprint = mesh_fingerprint
+    info.K = len(label_ids)
+    for k, v in enumerate(label_ids):
+        info.label_ids[k] = int(v)
+    info.threshold = threshold
+    m = None
+    if masks is not None:
+        m = np.ascontiguousarray(masks, dtype=np.uint32)
+        if m.shape[0] != info.n_nodes:
+            raise ValueError("masks length != n_nodes")
+        info.has_masks = 1
+    if lattice is not None:
+        (o, h, n) = lattice
+        info.is_lattice = 1
+        for a in range(3):
+            info.origin[a] = float(o[a])
+            info.n[a] = int(n[a])
+        info.h = float(h)
+    check(load_label_lib().nm_sidecar_write(str(path).encode(), ctypes.byref(info), ptr(labels, ctypes.c_int),
+                                            ptr(m, ctypes.c_uint32) if m is not None else None))
+
+
+def sidecar_read(path):
+    """(info dict, labels int32, masks uint32 or None)."""
+    lib = load_label_lib()
+    info = NmSidecarInfo()
+    check(lib.nm_sidecar_read_info(str(path).encode(), ctypes.byref(info)))
+    labels = np.empty(info.n_tets, np.int32)
+    masks = np.empty(info.n_nodes, np.uint32) if info.has_masks else None
+    check(lib.nm_sidecar_read(str(path).encode(), ctypes.byref(info), ptr(labels, ctypes.c_int),
+                              ptr(masks, ctypes.c_uint32) if masks is not None else None))
+    return info.as_dict(), labels, masks
 
 
 def exported_symbols(path=LABEL_LIB) -> set:

@@ -45,7 +45,7 @@ def _stale(out: Path, deps) -> bool:
 
 def LABEL_SOURCES():
     """CUDA translation units of libnestmesh_label.so (context.cuh is shared)."""
-    return [str(CSRC / f) for f in ("nestmesh_label.cu", "cell_build.cu", "group.cu", "mesh_ops.cu")]
+    return [str(CSRC / f) for f in ("nestmesh_label.cu", "cell_build.cu", "group.cu", "mesh_ops.cu", "sidecar.cu")]
 
 
 def compile_label_lib(out: Path, defs=(), log=None):

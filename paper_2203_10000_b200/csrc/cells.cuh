@@ -168,8 +168,8 @@ struct ClassifyParams {
   int K;
   bool preset;  // write the known inside bits into masks (false: masks = 0; sharded passes, shard > 0)
   std::uint32_t* unk;
-  std::uint32_t* masks;
-  std::uint32_t* flagmask;
+  std::uint32_t* masks;     // by point id
+  std::uint32_t* flagmask;  // by evaluation position
   double* s_out;
 };
 
@@ -214,7 +214,7 @@ static __global__ void k_cell_classify(const ClassifyParams prm) {
     }
     prm.unk[i] = unk;
     prm.masks[j] = prm.preset ? ins : 0u;
-    prm.flagmask[j] = 0u;
+    prm.flagmask[i] = 0u;  // flags are indexed by evaluation position
     if (prm.s_out)
       for (int c = 0; c < prm.K; ++c)
         if (!((unk >> c) & 1u)) prm.s_out[j * prm.K + c] = ((ins >> c) & 1u) ? 1.0 : 0.0;

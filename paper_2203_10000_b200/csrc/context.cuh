@@ -149,7 +149,6 @@ struct nm_ctx {
   // surfaces
   bool has_surfaces = false;
   bool strips = false;  // tile layout of the current surfaces
-  std::size_t flag_cap = 0;  // flagmask length when evaluating a subset (= node count)
   int K = 0;
   std::size_t nt_real = 0, nt_pad = 0, nv = 0;
   double cx = 0, cy = 0, cz = 0;
@@ -171,7 +170,7 @@ struct nm_ctx {
       dist_idx, dist_d32, dist_out, r_red, r_keys, r_keys2, r_S, r_idx, r_touched,
       r_mask, r_cnt, r_offs, r_flag, meshA_nodes, meshA_tets, meshA_labels, meshB_nodes, meshB_tets, meshB_labels,
       meshB_parent, masks2, order, keys, keys_alt, order_alt, cub_tmp, list, chunk, counters, count, tets, labels,
-      s_out, word, pair_cnt, pairs;
+      s_out, word, pair_cnt, pairs, pos_masks, fix_part;
 
   ~nm_ctx() {
     for (nmh::DBuf* b : {&dist_clus, &dist_slot, &dist_ord, &sp_part, &sp_det, &cell_state, &cell_child, &cell_cert, &cell_blk, &cell_grids, &clus, &clus_tri, &clus_tsph, &unk, &sp_list, &sp_chunk, &sp_cnt, &rep_pts, &rep_s,
@@ -181,7 +180,7 @@ struct nm_ctx {
                     &dist_tri, &dist_xyz, &dist_idx, &dist_d32, &dist_out, &r_red, &r_keys, &r_keys2, &r_S,
                     &r_idx, &r_touched, &r_mask, &r_cnt, &r_offs, &r_flag, &meshA_nodes, &meshA_tets, &meshA_labels,
                     &meshB_nodes, &meshB_tets, &meshB_labels, &meshB_parent, &masks2, &order, &keys,
-                    &keys_alt, &order_alt, &cub_tmp, &list, &chunk, &counters, &count, &tets, &labels, &s_out, &word, &pair_cnt, &pairs})
+                    &keys_alt, &order_alt, &cub_tmp, &list, &chunk, &counters, &count, &tets, &labels, &s_out, &word, &pair_cnt, &pairs, &pos_masks, &fix_part})
       b->release();
     for (auto& e : ev)
       if (e) cudaEventDestroy(e);

@@ -128,8 +128,12 @@ struct LabelParams {
   double cx, cy, cz;         // centring offset of the fp32 frame
   double T, band;
   float tau, delta;
-  std::uint32_t* masks;      // n
-  std::uint32_t* flagmask;   // n (bit k: pair (i,k) needs the fp64 fix-up)
+  // Outputs. Dense modes (0, 1) write both at the EVALUATION POSITION i
+  // (coalesced; the host un-permutes the masks with k_unpermute); the sparse
+  // mode ORs masks into masks[point id] (preset by k_cell_classify) and flags
+  // into flagmask[position]. Flags stay position-indexed for the fix-up.
+  std::uint32_t* masks;
+  std::uint32_t* flagmask;   // bit k: pair (point at position i, k) needs the fp64 fix-up
   const std::uint32_t* cull;  // per evaluation position: bit k = outside compartment k's 13-DOP
                               // (k_cull_mask); nullptr = off
   double* s_out;             // n*K or nullptr
@@ -501,12 +505,15 @@ static __global__ void __launch_bounds__(kBlock, (NP == 1 ? NM_MIN_BLOCKS : NM_M
 #pragma unroll
   for (int k = 0; k < P; ++k) {
     if (valid[k] && !(SPARSE && prm.sp_part)) {
-      if (gridDim.y == 1 && !SPARSE) {
-        prm.masks[pid[k]] = mask[k];
-        prm.flagmask[pid[k]] = fmask[k];
-      } else {
+      if (SPARSE) {
         if (mask[k]) atomicOr(prm.masks + pid[k], mask[k]);
-        if (fmask[k]) atomicOr(prm.flagmask + pid[k], fmask[k]);
+        if (fmask[k]) atomicOr(prm.flagmask + prm.sp_list[base + k], fmask[k]);
+      } else if (gridDim.y == 1) {  // evaluation order: coalesced stores
+        prm.masks[base + k] = mask[k];
+        prm.flagmask[base + k] = fmask[k];
+      } else {
+        if (mask[k]) atomicOr(prm.masks + base + k, mask[k]);
+        if (fmask[k]) atomicOr(prm.flagmask + base + k, fmask[k]);
       }
     }
   }
@@ -542,8 +549,8 @@ struct FinalizeParams {
   std::uint32_t po[32], fb[32];
   int K;
   double T, band;
-  std::uint32_t* masks;
-  std::uint32_t* flagmask;
+  std::uint32_t* masks;     // by point id
+  std::uint32_t* flagmask;  // by evaluation position
   double* s_out;
 };
 
@@ -565,7 +572,7 @@ static __global__ void k_sparse_finalize(const FinalizeParams prm) {
     const std::uint32_t j = prm.order ? prm.order[pos] : pos;
     const double s = acc * kInv2Pi;
     if (s >= prm.T) atomicOr(prm.masks + j, 1u << c);
-    if (det || !(fabs(s - prm.T) >= prm.band)) atomicOr(prm.flagmask + j, 1u << c);
+    if (det || !(fabs(s - prm.T) >= prm.band)) atomicOr(prm.flagmask + pos, 1u << c);
     if (prm.s_out) prm.s_out[static_cast<std::size_t>(j) * prm.K + c] = s;
   }
 }
@@ -674,9 +681,16 @@ static __global__ void __launch_bounds__(kSelBlock) k_select_write(Pred pred, st
 
 struct PredNonzero {
   const std::uint32_t* v;
-  const std::uint32_t* subset;  // nullable: item i is v[subset[i]]
-  __device__ bool operator()(std::size_t i) const { return v[subset ? subset[i] : i] != 0u; }
+  __device__ bool operator()(std::size_t i) const { return v[i] != 0u; }
 };
+
+// Dense node passes: masks[point id] = ms[evaluation position].
+static __global__ void k_unpermute(const std::uint32_t* __restrict__ order, std::size_t n,
+                                   const std::uint32_t* __restrict__ ms, std::uint32_t* __restrict__ masks) {
+  for (std::size_t i = blockIdx.x * static_cast<std::size_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<std::size_t>(gridDim.x) * blockDim.x)
+    masks[order ? __ldg(order + i) : i] = __ldg(ms + i);
+}
 
 struct PredStraddle {
   const uint4* tets;
@@ -705,14 +719,15 @@ struct PredStraddle {
 // ---------------------------------------------------------------------------
 struct FixupParams {
   const double* pts;
-  const std::uint32_t* list;    // flagged positions (point ids, or indices into subset)
-  const std::uint32_t* subset;  // nullable
+  const std::uint32_t* list;    // flagged evaluation positions
+  const std::uint32_t* order;   // position -> point id (nullable: identity)
   const std::uint32_t* count;   // device count of list
-  const std::uint32_t* flagmask;
+  const std::uint32_t* flagmask;  // by position
   const double* tri64;          // de-indexed fp64 triangles: 9 doubles per triangle, compartment ranges of comp_off
   const std::uint32_t* comp_off;  // K+1
   const std::uint32_t* pair_cnt;  // K: flagged pairs per compartment
   const std::uint32_t* pairs;     // per compartment (prefix of pair_cnt): positions into list
+  double* part;                   // per pair and triangle chunk: fp64 partial sums
   int K;
   double T, tie_eps;
   std::uint32_t* masks;
@@ -724,19 +739,19 @@ constexpr int kFixThreads = 128;
 constexpr int kFixLanes = 8;                          // threads per pair
 constexpr int kFixPairs = kFixThreads / kFixLanes;    // pairs per batch
 constexpr int kFixTile = 128;                         // triangles per shared-memory tile
+constexpr int kFixChunk = 2048;                       // triangles per work item (multiple of kFixTile)
 
-static __global__ void k_fix_count(const std::uint32_t* list, const std::uint32_t* subset, const std::uint32_t* count,
-                                   const std::uint32_t* flagmask, std::uint32_t* pair_cnt) {
+static __global__ void k_fix_count(const std::uint32_t* list, const std::uint32_t* count, const std::uint32_t* flagmask,
+                                   std::uint32_t* pair_cnt) {
   const std::uint32_t n = *count;
   for (std::uint32_t w = blockIdx.x * blockDim.x + threadIdx.x; w < n; w += gridDim.x * blockDim.x) {
-    const std::uint32_t i = subset ? subset[list[w]] : list[w];
-    for (std::uint32_t fm = flagmask[i]; fm; fm &= fm - 1) atomicAdd(pair_cnt + (__ffs(fm) - 1), 1u);
+    for (std::uint32_t fm = flagmask[list[w]]; fm; fm &= fm - 1) atomicAdd(pair_cnt + (__ffs(fm) - 1), 1u);
   }
 }
 
 // pair_fill: per-compartment cursors (zeroed); lists at the prefix of pair_cnt
-static __global__ void k_fix_fill(const std::uint32_t* list, const std::uint32_t* subset, const std::uint32_t* count,
-                                  const std::uint32_t* flagmask, const std::uint32_t* pair_cnt, int K,
+static __global__ void k_fix_fill(const std::uint32_t* list, const std::uint32_t* count, const std::uint32_t* flagmask,
+                                  const std::uint32_t* pair_cnt, int K,
                                   std::uint32_t* pair_fill, std::uint32_t* pairs) {
   __shared__ std::uint32_t off[33];
   if (threadIdx.x == 0) {
@@ -749,8 +764,7 @@ static __global__ void k_fix_fill(const std::uint32_t* list, const std::uint32_t
   __syncthreads();
   const std::uint32_t n = *count;
   for (std::uint32_t w = blockIdx.x * blockDim.x + threadIdx.x; w < n; w += gridDim.x * blockDim.x) {
-    const std::uint32_t i = subset ? subset[list[w]] : list[w];
-    for (std::uint32_t fm = flagmask[i]; fm; fm &= fm - 1) {
+    for (std::uint32_t fm = flagmask[list[w]]; fm; fm &= fm - 1) {
       const int c = __ffs(fm) - 1;
       pairs[off[c] + atomicAdd(pair_fill + c, 1u)] = w;
     }
@@ -766,42 +780,55 @@ static __global__ void k_deindex64(const double* xyz, const std::uint32_t* tri, 
   }
 }
 
+// Work item (CTA): compartment c, a batch of kFixPairs of its pairs and a
+// chunk of kFixChunk of its triangles. The chunk partial of every pair goes
+// to part[poff_c + j * nchunk_c + chunk]; k_fix_finalize adds the chunks in
+// order. Both the chunking and the lane striding depend only on c's triangle
+// count, so s is a pure function of (point, compartment).
+__device__ __forceinline__ std::uint32_t fix_nchunk(std::uint32_t ntri) {
+  return max(1u, (ntri + kFixChunk - 1) / kFixChunk);
+}
+
 static __global__ void __launch_bounds__(kFixThreads) k_fixup(const FixupParams prm) {
   __shared__ double s_tri[kFixTile * 9];
-  __shared__ std::uint32_t s_off[33], s_bo[33];
+  __shared__ std::uint32_t s_off[33], s_wo[33], s_po[33];
   const int K = prm.K;
   if (threadIdx.x == 0) {
-    std::uint32_t o = 0, b = 0;
+    std::uint32_t o = 0, wo = 0, po = 0;
     for (int c = 0; c < K; ++c) {
+      const std::uint32_t nch = fix_nchunk(prm.comp_off[c + 1] - prm.comp_off[c]);
       s_off[c] = o;
-      s_bo[c] = b;
+      s_wo[c] = wo;
+      s_po[c] = po;
       o += prm.pair_cnt[c];
-      b += (prm.pair_cnt[c] + kFixPairs - 1) / kFixPairs;
+      wo += (prm.pair_cnt[c] + kFixPairs - 1) / kFixPairs * nch;
+      po += prm.pair_cnt[c] * nch;
     }
-    s_bo[K] = b;
+    s_wo[K] = wo;
   }
   __syncthreads();
-  const std::uint32_t nbatch = s_bo[K];
+  const std::uint32_t nwork = s_wo[K];
   const int slot = threadIdx.x / kFixLanes, lane = threadIdx.x % kFixLanes;
-  unsigned long long pairs = 0, ties = 0;
-  for (std::uint32_t bt = blockIdx.x; bt < nbatch; bt += gridDim.x) {  // CTA-uniform loop
+  for (std::uint32_t wk = blockIdx.x; wk < nwork; wk += gridDim.x) {  // CTA-uniform loop
     int c = 0;
-    while (c + 1 < K && bt >= s_bo[c + 1]) ++c;
-    const std::uint32_t j = (bt - s_bo[c]) * kFixPairs + slot;
+    while (c + 1 < K && wk >= s_wo[c + 1]) ++c;
+    const std::uint32_t lo = prm.comp_off[c], hi = prm.comp_off[c + 1];
+    const std::uint32_t nch = fix_nchunk(hi - lo);
+    const std::uint32_t l = wk - s_wo[c], batch = l / nch, chunk = l % nch;
+    const std::uint32_t j = batch * kFixPairs + slot;
     const bool has = j < prm.pair_cnt[c];
-    std::uint32_t i = 0;
     double px = 0.0, py = 0.0, pz = 0.0;
     if (has) {
       const std::uint32_t w = prm.pairs[s_off[c] + j];
-      i = prm.subset ? prm.subset[prm.list[w]] : prm.list[w];
+      const std::uint32_t i = prm.order ? prm.order[prm.list[w]] : prm.list[w];
       px = prm.pts[3 * static_cast<std::size_t>(i)];
       py = prm.pts[3 * static_cast<std::size_t>(i) + 1];
       pz = prm.pts[3 * static_cast<std::size_t>(i) + 2];
     }
-    const std::uint32_t lo = prm.comp_off[c], hi = prm.comp_off[c + 1];
+    const std::uint32_t c0 = lo + chunk * kFixChunk, c1 = min(hi, c0 + kFixChunk);
     double sum = 0.0;
-    for (std::uint32_t t0 = lo; t0 < hi; t0 += kFixTile) {
-      const std::uint32_t m = min(static_cast<std::uint32_t>(kFixTile), hi - t0);
+    for (std::uint32_t t0 = c0; t0 < c1; t0 += kFixTile) {
+      const std::uint32_t m = min(static_cast<std::uint32_t>(kFixTile), c1 - t0);
       __syncthreads();  // the previous tile is consumed
       const double* src = prm.tri64 + 9 * static_cast<std::size_t>(t0);
       for (std::uint32_t q = threadIdx.x; q < 9 * m; q += kFixThreads) s_tri[q] = __ldg(src + q);
@@ -815,21 +842,50 @@ static __global__ void __launch_bounds__(kFixThreads) k_fixup(const FixupParams 
     }
 #pragma unroll
     for (int o = kFixLanes / 2; o > 0; o >>= 1) sum += __shfl_xor_sync(kFull, sum, o, kFixLanes);
-    if (has && lane == 0) {
-      const double s = sum / (2.0 * CUDART_PI);
-      if (s >= prm.T) atomicOr(prm.masks + i, 1u << c);
-      else atomicAnd(prm.masks + i, ~(1u << c));
-      ++pairs;
-      if (fabs(s - prm.T) < prm.tie_eps) ++ties;
-      if (prm.s_out) prm.s_out[static_cast<std::size_t>(i) * prm.K + c] = s;
+    if (has && lane == 0) prm.part[s_po[c] + j * nch + chunk] = sum;
+  }
+}
+
+// Per pair: the chunk partials added in chunk order, then threshold, tie
+// count and s (the fp64 result replaces the fp32 pass's bit).
+static __global__ void k_fix_finalize(const FixupParams prm) {
+  __shared__ std::uint32_t s_off[33], s_po[33], s_nch[32];
+  const int K = prm.K;
+  if (threadIdx.x == 0) {
+    std::uint32_t o = 0, po = 0;
+    for (int c = 0; c < K; ++c) {
+      const std::uint32_t nch = fix_nchunk(prm.comp_off[c + 1] - prm.comp_off[c]);
+      s_off[c] = o;
+      s_po[c] = po;
+      s_nch[c] = nch;
+      o += prm.pair_cnt[c];
+      po += prm.pair_cnt[c] * nch;
     }
+    s_off[K] = o;
+  }
+  __syncthreads();
+  unsigned pairs = 0, ties = 0;
+  for (std::uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < s_off[K]; q += gridDim.x * blockDim.x) {
+    int c = 0;
+    while (c + 1 < K && q >= s_off[c + 1]) ++c;
+    const std::uint32_t j = q - s_off[c], nch = s_nch[c];
+    double tot = 0.0;
+    for (std::uint32_t b = 0; b < nch; ++b) tot += prm.part[s_po[c] + j * nch + b];
+    const std::uint32_t w = prm.pairs[q];
+    const std::uint32_t i = prm.order ? prm.order[prm.list[w]] : prm.list[w];
+    const double s = tot / (2.0 * CUDART_PI);
+    if (s >= prm.T) atomicOr(prm.masks + i, 1u << c);
+    else atomicAnd(prm.masks + i, ~(1u << c));
+    ++pairs;
+    if (fabs(s - prm.T) < prm.tie_eps) ++ties;
+    if (prm.s_out) prm.s_out[static_cast<std::size_t>(i) * prm.K + c] = s;
   }
   if (prm.counters) {
-    pairs = __reduce_add_sync(kFull, static_cast<unsigned>(pairs));
-    ties = __reduce_add_sync(kFull, static_cast<unsigned>(ties));
+    pairs = __reduce_add_sync(kFull, pairs);
+    ties = __reduce_add_sync(kFull, ties);
     if ((threadIdx.x & 31) == 0 && (pairs || ties)) {
-      atomicAdd(prm.counters + 2, pairs);
-      atomicAdd(prm.counters + 3, ties);
+      atomicAdd(prm.counters + 2, static_cast<unsigned long long>(pairs));
+      atomicAdd(prm.counters + 3, static_cast<unsigned long long>(ties));
     }
   }
 }
@@ -1173,15 +1229,13 @@ static __global__ void k_cull_mask(const double* pts, const std::uint32_t* order
   }
 }
 
-// masks / flagmask of the evaluated points cleared before a compartment-split
-// k_label launch (which ORs its bits in).
-static __global__ void k_zero_masks(std::size_t n, const std::uint32_t* subset, std::uint32_t* masks,
-                             std::uint32_t* flagmask) {
+// Position-indexed masks / flags cleared before a compartment-split k_label
+// launch (which ORs its bits in).
+static __global__ void k_zero_masks(std::size_t n, std::uint32_t* masks, std::uint32_t* flagmask) {
   for (std::size_t i = blockIdx.x * static_cast<std::size_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<std::size_t>(gridDim.x) * blockDim.x) {
-    const std::size_t j = subset ? subset[i] : i;
-    masks[j] = 0u;
-    flagmask[j] = 0u;
+    masks[i] = 0u;
+    flagmask[i] = 0u;
   }
 }
 

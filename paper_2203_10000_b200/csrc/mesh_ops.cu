@@ -499,7 +499,6 @@ int nm_relabel(nm_ctx* c, const double* nodes, std::size_t n, const std::uint32_
     NM_CUDA(cudaMemsetAsync(d_masks, 0, std::max<std::size_t>(n, 1) * sizeof(std::uint32_t), st));
     const uint4* t4 = reinterpret_cast<const uint4*>(d_tets);
     face_adjacency(c, t4, nt, d_nbr, st);
-    c->flag_cap = std::max<std::size_t>(n, 1);
     int pass = 0;
     *converged = 0;
     std::uint64_t evaluated_total = 0;

@@ -327,10 +327,11 @@ void label_nodes_dev(nm_ctx* c, const double* d_pts, std::size_t n, double T, st
     return;
   }
   if (n > 0xffffffffull) throw Error("more than 2^32 points in one call");
-  auto* flagmask = c->flagmask.as<std::uint32_t>(d_subset ? c->flag_cap : n);
+  auto* flagmask = c->flagmask.as<std::uint32_t>(n);  // by evaluation position
   // every scratch buffer is sized before the first launch: a growing DBuf
   // frees its old block, and cudaFree would wait for the kernels
   auto* list = c->list.as<std::uint32_t>(n);
+  auto* ms = c->pos_masks.as<std::uint32_t>(n);  // dense passes: masks by evaluation position
   auto* d_count = c->count.as<std::uint32_t>(4);
   (void)c->chunk.as<std::uint32_t>(std::max<std::size_t>(1, (n + nm::kSelChunk - 1) / nm::kSelChunk));
   const std::uint32_t* order = d_subset;
@@ -366,7 +367,7 @@ void label_nodes_dev(nm_ctx* c, const double* d_pts, std::size_t n, double T, st
   prm.band = c->opt.band;
   prm.tau = c->opt.tau;
   prm.delta = c->opt.delta_mm;
-  prm.masks = d_masks;
+  prm.masks = d_masks;  // sparse passes; dense passes write ms (below)
   prm.flagmask = flagmask;
   prm.cull = nullptr;
   if ((c->opt.cull_outside == 2 && c->cells) || nshards >= 1) {
@@ -398,12 +399,13 @@ void label_nodes_dev(nm_ctx* c, const double* d_pts, std::size_t n, double T, st
   }
   prm.s_out = d_s;
   prm.counters = counters;
+  prm.masks = ms;
   const int np = prm.cull ? 1 : c->opt.pairs_per_thread;
   const std::size_t per_block = static_cast<std::size_t>(nm::kBlock) * 2 * np;
   const std::size_t nblocks = (n + per_block - 1) / per_block;
   const int csplit = compartment_split(c, nblocks, prm.split);
   if (csplit > 1) {
-    nm::k_zero_masks<<<grid_for(n, 256, c->sm_count * 16), 256, 0, st>>>(n, d_subset, d_masks, flagmask);
+    nm::k_zero_masks<<<grid_for(n, 256, c->sm_count * 16), 256, 0, st>>>(n, ms, flagmask);
     ++launches;
   }
   if (stats) NM_CUDA(cudaEventRecord(c->ev[1], st));
@@ -424,47 +426,57 @@ void label_nodes_dev(nm_ctx* c, const double* d_pts, std::size_t n, double T, st
   }
   NM_CUDA(cudaGetLastError());
   ++launches;
+  nm::k_unpermute<<<grid_for(n, 256, c->sm_count * 16), 256, 0, st>>>(order, n, ms, d_masks);
+  NM_CUDA(cudaGetLastError());
+  ++launches;
   }
   if (stats) NM_CUDA(cudaEventRecord(c->ev[2], st));
   // compaction of flagged points, per-compartment pair lists, fp64 fix-up
-  select(c, nm::PredNonzero{flagmask, d_subset}, n, list, d_count, st, launches);
+  select(c, nm::PredNonzero{flagmask}, n, list, d_count, st, launches);
   const int K = c->K;
   auto* pair_cnt = c->pair_cnt.as<std::uint32_t>(2 * 32);
   NM_CUDA(cudaMemsetAsync(pair_cnt, 0, 2 * 32 * sizeof(std::uint32_t), st));
-  nm::k_fix_count<<<grid_for(n, 256, c->sm_count * 4), 256, 0, st>>>(list, d_subset, d_count, flagmask, pair_cnt);
+  nm::k_fix_count<<<grid_for(n, 256, c->sm_count * 4), 256, 0, st>>>(list, d_count, flagmask, pair_cnt);
   NM_CUDA(cudaGetLastError());
   // one host synchronisation: the pair lists' size (the fix-up is the only
   // consumer, and its batch grid runs from the device-side counts)
   NM_CUDA(cudaMemcpyAsync(c->h_pcnt, pair_cnt, K * sizeof(std::uint32_t), cudaMemcpyDeviceToHost, st));
   NM_CUDA(cudaStreamSynchronize(st));
-  std::size_t total = 0;
-  for (int k = 0; k < K; ++k) total += c->h_pcnt[k];
+  std::size_t total = 0, nwork = 0, npart = 0;
+  for (int k = 0; k < K; ++k) {
+    const std::size_t ntri = c->comp_off_h[k + 1] - c->comp_off_h[k];
+    const std::size_t nch = std::max<std::size_t>(1, (ntri + nm::kFixChunk - 1) / nm::kFixChunk);
+    total += c->h_pcnt[k];
+    nwork += (c->h_pcnt[k] + nm::kFixPairs - 1) / nm::kFixPairs * nch;
+    npart += std::size_t(c->h_pcnt[k]) * nch;
+  }
   auto* pairs = c->pairs.as<std::uint32_t>(std::max<std::size_t>(total, 1));
+  auto* part = c->fix_part.as<double>(std::max<std::size_t>(npart, 1));
   launches += 1;
   if (total) {
-    nm::k_fix_fill<<<grid_for(n, 256, c->sm_count * 4), 256, 0, st>>>(list, d_subset, d_count, flagmask, pair_cnt, K,
+    nm::k_fix_fill<<<grid_for(n, 256, c->sm_count * 4), 256, 0, st>>>(list, d_count, flagmask, pair_cnt, K,
                                                                        pair_cnt + 32, pairs);
     nm::FixupParams fp{};
     fp.pts = d_pts;
     fp.list = list;
-    fp.subset = d_subset;
+    fp.order = order;
     fp.count = d_count;
     fp.flagmask = flagmask;
     fp.tri64 = static_cast<const double*>(c->tri64.p);
     fp.comp_off = static_cast<const std::uint32_t*>(c->comp_off.p);
     fp.pair_cnt = pair_cnt;
     fp.pairs = pairs;
+    fp.part = part;
     fp.K = K;
     fp.T = T;
     fp.tie_eps = c->opt.tie_eps;
     fp.masks = d_masks;
     fp.s_out = d_s;
     fp.counters = counters;
-    std::size_t nbatch = 0;
-    for (int k = 0; k < K; ++k) nbatch += (c->h_pcnt[k] + nm::kFixPairs - 1) / nm::kFixPairs;
-    nm::k_fixup<<<grid_for(nbatch, 1, c->sm_count * 8), nm::kFixThreads, 0, st>>>(fp);
+    nm::k_fixup<<<grid_for(nwork, 1, c->sm_count * 16), nm::kFixThreads, 0, st>>>(fp);
+    nm::k_fix_finalize<<<grid_for(total, 256, c->sm_count * 4), 256, 0, st>>>(fp);
     NM_CUDA(cudaGetLastError());
-    launches += 2;
+    launches += 3;
   }
   c->node_launches = launches;
   if (stats) {
