@@ -494,6 +494,44 @@ def main():
         cull["full_mesh_labeling_time_s"] = cull["mode2"]["full_mesh_labeling_time_s"]
         cull["labels_identical"] = cull["mode1"]["labels_identical"] and cull["mode2"]["labels_identical"]
 
+    # The C++ drop-in end to end (include/nestmesh/labeling.hpp, persistent
+    # nestmesh::Labeler; the mesh in the reference's own std::vector types, i.e.
+    # pageable host memory): build/libdropin_bench.so, built with the
+    # reference headers (tests/cpp/dropin_bench.cpp).
+    cpp = None
+    dl = ROOT / "build" / "libdropin_bench.so"
+    if rank == 0 and world == 1 and not args.no_e2e and dl.exists():
+        import ctypes
+        L = ctypes.CDLL(str(dl))
+        P = lambda a, t: a.ctypes.data_as(ctypes.POINTER(t))  # noqa: E731
+        sx = np.ascontiguousarray(S.xyz, np.float64)
+        st_ = np.ascontiguousarray(S.tri, np.uint32)
+        so = np.ascontiguousarray(S.comp_off, np.uint32)
+        sid = np.ascontiguousarray(S.label_ids, np.int32)
+        ref_labels = d_labels.cpu().numpy()
+        cpp = {"path": "nestmesh::Labeler::initial_label (C++, reference types, pageable std::vector buffers), "
+                       "host clock per call: H2D nodes + tets, labeling, D2H labels"}
+        for mode in (0, 2):
+            out = np.zeros(4, np.float64)
+            lab = np.empty(nt, np.int32)
+            k = min(args.steps, 3) if mode == 0 else args.steps
+            rc = L.dropin_bench(P(sx, ctypes.c_double), ctypes.c_size_t(sx.shape[0]), P(st_, ctypes.c_uint32),
+                                P(so, ctypes.c_uint32), ctypes.c_int(S.K), P(sid, ctypes.c_int),
+                                P(nodes, ctypes.c_double), ctypes.c_size_t(n), P(tets, ctypes.c_uint32),
+                                ctypes.c_size_t(nt), ctypes.c_int(mode), ctypes.c_int(k), P(out, ctypes.c_double),
+                                P(lab, ctypes.c_int))
+            if rc != 0:
+                cpp["cull%d" % mode] = {"error": "dropin_bench failed"}
+                continue
+            e = {"labeler_build_s": out[0], "first_call_s": out[1], "e2e_mean_s": out[2], "e2e_best_s": out[3],
+                 "steps": k, "evals_per_s_e2e": evals_total / out[2] if out[2] else None,
+                 "labels_identical": bool(np.array_equal(lab, ref_labels))}
+            if mode == 2 and cull and "e2e_full_mesh_labeling_time_s" in cull.get("mode2", {}):
+                e["vs_python_pinned_e2e"] = out[2] / cull["mode2"]["e2e_full_mesh_labeling_time_s"]
+            if mode == 0 and e2e:
+                e["vs_python_pinned_e2e"] = out[2] / (e2e["ms_per_step"] / 1e3)
+            cpp["cull%d" % mode] = e
+
     # N > 1: the certified-cell pass split by COST over the ranks (every rank
     # holds all nodes, evaluates its share of the pair lists; the disjoint
     # partial masks merge in one all-reduce), then each rank's tet range.
@@ -622,6 +660,7 @@ def main():
             "surface_layout": sinfo,
             "quality": quality,
             "cull_outside": cull,
+            "cpp_dropin_e2e": cpp,
         }
         print(json.dumps(line), flush=True)
     if use_dist:

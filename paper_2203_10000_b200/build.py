@@ -107,11 +107,30 @@ def build_cpp_dropin_test(force=False):
     return out
 
 
+def build_cpp_dropin_bench(force=False):
+    """tests/cpp/dropin_bench.cpp -> build/libdropin_bench.so: the C++ drop-in's
+    end-to-end leg of bench.py (reference types, pageable buffers)."""
+    ref_inc = Path("/root/reference/proj/include")
+    if not ref_inc.exists():
+        return None
+    out = ROOT / "build" / "libdropin_bench.so"
+    src = ROOT / "tests" / "cpp" / "dropin_bench.cpp"
+    deps = [src, ROOT / "include" / "nestmesh" / "labeling.hpp", ROOT / "include" / "nestmesh_label.h",
+            LIB / "libnestmesh_label.so"]
+    if force or _stale(out, deps):
+        out.parent.mkdir(exist_ok=True)
+        _run([CXX, "-std=c++20", "-O2", "-fPIC", "-shared", "-Wall", "-Wextra", f"-I{ref_inc}", f"-I{ROOT / 'include'}",
+              str(src), "-o", str(out), f"-L{LIB}", "-lnestmesh_label",
+              "-Wl,-rpath,$ORIGIN/../paper_2203_10000_b200/lib"])
+    return out
+
+
 def build_all(force=False) -> None:
     build_synth_lib(force)
     build_label_lib(force)
     build_oracle()
     build_cpp_dropin_test(force)
+    build_cpp_dropin_bench(force)
 
 
 if __name__ == "__main__":

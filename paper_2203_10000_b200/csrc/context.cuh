@@ -30,6 +30,7 @@
 #include "cells.cuh"
 #include "nestmesh_label.h"
 #include "refine.h"
+#include "staging.cuh"
 
 namespace nmh {
 
@@ -144,6 +145,22 @@ struct nm_ctx {
   std::uint32_t* h_word = nullptr;        // pinned: max tet node index read back from the side stream
   std::uint32_t* h_pcnt = nullptr;        // pinned: per-compartment flagged-pair counts of the fix-up (32)
   std::uint64_t node_launches = 0;        // launches of the last label_nodes_dev
+  // staged copies of pageable caller buffers (staging.cuh): main stream and
+  // the side stream (tet upload under the node pass), each with its own pool
+  nmh::Stager stage_main, stage_side;
+  std::unique_ptr<nmh::CopyPool> pool_main, pool_side;
+  nmh::CopyPool& pool(bool side) {
+    auto& p = side ? pool_side : pool_main;
+    if (!p) {
+      const int hw = static_cast<int>(std::thread::hardware_concurrency());
+      p = std::make_unique<nmh::CopyPool>(std::max(1, std::min(side ? 3 : 5, hw / 2 - 1)));
+    }
+    return *p;
+  }
+  void h2d(void* d, const void* h, std::size_t bytes, cudaStream_t st, bool side = false) {
+    (side ? stage_side : stage_main).h2d(d, h, bytes, st, pool(side));
+  }
+  void d2h(void* h, const void* d, std::size_t bytes, cudaStream_t st) { stage_main.d2h(h, d, bytes, st, pool(false)); }
   int sm_count = 0;
 
   // surfaces

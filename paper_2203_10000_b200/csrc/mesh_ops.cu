@@ -301,8 +301,8 @@ int nm_label_lattice(nm_ctx* c, const double* origin, double h, int nx, int ny, 
     if (nm_lattice_device(c, origin, h, nx, ny, nz, d_nodes, d_tets, st) != 0) throw Error(last_error());
     label_nodes_dev(c, d_nodes, nn, T, d_masks, nullptr, st, stats);
     label_tets_dev(c, d_tets, nt, d_masks, d_labels, st, stats);
-    if (labels_out) NM_CUDA(cudaMemcpyAsync(labels_out, d_labels, nt * sizeof(int), cudaMemcpyDeviceToHost, st));
-    if (masks_out) NM_CUDA(cudaMemcpyAsync(masks_out, d_masks, nn * sizeof(std::uint32_t), cudaMemcpyDeviceToHost, st));
+    if (labels_out) c->d2h(labels_out, d_labels, nt * sizeof(int), st);
+    if (masks_out) c->d2h(masks_out, d_masks, nn * sizeof(std::uint32_t), st);
     NM_CUDA(cudaStreamSynchronize(st));
   });
 }
@@ -434,8 +434,8 @@ int nm_label_centroids(nm_ctx* c, const double* nodes, std::size_t n, const std:
     auto* d_cen = c->pts.as<double>(3 * std::max<std::size_t>(nt, 1));
     auto* d_masks = c->masks.as<std::uint32_t>(std::max<std::size_t>(nt, 1));
     auto* d_labels = c->labels.as<int>(std::max<std::size_t>(nt, 1));
-    if (n) NM_CUDA(cudaMemcpyAsync(d_nodes, nodes, 3 * n * sizeof(double), cudaMemcpyHostToDevice, st));
-    if (nt) NM_CUDA(cudaMemcpyAsync(d_tets, tets, 4 * nt * sizeof(std::uint32_t), cudaMemcpyHostToDevice, st));
+    c->h2d(d_nodes, nodes, 3 * n * sizeof(double), st);
+    c->h2d(d_tets, tets, 4 * nt * sizeof(std::uint32_t), st);
     if (nt)
       nm::k_centroids<<<grid_for(nt, 256, c->sm_count * 32), 256, 0, st>>>(d_nodes, reinterpret_cast<const uint4*>(d_tets),
                                                                           nt, d_cen);
@@ -443,7 +443,7 @@ int nm_label_centroids(nm_ctx* c, const double* nodes, std::size_t n, const std:
     if (nt) {
       nm::k_mask_labels<<<grid_for(nt, 256, c->sm_count * 32), 256, 0, st>>>(d_masks, nt, d_labels, c->ids);
       NM_CUDA(cudaGetLastError());
-      NM_CUDA(cudaMemcpyAsync(labels_out, d_labels, nt * sizeof(int), cudaMemcpyDeviceToHost, st));
+      c->d2h(labels_out, d_labels, nt * sizeof(int), st);
     }
     NM_CUDA(cudaStreamSynchronize(st));
   });
@@ -492,9 +492,9 @@ int nm_relabel(nm_ctx* c, const double* nodes, std::size_t n, const std::uint32_
     auto* d_list = c->frontier.as<std::uint32_t>(std::max<std::size_t>(n, 1));  // frontier node ids
     auto* d_count = c->count.as<std::uint32_t>(4);
     auto* counters = c->counters.as<unsigned long long>(8);
-    if (n) NM_CUDA(cudaMemcpyAsync(d_pts, nodes, 3 * n * sizeof(double), cudaMemcpyHostToDevice, st));
-    if (nt) NM_CUDA(cudaMemcpyAsync(d_tets, tets, 4 * nt * sizeof(std::uint32_t), cudaMemcpyHostToDevice, st));
-    if (nt) NM_CUDA(cudaMemcpyAsync(d_labels, labels_io, nt * sizeof(int), cudaMemcpyHostToDevice, st));
+    c->h2d(d_pts, nodes, 3 * n * sizeof(double), st);
+    c->h2d(d_tets, tets, 4 * nt * sizeof(std::uint32_t), st);
+    c->h2d(d_labels, labels_io, nt * sizeof(int), st);
     NM_CUDA(cudaMemsetAsync(d_known, 0, std::max<std::size_t>(n, 1), st));
     NM_CUDA(cudaMemsetAsync(d_masks, 0, std::max<std::size_t>(n, 1) * sizeof(std::uint32_t), st));
     const uint4* t4 = reinterpret_cast<const uint4*>(d_tets);
@@ -541,7 +541,7 @@ int nm_relabel(nm_ctx* c, const double* nodes, std::size_t n, const std::uint32_
       }
     }
     *passes = std::min(pass, max_iters);
-    if (nt) NM_CUDA(cudaMemcpyAsync(labels_io, d_labels, nt * sizeof(int), cudaMemcpyDeviceToHost, st));
+    c->d2h(labels_io, d_labels, nt * sizeof(int), st);
     if (evaluated && n) NM_CUDA(cudaMemcpyAsync(evaluated, d_known, n, cudaMemcpyDeviceToHost, st));
     NM_CUDA(cudaStreamSynchronize(st));
     if (stats) {

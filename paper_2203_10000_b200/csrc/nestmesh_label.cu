@@ -1133,9 +1133,9 @@ int nm_label_nodes(nm_ctx* c, const double* pts, std::size_t n, double T, std::u
     NM_CUDA(cudaSetDevice(c->opt.device));
     auto* d_pts = c->pts.as<double>(3 * std::max<std::size_t>(n, 1));
     auto* d_masks = c->masks.as<std::uint32_t>(std::max<std::size_t>(n, 1));
-    if (n) NM_CUDA(cudaMemcpyAsync(d_pts, pts, 3 * n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    c->h2d(d_pts, pts, 3 * n * sizeof(double), c->stream);
     label_nodes_dev(c, d_pts, n, T, d_masks, nullptr, c->stream, stats);
-    if (n) NM_CUDA(cudaMemcpyAsync(masks_out, d_masks, n * sizeof(std::uint32_t), cudaMemcpyDeviceToHost, c->stream));
+    c->d2h(masks_out, d_masks, n * sizeof(std::uint32_t), c->stream);
     NM_CUDA(cudaStreamSynchronize(c->stream));
   });
 }
@@ -1147,9 +1147,9 @@ int nm_enclosure(nm_ctx* c, const double* pts, std::size_t n, double T, double* 
     auto* d_pts = c->pts.as<double>(3 * std::max<std::size_t>(n, 1));
     auto* d_masks = c->masks.as<std::uint32_t>(std::max<std::size_t>(n, 1));
     auto* d_s = c->s_out.as<double>(std::max<std::size_t>(n * c->K, 1));
-    if (n) NM_CUDA(cudaMemcpyAsync(d_pts, pts, 3 * n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    c->h2d(d_pts, pts, 3 * n * sizeof(double), c->stream);
     label_nodes_dev(c, d_pts, n, T, d_masks, d_s, c->stream, stats);
-    if (n) NM_CUDA(cudaMemcpyAsync(s_out, d_s, n * c->K * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    c->d2h(s_out, d_s, n * c->K * sizeof(double), c->stream);
     NM_CUDA(cudaStreamSynchronize(c->stream));
   });
 }
@@ -1164,11 +1164,11 @@ int nm_label_tets(nm_ctx* c, const std::uint32_t* tets, std::size_t nt, const st
     auto* d_tets = c->tets.as<std::uint32_t>(4 * std::max<std::size_t>(nt, 1));
     auto* d_masks = c->masks.as<std::uint32_t>(std::max<std::size_t>(n_nodes, 1));
     auto* d_labels = c->labels.as<int>(std::max<std::size_t>(nt, 1));
-    if (nt) NM_CUDA(cudaMemcpyAsync(d_tets, tets, 4 * nt * sizeof(std::uint32_t), cudaMemcpyHostToDevice, c->stream));
+    c->h2d(d_tets, tets, 4 * nt * sizeof(std::uint32_t), c->stream);
     check_tets_device(c, d_tets, tets, nt, n_nodes, c->stream);
-    if (n_nodes) NM_CUDA(cudaMemcpyAsync(d_masks, masks, n_nodes * sizeof(std::uint32_t), cudaMemcpyHostToDevice, c->stream));
+    c->h2d(d_masks, masks, n_nodes * sizeof(std::uint32_t), c->stream);
     label_tets_dev(c, d_tets, nt, d_masks, d_labels, c->stream, stats);
-    if (nt) NM_CUDA(cudaMemcpyAsync(labels_out, d_labels, nt * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    c->d2h(labels_out, d_labels, nt * sizeof(int), c->stream);
     NM_CUDA(cudaStreamSynchronize(c->stream));
   });
 }
@@ -1189,21 +1189,39 @@ int nm_label_mesh(nm_ctx* c, const double* nodes, std::size_t n, const std::uint
     auto* d_tets = c->tets.as<std::uint32_t>(4 * std::max<std::size_t>(nt, 1));
     auto* d_labels = c->labels.as<int>(std::max<std::size_t>(nt, 1));
     auto* d_word = c->word.as<std::uint32_t>(1);
-    if (n) NM_CUDA(cudaMemcpyAsync(d_pts, nodes, 3 * n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
-    // tet upload + index validation on the side stream, enqueued first so it
-    // runs under the whole node pass (which may synchronise the host once,
-    // for the sparse grid of certified-cell culling)
+    c->h2d(d_pts, nodes, 3 * n * sizeof(double), c->stream);
+    // tet upload + index validation on the side stream, from a helper host
+    // thread (a pageable tet array is staged by host copies), so it runs under
+    // the whole node pass (which synchronises the host for the fix-up's pair
+    // lists and, with certified cells, for the sparse grid)
+    std::exception_ptr side_err;
+    std::thread side_thread;
     if (nt) {
-      NM_CUDA(cudaMemcpyAsync(d_tets, tets, 4 * nt * sizeof(std::uint32_t), cudaMemcpyHostToDevice, c->side));
-      NM_CUDA(cudaMemsetAsync(d_word, 0, sizeof(std::uint32_t), c->side));
-      nm::k_max_index<<<grid_for(nt, 256, c->sm_count * 8), 256, 0, c->side>>>(reinterpret_cast<const uint4*>(d_tets),
-                                                                               nt, d_word);
-      NM_CUDA(cudaGetLastError());
-      NM_CUDA(cudaMemcpyAsync(c->h_word, d_word, sizeof(std::uint32_t), cudaMemcpyDeviceToHost, c->side));
-      NM_CUDA(cudaEventRecord(c->ev_side, c->side));
+      side_thread = std::thread([&] {
+        try {
+          NM_CUDA(cudaSetDevice(c->opt.device));
+          c->h2d(d_tets, tets, 4 * nt * sizeof(std::uint32_t), c->side, /*side=*/true);
+          NM_CUDA(cudaMemsetAsync(d_word, 0, sizeof(std::uint32_t), c->side));
+          nm::k_max_index<<<grid_for(nt, 256, c->sm_count * 8), 256, 0, c->side>>>(
+              reinterpret_cast<const uint4*>(d_tets), nt, d_word);
+          NM_CUDA(cudaGetLastError());
+          NM_CUDA(cudaMemcpyAsync(c->h_word, d_word, sizeof(std::uint32_t), cudaMemcpyDeviceToHost, c->side));
+          NM_CUDA(cudaEventRecord(c->ev_side, c->side));
+        } catch (...) {
+          side_err = std::current_exception();
+        }
+      });
     }
+    struct Join {
+      std::thread& t;
+      ~Join() {
+        if (t.joinable()) t.join();
+      }
+    } join{side_thread};
     label_nodes_dev(c, d_pts, n, T, d_masks, nullptr, c->stream, stats, nullptr, /*stats_deferred=*/true);
     if (nt) {
+      side_thread.join();
+      if (side_err) std::rethrow_exception(side_err);
       NM_CUDA(cudaStreamWaitEvent(c->stream, c->ev_side, 0));
       NM_CUDA(cudaEventSynchronize(c->ev_side));
       if (*c->h_word >= n) {
@@ -1213,9 +1231,8 @@ int nm_label_mesh(nm_ctx* c, const double* nodes, std::size_t n, const std::uint
     }
     if (stats && n) read_node_stats(c, n, c->stream, stats);
     label_tets_dev(c, d_tets, nt, d_masks, d_labels, c->stream, stats);
-    if (nt) NM_CUDA(cudaMemcpyAsync(labels_out, d_labels, nt * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
-    if (masks_out && n)
-      NM_CUDA(cudaMemcpyAsync(masks_out, d_masks, n * sizeof(std::uint32_t), cudaMemcpyDeviceToHost, c->stream));
+    c->d2h(labels_out, d_labels, nt * sizeof(int), c->stream);
+    if (masks_out) c->d2h(masks_out, d_masks, n * sizeof(std::uint32_t), c->stream);
     NM_CUDA(cudaStreamSynchronize(c->stream));
   });
 }

@@ -1,0 +1,190 @@
+// Host <-> device transfers of CALLER buffers for the host-buffer entry points
+// (nm_label_mesh & co., the C++ drop-in). Not part of the ABI.
+//
+// Pinned (page-locked or cudaHostRegister'ed) caller memory goes straight to
+// cudaMemcpyAsync. Pageable memory — what a std::vector<Vec3> is — would be
+// staged by the driver through its own small pinned buffers by ONE host
+// thread; here it is pipelined through kChunk pinned buffers instead, the
+// host copies done by a small persistent thread pool, each chunk's DMA
+// overlapping the host copy of the next one.
+#pragma once
+#include <condition_variable>
+#include <cstddef>
+#include <cstring>
+#include <functional>
+#include <mutex>
+#include <thread>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+namespace nmh {
+
+// Fixed pool of host threads running one parallel memcpy at a time (the
+// calling thread takes a slice too).
+class CopyPool {
+ public:
+  explicit CopyPool(int workers) {
+    for (int i = 0; i < workers; ++i) th_.emplace_back([this, i] { run(i); });
+  }
+  ~CopyPool() {
+    {
+      std::lock_guard<std::mutex> g(m_);
+      stop_ = true;
+    }
+    cv_.notify_all();
+    for (auto& t : th_) t.join();
+  }
+  CopyPool(const CopyPool&) = delete;
+  CopyPool& operator=(const CopyPool&) = delete;
+
+  void copy(void* dst, const void* src, std::size_t bytes) {
+    const int parts = static_cast<int>(th_.size()) + 1;
+    if (bytes < (std::size_t(1) << 20) || parts == 1) {
+      std::memcpy(dst, src, bytes);
+      return;
+    }
+    {
+      std::lock_guard<std::mutex> g(m_);
+      dst_ = static_cast<char*>(dst);
+      src_ = static_cast<const char*>(src);
+      bytes_ = bytes;
+      parts_ = parts;
+      pending_ = static_cast<int>(th_.size());
+      ++gen_;
+    }
+    cv_.notify_all();
+    slice(parts - 1);  // the caller's share
+    std::unique_lock<std::mutex> g(m_);
+    done_.wait(g, [this] { return pending_ == 0; });
+  }
+
+ private:
+  void slice(int k) {
+    const std::size_t per = (bytes_ / parts_ + 63) & ~std::size_t(63);
+    const std::size_t lo = std::min(bytes_, per * k), hi = k == parts_ - 1 ? bytes_ : std::min(bytes_, per * (k + 1));
+    if (hi > lo) std::memcpy(dst_ + lo, src_ + lo, hi - lo);
+  }
+  void run(int k) {
+    std::uint64_t seen = 0;
+    for (;;) {
+      {
+        std::unique_lock<std::mutex> g(m_);
+        cv_.wait(g, [&] { return stop_ || gen_ != seen; });
+        if (stop_) return;
+        seen = gen_;
+      }
+      slice(k);
+      {
+        std::lock_guard<std::mutex> g(m_);
+        if (--pending_ == 0) done_.notify_one();
+      }
+    }
+  }
+  std::vector<std::thread> th_;
+  std::mutex m_;
+  std::condition_variable cv_, done_;
+  bool stop_ = false;
+  std::uint64_t gen_ = 0;
+  char* dst_ = nullptr;
+  const char* src_ = nullptr;
+  std::size_t bytes_ = 0;
+  int parts_ = 1, pending_ = 0;
+};
+
+inline bool host_pinned(const void* p) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();  // clear: plain pageable memory on older drivers
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost || a.type == cudaMemoryTypeManaged;
+}
+
+// One pipeline of pinned chunk buffers bound to one stream at a time.
+class Stager {
+ public:
+  static constexpr std::size_t kChunk = std::size_t(16) << 20;
+  static constexpr int kBufs = 3;
+
+  Stager() = default;
+  ~Stager() { release(); }
+  Stager(const Stager&) = delete;
+  Stager& operator=(const Stager&) = delete;
+
+  // Enqueue dst_dev <- src_host on st. On return the caller's buffer has been
+  // read completely (it may be freed or reused); the DMA may still run.
+  void h2d(void* dst, const void* src, std::size_t bytes, cudaStream_t st, CopyPool& pool) {
+    if (!bytes) return;
+    if (bytes <= kChunk / 4 || host_pinned(src)) {
+      check(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st));
+      if (!host_pinned(src)) check(cudaStreamSynchronize(st));  // small pageable copy: the driver staged it
+      return;
+    }
+    init();
+    const auto* s = static_cast<const char*>(src);
+    auto* d = static_cast<char*>(dst);
+    for (std::size_t off = 0, i = 0; off < bytes; off += kChunk, ++i) {
+      const int b = static_cast<int>(i % kBufs);
+      const std::size_t len = std::min(kChunk, bytes - off);
+      check(cudaEventSynchronize(ev_[b]));  // the buffer's previous DMA is done
+      pool.copy(pin_[b], s + off, len);
+      check(cudaMemcpyAsync(d + off, pin_[b], len, cudaMemcpyHostToDevice, st));
+      check(cudaEventRecord(ev_[b], st));
+    }
+  }
+
+  // dst_host <- src_dev after the work already enqueued on st; returns when
+  // the caller's buffer holds the data.
+  void d2h(void* dst, const void* src, std::size_t bytes, cudaStream_t st, CopyPool& pool) {
+    if (!bytes) return;
+    if (bytes <= kChunk / 4 || host_pinned(dst)) {
+      check(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st));
+      check(cudaStreamSynchronize(st));
+      return;
+    }
+    init();
+    auto* h = static_cast<char*>(dst);
+    const auto* d = static_cast<const char*>(src);
+    const std::size_t n = (bytes + kChunk - 1) / kChunk;
+    auto len_of = [&](std::size_t i) { return std::min(kChunk, bytes - i * kChunk); };
+    for (std::size_t i = 0; i < n + 1; ++i) {
+      if (i < n) {  // DMA chunk i into its buffer (the buffer's host copy, chunk i - kBufs, is done)
+        const int b = static_cast<int>(i % kBufs);
+        check(cudaMemcpyAsync(pin_[b], d + i * kChunk, len_of(i), cudaMemcpyDeviceToHost, st));
+        check(cudaEventRecord(ev_[b], st));
+      }
+      if (i >= 1) {  // host copy of chunk i - 1 while chunk i streams in
+        const std::size_t j = i - 1;
+        const int b = static_cast<int>(j % kBufs);
+        check(cudaEventSynchronize(ev_[b]));
+        pool.copy(h + j * kChunk, pin_[b], len_of(j));
+      }
+    }
+  }
+
+  void release() {
+    for (int b = 0; b < kBufs; ++b) {
+      if (pin_[b]) cudaFreeHost(pin_[b]);
+      if (ev_[b]) cudaEventDestroy(ev_[b]);
+      pin_[b] = nullptr;
+      ev_[b] = nullptr;
+    }
+  }
+
+ private:
+  static void check(cudaError_t e) {
+    if (e != cudaSuccess) throw std::runtime_error(std::string("staging copy: ") + cudaGetErrorString(e));
+  }
+  void init() {
+    if (pin_[0]) return;
+    for (int b = 0; b < kBufs; ++b) {
+      check(cudaMallocHost(&pin_[b], kChunk));
+      check(cudaEventCreateWithFlags(&ev_[b], cudaEventDisableTiming));
+    }
+  }
+  void* pin_[kBufs] = {};
+  cudaEvent_t ev_[kBufs] = {};
+};
+
+}  // namespace nmh

@@ -96,6 +96,54 @@ int main(int argc, char** argv) {
     std::fprintf(stderr, "relabel != initial on the refined mesh\n");
     return 8;
   }
+  // persistent Labeler: surfaces (+ certified cells) uploaded once; initial
+  // labels, relabel after refinement and enclosure ratios over the same
+  // context equal the free functions
+  {
+    Labeler lab(seg);
+    std::vector<std::uint32_t> masks;
+    if (lab.initial_label(mesh, params, nullptr, &masks) != labels || masks.size() != mesh.node_count()) {
+      std::fprintf(stderr, "Labeler initial_label differs\n");
+      return 11;
+    }
+    if (lab.node_masks(mesh, params) != masks) {
+      std::fprintf(stderr, "Labeler node_masks differ\n");
+      return 12;
+    }
+    const RelabelResult lr = lab.relabel_recursive(refined, params, refined.labels);
+    if (lr.labels != rr.labels || lab.initial_label(refined, params) != rr.labels) {
+      std::fprintf(stderr, "Labeler relabel differs\n");
+      return 13;
+    }
+    const std::vector<double> s = lab.enclosure_ratios({Vec3{0, 0, 0}, Vec3{30, 0, 0}});
+    if (std::abs(s[0] - 1.0) > 1e-6 || std::abs(s[1] - 1.0) > 1e-6 || std::abs(s[2]) > 1e-6 || std::abs(s[3]) > 1e-6) {
+      std::fprintf(stderr, "Labeler enclosure_ratios KAT failed\n");
+      return 14;
+    }
+    if (lab.boundary_tets(mesh, masks) != boundary_tets(mesh, masks, 0xffffffffu, seg)) {
+      std::fprintf(stderr, "Labeler boundary_tets differ\n");
+      return 15;
+    }
+    // NonConvergence: one pass cannot fix labels from a
+    // coarse segmentation; the best labels travel with the exception
+    SurfaceSegmentation coarse = seg;
+    coarse.compartments[0].mesh = icosphere(6.0, 1);
+    coarse.compartments[1].mesh = icosphere(10.0, 1);
+    const std::vector<int> prev = initial_label(mesh, coarse, params);
+    SolidAngleParams one = params;
+    one.max_iters = 1;
+    try {
+      (void)lab.relabel_recursive(mesh, one, prev);
+      std::fprintf(stderr, "NonConvergence not thrown\n");
+      return 16;
+    } catch (const NonConvergence& e) {
+      if (e.best.passes != 1 || e.best.converged || e.best.labels.size() != prev.size()) return 17;
+    }
+    if (lab.relabel_recursive(mesh, params, prev).labels != labels) {
+      std::fprintf(stderr, "relabel from coarse labels != initial\n");
+      return 18;
+    }
+  }
   FILE* f = std::fopen(out_path, "wb");
   std::fwrite(labels.data(), sizeof(int), labels.size(), f);
   std::fclose(f);
