@@ -153,10 +153,12 @@ int nm_relabel(nm_ctx* ctx, const double* nodes, size_t n_nodes, const uint32_t*
                uint8_t* evaluated /* nullable */, nm_stats* stats);
 
 /* ---- single-process multi-GPU group (C/C++ hosts; SPEC.md:267 --label-workers)
- * One context per device (devices may repeat), contiguous node and tet
- * shards, node masks gathered through pinned host memory. Bit-identical to a
- * single device. (torch hosts use one process per GPU + NCCL instead:
- * paper_2203_10000_b200/distributed.py.) */
+ * One context per device (devices may repeat), one host thread per device,
+ * contiguous node and tet shards (or, with certified cells, cost-balanced
+ * shares of the pair lists). Node masks are exchanged on the devices: NCCL
+ * all-gather / all-reduce over NVLink when the devices are distinct, peer
+ * copies when a device repeats. Bit-identical to a single device. (torch
+ * hosts use one process per GPU: paper_2203_10000_b200/distributed.py.) */
 typedef struct nm_group nm_group;
 int nm_group_create(nm_group** g, int n_devices, const int* devices /* NULL = 0..n-1 */, const nm_options* opt);
 int nm_group_destroy(nm_group* g);
@@ -165,6 +167,8 @@ int nm_group_set_surfaces(nm_group* g, const double* xyz, size_t nv, const uint3
                           const uint32_t* comp_tri_off, int K, const int* label_ids);
 int nm_group_label_mesh(nm_group* g, const double* nodes, size_t n_nodes, const uint32_t* tets, size_t nt,
                         double threshold, int* labels_out, uint32_t* masks_out /* nullable */, nm_stats* stats);
+/* 1 when the group exchanges masks through NCCL (distinct devices, libnccl found) */
+int nm_group_uses_nccl(const nm_group* g);
 
 /* ---- device-resident entry points (asynchronous on `stream`) -------------- */
 int nm_label_nodes_device(nm_ctx* ctx, const double* d_pts, size_t n, double threshold, uint32_t* d_masks,
@@ -211,6 +215,17 @@ int nm_mesh_masks(const nm_mesh* m, uint32_t* masks);
  * and child order as nm_refine (bit-identical result). */
 int nm_refine_device(nm_ctx* ctx, const double* nodes, size_t n_nodes, const uint32_t* tets, size_t nt,
                      const int* labels /* nullable */, const uint32_t* selected, size_t n_selected, nm_mesh** out);
+
+/* The same on caller DEVICE arrays (asynchronous on `stream` apart from a
+ * few small count reads): inputs are validated on the device; the result
+ * stays on the device, nm_mesh_copy_device copies it into caller device
+ * buffers (nullable). Used by the multi-rank recursive driver, whose meshes
+ * never leave the GPUs. */
+int nm_refine_device_d(nm_ctx* ctx, const double* d_nodes, size_t n_nodes, const uint32_t* d_tets, size_t nt,
+                       const int* d_labels /* nullable */, const uint32_t* d_selected, size_t n_selected, void* stream,
+                       nm_mesh** out);
+int nm_mesh_copy_device(const nm_mesh* m, double* d_nodes, uint32_t* d_tets, int* d_labels, uint32_t* d_parent,
+                        void* stream);
 
 /* refine_boundary on the device: the tets labeled a or b
  * that share a face with a tet of the other label are refined with

@@ -158,6 +158,12 @@ LABEL_API = {
                                              c_u32_p, ctypes.c_int, c_i32_p]),
     "nm_group_label_mesh": (ctypes.c_int, [ctypes.c_void_p, c_double_p, ctypes.c_size_t, c_u32_p, ctypes.c_size_t,
                                            ctypes.c_double, c_i32_p, c_u32_p, ctypes.POINTER(NmStats)]),
+    "nm_group_uses_nccl": (ctypes.c_int, [ctypes.c_void_p]),
+    "nm_refine_device_d": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p,
+                                          ctypes.c_size_t, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t,
+                                          ctypes.c_void_p, ctypes.POINTER(ctypes.c_void_p)]),
+    "nm_mesh_copy_device": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                           ctypes.c_void_p, ctypes.c_void_p]),
     "nm_surface_info": (ctypes.c_int, [ctypes.c_void_p, c_i32_p, c_size_p, c_size_p, c_i32_p]),
     "nm_surface_segments": (ctypes.c_int, [ctypes.c_void_p, c_size_p, c_size_p]),
     "nm_cell_info": (ctypes.c_int, [ctypes.c_void_p] + [ctypes.POINTER(ctypes.c_uint64)] * 3
@@ -494,6 +500,31 @@ class Context:
         return on, ot, ol, om, st.as_dict()
 
     # -- device-resident entry points (torch tensors) ---------------------
+    def refine_device_tensors(self, d_nodes, d_tets, d_labels, d_sel, stream=None):
+        """refine_volume on torch CUDA tensors (nm_refine_device_d): returns
+        (nodes2, tets2, labels2, parent, n_old) as new tensors on the same
+        device; nothing crosses to the host but a few counts."""
+        import torch
+        h = ctypes.c_void_p()
+        check(self.lib.nm_refine_device_d(self.handle, d_nodes.data_ptr(), d_nodes.shape[0], d_tets.data_ptr(),
+                                          d_tets.shape[0], d_labels.data_ptr() if d_labels is not None else None,
+                                          d_sel.data_ptr(), d_sel.numel(), stream_handle(stream), ctypes.byref(h)))
+        try:
+            nn, ntt, nold = ctypes.c_size_t(), ctypes.c_size_t(), ctypes.c_size_t()
+            self.lib.nm_mesh_sizes(h, ctypes.byref(nn), ctypes.byref(ntt), ctypes.byref(nold))
+            dev = d_nodes.device
+            on = torch.empty((nn.value, 3), dtype=torch.float64, device=dev)
+            ot = torch.empty((ntt.value, 4), dtype=torch.int32, device=dev)
+            ol = torch.empty(ntt.value, dtype=torch.int32, device=dev)
+            op = torch.empty(ntt.value, dtype=torch.int32, device=dev)
+            cs = stream if stream is not None else torch.cuda.current_stream(dev)
+            check(self.lib.nm_mesh_copy_device(h, on.data_ptr(), ot.data_ptr(), ol.data_ptr(), op.data_ptr(),
+                                               stream_handle(cs)))
+            cs.synchronize()  # the handle's arrays are released below
+        finally:
+            self.lib.nm_mesh_free(h)
+        return on, ot, ol, op, nold.value
+
     def label_nodes_device(self, d_pts, d_masks, threshold=0.5, d_s=None, stream=None, stats=True):
         """d_pts: CUDA float64 tensor (n,3); d_masks: CUDA uint32/int32 tensor (n,)."""
         st = NmStats() if stats else None
@@ -549,6 +580,11 @@ class Group:
         h = ctypes.c_void_p()
         check(self.lib.nm_group_create(ctypes.byref(h), devs.size, ptr(devs, ctypes.c_int), ctypes.byref(opt)))
         self.handle = h
+
+    @property
+    def uses_nccl(self) -> bool:
+        """Masks exchanged by NCCL (distinct devices) rather than peer copies."""
+        return bool(self.lib.nm_group_uses_nccl(self.handle))
 
     def close(self):
         if getattr(self, "handle", None):

@@ -1,22 +1,102 @@
-// Single-process multi-GPU group API (nm_group_*).
+// Single-process multi-GPU group API (nm_group_*): the C/C++ hosts' path of
+// SPEC.md:265-267 (--label-workers; results independent of the worker count).
+//
+// One nm_ctx per device. Every device's share runs on its own host thread, so
+// the devices' node passes (which synchronise their host thread for the fix-up
+// pair lists and the certified-cell grid) overlap. The exchange stays on the
+// devices:
+//   * distinct devices: NCCL over NVLink/NVSwitch (ncclCommInitAll; the
+//     library is opened at run time, so a host without NCCL still links) —
+//     ncclAllGather of the contiguous node-mask shards, or, for the
+//     cost-balanced certified-cell pass, ncclAllReduce(sum) of the disjoint
+//     partial masks (disjoint bits add without carries);
+//   * a device listed twice (tests on one GPU): peer copies of the other
+//     contexts' shards, ordered by cross-stream events (no host staging).
+// Node masks are pure functions of position, so the labels are
+// bit-identical to one device for any group.
 #include "context.cuh"
+
+#include <dlfcn.h>
+#include <nccl.h>
 
 using namespace nmh;
 
-// Single-process multi-GPU group (for C/C++ hosts without torch): one nm_ctx
-// per device, contiguous node and tet shards, node masks gathered through a
-// pinned host buffer. Results are bit-identical to one device (node masks are
-// pure functions of position).
+namespace {
+
+// NCCL entry points resolved at run time (torch processes have already
+// loaded their bundled libnccl.so.2; others load the system one).
+struct Nccl {
+  decltype(&ncclCommInitAll) init_all = nullptr;
+  decltype(&ncclCommDestroy) destroy = nullptr;
+  decltype(&ncclAllGather) all_gather = nullptr;
+  decltype(&ncclAllReduce) all_reduce = nullptr;
+  decltype(&ncclGroupStart) group_start = nullptr;
+  decltype(&ncclGroupEnd) group_end = nullptr;
+  decltype(&ncclGetErrorString) error_string = nullptr;
+  bool ok = false;
+  static const Nccl& get() {
+    static Nccl n = [] {
+      Nccl x;
+      void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+      if (!h) return x;
+      x.init_all = reinterpret_cast<decltype(x.init_all)>(dlsym(h, "ncclCommInitAll"));
+      x.destroy = reinterpret_cast<decltype(x.destroy)>(dlsym(h, "ncclCommDestroy"));
+      x.all_gather = reinterpret_cast<decltype(x.all_gather)>(dlsym(h, "ncclAllGather"));
+      x.all_reduce = reinterpret_cast<decltype(x.all_reduce)>(dlsym(h, "ncclAllReduce"));
+      x.group_start = reinterpret_cast<decltype(x.group_start)>(dlsym(h, "ncclGroupStart"));
+      x.group_end = reinterpret_cast<decltype(x.group_end)>(dlsym(h, "ncclGroupEnd"));
+      x.error_string = reinterpret_cast<decltype(x.error_string)>(dlsym(h, "ncclGetErrorString"));
+      x.ok = x.init_all && x.destroy && x.all_gather && x.all_reduce && x.group_start && x.group_end && x.error_string;
+      return x;
+    }();
+    return n;
+  }
+};
+
+void nccl_check(ncclResult_t r, const char* what) {
+  if (r != ncclSuccess) throw Error(std::string(what) + ": " + Nccl::get().error_string(r));
+}
+
+// dst[i] |= src[i] (peer-copy merge of the cost-balanced partial masks)
+__global__ void k_or_into(std::uint32_t* __restrict__ dst, const std::uint32_t* __restrict__ src, std::size_t n) {
+  for (std::size_t i = blockIdx.x * static_cast<std::size_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<std::size_t>(gridDim.x) * blockDim.x)
+    dst[i] |= src[i];
+}
+
+// Run f(r) for every device on its own host thread; rethrow the first error.
+template <class F>
+void per_device(std::size_t R, F&& f) {
+  std::vector<std::exception_ptr> err(R);
+  std::vector<std::thread> th;
+  for (std::size_t r = 0; r < R; ++r)
+    th.emplace_back([&, r] {
+      try {
+        f(r);
+      } catch (...) {
+        err[r] = std::current_exception();
+      }
+    });
+  for (auto& t : th) t.join();
+  for (auto& e : err)
+    if (e) std::rethrow_exception(e);
+}
+
+}  // namespace
+
 struct nm_group {
   std::vector<nm_ctx*> ctx;
-  std::uint32_t* h_masks = nullptr;  // pinned gather buffer
-  std::size_t h_cap = 0;
-  std::uint32_t* h_part = nullptr;   // pinned per-device partial masks (certified-cell sharding)
-  std::size_t part_cap = 0;
+  std::vector<cudaEvent_t> done;    // per device: its node pass (and partial masks) are complete
+  std::vector<ncclComm_t> comms;    // distinct devices: one NCCL communicator per device
+  bool distinct = false;
   ~nm_group() {
+    for (std::size_t r = 0; r < comms.size(); ++r)
+      if (comms[r]) Nccl::get().destroy(comms[r]);
+    for (std::size_t r = 0; r < done.size(); ++r) {
+      cudaSetDevice(ctx[r]->opt.device);
+      cudaEventDestroy(done[r]);
+    }
     for (nm_ctx* c : ctx) nm_destroy(c);
-    if (h_masks) cudaFreeHost(h_masks);
-    if (h_part) cudaFreeHost(h_part);
   }
 };
 
@@ -28,14 +108,42 @@ int nm_group_create(nm_group** out, int n, const int* devices, const nm_options*
     *out = nullptr;
     if (n < 1) throw Error("group needs at least one device");
     std::unique_ptr<nm_group> g(new nm_group);
+    std::vector<int> devs;
     for (int r = 0; r < n; ++r) {
       nm_options o;
       if (opt) o = *opt;
       else nm_default_options(&o);
       o.device = devices ? devices[r] : r;
+      devs.push_back(o.device);
       nm_ctx* c = nullptr;
       if (nm_create(&c, &o) != 0) throw Error(last_error());
       g->ctx.push_back(c);
+      cudaEvent_t e;
+      NM_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      g->done.push_back(e);
+    }
+    std::vector<int> sorted = devs;
+    std::sort(sorted.begin(), sorted.end());
+    g->distinct = std::adjacent_find(sorted.begin(), sorted.end()) == sorted.end();
+    // NM_GROUP_NCCL=1: communicators even for a single device (exercises the
+    // NCCL exchange on a one-GPU box; a 1-rank all-gather is a copy)
+    const char* force = std::getenv("NM_GROUP_NCCL");
+    const bool want_nccl = g->distinct && (n > 1 || (force && force[0] == '1'));
+    if (want_nccl) {
+      for (int a : devs)
+        for (int b : devs) {
+          int can = 0;
+          if (a != b && cudaDeviceCanAccessPeer(&can, a, b) == cudaSuccess && can) {
+            NM_CUDA(cudaSetDevice(a));
+            const cudaError_t e = cudaDeviceEnablePeerAccess(b, 0);
+            if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) NM_CUDA(e);
+            cudaGetLastError();
+          }
+        }
+      if (Nccl::get().ok) {
+        g->comms.assign(n, nullptr);
+        nccl_check(Nccl::get().init_all(g->comms.data(), n, devs.data()), "ncclCommInitAll");
+      }
     }
     *out = g.release();
   });
@@ -51,8 +159,9 @@ int nm_group_set_surfaces(nm_group* g, const double* xyz, std::size_t nv, const 
                           const std::uint32_t* comp_off, int K, const int* label_ids) {
   return guarded([&] {
     if (!g) throw Error("null group");
-    for (nm_ctx* c : g->ctx)
-      if (nm_set_surfaces(c, xyz, nv, tri, nt, comp_off, K, label_ids) != 0) throw Error(last_error());
+    per_device(g->ctx.size(), [&](std::size_t r) {
+      if (nm_set_surfaces(g->ctx[r], xyz, nv, tri, nt, comp_off, K, label_ids) != 0) throw Error(last_error());
+    });
   });
 }
 
@@ -64,88 +173,94 @@ int nm_group_label_mesh(nm_group* g, const double* nodes, std::size_t n, const s
     const std::size_t R = g->ctx.size();
     const std::size_t per_n = (n + R - 1) / R, per_t = (nt + R - 1) / R;
     if (stats) std::memset(stats, 0, sizeof *stats);
-    if (g->h_cap < n) {
-      if (g->h_masks) cudaFreeHost(g->h_masks);
-      g->h_masks = nullptr;
-      g->h_cap = 0;
-      NM_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&g->h_masks), std::max<std::size_t>(n, 1) * 4, cudaHostAllocPortable));
-      g->h_cap = n;
-    }
-    // 1) node pass. With certified cells the work per point is far from
-    // uniform (only pairs near a surface are evaluated), so every device
-    // takes a cost-balanced share of the pair lists of ALL points and the
-    // disjoint partial masks are OR-ed; otherwise contiguous node shards.
+    for (nm_ctx* c : g->ctx) require_surfaces(c);
+    // With certified cells the work per point is far from uniform (only pairs
+    // near a surface are evaluated), so every device takes a cost-balanced
+    // share of the pair lists of ALL points (disjoint partial masks);
+    // otherwise contiguous node shards (padded to R * per_n for the gather).
     const bool by_pairs = R > 1 && g->ctx[0]->opt.cull_outside == 2 && g->ctx[0]->cells;
-    if (by_pairs && g->part_cap < R * n) {
-      if (g->h_part) cudaFreeHost(g->h_part);
-      g->h_part = nullptr;
-      g->part_cap = 0;
-      NM_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&g->h_part), std::max<std::size_t>(R * n, 1) * 4,
-                            cudaHostAllocPortable));
-      g->part_cap = R * n;
-    }
-    for (std::size_t r = 0; by_pairs && r < R; ++r) {
+    const std::size_t len = by_pairs ? n : R * per_n;  // full mask buffer per device
+    std::vector<std::uint32_t*> d_all(R);
+    // 1) node passes, one host thread per device
+    per_device(R, [&](std::size_t r) {
       nm_ctx* c = g->ctx[r];
-      require_surfaces(c);
       NM_CUDA(cudaSetDevice(c->opt.device));
-      auto* d_pts = c->pts.as<double>(3 * std::max<std::size_t>(n, 1));
-      auto* d_m = c->masks2.as<std::uint32_t>(std::max<std::size_t>(n, 1));
-      if (n) {
-        NM_CUDA(cudaMemcpyAsync(d_pts, nodes, 3 * n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
-        label_nodes_dev(c, d_pts, n, T, d_m, nullptr, c->stream, nullptr, nullptr, false, static_cast<int>(r),
-                        static_cast<int>(R));
-        NM_CUDA(cudaMemcpyAsync(g->h_part + r * n, d_m, n * 4, cudaMemcpyDeviceToHost, c->stream));
+      d_all[r] = c->masks.as<std::uint32_t>(std::max<std::size_t>(len, 1));
+      (void)c->masks2.as<std::uint32_t>(std::max<std::size_t>(n, 1));  // merge scratch, sized before any launch
+      if (by_pairs) {
+        auto* d_pts = c->pts.as<double>(3 * std::max<std::size_t>(n, 1));
+        c->h2d(d_pts, nodes, 3 * n * sizeof(double), c->stream);
+        if (n)
+          label_nodes_dev(c, d_pts, n, T, d_all[r], nullptr, c->stream, nullptr, nullptr, false, static_cast<int>(r),
+                          static_cast<int>(R));
+      } else {
+        const std::size_t lo = std::min(n, r * per_n), hi = std::min(n, lo + per_n);
+        auto* d_pts = c->pts.as<double>(3 * std::max<std::size_t>(hi - lo, 1));
+        c->h2d(d_pts, nodes + 3 * lo, 3 * (hi - lo) * sizeof(double), c->stream);
+        if (hi > lo) label_nodes_dev(c, d_pts, hi - lo, T, d_all[r] + r * per_n, nullptr, c->stream, nullptr);
+        if (hi - lo < per_n)  // padding of the last shard(s)
+          NM_CUDA(cudaMemsetAsync(d_all[r] + r * per_n + (hi - lo), 0, (per_n - (hi - lo)) * 4, c->stream));
       }
-    }
-    for (std::size_t r = 0; !by_pairs && r < R; ++r) {
-      nm_ctx* c = g->ctx[r];
-      require_surfaces(c);
-      NM_CUDA(cudaSetDevice(c->opt.device));
-      const std::size_t lo = std::min(n, r * per_n), hi = std::min(n, lo + per_n);
-      auto* d_pts = c->pts.as<double>(3 * std::max<std::size_t>(hi - lo, 1));
-      auto* d_m = c->masks2.as<std::uint32_t>(std::max<std::size_t>(hi - lo, 1));
-      if (hi > lo) {
-        NM_CUDA(cudaMemcpyAsync(d_pts, nodes + 3 * lo, 3 * (hi - lo) * sizeof(double), cudaMemcpyHostToDevice, c->stream));
-        label_nodes_dev(c, d_pts, hi - lo, T, d_m, nullptr, c->stream, nullptr);
-        NM_CUDA(cudaMemcpyAsync(g->h_masks + lo, d_m, (hi - lo) * 4, cudaMemcpyDeviceToHost, c->stream));
-      }
-    }
-    for (nm_ctx* c : g->ctx) {
-      NM_CUDA(cudaSetDevice(c->opt.device));
-      NM_CUDA(cudaStreamSynchronize(c->stream));
-    }
-    if (by_pairs) {
-      const int nchunk = 64;
-      parallel_for(nchunk, [&](int q) {
-        const std::size_t lo = n * q / nchunk, hi = n * (q + 1) / nchunk;
-        for (std::size_t i = lo; i < hi; ++i) {
-          std::uint32_t m = 0;
-          for (std::size_t r = 0; r < R; ++r) m |= g->h_part[r * n + i];
-          g->h_masks[i] = m;
+      NM_CUDA(cudaEventRecord(g->done[r], c->stream));
+    });
+    // 2) exchange on the devices
+    if ((R > 1 || !g->comms.empty()) && n) {
+      if (!g->comms.empty()) {
+        const Nccl& nc = Nccl::get();
+        nccl_check(nc.group_start(), "ncclGroupStart");
+        for (std::size_t r = 0; r < R; ++r) {
+          nm_ctx* c = g->ctx[r];
+          NM_CUDA(cudaSetDevice(c->opt.device));
+          if (by_pairs)
+            nccl_check(nc.all_reduce(d_all[r], d_all[r], n, ncclUint32, ncclSum, g->comms[r], c->stream), "ncclAllReduce");
+          else
+            nccl_check(nc.all_gather(d_all[r] + r * per_n, d_all[r], per_n, ncclUint32, g->comms[r], c->stream),
+                       "ncclAllGather");
         }
-      });
+        nccl_check(nc.group_end(), "ncclGroupEnd");
+      } else {
+        // peer copies (a device listed more than once, or no NCCL), ordered
+        // after each source's node pass by its event
+        for (std::size_t r = 0; r < R; ++r) {
+          nm_ctx* c = g->ctx[r];
+          NM_CUDA(cudaSetDevice(c->opt.device));
+          auto* tmp = c->masks2.as<std::uint32_t>(std::max<std::size_t>(n, 1));
+          for (std::size_t q = 0; q < R; ++q) {
+            if (q == r) continue;
+            NM_CUDA(cudaStreamWaitEvent(c->stream, g->done[q], 0));
+            const int dq = g->ctx[q]->opt.device, dr = c->opt.device;
+            if (by_pairs) {
+              NM_CUDA(cudaMemcpyPeerAsync(tmp, dr, d_all[q], dq, n * 4, c->stream));
+              k_or_into<<<grid_for(n, 256, c->sm_count * 8), 256, 0, c->stream>>>(d_all[r], tmp, n);
+              NM_CUDA(cudaGetLastError());
+            } else {
+              NM_CUDA(cudaMemcpyPeerAsync(d_all[r] + q * per_n, dr, d_all[q] + q * per_n, dq, per_n * 4, c->stream));
+            }
+          }
+        }
+      }
     }
-    // 2) gathered masks to every device, tet shards
-    for (std::size_t r = 0; r < R; ++r) {
+    // 3) tet shards on every device, labels back into the caller's array
+    per_device(R, [&](std::size_t r) {
       nm_ctx* c = g->ctx[r];
       NM_CUDA(cudaSetDevice(c->opt.device));
       const std::size_t lo = std::min(nt, r * per_t), hi = std::min(nt, lo + per_t);
-      auto* d_m = c->masks.as<std::uint32_t>(std::max<std::size_t>(n, 1));
       auto* d_t = c->tets.as<std::uint32_t>(4 * std::max<std::size_t>(hi - lo, 1));
       auto* d_l = c->labels.as<int>(std::max<std::size_t>(hi - lo, 1));
-      if (n) NM_CUDA(cudaMemcpyAsync(d_m, g->h_masks, n * 4, cudaMemcpyHostToDevice, c->stream));
+      c->h2d(d_t, tets + 4 * lo, 4 * (hi - lo) * sizeof(std::uint32_t), c->stream);
       if (hi > lo) {
-        NM_CUDA(cudaMemcpyAsync(d_t, tets + 4 * lo, 4 * (hi - lo) * sizeof(std::uint32_t), cudaMemcpyHostToDevice,
-                                c->stream));
-        label_tets_dev(c, d_t, hi - lo, d_m, d_l, c->stream, nullptr);
-        NM_CUDA(cudaMemcpyAsync(labels_out + lo, d_l, (hi - lo) * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+        label_tets_dev(c, d_t, hi - lo, d_all[r], d_l, c->stream, nullptr);
+        c->d2h(labels_out + lo, d_l, (hi - lo) * sizeof(int), c->stream);
       }
-    }
-    for (nm_ctx* c : g->ctx) {
-      NM_CUDA(cudaSetDevice(c->opt.device));
+      if (r == 0 && masks_out) c->d2h(masks_out, d_all[0], n * 4, c->stream);
       NM_CUDA(cudaStreamSynchronize(c->stream));
+      // peer copies read the other devices' buffers: keep them until all are done
+      NM_CUDA(cudaEventRecord(g->done[r], c->stream));
+    });
+    for (std::size_t r = 0; r < R; ++r) {
+      NM_CUDA(cudaSetDevice(g->ctx[r]->opt.device));
+      NM_CUDA(cudaEventSynchronize(g->done[r]));
     }
-    if (masks_out && n) std::memcpy(masks_out, g->h_masks, n * 4);
     if (stats) {
       stats->points = n;
       stats->triangles = g->ctx[0]->nt_real;
@@ -153,5 +268,7 @@ int nm_group_label_mesh(nm_group* g, const double* nodes, std::size_t n, const s
     }
   });
 }
+
+int nm_group_uses_nccl(const nm_group* g) { return g && !g->comms.empty() ? 1 : 0; }
 
 }  // extern "C"

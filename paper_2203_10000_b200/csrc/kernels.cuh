@@ -1252,4 +1252,14 @@ static __global__ void k_max_index(const uint4* __restrict__ tets, std::size_t n
   if ((threadIdx.x & 31) == 0) atomicMax(out, m);
 }
 
+// Largest value of a uint32 array (device-side range checks of caller ids).
+static __global__ void k_max_u32(const std::uint32_t* __restrict__ v, std::size_t n, std::uint32_t* __restrict__ out) {
+  std::uint32_t m = 0;
+  for (std::size_t i = blockIdx.x * static_cast<std::size_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<std::size_t>(gridDim.x) * blockDim.x)
+    m = max(m, __ldg(v + i));
+  m = __reduce_max_sync(kFull, m);
+  if ((threadIdx.x & 31) == 0) atomicMax(out, m);
+}
+
 }  // namespace nm

@@ -580,6 +580,62 @@ int nm_refine_device(nm_ctx* c, const double* nodes, std::size_t n, const std::u
   });
 }
 
+int nm_refine_device_d(nm_ctx* c, const double* d_nodes, std::size_t n, const std::uint32_t* d_tets, std::size_t nt,
+                       const int* d_labels, const std::uint32_t* d_sel, std::size_t ns, void* stream, nm_mesh** out) {
+  return guarded([&] {
+    if (!c) throw Error("null context");
+    if (!out) throw Error("null output pointer");
+    *out = nullptr;
+    if (ns > nt) throw Error("InvalidSelection: more selected tets than tets (SPEC.md:292)");
+    if (n > 0xffffffffull || nt > 0xffffffffull) throw Error("mesh exceeds 32-bit ids");
+    NM_CUDA(cudaSetDevice(c->opt.device));
+    cudaStream_t st = c->pick(stream);
+    // device-side validation of the inputs (the caller's arrays never reach the host)
+    if (nt) {
+      auto* d_word = c->word.as<std::uint32_t>(2);
+      NM_CUDA(cudaMemsetAsync(d_word, 0, 2 * sizeof(std::uint32_t), st));
+      nm::k_max_index<<<grid_for(nt, 256, c->sm_count * 8), 256, 0, st>>>(reinterpret_cast<const uint4*>(d_tets), nt,
+                                                                          d_word);
+      if (ns)
+        nm::k_max_u32<<<grid_for(ns, 256, c->sm_count * 8), 256, 0, st>>>(d_sel, ns, d_word + 1);
+      NM_CUDA(cudaGetLastError());
+      std::uint32_t h[2];
+      NM_CUDA(cudaMemcpyAsync(h, d_word, sizeof h, cudaMemcpyDeviceToHost, st));
+      NM_CUDA(cudaStreamSynchronize(st));
+      if (h[0] >= n) throw Error("a tet references a node >= node count");
+      if (ns && h[1] >= nt) throw Error("InvalidSelection: selected tet id out of range (SPEC.md:292)");
+    }
+    const int* lab = d_labels;
+    if (!lab) {
+      auto* z = c->meshA_labels.as<int>(std::max<std::size_t>(nt, 1));
+      NM_CUDA(cudaMemsetAsync(z, 0, std::max<std::size_t>(nt, 1) * sizeof(int), st));
+      lab = z;
+    }
+    std::uint64_t l = 0;
+    const auto [n2, nt2] = refine_dev(c, d_nodes, n, d_tets, nt, lab, d_sel, static_cast<std::uint32_t>(ns), st, l);
+    *out = make_device_mesh(c, c->meshB_nodes, c->meshB_tets, c->meshB_labels, &c->meshB_parent, nullptr, n2, nt2, n,
+                            st);
+    NM_CUDA(cudaStreamSynchronize(st));  // the handle's arrays are complete for any stream that reads them
+  });
+}
+
+int nm_mesh_copy_device(const nm_mesh* m, double* d_nodes, std::uint32_t* d_tets, int* d_labels, std::uint32_t* d_parent,
+                        void* stream) {
+  return guarded([&] {
+    if (!m || m->dev.device < 0) throw Error("not a device-resident mesh");
+    NM_CUDA(cudaSetDevice(m->dev.device));
+    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : cudaStreamLegacy;
+    const auto& d = m->dev;
+    auto cp = [&](void* dst, const void* src, std::size_t bytes) {
+      if (dst && bytes) NM_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, st));
+    };
+    cp(d_nodes, d.nodes, 3 * d.nn * sizeof(double));
+    cp(d_tets, d.tets, 4 * d.nt * sizeof(std::uint32_t));
+    cp(d_labels, d.labels, d.nt * sizeof(int));
+    cp(d_parent, d.parent, d.nt * sizeof(std::uint32_t));
+  });
+}
+
 int nm_refine_boundary(nm_ctx* c, const double* nodes, std::size_t n, const std::uint32_t* tets, std::size_t nt,
                        const int* labels, int label_a, int label_b, nm_mesh** out) {
   return guarded([&] {

@@ -12,6 +12,8 @@
 #include <cstddef>
 #include <cstring>
 #include <functional>
+#include <stdexcept>
+#include <string>
 #include <mutex>
 #include <thread>
 #include <vector>

@@ -136,9 +136,23 @@ def gather_labels(labels: "torch.Tensor", sh: Shard, group=None) -> "torch.Tenso
     return all_gather_masks(labels, sh, group)
 
 
+def _gather_into(out, buf, group):
+    """all_gather_into_tensor; a host-side collective when the backend is gloo
+    and the tensors live on the GPU (single-GPU multi-rank runs, tests)."""
+    import torch
+    import torch.distributed as dist
+    if buf.is_cuda and dist.get_backend(group) == "gloo":
+        host = torch.empty(out.shape, dtype=out.dtype)
+        dist.all_gather_into_tensor(host, buf.cpu(), group=group)
+        out.copy_(host)
+    else:
+        dist.all_gather_into_tensor(out, buf, group=group)
+
+
 def all_gather_varlen(local: "torch.Tensor", group=None) -> "torch.Tensor":
     """All-gather of variable-length 1-D tensors (rank order preserved):
-    counts first, then equal padded buffers."""
+    counts first, then equal padded buffers. Device tensors
+    stay on the device with NCCL."""
     import torch
     import torch.distributed as dist
     if not (dist.is_available() and dist.is_initialized()):
@@ -146,13 +160,13 @@ def all_gather_varlen(local: "torch.Tensor", group=None) -> "torch.Tensor":
     world = dist.get_world_size(group)
     cnt = torch.tensor([local.shape[0]], dtype=torch.int64, device=local.device)
     cnts = torch.empty(world, dtype=torch.int64, device=local.device)
-    dist.all_gather_into_tensor(cnts, cnt, group=group)
+    _gather_into(cnts, cnt, group)
     cl = [int(c) for c in cnts.tolist()]
     mx = max(cl) if cl else 0
     buf = torch.zeros(max(mx, 1), dtype=local.dtype, device=local.device)
     buf[: local.shape[0]] = local
     out = torch.empty(world * max(mx, 1), dtype=local.dtype, device=local.device)
-    dist.all_gather_into_tensor(out, buf, group=group)
+    _gather_into(out, buf, group)
     parts = [out[r * max(mx, 1): r * max(mx, 1) + cl[r]] for r in range(world)]
     return torch.cat(parts) if parts else local[:0]
 
@@ -191,3 +205,48 @@ def refine_relabel_sharded(nodes, tets, masks, levels, node_fn, flag_fn, refine_
     t_local = torch.as_tensor(np.ascontiguousarray(tets[tsh.lo:tsh.hi]).view(np.int32), device=device)
     labels = tet_fn(t_local, masks)
     return nodes, tets, labels, tsh, masks
+
+
+def refine_relabel_device(ctx, d_nodes, d_tets, d_masks, levels: int, rank: int, world: int, group=None,
+                          active_mask: int = 0xFFFFFFFF):
+    """The recursive boundary driver over `world` ranks with the mesh resident
+    on every rank's GPU. Per level:
+      1. each rank flags the straddling tets of ITS tet range on the device
+         (nm_flag_boundary_device: ordered compaction);
+      2. the flag lists are all-gathered (NCCL; ascending, so every rank gets
+         the same global selection);
+      3. every rank refines the same mesh with the same selection on its GPU
+         (nm_refine_device_d; deterministic numbering -> identical meshes);
+      4. each rank evaluates ITS shard of the new nodes and the new masks are
+         all-gathered (NCCL).
+    Nothing crosses to the host but counts. Returns (nodes, tets, labels of
+    this rank's tet range, tet shard, masks), all device tensors; equal bit
+    for bit to nm_refine_relabel on one GPU.
+
+    ctx: a Context on this rank's device with the surfaces set; d_nodes
+    (N,3) float64, d_tets (T,4) int32, d_masks (N,) int32 CUDA tensors."""
+    import torch
+    dev = d_nodes.device
+    cs = torch.cuda.current_stream(dev)  # every kernel ordered with the torch collectives on this stream
+    for _ in range(levels):
+        tsh = shard(d_tets.shape[0], world, rank)
+        ids = torch.empty(max(tsh.size, 1), dtype=torch.int32, device=dev)
+        cnt = torch.zeros(1, dtype=torch.int32, device=dev)
+        if tsh.size:
+            ctx.flag_boundary_device(d_tets[tsh.lo:tsh.hi], d_masks, ids, cnt, active_mask=active_mask, stream=cs)
+        k = int(cnt.item())
+        sel = all_gather_varlen(ids[:k].to(torch.int64) + tsh.lo, group).to(torch.int32)
+        nodes2, tets2, _, _, n_old = ctx.refine_device_tensors(d_nodes, d_tets, None, sel, stream=cs)
+        new = nodes2[n_old:]
+        nsh = shard(new.shape[0], world, rank)
+        m_local = torch.zeros(max(nsh.per, 1), dtype=torch.int32, device=dev)
+        if nsh.size:
+            ctx.label_nodes_device(new[nsh.lo:nsh.hi], m_local[: nsh.size], stream=cs, stats=False)
+        m_new = all_gather_masks(m_local[: nsh.per], nsh, group) if nsh.per else m_local[:0]
+        d_masks = torch.cat([d_masks, m_new])
+        d_nodes, d_tets = nodes2, tets2
+    tsh = shard(d_tets.shape[0], world, rank)
+    labels = torch.empty(max(tsh.size, 1), dtype=torch.int32, device=dev)[: tsh.size]
+    if tsh.size:
+        ctx.label_tets_device(d_tets[tsh.lo:tsh.hi], d_masks, labels, stream=cs, stats=False)
+    return d_nodes, d_tets, labels, tsh, d_masks

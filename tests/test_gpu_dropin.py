@@ -166,6 +166,28 @@ def test_group_multi_context_bitwise(devices, cull):
         c.set_surfaces(S.xyz, S.tri, S.comp_off, S.label_ids)
         ref, mref, _ = c.label_mesh(nodes, tets, want_masks=True)
     with Group(devices, cull_outside=cull) as g:
+        assert not g.uses_nccl                      # one GPU: peer copies between the contexts
+        g.set_surfaces(S.xyz, S.tri, S.comp_off, S.label_ids)
+        lab, m = g.label_mesh(nodes, tets)
+    np.testing.assert_array_equal(lab, ref)
+    np.testing.assert_array_equal(m, mref)
+
+
+def test_group_nccl_exchange_one_device(monkeypatch):
+    """The NCCL exchange of nm_group (ncclCommInitAll + ncclAllGather in
+    place), forced on for a single device (NM_GROUP_NCCL=1): same labels and
+    masks as a plain context. With distinct devices this is the path every
+    multi-GPU group takes."""
+    from paper_2203_10000_b200._native import Context, Group
+    monkeypatch.setenv("NM_GROUP_NCCL", "1")
+    cfg = synth.config(2)
+    S = cfg.surfaces
+    nodes, tets = cfg.lattice_mesh()
+    with Context(0) as c:
+        c.set_surfaces(S.xyz, S.tri, S.comp_off, S.label_ids)
+        ref, mref, _ = c.label_mesh(nodes, tets, want_masks=True)
+    with Group([0]) as g:
+        assert g.uses_nccl
         g.set_surfaces(S.xyz, S.tri, S.comp_off, S.label_ids)
         lab, m = g.label_mesh(nodes, tets)
     np.testing.assert_array_equal(lab, ref)
@@ -268,6 +290,61 @@ def test_two_ranks_recursive_driver_gpu(tmp_path):
         c.set_surfaces(S.xyz, S.tri, S.comp_off, S.label_ids)
         n2, t2, lab, masks, st = c.refine_relabel(nodes, tets, levels=2)
     np.testing.assert_array_equal(np.load(tmp_path / "tets.npy"), t2)
+    np.testing.assert_array_equal(np.load(tmp_path / "labels.npy"), lab)
+
+
+def _gpu_rank_recursive_device(rank, world, port, out_dir):
+    import torch
+    import torch.distributed as dist
+    from paper_2203_10000_b200._native import Context
+    from paper_2203_10000_b200.distributed import gather_labels, refine_relabel_device
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        cfg = synth.config(2)
+        S = cfg.surfaces
+        nodes, tets = synth.lattice_mesh((-110.0, -110.0, -110.0), 5.0, (44, 44, 44))
+        ctx = Context(0)
+        ctx.set_surfaces(S.xyz, S.tri, S.comp_off, S.label_ids)
+        d_nodes = torch.from_numpy(nodes).cuda()
+        d_tets = torch.from_numpy(tets.view(np.int32)).cuda()
+        d_m = torch.zeros(nodes.shape[0], dtype=torch.int32, device="cuda")
+        ctx.label_nodes_device(d_nodes, d_m, stream=torch.cuda.current_stream(), stats=False)
+        n2, t2, labels, tsh, masks = refine_relabel_device(ctx, d_nodes, d_tets, d_m, 2, rank, world)
+        full = gather_labels(labels, tsh)
+        if rank == 0:
+            np.save(os.path.join(out_dir, "labels.npy"), full.cpu().numpy())
+            np.save(os.path.join(out_dir, "tets.npy"), t2.cpu().numpy().view(np.uint32))
+            np.save(os.path.join(out_dir, "nodes.npy"), n2.cpu().numpy())
+            np.save(os.path.join(out_dir, "masks.npy"), masks.cpu().numpy().view(np.uint32))
+        ctx.close()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_ranks_recursive_driver_device_resident(tmp_path, world):
+    """The device-resident multi-rank recursive driver (refine_relabel_device:
+    flags, refinement, new-node masks all on the GPU; only counts reach the
+    host) over 2 and 3 ranks equals the single-process nm_refine_relabel bit
+    for bit (nodes, tets, masks, labels)."""
+    import socket
+    import torch.multiprocessing as mp
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    mp.spawn(_gpu_rank_recursive_device, args=(world, port, str(tmp_path)), nprocs=world, join=True)
+    from paper_2203_10000_b200._native import Context
+    cfg = synth.config(2)
+    S = cfg.surfaces
+    nodes, tets = synth.lattice_mesh((-110.0, -110.0, -110.0), 5.0, (44, 44, 44))
+    with Context(0) as c:
+        c.set_surfaces(S.xyz, S.tri, S.comp_off, S.label_ids)
+        n2, t2, lab, masks, st = c.refine_relabel(nodes, tets, levels=2)
+    np.testing.assert_array_equal(np.load(tmp_path / "nodes.npy"), n2)
+    np.testing.assert_array_equal(np.load(tmp_path / "tets.npy"), t2)
+    np.testing.assert_array_equal(np.load(tmp_path / "masks.npy"), masks)
     np.testing.assert_array_equal(np.load(tmp_path / "labels.npy"), lab)
 
 
