@@ -512,7 +512,7 @@ def main():
         cpp = {"path": "nestmesh::Labeler::initial_label (C++, reference types, pageable std::vector buffers), "
                        "host clock per call: H2D nodes + tets, labeling, D2H labels"}
         for mode in (0, 2):
-            out = np.zeros(4, np.float64)
+            out = np.zeros(6, np.float64)
             lab = np.empty(nt, np.int32)
             k = min(args.steps, 3) if mode == 0 else args.steps
             rc = L.dropin_bench(P(sx, ctypes.c_double), ctypes.c_size_t(sx.shape[0]), P(st_, ctypes.c_uint32),
@@ -524,12 +524,17 @@ def main():
                 cpp["cull%d" % mode] = {"error": "dropin_bench failed"}
                 continue
             e = {"labeler_build_s": out[0], "first_call_s": out[1], "e2e_mean_s": out[2], "e2e_best_s": out[3],
+                 "e2e_into_mesh_labels_mean_s": out[4], "e2e_into_mesh_labels_best_s": out[5],
                  "steps": k, "evals_per_s_e2e": evals_total / out[2] if out[2] else None,
                  "labels_identical": bool(np.array_equal(lab, ref_labels))}
+            pinned = None
             if mode == 2 and cull and "e2e_full_mesh_labeling_time_s" in cull.get("mode2", {}):
-                e["vs_python_pinned_e2e"] = out[2] / cull["mode2"]["e2e_full_mesh_labeling_time_s"]
+                pinned = cull["mode2"]["e2e_full_mesh_labeling_time_s"]
             if mode == 0 and e2e:
-                e["vs_python_pinned_e2e"] = out[2] / (e2e["ms_per_step"] / 1e3)
+                pinned = e2e["ms_per_step"] / 1e3
+            if pinned:
+                e["vs_python_pinned_e2e"] = out[2] / pinned
+                e["into_vs_python_pinned_e2e"] = out[4] / pinned
             cpp["cull%d" % mode] = e
 
     # N > 1: the certified-cell pass split by COST over the ranks (every rank

@@ -248,7 +248,18 @@ class Labeler {
   /// initial_label. masks_out (nullable) receives the node masks.
   std::vector<int> initial_label(const TetrahedralMesh& mesh, const SolidAngleParams& params, nm_stats* stats = nullptr,
                                  std::vector<std::uint32_t>* masks_out = nullptr) {
-    std::vector<int> labels(mesh.tet_count());
+    std::vector<int> labels;
+    initial_label_into(mesh, params, labels, stats, masks_out);
+    return labels;
+  }
+
+  /// initial_label into a caller vector (e.g. mesh.labels), reused without a
+  /// new allocation when its capacity suffices: repeated labeling of large
+  /// meshes does not pay the first-touch and zero-fill of a fresh 4 B/tet
+  /// array per call.
+  void initial_label_into(const TetrahedralMesh& mesh, const SolidAngleParams& params, std::vector<int>& labels,
+                          nm_stats* stats = nullptr, std::vector<std::uint32_t>* masks_out = nullptr) {
+    labels.resize(mesh.tet_count());
     std::uint32_t* m = nullptr;
     if (masks_out) {
       masks_out->resize(mesh.node_count());
@@ -262,7 +273,6 @@ class Labeler {
       detail::check(nm_label_mesh(ctx_.get(), detail::xyz_of(mesh.nodes), mesh.node_count(),
                                   detail::idx_of(mesh.tetrahedra), mesh.tet_count(), params.threshold, labels.data(),
                                   m, stats));
-    return labels;
   }
 
   /// relabel_recursive. Throws NonConvergence (carrying the

@@ -221,11 +221,13 @@ static __global__ void __launch_bounds__(kBlock, (NP == 1 ? NM_MIN_BLOCKS : NM_M
     const std::size_t i = base + k;
     valid[k] = i < n_end;
     std::size_t ii = valid[k] ? i : n_end - 1;
-    if (SPARSE) ii = prm.sp_list[ii];
-    const std::uint32_t j = prm.order ? prm.order[ii] : static_cast<std::uint32_t>(ii);
+    // points, order and lists are read once: streaming loads (evict-first),
+    // so they do not push the triangle tiles (re-read by every CTA) out of L2
+    if (SPARSE) ii = __ldcs(prm.sp_list + ii);
+    const std::uint32_t j = prm.order ? __ldcs(prm.order + ii) : static_cast<std::uint32_t>(ii);
     pid[k] = j;
-    const double dx = prm.pts[3 * static_cast<std::size_t>(j)] - prm.cx, dy = prm.pts[3 * static_cast<std::size_t>(j) + 1] - prm.cy,
-                 dz = prm.pts[3 * static_cast<std::size_t>(j) + 2] - prm.cz;
+    const double* pj = prm.pts + 3 * static_cast<std::size_t>(j);
+    const double dx = __ldcs(pj) - prm.cx, dy = __ldcs(pj + 1) - prm.cy, dz = __ldcs(pj + 2) - prm.cz;
     const float fx = static_cast<float>(dx), fy = static_cast<float>(dy), fz = static_cast<float>(dz);
     const float gx = static_cast<float>(dx - fx), gy = static_cast<float>(dy - fy), gz = static_cast<float>(dz - fz);
     if (k & 1) {
@@ -508,9 +510,9 @@ static __global__ void __launch_bounds__(kBlock, (NP == 1 ? NM_MIN_BLOCKS : NM_M
       if (SPARSE) {
         if (mask[k]) atomicOr(prm.masks + pid[k], mask[k]);
         if (fmask[k]) atomicOr(prm.flagmask + prm.sp_list[base + k], fmask[k]);
-      } else if (gridDim.y == 1) {  // evaluation order: coalesced stores
-        prm.masks[base + k] = mask[k];
-        prm.flagmask[base + k] = fmask[k];
+      } else if (gridDim.y == 1) {  // evaluation order: coalesced, streaming stores
+        __stcs(prm.masks + base + k, mask[k]);
+        __stcs(prm.flagmask + base + k, fmask[k]);
       } else {
         if (mask[k]) atomicOr(prm.masks + base + k, mask[k]);
         if (fmask[k]) atomicOr(prm.flagmask + base + k, fmask[k]);
@@ -689,7 +691,7 @@ static __global__ void k_unpermute(const std::uint32_t* __restrict__ order, std:
                                    const std::uint32_t* __restrict__ ms, std::uint32_t* __restrict__ masks) {
   for (std::size_t i = blockIdx.x * static_cast<std::size_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<std::size_t>(gridDim.x) * blockDim.x)
-    masks[order ? __ldg(order + i) : i] = __ldg(ms + i);
+    masks[order ? __ldcs(order + i) : i] = __ldcs(ms + i);
 }
 
 struct PredStraddle {
@@ -900,9 +902,9 @@ static __global__ void k_label_tets(const uint4* __restrict__ tets, std::size_t 
   const int* id = stage_ids(ids, s_ids);
   for (std::size_t i = blockIdx.x * static_cast<std::size_t>(blockDim.x) + threadIdx.x; i < nt;
        i += static_cast<std::size_t>(gridDim.x) * blockDim.x) {
-    const uint4 t = __ldg(tets + i);
+    const uint4 t = __ldcs(tets + i);  // read once; the gathered masks stay in L2
     const std::uint32_t m = __ldg(masks + t.x) & __ldg(masks + t.y) & __ldg(masks + t.z) & __ldg(masks + t.w);
-    labels[i] = m ? id[__ffs(m) - 1] : 0;
+    __stcs(labels + i, m ? id[__ffs(m) - 1] : 0);
   }
 }
 
@@ -914,12 +916,16 @@ static __global__ void k_label_tets(const uint4* __restrict__ tets, std::size_t 
 namespace nm {
 
 // Outward face i of a tet (mesh.hpp:57-64), sorted into (a <= b <= c).
+// face f of a tet in outward order (mesh.hpp:57-64: {1,2,3} {0,3,2} {0,1,3}
+// {0,2,1}), by selects (no local-memory table)
+__device__ __forceinline__ void face_verts(const uint4 t, int f, std::uint32_t& a, std::uint32_t& b, std::uint32_t& c) {
+  a = f == 0 ? t.y : t.x;
+  b = f == 0 ? t.z : (f == 1 ? t.w : (f == 2 ? t.y : t.z));
+  c = f == 0 ? t.w : (f == 1 ? t.z : (f == 2 ? t.w : t.y));
+}
+
 __device__ __forceinline__ void face_key(const uint4 t, int f, std::uint32_t& a, std::uint32_t& b, std::uint32_t& c) {
-  const std::uint32_t v[4] = {t.x, t.y, t.z, t.w};
-  const int F[4][3] = {{1, 2, 3}, {0, 3, 2}, {0, 1, 3}, {0, 2, 1}};
-  a = v[F[f][0]];
-  b = v[F[f][1]];
-  c = v[F[f][2]];
+  face_verts(t, f, a, b, c);
   if (a > b) { const std::uint32_t s = a; a = b; b = s; }
   if (b > c) { const std::uint32_t s = b; b = c; c = s; }
   if (a > b) { const std::uint32_t s = a; a = b; b = s; }
@@ -1058,7 +1064,8 @@ static __global__ void k_region(const int* labels, std::size_t nt, const LabelId
        t += static_cast<std::size_t>(gridDim.x) * blockDim.x) {
     const int l = labels[t];
     bool in = false;
-    for (int k = 0; k < n_set; ++k) in |= set.id[k] == l;
+#pragma unroll
+    for (int k = 0; k < 32; ++k) in |= k < n_set && set.id[k] == l;  // constant indices: no local copy
     in_region[t] = in ? 1 : 0;
   }
 }
@@ -1085,13 +1092,11 @@ static __global__ void k_face_tris(const uint4* tets, const std::uint32_t* faces
                             std::uint32_t* t1, std::uint32_t* t2) {
   for (std::uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nb; i += gridDim.x * blockDim.x) {
     const std::uint32_t f = faces[i];
-    const uint4 e = tets[f >> 2];
-    const std::uint32_t v[4] = {e.x, e.y, e.z, e.w};
-    const int F[4][3] = {{1, 2, 3}, {0, 3, 2}, {0, 1, 3}, {0, 2, 1}};
-    const int k = f & 3;
-    t0[i] = v[F[k][0]];
-    t1[i] = v[F[k][1]];
-    t2[i] = v[F[k][2]];
+    std::uint32_t a, b, c;
+    face_verts(tets[f >> 2], static_cast<int>(f & 3), a, b, c);
+    t0[i] = a;
+    t1[i] = b;
+    t2[i] = c;
   }
 }
 

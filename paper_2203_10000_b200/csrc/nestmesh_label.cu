@@ -1189,11 +1189,19 @@ int nm_label_mesh(nm_ctx* c, const double* nodes, std::size_t n, const std::uint
     auto* d_tets = c->tets.as<std::uint32_t>(4 * std::max<std::size_t>(nt, 1));
     auto* d_labels = c->labels.as<int>(std::max<std::size_t>(nt, 1));
     auto* d_word = c->word.as<std::uint32_t>(1);
-    c->h2d(d_pts, nodes, 3 * n * sizeof(double), c->stream);
     // tet upload + index validation on the side stream, from a helper host
-    // thread (a pageable tet array is staged by host copies), so it runs under
-    // the whole node pass (which synchronises the host for the fix-up's pair
-    // lists and, with certified cells, for the sparse grid)
+    // thread (a pageable tet array is staged by host copies), started first so
+    // it runs under the node upload and the whole node pass (which
+    // synchronises the host for the fix-up's pair lists and, with certified
+    // cells, for the sparse grid)
+    const bool timing = std::getenv("NM_TIMING") != nullptr;
+    const auto t_start = std::chrono::steady_clock::now();
+    auto lap = [&](const char* what) {
+      if (!timing) return;
+      NM_CUDA(cudaStreamSynchronize(c->stream));
+      std::fprintf(stderr, "[nm_label_mesh] %-14s %8.2f ms\n", what,
+                   std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count());
+    };
     std::exception_ptr side_err;
     std::thread side_thread;
     if (nt) {
@@ -1218,9 +1226,13 @@ int nm_label_mesh(nm_ctx* c, const double* nodes, std::size_t n, const std::uint
         if (t.joinable()) t.join();
       }
     } join{side_thread};
+    c->h2d(d_pts, nodes, 3 * n * sizeof(double), c->stream);
+    lap("nodes h2d");
     label_nodes_dev(c, d_pts, n, T, d_masks, nullptr, c->stream, stats, nullptr, /*stats_deferred=*/true);
+    lap("node pass");
     if (nt) {
       side_thread.join();
+      lap("tets h2d joined");
       if (side_err) std::rethrow_exception(side_err);
       NM_CUDA(cudaStreamWaitEvent(c->stream, c->ev_side, 0));
       NM_CUDA(cudaEventSynchronize(c->ev_side));
@@ -1231,8 +1243,10 @@ int nm_label_mesh(nm_ctx* c, const double* nodes, std::size_t n, const std::uint
     }
     if (stats && n) read_node_stats(c, n, c->stream, stats);
     label_tets_dev(c, d_tets, nt, d_masks, d_labels, c->stream, stats);
+    lap("tet labels");
     c->d2h(labels_out, d_labels, nt * sizeof(int), c->stream);
     if (masks_out) c->d2h(masks_out, d_masks, n * sizeof(std::uint32_t), c->stream);
+    lap("d2h");
     NM_CUDA(cudaStreamSynchronize(c->stream));
   });
 }

@@ -90,15 +90,20 @@ def opcounts(path, sass_hash, evals, config, points, note=""):
     import json
     rows = [r for r in csv.reader(open(path)) if len(r) > 10]
     h = rows[0]
-    col = h.index("sass__thread_inst_executed_true_per_opcode")
     kcol = h.index("Kernel Name")
-    cands = [r for r in rows[1:] if "k_label<" in r[kcol] and "(" in r[col]]
-    r = cands[-1]
-    thr = _opcode_counts(r[col])
-    warp = _opcode_counts(r[h.index("sass__inst_executed_per_opcode")]) if "sass__inst_executed_per_opcode" in h else {}
+    if "Metric Name" in h:  # long format: one metric per row
+        mi, vi = h.index("Metric Name"), h.index("Metric Value")
+        last_id = [r for r in rows[1:] if "k_label<" in r[kcol]][-1][h.index("ID")]
+        cells = {r[mi]: r[vi] for r in rows[1:] if r[h.index("ID")] == last_id}
+        r = next(r for r in rows[1:] if r[h.index("ID")] == last_id)
+    else:
+        r = [r for r in rows[1:] if "k_label<" in r[kcol]][-1]
+        cells = dict(zip(h, r))
+    thr = _opcode_counts(cells["sass__thread_inst_executed_true_per_opcode"])
+    warp = _opcode_counts(cells["sass__inst_executed_per_opcode"]) if "sass__inst_executed_per_opcode" in cells else {}
     lane_ops = sum(thr.get(k, 0) * w for k, w in FP32_PIPE.items())
     evals = int(evals)
-    out = {"kernel": r[kcol], "sass_sha16": sass_hash, "config": config, "points": int(points), "evals": evals,
+    out = {"kernel": r[kcol], "grid": r[h.index("Grid Size")], "sass_sha16": sass_hash, "config": config, "points": int(points), "evals": evals,
            "fp32_lane_ops": lane_ops, "fp32_lane_ops_per_eval": lane_ops / evals,
            "mufu_per_eval": thr.get("MUFU", 0) / evals,
            "thread_inst_per_eval": {k: v / evals for k, v in sorted(thr.items(), key=lambda kv: -kv[1])[:16]},

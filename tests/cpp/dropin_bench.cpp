@@ -57,18 +57,28 @@ extern "C" int dropin_bench(const double* sxyz, std::size_t nv, const std::uint3
     SolidAngleParams params;
     std::vector<int> labels = lab.initial_label(mesh, params);  // warm-up (first-use allocations)
     const auto t2 = clk::now();
-    double total = 0.0, best = 1e300;
-    for (int i = 0; i < steps; ++i) {
+    double total = 0.0, best = 1e300, total_into = 0.0, best_into = 1e300;
+    for (int i = 0; i < steps; ++i) {  // by value: a fresh std::vector<int> per call
       const auto a = clk::now();
       labels = lab.initial_label(mesh, params);
       const double d = sec(a, clk::now());
       total += d;
       best = d < best ? d : best;
     }
+    for (int i = 0; i < steps; ++i) {  // into mesh.labels (reused storage)
+      const auto a = clk::now();
+      lab.initial_label_into(mesh, params, mesh.labels);
+      const double d = sec(a, clk::now());
+      total_into += d;
+      best_into = d < best_into ? d : best_into;
+    }
+    if (mesh.labels != labels) throw std::runtime_error("initial_label_into != initial_label");
     out[0] = sec(t0, t1);
     out[1] = sec(t1, t2);
     out[2] = steps ? total / steps : 0.0;
     out[3] = steps ? best : 0.0;
+    out[4] = steps ? total_into / steps : 0.0;
+    out[5] = steps ? best_into : 0.0;
     std::memcpy(labels_out, labels.data(), nt * sizeof(int));
     return 0;
   } catch (const std::exception& e) {
