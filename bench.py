@@ -631,7 +631,11 @@ def main():
             "peak": lane_peak, "unit": "FP32 lane-ops/s",
             "frac": achieved * ops_pe / lane_peak if ops_pe else None,
             "traffic": traffic,
-            "algorithmic_bytes": nsh.size * (24 + 8),
+            # per point: fp64 xyz + evaluation order in, mask + flag out; plus
+            # the triangle tiles once (48 B per padded triangle slot + the
+            # 5-float4 subtile records)
+            "algorithmic_bytes": nsh.size * (24 + 4 + 8) + sinfo["slots"] * 48
+                                 + sinfo["slots"] // 32 * 80,
             "peak_basis": f"{sms} SMs x {FP32_LANES_PER_SM} FP32 lanes x {sm_max:.0f} MHz (MEASURED_PEAKS.json sm_max_mhz)",
             "evals_per_s": achieved,
             "fp32_lane_ops_per_eval": ops_pe,

@@ -98,8 +98,8 @@ def build_cpp_dropin_test(force=False):
         return None
     out = ROOT / "build" / "dropin_test"
     src = ROOT / "tests" / "cpp" / "dropin_test.cpp"
-    deps = [src, ROOT / "include" / "nestmesh" / "labeling.hpp", ROOT / "include" / "nestmesh_label.h",
-            LIB / "libnestmesh_label.so"]
+    deps = [src, ROOT / "include" / "nestmesh" / "labeling.hpp", ROOT / "include" / "nestmesh" / "label_sidecar.hpp",
+            ROOT / "include" / "nestmesh_label.h", LIB / "libnestmesh_label.so"]
     if force or _stale(out, deps):
         out.parent.mkdir(exist_ok=True)
         _run([CXX, "-std=c++20", "-O2", "-Wall", "-Wextra", f"-I{ref_inc}", f"-I{ROOT / 'include'}", str(src),

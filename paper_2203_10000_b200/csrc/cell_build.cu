@@ -152,6 +152,16 @@ class CellBuild : public CellBuilder {
       if (total_ > 0xffffffffull) throw Error("certified-cell grids exceed 2^32 cells");
       coff_[k + 1] = coff_[k] + (order[k].size() + nm::kCluster - 1) / nm::kCluster;
     }
+    // memory budget: per level-1 cell ~13 B of host arrays (certified flag,
+    // block and run indices, code) and ~5 B on the device (flag, code), plus
+    // up to 64 B of children per uncertified cell. A cell_axis that would need
+    // more than kHostBudget of host memory fails here instead of driving the
+    // host into the OOM killer (cfg5 at the default axis 120: 18.5M cells).
+    constexpr double kHostBudget = 8e9;
+    if (double(total_) * 18.0 > kHostBudget)
+      throw Error("certified-cell grids of " + std::to_string(total_) + " cells (~" +
+                  std::to_string(static_cast<long long>(double(total_) * 18.0 / 1e6)) +
+                  " MB) exceed the 8 GB build budget: lower nm_options.cell_axis");
     const std::size_t ncl = coff_[K];
     std::vector<float4> clus(ncl), tsph(ncl * nm::kCluster);
     std::vector<std::uint32_t> ctri(ncl * nm::kCluster);

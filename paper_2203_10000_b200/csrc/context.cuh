@@ -155,12 +155,14 @@ struct nm_ctx {
       const int hw = static_cast<int>(std::thread::hardware_concurrency());
       // measured on the GPU box (probes/staging.cu, 16 host threads): host
       // copies reach ~73 GB/s with 8 threads, the pinned DMA ~55 GB/s
-      p = std::make_unique<nmh::CopyPool>(std::max(1, std::min(side ? 5 : 7, hw / 2 - 1)));
+      p = std::make_unique<nmh::CopyPool>(std::max(1, side ? std::min(3, hw / 4) : std::min(11, hw - 5)));
     }
     return *p;
   }
-  void h2d(void* d, const void* h, std::size_t bytes, cudaStream_t st, bool side = false) {
-    (side ? stage_side : stage_main).h2d(d, h, bytes, st, pool(side));
+  // side: the side stream's chunk buffers; the copy pool is the main one
+  // unless side_pool (a caller that copies concurrently with another stager)
+  void h2d(void* d, const void* h, std::size_t bytes, cudaStream_t st, bool side = false, bool side_pool = false) {
+    (side ? stage_side : stage_main).h2d(d, h, bytes, st, pool(side_pool));
   }
   void d2h(void* h, const void* d, std::size_t bytes, cudaStream_t st) { stage_main.d2h(h, d, bytes, st, pool(false)); }
   int sm_count = 0;

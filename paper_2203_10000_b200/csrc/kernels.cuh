@@ -40,6 +40,15 @@ constexpr int kSubUnroll = NM_SUB_UNROLL;
 #ifndef NM_MIN_BLOCKS_NP2
 #define NM_MIN_BLOCKS_NP2 3             // resident CTAs per SM requested for k_label<2>
 #endif
+#ifndef NM_STAGES
+// default: the two-buffer pipeline with one CTA barrier per tile; an
+// explicit NM_STAGES selects the full/empty-mbarrier pipeline of that depth
+#define NM_STAGES 2
+#ifndef NM_BARRIER_PIPELINE
+#define NM_BARRIER_PIPELINE
+#endif
+#endif
+constexpr int kStages = NM_STAGES;
 constexpr unsigned kFull = 0xffffffffu;
 constexpr double kInv2Pi = 0.15915494309189533576888376337251;
 
@@ -66,6 +75,9 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
                    smem_addr(dst)),
                "l"(src), "r"(bytes), "r"(smem_addr(bar))
                : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
 }
 __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
   asm volatile(
@@ -187,9 +199,15 @@ static __global__ void __launch_bounds__(kBlock, (NP == 1 ? NM_MIN_BLOCKS : NM_M
   // elected thread), completion signalled on one mbarrier per buffer: tile
   // t + 1 streams in from L2 while the CTA evaluates tile t.
   constexpr unsigned kSubF4Tile = kSubPerTile * kSubRec;
-  __shared__ alignas(128) float4 s_tri_buf[2][kTileF4];
-  __shared__ alignas(128) float4 s_sub_buf[2][kSubF4Tile];
-  __shared__ alignas(8) unsigned long long s_bar[2];
+  // kStages tile buffers: "full" mbarriers (bulk-copy transaction counts)
+  // and "empty" mbarriers (one arrival per warp when it is done with the
+  // buffer), so warps may drift up to kStages - 1 tiles apart without a CTA
+  // barrier per tile (NM_BARRIER_PIPELINE: the round-1 two-buffer scheme
+  // with one __syncthreads per tile).
+  __shared__ alignas(128) float4 s_tri_buf[kStages][kTileF4];
+  __shared__ alignas(128) float4 s_sub_buf[kStages][kSubF4Tile];
+  __shared__ alignas(8) unsigned long long s_bar[kStages];
+  __shared__ alignas(8) unsigned long long s_empty[kStages];
   __shared__ unsigned s_skip;
 
   std::size_t base = (static_cast<std::size_t>(blockIdx.x) * kBlock + threadIdx.x) * P;
@@ -249,8 +267,10 @@ static __global__ void __launch_bounds__(kBlock, (NP == 1 ? NM_MIN_BLOCKS : NM_M
   // Compartments every point of the CTA is outside of (exact culling) are
   // skipped by producer and consumers alike; the tile sequence is fixed here.
   if (threadIdx.x == 0) {
-    mbar_init(&s_bar[0], 1);
-    mbar_init(&s_bar[1], 1);
+    for (int b = 0; b < kStages; ++b) {
+      mbar_init(&s_bar[b], 1);
+      mbar_init(&s_empty[b], kBlock / 32);
+    }
     s_skip = ~0u;
     fence_mbar_init();
   }
@@ -267,8 +287,14 @@ static __global__ void __launch_bounds__(kBlock, (NP == 1 ? NM_MIN_BLOCKS : NM_M
     skip = s_skip;
   }
   const int c_lo = SPARSE ? c_sp : prm.split[blockIdx.y], c_hi = SPARSE ? c_sp + 1 : prm.split[blockIdx.y + 1];
-  // producer state (thread 0): next tile to fetch and its compartment
-  int pf_c = 0, pf_t = -1;
+  // producer state (thread 0 only): next tile to fetch, its compartment and
+  // the tiles issued so far, kept in shared memory so they take no register
+  // in the consumer threads
+  __shared__ int s_pf_c, s_pf_t;
+  __shared__ unsigned s_issued;
+  int& pf_c = s_pf_c;
+  int& pf_t = s_pf_t;
+  unsigned& issued = s_issued;
   // tile range of compartment c for this CTA (split sparse: one fold block)
   auto t_first = [&](int c) { return SPARSE ? t_lo : static_cast<int>(prm.comp_tiles[c]); };
   auto t_last = [&](int c) { return SPARSE ? t_hi : static_cast<int>(prm.comp_tiles[c + 1]); };
@@ -287,9 +313,21 @@ static __global__ void __launch_bounds__(kBlock, (NP == 1 ? NM_MIN_BLOCKS : NM_M
     bulk_g2s(s_tri_buf[b], prm.tri + static_cast<std::size_t>(pf_t) * kTileF4, kTileF4 * 16u, &s_bar[b]);
     bulk_g2s(s_sub_buf[b], prm.sub + static_cast<std::size_t>(pf_t) * kSubF4Tile, kSubF4Tile * 16u, &s_bar[b]);
   };
+  auto pf_next = [&] {  // producer: advance to the next tile of the sequence
+    if (pf_t >= 0 && ++pf_t >= t_last(pf_c)) pf_seek(pf_c + 1);
+  };
   if (threadIdx.x == 0) {
+    issued = 0;
     pf_seek(c_lo);
+#ifdef NM_BARRIER_PIPELINE
     if (pf_t >= 0) pf_issue(0);
+#else
+    for (int q = 0; q < kStages - 1 && pf_t >= 0; ++q) {
+      pf_issue(q);
+      ++issued;
+      pf_next();
+    }
+#endif
   }
   unsigned it = 0;
 
@@ -313,13 +351,27 @@ static __global__ void __launch_bounds__(kBlock, (NP == 1 ? NM_MIN_BLOCKS : NM_M
     for (int k = 0; k < P; ++k) outside[k] = CULL && ((cull[k] >> c) & 1u);
     if (CULL && ((skip >> c) & 1u)) tile = tile_end;
     for (; tile < tile_end; ++tile) {
+#ifdef NM_BARRIER_PIPELINE
       const int buf = it & 1u;
       if (threadIdx.x == 0) {
         // buffer buf ^ 1 was released by the barrier closing the previous tile
-        if (pf_t >= 0 && ++pf_t >= t_last(pf_c)) pf_seek(pf_c + 1);
+        pf_next();
         if (pf_t >= 0) pf_issue(buf ^ 1);
       }
       mbar_wait(&s_bar[buf], (it >> 1) & 1u);
+#else
+      const int buf = static_cast<int>(it % kStages);
+      if (threadIdx.x == 0 && pf_t >= 0) {
+        // tile `issued` (= it + kStages - 1) goes to the buffer that held tile
+        // issued - kStages: wait until every warp has released it
+        const unsigned b = issued % kStages;
+        if (issued >= static_cast<unsigned>(kStages)) mbar_wait(&s_empty[b], ((issued / kStages) - 1) & 1u);
+        pf_issue(static_cast<int>(b));
+        ++issued;
+        pf_next();
+      }
+      mbar_wait(&s_bar[buf], (it / kStages) & 1u);
+#endif
       ++it;
       const float4* const s_tri = s_tri_buf[buf];
       const float4* const s_sub = s_sub_buf[buf];
@@ -481,7 +533,12 @@ static __global__ void __launch_bounds__(kBlock, (NP == 1 ? NM_MIN_BLOCKS : NM_M
           blk64[k] = 0.0;
         }
       }
+#ifdef NM_BARRIER_PIPELINE
       __syncthreads();  // every warp is done with buffer buf: the producer may refill it
+#else
+      __syncwarp();  // this warp's reads of buffer buf are done
+      if ((threadIdx.x & 31) == 0) mbar_arrive(&s_empty[buf]);
+#endif
     }
     if (SPARSE && prm.sp_part) {  // split: this CTA's fold-block partials, added by k_sparse_finalize
       const unsigned nfb = prm.sp_fb[c];

@@ -1190,10 +1190,9 @@ int nm_label_mesh(nm_ctx* c, const double* nodes, std::size_t n, const std::uint
     auto* d_labels = c->labels.as<int>(std::max<std::size_t>(nt, 1));
     auto* d_word = c->word.as<std::uint32_t>(1);
     // tet upload + index validation on the side stream, from a helper host
-    // thread (a pageable tet array is staged by host copies), started first so
-    // it runs under the node upload and the whole node pass (which
-    // synchronises the host for the fix-up's pair lists and, with certified
-    // cells, for the sparse grid)
+    // thread (a pageable tet array is staged by host copies), so it runs under
+    // the whole node pass (which synchronises the host for the fix-up's pair
+    // lists and, with certified cells, for the sparse grid)
     const bool timing = std::getenv("NM_TIMING") != nullptr;
     const auto t_start = std::chrono::steady_clock::now();
     auto lap = [&](const char* what) {
@@ -1202,13 +1201,19 @@ int nm_label_mesh(nm_ctx* c, const double* nodes, std::size_t n, const std::uint
       std::fprintf(stderr, "[nm_label_mesh] %-14s %8.2f ms\n", what,
                    std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count());
     };
+    // the nodes first (every host copy thread on them: the node pass needs
+    // all of them), then the tets on the side thread under the node pass
+    c->h2d(d_pts, nodes, 3 * n * sizeof(double), c->stream);
+    lap("nodes h2d");
     std::exception_ptr side_err;
     std::thread side_thread;
     if (nt) {
       side_thread = std::thread([&] {
         try {
           NM_CUDA(cudaSetDevice(c->opt.device));
-          c->h2d(d_tets, tets, 4 * nt * sizeof(std::uint32_t), c->side, /*side=*/true);
+          // the main copy pool: the node copies are done, the main thread
+          // only drives the node pass until it joins this thread
+          c->h2d(d_tets, tets, 4 * nt * sizeof(std::uint32_t), c->side, /*side=*/true, /*side_pool=*/false);
           NM_CUDA(cudaMemsetAsync(d_word, 0, sizeof(std::uint32_t), c->side));
           nm::k_max_index<<<grid_for(nt, 256, c->sm_count * 8), 256, 0, c->side>>>(
               reinterpret_cast<const uint4*>(d_tets), nt, d_word);
@@ -1226,8 +1231,6 @@ int nm_label_mesh(nm_ctx* c, const double* nodes, std::size_t n, const std::uint
         if (t.joinable()) t.join();
       }
     } join{side_thread};
-    c->h2d(d_pts, nodes, 3 * n * sizeof(double), c->stream);
-    lap("nodes h2d");
     label_nodes_dev(c, d_pts, n, T, d_masks, nullptr, c->stream, stats, nullptr, /*stats_deferred=*/true);
     lap("node pass");
     if (nt) {

@@ -10,5 +10,6 @@ out = b.LIB / "variants" / f"{name}.so"
 out.parent.mkdir(parents=True, exist_ok=True)
 lines = b.compile_label_lib(out, defs).splitlines()
 for i, l in enumerate(lines):
-    if "k_labelILi1ELb1ELb0" in l and "Compiling" in l:
-        print(name, lines[i + 2].strip(), "|", lines[i + 3].strip())
+    if "Function properties for _ZN2nm7k_labelILi1ELb1ELi0EE" in l:
+        print(name, lines[i + 1].strip(), "|", lines[i + 2].strip())
+        break

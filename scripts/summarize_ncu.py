@@ -46,7 +46,7 @@ def launches(path):
         print(f"{c:8d} {v / 1e6:12.3f} {100 * v / tot:7.2f}%  {k[:110]}")
 
 
-def traffic(path):
+def traffic(path, sass_hash=None, points=None, note=""):
     """k_label DRAM bytes per launch from a launch list taken with
     --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,lts__t_bytes.sum"""
     import json
@@ -64,9 +64,14 @@ def traffic(path):
         per[r[ii]][r[mi]] = v * scale
     last = per[sorted(per, key=int)[-1]]
     rd, wr = last.get("dram__bytes_read.sum", 0.0), last.get("dram__bytes_write.sum", 0.0)
-    print(json.dumps({"kernel": "k_label<1,1>", "config": 5, "launches_seen": len(per), "dram_bytes_read": rd,
-                      "dram_bytes_write": wr, "traffic_bytes": rd + wr, "lts_bytes": last.get("lts__t_bytes.sum"),
-                      "gpu_time_ns": last.get("gpu__time_duration.sum")}, indent=1))
+    pts = int(points) if points else None
+    print(json.dumps({"kernel": "k_label<1,1,0>", "config": 5, "sass_sha16": sass_hash, "points": pts,
+                      "launches_seen": len(per), "dram_bytes_read": rd, "dram_bytes_write": wr,
+                      "traffic_bytes": rd + wr,
+                      "algorithmic_bytes": pts * (24 + 4 + 8) if pts else None,
+                      "lts_bytes": last.get("lts__t_bytes.sum"), "gpu_time_ns_under_ncu": last.get("gpu__time_duration.sum"),
+                      "source": "ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum of one full-mesh k_label launch",
+                      "note": note}, indent=1))
 
 
 FP32_PIPE = {"FFMA2": 2, "FADD2": 2, "FMUL2": 2, "FFMA": 1, "FADD": 1, "FMUL": 1}

@@ -7,6 +7,7 @@
 #include <cstdio>
 #include <cstdlib>
 
+#include "nestmesh/label_sidecar.hpp"
 #include "nestmesh/labeling.hpp"
 #include "nestmesh/lattice.hpp"
 #include "nestmesh/primitives.hpp"
@@ -143,6 +144,36 @@ int main(int argc, char** argv) {
       std::fprintf(stderr, "relabel from coarse labels != initial\n");
       return 18;
     }
+  }
+  // label sidecar next to a tetmesh v1 file written by the reference's own
+  // save_tetmesh (mesh.hpp:238-289): the lattice is labeled on the device
+  // straight into the sidecar; the mesh read back by load_tetmesh matches it
+  {
+    Labeler lab(seg);
+    const std::string mesh_path = std::string(out_path) + ".tetmesh";
+    save_tetmesh(mesh_path, mesh);
+    const nm_sidecar_info info = label_lattice_to_sidecar(lab, spec, params, label_sidecar_path(mesh_path));
+    TetrahedralMesh back = load_tetmesh(mesh_path);
+    const LabelSidecar sc = read_label_sidecar(label_sidecar_path(mesh_path));
+    apply_label_sidecar(back, sc);
+    if (back.labels != labels || sc.info.mesh_fingerprint != info.mesh_fingerprint ||
+        generate_lattice_mesh(sidecar_lattice(sc)).nodes.size() != mesh.node_count()) {
+      std::fprintf(stderr, "label sidecar round trip failed\n");
+      return 19;
+    }
+    // an explicit (refined) mesh: sidecar tied by its fingerprint
+    TetrahedralMesh r2 = refined;
+    r2.labels = rr.labels;
+    write_label_sidecar(mesh_path + ".refined.nmlabels", r2, seg, params);
+    TetrahedralMesh other = mesh;
+    try {
+      apply_label_sidecar(other, read_label_sidecar(mesh_path + ".refined.nmlabels"));
+      return 20;
+    } catch (const LabelingError&) {
+    }
+    TetrahedralMesh r3 = refined;
+    apply_label_sidecar(r3, read_label_sidecar(mesh_path + ".refined.nmlabels"));
+    if (r3.labels != rr.labels) return 21;
   }
   FILE* f = std::fopen(out_path, "wb");
   std::fwrite(labels.data(), sizeof(int), labels.size(), f);

@@ -718,3 +718,18 @@ def test_cell_culling_winding_number_two():
     _, s_ref = oracle.label_nodes(probe, S, want_s=True)
     np.testing.assert_allclose(s_cell, s_ref, rtol=0, atol=S_EXPECT)
     assert abs(s_cell[0, 0] - 2.0) < 1e-5 and abs(s_cell[1, 0] - 1.0) < 1e-5 and s_cell[2, 0] == 0.0
+
+
+def test_cell_axis_memory_budget():
+    """A certified-cell grid whose build would need more than the 8 GB host
+    budget (cell_axis 1024 on a cube: ~1.1e9 cells) fails in nm_set_surfaces
+    with a message, instead of exhausting host memory."""
+    from paper_2203_10000_b200._native import Context, NativeError
+    bx, bt = synth.box_surface([0, 0, 0], [10, 10, 10])
+    with Context(0, cull_outside=2, cell_axis=1024) as c:
+        with pytest.raises(NativeError, match="cell_axis"):
+            c.set_surfaces(bx, bt, np.array([0, 12], np.uint32), np.array([1], np.int32))
+    with Context(0, cull_outside=2, cell_axis=256) as c:   # ~0.3 GB: within budget
+        c.set_surfaces(bx, bt, np.array([0, 12], np.uint32), np.array([1], np.int32))
+        m, _ = c.label_nodes(np.array([[5.0, 5, 5], [20.0, 5, 5]]))
+        np.testing.assert_array_equal(m, [1, 0])
