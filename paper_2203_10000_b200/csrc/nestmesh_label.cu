@@ -636,6 +636,14 @@ int nm_set_surfaces(nm_ctx* c, const double* xyz, std::size_t nv, const std::uin
     for (std::size_t i = 0; i < 3 * nt; ++i)
       if (tri[i] >= nv) throw Error("triangle index out of range");
     NM_CUDA(cudaSetDevice(c->opt.device));
+    const bool verbose = std::getenv("NM_CELL_VERBOSE") != nullptr;
+    auto t_prev = std::chrono::steady_clock::now();
+    auto lap = [&](const char* what) {
+      if (!verbose) return;
+      const auto t = std::chrono::steady_clock::now();
+      std::fprintf(stderr, "[surfaces] %-8s %8.1f ms\n", what, std::chrono::duration<double, std::milli>(t - t_prev).count());
+      t_prev = t;
+    };
     // Domain box and centring offset of the fp32 frame.
     double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
     for (std::size_t i = 0; i < nv; ++i)
@@ -700,6 +708,7 @@ int nm_set_surfaces(nm_ctx* c, const double* xyz, std::size_t nv, const std::uin
         dst[2 * j + 1] = std::nextafter(float(hi + m), INFINITY);
       }
     });
+    lap("dop");
     std::unique_ptr<CellBuilder> cells;
     std::exception_ptr cells_err;
     struct Joiner {
@@ -801,6 +810,7 @@ int nm_set_surfaces(nm_ctx* c, const double* xyz, std::size_t nv, const std::uin
       const std::size_t per_tile = nm::kTile / nm::kSegTris;
       for (int k = 0; k < K; ++k) strip_slots += (segs[k].size() + per_tile - 1) / per_tile * nm::kTile;
     }
+    lap("strips");
     std::size_t soup_slots = 0;
     for (int k = 0; k < K; ++k) soup_slots += (comp_off[k + 1] - comp_off[k] + nm::kTile - 1) / nm::kTile * nm::kTile;
     // auto: strips when their padding costs less than the ~1.5x op saving
@@ -906,6 +916,7 @@ int nm_set_surfaces(nm_ctx* c, const double* xyz, std::size_t nv, const std::uin
       }
     }
     // (factor-2 margins: |v - c| <= emax + G/2 + Gc/2 < 2^24 G)
+    lap("grid");
     double Gc = std::ldexp(1.0, std::max(-120, std::ilogb(std::max(cmax, 1e-30)) + 1 - 23));
     const double G = std::ldexp(1.0, std::max(-120, std::ilogb(std::max(emax + Gc, 1e-30)) + 1 - 22));
     Gc = std::max(Gc, G);  // centres on the vertex grid too
@@ -1032,6 +1043,7 @@ int nm_set_surfaces(nm_ctx* c, const double* xyz, std::size_t nv, const std::uin
         }
       }
     });
+    lap("pack");
     if (inexact) throw Error("internal: a snapped subtile coordinate is not exact in fp32");
     c->strips = use_strips;
     auto up = [&](DBuf& b, const void* src, std::size_t bytes) { up_on(b, src, bytes, c->stream); };
@@ -1041,7 +1053,9 @@ int nm_set_surfaces(nm_ctx* c, const double* xyz, std::size_t nv, const std::uin
     up(c->comp_tiles, tiles.data(), tiles.size() * sizeof(std::uint32_t));
     up(c->comp_box, hbox.data(), hbox.size() * sizeof(float4));
     NM_CUDA(cudaStreamSynchronize(c->stream));
+    lap("upload");
     if (cells_thread.t.joinable()) cells_thread.t.join();
+    lap("cells-join");
     if (cells_err) std::rethrow_exception(cells_err);
     NM_CUDA(cudaStreamSynchronize(c->side));
     c->comp_tiles_h = tiles;
@@ -1054,6 +1068,7 @@ int nm_set_surfaces(nm_ctx* c, const double* xyz, std::size_t nv, const std::uin
     c->comp_off_h.assign(comp_off, comp_off + K + 1);
     c->has_surfaces = true;
     if (cells) cells->finish();  // representatives need the tiles: after the packing
+    lap("cells-fin");
   });
 }
 

@@ -1,0 +1,18 @@
+#!/bin/bash
+# round 2 production evidence for the current build: GPU suite, bench, ncu
+cd "$GRAFT_REPO_ROOT"
+O=gpurun_out/r02l
+mkdir -p $O
+timeout 2400 python -m pytest tests -x -q -m gpu --durations=10 > $O/pytest_gpu.log 2>&1
+echo "pytest exit $?" >> $O/pytest_gpu.log
+tail -3 $O/pytest_gpu.log
+NM_CELL_VERBOSE=1 python scripts/cells_quick.py 5 > $O/set_surfaces_cfg5.txt 2>&1
+NM_CELL_VERBOSE=1 python scripts/cells_quick.py 3 > $O/set_surfaces_cfg3.txt 2>&1
+timeout 1800 python bench.py --steps 5 --warmup 3 > $O/bench.json 2> $O/bench.err
+echo "bench exit $?"
+timeout 900 python bench.py --impl reference --steps 3 --warmup 3 > $O/bench_ref.json 2> $O/bench_ref.err
+for c in 2 3; do timeout 900 python bench.py --config $c --steps 5 --warmup 3 --no-cpu-baseline > $O/bench_cfg$c.json 2> $O/bench_cfg$c.err; done
+timeout 900 python bench.py --config 4 --steps 2 --warmup 3 > $O/bench_cfg4.json 2> $O/bench_cfg4.err
+rm -rf gpurun_out/ncu_r02
+bash scripts/gpu_ncu_r02.sh > $O/ncu_script.log 2>&1
+tail -3 $O/ncu_script.log
