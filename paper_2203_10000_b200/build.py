@@ -75,6 +75,17 @@ def build_label_lib(force=False) -> Path:
     return out
 
 
+def build_checked_lib(force=False) -> Path:
+    """lib/checked/libnestmesh_label.so: the same sources with NM_CHECKED
+    (device-side bounds checks, csrc/check.cuh) for tests/test_gpu_checked.py."""
+    out = LIB / "checked" / "libnestmesh_label.so"
+    out.parent.mkdir(parents=True, exist_ok=True)
+    deps = list(CSRC.glob("*.cu")) + list(CSRC.glob("*.cuh")) + [CSRC / "refine.cpp", ROOT / "include" / "nestmesh_label.h"]
+    if force or _stale(out, deps):
+        compile_label_lib(out, defs=("NM_CHECKED",), log=out.parent / "ptxas_checked.log")
+    return out
+
+
 def build_synth_lib(force=False) -> Path:
     LIB.mkdir(exist_ok=True)
     out = LIB / "libnestmesh_synth.so"
@@ -128,6 +139,7 @@ def build_cpp_dropin_bench(force=False):
 def build_all(force=False) -> None:
     build_synth_lib(force)
     build_label_lib(force)
+    build_checked_lib(force)
     build_oracle()
     build_cpp_dropin_test(force)
     build_cpp_dropin_bench(force)

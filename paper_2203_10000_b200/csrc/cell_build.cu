@@ -36,12 +36,16 @@ class CellBuild : public CellBuilder {
   }
 
   void prepare() override {
+    NvtxRange nvtx("nm certified cells: prepare");
     NM_CUDA(cudaSetDevice(c_->opt.device));
     geometry();
     certify();
     runs();
   }
-  void finish() override { resolve(); }
+  void finish() override {
+    NvtxRange nvtx("nm certified cells: resolve");
+    resolve();
+  }
 
  private:
   // run value of a level-1 or child run: 0 / 1 known; kRep + r: the
@@ -618,6 +622,8 @@ class CellBuild : public CellBuilder {
     prm.pts = static_cast<const double*>(c_->rep_pts.p);
     prm.n = R;
     prm.order = nullptr;
+    prm.n_pts = R;
+    prm.n_tiles = c_->comp_tiles_h.empty() ? 0u : c_->comp_tiles_h.back();
     prm.tri = static_cast<const float4*>(c_->tri.p);
     prm.sub = static_cast<const float4*>(c_->sub.p);
     prm.cont = static_cast<const std::uint32_t*>(c_->cont.p);

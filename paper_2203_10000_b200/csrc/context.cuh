@@ -28,6 +28,8 @@
 #include "refine.cuh"
 #include "distance.cuh"
 #include "cells.cuh"
+#include <nvtx3/nvToolsExt.h>
+
 #include "nestmesh_label.h"
 #include "refine.h"
 #include "staging.cuh"
@@ -37,6 +39,15 @@ namespace nmh {
 // certified-cell grid: cells along each compartment's longest side (nm_options.cell_axis = 0)
 constexpr int kDefaultCellAxis = 120;
 
+
+// NVTX range for profilers (nsys / ncu --nvtx): the phases of a call show up
+// on the timeline; without a tool attached a push/pop is a few ns.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 // thread-local message of the last failed C ABI call (nm_last_error)
 inline std::string& last_error() {
@@ -252,7 +263,7 @@ void label_nodes_dev(nm_ctx* c, const double* d_pts, std::size_t n, double T, st
                      bool stats_deferred = false, int shard = 0, int nshards = 0);
 void read_node_stats(nm_ctx* c, std::size_t n, cudaStream_t st, nm_stats* stats);
 void label_tets_dev(nm_ctx* c, const std::uint32_t* d_tets, std::size_t nt, const std::uint32_t* d_masks, int* d_labels,
-                    cudaStream_t st, nm_stats* stats);
+                    cudaStream_t st, nm_stats* stats, std::size_t n_nodes = ~std::size_t(0));
 void check_tets(const std::uint32_t* tets, std::size_t nt, std::size_t n_nodes);
 void check_tets_device(nm_ctx* c, const std::uint32_t* d_tets, const std::uint32_t* h_tets, std::size_t nt,
                        std::size_t n_nodes, cudaStream_t st);

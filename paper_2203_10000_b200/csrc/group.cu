@@ -249,7 +249,7 @@ int nm_group_label_mesh(nm_group* g, const double* nodes, std::size_t n, const s
       auto* d_l = c->labels.as<int>(std::max<std::size_t>(hi - lo, 1));
       c->h2d(d_t, tets + 4 * lo, 4 * (hi - lo) * sizeof(std::uint32_t), c->stream);
       if (hi > lo) {
-        label_tets_dev(c, d_t, hi - lo, d_all[r], d_l, c->stream, nullptr);
+        label_tets_dev(c, d_t, hi - lo, d_all[r], d_l, c->stream, nullptr, n);
         c->d2h(labels_out + lo, d_l, (hi - lo) * sizeof(int), c->stream);
       }
       if (r == 0 && masks_out) c->d2h(masks_out, d_all[0], n * 4, c->stream);

@@ -13,6 +13,7 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include "check.cuh"
 #include "vos.cuh"
 
 namespace nm {
@@ -129,6 +130,8 @@ struct LabelParams {
   const double* pts;         // fp64 xyz, original frame
   std::size_t n;
   const std::uint32_t* order;  // evaluation order (Morton); nullptr = identity
+  std::size_t n_pts;           // length of pts (points), for the checked build; SIZE_MAX: unknown (subset passes)
+  std::uint32_t n_tiles;       // tiles of the surface set (checked build)
   const float4* tri;         // soup: 3 float4 per triangle (a.xyz,N.x) (b.xyz,N.y) (c.xyz,N.z);
                              // strip: kSegF4 float4 per 8-triangle segment (vos.cuh)
   const std::uint32_t* cont;  // strip layout: per tile, bit sidx * kGroups + j = segment j of subtile
@@ -243,6 +246,7 @@ static __global__ void __launch_bounds__(kBlock, (NP == 1 ? NM_MIN_BLOCKS : NM_M
     // so they do not push the triangle tiles (re-read by every CTA) out of L2
     if (SPARSE) ii = __ldcs(prm.sp_list + ii);
     const std::uint32_t j = prm.order ? __ldcs(prm.order + ii) : static_cast<std::uint32_t>(ii);
+    NM_DCHECK(j < prm.n_pts, "k_label: point id out of range");
     pid[k] = j;
     const double* pj = prm.pts + 3 * static_cast<std::size_t>(j);
     const double dx = __ldcs(pj) - prm.cx, dy = __ldcs(pj + 1) - prm.cy, dz = __ldcs(pj + 2) - prm.cz;
@@ -308,6 +312,7 @@ static __global__ void __launch_bounds__(kBlock, (NP == 1 ? NM_MIN_BLOCKS : NM_M
     pf_t = -1;
   };
   auto pf_issue = [&](int b) {
+    NM_DCHECK(pf_t >= 0 && static_cast<std::uint32_t>(pf_t) < prm.n_tiles, "k_label: tile out of range");
     fence_proxy_async_smem();
     mbar_expect_tx(&s_bar[b], (kTileF4 + kSubF4Tile) * 16u);
     bulk_g2s(s_tri_buf[b], prm.tri + static_cast<std::size_t>(pf_t) * kTileF4, kTileF4 * 16u, &s_bar[b]);
@@ -375,6 +380,7 @@ static __global__ void __launch_bounds__(kBlock, (NP == 1 ? NM_MIN_BLOCKS : NM_M
       ++it;
       const float4* const s_tri = s_tri_buf[buf];
       const float4* const s_sub = s_sub_buf[buf];
+      NM_DCHECK(static_cast<std::uint32_t>(tile) < prm.n_tiles, "k_label: consumer tile out of range");
       const std::uint32_t tcont = STRIP ? __ldg(prm.cont + tile) : 0u;
 
       float2 acc[NP];
@@ -565,9 +571,11 @@ static __global__ void __launch_bounds__(kBlock, (NP == 1 ? NM_MIN_BLOCKS : NM_M
   for (int k = 0; k < P; ++k) {
     if (valid[k] && !(SPARSE && prm.sp_part)) {
       if (SPARSE) {
+        NM_DCHECK(prm.sp_list[base + k] < prm.n, "k_label: sparse position out of range");
         if (mask[k]) atomicOr(prm.masks + pid[k], mask[k]);
         if (fmask[k]) atomicOr(prm.flagmask + prm.sp_list[base + k], fmask[k]);
       } else if (gridDim.y == 1) {  // evaluation order: coalesced, streaming stores
+        NM_DCHECK(base + k < prm.n, "k_label: position out of range");
         __stcs(prm.masks + base + k, mask[k]);
         __stcs(prm.flagmask + base + k, fmask[k]);
       } else {
@@ -745,10 +753,14 @@ struct PredNonzero {
 
 // Dense node passes: masks[point id] = ms[evaluation position].
 static __global__ void k_unpermute(const std::uint32_t* __restrict__ order, std::size_t n,
-                                   const std::uint32_t* __restrict__ ms, std::uint32_t* __restrict__ masks) {
+                                   const std::uint32_t* __restrict__ ms, std::uint32_t* __restrict__ masks,
+                                   std::size_t n_pts) {
   for (std::size_t i = blockIdx.x * static_cast<std::size_t>(blockDim.x) + threadIdx.x; i < n;
-       i += static_cast<std::size_t>(gridDim.x) * blockDim.x)
-    masks[order ? __ldcs(order + i) : i] = __ldcs(ms + i);
+       i += static_cast<std::size_t>(gridDim.x) * blockDim.x) {
+    const std::size_t j = order ? __ldcs(order + i) : i;
+    NM_DCHECK(j < n_pts, "k_unpermute: point id out of range");
+    masks[j] = __ldcs(ms + i);
+  }
 }
 
 struct PredStraddle {
@@ -787,6 +799,7 @@ struct FixupParams {
   const std::uint32_t* pair_cnt;  // K: flagged pairs per compartment
   const std::uint32_t* pairs;     // per compartment (prefix of pair_cnt): positions into list
   double* part;                   // per pair and triangle chunk: fp64 partial sums
+  std::size_t n_pts, n_tri, n_part;  // checked build: lengths of pts, tri64 (triangles), part
   int K;
   double T, tie_eps;
   std::uint32_t* masks;
@@ -797,8 +810,9 @@ struct FixupParams {
 constexpr int kFixThreads = 128;
 constexpr int kFixLanes = 8;                          // threads per pair
 constexpr int kFixPairs = kFixThreads / kFixLanes;    // pairs per batch
-constexpr int kFixTile = 128;                         // triangles per shared-memory tile
+constexpr int kFixTile = 256;                         // triangles per shared-memory tile (two buffers)
 constexpr int kFixChunk = 2048;                       // triangles per work item (multiple of kFixTile)
+constexpr std::size_t kFixSmem = 2 * kFixTile * 9 * sizeof(double);  // k_fixup dynamic shared memory
 
 static __global__ void k_fix_count(const std::uint32_t* list, const std::uint32_t* count, const std::uint32_t* flagmask,
                                    std::uint32_t* pair_cnt) {
@@ -848,8 +862,20 @@ __device__ __forceinline__ std::uint32_t fix_nchunk(std::uint32_t ntri) {
   return max(1u, (ntri + kFixChunk - 1) / kFixChunk);
 }
 
+// 8-byte asynchronous global -> shared copies (LDGSTS): the next triangle
+// tile streams in while the current one is evaluated (fp64 triangles start at
+// any 8-byte offset, so no bulk copy)
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_addr(smem)), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
 static __global__ void __launch_bounds__(kFixThreads) k_fixup(const FixupParams prm) {
-  __shared__ double s_tri[kFixTile * 9];
+  extern __shared__ double s_fix[];  // two tiles of kFixTile fp64 triangles (dynamic: 36 KB)
   __shared__ std::uint32_t s_off[33], s_wo[33], s_po[33];
   const int K = prm.K;
   if (threadIdx.x == 0) {
@@ -880,27 +906,45 @@ static __global__ void __launch_bounds__(kFixThreads) k_fixup(const FixupParams 
     if (has) {
       const std::uint32_t w = prm.pairs[s_off[c] + j];
       const std::uint32_t i = prm.order ? prm.order[prm.list[w]] : prm.list[w];
+      NM_DCHECK(i < prm.n_pts, "k_fixup: point id out of range");
       px = prm.pts[3 * static_cast<std::size_t>(i)];
       py = prm.pts[3 * static_cast<std::size_t>(i) + 1];
       pz = prm.pts[3 * static_cast<std::size_t>(i) + 2];
     }
     const std::uint32_t c0 = lo + chunk * kFixChunk, c1 = min(hi, c0 + kFixChunk);
+    NM_DCHECK(c1 <= prm.n_tri && c0 <= c1, "k_fixup: triangle chunk out of range");
     double sum = 0.0;
-    for (std::uint32_t t0 = c0; t0 < c1; t0 += kFixTile) {
+    auto load = [&](int buf, std::uint32_t t0) {
       const std::uint32_t m = min(static_cast<std::uint32_t>(kFixTile), c1 - t0);
-      __syncthreads();  // the previous tile is consumed
       const double* src = prm.tri64 + 9 * static_cast<std::size_t>(t0);
-      for (std::uint32_t q = threadIdx.x; q < 9 * m; q += kFixThreads) s_tri[q] = __ldg(src + q);
-      __syncthreads();
+      double* dst = s_fix + buf * (kFixTile * 9);
+      for (std::uint32_t q = threadIdx.x; q < 9 * m; q += kFixThreads) cp_async8(dst + q, src + q);
+      cp_async_commit();
+    };
+    __syncthreads();  // both buffers are free (previous work item done)
+    load(0, c0);
+    int buf = 0;
+    for (std::uint32_t t0 = c0; t0 < c1; t0 += kFixTile, buf ^= 1) {
+      const std::uint32_t m = min(static_cast<std::uint32_t>(kFixTile), c1 - t0);
+      if (t0 + kFixTile < c1) {  // next tile into the other buffer (released by the barrier below)
+        load(buf ^ 1, t0 + kFixTile);
+        cp_async_wait<1>();
+      } else {
+        cp_async_wait<0>();
+      }
+      __syncthreads();  // tile t0 is in buffer buf for every thread
       if (has) {
+        const double* tile = s_fix + buf * (kFixTile * 9);
         for (std::uint32_t u = lane; u < m; u += kFixLanes) {
-          const double* e = s_tri + 9 * u;
-          sum += vos_half_angle64(e, e + 3, e + 6, px, py, pz);
+          const double* e = tile + 9 * u;
+          sum += vos_half_angle64_fma(e, e + 3, e + 6, px, py, pz);
         }
       }
+      __syncthreads();  // buffer buf is consumed: the next iteration may refill it
     }
 #pragma unroll
     for (int o = kFixLanes / 2; o > 0; o >>= 1) sum += __shfl_xor_sync(kFull, sum, o, kFixLanes);
+    NM_DCHECK(!has || s_po[c] + j * nch + chunk < prm.n_part, "k_fixup: partial slot out of range");
     if (has && lane == 0) prm.part[s_po[c] + j * nch + chunk] = sum;
   }
 }
@@ -929,9 +973,11 @@ static __global__ void k_fix_finalize(const FixupParams prm) {
     while (c + 1 < K && q >= s_off[c + 1]) ++c;
     const std::uint32_t j = q - s_off[c], nch = s_nch[c];
     double tot = 0.0;
+    NM_DCHECK(s_po[c] + (j + 1) * nch <= prm.n_part, "k_fix_finalize: partials out of range");
     for (std::uint32_t b = 0; b < nch; ++b) tot += prm.part[s_po[c] + j * nch + b];
     const std::uint32_t w = prm.pairs[q];
     const std::uint32_t i = prm.order ? prm.order[prm.list[w]] : prm.list[w];
+    NM_DCHECK(i < prm.n_pts, "k_fix_finalize: point id out of range");
     const double s = tot / (2.0 * CUDART_PI);
     if (s >= prm.T) atomicOr(prm.masks + i, 1u << c);
     else atomicAnd(prm.masks + i, ~(1u << c));
@@ -954,12 +1000,13 @@ static __global__ void k_fix_finalize(const FixupParams prm) {
 // four nodes, else 0.
 // ---------------------------------------------------------------------------
 static __global__ void k_label_tets(const uint4* __restrict__ tets, std::size_t nt, const std::uint32_t* __restrict__ masks,
-                             int* __restrict__ labels, const LabelIds ids) {
+                             int* __restrict__ labels, const LabelIds ids, std::size_t n_nodes) {
   __shared__ int s_ids[32];
   const int* id = stage_ids(ids, s_ids);
   for (std::size_t i = blockIdx.x * static_cast<std::size_t>(blockDim.x) + threadIdx.x; i < nt;
        i += static_cast<std::size_t>(gridDim.x) * blockDim.x) {
     const uint4 t = __ldcs(tets + i);  // read once; the gathered masks stay in L2
+    NM_DCHECK(t.x < n_nodes && t.y < n_nodes && t.z < n_nodes && t.w < n_nodes, "k_label_tets: node id out of range");
     const std::uint32_t m = __ldg(masks + t.x) & __ldg(masks + t.y) & __ldg(masks + t.z) & __ldg(masks + t.w);
     __stcs(labels + i, m ? id[__ffs(m) - 1] : 0);
   }

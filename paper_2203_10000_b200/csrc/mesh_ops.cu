@@ -300,7 +300,7 @@ int nm_label_lattice(nm_ctx* c, const double* origin, double h, int nx, int ny, 
     auto* d_labels = c->labels.as<int>(nt);
     if (nm_lattice_device(c, origin, h, nx, ny, nz, d_nodes, d_tets, st) != 0) throw Error(last_error());
     label_nodes_dev(c, d_nodes, nn, T, d_masks, nullptr, st, stats);
-    label_tets_dev(c, d_tets, nt, d_masks, d_labels, st, stats);
+    label_tets_dev(c, d_tets, nt, d_masks, d_labels, st, stats, nn);
     if (labels_out) c->d2h(labels_out, d_labels, nt * sizeof(int), st);
     if (masks_out) c->d2h(masks_out, d_masks, nn * sizeof(std::uint32_t), st);
     NM_CUDA(cudaStreamSynchronize(st));
@@ -719,7 +719,7 @@ int nm_refine_relabel(nm_ctx* c, const double* nodes, std::size_t n, const std::
       auto* d_labels = Al->as<int>(std::max<std::size_t>(cnt_t, 1));
       nm_stats ts{};
       label_tets_dev(c, reinterpret_cast<const std::uint32_t*>(At->p), cnt_t, static_cast<std::uint32_t*>(M->p), d_labels,
-                     st, stats ? &ts : nullptr);
+                     st, stats ? &ts : nullptr, cn);
       acc(ts);
       if (lvl == levels) break;
       // straddling tets (device compaction)

@@ -18,26 +18,45 @@ struct Strip {
   std::vector<std::uint32_t> t;
 };
 
-std::vector<Strip> stripify(const std::uint32_t* tri, std::uint32_t t0, std::uint32_t t1) {
+std::vector<Strip> stripify(const std::uint32_t* tri, std::uint32_t t0, std::uint32_t t1, std::size_t nv) {
   const std::uint32_t m = t1 - t0;
-  std::unordered_map<std::uint64_t, std::array<std::int64_t, 2>> edges;
-  edges.reserve(static_cast<std::size_t>(m) * 2);
-  auto key = [](std::uint32_t a, std::uint32_t b) {
-    return a < b ? (std::uint64_t(a) << 32 | b) : (std::uint64_t(b) << 32 | a);
-  };
+  // edge adjacency through vertex -> incident-triangle lists (counting sort
+  // over the vertex ids, linear time): adj[3 i + j] = the other triangle on
+  // edge (e_j, e_{j+1}) of triangle i, -1 on a border
+  std::vector<std::uint32_t> start(nv + 1, 0);
+  for (std::uint32_t i = 0; i < m; ++i)
+    for (int j = 0; j < 3; ++j) ++start[tri[3 * std::size_t(t0 + i) + j] + 1];
+  for (std::size_t v = 0; v < nv; ++v) start[v + 1] += start[v];
+  std::vector<std::uint32_t> inc(3 * std::size_t(m));
+  {
+    std::vector<std::uint32_t> cur(start.begin(), start.end() - 1);
+    for (std::uint32_t i = 0; i < m; ++i)
+      for (int j = 0; j < 3; ++j) inc[cur[tri[3 * std::size_t(t0 + i) + j]]++] = i;
+  }
+  std::vector<std::int64_t> adj(3 * std::size_t(m), -1);
   for (std::uint32_t i = 0; i < m; ++i) {
     const std::uint32_t* e = tri + 3 * std::size_t(t0 + i);
     for (int j = 0; j < 3; ++j) {
-      auto [it, ins] = edges.try_emplace(key(e[j], e[(j + 1) % 3]), std::array<std::int64_t, 2>{-1, -1});
-      auto& s = it->second;
-      if (s[0] < 0) s[0] = i;
-      else if (s[1] < 0) s[1] = i;
+      const std::uint32_t a = e[j], b = e[(j + 1) % 3];
+      for (std::uint32_t q = start[a]; q < start[a + 1]; ++q) {
+        const std::uint32_t o = inc[q];
+        if (o == i) continue;
+        const std::uint32_t* f = tri + 3 * std::size_t(t0 + o);
+        if (f[0] == b || f[1] == b || f[2] == b) {
+          adj[3 * std::size_t(i) + j] = o;
+          break;
+        }
+      }
     }
   }
   std::vector<std::uint8_t> used(m, 0);
   auto nbr = [&](std::uint32_t i, std::uint32_t a, std::uint32_t b) -> std::int64_t {
-    const auto& s = edges.at(key(a, b));
-    return s[0] == static_cast<std::int64_t>(i) ? s[1] : s[0];
+    const std::uint32_t* e = tri + 3 * std::size_t(t0 + i);
+    for (int j = 0; j < 3; ++j) {
+      const std::uint32_t x = e[j], y = e[(j + 1) % 3];
+      if ((x == a && y == b) || (x == b && y == a)) return adj[3 * std::size_t(i) + j];
+    }
+    return -1;
   };
   std::vector<int> deg(m, 0);
   for (std::uint32_t i = 0; i < m; ++i) {
@@ -315,6 +334,7 @@ void label_nodes_dev(nm_ctx* c, const double* d_pts, std::size_t n, double T, st
                      int nshards) {
   require_surfaces(c);
   if (!(T > 0.0 && T < 1.0)) throw Error("threshold must lie in (0, 1) (SPEC.md:216)");
+  NvtxRange nvtx_pass("nm node pass");
   std::uint64_t launches = 0;
   auto* counters = c->counters.as<unsigned long long>(8);
   NM_CUDA(cudaMemsetAsync(counters, 0, 8 * sizeof(unsigned long long), st));
@@ -355,6 +375,8 @@ void label_nodes_dev(nm_ctx* c, const double* d_pts, std::size_t n, double T, st
   prm.pts = d_pts;
   prm.n = n;
   prm.order = order;
+  prm.n_pts = d_subset ? ~std::size_t(0) : n;
+  prm.n_tiles = c->comp_tiles_h.empty() ? 0u : c->comp_tiles_h.back();
   prm.tri = static_cast<const float4*>(c->tri.p);
   prm.sub = static_cast<const float4*>(c->sub.p);
   prm.cont = static_cast<const std::uint32_t*>(c->cont.p);
@@ -426,12 +448,14 @@ void label_nodes_dev(nm_ctx* c, const double* d_pts, std::size_t n, double T, st
   }
   NM_CUDA(cudaGetLastError());
   ++launches;
-  nm::k_unpermute<<<grid_for(n, 256, c->sm_count * 16), 256, 0, st>>>(order, n, ms, d_masks);
+  nm::k_unpermute<<<grid_for(n, 256, c->sm_count * 16), 256, 0, st>>>(order, n, ms, d_masks,
+                                                                       d_subset ? ~std::size_t(0) : n);
   NM_CUDA(cudaGetLastError());
   ++launches;
   }
   if (stats) NM_CUDA(cudaEventRecord(c->ev[2], st));
   // compaction of flagged points, per-compartment pair lists, fp64 fix-up
+  NvtxRange nvtx_fix("nm fp64 fix-up");
   select(c, nm::PredNonzero{flagmask}, n, list, d_count, st, launches);
   const int K = c->K;
   auto* pair_cnt = c->pair_cnt.as<std::uint32_t>(2 * 32);
@@ -460,6 +484,9 @@ void label_nodes_dev(nm_ctx* c, const double* d_pts, std::size_t n, double T, st
     fp.pts = d_pts;
     fp.list = list;
     fp.order = order;
+    fp.n_pts = d_subset ? ~std::size_t(0) : n;
+    fp.n_tri = c->nt_real;
+    fp.n_part = npart;
     fp.count = d_count;
     fp.flagmask = flagmask;
     fp.tri64 = static_cast<const double*>(c->tri64.p);
@@ -473,7 +500,8 @@ void label_nodes_dev(nm_ctx* c, const double* d_pts, std::size_t n, double T, st
     fp.masks = d_masks;
     fp.s_out = d_s;
     fp.counters = counters;
-    nm::k_fixup<<<grid_for(nwork, 1, c->sm_count * 16), nm::kFixThreads, 0, st>>>(fp);
+    static_assert(nm::kFixSmem <= 48 * 1024, "k_fixup tiles must fit the default dynamic shared memory");
+    nm::k_fixup<<<grid_for(nwork, 1, c->sm_count * 16), nm::kFixThreads, nm::kFixSmem, st>>>(fp);
     nm::k_fix_finalize<<<grid_for(total, 256, c->sm_count * 4), 256, 0, st>>>(fp);
     NM_CUDA(cudaGetLastError());
     launches += 3;
@@ -511,12 +539,13 @@ void read_node_stats(nm_ctx* c, std::size_t n, cudaStream_t st, nm_stats* stats)
 }
 
 void label_tets_dev(nm_ctx* c, const std::uint32_t* d_tets, std::size_t nt, const std::uint32_t* d_masks, int* d_labels,
-                    cudaStream_t st, nm_stats* stats) {
+                    cudaStream_t st, nm_stats* stats, std::size_t n_nodes) {
   require_surfaces(c);
   if (nt == 0) return;
+  NvtxRange nvtx_tets("nm tet labels");
   if (stats) NM_CUDA(cudaEventRecord(c->ev[4], st));
   nm::k_label_tets<<<grid_for(nt, 256, c->sm_count * 32), 256, 0, st>>>(reinterpret_cast<const uint4*>(d_tets), nt,
-                                                                        d_masks, d_labels, c->ids);
+                                                                        d_masks, d_labels, c->ids, n_nodes);
   NM_CUDA(cudaGetLastError());
   if (stats) {
     NM_CUDA(cudaEventRecord(c->ev[5], st));
@@ -628,6 +657,7 @@ int nm_set_surfaces(nm_ctx* c, const double* xyz, std::size_t nv, const std::uin
   return guarded([&] {
     if (!c) throw Error("null context");
     if (K < 1 || K > 32) throw Error("compartment count must be in [1, 32]");
+    NvtxRange nvtx_surf("nm_set_surfaces");
     if (comp_off[0] != 0 || comp_off[K] != nt) throw Error("comp_tri_off must start at 0 and end at the triangle count");
     for (int k = 0; k < K; ++k) {
       if (comp_off[k + 1] < comp_off[k]) throw Error("comp_tri_off must be non-decreasing");
@@ -768,7 +798,7 @@ int nm_set_surfaces(nm_ctx* c, const double* xyz, std::size_t nv, const std::uin
     const bool try_strips = c->opt.layout != 1;
     if (try_strips) {
       parallel_for(K, [&](int k) {
-        const std::vector<Strip> strips = stripify(tri, comp_off[k], comp_off[k + 1]);
+        const std::vector<Strip> strips = stripify(tri, comp_off[k], comp_off[k + 1], nv);
         struct Chunk {
           std::uint32_t key;
           bool full;
@@ -1182,7 +1212,7 @@ int nm_label_tets(nm_ctx* c, const std::uint32_t* tets, std::size_t nt, const st
     c->h2d(d_tets, tets, 4 * nt * sizeof(std::uint32_t), c->stream);
     check_tets_device(c, d_tets, tets, nt, n_nodes, c->stream);
     c->h2d(d_masks, masks, n_nodes * sizeof(std::uint32_t), c->stream);
-    label_tets_dev(c, d_tets, nt, d_masks, d_labels, c->stream, stats);
+    label_tets_dev(c, d_tets, nt, d_masks, d_labels, c->stream, stats, n_nodes);
     c->d2h(labels_out, d_labels, nt * sizeof(int), c->stream);
     NM_CUDA(cudaStreamSynchronize(c->stream));
   });
@@ -1260,7 +1290,7 @@ int nm_label_mesh(nm_ctx* c, const double* nodes, std::size_t n, const std::uint
       }
     }
     if (stats && n) read_node_stats(c, n, c->stream, stats);
-    label_tets_dev(c, d_tets, nt, d_masks, d_labels, c->stream, stats);
+    label_tets_dev(c, d_tets, nt, d_masks, d_labels, c->stream, stats, n);
     lap("tet labels");
     c->d2h(labels_out, d_labels, nt * sizeof(int), c->stream);
     if (masks_out) c->d2h(masks_out, d_masks, n * sizeof(std::uint32_t), c->stream);

@@ -245,7 +245,7 @@ int nm_label_lattice_sidecar(nm_ctx* c, const double* origin, double h, int nx, 
     auto* d_labels = c->labels.as<int>(nt);
     if (nm_lattice_device(c, origin, h, nx, ny, nz, d_nodes, d_tets, st) != 0) throw Error(last_error());
     label_nodes_dev(c, d_nodes, nn, T, d_masks, nullptr, st, stats);
-    label_tets_dev(c, d_tets, nt, d_masks, d_labels, st, stats);
+    label_tets_dev(c, d_tets, nt, d_masks, d_labels, st, stats, nn);
     nm_sidecar_info info{};
     info.n_nodes = nn;
     info.n_tets = nt;

@@ -19,6 +19,7 @@
 #include <vector>
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 namespace nmh {
 
@@ -124,6 +125,7 @@ class Stager {
       return;
     }
     init();
+    nvtxRangePushA("nm staged h2d");
     const auto* s = static_cast<const char*>(src);
     auto* d = static_cast<char*>(dst);
     for (std::size_t off = 0, i = 0; off < bytes; off += kChunk, ++i) {
@@ -134,6 +136,7 @@ class Stager {
       check(cudaMemcpyAsync(d + off, pin_[b], len, cudaMemcpyHostToDevice, st));
       check(cudaEventRecord(ev_[b], st));
     }
+    nvtxRangePop();
   }
 
   // dst_host <- src_dev after the work already enqueued on st; returns when

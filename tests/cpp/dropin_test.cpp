@@ -121,6 +121,20 @@ int main(int argc, char** argv) {
       std::fprintf(stderr, "Labeler enclosure_ratios KAT failed\n");
       return 14;
     }
+    // centroid mode: the volume labeled inside the inner sphere (R = 6,
+    // h = 0.75 = R/8) is within SPEC.md:240's [0.9, 1.0] of the sphere volume
+    {
+      const std::vector<int> cl = lab.centroid_label(mesh, params);
+      double vol = 0.0;
+      for (std::size_t t = 0; t < mesh.tet_count(); ++t)
+        if (cl[t] == 3) vol += std::abs(tet_signed_volume(mesh.nodes[mesh.tetrahedra[t][0]], mesh.nodes[mesh.tetrahedra[t][1]],
+                                                          mesh.nodes[mesh.tetrahedra[t][2]], mesh.nodes[mesh.tetrahedra[t][3]]));
+      const double ratio = vol / (4.0 / 3.0 * 3.14159265358979323846 * 216.0);
+      if (ratio < 0.9 || ratio > 1.0) {
+        std::fprintf(stderr, "centroid-mode volume ratio %.4f outside [0.9, 1.0]\n", ratio);
+        return 22;
+      }
+    }
     if (lab.boundary_tets(mesh, masks) != boundary_tets(mesh, masks, 0xffffffffu, seg)) {
       std::fprintf(stderr, "Labeler boundary_tets differ\n");
       return 15;
