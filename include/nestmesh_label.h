@@ -283,6 +283,11 @@ int nm_surface_segments(nm_ctx* ctx, size_t* segments, size_t* continued);
  * evaluations of the last node pass that were not resolved by culling. */
 int nm_cell_info(nm_ctx* ctx, uint64_t* cells, uint64_t* certified, uint64_t* reps, double* ms_build,
                  uint64_t* last_pairs, uint64_t* last_evals);
+/* The certified-cell codes (per level-1 cell: 0 unknown, 1 / 2 winding number
+ * 0 / 1, 3 + b children in block b) and child states (0 unknown, 1 / 2), for
+ * tests and tools; sizes first with null buffers. */
+int nm_cell_dump(nm_ctx* ctx, uint32_t* codes, size_t codes_cap, uint8_t* children, size_t children_cap,
+                 size_t* n_codes, size_t* n_children);
 
 /* ---- binary label / node-mask sidecar next to tetmesh v1 -----------------
  * The reference writes meshes as %.17g text (write_tetmesh, mesh.hpp:238-289).

@@ -159,6 +159,8 @@ LABEL_API = {
     "nm_group_label_mesh": (ctypes.c_int, [ctypes.c_void_p, c_double_p, ctypes.c_size_t, c_u32_p, ctypes.c_size_t,
                                            ctypes.c_double, c_i32_p, c_u32_p, ctypes.POINTER(NmStats)]),
     "nm_group_uses_nccl": (ctypes.c_int, [ctypes.c_void_p]),
+    "nm_cell_dump": (ctypes.c_int, [ctypes.c_void_p, c_u32_p, ctypes.c_size_t, c_u8_p, ctypes.c_size_t, c_size_p,
+                                    c_size_p]),
     "nm_refine_device_d": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p,
                                           ctypes.c_size_t, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t,
                                           ctypes.c_void_p, ctypes.POINTER(ctypes.c_void_p)]),
@@ -288,6 +290,16 @@ class Context:
         check(self.lib.nm_surface_segments(self.handle, ctypes.byref(segs), ctypes.byref(cont)))
         return {"K": K.value, "triangles": t.value, "slots": tp.value, "layout": "strips" if lay.value == 2 else "triangles",
                 "segments": segs.value, "continued_segments": cont.value}
+
+    def cell_dump(self):
+        """(codes uint32 per level-1 cell, child states uint8) of the certified cells."""
+        nc, nch = ctypes.c_size_t(), ctypes.c_size_t()
+        check(self.lib.nm_cell_dump(self.handle, None, 0, None, 0, ctypes.byref(nc), ctypes.byref(nch)))
+        codes = np.empty(nc.value, np.uint32)
+        ch = np.empty(nch.value, np.uint8)
+        check(self.lib.nm_cell_dump(self.handle, ptr(codes, ctypes.c_uint32), codes.size, ptr(ch, ctypes.c_uint8),
+                                    ch.size, ctypes.byref(nc), ctypes.byref(nch)))
+        return codes, ch
 
     def cell_info(self):
         """Certified-cell culling (cull_outside=2): grid size, certified cells,

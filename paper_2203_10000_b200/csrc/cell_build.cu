@@ -28,7 +28,7 @@ class CellBuild : public CellBuilder {
             const std::vector<float4>& hbox, cudaStream_t st)
       : c_(c), xyz_(xyz), tri_(tri), comp_off_(comp_off), hbox_(hbox), K_(c->K), ctr_{c->cx, c->cy, c->cz},
         st_(st), t0_(std::chrono::steady_clock::now()), tl_(t0_),
-        verbose_(std::getenv("NM_CELL_VERBOSE") != nullptr) {}
+        verbose_(std::getenv("NM_CELL_VERBOSE") != nullptr), device_(std::getenv("NM_CELLS_HOST") == nullptr) {}
 
   ~CellBuild() override {
     for (cudaEvent_t e : child_ev_)
@@ -39,12 +39,18 @@ class CellBuild : public CellBuilder {
     NvtxRange nvtx("nm certified cells: prepare");
     NM_CUDA(cudaSetDevice(c_->opt.device));
     geometry();
-    certify();
-    runs();
+    if (device_) {
+      certify_device();
+      runs_device();
+    } else {
+      certify();
+      runs();
+    }
   }
   void finish() override {
     NvtxRange nvtx("nm certified cells: resolve");
-    resolve();
+    if (device_) resolve_device();
+    else resolve();
   }
 
  private:
@@ -71,6 +77,11 @@ class CellBuild : public CellBuilder {
   cudaStream_t st_;
   std::chrono::steady_clock::time_point t0_, tl_;
   bool verbose_;
+  // device run logic (cells.cuh k_runs_*; NM_CELLS_HOST=1: the host
+  // restatement below, the reference the device path is tested against)
+  bool device_;
+  std::uint32_t nrows_ = 0;
+  std::vector<unsigned> rep_cnt_d_, rep_first_d_;
 
   std::vector<nm::CellGrid> G_;
   std::vector<std::size_t> coff_;       // first cluster of each compartment
@@ -382,6 +393,168 @@ class CellBuild : public CellBuilder {
     });
   }
 
+  // ---- device path: certification + child blocks, runs, codes ----
+  void certify_device() {
+    const int K = K_;
+    auto* cert_d = c_->cell_cert.as<std::uint8_t>(std::max<std::size_t>(total_, 1));
+    up(c_->cell_grids, G_.data(), G_.size() * sizeof(nm::CellGrid));
+    up(c_->cell_dop, hbox_.data(), hbox_.size() * sizeof(float4));
+    for (int k = 0; k < K; ++k) {
+      if (!cells(k)) continue;
+      const std::size_t nbrick =
+          static_cast<std::size_t>((G_[k].nx + 3) / 4) * ((G_[k].ny + 3) / 4) * ((G_[k].nz + 1) / 2);
+      nm::k_cell_certify<<<static_cast<unsigned>((nbrick * 32 + 255) / 256), 256, 0, st_>>>(
+          G_[k], clus_k(k), nclus(k), ctri_k(k), tsph_k(k), static_cast<const double*>(c_->xyz64.p),
+          static_cast<const std::uint32_t*>(c_->tri_idx.p), c_->cx, c_->cy, c_->cz, cert_d);
+    }
+    // child block of every uncertified cell: exclusive scan of the
+    // uncertified flags in cell order (= the host path's numbering)
+    const std::size_t n = std::max<std::size_t>(total_, 1);
+    auto* unc = c_->cell_unc.as<std::uint32_t>(n);
+    auto* blk = c_->cell_blkidx.as<std::uint32_t>(n);
+    if (total_) {
+      nm::k_uncert<<<grid_for(total_, 256, c_->sm_count * 8), 256, 0, st_>>>(cert_d, total_, unc);
+      std::size_t tmp = 0;
+      NM_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, unc, blk, static_cast<int>(total_), st_));
+      void* t = c_->cub_tmp2.get(tmp);
+      NM_CUDA(cub::DeviceScan::ExclusiveSum(t, tmp, unc, blk, static_cast<int>(total_), st_));
+    }
+    NM_CUDA(cudaGetLastError());
+    // boff_[k] = blk at the compartment's first cell (read back, K + 1 words)
+    std::vector<std::uint32_t> hb(2, 0);
+    if (total_) {
+      NM_CUDA(cudaMemcpyAsync(&hb[0], blk + total_ - 1, 4, cudaMemcpyDeviceToHost, st_));
+      NM_CUDA(cudaMemcpyAsync(&hb[1], unc + total_ - 1, 4, cudaMemcpyDeviceToHost, st_));
+    }
+    std::vector<std::uint32_t> first(K, 0);
+    for (int k = 0; k < K; ++k)
+      if (cells(k)) NM_CUDA(cudaMemcpyAsync(&first[k], blk + G_[k].off, 4, cudaMemcpyDeviceToHost, st_));
+    NM_CUDA(cudaStreamSynchronize(st_));
+    const std::size_t nblk = total_ ? std::size_t(hb[0]) + hb[1] : 0;
+    boff_.assign(K + 1, nblk);
+    for (int k = K - 1; k >= 0; --k) boff_[k] = cells(k) ? first[k] : boff_[k + 1];
+    lap("l1");
+    nchild_ = nblk * nm::kChildren;
+    if (!nblk) return;
+    auto* blk_cells = c_->cell_blk.as<std::uint32_t>(nblk);
+    nm::k_block_cells<<<grid_for(total_, 256, c_->sm_count * 8), 256, 0, st_>>>(
+        cert_d, blk, total_, static_cast<const nm::CellGrid*>(c_->cell_grids.p), K, blk_cells);
+    auto* ch_d = c_->cell_child.as<std::uint8_t>(nchild_);
+    for (int k = 0; k < K; ++k) {
+      const std::size_t nb = boff_[k + 1] - boff_[k];
+      if (!nb) continue;
+      nm::k_child_certify<<<static_cast<unsigned>((nb * 64 + 255) / 256), 256, 0, st_>>>(
+          G_[k], blk_cells + boff_[k], nb, clus_k(k), nclus(k), ctri_k(k), tsph_k(k),
+          static_cast<const double*>(c_->xyz64.p), static_cast<const std::uint32_t*>(c_->tri_idx.p), c_->cx, c_->cy,
+          c_->cz, ch_d + boff_[k] * nm::kChildren);
+    }
+    NM_CUDA(cudaGetLastError());
+    lap("l2");
+  }
+
+  nm::RunParams run_params(bool fill) {
+    nm::RunParams p{};
+    p.grids = static_cast<const nm::CellGrid*>(c_->cell_grids.p);
+    p.K = K_;
+    p.row_first = static_cast<const std::uint32_t*>(c_->row_first.p);
+    p.cert = static_cast<const std::uint8_t*>(c_->cell_cert.p);
+    p.blk = static_cast<const std::uint32_t*>(c_->cell_blkidx.p);
+    p.child = static_cast<const std::uint8_t*>(c_->cell_child.p);
+    p.dop4 = static_cast<const float4*>(c_->cell_dop.p);
+    p.ctr0 = ctr_[0];
+    p.ctr1 = ctr_[1];
+    p.ctr2 = ctr_[2];
+    p.cellval = static_cast<std::int32_t*>(c_->cell_val.p);
+    p.childval = static_cast<std::int32_t*>(c_->child_val.p);
+    p.rep_cursor = static_cast<unsigned*>(c_->rep_cur.p);
+    p.rep_first = static_cast<const unsigned*>(c_->rep_cur.p) + 32;
+    p.rep_pts = static_cast<double*>(c_->rep_pts.p);
+    p.fill = fill ? 1 : 0;
+    return p;
+  }
+
+  void runs_device() {
+    const int K = K_;
+    std::vector<std::uint32_t> rf(K + 1, 0);
+    for (int k = 0; k < K; ++k) rf[k + 1] = rf[k] + (cells(k) ? static_cast<std::uint32_t>(G_[k].ny * G_[k].nz) : 0u);
+    nrows_ = rf[K];
+    up(c_->row_first, rf.data(), rf.size() * sizeof(std::uint32_t));
+    (void)c_->cell_val.as<std::int32_t>(std::max<std::size_t>(total_, 1));
+    (void)c_->child_val.as<std::int32_t>(std::max<std::size_t>(nchild_, 1));
+    auto* cur = c_->rep_cur.as<unsigned>(64);  // [0, 32) cursors, [32, 64) slot bases
+    (void)c_->rep_pts.as<double>(3);
+    NM_CUDA(cudaMemsetAsync(cur, 0, 64 * sizeof(unsigned), st_));
+    if (!nrows_) {
+      rep_cnt_d_.assign(K, 0);
+      rep_first_d_.assign(K + 1, 0);
+      nreps_ = 0;
+      return;
+    }
+    // count pass: representatives per compartment
+    nm::k_runs_l1<<<grid_for(nrows_, 128, c_->sm_count * 16), 128, 0, st_>>>(run_params(false), nrows_);
+    nm::k_runs_fine<<<grid_for(std::size_t(nrows_) * 16, 128, c_->sm_count * 16), 128, 0, st_>>>(run_params(false),
+                                                                                                   nrows_);
+    NM_CUDA(cudaGetLastError());
+    rep_cnt_d_.assign(K, 0);
+    NM_CUDA(cudaMemcpyAsync(rep_cnt_d_.data(), cur, K * sizeof(unsigned), cudaMemcpyDeviceToHost, st_));
+    NM_CUDA(cudaStreamSynchronize(st_));
+    rep_first_d_.assign(K + 1, 0);
+    for (int k = 0; k < K; ++k) rep_first_d_[k + 1] = rep_first_d_[k] + rep_cnt_d_[k];
+    nreps_ = rep_first_d_[K];
+    auto* pts = c_->rep_pts.as<double>(3 * std::max<std::size_t>(nreps_, 1));
+    (void)pts;
+    cur = static_cast<unsigned*>(c_->rep_cur.p);
+    NM_CUDA(cudaMemsetAsync(cur, 0, 32 * sizeof(unsigned), st_));
+    NM_CUDA(cudaMemcpyAsync(cur + 32, rep_first_d_.data(), K * sizeof(unsigned), cudaMemcpyHostToDevice, st_));
+    NM_CUDA(cudaMemsetAsync(c_->cell_val.p, 0xff, std::max<std::size_t>(total_, 1) * sizeof(std::int32_t), st_));
+    if (nchild_) NM_CUDA(cudaMemsetAsync(c_->child_val.p, 0xff, nchild_ * sizeof(std::int32_t), st_));
+    // fill pass: values, representative points (level-1 values first: the
+    // fine runs copy their neighbour parents')
+    nm::k_runs_l1<<<grid_for(nrows_, 128, c_->sm_count * 16), 128, 0, st_>>>(run_params(true), nrows_);
+    nm::k_runs_fine<<<grid_for(std::size_t(nrows_) * 16, 128, c_->sm_count * 16), 128, 0, st_>>>(run_params(true),
+                                                                                                   nrows_);
+    NM_CUDA(cudaGetLastError());
+    NM_CUDA(cudaStreamSynchronize(st_));  // rep_first_d_ (host) must outlive its copy
+    lap("runs");
+  }
+
+  void resolve_device() {
+    const int K = K_;
+    const std::size_t R = nreps_;
+    auto* rep_w = c_->rep_w.as<std::int32_t>(std::max<std::size_t>(R, 1));
+    if (R) {
+      evaluate_reps_device(R);
+      auto* s_dev = static_cast<const double*>(c_->rep_s.p);
+      nm::k_rep_values<<<grid_for(R, 256, c_->sm_count * 4), 256, 0, st_>>>(
+          s_dev, static_cast<std::uint32_t>(R), K, static_cast<const unsigned*>(c_->rep_cur.p) + 32, rep_w);
+    }
+    lap("reps");
+    auto* cnt = c_->cell_cnt.as<unsigned long long>(1);
+    NM_CUDA(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long), st_));
+    auto* state_d = c_->cell_state.as<std::uint32_t>(std::max<std::size_t>(total_, 1));
+    if (total_)
+      nm::k_cell_codes<<<grid_for(total_, 256, c_->sm_count * 8), 256, 0, st_>>>(
+          total_, static_cast<const std::uint8_t*>(c_->cell_cert.p), static_cast<const std::uint32_t*>(c_->cell_blkidx.p),
+          static_cast<const std::int32_t*>(c_->cell_val.p), rep_w, state_d, cnt);
+    (void)c_->cell_child.get(std::max<std::size_t>(nchild_, 1));
+    if (nchild_)
+      nm::k_child_codes<<<grid_for(nchild_, 256, c_->sm_count * 8), 256, 0, st_>>>(
+          nchild_, static_cast<std::uint8_t*>(c_->cell_child.p), static_cast<const std::int32_t*>(c_->child_val.p), rep_w,
+          cnt);
+    NM_CUDA(cudaGetLastError());
+    unsigned long long ncert = 0;
+    NM_CUDA(cudaMemcpyAsync(&ncert, cnt, sizeof ncert, cudaMemcpyDeviceToHost, st_));
+    NM_CUDA(cudaStreamSynchronize(st_));
+    lap("codes");
+    c_->cells_total = total_ + nchild_;
+    c_->cells_l1 = total_;
+    c_->cells_children = nchild_;
+    c_->cells_certified = ncert;
+    c_->cell_reps = nreps_;
+    c_->cells = true;
+    c_->ms_cells = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0_).count();
+  }
+
   // ---- runs: every maximal x-run of certified cells gets one winding number ----
   // per-slab results, merged per compartment in slab order
   struct SlabRuns {
@@ -595,10 +768,50 @@ class CellBuild : public CellBuilder {
     NM_CUDA(cudaStreamSynchronize(st_));
     lap("final");
     c_->cells_total = total_ + nchild_;
+    c_->cells_l1 = total_;
+    c_->cells_children = nchild_;
     c_->cells_certified = std::accumulate(ncert.begin(), ncert.end(), std::size_t(0));
     c_->cell_reps = nreps_;
     c_->cells = true;
     c_->ms_cells = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0_).count();
+  }
+
+  // device path: the representatives are already in c_->rep_pts (grouped by
+  // compartment, rep_first_d_); s of each against its own compartment lands
+  // in c_->rep_s (k_rep_values turns it into w)
+  void evaluate_reps_device(std::size_t R) {
+    const int K = K_;
+    auto* s_dev = c_->rep_s.as<double>(R * K);
+    auto* m_dev = c_->rep_m.as<std::uint32_t>(R);
+    auto* f_dev = c_->rep_f.as<std::uint32_t>(R);
+    auto* list = c_->sp_list.as<std::uint32_t>(R);
+    nm::k_iota<<<grid_for(R, 256, c_->sm_count * 4), 256, 0, st_>>>(list, R);
+    NM_CUDA(cudaMemsetAsync(m_dev, 0, R * sizeof(std::uint32_t), st_));
+    NM_CUDA(cudaMemsetAsync(f_dev, 0, R * sizeof(std::uint32_t), st_));
+    nm::LabelParams prm{};
+    prm.pts = static_cast<const double*>(c_->rep_pts.p);
+    prm.n = R;
+    prm.order = nullptr;
+    prm.n_pts = R;
+    prm.n_tiles = c_->comp_tiles_h.empty() ? 0u : c_->comp_tiles_h.back();
+    prm.tri = static_cast<const float4*>(c_->tri.p);
+    prm.sub = static_cast<const float4*>(c_->sub.p);
+    prm.cont = static_cast<const std::uint32_t*>(c_->cont.p);
+    prm.comp_tiles = static_cast<const std::uint32_t*>(c_->comp_tiles.p);
+    prm.K = K;
+    prm.cx = c_->cx;
+    prm.cy = c_->cy;
+    prm.cz = c_->cz;
+    prm.T = 0.5;
+    prm.band = c_->opt.band;
+    prm.tau = c_->opt.tau;
+    prm.delta = c_->opt.delta_mm;
+    prm.masks = m_dev;
+    prm.flagmask = f_dev;
+    prm.s_out = s_dev;
+    prm.sp_list = list;
+    std::vector<std::uint32_t> cnt(rep_cnt_d_.begin(), rep_cnt_d_.end());
+    launch_sparse(c_, prm, cnt, st_);
   }
 
   // s at every representative (sparse k_label against its own compartment);

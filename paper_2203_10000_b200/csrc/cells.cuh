@@ -227,4 +227,219 @@ struct PredBit {
   __device__ bool operator()(std::size_t i) const { return (v[i] >> bit) & 1u; }
 };
 
+// ---------------------------------------------------------------------------
+// Device run logic of the certified-cell build (round 2; the host restatement
+// in cell_build.cu, NM_CELLS_HOST=1, is the reference it is tested against,
+// bit for bit). Same rules, same fp operations in the same order (explicit
+// _rn intrinsics: no contraction), so the codes are identical:
+//   * k_runs_l1, one thread per grid row: every maximal x-run of certified
+//     cells gets 0 (an end at the grid edge or outside the 13-DOP) or a
+//     representative at its middle cell;
+//   * k_runs_fine, one thread per (row, sy, sz) child sub-row: in every
+//     segment of uncertified cells, each run of certified children gets the
+//     neighbour parent's value (run touching the segment's start / end), 0
+//     (grid edge, 13-DOP) or a representative;
+//   * the representatives are evaluated by the sparse k_label and
+//     k_rep_values turns s into w (0, 1 or unresolved);
+//   * k_cell_codes / k_child_codes write the final codes.
+// Values: -1 unresolved, 0 / 1 known w, 2 + r representative r (global
+// slot). Representative slots come from per-compartment atomic cursors: their
+// numbering varies, the codes do not (each representative is evaluated on its
+// own).
+// ---------------------------------------------------------------------------
+struct RunParams {
+  const CellGrid* grids;
+  int K;
+  const std::uint32_t* row_first;  // K + 1: first global row of each compartment (rows = ny nz)
+  const std::uint8_t* cert;        // per cell: 1 certified
+  const std::uint32_t* blk;        // per cell: global child block (uncertified cells)
+  const std::uint8_t* child;       // per child: 1 certified
+  const float4* dop4;              // 13-DOP slabs (kDopF4 float4 per compartment)
+  double ctr0, ctr1, ctr2;         // centring offset (representatives are stored in the original frame)
+  std::int32_t* cellval;           // per cell (fill pass)
+  std::int32_t* childval;          // per child (fill pass)
+  unsigned* rep_cursor;            // K per-compartment counters
+  const unsigned* rep_first;       // K slot bases (fill pass)
+  double* rep_pts;                 // 3 per representative (fill pass)
+  int fill;                        // 0: count representatives only
+};
+
+__device__ __forceinline__ bool outside_dop_rn(const float4* dop4, int k, double x, double y, double z) {
+  const float* dop = reinterpret_cast<const float*>(dop4 + static_cast<std::size_t>(k) * kDopF4);
+  const float xf = static_cast<float>(x), yf = static_cast<float>(y), zf = static_cast<float>(z);
+#pragma unroll
+  for (int d = 0; d < kDopDirs; ++d) {
+    const float pr =
+        __fadd_rn(__fadd_rn(__fmul_rn(dop_dir(d, 0), xf), __fmul_rn(dop_dir(d, 1), yf)), __fmul_rn(dop_dir(d, 2), zf));
+    if (pr < __ldg(dop + 2 * d) || pr > __ldg(dop + 2 * d + 1)) return true;
+  }
+  return false;
+}
+
+__device__ __forceinline__ std::int32_t new_rep(const RunParams& p, int k, double x, double y, double z) {
+  const unsigned slot = atomicAdd(p.rep_cursor + k, 1u);
+  if (!p.fill) return 0;
+  const unsigned r = p.rep_first[k] + slot;
+  p.rep_pts[3 * static_cast<std::size_t>(r)] = __dadd_rn(x, p.ctr0);
+  p.rep_pts[3 * static_cast<std::size_t>(r) + 1] = __dadd_rn(y, p.ctr1);
+  p.rep_pts[3 * static_cast<std::size_t>(r) + 2] = __dadd_rn(z, p.ctr2);
+  return 2 + static_cast<std::int32_t>(r);
+}
+
+__device__ __forceinline__ int row_compartment(const RunParams& p, std::uint32_t row) {
+  int k = 0;
+  while (k + 1 < p.K && row >= p.row_first[k + 1]) ++k;
+  return k;
+}
+
+static __global__ void k_runs_l1(const RunParams p, std::uint32_t nrows) {
+  for (std::uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < nrows; r += gridDim.x * blockDim.x) {
+    const int k = row_compartment(p, r);
+    const CellGrid g = p.grids[k];
+    const std::uint32_t lr = r - p.row_first[k];
+    const int iy = static_cast<int>(lr % static_cast<std::uint32_t>(g.ny)), iz = static_cast<int>(lr / g.ny);
+    const std::size_t row = g.off + (static_cast<std::size_t>(iz) * g.ny + iy) * g.nx;
+    const double y = __dadd_rn(g.oy, __dmul_rn(iy + 0.5, g.B)), z = __dadd_rn(g.oz, __dmul_rn(iz + 0.5, g.B));
+    for (int ix = 0; ix < g.nx;) {
+      const bool c1 = p.cert[row + ix] != 0;
+      int jx = ix;
+      while (jx + 1 < g.nx && (p.cert[row + jx + 1] != 0) == c1) ++jx;
+      if (c1) {
+        std::int32_t v;
+        if (ix == 0 || jx == g.nx - 1 || outside_dop_rn(p.dop4, k, __dadd_rn(g.ox, __dmul_rn(ix + 0.5, g.B)), y, z) ||
+            outside_dop_rn(p.dop4, k, __dadd_rn(g.ox, __dmul_rn(jx + 0.5, g.B)), y, z))
+          v = 0;
+        else
+          v = new_rep(p, k, __dadd_rn(g.ox, __dmul_rn((ix + jx) / 2 + 0.5, g.B)), y, z);
+        if (p.fill)
+          for (int q = ix; q <= jx; ++q) p.cellval[row + q] = v;
+      }
+      ix = jx + 1;
+    }
+  }
+}
+
+static __global__ void k_runs_fine(const RunParams p, std::uint32_t nrows) {
+  constexpr int S = kSubCells;
+  for (std::size_t t = blockIdx.x * static_cast<std::size_t>(blockDim.x) + threadIdx.x; t < std::size_t(nrows) * S * S;
+       t += static_cast<std::size_t>(gridDim.x) * blockDim.x) {
+    const std::uint32_t r = static_cast<std::uint32_t>(t / (S * S));
+    const int sy = static_cast<int>(t % S), sz = static_cast<int>((t / S) % S);
+    const int k = row_compartment(p, r);
+    const CellGrid g = p.grids[k];
+    const std::uint32_t lr = r - p.row_first[k];
+    const int iy = static_cast<int>(lr % static_cast<std::uint32_t>(g.ny)), iz = static_cast<int>(lr / g.ny);
+    const std::size_t row = g.off + (static_cast<std::size_t>(iz) * g.ny + iy) * g.nx;
+    const double b = g.B / S;
+    const double yy = __dadd_rn(__dadd_rn(g.oy, __dmul_rn(static_cast<double>(iy), g.B)), __dmul_rn(sy + 0.5, b));
+    const double zz = __dadd_rn(__dadd_rn(g.oz, __dmul_rn(static_cast<double>(iz), g.B)), __dmul_rn(sz + 0.5, b));
+    auto cidx = [&](int f) {  // child index of fine x cell f in this sub-row
+      return static_cast<std::size_t>(p.blk[row + f / S]) * kChildren + (sz * S + sy) * S + f % S;
+    };
+    for (int ix = 0; ix < g.nx;) {
+      const bool c1 = p.cert[row + ix] != 0;
+      int jx = ix;
+      while (jx + 1 < g.nx && (p.cert[row + jx + 1] != 0) == c1) ++jx;
+      if (!c1) {
+        const int f_lo = S * ix, f_hi = S * jx + S - 1;
+        for (int f = f_lo; f <= f_hi;) {
+          if (!p.child[cidx(f)]) {
+            ++f;
+            continue;
+          }
+          int e = f;
+          while (e + 1 <= f_hi && p.child[cidx(e + 1)]) ++e;
+          std::int32_t v;
+          if (f == f_lo) {
+            v = ix == 0 ? 0 : (p.fill ? p.cellval[row + ix - 1] : 0);
+          } else if (e == f_hi) {
+            v = jx == g.nx - 1 ? 0 : (p.fill ? p.cellval[row + jx + 1] : 0);
+          } else if (outside_dop_rn(p.dop4, k, __dadd_rn(g.ox, __dmul_rn(f + 0.5, b)), yy, zz) ||
+                     outside_dop_rn(p.dop4, k, __dadd_rn(g.ox, __dmul_rn(e + 0.5, b)), yy, zz)) {
+            v = 0;
+          } else {
+            v = new_rep(p, k, __dadd_rn(g.ox, __dmul_rn((f + e) / 2 + 0.5, b)), yy, zz);
+          }
+          if (p.fill)
+            for (int q = f; q <= e; ++q) p.childval[cidx(q)] = v;
+          f = e + 1;
+        }
+      }
+      ix = jx + 1;
+    }
+  }
+}
+
+// w of every representative: round(s) when within 1e-3 of 0 or 1, else -1
+static __global__ void k_rep_values(const double* s, std::uint32_t nreps, int K, const unsigned* rep_first,
+                                    std::int32_t* w_out) {
+  for (std::uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < nreps; r += gridDim.x * blockDim.x) {
+    int k = 0;
+    while (k + 1 < K && r >= rep_first[k + 1]) ++k;
+    const double v = s[static_cast<std::size_t>(r) * K + k];
+    const double w = round(v);
+    w_out[r] = (fabs(v - w) < 1e-3 && (w == 0.0 || w == 1.0)) ? static_cast<std::int32_t>(w) : -1;
+  }
+}
+
+__device__ __forceinline__ std::int32_t decode_w(std::int32_t v, const std::int32_t* rep_w) {
+  return v < 0 ? -1 : (v < 2 ? v : rep_w[v - 2]);
+}
+
+static __global__ void k_cell_codes(std::size_t ncells, const std::uint8_t* cert, const std::uint32_t* blk,
+                                    const std::int32_t* cellval, const std::int32_t* rep_w, std::uint32_t* code,
+                                    unsigned long long* ncert) {
+  unsigned long long m = 0;
+  for (std::size_t q = blockIdx.x * static_cast<std::size_t>(blockDim.x) + threadIdx.x; q < ncells;
+       q += static_cast<std::size_t>(gridDim.x) * blockDim.x) {
+    std::uint32_t c;
+    if (!cert[q]) {
+      c = 3u + blk[q];
+    } else {
+      const std::int32_t w = decode_w(cellval[q], rep_w);
+      c = w < 0 ? 0u : static_cast<std::uint32_t>(1 + w);
+    }
+    code[q] = c;
+    m += (c == 1u || c == 2u);
+  }
+  m = __reduce_add_sync(kFull, static_cast<unsigned>(m));
+  if ((threadIdx.x & 31) == 0 && m) atomicAdd(ncert, m);
+}
+
+// in place: child certification flag -> child code (0 unknown, 1 + w)
+static __global__ void k_child_codes(std::size_t nchild, std::uint8_t* child, const std::int32_t* childval,
+                                     const std::int32_t* rep_w, unsigned long long* ncert) {
+  unsigned long long m = 0;
+  for (std::size_t i = blockIdx.x * static_cast<std::size_t>(blockDim.x) + threadIdx.x; i < nchild;
+       i += static_cast<std::size_t>(gridDim.x) * blockDim.x) {
+    std::uint8_t c = 0;
+    if (child[i]) {
+      const std::int32_t w = decode_w(childval[i], rep_w);
+      c = w < 0 ? 0 : static_cast<std::uint8_t>(1 + w);
+    }
+    child[i] = c;
+    m += c != 0;
+  }
+  m = __reduce_add_sync(kFull, static_cast<unsigned>(m));
+  if ((threadIdx.x & 31) == 0 && m) atomicAdd(ncert, m);
+}
+
+// uncertified-cell flags (for the child-block scan) and the block list
+static __global__ void k_uncert(const std::uint8_t* cert, std::size_t n, std::uint32_t* unc) {
+  for (std::size_t q = blockIdx.x * static_cast<std::size_t>(blockDim.x) + threadIdx.x; q < n;
+       q += static_cast<std::size_t>(gridDim.x) * blockDim.x)
+    unc[q] = cert[q] ? 0u : 1u;
+}
+// block b = blk[q] of uncertified cell q -> its compartment-local cell index
+static __global__ void k_block_cells(const std::uint8_t* cert, const std::uint32_t* blk, std::size_t n,
+                                     const CellGrid* grids, int K, std::uint32_t* blk_cells) {
+  for (std::size_t q = blockIdx.x * static_cast<std::size_t>(blockDim.x) + threadIdx.x; q < n;
+       q += static_cast<std::size_t>(gridDim.x) * blockDim.x) {
+    if (cert[q]) continue;
+    int k = 0;
+    while (k + 1 < K && q >= grids[k + 1].off) ++k;
+    blk_cells[blk[q]] = static_cast<std::uint32_t>(q - grids[k].off);
+  }
+}
+
 }  // namespace nm

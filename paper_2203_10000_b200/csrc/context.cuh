@@ -192,8 +192,10 @@ struct nm_ctx {
   nmh::DBuf tri, sub, cont, comp_tiles, xyz64, tri_idx, tri64, comp_off, comp_box, cullmask;
   // certified cells (cull_outside = 2, cells.cuh)
   bool cells = false;
-  nmh::DBuf dist_clus, dist_slot, dist_ord, sp_part, sp_det, cell_state, cell_child, cell_cert, cell_blk, cell_grids, clus, clus_tri, clus_tsph, unk, sp_list, sp_chunk, sp_cnt, rep_pts, rep_s, rep_m, rep_f;
+  nmh::DBuf dist_clus, dist_slot, dist_ord, sp_part, sp_det, cell_state, cell_child, cell_cert, cell_blk, cell_grids, clus, clus_tri, clus_tsph, unk, sp_list, sp_chunk, sp_cnt, rep_pts, rep_s, rep_m, rep_f,
+      cell_unc, cell_blkidx, cell_val, child_val, row_first, rep_cur, rep_w, cell_dop, cell_cnt, cub_tmp2;
   std::uint64_t cells_total = 0, cells_certified = 0, cell_reps = 0, sparse_pairs = 0, sparse_evals = 0;
+  std::uint64_t cells_l1 = 0, cells_children = 0;  // level-1 cells and children (nm_cell_dump)
   double ms_cells = 0.0;  // host wall time of the certification (nm_set_surfaces)
   std::vector<std::uint32_t> comp_off_h;
 
@@ -206,7 +208,7 @@ struct nm_ctx {
 
   ~nm_ctx() {
     for (nmh::DBuf* b : {&dist_clus, &dist_slot, &dist_ord, &sp_part, &sp_det, &cell_state, &cell_child, &cell_cert, &cell_blk, &cell_grids, &clus, &clus_tri, &clus_tsph, &unk, &sp_list, &sp_chunk, &sp_cnt, &rep_pts, &rep_s,
-                    &rep_m, &rep_f})
+                    &rep_m, &rep_f, &cell_unc, &cell_blkidx, &cell_val, &child_val, &row_first, &rep_cur, &rep_w, &cell_dop, &cell_cnt, &cub_tmp2})
       b->release();
     for (nmh::DBuf* b : {&tri, &sub, &cont, &comp_tiles, &xyz64, &tri_idx, &tri64, &comp_off, &comp_box, &cullmask, &pts, &masks, &flagmask, &nbr, &known, &want, &fkeys, &frontier, &lex, &region, &bfaces, &btri,
                     &dist_tri, &dist_xyz, &dist_idx, &dist_d32, &dist_out, &r_red, &r_keys, &r_keys2, &r_S,

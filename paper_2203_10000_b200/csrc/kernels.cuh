@@ -810,7 +810,7 @@ struct FixupParams {
 constexpr int kFixThreads = 128;
 constexpr int kFixLanes = 8;                          // threads per pair
 constexpr int kFixPairs = kFixThreads / kFixLanes;    // pairs per batch
-constexpr int kFixTile = 256;                         // triangles per shared-memory tile (two buffers)
+constexpr int kFixTile = 128;                         // triangles per shared-memory tile (two buffers, 18 KB: ~8 CTAs per SM)
 constexpr int kFixChunk = 2048;                       // triangles per work item (multiple of kFixTile)
 constexpr std::size_t kFixSmem = 2 * kFixTile * 9 * sizeof(double);  // k_fixup dynamic shared memory
 
@@ -875,7 +875,7 @@ __device__ __forceinline__ void cp_async_wait() {
 }
 
 static __global__ void __launch_bounds__(kFixThreads) k_fixup(const FixupParams prm) {
-  extern __shared__ double s_fix[];  // two tiles of kFixTile fp64 triangles (dynamic: 36 KB)
+  extern __shared__ double s_fix[];  // two tiles of kFixTile fp64 triangles (dynamic shared memory)
   __shared__ std::uint32_t s_off[33], s_wo[33], s_po[33];
   const int K = prm.K;
   if (threadIdx.x == 0) {
@@ -937,7 +937,9 @@ static __global__ void __launch_bounds__(kFixThreads) k_fixup(const FixupParams 
         const double* tile = s_fix + buf * (kFixTile * 9);
         for (std::uint32_t u = lane; u < m; u += kFixLanes) {
           const double* e = tile + 9 * u;
-          sum += vos_half_angle64_fma(e, e + 3, e + 6, px, py, pz);
+          // the oracle's exact operand order (no FMA): on-surface points
+          // (num = +-0) must get the oracle's atan2 branch
+          sum += vos_half_angle64(e, e + 3, e + 6, px, py, pz);
         }
       }
       __syncthreads();  // buffer buf is consumed: the next iteration may refill it

@@ -715,29 +715,56 @@ int nm_set_surfaces(nm_ctx* c, const double* xyz, std::size_t nv, const std::uin
     // + 1e-5 |bound| (covers the fp32 rounding of the point and of the
     // projection in the kernel) and rounded outward.
     std::vector<float4> hbox(static_cast<std::size_t>(K) * nm::kDopF4);
-    parallel_for(K, [&](int k) {
-      float* dst = reinterpret_cast<float*>(&hbox[static_cast<std::size_t>(k) * nm::kDopF4]);
-      for (int q = 0; q < 4 * nm::kDopF4; ++q) dst[q] = 0.0f;
-      for (int j = 0; j < nm::kDopDirs; ++j) {
-        double lo = 1e300, hi = -1e300;
-        for (std::uint32_t t = comp_off[k]; t < comp_off[k + 1]; ++t)
+    // (one pass over the compartment's triangle corners, all 13 directions
+    // per corner; chunks of triangles on every host thread, merged per
+    // compartment: min/max are order-independent)
+    {
+      constexpr std::uint32_t kDopChunk = 16384;
+      std::vector<std::pair<int, std::uint32_t>> items;  // (compartment, first triangle)
+      for (int k = 0; k < K; ++k)
+        for (std::uint32_t t = comp_off[k]; t < comp_off[k + 1]; t += kDopChunk) items.emplace_back(k, t);
+      std::vector<std::array<double, 2 * nm::kDopDirs>> part(items.size());
+      parallel_for(static_cast<int>(items.size()), [&](int i) {
+        const int k = items[i].first;
+        const std::uint32_t t1 = std::min(comp_off[k + 1], items[i].second + kDopChunk);
+        auto& b = part[i];
+        for (int j = 0; j < nm::kDopDirs; ++j) {
+          b[2 * j] = 1e300;
+          b[2 * j + 1] = -1e300;
+        }
+        for (std::uint32_t t = items[i].second; t < t1; ++t)
           for (int v = 0; v < 3; ++v) {
             const double* X = xyz + 3 * std::size_t(tri[3 * t + v]);
-            double pr = 0.0;
-            for (int a = 0; a < 3; ++a) pr += double(nm::dop_dir(j, a)) * (X[a] - ctr[a]);
-            lo = std::min(lo, pr);
-            hi = std::max(hi, pr);
+            const double d[3] = {X[0] - ctr[0], X[1] - ctr[1], X[2] - ctr[2]};
+            for (int j = 0; j < nm::kDopDirs; ++j) {
+              double pr = 0.0;
+              for (int a = 0; a < 3; ++a) pr += double(nm::dop_dir(j, a)) * d[a];
+              b[2 * j] = std::min(b[2 * j], pr);
+              b[2 * j + 1] = std::max(b[2 * j + 1], pr);
+            }
           }
-        if (comp_off[k + 1] == comp_off[k]) {  // empty compartment: everything outside
-          dst[2 * j] = 1e30f;
-          dst[2 * j + 1] = -1e30f;
-          continue;
+      });
+      for (int k = 0; k < K; ++k) {
+        float* dst = reinterpret_cast<float*>(&hbox[static_cast<std::size_t>(k) * nm::kDopF4]);
+        for (int q = 0; q < 4 * nm::kDopF4; ++q) dst[q] = 0.0f;
+        for (int j = 0; j < nm::kDopDirs; ++j) {
+          double lo = 1e300, hi = -1e300;
+          for (std::size_t i = 0; i < items.size(); ++i)
+            if (items[i].first == k) {
+              lo = std::min(lo, part[i][2 * j]);
+              hi = std::max(hi, part[i][2 * j + 1]);
+            }
+          if (comp_off[k + 1] == comp_off[k]) {  // empty compartment: everything outside
+            dst[2 * j] = 1e30f;
+            dst[2 * j + 1] = -1e30f;
+            continue;
+          }
+          const double m = 1e-3 + 1e-5 * std::max(std::fabs(lo), std::fabs(hi));
+          dst[2 * j] = std::nextafter(float(lo - m), -INFINITY);
+          dst[2 * j + 1] = std::nextafter(float(hi + m), INFINITY);
         }
-        const double m = 1e-3 + 1e-5 * std::max(std::fabs(lo), std::fabs(hi));
-        dst[2 * j] = std::nextafter(float(lo - m), -INFINITY);
-        dst[2 * j + 1] = std::nextafter(float(hi + m), INFINITY);
       }
-    });
+    }
     lap("dop");
     std::unique_ptr<CellBuilder> cells;
     std::exception_ptr cells_err;
@@ -891,6 +918,10 @@ int nm_set_surfaces(nm_ctx* c, const double* xyz, std::size_t nv, const std::uin
     // for every point not within G of a surface (such points are caught by
     // the near-face / near-vertex detector and re-evaluated in fp64 on the
     // original vertices).
+    constexpr std::uint32_t kTileChunk = 8;
+    auto tile_comp = [&](std::uint32_t tl) {  // compartment owning tile tl
+      return static_cast<int>(std::upper_bound(tiles.begin(), tiles.end(), tl) - tiles.begin()) - 1;
+    };
     auto gather = [&](int k, std::uint32_t tl, int sidx, std::vector<const double*>& srcv) {
       const std::size_t nreal = use_strips ? segs[k].size() : order[k].size();
       // fallback vertex for all-pad units: the compartment's first vertex
@@ -926,23 +957,30 @@ int nm_set_surfaces(nm_ctx* c, const double* xyz, std::size_t nv, const std::uin
     // (|v - c| / G < 2^23 with c rounded to Gc)
     double cmax = 0.0, emax = 0.0;
     {
-      std::vector<double> cm(K, 0.0), em(K, 0.0);
-      parallel_for(K, [&](int k) {
+      // work items: chunks of kTileChunk tiles over all compartments (every
+      // host thread busy whatever the compartment sizes)
+      const int nitems = static_cast<int>((ntiles + kTileChunk - 1) / kTileChunk);
+      std::vector<double> cm(std::max(nitems, 1), 0.0), em(std::max(nitems, 1), 0.0);
+      parallel_for(nitems, [&](int i) {
         std::vector<const double*> srcv;
-        for (std::uint32_t tl = tiles[k]; tl < tiles[k + 1]; ++tl)
+        const std::uint32_t t0 = static_cast<std::uint32_t>(i) * kTileChunk,
+                            t1 = std::min<std::uint32_t>(static_cast<std::uint32_t>(ntiles), t0 + kTileChunk);
+        for (std::uint32_t tl = t0; tl < t1; ++tl) {
+          const int k = tile_comp(tl);
           for (int sidx = 0; sidx < nm::kSubPerTile; ++sidx) {
             gather(k, tl, sidx, srcv);
             double mid[3], half[3];
             mid_of(srcv, mid, half);
             for (int a = 0; a < 3; ++a) {
-              cm[k] = std::max(cm[k], std::fabs(mid[a]));
-              em[k] = std::max(em[k], half[a]);
+              cm[i] = std::max(cm[i], std::fabs(mid[a]));
+              em[i] = std::max(em[i], half[a]);
             }
           }
+        }
       });
-      for (int k = 0; k < K; ++k) {
-        cmax = std::max(cmax, cm[k]);
-        emax = std::max(emax, em[k]);
+      for (int i = 0; i < nitems; ++i) {
+        cmax = std::max(cmax, cm[i]);
+        emax = std::max(emax, em[i]);
       }
     }
     // (factor-2 margins: |v - c| <= emax + G/2 + Gc/2 < 2^24 G)
@@ -953,10 +991,13 @@ int nm_set_surfaces(nm_ctx* c, const double* xyz, std::size_t nv, const std::uin
     c->snap_grid = G;
     std::atomic<bool> inexact{false};
     auto snap = [&](double x, double g) { return std::nearbyint(x / g) * g; };
-    parallel_for(K, [&](int k) {  // compartments own disjoint tile ranges
-      const std::size_t nreal = use_strips ? segs[k].size() : order[k].size();
+    parallel_for(static_cast<int>((ntiles + kTileChunk - 1) / kTileChunk), [&](int item) {  // disjoint tile ranges
       std::vector<const double*> srcv;
-      for (std::uint32_t tl = tiles[k]; tl < tiles[k + 1]; ++tl) {
+      const std::uint32_t t0 = static_cast<std::uint32_t>(item) * kTileChunk,
+                          t1 = std::min<std::uint32_t>(static_cast<std::uint32_t>(ntiles), t0 + kTileChunk);
+      for (std::uint32_t tl = t0; tl < t1; ++tl) {
+        const int k = tile_comp(tl);
+        const std::size_t nreal = use_strips ? segs[k].size() : order[k].size();
         for (int sidx = 0; sidx < nm::kSubPerTile; ++sidx) {
           const std::size_t u0 = gather(k, tl, sidx, srcv);
           const int nunits = use_strips ? nm::kSub / nm::kSegTris : nm::kSub;
@@ -1076,7 +1117,10 @@ int nm_set_surfaces(nm_ctx* c, const double* xyz, std::size_t nv, const std::uin
     lap("pack");
     if (inexact) throw Error("internal: a snapped subtile coordinate is not exact in fp32");
     c->strips = use_strips;
-    auto up = [&](DBuf& b, const void* src, std::size_t bytes) { up_on(b, src, bytes, c->stream); };
+    auto up = [&](DBuf& b, const void* src, std::size_t bytes) {  // pinned chunk staging (staging.cuh)
+      void* d = b.get(std::max<std::size_t>(bytes, 1));
+      c->h2d(d, src, bytes, c->stream);
+    };
     up(c->tri, htri.data(), htri.size() * sizeof(float4));
     up(c->sub, hsub.data(), hsub.size() * sizeof(float4));
     up(c->cont, hcont.data(), hcont.size() * sizeof(std::uint32_t));
@@ -1112,6 +1156,21 @@ int nm_cell_info(nm_ctx* c, uint64_t* cells, uint64_t* certified, uint64_t* reps
     if (ms_build) *ms_build = c->ms_cells;
     if (last_pairs) *last_pairs = c->sparse_pairs;
     if (last_evals) *last_evals = c->sparse_evals;
+  });
+}
+
+int nm_cell_dump(nm_ctx* c, uint32_t* codes, size_t codes_cap, uint8_t* children, size_t children_cap, size_t* n_codes,
+                 size_t* n_children) {
+  return guarded([&] {
+    require_surfaces(c);
+    if (!c->cells) throw Error("no certified cells (cull_outside = 2)");
+    NM_CUDA(cudaSetDevice(c->opt.device));
+    if (n_codes) *n_codes = c->cells_l1;
+    if (n_children) *n_children = c->cells_children;
+    if (codes && codes_cap >= c->cells_l1 && c->cells_l1)
+      NM_CUDA(cudaMemcpy(codes, c->cell_state.p, c->cells_l1 * sizeof(std::uint32_t), cudaMemcpyDeviceToHost));
+    if (children && children_cap >= c->cells_children && c->cells_children)
+      NM_CUDA(cudaMemcpy(children, c->cell_child.p, c->cells_children, cudaMemcpyDeviceToHost));
   });
 }
 

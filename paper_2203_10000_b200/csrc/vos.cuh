@@ -422,31 +422,5 @@ __device__ __forceinline__ double vos_half_angle64(const double* a, const double
   return atan2(num, den);
 }
 
-// The fix-up's evaluator: the same VOS formula in fp64 with fused
-// multiply-adds (dot products, cross product, denominator): ~40 % fewer
-// FP64-pipe operations than the oracle's unfused operand order and at least
-// as accurate; it differs from the oracle (vos_half_angle64's order) by a few
-// ulp per term (tests: s of fixed-up pairs within 1e-12 of the oracle).
-__device__ __forceinline__ double vos_half_angle64_fma(const double* a, const double* b, const double* c, double px,
-                                                       double py, double pz) {
-  const double x1 = __dsub_rn(a[0], px), y1 = __dsub_rn(a[1], py), z1 = __dsub_rn(a[2], pz);
-  const double x2 = __dsub_rn(b[0], px), y2 = __dsub_rn(b[1], py), z2 = __dsub_rn(b[2], pz);
-  const double x3 = __dsub_rn(c[0], px), y3 = __dsub_rn(c[1], py), z3 = __dsub_rn(c[2], pz);
-  auto dot = [](double ax, double ay, double az, double bx, double by, double bz) {
-    return __fma_rn(az, bz, __fma_rn(ay, by, __dmul_rn(ax, bx)));
-  };
-  const double l1 = __dsqrt_rn(dot(x1, y1, z1, x1, y1, z1));
-  const double l2 = __dsqrt_rn(dot(x2, y2, z2, x2, y2, z2));
-  const double l3 = __dsqrt_rn(dot(x3, y3, z3, x3, y3, z3));
-  const double cx = __fma_rn(y2, z3, -__dmul_rn(z2, y3));
-  const double cy = __fma_rn(z2, x3, -__dmul_rn(x2, z3));
-  const double cz = __fma_rn(x2, y3, -__dmul_rn(y2, x3));
-  const double num = dot(x1, y1, z1, cx, cy, cz);
-  double den = __dmul_rn(__dmul_rn(l1, l2), l3);
-  den = __fma_rn(dot(x1, y1, z1, x2, y2, z2), l3, den);
-  den = __fma_rn(dot(x1, y1, z1, x3, y3, z3), l2, den);
-  den = __fma_rn(dot(x2, y2, z2, x3, y3, z3), l1, den);
-  return atan2(num, den);
-}
 
 }  // namespace nm

@@ -733,3 +733,30 @@ def test_cell_axis_memory_budget():
         c.set_surfaces(bx, bt, np.array([0, 12], np.uint32), np.array([1], np.int32))
         m, _ = c.label_nodes(np.array([[5.0, 5, 5], [20.0, 5, 5]]))
         np.testing.assert_array_equal(m, [1, 0])
+
+
+@pytest.mark.parametrize("cfg_id", [2, 3, 5])
+def test_device_cell_build_equals_host_build(cfg_id, monkeypatch):
+    """The certified-cell build's run logic on the device (cells.cuh
+    k_runs_* / k_rep_values / k_*_codes, the default) produces the SAME
+    level-1 codes and child states, bit for bit, as the host restatement
+    (NM_CELLS_HOST=1), and the same certified / representative counts."""
+    from paper_2203_10000_b200._native import Context
+    cfg = synth.config(cfg_id)
+    S = cfg.surfaces
+    out = {}
+    for mode in ("host", "device"):
+        if mode == "host":
+            monkeypatch.setenv("NM_CELLS_HOST", "1")
+        else:
+            monkeypatch.delenv("NM_CELLS_HOST", raising=False)
+        with Context(0, cull_outside=2) as c:
+            c.set_surfaces(S.xyz, S.tri, S.comp_off, S.label_ids)
+            codes, ch = c.cell_dump()
+            info = c.cell_info()
+        out[mode] = (codes, ch, info)
+    np.testing.assert_array_equal(out["device"][0], out["host"][0])
+    np.testing.assert_array_equal(out["device"][1], out["host"][1])
+    for k in ("cells", "certified", "reps"):
+        assert out["device"][2][k] == out["host"][2][k], k
+    assert (out["device"][0] == 2).any() and (out["device"][1] == 1).any()
