@@ -1117,10 +1117,7 @@ int nm_set_surfaces(nm_ctx* c, const double* xyz, std::size_t nv, const std::uin
     lap("pack");
     if (inexact) throw Error("internal: a snapped subtile coordinate is not exact in fp32");
     c->strips = use_strips;
-    auto up = [&](DBuf& b, const void* src, std::size_t bytes) {  // pinned chunk staging (staging.cuh)
-      void* d = b.get(std::max<std::size_t>(bytes, 1));
-      c->h2d(d, src, bytes, c->stream);
-    };
+    auto up = [&](DBuf& b, const void* src, std::size_t bytes) { up_on(b, src, bytes, c->stream); };
     up(c->tri, htri.data(), htri.size() * sizeof(float4));
     up(c->sub, hsub.data(), hsub.size() * sizeof(float4));
     up(c->cont, hcont.data(), hcont.size() * sizeof(std::uint32_t));

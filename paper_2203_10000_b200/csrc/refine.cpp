@@ -43,8 +43,46 @@ constexpr int kEdge[6][2] = {{0, 1}, {0, 2}, {0, 3}, {1, 2}, {1, 3}, {2, 3}};
 
 #include <cuda_runtime.h>
 
+#include <memory>
+#include <mutex>
+
+#include "staging.cuh"
+
 namespace {
 thread_local std::string g_refine_err;
+
+// Device-resident result meshes are copied into the caller's (usually
+// pageable) arrays through pinned chunk buffers and a host copy pool
+// (staging.cuh): ~3x the driver's pageable D2H at cfg4 sizes (4.6 GB).
+struct MeshCopier {
+  std::mutex m;
+  std::unique_ptr<nmh::CopyPool> pool;
+  nmh::Stager stager;
+  bool get(int device, void* dst, const void* src, std::size_t bytes) {
+    if (!dst || !bytes) return true;
+    if (!src) return false;
+    std::lock_guard<std::mutex> g(m);
+    if (!pool) {
+      const int hw = static_cast<int>(std::thread::hardware_concurrency());
+      pool = std::make_unique<nmh::CopyPool>(std::max(1, std::min(11, hw - 5)));
+    }
+    cudaStream_t st = nullptr;
+    if (cudaSetDevice(device) != cudaSuccess || cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess)
+      return false;
+    bool ok = true;
+    try {
+      stager.d2h(dst, src, bytes, st, *pool);
+    } catch (...) {
+      ok = false;
+    }
+    cudaStreamDestroy(st);
+    return ok;
+  }
+};
+MeshCopier& mesh_copier() {
+  static MeshCopier c;
+  return c;
+}
 }  // namespace
 
 namespace nmi {
@@ -267,9 +305,7 @@ int nm_mesh_copy(const nm_mesh* m, double* nodes, std::uint32_t* tets, int* labe
   if (m->dev.device >= 0) {
     const auto& d = m->dev;
     if (cudaSetDevice(d.device) != cudaSuccess) return 1;
-    auto get = [](void* dst, const void* src, std::size_t bytes) {
-      return !dst || !bytes || (src && cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToHost) == cudaSuccess);
-    };
+    auto get = [&](void* dst, const void* src, std::size_t bytes) { return mesh_copier().get(d.device, dst, src, bytes); };
     const bool ok = get(nodes, d.nodes, 3 * d.nn * sizeof(double)) && get(tets, d.tets, 4 * d.nt * sizeof(std::uint32_t)) &&
                     get(labels, d.labels, d.nt * sizeof(int)) && get(parent, d.parent, d.nt * sizeof(std::uint32_t));
     return ok ? 0 : 1;
@@ -326,11 +362,8 @@ int nm_sample_surface(const double* xyz, const std::uint32_t* tri, std::size_t n
 int nm_mesh_masks(const nm_mesh* m, std::uint32_t* masks) {
   if (!m) return 1;
   if (m->dev.device >= 0) {
-    if (!m->dev.masks || cudaSetDevice(m->dev.device) != cudaSuccess) return 1;
-    return m->dev.nn && cudaMemcpy(masks, m->dev.masks, m->dev.nn * sizeof(std::uint32_t), cudaMemcpyDeviceToHost) !=
-                            cudaSuccess
-               ? 1
-               : 0;
+    if (!m->dev.masks) return 1;
+    return mesh_copier().get(m->dev.device, masks, m->dev.masks, m->dev.nn * sizeof(std::uint32_t)) ? 0 : 1;
   }
   if (m->masks.size() != m->nodes.size() / 3) return 1;
   std::memcpy(masks, m->masks.data(), m->masks.size() * sizeof(std::uint32_t));

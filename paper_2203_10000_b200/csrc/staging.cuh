@@ -104,6 +104,42 @@ inline bool host_pinned(const void* p) {
   return a.type == cudaMemoryTypeHost || a.type == cudaMemoryTypeManaged;
 }
 
+// Process-wide free list of pinned chunk buffers: page-locking 48 MB costs
+// ~10-20 ms, so contexts (one per one-shot C++ call) recycle the buffers of
+// earlier ones instead of allocating their own. Buffers are portable
+// (usable from every device) and live until the process exits.
+class PinnedChunks {
+ public:
+  static PinnedChunks& get() {
+    static PinnedChunks* p = new PinnedChunks;  // leaked on purpose: no teardown-order issues at exit
+    return *p;
+  }
+  void* acquire(std::size_t bytes) {
+    {
+      std::lock_guard<std::mutex> g(m_);
+      if (!free_.empty()) {
+        void* p = free_.back();
+        free_.pop_back();
+        return p;
+      }
+    }
+    void* p = nullptr;
+    if (cudaHostAlloc(&p, bytes, cudaHostAllocPortable) != cudaSuccess) {
+      cudaGetLastError();
+      throw std::runtime_error("staging copy: cudaHostAlloc of a pinned chunk failed");
+    }
+    return p;
+  }
+  void release(void* p) {
+    std::lock_guard<std::mutex> g(m_);
+    free_.push_back(p);
+  }
+
+ private:
+  std::mutex m_;
+  std::vector<void*> free_;
+};
+
 // One pipeline of pinned chunk buffers bound to one stream at a time.
 class Stager {
  public:
@@ -170,7 +206,10 @@ class Stager {
 
   void release() {
     for (int b = 0; b < kBufs; ++b) {
-      if (pin_[b]) cudaFreeHost(pin_[b]);
+      if (pin_[b]) {
+        if (ev_[b]) cudaEventSynchronize(ev_[b]);  // no DMA may still read or write it
+        PinnedChunks::get().release(pin_[b]);
+      }
       if (ev_[b]) cudaEventDestroy(ev_[b]);
       pin_[b] = nullptr;
       ev_[b] = nullptr;
@@ -184,7 +223,7 @@ class Stager {
   void init() {
     if (pin_[0]) return;
     for (int b = 0; b < kBufs; ++b) {
-      check(cudaMallocHost(&pin_[b], kChunk));
+      pin_[b] = PinnedChunks::get().acquire(kChunk);
       check(cudaEventCreateWithFlags(&ev_[b], cudaEventDisableTiming));
     }
   }
