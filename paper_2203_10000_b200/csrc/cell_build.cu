@@ -25,8 +25,9 @@ class CellBuild : public CellBuilder {
   // set; prepare() may run on a host thread beside the tile packing (it uses
   // its own stream); finish() needs the tiles (representatives run k_label).
   CellBuild(nm_ctx* c, const double* xyz, const std::uint32_t* tri, const std::uint32_t* comp_off,
-            const std::vector<float4>& hbox, cudaStream_t st)
-      : c_(c), xyz_(xyz), tri_(tri), comp_off_(comp_off), hbox_(hbox), K_(c->K), ctr_{c->cx, c->cy, c->cz},
+            const std::vector<float4>& hbox, cudaStream_t st, std::shared_future<void> dop_ready)
+      : c_(c), xyz_(xyz), tri_(tri), comp_off_(comp_off), hbox_(hbox), dop_ready_(std::move(dop_ready)), K_(c->K),
+        ctr_{c->cx, c->cy, c->cz},
         st_(st), t0_(std::chrono::steady_clock::now()), tl_(t0_),
         verbose_(std::getenv("NM_CELL_VERBOSE") != nullptr), device_(std::getenv("NM_CELLS_HOST") == nullptr) {}
 
@@ -39,6 +40,7 @@ class CellBuild : public CellBuilder {
     NvtxRange nvtx("nm certified cells: prepare");
     NM_CUDA(cudaSetDevice(c_->opt.device));
     geometry();
+    dop_ready_.get();  // the 13-DOP (computed by the caller meanwhile) is needed from here on
     if (device_) {
       certify_device();
       runs_device();
@@ -72,6 +74,7 @@ class CellBuild : public CellBuilder {
   const std::uint32_t* tri_;
   const std::uint32_t* comp_off_;
   const std::vector<float4>& hbox_;
+  std::shared_future<void> dop_ready_;  // hbox_ is complete
   const int K_;
   const double ctr_[3];
   cudaStream_t st_;
@@ -869,8 +872,8 @@ class CellBuild : public CellBuilder {
 
 std::unique_ptr<CellBuilder> make_cell_builder(nm_ctx* c, const double* xyz, const std::uint32_t* tri,
                                                const std::uint32_t* comp_off, const std::vector<float4>& hbox,
-                                               cudaStream_t st) {
-  return std::make_unique<CellBuild>(c, xyz, tri, comp_off, hbox, st);
+                                               cudaStream_t st, std::shared_future<void> dop_ready) {
+  return std::make_unique<CellBuild>(c, xyz, tri, comp_off, hbox, st, std::move(dop_ready));
 }
 
 }  // namespace nmh

@@ -11,6 +11,7 @@
 #include <cstring>
 #include <cstdlib>
 #include <exception>
+#include <future>
 #include <memory>
 #include <numeric>
 #include <queue>
@@ -283,9 +284,10 @@ class CellBuilder {
   virtual void prepare() = 0;
   virtual void finish() = 0;
 };
+// hbox is filled by the caller concurrently; dop_ready is set when it is
 std::unique_ptr<CellBuilder> make_cell_builder(nm_ctx* c, const double* xyz, const std::uint32_t* tri,
                                                const std::uint32_t* comp_off, const std::vector<float4>& hbox,
-                                               cudaStream_t st);
+                                               cudaStream_t st, std::shared_future<void> dop_ready);
 
 // ---- mesh operations (mesh_ops.cu) ----
 std::uint32_t* lex_order3(nm_ctx* c, const std::uint32_t* k0, const std::uint32_t* k1, const std::uint32_t* k2,

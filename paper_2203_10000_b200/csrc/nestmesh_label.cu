@@ -715,6 +715,37 @@ int nm_set_surfaces(nm_ctx* c, const double* xyz, std::size_t nv, const std::uin
     // + 1e-5 |bound| (covers the fp32 rounding of the point and of the
     // projection in the kernel) and rounded outward.
     std::vector<float4> hbox(static_cast<std::size_t>(K) * nm::kDopF4);
+    // The certified-cell build starts now on its own host thread and stream:
+    // its geometry phase does not need the 13-DOP, which it waits for through
+    // dop_ready (set below, or set with an error if this thread throws first).
+    std::promise<void> dop_ready;
+    std::unique_ptr<CellBuilder> cells;
+    std::exception_ptr cells_err;
+    struct Joiner {
+      std::thread t;
+      ~Joiner() {
+        if (t.joinable()) t.join();
+      }
+    } cells_thread;
+    if (c->opt.cull_outside == 2) {
+      cells = make_cell_builder(c, xyz, tri, comp_off, hbox, c->side, dop_ready.get_future().share());
+      cells_thread.t = std::thread([&] {
+        try {
+          cells->prepare();
+        } catch (...) {
+          cells_err = std::current_exception();
+        }
+      });
+    }
+    // declared after the joiner, so destroyed first: on an exception below the
+    // cell thread is released (with an error) before it is joined
+    struct DopGuard {
+      std::promise<void>& p;
+      bool set = false;
+      ~DopGuard() {
+        if (!set) p.set_exception(std::make_exception_ptr(Error("13-DOP not computed")));
+      }
+    } dop_guard{dop_ready};
     // (one pass over the compartment's triangle corners, all 13 directions
     // per corner; chunks of triangles on every host thread, merged per
     // compartment: min/max are order-independent)
@@ -765,25 +796,9 @@ int nm_set_surfaces(nm_ctx* c, const double* xyz, std::size_t nv, const std::uin
         }
       }
     }
+    dop_ready.set_value();
+    dop_guard.set = true;
     lap("dop");
-    std::unique_ptr<CellBuilder> cells;
-    std::exception_ptr cells_err;
-    struct Joiner {
-      std::thread t;
-      ~Joiner() {
-        if (t.joinable()) t.join();
-      }
-    } cells_thread;
-    if (c->opt.cull_outside == 2) {
-      cells = make_cell_builder(c, xyz, tri, comp_off, hbox, c->side);
-      cells_thread.t = std::thread([&] {
-        try {
-          cells->prepare();
-        } catch (...) {
-          cells_err = std::current_exception();
-        }
-      });
-    }
 
     auto morton = [&](const double* m) {
       std::uint32_t q[3];
@@ -900,8 +915,11 @@ int nm_set_surfaces(nm_ctx* c, const double* xyz, std::size_t nv, const std::uin
     const std::size_t npad = ntiles * nm::kTile;
     const int sub_f4 = use_strips ? (nm::kSub / nm::kSegTris) * nm::kSegF4 : nm::kSub * 3;
     const std::size_t tile_f4 = static_cast<std::size_t>(sub_f4) * nm::kSubPerTile;
-    std::vector<float4> htri(ntiles * tile_f4);
-    std::vector<float4> hsub(ntiles * nm::kSubPerTile * nm::kSubRec);
+    // written in full by the packing below (every float4 of every record):
+    // no zero-fill of ~50 MB on this thread before the parallel pass
+    const std::size_t htri_n = ntiles * tile_f4, hsub_n = ntiles * nm::kSubPerTile * nm::kSubRec;
+    std::unique_ptr<float4[]> htri(new float4[std::max<std::size_t>(htri_n, 1)]);
+    std::unique_ptr<float4[]> hsub(new float4[std::max<std::size_t>(hsub_n, 1)]);
     std::vector<std::uint32_t> hcont(std::max<std::size_t>(ntiles, 1), 0u);
     static_assert(nm::kSubPerTile * nm::kGroups <= 32, "continuation bits of a tile must fit a uint32");
     const double far_ratio = c->opt.far_ratio, far_abs = c->opt.far_abs_mm;
@@ -1117,9 +1135,12 @@ int nm_set_surfaces(nm_ctx* c, const double* xyz, std::size_t nv, const std::uin
     lap("pack");
     if (inexact) throw Error("internal: a snapped subtile coordinate is not exact in fp32");
     c->strips = use_strips;
-    auto up = [&](DBuf& b, const void* src, std::size_t bytes) { up_on(b, src, bytes, c->stream); };
-    up(c->tri, htri.data(), htri.size() * sizeof(float4));
-    up(c->sub, hsub.data(), hsub.size() * sizeof(float4));
+    auto up = [&](DBuf& b, const void* src, std::size_t bytes) {  // pinned chunk staging (recycled chunks)
+      void* d = b.get(std::max<std::size_t>(bytes, 1));
+      c->h2d(d, src, bytes, c->stream);
+    };
+    up(c->tri, htri.get(), htri_n * sizeof(float4));
+    up(c->sub, hsub.get(), hsub_n * sizeof(float4));
     up(c->cont, hcont.data(), hcont.size() * sizeof(std::uint32_t));
     up(c->comp_tiles, tiles.data(), tiles.size() * sizeof(std::uint32_t));
     up(c->comp_box, hbox.data(), hbox.size() * sizeof(float4));
