@@ -271,6 +271,86 @@ def run_recursive(args):
     return 0
 
 
+def run_recursive_dist(args):
+    """cfg4 over N ranks (torchrun): the device-resident recursive driver
+    (distributed.refine_relabel_device): every rank holds the mesh on its GPU,
+    flags its tet range, the flag lists and the new-node masks are all-gathered
+    (NCCL), every rank refines identically and evaluates its shard of the new
+    nodes. value = evals of the new-node passes (all ranks) / the max-over-
+    ranks device time of the whole driver (CUDA events); the result is checked
+    against the single-GPU nm_refine_relabel on rank 0."""
+    import torch
+    import torch.distributed as dist
+    from paper_2203_10000_b200 import synth
+    from paper_2203_10000_b200._native import Context
+    from paper_2203_10000_b200.distributed import gather_labels, refine_relabel_device
+    rank, local, world = dist_env()
+    backend = os.environ.get("NM_DIST_BACKEND", "nccl")
+    if os.environ.get("NM_SAME_DEVICE") == "1":
+        local = 0
+    torch.cuda.set_device(local)
+    if backend == "nccl":
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        dist.init_process_group(backend)
+    cfg = synth.config(4)
+    S = cfg.surfaces
+    nodes, tets = cfg.lattice_mesh()
+    ctx = Context(local)
+    ctx.set_surfaces(S.xyz, S.tri, S.comp_off, S.label_ids)
+    d_nodes = torch.from_numpy(nodes).cuda()
+    d_tets = torch.from_numpy(tets.view(np.int32)).cuda()
+    d_m0 = torch.zeros(nodes.shape[0], dtype=torch.int32, device="cuda")
+    stream = torch.cuda.current_stream()
+    ctx.label_nodes_device(d_nodes, d_m0, stream=stream, stats=False)
+
+    def allmax(x):
+        t = torch.tensor([x], dtype=torch.float64, device="cuda" if backend == "nccl" else "cpu")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    out = None
+    for _ in range(args.warmup):
+        out = refine_relabel_device(ctx, d_nodes, d_tets, d_m0, args.levels, rank, world)
+    torch.cuda.synchronize()
+    times = []
+    for _ in range(args.steps):
+        dist.barrier()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        out = refine_relabel_device(ctx, d_nodes, d_tets, d_m0, args.levels, rank, world)
+        b.record(stream)
+        torch.cuda.synchronize()
+        times.append(a.elapsed_time(b))
+    ms = allmax(sum(times) / len(times))
+    n2, t2, labels, tsh, masks = out
+    new_nodes = int(n2.shape[0] - nodes.shape[0])
+    evals = new_nodes * S.n_triangles
+    full = gather_labels(labels, tsh)
+    same = None
+    if rank == 0:
+        m2, t2r, labr, maskr, _ = ctx.refine_relabel(nodes, tets, masks=d_m0.cpu().numpy().view(np.uint32),
+                                                     levels=args.levels)
+        same = bool(np.array_equal(full.cpu().numpy(), labr) and np.array_equal(t2.cpu().numpy().view(np.uint32), t2r)
+                    and np.array_equal(masks.cpu().numpy().view(np.uint32), maskr))
+        line = {
+            "metric": METRIC, "value": evals / (ms / 1e3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": f"cfg4: cfg3 + {args.levels} levels of straddle-tet refinement, new nodes only, "
+                                   f"{world} ranks (device-resident driver, NCCL exchange)",
+                       "initial_nodes": int(nodes.shape[0]), "refined_nodes": int(n2.shape[0]),
+                       "refined_tets": int(t2.shape[0]), "new_nodes_evaluated": new_nodes,
+                       "triangles": S.n_triangles, "parallelism": f"dp{world}"},
+            "recursive_equals_single_gpu_driver": same,
+        }
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
+    ctx.close()
+    return 0
+
+
 def workload_config(cfg, n_nodes, n_tets, world):
     S = cfg.surfaces
     names = {1: "cfg1 icosphere L3 / 32^3 lattice", 2: "cfg2 4 nested perturbed spheres / 2 mm lattice",
@@ -301,6 +381,8 @@ def main():
     if args.impl == "reference":
         return run_reference(args)
     if args.config == 4:
+        if int(os.environ.get("WORLD_SIZE", "1")) > 1:
+            return run_recursive_dist(args)
         return run_recursive(args)
 
     import torch

@@ -390,6 +390,23 @@ def test_bench_multi_rank_on_one_gpu(world):
     assert bal["ranks"] == world and bal["labels_identical"] and bal["full_mesh_labeling_time_s"] > 0
 
 
+def test_bench_cfg4_two_ranks_on_one_gpu():
+    """bench.py --config 4 under torchrun (2 ranks sharing cuda:0, gloo host
+    collective): the device-resident recursive driver runs end to end and
+    equals the single-GPU nm_refine_relabel (nodes, tets, masks, labels)."""
+    env = dict(os.environ, NM_DIST_BACKEND="gloo", NM_SAME_DEVICE="1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr=127.0.0.1", "--master-port=29644", str(ROOT / "bench.py"), "--gpus", "2",
+           "--config", "4", "--steps", "1", "--warmup", "3"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=1500, env=env, cwd=str(ROOT))
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    line = json.loads(lines[0])
+    assert line["n_gpus"] == 2 and line["value"] > 0
+    assert line["recursive_equals_single_gpu_driver"] is True
+
+
 @pytest.mark.parametrize("cull", [0, 1, 2])
 def test_shard_device_partials_are_disjoint_and_balanced(cull):
     """nm_label_nodes_shard_device: for 1, 2, 3 and 5 shards the partial masks
