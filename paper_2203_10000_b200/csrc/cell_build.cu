@@ -25,8 +25,10 @@ class CellBuild : public CellBuilder {
   // set; prepare() may run on a host thread beside the tile packing (it uses
   // its own stream); finish() needs the tiles (representatives run k_label).
   CellBuild(nm_ctx* c, const double* xyz, const std::uint32_t* tri, const std::uint32_t* comp_off,
-            const std::vector<float4>& hbox, cudaStream_t st, std::shared_future<void> dop_ready)
-      : c_(c), xyz_(xyz), tri_(tri), comp_off_(comp_off), hbox_(hbox), dop_ready_(std::move(dop_ready)), K_(c->K),
+            const std::vector<float4>& hbox, const std::vector<double>& hext, cudaStream_t st,
+            std::shared_future<void> dop_ready)
+      : c_(c), xyz_(xyz), tri_(tri), comp_off_(comp_off), hbox_(hbox), hext_(hext), dop_ready_(std::move(dop_ready)),
+        K_(c->K),
         ctr_{c->cx, c->cy, c->cz},
         st_(st), t0_(std::chrono::steady_clock::now()), tl_(t0_),
         verbose_(std::getenv("NM_CELL_VERBOSE") != nullptr), device_(std::getenv("NM_CELLS_HOST") == nullptr) {}
@@ -39,8 +41,8 @@ class CellBuild : public CellBuilder {
   void prepare() override {
     NvtxRange nvtx("nm certified cells: prepare");
     NM_CUDA(cudaSetDevice(c_->opt.device));
+    dop_ready_.get();  // the extents / 13-DOP (computed on the device by the caller)
     geometry();
-    dop_ready_.get();  // the 13-DOP (computed by the caller meanwhile) is needed from here on
     if (device_) {
       certify_device();
       runs_device();
@@ -74,7 +76,8 @@ class CellBuild : public CellBuilder {
   const std::uint32_t* tri_;
   const std::uint32_t* comp_off_;
   const std::vector<float4>& hbox_;
-  std::shared_future<void> dop_ready_;  // hbox_ is complete
+  const std::vector<double>& hext_;     // per compartment: 13-DOP minima, maxima (fp64; the first 3 = the box)
+  std::shared_future<void> dop_ready_;  // hbox_ and hext_ are complete
   const int K_;
   const double ctr_[3];
   cudaStream_t st_;
@@ -114,7 +117,8 @@ class CellBuild : public CellBuilder {
   void lap(const char* what) {
     if (!verbose_) return;
     const auto t = std::chrono::steady_clock::now();
-    std::fprintf(stderr, "[cells] %-6s %8.1f ms\n", what, std::chrono::duration<double, std::milli>(t - tl_).count());
+    std::fprintf(stderr, "[cells] %-6s %8.1f ms  (at %6.1f)\n", what, std::chrono::duration<double, std::milli>(t - tl_).count(),
+                 std::chrono::duration<double, std::milli>(t - c_->surf_t0).count());
     tl_ = t;
   }
   // host arrays allocated uninitialised: every entry is written (by a copy or
@@ -130,10 +134,13 @@ class CellBuild : public CellBuilder {
     madvise(p, bytes, MADV_HUGEPAGE);  // advisory: ignored where THP is off
     return HostArr<T>(static_cast<T*>(p));
   }
+  // host <-> device through the context's side stager (pinned chunks, never
+  // a pageable cudaMemcpyAsync: see staging.cuh)
   void up(DBuf& b, const void* src, std::size_t bytes) {
     void* d = b.get(std::max<std::size_t>(bytes, 1));
-    if (bytes) NM_CUDA(cudaMemcpyAsync(d, src, bytes, cudaMemcpyHostToDevice, st_));
+    c_->h2d(d, src, bytes, st_, /*side=*/true, /*side_pool=*/true);
   }
+  void down(void* h, const void* d, std::size_t bytes) { c_->d2h(h, d, bytes, st_, /*side=*/true, /*side_pool=*/true); }
   std::size_t cells(int k) const { return static_cast<std::size_t>(G_[k].nx) * G_[k].ny * G_[k].nz; }
   const float4* clus_k(int k) const { return static_cast<const float4*>(c_->clus.p) + coff_[k]; }
   const std::uint32_t* ctri_k(int k) const {
@@ -156,19 +163,19 @@ class CellBuild : public CellBuilder {
   }
 
   // ---- geometry: per compartment its grid and Morton-ordered clusters ----
-  // (per compartment: bounds, grid and Morton order; then the cluster and
-  // triangle spheres in chunks of clusters over all threads, written in place)
+  // (grid from the compartment's box, hext_; on the device: centroid Morton
+  // keys, a stable per-compartment sort, the cluster and triangle spheres,
+  // geometry.cuh)
   void geometry() {
     const int K = K_;
     G_.assign(K, nm::CellGrid{});
     coff_.assign(K + 1, 0);
-    std::vector<std::vector<std::uint32_t>> order(K);
-    parallel_for(K, [&](int k) { compartment_grid(k, order[k]); });
     for (int k = 0; k < K; ++k) {
+      compartment_grid(k);
       G_[k].off = static_cast<std::uint32_t>(total_);
       total_ += cells(k);
       if (total_ > 0xffffffffull) throw Error("certified-cell grids exceed 2^32 cells");
-      coff_[k + 1] = coff_[k] + (order[k].size() + nm::kCluster - 1) / nm::kCluster;
+      coff_[k + 1] = coff_[k] + (comp_off_[k + 1] - comp_off_[k] + nm::kCluster - 1) / nm::kCluster;
     }
     // memory budget: per level-1 cell ~13 B of host arrays (certified flag,
     // block and run indices, code) and ~5 B on the device (flag, code), plus
@@ -181,88 +188,48 @@ class CellBuild : public CellBuilder {
                   std::to_string(static_cast<long long>(double(total_) * 18.0 / 1e6)) +
                   " MB) exceed the 8 GB build budget: lower nm_options.cell_axis");
     const std::size_t ncl = coff_[K];
-    std::vector<float4> clus(ncl), tsph(ncl * nm::kCluster);
-    std::vector<std::uint32_t> ctri(ncl * nm::kCluster);
-    constexpr std::size_t kChunk = 256;  // clusters per work item
-    parallel_for(static_cast<int>((ncl + kChunk - 1) / kChunk), [&](int i) {
-      const std::size_t q0 = i * kChunk, q1 = std::min(ncl, q0 + kChunk);
-      int k = static_cast<int>(std::upper_bound(coff_.begin(), coff_.end(), q0) - coff_.begin()) - 1;
-      for (std::size_t q = q0; q < q1; ++q) {
-        while (q >= coff_[k + 1]) ++k;
-        const std::vector<std::uint32_t>& ord = order[k];
-        const std::size_t i0 = (q - coff_[k]) * nm::kCluster, i1 = std::min(ord.size(), i0 + nm::kCluster);
-        clus[q] = sphere(ord.data() + i0, ord.data() + i1);
-        for (std::size_t j = 0; j < nm::kCluster; ++j) {
-          const std::size_t t = i0 + j;
-          ctri[q * nm::kCluster + j] = t < i1 ? ord[t] : 0xffffffffu;
-          tsph[q * nm::kCluster + j] = t < i1 ? sphere(ord.data() + t, ord.data() + t + 1)
-                                             : make_float4(0.f, 0.f, 0.f, -1e30f);
-        }
-      }
-    });
+    const std::uint32_t nt = comp_off_[K];
+    std::vector<std::uint32_t> coff(K + 1);
+    for (int k = 0; k <= K; ++k) coff[k] = static_cast<std::uint32_t>(coff_[k]);
+    up(c_->cert_coff, coff.data(), coff.size() * sizeof(std::uint32_t));
+    c_->trace("cells", "geo: coff up");
+    auto* clus = c_->clus.as<float4>(std::max<std::size_t>(ncl, 1));
+    auto* ctri = c_->clus_tri.as<std::uint32_t>(std::max<std::size_t>(ncl, 1) * nm::kCluster);
+    auto* tsph = c_->clus_tsph.as<float4>(std::max<std::size_t>(ncl, 1) * nm::kCluster);
+    if (nt) {
+      const auto* xyz = static_cast<const double*>(c_->xyz64.p);
+      const auto* tri = static_cast<const std::uint32_t*>(c_->tri_idx.p);
+      const auto* coffd = static_cast<const std::uint32_t*>(c_->comp_off.p);
+      auto* keys = c_->geo_keys.as<unsigned long long>(nt);
+      auto* vals = c_->geo_vals.as<std::uint32_t>(nt);
+      auto* keys2 = c_->geo_keys2.as<unsigned long long>(nt);
+      auto* vals2 = c_->geo_vals2.as<std::uint32_t>(nt);
+      c_->trace("cells", "geo: allocs");
+      const nm::MortonFrame f{ctr_[0], ctr_[1], ctr_[2], c_->lo[0], c_->lo[1], c_->lo[2], c_->span};
+      nm::k_tri_morton<<<grid_for(nt, 256, c_->sm_count * 8), 256, 0, st_>>>(xyz, tri, coffd, K, nt, f, keys, vals);
+      int end_bit = 30;
+      while ((1 << (end_bit - 30)) < K) ++end_bit;
+      std::size_t tmp = 0;
+      NM_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, keys, keys2, vals, vals2, static_cast<int>(nt), 0, end_bit,
+                                              st_));
+      void* t = c_->cub_tmp2.get(tmp);
+      NM_CUDA(cub::DeviceRadixSort::SortPairs(t, tmp, keys, keys2, vals, vals2, static_cast<int>(nt), 0, end_bit, st_));
+      nm::k_cluster_spheres<<<static_cast<unsigned>((ncl * 32 + 255) / 256), 256, 0, st_>>>(
+          xyz, tri, coffd, static_cast<const std::uint32_t*>(c_->cert_coff.p), K, static_cast<std::uint32_t>(ncl),
+          ctr_[0], ctr_[1], ctr_[2], vals2, clus, ctri, tsph);
+      NM_CUDA(cudaGetLastError());
+      c_->trace("cells", "geo: launched");
+    }
     lap("setup");
-    up(c_->clus, clus.data(), clus.size() * sizeof(float4));
-    up(c_->clus_tri, ctri.data(), ctri.size() * sizeof(std::uint32_t));
-    up(c_->clus_tsph, tsph.data(), tsph.size() * sizeof(float4));
   }
 
-  // bounding sphere of triangles [b, e) in the centred frame: fp32 centre of
-  // the vertex box, radius rounded up with the kernel's margins (1e-6
-  // relative + 1e-5 mm + 4e-6 |centre|)
-  float4 sphere(const std::uint32_t* b, const std::uint32_t* e) const {
-    const double* ctr = ctr_;
-    double blo[3] = {1e300, 1e300, 1e300}, bhi[3] = {-1e300, -1e300, -1e300};
-    for (const std::uint32_t* t = b; t < e; ++t)
-      for (int v = 0; v < 3; ++v)
-        for (int a = 0; a < 3; ++a) {
-          const double x = xyz_[3 * std::size_t(tri_[3 * *t + v]) + a] - ctr[a];
-          blo[a] = std::min(blo[a], x);
-          bhi[a] = std::max(bhi[a], x);
-        }
-    const float fc[3] = {float(0.5 * (blo[0] + bhi[0])), float(0.5 * (blo[1] + bhi[1])),
-                         float(0.5 * (blo[2] + bhi[2]))};
-    double rho = 0.0;
-    for (const std::uint32_t* t = b; t < e; ++t)
-      for (int v = 0; v < 3; ++v) {
-        double d2 = 0.0;
-        for (int a = 0; a < 3; ++a) {
-          const double d = xyz_[3 * std::size_t(tri_[3 * *t + v]) + a] - ctr[a] - double(fc[a]);
-          d2 += d * d;
-        }
-        rho = std::max(rho, std::sqrt(d2));
-      }
-    const double rel = 4e-6 * (std::fabs(fc[0]) + std::fabs(fc[1]) + std::fabs(fc[2]));
-    return make_float4(fc[0], fc[1], fc[2], std::nextafter(float(rho * (1.0 + 1e-6) + 1e-5 + rel), INFINITY));
-  }
-
-  // compartment k: its triangles in Morton order of their centroids and its grid
-  void compartment_grid(int k, std::vector<std::uint32_t>& order) {
-    const double* ctr = ctr_;
-    const double* xyz = xyz_;
-    const std::uint32_t* tri = tri_;
-    const std::uint32_t b = comp_off_[k], e = comp_off_[k + 1];
+  // compartment k's grid: cubes of edge B = longest box side / cell_axis,
+  // one cube of margin around the box
+  void compartment_grid(int k) {
     nm::CellGrid g{0.0, 0.0, 0.0, 1.0, 0, 0, 0, 0u};
-    if (e > b) {
-      double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
-      std::vector<std::pair<std::uint32_t, std::uint32_t>> kk;
-      kk.reserve(e - b);
-      for (std::uint32_t t = b; t < e; ++t) {
-        double m[3] = {0, 0, 0};
-        for (int v = 0; v < 3; ++v)
-          for (int a = 0; a < 3; ++a) {
-            const double x = xyz[3 * std::size_t(tri[3 * t + v]) + a] - ctr[a];
-            lo[a] = std::min(lo[a], x);
-            hi[a] = std::max(hi[a], x);
-            m[a] += x / 3.0;
-          }
-        std::uint32_t q[3];
-        for (int a = 0; a < 3; ++a)
-          q[a] = static_cast<std::uint32_t>(std::clamp((m[a] + ctr[a] - c_->lo[a]) / c_->span * 1024.0, 0.0, 1023.0));
-        kk.emplace_back(spread10h(q[0]) | (spread10h(q[1]) << 1) | (spread10h(q[2]) << 2), t);
-      }
-      std::stable_sort(kk.begin(), kk.end(), [](auto& x, auto& y) { return x.first < y.first; });
-      order.resize(kk.size());
-      for (std::size_t i = 0; i < kk.size(); ++i) order[i] = kk[i].second;
+    if (comp_off_[k + 1] > comp_off_[k]) {
+      const double* e = hext_.data() + static_cast<std::size_t>(k) * nm::kExtQ;
+      const double lo[3] = {e[0], e[1], e[2]}, hi[3] = {e[nm::kDopDirs], e[nm::kDopDirs + 1], e[nm::kDopDirs + 2]};
       const double ext = std::max({hi[0] - lo[0], hi[1] - lo[1], hi[2] - lo[2]});
       g.B = std::max(ext / c_->opt.cell_axis, 1e-3);
       int n3[3];
@@ -401,15 +368,21 @@ class CellBuild : public CellBuilder {
     const int K = K_;
     auto* cert_d = c_->cell_cert.as<std::uint8_t>(std::max<std::size_t>(total_, 1));
     up(c_->cell_grids, G_.data(), G_.size() * sizeof(nm::CellGrid));
-    up(c_->cell_dop, hbox_.data(), hbox_.size() * sizeof(float4));
+    // one launch over every compartment's bricks (cells.cuh k_cell_certify_all)
+    std::vector<unsigned long long> first(K + 1, 0);
     for (int k = 0; k < K; ++k) {
-      if (!cells(k)) continue;
-      const std::size_t nbrick =
-          static_cast<std::size_t>((G_[k].nx + 3) / 4) * ((G_[k].ny + 3) / 4) * ((G_[k].nz + 1) / 2);
-      nm::k_cell_certify<<<static_cast<unsigned>((nbrick * 32 + 255) / 256), 256, 0, st_>>>(
-          G_[k], clus_k(k), nclus(k), ctri_k(k), tsph_k(k), static_cast<const double*>(c_->xyz64.p),
-          static_cast<const std::uint32_t*>(c_->tri_idx.p), c_->cx, c_->cy, c_->cz, cert_d);
+      const unsigned long long nbrick =
+          cells(k) ? static_cast<unsigned long long>((G_[k].nx + 3) / 4) * ((G_[k].ny + 3) / 4) * ((G_[k].nz + 1) / 2) : 0;
+      first[k + 1] = first[k] + nbrick;
     }
+    up(c_->cert_first, first.data(), first.size() * sizeof(unsigned long long));
+    nm::CertifyParams cp = certify_params();
+    cp.first = static_cast<const unsigned long long*>(c_->cert_first.p);
+    cp.out = cert_d;
+    cp.warps = first[K];
+    c_->trace("cells", "l1: ups");
+    if (cp.warps)
+      nm::k_cell_certify_all<<<static_cast<unsigned>((cp.warps * 32 + 255) / 256), 256, 0, st_>>>(cp);
     // child block of every uncertified cell: exclusive scan of the
     // uncertified flags in cell order (= the host path's numbering)
     const std::size_t n = std::max<std::size_t>(total_, 1);
@@ -423,19 +396,22 @@ class CellBuild : public CellBuilder {
       NM_CUDA(cub::DeviceScan::ExclusiveSum(t, tmp, unc, blk, static_cast<int>(total_), st_));
     }
     NM_CUDA(cudaGetLastError());
-    // boff_[k] = blk at the compartment's first cell (read back, K + 1 words)
-    std::vector<std::uint32_t> hb(2, 0);
+    // boff_[k] = blk at the compartment's first cell (gathered on the device,
+    // read back in one copy: K + 2 words)
+    std::vector<std::uint32_t> hw(K + 2, 0);
     if (total_) {
-      NM_CUDA(cudaMemcpyAsync(&hb[0], blk + total_ - 1, 4, cudaMemcpyDeviceToHost, st_));
-      NM_CUDA(cudaMemcpyAsync(&hb[1], unc + total_ - 1, 4, cudaMemcpyDeviceToHost, st_));
+      auto* w = c_->cell_words.as<std::uint32_t>(K + 2);
+      NM_CUDA(cudaMemsetAsync(w, 0, (K + 2) * sizeof(std::uint32_t), st_));
+      NM_CUDA(cudaMemcpyAsync(w + K, blk + total_ - 1, 4, cudaMemcpyDeviceToDevice, st_));
+      NM_CUDA(cudaMemcpyAsync(w + K + 1, unc + total_ - 1, 4, cudaMemcpyDeviceToDevice, st_));
+      for (int k = 0; k < K; ++k)
+        if (cells(k)) NM_CUDA(cudaMemcpyAsync(w + k, blk + G_[k].off, 4, cudaMemcpyDeviceToDevice, st_));
+      c_->trace("cells", "l1: scan launched");
+      down(hw.data(), w, (K + 2) * sizeof(std::uint32_t));
     }
-    std::vector<std::uint32_t> first(K, 0);
-    for (int k = 0; k < K; ++k)
-      if (cells(k)) NM_CUDA(cudaMemcpyAsync(&first[k], blk + G_[k].off, 4, cudaMemcpyDeviceToHost, st_));
-    NM_CUDA(cudaStreamSynchronize(st_));
-    const std::size_t nblk = total_ ? std::size_t(hb[0]) + hb[1] : 0;
+    const std::size_t nblk = total_ ? std::size_t(hw[K]) + hw[K + 1] : 0;
     boff_.assign(K + 1, nblk);
-    for (int k = K - 1; k >= 0; --k) boff_[k] = cells(k) ? first[k] : boff_[k + 1];
+    for (int k = K - 1; k >= 0; --k) boff_[k] = cells(k) ? hw[k] : boff_[k + 1];
     lap("l1");
     nchild_ = nblk * nm::kChildren;
     if (!nblk) return;
@@ -443,16 +419,33 @@ class CellBuild : public CellBuilder {
     nm::k_block_cells<<<grid_for(total_, 256, c_->sm_count * 8), 256, 0, st_>>>(
         cert_d, blk, total_, static_cast<const nm::CellGrid*>(c_->cell_grids.p), K, blk_cells);
     auto* ch_d = c_->cell_child.as<std::uint8_t>(nchild_);
-    for (int k = 0; k < K; ++k) {
-      const std::size_t nb = boff_[k + 1] - boff_[k];
-      if (!nb) continue;
-      nm::k_child_certify<<<static_cast<unsigned>((nb * 64 + 255) / 256), 256, 0, st_>>>(
-          G_[k], blk_cells + boff_[k], nb, clus_k(k), nclus(k), ctri_k(k), tsph_k(k),
-          static_cast<const double*>(c_->xyz64.p), static_cast<const std::uint32_t*>(c_->tri_idx.p), c_->cx, c_->cy,
-          c_->cz, ch_d + boff_[k] * nm::kChildren);
-    }
+    std::vector<unsigned long long> first2(K + 1, 0);
+    for (int k = 0; k <= K; ++k) first2[k] = 2ull * boff_[k];
+    up(c_->cert_first2, first2.data(), first2.size() * sizeof(unsigned long long));
+    nm::CertifyParams cp2 = certify_params();
+    cp2.first = static_cast<const unsigned long long*>(c_->cert_first2.p);
+    cp2.cells = blk_cells;
+    cp2.out = ch_d;
+    cp2.warps = first2[K];
+    nm::k_child_certify_all<<<static_cast<unsigned>((cp2.warps * 32 + 255) / 256), 256, 0, st_>>>(cp2);
     NM_CUDA(cudaGetLastError());
     lap("l2");
+  }
+
+  nm::CertifyParams certify_params() const {
+    nm::CertifyParams p{};
+    p.grids = static_cast<const nm::CellGrid*>(c_->cell_grids.p);
+    p.K = K_;
+    p.coff = static_cast<const std::uint32_t*>(c_->cert_coff.p);
+    p.clus = static_cast<const float4*>(c_->clus.p);
+    p.clus_tri = static_cast<const std::uint32_t*>(c_->clus_tri.p);
+    p.tsph = static_cast<const float4*>(c_->clus_tsph.p);
+    p.xyz = static_cast<const double*>(c_->xyz64.p);
+    p.tri = static_cast<const std::uint32_t*>(c_->tri_idx.p);
+    p.cx = c_->cx;
+    p.cy = c_->cy;
+    p.cz = c_->cz;
+    return p;
   }
 
   nm::RunParams run_params(bool fill) {
@@ -463,7 +456,7 @@ class CellBuild : public CellBuilder {
     p.cert = static_cast<const std::uint8_t*>(c_->cell_cert.p);
     p.blk = static_cast<const std::uint32_t*>(c_->cell_blkidx.p);
     p.child = static_cast<const std::uint8_t*>(c_->cell_child.p);
-    p.dop4 = static_cast<const float4*>(c_->cell_dop.p);
+    p.dop4 = static_cast<const float4*>(c_->comp_box.p);  // the 13-DOP slabs (k_extents_finalize)
     p.ctr0 = ctr_[0];
     p.ctr1 = ctr_[1];
     p.ctr2 = ctr_[2];
@@ -482,11 +475,14 @@ class CellBuild : public CellBuilder {
     for (int k = 0; k < K; ++k) rf[k + 1] = rf[k] + (cells(k) ? static_cast<std::uint32_t>(G_[k].ny * G_[k].nz) : 0u);
     nrows_ = rf[K];
     up(c_->row_first, rf.data(), rf.size() * sizeof(std::uint32_t));
+    c_->trace("cells", "runs: row_first up");
     (void)c_->cell_val.as<std::int32_t>(std::max<std::size_t>(total_, 1));
     (void)c_->child_val.as<std::int32_t>(std::max<std::size_t>(nchild_, 1));
+    c_->trace("cells", "runs: val allocs");
     auto* cur = c_->rep_cur.as<unsigned>(64);  // [0, 32) cursors, [32, 64) slot bases
     (void)c_->rep_pts.as<double>(3);
     NM_CUDA(cudaMemsetAsync(cur, 0, 64 * sizeof(unsigned), st_));
+    c_->trace("cells", "runs: memset");
     if (!nrows_) {
       rep_cnt_d_.assign(K, 0);
       rep_first_d_.assign(K + 1, 0);
@@ -499,8 +495,9 @@ class CellBuild : public CellBuilder {
                                                                                                    nrows_);
     NM_CUDA(cudaGetLastError());
     rep_cnt_d_.assign(K, 0);
-    NM_CUDA(cudaMemcpyAsync(rep_cnt_d_.data(), cur, K * sizeof(unsigned), cudaMemcpyDeviceToHost, st_));
-    NM_CUDA(cudaStreamSynchronize(st_));
+    c_->trace("cells", "runs: count launched");
+    down(rep_cnt_d_.data(), cur, K * sizeof(unsigned));
+    c_->trace("cells", "runs: counts read");
     rep_first_d_.assign(K + 1, 0);
     for (int k = 0; k < K; ++k) rep_first_d_[k + 1] = rep_first_d_[k] + rep_cnt_d_[k];
     nreps_ = rep_first_d_[K];
@@ -508,7 +505,7 @@ class CellBuild : public CellBuilder {
     (void)pts;
     cur = static_cast<unsigned*>(c_->rep_cur.p);
     NM_CUDA(cudaMemsetAsync(cur, 0, 32 * sizeof(unsigned), st_));
-    NM_CUDA(cudaMemcpyAsync(cur + 32, rep_first_d_.data(), K * sizeof(unsigned), cudaMemcpyHostToDevice, st_));
+    c_->h2d(cur + 32, rep_first_d_.data(), K * sizeof(unsigned), st_, /*side=*/true, /*side_pool=*/true);
     NM_CUDA(cudaMemsetAsync(c_->cell_val.p, 0xff, std::max<std::size_t>(total_, 1) * sizeof(std::int32_t), st_));
     if (nchild_) NM_CUDA(cudaMemsetAsync(c_->child_val.p, 0xff, nchild_ * sizeof(std::int32_t), st_));
     // fill pass: values, representative points (level-1 values first: the
@@ -517,7 +514,6 @@ class CellBuild : public CellBuilder {
     nm::k_runs_fine<<<grid_for(std::size_t(nrows_) * 16, 128, c_->sm_count * 16), 128, 0, st_>>>(run_params(true),
                                                                                                    nrows_);
     NM_CUDA(cudaGetLastError());
-    NM_CUDA(cudaStreamSynchronize(st_));  // rep_first_d_ (host) must outlive its copy
     lap("runs");
   }
 
@@ -546,8 +542,7 @@ class CellBuild : public CellBuilder {
           cnt);
     NM_CUDA(cudaGetLastError());
     unsigned long long ncert = 0;
-    NM_CUDA(cudaMemcpyAsync(&ncert, cnt, sizeof ncert, cudaMemcpyDeviceToHost, st_));
-    NM_CUDA(cudaStreamSynchronize(st_));
+    down(&ncert, cnt, sizeof ncert);
     lap("codes");
     c_->cells_total = total_ + nchild_;
     c_->cells_l1 = total_;
@@ -872,8 +867,9 @@ class CellBuild : public CellBuilder {
 
 std::unique_ptr<CellBuilder> make_cell_builder(nm_ctx* c, const double* xyz, const std::uint32_t* tri,
                                                const std::uint32_t* comp_off, const std::vector<float4>& hbox,
-                                               cudaStream_t st, std::shared_future<void> dop_ready) {
-  return std::make_unique<CellBuild>(c, xyz, tri, comp_off, hbox, st, std::move(dop_ready));
+                                               const std::vector<double>& hext, cudaStream_t st,
+                                               std::shared_future<void> dop_ready) {
+  return std::make_unique<CellBuild>(c, xyz, tri, comp_off, hbox, hext, st, std::move(dop_ready));
 }
 
 }  // namespace nmh

@@ -151,6 +151,179 @@ static __global__ void __launch_bounds__(256) k_child_certify(const CellGrid g, 
   out[(w / 2) * kChildren + (2 * half + lane / 16) * 16 + lane % 16] = hit ? 0 : 1;
 }
 
+// ---------------------------------------------------------------------------
+// Round-2 certification (the device build; the host-run path above keeps the
+// per-lane kernels, and tests compare the two builds bit for bit). Same
+// decision per cube as warp_certify: "some triangle of the compartment has
+// exact fp64 distance <= rb from the cube centre". Only the conservative
+// fp32 pre-filters are organised differently:
+//   * per candidate cluster, lane t holds triangle t's sphere and tests it
+//     against all 32 cube balls of the warp at once (the cube centres lie on
+//     a 4 x 4 x 2 lattice: 4 + 4 + 2 squared offsets, 32 sums), with the
+//     largest lane margin — a superset of each lane's own candidates;
+//   * one ballot per needing cube transposes the masks, and each cube runs
+//     the exact test on its own candidate triangles.
+// This replaces 32 dependent per-lane loads + tests per cluster with one
+// coalesced load and a 5-stage shuffle transpose; the compartments' grids go
+// in ONE launch.
+// ---------------------------------------------------------------------------
+struct CertifyParams {
+  const CellGrid* grids;        // K
+  int K;
+  const unsigned long long* first;  // K + 1: first work warp of each compartment
+  const std::uint32_t* coff;    // K + 1: first cluster of each compartment
+  const float4* clus;           // cluster spheres (all compartments)
+  const std::uint32_t* clus_tri;
+  const float4* tsph;
+  const double* xyz;
+  const std::uint32_t* tri;
+  double cx, cy, cz;
+  const std::uint32_t* cells;   // level 2: global child block -> compartment-local level-1 cell
+  std::uint8_t* out;            // level 1: cert flags by global cell; level 2: child flags
+  unsigned long long warps;     // total work warps
+};
+
+static __device__ bool warp_certify_coop(double Ox, double Oy, double Oz, double e, bool active,
+                                         const CertifyParams& p, std::uint32_t c0, int nclus) {
+  const int lane = threadIdx.x & 31;
+  const double Cx = Ox + (lane % 4 + 0.5) * e, Cy = Oy + ((lane / 4) % 4 + 0.5) * e, Cz = Oz + (lane / 16 + 0.5) * e;
+  const double rb = cell_ball(e);
+  const float bx = static_cast<float>(Ox + 2.0 * e), by = static_cast<float>(Oy + 2.0 * e), bz = static_cast<float>(Oz + e);
+  const float fbr = static_cast<float>(e * 2.1794494717703369 + rb) + 1e-3f + 4e-6f * (fabsf(bx) + fabsf(by) + fabsf(bz));
+  const float fx = static_cast<float>(Cx), fy = static_cast<float>(Cy), fz = static_cast<float>(Cz);
+  const float frb = static_cast<float>(rb) + 1e-3f + 4e-6f * (fabsf(fx) + fabsf(fy) + fabsf(fz));
+  // the warp's cube lattice (the lanes' own fp32 centres) and the largest margin
+  float X[4], Y[4], Z[2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    X[i] = __shfl_sync(kFull, fx, i);
+    Y[i] = __shfl_sync(kFull, fy, 4 * i);
+  }
+  Z[0] = __shfl_sync(kFull, fz, 0);
+  Z[1] = __shfl_sync(kFull, fz, 16);
+  float frbm = frb;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) frbm = fmaxf(frbm, __shfl_xor_sync(kFull, frbm, o));
+  const float4* clus = p.clus + c0;
+  const std::uint32_t* ctri = p.clus_tri + static_cast<std::size_t>(c0) * kCluster;
+  const float4* tsph = p.tsph + static_cast<std::size_t>(c0) * kCluster;
+  const V3t<double> pt{Cx + p.cx, Cy + p.cy, Cz + p.cz};
+  bool hit = !active;
+  for (int q0 = 0; q0 < nclus; q0 += 32) {
+    bool cand = false;
+    if (q0 + lane < nclus) {
+      const float4 s = __ldg(clus + q0 + lane);
+      const float dx = bx - s.x, dy = by - s.y, dz = bz - s.z;
+      const float R = fbr + s.w;
+      cand = dx * dx + dy * dy + dz * dz <= R * R;
+    }
+    unsigned bal = __ballot_sync(kFull, cand);
+    while (bal) {
+      const int q = q0 + __ffs(bal) - 1;
+      bal &= bal - 1;
+      // cubes (lanes) still open whose ball meets the cluster sphere
+      bool need = false;
+      if (!hit) {
+        const float4 s = __ldg(clus + q);
+        const float dx = fx - s.x, dy = fy - s.y, dz = fz - s.z;
+        const float R = frb + s.w;
+        need = dx * dx + dy * dy + dz * dz <= R * R;
+      }
+      unsigned needm = __ballot_sync(kFull, need);
+      if (!needm) continue;
+      // lane t: which cubes' balls meet triangle t's sphere (pads: w < 0)
+      const float4 ts = __ldg(tsph + static_cast<std::size_t>(q) * kCluster + lane);
+      unsigned m = 0;
+      if (ts.w >= 0.0f) {
+        const float R = frbm + ts.w, R2 = R * R;
+        float dx2[4], dy2[4], dz2[2];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const float dx = X[i] - ts.x, dy = Y[i] - ts.y;
+          dx2[i] = dx * dx;
+          dy2[i] = dy * dy;
+        }
+        dz2[0] = (Z[0] - ts.z) * (Z[0] - ts.z);
+        dz2[1] = (Z[1] - ts.z) * (Z[1] - ts.z);
+#pragma unroll
+        for (int kz = 0; kz < 2; ++kz)
+#pragma unroll
+          for (int jy = 0; jy < 4; ++jy) {
+            const float yz = dy2[jy] + dz2[kz];
+#pragma unroll
+            for (int ix = 0; ix < 4; ++ix) m |= (yz + dx2[ix] <= R2 ? 1u : 0u) << (ix + 4 * jy + 16 * kz);
+          }
+      }
+      m &= needm;
+      // transpose the 32 x 32 bit matrix (row t = triangle t's cube mask) so
+      // that lane L holds cube L's candidate triangles: five block-swap stages
+      unsigned mine = m;
+#pragma unroll
+      for (int j = 16; j > 0; j >>= 1) {
+        const unsigned M = j == 16 ? 0x0000ffffu : j == 8 ? 0x00ff00ffu : j == 4 ? 0x0f0f0f0fu : j == 2 ? 0x33333333u : 0x55555555u;
+        const unsigned o = __shfl_xor_sync(kFull, mine, j);
+        mine = (lane & j) ? ((mine & ~M) | ((o >> j) & M)) : ((mine & M) | ((o & M) << j));
+      }
+      while (mine && !hit) {
+        const int t = __ffs(mine) - 1;
+        mine &= mine - 1;
+        const std::uint32_t tid = __ldg(ctri + static_cast<std::size_t>(q) * kCluster + t);
+        const std::uint32_t* ev = p.tri + 3 * static_cast<std::size_t>(tid);
+        const double* A = p.xyz + 3 * static_cast<std::size_t>(ev[0]);
+        const double* Bv = p.xyz + 3 * static_cast<std::size_t>(ev[1]);
+        const double* Cv = p.xyz + 3 * static_cast<std::size_t>(ev[2]);
+        const double d2 = point_tri_dist2<double>(pt, {A[0], A[1], A[2]}, {Bv[0], Bv[1], Bv[2]}, {Cv[0], Cv[1], Cv[2]});
+        hit = !(d2 > rb * rb);  // NaN (degenerate) counts as a hit
+      }
+    }
+    if (__all_sync(kFull, hit)) break;
+  }
+  return hit;
+}
+
+__device__ __forceinline__ int work_compartment(const CertifyParams& p, unsigned long long w) {
+  int k = 0;
+  while (k + 1 < p.K && w >= p.first[k + 1]) ++k;
+  return k;
+}
+
+// level 1, all compartments: one warp per 4 x 4 x 2 brick (first[] = brick prefix)
+static __global__ void __launch_bounds__(256) k_cell_certify_all(const CertifyParams p) {
+  const unsigned long long w = (blockIdx.x * static_cast<unsigned long long>(blockDim.x) + threadIdx.x) / 32;
+  if (w >= p.warps) return;  // warp-uniform
+  const int k = work_compartment(p, w);
+  const CellGrid g = p.grids[k];
+  const int lane = threadIdx.x & 31;
+  const unsigned long long lw = w - p.first[k];
+  const int bx = (g.nx + 3) / 4, by = (g.ny + 3) / 4;
+  const int i0 = static_cast<int>(lw % bx) * 4, j0 = static_cast<int>((lw / bx) % by) * 4,
+            k0 = static_cast<int>(lw / (static_cast<unsigned long long>(bx) * by)) * 2;
+  const int ix = i0 + lane % 4, iy = j0 + (lane / 4) % 4, iz = k0 + lane / 16;
+  const bool active = ix < g.nx && iy < g.ny && iz < g.nz;
+  const bool hit = warp_certify_coop(g.ox + i0 * g.B, g.oy + j0 * g.B, g.oz + k0 * g.B, g.B, active, p, p.coff[k],
+                                     static_cast<int>(p.coff[k + 1] - p.coff[k]));
+  if (active) p.out[g.off + (static_cast<std::size_t>(iz) * g.ny + iy) * g.nx + ix] = hit ? 0 : 1;
+}
+
+// level 2, all compartments: one warp per half child block (first[] = 2 x block prefix)
+static __global__ void __launch_bounds__(256) k_child_certify_all(const CertifyParams p) {
+  const unsigned long long w = (blockIdx.x * static_cast<unsigned long long>(blockDim.x) + threadIdx.x) / 32;
+  if (w >= p.warps) return;  // warp-uniform
+  const int k = work_compartment(p, w);
+  const CellGrid g = p.grids[k];
+  const int lane = threadIdx.x & 31;
+  const unsigned long long b = w / 2;  // global child block
+  const std::uint32_t cell = p.cells[b];
+  const int half = static_cast<int>(w % 2);
+  const int ix = static_cast<int>(cell % g.nx);
+  const int iy = static_cast<int>((cell / g.nx) % g.ny);
+  const int iz = static_cast<int>(cell / (static_cast<std::uint32_t>(g.nx) * g.ny));
+  const double e = g.B / kSubCells;
+  const bool hit = warp_certify_coop(g.ox + ix * g.B, g.oy + iy * g.B, g.oz + iz * g.B + 2 * half * e, e, true, p,
+                                     p.coff[k], static_cast<int>(p.coff[k + 1] - p.coff[k]));
+  p.out[b * kChildren + (2 * half + lane / 16) * 16 + lane % 16] = hit ? 0 : 1;
+}
+
 // Per evaluation position i (point order[i]): unk bit c = pair (point, c)
 // still to be evaluated; ins bit c = known inside (certified w = 1). The
 // point's masks / flagmask / s entries of the known pairs are written here;

@@ -13,6 +13,7 @@
 #include <exception>
 #include <future>
 #include <memory>
+#include <mutex>
 #include <numeric>
 #include <queue>
 #include <unordered_map>
@@ -29,6 +30,7 @@
 #include "refine.cuh"
 #include "distance.cuh"
 #include "cells.cuh"
+#include "geometry.cuh"
 #include <nvtx3/nvToolsExt.h>
 
 #include "nestmesh_label.h"
@@ -67,8 +69,101 @@ struct Error : std::runtime_error {
       throw Error(std::string(#x) + ": " + cudaGetErrorName(e_) + " " + cudaGetErrorString(e_));       \
   } while (0)
 
+// Device memory of the library: one stream-ordered pool per device, which
+// keeps freed memory (up to kRetain) instead of returning it to the driver.
+// Fresh cudaMalloc calls were measured at up to ~170 ms for ~45 MB on the GPU
+// box when a context had just freed its buffers (one-shot contexts, tests);
+// a pool allocation reuses the previous context's memory. Allocations and
+// frees are ordered on a private per-device stream (synchronised after an
+// allocation, so the memory is usable from any stream).
+class DevicePool {
+ public:
+  static constexpr std::uint64_t kRetain = std::uint64_t(32) << 30;
+  struct Dev {
+    cudaMemPool_t pool = nullptr;
+    cudaStream_t st = nullptr;
+  };
+  static Dev& of(int dev) {
+    static std::mutex m;
+    static auto* devs = new std::vector<Dev>();  // leaked on purpose: no teardown-order issues at exit
+    std::lock_guard<std::mutex> g(m);
+    if (static_cast<int>(devs->size()) <= dev) devs->resize(dev + 1);
+    Dev& d = (*devs)[dev];
+    if (!d.pool) {
+      cudaMemPoolProps props{};
+      props.allocType = cudaMemAllocationTypePinned;
+      props.location.type = cudaMemLocationTypeDevice;
+      props.location.id = dev;
+      NM_CUDA(cudaMemPoolCreate(&d.pool, &props));
+      std::uint64_t thr = kRetain;
+      NM_CUDA(cudaMemPoolSetAttribute(d.pool, cudaMemPoolAttrReleaseThreshold, &thr));
+      NM_CUDA(cudaStreamCreateWithFlags(&d.st, cudaStreamNonBlocking));
+    }
+    return d;
+  }
+  static void* alloc(std::size_t bytes, int* dev_out) {
+    int dev = 0;
+    NM_CUDA(cudaGetDevice(&dev));
+    Dev& d = of(dev);
+    void* p = nullptr;
+    NM_CUDA(cudaMallocFromPoolAsync(&p, bytes, d.pool, d.st));
+    NM_CUDA(cudaStreamSynchronize(d.st));
+    *dev_out = dev;
+    return p;
+  }
+  // caller guarantees no queued work uses p any more
+  static void free(void* p, int dev) {
+    if (p) cudaFreeAsync(p, of(dev).st);
+  }
+};
+
+// Device buffers retired by a DBuf that grew: queued work may still read
+// them, so they are freed per device at the end of the C ABI call (guarded)
+// after one device synchronisation — never by a cudaFree in the middle of a
+// call, which would wait for the whole device and block other host threads'
+// CUDA calls meanwhile (the certified-cell thread of nm_set_surfaces beside
+// the main thread's uploads; probes/copy_hol.cu).
+class Retired {
+ public:
+  static Retired& get() {
+    static Retired* r = new Retired;  // leaked on purpose: no teardown-order issues at exit
+    return *r;
+  }
+  void add(void* p, int dev) {
+    std::lock_guard<std::mutex> g(m_);
+    v_.emplace_back(dev, p);
+  }
+  void drain_current_device() {
+    int d = 0;
+    if (cudaGetDevice(&d) != cudaSuccess) return;
+    std::vector<void*> mine;
+    {
+      std::lock_guard<std::mutex> g(m_);
+      for (std::size_t i = 0; i < v_.size();) {
+        if (v_[i].first == d) {
+          mine.push_back(v_[i].second);
+          v_[i] = v_.back();
+          v_.pop_back();
+        } else {
+          ++i;
+        }
+      }
+    }
+    if (mine.empty()) return;
+    cudaDeviceSynchronize();
+    for (void* p : mine) DevicePool::free(p, d);
+  }
+
+ private:
+  std::mutex m_;
+  std::vector<std::pair<int, void*>> v_;
+};
+
 template <class F>
 inline int guarded(F&& f) {
+  struct Drain {
+    ~Drain() { Retired::get().drain_current_device(); }
+  } drain;
   try {
     f();
     return 0;
@@ -81,17 +176,33 @@ inline int guarded(F&& f) {
   }
 }
 
-// Growable device buffer.
+// Growable device buffer (DevicePool memory). The owner synchronises the
+// device before destroying it (nm_ctx's destructor).
 struct DBuf {
   void* p = nullptr;
   std::size_t cap = 0;
+  int dev = 0;
+  DBuf() = default;
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  DBuf(DBuf&& o) noexcept : p(o.p), cap(o.cap), dev(o.dev) {
+    o.p = nullptr;
+    o.cap = 0;
+  }
+  DBuf& operator=(DBuf&& o) noexcept {  // swaps (std::swap of two buffers)
+    std::swap(p, o.p);
+    std::swap(cap, o.cap);
+    std::swap(dev, o.dev);
+    return *this;
+  }
+  ~DBuf() { DevicePool::free(p, dev); }
   void* get(std::size_t bytes) {
     if (bytes > cap) {
-      if (p) cudaFree(p);
+      if (p) Retired::get().add(p, dev);  // freed after the call (Retired)
       p = nullptr;
       cap = 0;
       const std::size_t want = std::max<std::size_t>(bytes, 256);
-      NM_CUDA(cudaMalloc(&p, want));
+      p = DevicePool::alloc(want, &dev);
       cap = want;
     }
     return p;
@@ -99,11 +210,6 @@ struct DBuf {
   template <class T>
   T* as(std::size_t count) {
     return static_cast<T*>(get(count * sizeof(T)));
-  }
-  void release() {
-    if (p) cudaFree(p);
-    p = nullptr;
-    cap = 0;
   }
 };
 
@@ -176,7 +282,9 @@ struct nm_ctx {
   void h2d(void* d, const void* h, std::size_t bytes, cudaStream_t st, bool side = false, bool side_pool = false) {
     (side ? stage_side : stage_main).h2d(d, h, bytes, st, pool(side_pool));
   }
-  void d2h(void* h, const void* d, std::size_t bytes, cudaStream_t st) { stage_main.d2h(h, d, bytes, st, pool(false)); }
+  void d2h(void* h, const void* d, std::size_t bytes, cudaStream_t st, bool side = false, bool side_pool = false) {
+    (side ? stage_side : stage_main).d2h(h, d, bytes, st, pool(side_pool));
+  }
   int sm_count = 0;
 
   // surfaces
@@ -189,12 +297,23 @@ struct nm_ctx {
   nm::LabelIds ids{};
   std::vector<std::uint32_t> comp_tiles_h;  // host copy of the K+1 tile offsets
   std::size_t n_continued = 0;              // strip segments continuing the previous one (cont bits set)
+  std::chrono::steady_clock::time_point surf_t0{};  // start of the last nm_set_surfaces (NM_CELL_VERBOSE laps)
+  int trace_level = -1;  // NM_CELL_VERBOSE >= 2: fine timestamps (trace())
+  void trace(const char* tag, const char* what) {
+    if (trace_level < 0) {
+      const char* v = std::getenv("NM_CELL_VERBOSE");
+      trace_level = v ? std::atoi(v) : 0;
+    }
+    if (trace_level < 2) return;
+    std::fprintf(stderr, "    [%s] %-24s at %7.2f\n", tag, what,
+                 std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - surf_t0).count());
+  }
   double snap_grid = 0.0;                   // vertex snapping grid of the fp32 subtile frames (mm, power of two)
   nmh::DBuf tri, sub, cont, comp_tiles, xyz64, tri_idx, tri64, comp_off, comp_box, cullmask;
   // certified cells (cull_outside = 2, cells.cuh)
   bool cells = false;
   nmh::DBuf dist_clus, dist_slot, dist_ord, sp_part, sp_det, cell_state, cell_child, cell_cert, cell_blk, cell_grids, clus, clus_tri, clus_tsph, unk, sp_list, sp_chunk, sp_cnt, rep_pts, rep_s, rep_m, rep_f,
-      cell_unc, cell_blkidx, cell_val, child_val, row_first, rep_cur, rep_w, cell_dop, cell_cnt, cub_tmp2;
+      cell_unc, cell_blkidx, cell_val, child_val, row_first, rep_cur, rep_w, cell_dop, cell_cnt, cub_tmp2, cell_words, cert_first, cert_first2, cert_coff, ext_items, ext_first, ext_part, ext_val, geo_keys, geo_vals, geo_keys2, geo_vals2;
   std::uint64_t cells_total = 0, cells_certified = 0, cell_reps = 0, sparse_pairs = 0, sparse_evals = 0;
   std::uint64_t cells_l1 = 0, cells_children = 0;  // level-1 cells and children (nm_cell_dump)
   double ms_cells = 0.0;  // host wall time of the certification (nm_set_surfaces)
@@ -208,15 +327,9 @@ struct nm_ctx {
       s_out, word, pair_cnt, pairs, pos_masks, fix_part;
 
   ~nm_ctx() {
-    for (nmh::DBuf* b : {&dist_clus, &dist_slot, &dist_ord, &sp_part, &sp_det, &cell_state, &cell_child, &cell_cert, &cell_blk, &cell_grids, &clus, &clus_tri, &clus_tsph, &unk, &sp_list, &sp_chunk, &sp_cnt, &rep_pts, &rep_s,
-                    &rep_m, &rep_f, &cell_unc, &cell_blkidx, &cell_val, &child_val, &row_first, &rep_cur, &rep_w, &cell_dop, &cell_cnt, &cub_tmp2})
-      b->release();
-    for (nmh::DBuf* b : {&tri, &sub, &cont, &comp_tiles, &xyz64, &tri_idx, &tri64, &comp_off, &comp_box, &cullmask, &pts, &masks, &flagmask, &nbr, &known, &want, &fkeys, &frontier, &lex, &region, &bfaces, &btri,
-                    &dist_tri, &dist_xyz, &dist_idx, &dist_d32, &dist_out, &r_red, &r_keys, &r_keys2, &r_S,
-                    &r_idx, &r_touched, &r_mask, &r_cnt, &r_offs, &r_flag, &meshA_nodes, &meshA_tets, &meshA_labels,
-                    &meshB_nodes, &meshB_tets, &meshB_labels, &meshB_parent, &masks2, &order, &keys,
-                    &keys_alt, &order_alt, &cub_tmp, &list, &chunk, &counters, &count, &tets, &labels, &s_out, &word, &pair_cnt, &pairs, &pos_masks, &fix_part})
-      b->release();
+    // every DBuf member frees its memory after this body: nothing queued by
+    // this context (on its streams or on a caller's stream) may still use it
+    cudaDeviceSynchronize();
     for (auto& e : ev)
       if (e) cudaEventDestroy(e);
     if (ev_side) cudaEventDestroy(ev_side);
@@ -287,7 +400,8 @@ class CellBuilder {
 // hbox is filled by the caller concurrently; dop_ready is set when it is
 std::unique_ptr<CellBuilder> make_cell_builder(nm_ctx* c, const double* xyz, const std::uint32_t* tri,
                                                const std::uint32_t* comp_off, const std::vector<float4>& hbox,
-                                               cudaStream_t st, std::shared_future<void> dop_ready);
+                                               const std::vector<double>& hext, cudaStream_t st,
+                                               std::shared_future<void> dop_ready);
 
 // ---- mesh operations (mesh_ops.cu) ----
 std::uint32_t* lex_order3(nm_ctx* c, const std::uint32_t* k0, const std::uint32_t* k1, const std::uint32_t* k2,

@@ -264,9 +264,11 @@ std::vector<std::uint32_t> classify_cells(nm_ctx* c, const double* d_pts, std::s
     nm::k_select_scan<<<1, 1024, 0, st>>>(chunk + k * nb, nb, dcnt + k);
     launches += 2;
   }
-  std::vector<std::uint32_t> cnt(K);
-  NM_CUDA(cudaMemcpyAsync(cnt.data(), dcnt, K * sizeof(std::uint32_t), cudaMemcpyDeviceToHost, st));
+  // (through the context's pinned words: a pageable read-back would be a
+  // driver-staged copy, serialised with other host threads' copies)
+  NM_CUDA(cudaMemcpyAsync(c->h_pcnt, dcnt, K * sizeof(std::uint32_t), cudaMemcpyDeviceToHost, st));
   NM_CUDA(cudaStreamSynchronize(st));
+  std::vector<std::uint32_t> cnt(c->h_pcnt, c->h_pcnt + K);
   std::size_t total = 0;
   for (int k = 0; k < K; ++k) total += cnt[k];
   if (total > 0xffffffffull) throw Error("more than 2^32 (point, compartment) pairs to evaluate in one call");
@@ -668,10 +670,13 @@ int nm_set_surfaces(nm_ctx* c, const double* xyz, std::size_t nv, const std::uin
     NM_CUDA(cudaSetDevice(c->opt.device));
     const bool verbose = std::getenv("NM_CELL_VERBOSE") != nullptr;
     auto t_prev = std::chrono::steady_clock::now();
+    c->surf_t0 = t_prev;
     auto lap = [&](const char* what) {
       if (!verbose) return;
       const auto t = std::chrono::steady_clock::now();
-      std::fprintf(stderr, "[surfaces] %-8s %8.1f ms\n", what, std::chrono::duration<double, std::milli>(t - t_prev).count());
+      std::fprintf(stderr, "[surfaces] %-10s %8.1f ms  (at %6.1f)\n", what,
+                   std::chrono::duration<double, std::milli>(t - t_prev).count(),
+                   std::chrono::duration<double, std::milli>(t - c->surf_t0).count());
       t_prev = t;
     };
     // Domain box and centring offset of the fp32 frame.
@@ -689,6 +694,7 @@ int nm_set_surfaces(nm_ctx* c, const double* xyz, std::size_t nv, const std::uin
     c->cx = ctr[0];
     c->cy = ctr[1];
     c->cz = ctr[2];
+    lap("box");
 
     c->has_surfaces = false;
     c->cells = false;
@@ -696,12 +702,15 @@ int nm_set_surfaces(nm_ctx* c, const double* xyz, std::size_t nv, const std::uin
     // fp64 originals (fix-up, cell certification) and the 13-DOP of every
     // compartment first: the certified-cell build (cull_outside = 2) starts on
     // its own host thread and stream while the tiles are packed below.
-    auto up_on = [&](DBuf& b, const void* src, std::size_t bytes, cudaStream_t st) {
-      void* d = b.get(bytes);
-      if (bytes) NM_CUDA(cudaMemcpyAsync(d, src, bytes, cudaMemcpyHostToDevice, st));
+    auto up_on = [&](DBuf& b, const void* src, std::size_t bytes, cudaStream_t st) {  // pinned chunk staging
+      void* d = b.get(std::max<std::size_t>(bytes, 1));
+      c->h2d(d, src, bytes, st);
     };
+    c->trace("main", "up64 start");
     up_on(c->xyz64, xyz, nv * 3 * sizeof(double), c->side);
+    c->trace("main", "xyz64 staged");
     up_on(c->tri_idx, tri, nt * 3 * sizeof(std::uint32_t), c->side);
+    c->trace("main", "tri_idx staged");
     up_on(c->comp_off, comp_off, (K + 1) * sizeof(std::uint32_t), c->side);
     // de-indexed fp64 triangles (72 B each, file order) for the fix-up
     {
@@ -711,13 +720,18 @@ int nm_set_surfaces(nm_ctx* c, const double* xyz, std::size_t nv, const std::uin
             static_cast<const double*>(c->xyz64.p), static_cast<const std::uint32_t*>(c->tri_idx.p), nt, t64);
       NM_CUDA(cudaGetLastError());
     }
+    lap("up64");
     // 13-DOP: slab bounds over the vertices (centred frame), widened by 1e-3 mm
     // + 1e-5 |bound| (covers the fp32 rounding of the point and of the
-    // projection in the kernel) and rounded outward.
+    // projection in the kernel) and rounded outward. On the device
+    // (geometry.cuh): chunks of triangles per block, merged per compartment
+    // (min / max are order-independent); the fp64 extents (the first three
+    // directions are the compartment's box) also size the cell grids.
     std::vector<float4> hbox(static_cast<std::size_t>(K) * nm::kDopF4);
-    // The certified-cell build starts now on its own host thread and stream:
-    // its geometry phase does not need the 13-DOP, which it waits for through
-    // dop_ready (set below, or set with an error if this thread throws first).
+    std::vector<double> hext(static_cast<std::size_t>(K) * nm::kExtQ);
+    // The certified-cell build starts now on its own host thread and stream;
+    // it waits for the extents through dop_ready (set below, or set with an
+    // error if this thread throws first).
     std::promise<void> dop_ready;
     std::unique_ptr<CellBuilder> cells;
     std::exception_ptr cells_err;
@@ -728,7 +742,7 @@ int nm_set_surfaces(nm_ctx* c, const double* xyz, std::size_t nv, const std::uin
       }
     } cells_thread;
     if (c->opt.cull_outside == 2) {
-      cells = make_cell_builder(c, xyz, tri, comp_off, hbox, c->side, dop_ready.get_future().share());
+      cells = make_cell_builder(c, xyz, tri, comp_off, hbox, hext, c->side, dop_ready.get_future().share());
       cells_thread.t = std::thread([&] {
         try {
           cells->prepare();
@@ -737,6 +751,7 @@ int nm_set_surfaces(nm_ctx* c, const double* xyz, std::size_t nv, const std::uin
         }
       });
     }
+    lap("cells-go");
     // declared after the joiner, so destroyed first: on an exception below the
     // cell thread is released (with an error) before it is joined
     struct DopGuard {
@@ -746,55 +761,32 @@ int nm_set_surfaces(nm_ctx* c, const double* xyz, std::size_t nv, const std::uin
         if (!set) p.set_exception(std::make_exception_ptr(Error("13-DOP not computed")));
       }
     } dop_guard{dop_ready};
-    // (one pass over the compartment's triangle corners, all 13 directions
-    // per corner; chunks of triangles on every host thread, merged per
-    // compartment: min/max are order-independent)
     {
-      constexpr std::uint32_t kDopChunk = 16384;
-      std::vector<std::pair<int, std::uint32_t>> items;  // (compartment, first triangle)
-      for (int k = 0; k < K; ++k)
-        for (std::uint32_t t = comp_off[k]; t < comp_off[k + 1]; t += kDopChunk) items.emplace_back(k, t);
-      std::vector<std::array<double, 2 * nm::kDopDirs>> part(items.size());
-      parallel_for(static_cast<int>(items.size()), [&](int i) {
-        const int k = items[i].first;
-        const std::uint32_t t1 = std::min(comp_off[k + 1], items[i].second + kDopChunk);
-        auto& b = part[i];
-        for (int j = 0; j < nm::kDopDirs; ++j) {
-          b[2 * j] = 1e300;
-          b[2 * j + 1] = -1e300;
-        }
-        for (std::uint32_t t = items[i].second; t < t1; ++t)
-          for (int v = 0; v < 3; ++v) {
-            const double* X = xyz + 3 * std::size_t(tri[3 * t + v]);
-            const double d[3] = {X[0] - ctr[0], X[1] - ctr[1], X[2] - ctr[2]};
-            for (int j = 0; j < nm::kDopDirs; ++j) {
-              double pr = 0.0;
-              for (int a = 0; a < 3; ++a) pr += double(nm::dop_dir(j, a)) * d[a];
-              b[2 * j] = std::min(b[2 * j], pr);
-              b[2 * j + 1] = std::max(b[2 * j + 1], pr);
-            }
-          }
-      });
+      constexpr std::uint32_t kExtChunk = 8192;
+      std::vector<nm::ExtentItem> items;
+      std::vector<std::uint32_t> item_first(K + 1, 0);
       for (int k = 0; k < K; ++k) {
-        float* dst = reinterpret_cast<float*>(&hbox[static_cast<std::size_t>(k) * nm::kDopF4]);
-        for (int q = 0; q < 4 * nm::kDopF4; ++q) dst[q] = 0.0f;
-        for (int j = 0; j < nm::kDopDirs; ++j) {
-          double lo = 1e300, hi = -1e300;
-          for (std::size_t i = 0; i < items.size(); ++i)
-            if (items[i].first == k) {
-              lo = std::min(lo, part[i][2 * j]);
-              hi = std::max(hi, part[i][2 * j + 1]);
-            }
-          if (comp_off[k + 1] == comp_off[k]) {  // empty compartment: everything outside
-            dst[2 * j] = 1e30f;
-            dst[2 * j + 1] = -1e30f;
-            continue;
-          }
-          const double m = 1e-3 + 1e-5 * std::max(std::fabs(lo), std::fabs(hi));
-          dst[2 * j] = std::nextafter(float(lo - m), -INFINITY);
-          dst[2 * j + 1] = std::nextafter(float(hi + m), INFINITY);
-        }
+        item_first[k] = static_cast<std::uint32_t>(items.size());
+        for (std::uint32_t t = comp_off[k]; t < comp_off[k + 1]; t += kExtChunk)
+          items.push_back({k, t, std::min(comp_off[k + 1], t + kExtChunk)});
       }
+      item_first[K] = static_cast<std::uint32_t>(items.size());
+      auto* d_items = c->ext_items.as<nm::ExtentItem>(std::max<std::size_t>(items.size(), 1));
+      auto* d_first = c->ext_first.as<std::uint32_t>(K + 1);
+      auto* d_part = c->ext_part.as<double>(std::max<std::size_t>(items.size(), 1) * nm::kExtQ);
+      auto* d_ext = c->ext_val.as<double>(static_cast<std::size_t>(K) * nm::kExtQ);
+      auto* d_box = c->comp_box.as<float4>(static_cast<std::size_t>(K) * nm::kDopF4);
+      c->h2d(d_items, items.data(), items.size() * sizeof(nm::ExtentItem), c->side);
+      c->h2d(d_first, item_first.data(), item_first.size() * sizeof(std::uint32_t), c->side);
+      if (!items.empty())
+        nm::k_extents_items<<<static_cast<unsigned>(items.size()), 256, 0, c->side>>>(
+            d_items, static_cast<const double*>(c->xyz64.p), static_cast<const std::uint32_t*>(c->tri_idx.p), ctr[0],
+            ctr[1], ctr[2], d_part);
+      nm::k_extents_finalize<<<K, 32, 0, c->side>>>(d_part, d_first, static_cast<const std::uint32_t*>(c->comp_off.p),
+                                                    d_ext, d_box);
+      NM_CUDA(cudaGetLastError());
+      c->d2h(hext.data(), d_ext, hext.size() * sizeof(double), c->side);
+      c->d2h(hbox.data(), d_box, hbox.size() * sizeof(float4), c->side);
     }
     dop_ready.set_value();
     dop_guard.set = true;
@@ -1137,13 +1129,16 @@ int nm_set_surfaces(nm_ctx* c, const double* xyz, std::size_t nv, const std::uin
     c->strips = use_strips;
     auto up = [&](DBuf& b, const void* src, std::size_t bytes) {  // pinned chunk staging (recycled chunks)
       void* d = b.get(std::max<std::size_t>(bytes, 1));
+      c->trace("main", "  alloc");
       c->h2d(d, src, bytes, c->stream);
+      c->trace("main", "  staged");
     };
     up(c->tri, htri.get(), htri_n * sizeof(float4));
+    lap("up-tri");
     up(c->sub, hsub.get(), hsub_n * sizeof(float4));
     up(c->cont, hcont.data(), hcont.size() * sizeof(std::uint32_t));
     up(c->comp_tiles, tiles.data(), tiles.size() * sizeof(std::uint32_t));
-    up(c->comp_box, hbox.data(), hbox.size() * sizeof(float4));
+    // (comp_box: written on the device by k_extents_finalize)
     NM_CUDA(cudaStreamSynchronize(c->stream));
     lap("upload");
     if (cells_thread.t.joinable()) cells_thread.t.join();

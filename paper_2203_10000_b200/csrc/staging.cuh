@@ -8,7 +8,10 @@
 // host copies done by a small persistent thread pool, each chunk's DMA
 // overlapping the host copy of the next one.
 #pragma once
+#include <chrono>
 #include <condition_variable>
+#include <cstdio>
+#include <cstdlib>
 #include <cstddef>
 #include <cstring>
 #include <functional>
@@ -153,33 +156,51 @@ class Stager {
 
   // Enqueue dst_dev <- src_host on st. On return the caller's buffer has been
   // read completely (it may be freed or reused); the DMA may still run.
+  // Pageable buffers of ANY size go through the pinned chunks: a pageable
+  // cudaMemcpyAsync is staged by the driver synchronously, and from a second
+  // host thread it was seen to wait for the other thread's queued kernels
+  // (nm_set_surfaces: tile upload beside the certified-cell build).
   void h2d(void* dst, const void* src, std::size_t bytes, cudaStream_t st, CopyPool& pool) {
     if (!bytes) return;
-    if (bytes <= kChunk / 4 || host_pinned(src)) {
+    if (host_pinned(src)) {
       check(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st));
-      if (!host_pinned(src)) check(cudaStreamSynchronize(st));  // small pageable copy: the driver staged it
       return;
     }
+    const auto t0 = std::chrono::steady_clock::now();
     init();
+    const auto t1 = std::chrono::steady_clock::now();
+    double t_ev = 0, t_cp = 0, t_dma = 0;
+    auto msd = [](std::chrono::steady_clock::time_point a, std::chrono::steady_clock::time_point b) {
+      return std::chrono::duration<double, std::milli>(b - a).count();
+    };
     nvtxRangePushA("nm staged h2d");
     const auto* s = static_cast<const char*>(src);
     auto* d = static_cast<char*>(dst);
     for (std::size_t off = 0, i = 0; off < bytes; off += kChunk, ++i) {
       const int b = static_cast<int>(i % kBufs);
       const std::size_t len = std::min(kChunk, bytes - off);
+      const auto a0 = std::chrono::steady_clock::now();
       check(cudaEventSynchronize(ev_[b]));  // the buffer's previous DMA is done
+      const auto a1 = std::chrono::steady_clock::now();
       pool.copy(pin_[b], s + off, len);
+      const auto a2 = std::chrono::steady_clock::now();
       check(cudaMemcpyAsync(d + off, pin_[b], len, cudaMemcpyHostToDevice, st));
       check(cudaEventRecord(ev_[b], st));
+      t_ev += msd(a0, a1);
+      t_cp += msd(a1, a2);
+      t_dma += msd(a2, std::chrono::steady_clock::now());
     }
     nvtxRangePop();
+    if (trace_on())
+      std::fprintf(stderr, "      [stager] h2d %9zu B: init %.2f, event waits %.2f, host copies %.2f, dma enqueue %.2f ms\n",
+                   bytes, msd(t0, t1), t_ev, t_cp, t_dma);
   }
 
   // dst_host <- src_dev after the work already enqueued on st; returns when
   // the caller's buffer holds the data.
   void d2h(void* dst, const void* src, std::size_t bytes, cudaStream_t st, CopyPool& pool) {
     if (!bytes) return;
-    if (bytes <= kChunk / 4 || host_pinned(dst)) {
+    if (host_pinned(dst)) {
       check(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st));
       check(cudaStreamSynchronize(st));
       return;
@@ -226,6 +247,13 @@ class Stager {
       pin_[b] = PinnedChunks::get().acquire(kChunk);
       check(cudaEventCreateWithFlags(&ev_[b], cudaEventDisableTiming));
     }
+  }
+  static bool trace_on() {
+    static const bool on = [] {
+      const char* v = std::getenv("NM_CELL_VERBOSE");
+      return v && std::atoi(v) >= 3;
+    }();
+    return on;
   }
   void* pin_[kBufs] = {};
   cudaEvent_t ev_[kBufs] = {};

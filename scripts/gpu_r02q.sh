@@ -1,0 +1,12 @@
+#!/bin/bash
+# cooperative certification kernels + staged cell-build copies: cell tests, set_surfaces phases, launch list
+cd "$GRAFT_REPO_ROOT"
+O=gpurun_out/r02q
+mkdir -p $O
+timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -m gpu -k "cell or cull" > $O/pytest_cells.log 2>&1
+echo "pytest exit $?" >> $O/pytest_cells.log
+NM_CELL_VERBOSE=1 python scripts/surf_quick.py 5 4 > $O/surf_cfg5.txt 2>&1
+python scripts/surf_quick.py 3 2 > $O/surf_cfg3.txt 2>&1
+ncu --metrics gpu__time_duration.sum --clock-control none -c 200 --csv --log-file $O/launches_surf.csv \
+    python scripts/surf_quick.py 5 1 > $O/ncu_launches.log 2>&1
+ls -la $O
