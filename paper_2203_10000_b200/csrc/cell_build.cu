@@ -189,9 +189,12 @@ class CellBuild : public CellBuilder {
                   " MB) exceed the 8 GB build budget: lower nm_options.cell_axis");
     const std::size_t ncl = coff_[K];
     const std::uint32_t nt = comp_off_[K];
-    std::vector<std::uint32_t> coff(K + 1);
+    std::vector<std::uint32_t> coff(2 * (K + 1), 0);  // cluster offsets, then supercluster offsets
     for (int k = 0; k <= K; ++k) coff[k] = static_cast<std::uint32_t>(coff_[k]);
+    for (int k = 0; k < K; ++k) coff[K + 1 + k + 1] = coff[K + 1 + k] + (coff[k + 1] - coff[k] + 31) / 32;
+    const std::uint32_t nsup = coff[2 * K + 1];
     up(c_->cert_coff, coff.data(), coff.size() * sizeof(std::uint32_t));
+    auto* sup = c_->clus_sup.as<float4>(std::max<std::uint32_t>(nsup, 1));
     c_->trace("cells", "geo: coff up");
     auto* clus = c_->clus.as<float4>(std::max<std::size_t>(ncl, 1));
     auto* ctri = c_->clus_tri.as<std::uint32_t>(std::max<std::size_t>(ncl, 1) * nm::kCluster);
@@ -217,6 +220,9 @@ class CellBuild : public CellBuilder {
       nm::k_cluster_spheres<<<static_cast<unsigned>((ncl * 32 + 255) / 256), 256, 0, st_>>>(
           xyz, tri, coffd, static_cast<const std::uint32_t*>(c_->cert_coff.p), K, static_cast<std::uint32_t>(ncl),
           ctr_[0], ctr_[1], ctr_[2], vals2, clus, ctri, tsph);
+      const auto* coffd2 = static_cast<const std::uint32_t*>(c_->cert_coff.p);
+      nm::k_super_spheres<<<static_cast<unsigned>((std::size_t(nsup) * 32 + 255) / 256), 256, 0, st_>>>(
+          clus, coffd2, coffd2 + K + 1, K, nsup, sup);
       NM_CUDA(cudaGetLastError());
       c_->trace("cells", "geo: launched");
     }
@@ -437,6 +443,8 @@ class CellBuild : public CellBuilder {
     p.grids = static_cast<const nm::CellGrid*>(c_->cell_grids.p);
     p.K = K_;
     p.coff = static_cast<const std::uint32_t*>(c_->cert_coff.p);
+    p.soff = p.coff + K_ + 1;
+    p.sup = static_cast<const float4*>(c_->clus_sup.p);
     p.clus = static_cast<const float4*>(c_->clus.p);
     p.clus_tri = static_cast<const std::uint32_t*>(c_->clus_tri.p);
     p.tsph = static_cast<const float4*>(c_->clus_tsph.p);
@@ -445,6 +453,33 @@ class CellBuild : public CellBuilder {
     p.cx = c_->cx;
     p.cy = c_->cy;
     p.cz = c_->cz;
+    return p;
+  }
+
+  nm::L1Params l1_params(std::size_t max_runs) {
+    nm::L1Params p{};
+    p.grids = static_cast<const nm::CellGrid*>(c_->cell_grids.p);
+    p.K = K_;
+    p.row_first = static_cast<const std::uint32_t*>(c_->row_first.p);
+    p.cert = static_cast<const std::uint8_t*>(c_->cell_cert.p);
+    p.dop4 = static_cast<const float4*>(c_->comp_box.p);
+    p.rowruns = c_->l1_rowruns.as<std::uint32_t>(std::max<std::uint32_t>(nrows_, 1));
+    p.runfirst = c_->l1_runfirst.as<std::uint32_t>(std::max<std::uint32_t>(nrows_, 1));
+    p.cellrun = c_->l1_cellrun.as<std::int32_t>(std::max<std::size_t>(total_, 1));
+    p.parent = c_->l1_parent.as<std::uint32_t>(max_runs);
+    p.runrow = c_->l1_runrow.as<std::uint32_t>(max_runs);
+    p.runx = c_->l1_runx.as<std::uint32_t>(max_runs);
+    p.zero = c_->l1_zero.as<std::uint32_t>(max_runs);
+    p.rootval = c_->l1_rootval.as<std::int32_t>(max_runs);
+    p.cellval = static_cast<std::int32_t*>(c_->cell_val.p);
+    p.nruns = c_->l1_nruns.as<std::uint32_t>(1);
+    p.rep_cursor = static_cast<unsigned*>(c_->rep_cur.p);
+    p.rep_first = static_cast<const unsigned*>(c_->rep_cur.p) + 32;
+    p.rep_pts = static_cast<double*>(c_->rep_pts.p);
+    p.ctr0 = ctr_[0];
+    p.ctr1 = ctr_[1];
+    p.ctr2 = ctr_[2];
+    p.fill = 0;
     return p;
   }
 
@@ -489,8 +524,30 @@ class CellBuild : public CellBuilder {
       nreps_ = 0;
       return;
     }
-    // count pass: representatives per compartment
-    nm::k_runs_l1<<<grid_for(nrows_, 128, c_->sm_count * 16), 128, 0, st_>>>(run_params(false), nrows_);
+    // level-1 runs -> components (cells.cuh k_l1_*): numbered, united, one
+    // representative per component; per-run arrays sized for the most runs a
+    // row can hold (no host synchronisation before the counts below)
+    std::size_t max_runs = 0;
+    for (int k = 0; k < K; ++k)
+      if (cells(k)) max_runs += static_cast<std::size_t>(G_[k].ny) * G_[k].nz * ((G_[k].nx + 1) / 2);
+    nm::L1Params lp = l1_params(std::max<std::size_t>(max_runs, 1));
+    const unsigned gr = grid_for(nrows_, 128, c_->sm_count * 16), grr = grid_for(max_runs, 256, c_->sm_count * 16);
+    nm::k_l1_count<<<gr, 128, 0, st_>>>(lp, nrows_);
+    {
+      std::size_t tmp = 0;
+      NM_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, lp.rowruns, const_cast<std::uint32_t*>(lp.runfirst),
+                                            static_cast<int>(nrows_), st_));
+      void* t = c_->cub_tmp2.get(tmp);
+      NM_CUDA(cub::DeviceScan::ExclusiveSum(t, tmp, lp.rowruns, const_cast<std::uint32_t*>(lp.runfirst),
+                                            static_cast<int>(nrows_), st_));
+    }
+    nm::k_l1_total<<<1, 1, 0, st_>>>(lp, nrows_);
+    nm::k_l1_label<<<gr, 128, 0, st_>>>(lp, nrows_);
+    nm::k_l1_union<<<gr, 128, 0, st_>>>(lp, nrows_);
+    nm::k_l1_flatten<<<grr, 256, 0, st_>>>(lp);
+    nm::k_l1_zero<<<grr, 256, 0, st_>>>(lp);
+    // count pass: representatives per compartment (components, fine runs)
+    nm::k_l1_roots<<<grr, 256, 0, st_>>>(lp);
     nm::k_runs_fine<<<grid_for(std::size_t(nrows_) * 16, 128, c_->sm_count * 16), 128, 0, st_>>>(run_params(false),
                                                                                                    nrows_);
     NM_CUDA(cudaGetLastError());
@@ -510,7 +567,10 @@ class CellBuild : public CellBuilder {
     if (nchild_) NM_CUDA(cudaMemsetAsync(c_->child_val.p, 0xff, nchild_ * sizeof(std::int32_t), st_));
     // fill pass: values, representative points (level-1 values first: the
     // fine runs copy their neighbour parents')
-    nm::k_runs_l1<<<grid_for(nrows_, 128, c_->sm_count * 16), 128, 0, st_>>>(run_params(true), nrows_);
+    lp = l1_params(std::max<std::size_t>(max_runs, 1));
+    lp.fill = 1;
+    nm::k_l1_roots<<<grr, 256, 0, st_>>>(lp);
+    nm::k_l1_cellval<<<gr, 128, 0, st_>>>(lp, nrows_);
     nm::k_runs_fine<<<grid_for(std::size_t(nrows_) * 16, 128, c_->sm_count * 16), 128, 0, st_>>>(run_params(true),
                                                                                                    nrows_);
     NM_CUDA(cudaGetLastError());
@@ -621,8 +681,67 @@ class CellBuild : public CellBuilder {
         reps_[k].insert(reps_[k].end(), part[i].reps.begin(), part[i].reps.end());
         run_val_[k].insert(run_val_[k].end(), part[i].run_val.begin(), part[i].run_val.end());
       }
+      components(k);
     });
     lap("merge");
+  }
+
+  // Level-1 runs of compartment k joined into components (the rule of
+  // cells.cuh k_l1_*): runs touching through a face in the rows y + 1 / z + 1
+  // share their winding number; a component with a 0 run is 0, any other
+  // keeps only its smallest run's representative. Representatives no run
+  // refers to any more are dropped (the fine runs keep theirs).
+  void components(int k) {
+    const nm::CellGrid& g = G_[k];
+    std::vector<std::int64_t>& rv = run_val_[k];
+    const std::size_t R = rv.size();
+    if (!R) return;
+    std::vector<std::uint32_t> par(R);
+    std::iota(par.begin(), par.end(), 0u);
+    auto find = [&](std::uint32_t x) {
+      while (par[x] != x) x = par[x] = par[par[x]];
+      return x;
+    };
+    for (int iz = 0; iz < g.nz; ++iz)
+      for (int iy = 0; iy < g.ny; ++iy)
+        for (int ix = 0; ix < g.nx; ++ix) {
+          const std::size_t q = g.off + (static_cast<std::size_t>(iz) * g.ny + iy) * g.nx + ix;
+          if (!cert1_[q]) continue;
+          const std::size_t nb[2] = {iy + 1 < g.ny ? q + g.nx : 0, iz + 1 < g.nz ? q + std::size_t(g.nx) * g.ny : 0};
+          for (std::size_t n : nb) {
+            if (!n || !cert1_[n]) continue;
+            std::uint32_t a = find(static_cast<std::uint32_t>(run_of_[q])), b = find(static_cast<std::uint32_t>(run_of_[n]));
+            if (a != b) par[std::max(a, b)] = std::min(a, b);  // the root is the component's smallest run
+          }
+        }
+    std::vector<std::uint8_t> zero(R, 0);
+    for (std::uint32_t r = 0; r < R; ++r)
+      if (rv[r] == 0) zero[find(r)] = 1;
+    for (std::uint32_t r = 0; r < R; ++r) {
+      const std::uint32_t root = find(r);
+      rv[r] = zero[root] ? 0 : rv[root];  // the root's representative (kRep + index)
+    }
+    // compact the representatives: those of the component roots and of the
+    // fine runs, in their old order
+    const std::size_t np = reps_[k].size() / 3;
+    std::vector<std::int64_t> remap(np, -1);
+    for (std::int64_t v : rv)
+      if (v >= kRep && v < kRun) remap[static_cast<std::size_t>(v - kRep)] = 0;
+    for (std::size_t i = slab_first_[k]; i < slab_first_[k + 1]; ++i)
+      for (const FineRun& fr : fine_[i])
+        if (fr.v >= kRep && fr.v < kRun) remap[static_cast<std::size_t>(fr.v - kRep)] = 0;
+    std::vector<double> kept;
+    for (std::size_t j = 0; j < np; ++j)
+      if (remap[j] == 0) {
+        remap[j] = static_cast<std::int64_t>(kept.size() / 3);
+        kept.insert(kept.end(), reps_[k].begin() + 3 * j, reps_[k].begin() + 3 * j + 3);
+      }
+    reps_[k] = std::move(kept);
+    for (std::int64_t& v : rv)
+      if (v >= kRep && v < kRun) v = kRep + remap[static_cast<std::size_t>(v - kRep)];
+    for (std::size_t i = slab_first_[k]; i < slab_first_[k + 1]; ++i)
+      for (FineRun& fr : fine_[i])
+        if (fr.v >= kRep && fr.v < kRun) fr.v = kRep + remap[static_cast<std::size_t>(fr.v - kRep)];
   }
 
   std::int64_t new_rep(SlabRuns& out, double x, double y, double z) {

@@ -172,6 +172,8 @@ struct CertifyParams {
   int K;
   const unsigned long long* first;  // K + 1: first work warp of each compartment
   const std::uint32_t* coff;    // K + 1: first cluster of each compartment
+  const std::uint32_t* soff;    // K + 1: first supercluster (32 clusters) of each compartment
+  const float4* sup;            // supercluster spheres
   const float4* clus;           // cluster spheres (all compartments)
   const std::uint32_t* clus_tri;
   const float4* tsph;
@@ -184,7 +186,11 @@ struct CertifyParams {
 };
 
 static __device__ bool warp_certify_coop(double Ox, double Oy, double Oz, double e, bool active,
-                                         const CertifyParams& p, std::uint32_t c0, int nclus) {
+                                         const CertifyParams& p, int k) {
+  const std::uint32_t c0 = p.coff[k];
+  const int nclus = static_cast<int>(p.coff[k + 1] - c0);
+  const float4* sup = p.sup + p.soff[k];
+  const int nsup = static_cast<int>(p.soff[k + 1] - p.soff[k]);
   const int lane = threadIdx.x & 31;
   const double Cx = Ox + (lane % 4 + 0.5) * e, Cy = Oy + ((lane / 4) % 4 + 0.5) * e, Cz = Oz + (lane / 16 + 0.5) * e;
   const double rb = cell_ball(e);
@@ -209,74 +215,87 @@ static __device__ bool warp_certify_coop(double Ox, double Oy, double Oz, double
   const float4* tsph = p.tsph + static_cast<std::size_t>(c0) * kCluster;
   const V3t<double> pt{Cx + p.cx, Cy + p.cy, Cz + p.cz};
   bool hit = !active;
-  for (int q0 = 0; q0 < nclus; q0 += 32) {
-    bool cand = false;
-    if (q0 + lane < nclus) {
-      const float4 s = __ldg(clus + q0 + lane);
+  // superclusters (32 clusters) meeting the brick's ball, then their clusters
+  for (int g0 = 0; g0 < nsup; g0 += 32) {
+    bool scand = false;
+    if (g0 + lane < nsup) {
+      const float4 s = __ldg(sup + g0 + lane);
       const float dx = bx - s.x, dy = by - s.y, dz = bz - s.z;
       const float R = fbr + s.w;
-      cand = dx * dx + dy * dy + dz * dz <= R * R;
+      scand = dx * dx + dy * dy + dz * dz <= R * R;
     }
-    unsigned bal = __ballot_sync(kFull, cand);
-    while (bal) {
-      const int q = q0 + __ffs(bal) - 1;
-      bal &= bal - 1;
-      // cubes (lanes) still open whose ball meets the cluster sphere
-      bool need = false;
-      if (!hit) {
-        const float4 s = __ldg(clus + q);
-        const float dx = fx - s.x, dy = fy - s.y, dz = fz - s.z;
-        const float R = frb + s.w;
-        need = dx * dx + dy * dy + dz * dz <= R * R;
+    unsigned sbal = __ballot_sync(kFull, scand);
+    while (sbal) {
+      const int q0 = (g0 + __ffs(sbal) - 1) * 32;
+      sbal &= sbal - 1;
+      bool cand = false;
+      if (q0 + lane < nclus) {
+        const float4 s = __ldg(clus + q0 + lane);
+        const float dx = bx - s.x, dy = by - s.y, dz = bz - s.z;
+        const float R = fbr + s.w;
+        cand = dx * dx + dy * dy + dz * dz <= R * R;
       }
-      unsigned needm = __ballot_sync(kFull, need);
-      if (!needm) continue;
-      // lane t: which cubes' balls meet triangle t's sphere (pads: w < 0)
-      const float4 ts = __ldg(tsph + static_cast<std::size_t>(q) * kCluster + lane);
-      unsigned m = 0;
-      if (ts.w >= 0.0f) {
-        const float R = frbm + ts.w, R2 = R * R;
-        float dx2[4], dy2[4], dz2[2];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const float dx = X[i] - ts.x, dy = Y[i] - ts.y;
-          dx2[i] = dx * dx;
-          dy2[i] = dy * dy;
+      unsigned bal = __ballot_sync(kFull, cand);
+      while (bal) {
+        const int q = q0 + __ffs(bal) - 1;
+        bal &= bal - 1;
+        // cubes (lanes) still open whose ball meets the cluster sphere
+        bool need = false;
+        if (!hit) {
+          const float4 s = __ldg(clus + q);
+          const float dx = fx - s.x, dy = fy - s.y, dz = fz - s.z;
+          const float R = frb + s.w;
+          need = dx * dx + dy * dy + dz * dz <= R * R;
         }
-        dz2[0] = (Z[0] - ts.z) * (Z[0] - ts.z);
-        dz2[1] = (Z[1] - ts.z) * (Z[1] - ts.z);
+        unsigned needm = __ballot_sync(kFull, need);
+        if (!needm) continue;
+        // lane t: which cubes' balls meet triangle t's sphere (pads: w < 0)
+        const float4 ts = __ldg(tsph + static_cast<std::size_t>(q) * kCluster + lane);
+        unsigned m = 0;
+        if (ts.w >= 0.0f) {
+          const float R = frbm + ts.w, R2 = R * R;
+          float dx2[4], dy2[4], dz2[2];
 #pragma unroll
-        for (int kz = 0; kz < 2; ++kz)
-#pragma unroll
-          for (int jy = 0; jy < 4; ++jy) {
-            const float yz = dy2[jy] + dz2[kz];
-#pragma unroll
-            for (int ix = 0; ix < 4; ++ix) m |= (yz + dx2[ix] <= R2 ? 1u : 0u) << (ix + 4 * jy + 16 * kz);
+          for (int i = 0; i < 4; ++i) {
+            const float dx = X[i] - ts.x, dy = Y[i] - ts.y;
+            dx2[i] = dx * dx;
+            dy2[i] = dy * dy;
           }
-      }
-      m &= needm;
-      // transpose the 32 x 32 bit matrix (row t = triangle t's cube mask) so
-      // that lane L holds cube L's candidate triangles: five block-swap stages
-      unsigned mine = m;
+          dz2[0] = (Z[0] - ts.z) * (Z[0] - ts.z);
+          dz2[1] = (Z[1] - ts.z) * (Z[1] - ts.z);
 #pragma unroll
-      for (int j = 16; j > 0; j >>= 1) {
-        const unsigned M = j == 16 ? 0x0000ffffu : j == 8 ? 0x00ff00ffu : j == 4 ? 0x0f0f0f0fu : j == 2 ? 0x33333333u : 0x55555555u;
-        const unsigned o = __shfl_xor_sync(kFull, mine, j);
-        mine = (lane & j) ? ((mine & ~M) | ((o >> j) & M)) : ((mine & M) | ((o & M) << j));
+          for (int kz = 0; kz < 2; ++kz)
+#pragma unroll
+            for (int jy = 0; jy < 4; ++jy) {
+              const float yz = dy2[jy] + dz2[kz];
+#pragma unroll
+              for (int ix = 0; ix < 4; ++ix) m |= (yz + dx2[ix] <= R2 ? 1u : 0u) << (ix + 4 * jy + 16 * kz);
+            }
+        }
+        m &= needm;
+        // transpose the 32 x 32 bit matrix (row t = triangle t's cube mask) so
+        // that lane L holds cube L's candidate triangles: five block-swap stages
+        unsigned mine = m;
+#pragma unroll
+        for (int j = 16; j > 0; j >>= 1) {
+          const unsigned M = j == 16 ? 0x0000ffffu : j == 8 ? 0x00ff00ffu : j == 4 ? 0x0f0f0f0fu : j == 2 ? 0x33333333u : 0x55555555u;
+          const unsigned o = __shfl_xor_sync(kFull, mine, j);
+          mine = (lane & j) ? ((mine & ~M) | ((o >> j) & M)) : ((mine & M) | ((o & M) << j));
+        }
+        while (mine && !hit) {
+          const int t = __ffs(mine) - 1;
+          mine &= mine - 1;
+          const std::uint32_t tid = __ldg(ctri + static_cast<std::size_t>(q) * kCluster + t);
+          const std::uint32_t* ev = p.tri + 3 * static_cast<std::size_t>(tid);
+          const double* A = p.xyz + 3 * static_cast<std::size_t>(ev[0]);
+          const double* Bv = p.xyz + 3 * static_cast<std::size_t>(ev[1]);
+          const double* Cv = p.xyz + 3 * static_cast<std::size_t>(ev[2]);
+          const double d2 = point_tri_dist2<double>(pt, {A[0], A[1], A[2]}, {Bv[0], Bv[1], Bv[2]}, {Cv[0], Cv[1], Cv[2]});
+          hit = !(d2 > rb * rb);  // NaN (degenerate) counts as a hit
+        }
       }
-      while (mine && !hit) {
-        const int t = __ffs(mine) - 1;
-        mine &= mine - 1;
-        const std::uint32_t tid = __ldg(ctri + static_cast<std::size_t>(q) * kCluster + t);
-        const std::uint32_t* ev = p.tri + 3 * static_cast<std::size_t>(tid);
-        const double* A = p.xyz + 3 * static_cast<std::size_t>(ev[0]);
-        const double* Bv = p.xyz + 3 * static_cast<std::size_t>(ev[1]);
-        const double* Cv = p.xyz + 3 * static_cast<std::size_t>(ev[2]);
-        const double d2 = point_tri_dist2<double>(pt, {A[0], A[1], A[2]}, {Bv[0], Bv[1], Bv[2]}, {Cv[0], Cv[1], Cv[2]});
-        hit = !(d2 > rb * rb);  // NaN (degenerate) counts as a hit
-      }
+      if (__all_sync(kFull, hit)) return hit;
     }
-    if (__all_sync(kFull, hit)) break;
   }
   return hit;
 }
@@ -300,8 +319,7 @@ static __global__ void __launch_bounds__(256) k_cell_certify_all(const CertifyPa
             k0 = static_cast<int>(lw / (static_cast<unsigned long long>(bx) * by)) * 2;
   const int ix = i0 + lane % 4, iy = j0 + (lane / 4) % 4, iz = k0 + lane / 16;
   const bool active = ix < g.nx && iy < g.ny && iz < g.nz;
-  const bool hit = warp_certify_coop(g.ox + i0 * g.B, g.oy + j0 * g.B, g.oz + k0 * g.B, g.B, active, p, p.coff[k],
-                                     static_cast<int>(p.coff[k + 1] - p.coff[k]));
+  const bool hit = warp_certify_coop(g.ox + i0 * g.B, g.oy + j0 * g.B, g.oz + k0 * g.B, g.B, active, p, k);
   if (active) p.out[g.off + (static_cast<std::size_t>(iz) * g.ny + iy) * g.nx + ix] = hit ? 0 : 1;
 }
 
@@ -319,8 +337,7 @@ static __global__ void __launch_bounds__(256) k_child_certify_all(const CertifyP
   const int iy = static_cast<int>((cell / g.nx) % g.ny);
   const int iz = static_cast<int>(cell / (static_cast<std::uint32_t>(g.nx) * g.ny));
   const double e = g.B / kSubCells;
-  const bool hit = warp_certify_coop(g.ox + ix * g.B, g.oy + iy * g.B, g.oz + iz * g.B + 2 * half * e, e, true, p,
-                                     p.coff[k], static_cast<int>(p.coff[k + 1] - p.coff[k]));
+  const bool hit = warp_certify_coop(g.ox + ix * g.B, g.oy + iy * g.B, g.oz + iz * g.B + 2 * half * e, e, true, p, k);
   p.out[b * kChildren + (2 * half + lane / 16) * 16 + lane % 16] = hit ? 0 : 1;
 }
 
@@ -465,30 +482,194 @@ __device__ __forceinline__ int row_compartment(const RunParams& p, std::uint32_t
   return k;
 }
 
-static __global__ void k_runs_l1(const RunParams p, std::uint32_t nrows) {
+// ---- level-1 runs as one connected component per surface-free region ----
+// Face-adjacent certified cells have overlapping balls, so all certified
+// cells connected through faces lie in one surface-free connected set and
+// share one winding number. The x-runs of every row are numbered (row-major,
+// so within a compartment in the host restatement's order) and united with
+// the runs they touch in the rows y + 1 and z + 1 (lock-free union-find,
+// larger root hooked under the smaller: the root is the component's smallest
+// run). A component with a run that ends at the grid edge or outside the
+// 13-DOP is 0; any other component gets ONE representative, at its root
+// run's middle cell. (Round 1 gave every run its own representative.)
+struct L1Params {
+  const CellGrid* grids;
+  int K;
+  const std::uint32_t* row_first;  // K + 1: first global row of each compartment
+  const std::uint8_t* cert;        // per cell: 1 certified
+  const float4* dop4;
+  std::uint32_t* rowruns;          // per row: number of certified runs (count pass)
+  const std::uint32_t* runfirst;   // per row: first run id (exclusive scan of rowruns)
+  std::int32_t* cellrun;           // per certified cell: its run id
+  std::uint32_t* parent;           // per run: union-find parent (flattened: the root)
+  std::uint32_t* runrow;           // per run: its row
+  std::uint32_t* runx;             // per run: ix0 | ix1 << 16
+  std::uint32_t* zero;             // per run: 1 = 0 known (edge / 13-DOP); per root after k_l1_flatten: the component's
+  std::int32_t* rootval;           // per root run: 0, or 2 + representative slot
+  std::int32_t* cellval;           // per cell (k_l1_cellval)
+  std::uint32_t* nruns;            // total runs (k_l1_total)
+  unsigned* rep_cursor;            // K per-compartment counters
+  const unsigned* rep_first;       // K slot bases (fill)
+  double* rep_pts;
+  double ctr0, ctr1, ctr2;
+  int fill;
+};
+
+struct RowPos {
+  int k, iy, iz;
+  std::size_t row;  // global index of the row's cell ix = 0
+};
+
+__device__ __forceinline__ RowPos row_pos(const CellGrid* grids, const std::uint32_t* row_first, int K, std::uint32_t r) {
+  int k = 0;
+  while (k + 1 < K && r >= row_first[k + 1]) ++k;
+  const CellGrid& g = grids[k];
+  const std::uint32_t lr = r - row_first[k];
+  RowPos q;
+  q.k = k;
+  q.iy = static_cast<int>(lr % static_cast<std::uint32_t>(g.ny));
+  q.iz = static_cast<int>(lr / g.ny);
+  q.row = g.off + (static_cast<std::size_t>(q.iz) * g.ny + q.iy) * g.nx;
+  return q;
+}
+
+static __global__ void k_l1_count(const L1Params p, std::uint32_t nrows) {
   for (std::uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < nrows; r += gridDim.x * blockDim.x) {
-    const int k = row_compartment(p, r);
-    const CellGrid g = p.grids[k];
-    const std::uint32_t lr = r - p.row_first[k];
-    const int iy = static_cast<int>(lr % static_cast<std::uint32_t>(g.ny)), iz = static_cast<int>(lr / g.ny);
-    const std::size_t row = g.off + (static_cast<std::size_t>(iz) * g.ny + iy) * g.nx;
-    const double y = __dadd_rn(g.oy, __dmul_rn(iy + 0.5, g.B)), z = __dadd_rn(g.oz, __dmul_rn(iz + 0.5, g.B));
+    const RowPos q = row_pos(p.grids, p.row_first, p.K, r);
+    const int nx = p.grids[q.k].nx;
+    std::uint32_t n = 0;
+    bool prev = false;
+    for (int ix = 0; ix < nx; ++ix) {
+      const bool c = p.cert[q.row + ix] != 0;
+      n += c && !prev;
+      prev = c;
+    }
+    p.rowruns[r] = n;
+  }
+}
+
+static __global__ void k_l1_label(const L1Params p, std::uint32_t nrows) {
+  for (std::uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < nrows; r += gridDim.x * blockDim.x) {
+    const RowPos q = row_pos(p.grids, p.row_first, p.K, r);
+    const CellGrid g = p.grids[q.k];
+    const double y = __dadd_rn(g.oy, __dmul_rn(q.iy + 0.5, g.B)), z = __dadd_rn(g.oz, __dmul_rn(q.iz + 0.5, g.B));
+    std::uint32_t id = p.runfirst[r];
     for (int ix = 0; ix < g.nx;) {
-      const bool c1 = p.cert[row + ix] != 0;
+      const bool c1 = p.cert[q.row + ix] != 0;
       int jx = ix;
-      while (jx + 1 < g.nx && (p.cert[row + jx + 1] != 0) == c1) ++jx;
+      while (jx + 1 < g.nx && (p.cert[q.row + jx + 1] != 0) == c1) ++jx;
       if (c1) {
-        std::int32_t v;
-        if (ix == 0 || jx == g.nx - 1 || outside_dop_rn(p.dop4, k, __dadd_rn(g.ox, __dmul_rn(ix + 0.5, g.B)), y, z) ||
-            outside_dop_rn(p.dop4, k, __dadd_rn(g.ox, __dmul_rn(jx + 0.5, g.B)), y, z))
-          v = 0;
-        else
-          v = new_rep(p, k, __dadd_rn(g.ox, __dmul_rn((ix + jx) / 2 + 0.5, g.B)), y, z);
-        if (p.fill)
-          for (int q = ix; q <= jx; ++q) p.cellval[row + q] = v;
+        const bool z0 = ix == 0 || jx == g.nx - 1 ||
+                        outside_dop_rn(p.dop4, q.k, __dadd_rn(g.ox, __dmul_rn(ix + 0.5, g.B)), y, z) ||
+                        outside_dop_rn(p.dop4, q.k, __dadd_rn(g.ox, __dmul_rn(jx + 0.5, g.B)), y, z);
+        p.zero[id] = z0 ? 1u : 0u;
+        p.parent[id] = id;
+        p.runrow[id] = r;
+        p.runx[id] = static_cast<std::uint32_t>(ix) | (static_cast<std::uint32_t>(jx) << 16);
+        for (int x = ix; x <= jx; ++x) p.cellrun[q.row + x] = static_cast<std::int32_t>(id);
+        ++id;
       }
       ix = jx + 1;
     }
+  }
+}
+
+__device__ __forceinline__ std::uint32_t uf_find(std::uint32_t* parent, std::uint32_t x) {
+  for (;;) {
+    const std::uint32_t px = __ldcg(parent + x);
+    if (px == x) return x;
+    const std::uint32_t gp = __ldcg(parent + px);
+    if (gp != px) parent[x] = gp;  // path halving (only ever points closer to the root)
+    x = px;
+  }
+}
+
+__device__ __forceinline__ void uf_unite(std::uint32_t* parent, std::uint32_t a, std::uint32_t b) {
+  for (;;) {
+    a = uf_find(parent, a);
+    b = uf_find(parent, b);
+    if (a == b) return;
+    if (a > b) {
+      const std::uint32_t t = a;
+      a = b;
+      b = t;
+    }
+    const std::uint32_t old = atomicCAS(parent + b, b, a);  // hook the larger root under the smaller
+    if (old == b) return;
+    b = old;
+  }
+}
+
+// runs of row r with the runs they touch in the rows y + 1 and z + 1
+static __global__ void k_l1_union(const L1Params p, std::uint32_t nrows) {
+  for (std::uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < nrows; r += gridDim.x * blockDim.x) {
+    const RowPos q = row_pos(p.grids, p.row_first, p.K, r);
+    const CellGrid& g = p.grids[q.k];
+    const std::size_t dn[2] = {static_cast<std::size_t>(g.nx), static_cast<std::size_t>(g.nx) * g.ny};
+    const bool has[2] = {q.iy + 1 < g.ny, q.iz + 1 < g.nz};
+    for (int ix = 0; ix < g.nx; ++ix) {
+      const std::size_t c = q.row + ix;
+      if (!p.cert[c]) continue;
+      const std::uint32_t a = static_cast<std::uint32_t>(p.cellrun[c]);
+      for (int d = 0; d < 2; ++d) {
+        if (!has[d]) continue;
+        const std::size_t n = c + dn[d];
+        if (!p.cert[n]) continue;
+        const std::int32_t b = p.cellrun[n];
+        if (ix > 0 && p.cert[c - 1] && p.cert[n - 1] && p.cellrun[n - 1] == b) continue;  // same pair as at ix - 1
+        uf_unite(p.parent, a, static_cast<std::uint32_t>(b));
+      }
+    }
+  }
+}
+
+static __global__ void k_l1_total(const L1Params p, std::uint32_t nrows) {
+  *p.nruns = nrows ? p.runfirst[nrows - 1] + p.rowruns[nrows - 1] : 0u;
+}
+
+// parent = root; a component with a known-0 run is 0
+static __global__ void k_l1_flatten(const L1Params p) {
+  const std::uint32_t nruns = *p.nruns;
+  for (std::uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nruns; i += gridDim.x * blockDim.x) {
+    const std::uint32_t root = uf_find(p.parent, i);
+    p.parent[i] = root;
+  }
+}
+static __global__ void k_l1_zero(const L1Params p) {
+  const std::uint32_t nruns = *p.nruns;
+  for (std::uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nruns; i += gridDim.x * blockDim.x)
+    if (p.zero[i] && p.parent[i] != i) atomicOr(p.zero + p.parent[i], 1u);
+}
+
+// one representative per non-zero component, at its root run's middle cell
+// (count pass: per-compartment counts; fill: slot, point, rootval)
+static __global__ void k_l1_roots(const L1Params p) {
+  const std::uint32_t nruns = *p.nruns;
+  for (std::uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nruns; i += gridDim.x * blockDim.x) {
+    if (p.parent[i] != i) continue;
+    if (p.zero[i]) {
+      if (p.fill) p.rootval[i] = 0;
+      continue;
+    }
+    const RowPos q = row_pos(p.grids, p.row_first, p.K, p.runrow[i]);
+    const unsigned slot = atomicAdd(p.rep_cursor + q.k, 1u);
+    if (!p.fill) continue;
+    const CellGrid g = p.grids[q.k];
+    const int ix = static_cast<int>(p.runx[i] & 0xffffu), jx = static_cast<int>(p.runx[i] >> 16);
+    const unsigned rr = p.rep_first[q.k] + slot;
+    p.rep_pts[3 * static_cast<std::size_t>(rr)] = __dadd_rn(__dadd_rn(g.ox, __dmul_rn((ix + jx) / 2 + 0.5, g.B)), p.ctr0);
+    p.rep_pts[3 * static_cast<std::size_t>(rr) + 1] = __dadd_rn(__dadd_rn(g.oy, __dmul_rn(q.iy + 0.5, g.B)), p.ctr1);
+    p.rep_pts[3 * static_cast<std::size_t>(rr) + 2] = __dadd_rn(__dadd_rn(g.oz, __dmul_rn(q.iz + 0.5, g.B)), p.ctr2);
+    p.rootval[i] = 2 + static_cast<std::int32_t>(rr);
+  }
+}
+
+static __global__ void k_l1_cellval(const L1Params p, std::uint32_t nrows) {
+  for (std::uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < nrows; r += gridDim.x * blockDim.x) {
+    const RowPos q = row_pos(p.grids, p.row_first, p.K, r);
+    const int nx = p.grids[q.k].nx;
+    for (int ix = 0; ix < nx; ++ix)
+      if (p.cert[q.row + ix]) p.cellval[q.row + ix] = p.rootval[p.parent[p.cellrun[q.row + ix]]];
   }
 }
 

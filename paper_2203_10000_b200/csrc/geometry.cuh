@@ -220,4 +220,42 @@ static __global__ void k_cluster_spheres(const double* __restrict__ xyz, const s
   if (lane == 0) clus[q] = make_float4(fc[0], fc[1], fc[2], sphere_radius(rho, fc));
 }
 
+// one warp per supercluster g (32 consecutive clusters of one compartment):
+// a sphere containing every cluster sphere (fp32 centre of the box of the
+// cluster balls, radius from it in fp64, rounded up)
+static __global__ void k_super_spheres(const float4* __restrict__ clus, const std::uint32_t* __restrict__ coff,
+                                       const std::uint32_t* __restrict__ soff, int K, std::uint32_t nsup,
+                                       float4* __restrict__ sup) {
+  const std::uint32_t g = (blockIdx.x * blockDim.x + threadIdx.x) / 32;
+  if (g >= nsup) return;  // warp-uniform
+  const int lane = threadIdx.x & 31;
+  int k = 0;
+  while (k + 1 < K && g >= soff[k + 1]) ++k;
+  const std::uint32_t q = coff[k] + (g - soff[k]) * 32 + lane;
+  const bool real = q < coff[k + 1];
+  float4 s = real ? clus[q] : make_float4(0.f, 0.f, 0.f, 0.f);
+  double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
+  if (real) {
+    const double c[3] = {s.x, s.y, s.z};
+    for (int a = 0; a < 3; ++a) {
+      lo[a] = c[a] - s.w;
+      hi[a] = c[a] + s.w;
+    }
+  }
+  for (int a = 0; a < 3; ++a)
+    for (int o = 16; o > 0; o >>= 1) {
+      lo[a] = fmin(lo[a], __shfl_xor_sync(kFull, lo[a], o));
+      hi[a] = fmax(hi[a], __shfl_xor_sync(kFull, hi[a], o));
+    }
+  const float fc[3] = {static_cast<float>(0.5 * (lo[0] + hi[0])), static_cast<float>(0.5 * (lo[1] + hi[1])),
+                       static_cast<float>(0.5 * (lo[2] + hi[2]))};
+  double r = 0.0;
+  if (real) {
+    const double dx = double(s.x) - fc[0], dy = double(s.y) - fc[1], dz = double(s.z) - fc[2];
+    r = sqrt(dx * dx + dy * dy + dz * dz) + s.w;
+  }
+  for (int o = 16; o > 0; o >>= 1) r = fmax(r, __shfl_xor_sync(kFull, r, o));
+  if (lane == 0) sup[g] = make_float4(fc[0], fc[1], fc[2], nextafterf(static_cast<float>(r * (1.0 + 1e-6) + 1e-5), INFINITY));
+}
+
 }  // namespace nm

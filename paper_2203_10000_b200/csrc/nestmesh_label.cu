@@ -8,123 +8,11 @@
 // pass (dense, 13-DOP culled, sparse / certified-cell, sharded), tet labels
 // and the labeling entry points. See context.cuh for the others.
 #include "context.cuh"
+#include "strips.h"
 
 using namespace nmh;
 
 namespace {
-
-struct Strip {
-  std::vector<std::uint32_t> v;
-  std::vector<std::uint32_t> t;
-};
-
-std::vector<Strip> stripify(const std::uint32_t* tri, std::uint32_t t0, std::uint32_t t1, std::size_t nv) {
-  const std::uint32_t m = t1 - t0;
-  // edge adjacency through vertex -> incident-triangle lists (counting sort
-  // over the vertex ids, linear time): adj[3 i + j] = the other triangle on
-  // edge (e_j, e_{j+1}) of triangle i, -1 on a border
-  std::vector<std::uint32_t> start(nv + 1, 0);
-  for (std::uint32_t i = 0; i < m; ++i)
-    for (int j = 0; j < 3; ++j) ++start[tri[3 * std::size_t(t0 + i) + j] + 1];
-  for (std::size_t v = 0; v < nv; ++v) start[v + 1] += start[v];
-  std::vector<std::uint32_t> inc(3 * std::size_t(m));
-  {
-    std::vector<std::uint32_t> cur(start.begin(), start.end() - 1);
-    for (std::uint32_t i = 0; i < m; ++i)
-      for (int j = 0; j < 3; ++j) inc[cur[tri[3 * std::size_t(t0 + i) + j]]++] = i;
-  }
-  std::vector<std::int64_t> adj(3 * std::size_t(m), -1);
-  for (std::uint32_t i = 0; i < m; ++i) {
-    const std::uint32_t* e = tri + 3 * std::size_t(t0 + i);
-    for (int j = 0; j < 3; ++j) {
-      const std::uint32_t a = e[j], b = e[(j + 1) % 3];
-      for (std::uint32_t q = start[a]; q < start[a + 1]; ++q) {
-        const std::uint32_t o = inc[q];
-        if (o == i) continue;
-        const std::uint32_t* f = tri + 3 * std::size_t(t0 + o);
-        if (f[0] == b || f[1] == b || f[2] == b) {
-          adj[3 * std::size_t(i) + j] = o;
-          break;
-        }
-      }
-    }
-  }
-  std::vector<std::uint8_t> used(m, 0);
-  auto nbr = [&](std::uint32_t i, std::uint32_t a, std::uint32_t b) -> std::int64_t {
-    const std::uint32_t* e = tri + 3 * std::size_t(t0 + i);
-    for (int j = 0; j < 3; ++j) {
-      const std::uint32_t x = e[j], y = e[(j + 1) % 3];
-      if ((x == a && y == b) || (x == b && y == a)) return adj[3 * std::size_t(i) + j];
-    }
-    return -1;
-  };
-  std::vector<int> deg(m, 0);
-  for (std::uint32_t i = 0; i < m; ++i) {
-    const std::uint32_t* e = tri + 3 * std::size_t(t0 + i);
-    for (int j = 0; j < 3; ++j) deg[i] += nbr(i, e[j], e[(j + 1) % 3]) >= 0;
-  }
-  using QE = std::pair<int, std::uint32_t>;
-  std::priority_queue<QE, std::vector<QE>, std::greater<QE>> pq;
-  for (std::uint32_t i = 0; i < m; ++i) pq.emplace(deg[i], i);
-  std::vector<std::uint32_t> mark(m, 0);
-  std::uint32_t stamp = 0;
-  // forward walk from triangle i with vertex order (a,b,c)
-  auto walk = [&](std::uint32_t i, std::uint32_t a, std::uint32_t b, std::uint32_t c, std::vector<std::uint32_t>& vs,
-                  std::vector<std::uint32_t>& ts) {
-    vs.assign({a, b, c});
-    ts.assign({i});
-    mark[i] = stamp;
-    std::uint32_t cur = i;
-    for (;;) {
-      const std::uint32_t u = vs[vs.size() - 2], w = vs.back();
-      const std::int64_t n = nbr(cur, u, w);
-      if (n < 0 || used[n] || mark[n] == stamp) break;
-      const std::uint32_t* e = tri + 3 * std::size_t(t0 + n);
-      std::uint32_t x = e[0];
-      for (int j = 0; j < 3; ++j)
-        if (e[j] != u && e[j] != w) x = e[j];
-      vs.push_back(x);
-      ts.push_back(static_cast<std::uint32_t>(n));
-      mark[n] = stamp;
-      cur = static_cast<std::uint32_t>(n);
-    }
-  };
-  std::vector<Strip> out;
-  std::vector<std::uint32_t> fv, ft, bv, btt;
-  while (!pq.empty()) {
-    auto [d, i] = pq.top();
-    pq.pop();
-    if (used[i] || d != deg[i]) continue;
-    const std::uint32_t* e = tri + 3 * std::size_t(t0 + i);
-    Strip best;
-    for (int r = 0; r < 3; ++r) {
-      const std::uint32_t a = e[r], b = e[(r + 1) % 3], c = e[(r + 2) % 3];
-      ++stamp;
-      walk(i, a, b, c, fv, ft);
-      // backward: walk from the reversed start without reusing forward triangles
-      std::vector<std::uint32_t> keep(ft.begin(), ft.end());
-      walk(i, c, b, a, bv, btt);
-      // bv = c,b,a,x,y,...; combined vertex sequence = reverse(bv) + fv[3:]
-      Strip s;
-      s.v.assign(bv.rbegin(), bv.rend());
-      s.v.insert(s.v.end(), fv.begin() + 3, fv.end());
-      s.t.assign(btt.rbegin(), btt.rend());  // ..., i
-      s.t.insert(s.t.end(), ft.begin() + 1, ft.end());
-      if (s.t.size() > best.t.size()) best = std::move(s);
-    }
-    for (std::uint32_t t : best.t) used[t] = 1;
-    for (std::uint32_t t : best.t) {
-      const std::uint32_t* f = tri + 3 * std::size_t(t0 + t);
-      for (int j = 0; j < 3; ++j) {
-        const std::int64_t n = nbr(t, f[j], f[(j + 1) % 3]);
-        if (n >= 0 && !used[n]) pq.emplace(--deg[n], static_cast<std::uint32_t>(n));
-      }
-    }
-    for (auto& t : best.t) t += t0;
-    out.push_back(std::move(best));
-  }
-  return out;
-}
 
 }  // namespace
 
@@ -660,17 +548,27 @@ int nm_set_surfaces(nm_ctx* c, const double* xyz, std::size_t nv, const std::uin
     if (!c) throw Error("null context");
     if (K < 1 || K > 32) throw Error("compartment count must be in [1, 32]");
     NvtxRange nvtx_surf("nm_set_surfaces");
+    const auto t_entry = std::chrono::steady_clock::now();
     if (comp_off[0] != 0 || comp_off[K] != nt) throw Error("comp_tri_off must start at 0 and end at the triangle count");
     for (int k = 0; k < K; ++k) {
       if (comp_off[k + 1] < comp_off[k]) throw Error("comp_tri_off must be non-decreasing");
       if (label_ids[k] <= 0) throw Error("compartment label ids must be > 0 (0 is the bounding box)");
     }
-    for (std::size_t i = 0; i < 3 * nt; ++i)
-      if (tri[i] >= nv) throw Error("triangle index out of range");
+    {
+      constexpr std::size_t kChunk = std::size_t(1) << 20;
+      std::atomic<bool> bad{false};
+      parallel_for(static_cast<int>((3 * nt + kChunk - 1) / kChunk), [&](int ch) {
+        const std::size_t i0 = static_cast<std::size_t>(ch) * kChunk, i1 = std::min(3 * nt, i0 + kChunk);
+        std::uint32_t mx = 0;
+        for (std::size_t i = i0; i < i1; ++i) mx = std::max(mx, tri[i]);
+        if (mx >= nv) bad = true;
+      });
+      if (bad) throw Error("triangle index out of range");
+    }
     NM_CUDA(cudaSetDevice(c->opt.device));
     const bool verbose = std::getenv("NM_CELL_VERBOSE") != nullptr;
-    auto t_prev = std::chrono::steady_clock::now();
-    c->surf_t0 = t_prev;
+    auto t_prev = t_entry;
+    c->surf_t0 = t_entry;
     auto lap = [&](const char* what) {
       if (!verbose) return;
       const auto t = std::chrono::steady_clock::now();
@@ -679,13 +577,27 @@ int nm_set_surfaces(nm_ctx* c, const double* xyz, std::size_t nv, const std::uin
                    std::chrono::duration<double, std::milli>(t - c->surf_t0).count());
       t_prev = t;
     };
+    lap("validate");
     // Domain box and centring offset of the fp32 frame.
     double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
-    for (std::size_t i = 0; i < nv; ++i)
-      for (int a = 0; a < 3; ++a) {
-        lo[a] = std::min(lo[a], xyz[3 * i + a]);
-        hi[a] = std::max(hi[a], xyz[3 * i + a]);
-      }
+    {
+      constexpr std::size_t kChunk = std::size_t(1) << 16;  // vertices per work item (min / max: any order)
+      const int nch = static_cast<int>((nv + kChunk - 1) / kChunk);
+      std::vector<std::array<double, 6>> part(std::max(nch, 1), {1e300, 1e300, 1e300, -1e300, -1e300, -1e300});
+      parallel_for(nch, [&](int ch) {
+        auto& b = part[ch];
+        for (std::size_t i = static_cast<std::size_t>(ch) * kChunk; i < std::min(nv, (ch + 1) * kChunk); ++i)
+          for (int a = 0; a < 3; ++a) {
+            b[a] = std::min(b[a], xyz[3 * i + a]);
+            b[3 + a] = std::max(b[3 + a], xyz[3 * i + a]);
+          }
+      });
+      for (const auto& b : part)
+        for (int a = 0; a < 3; ++a) {
+          lo[a] = std::min(lo[a], b[a]);
+          hi[a] = std::max(hi[a], b[3 + a]);
+        }
+    }
     if (nv == 0) lo[0] = lo[1] = lo[2] = hi[0] = hi[1] = hi[2] = 0.0;
     const double ctr[3] = {0.5 * (lo[0] + hi[0]), 0.5 * (lo[1] + hi[1]), 0.5 * (lo[2] + hi[2])};
     double span = std::max({hi[0] - lo[0], hi[1] - lo[1], hi[2] - lo[2], 1e-6}) * 1.5;
@@ -699,69 +611,29 @@ int nm_set_surfaces(nm_ctx* c, const double* xyz, std::size_t nv, const std::uin
     c->has_surfaces = false;
     c->cells = false;
     c->K = K;
-    // fp64 originals (fix-up, cell certification) and the 13-DOP of every
-    // compartment first: the certified-cell build (cull_outside = 2) starts on
-    // its own host thread and stream while the tiles are packed below.
-    auto up_on = [&](DBuf& b, const void* src, std::size_t bytes, cudaStream_t st) {  // pinned chunk staging
-      void* d = b.get(std::max<std::size_t>(bytes, 1));
-      c->h2d(d, src, bytes, st);
-    };
-    c->trace("main", "up64 start");
-    up_on(c->xyz64, xyz, nv * 3 * sizeof(double), c->side);
-    c->trace("main", "xyz64 staged");
-    up_on(c->tri_idx, tri, nt * 3 * sizeof(std::uint32_t), c->side);
-    c->trace("main", "tri_idx staged");
-    up_on(c->comp_off, comp_off, (K + 1) * sizeof(std::uint32_t), c->side);
-    // de-indexed fp64 triangles (72 B each, file order) for the fix-up
-    {
+    // Device prelude: the fp64 originals (fix-up, cell certification), the
+    // de-indexed fp64 triangles and the 13-DOP / box of every compartment
+    // (geometry.cuh: chunks of triangles per block, merged per compartment;
+    // slab bounds over the vertices in the centred frame, widened by 1e-3 mm
+    // + 1e-5 |bound| and rounded outward; the fp64 extents also size the cell
+    // grids). With certified cells (cull_outside = 2) the prelude and then
+    // the cell build run on their own host thread, stream and stager while
+    // this thread packs the tiles; otherwise the prelude runs here.
+    std::vector<float4> hbox(static_cast<std::size_t>(K) * nm::kDopF4);
+    std::vector<double> hext(static_cast<std::size_t>(K) * nm::kExtQ);
+    auto prelude = [&](bool side) {
+      auto up_on = [&](DBuf& b, const void* src, std::size_t bytes) {  // pinned chunk staging
+        void* d = b.get(std::max<std::size_t>(bytes, 1));
+        c->h2d(d, src, bytes, c->side, side, side);
+      };
+      up_on(c->xyz64, xyz, nv * 3 * sizeof(double));
+      up_on(c->tri_idx, tri, nt * 3 * sizeof(std::uint32_t));
+      up_on(c->comp_off, comp_off, (K + 1) * sizeof(std::uint32_t));
+      c->trace(side ? "cells" : "main", "prelude: uploads");
       auto* t64 = c->tri64.as<double>(std::max<std::size_t>(9 * nt, 1));
       if (nt)
         nm::k_deindex64<<<grid_for(9 * nt, 256, c->sm_count * 16), 256, 0, c->side>>>(
             static_cast<const double*>(c->xyz64.p), static_cast<const std::uint32_t*>(c->tri_idx.p), nt, t64);
-      NM_CUDA(cudaGetLastError());
-    }
-    lap("up64");
-    // 13-DOP: slab bounds over the vertices (centred frame), widened by 1e-3 mm
-    // + 1e-5 |bound| (covers the fp32 rounding of the point and of the
-    // projection in the kernel) and rounded outward. On the device
-    // (geometry.cuh): chunks of triangles per block, merged per compartment
-    // (min / max are order-independent); the fp64 extents (the first three
-    // directions are the compartment's box) also size the cell grids.
-    std::vector<float4> hbox(static_cast<std::size_t>(K) * nm::kDopF4);
-    std::vector<double> hext(static_cast<std::size_t>(K) * nm::kExtQ);
-    // The certified-cell build starts now on its own host thread and stream;
-    // it waits for the extents through dop_ready (set below, or set with an
-    // error if this thread throws first).
-    std::promise<void> dop_ready;
-    std::unique_ptr<CellBuilder> cells;
-    std::exception_ptr cells_err;
-    struct Joiner {
-      std::thread t;
-      ~Joiner() {
-        if (t.joinable()) t.join();
-      }
-    } cells_thread;
-    if (c->opt.cull_outside == 2) {
-      cells = make_cell_builder(c, xyz, tri, comp_off, hbox, hext, c->side, dop_ready.get_future().share());
-      cells_thread.t = std::thread([&] {
-        try {
-          cells->prepare();
-        } catch (...) {
-          cells_err = std::current_exception();
-        }
-      });
-    }
-    lap("cells-go");
-    // declared after the joiner, so destroyed first: on an exception below the
-    // cell thread is released (with an error) before it is joined
-    struct DopGuard {
-      std::promise<void>& p;
-      bool set = false;
-      ~DopGuard() {
-        if (!set) p.set_exception(std::make_exception_ptr(Error("13-DOP not computed")));
-      }
-    } dop_guard{dop_ready};
-    {
       constexpr std::uint32_t kExtChunk = 8192;
       std::vector<nm::ExtentItem> items;
       std::vector<std::uint32_t> item_first(K + 1, 0);
@@ -776,8 +648,8 @@ int nm_set_surfaces(nm_ctx* c, const double* xyz, std::size_t nv, const std::uin
       auto* d_part = c->ext_part.as<double>(std::max<std::size_t>(items.size(), 1) * nm::kExtQ);
       auto* d_ext = c->ext_val.as<double>(static_cast<std::size_t>(K) * nm::kExtQ);
       auto* d_box = c->comp_box.as<float4>(static_cast<std::size_t>(K) * nm::kDopF4);
-      c->h2d(d_items, items.data(), items.size() * sizeof(nm::ExtentItem), c->side);
-      c->h2d(d_first, item_first.data(), item_first.size() * sizeof(std::uint32_t), c->side);
+      c->h2d(d_items, items.data(), items.size() * sizeof(nm::ExtentItem), c->side, side, side);
+      c->h2d(d_first, item_first.data(), item_first.size() * sizeof(std::uint32_t), c->side, side, side);
       if (!items.empty())
         nm::k_extents_items<<<static_cast<unsigned>(items.size()), 256, 0, c->side>>>(
             d_items, static_cast<const double*>(c->xyz64.p), static_cast<const std::uint32_t*>(c->tri_idx.p), ctr[0],
@@ -785,12 +657,35 @@ int nm_set_surfaces(nm_ctx* c, const double* xyz, std::size_t nv, const std::uin
       nm::k_extents_finalize<<<K, 32, 0, c->side>>>(d_part, d_first, static_cast<const std::uint32_t*>(c->comp_off.p),
                                                     d_ext, d_box);
       NM_CUDA(cudaGetLastError());
-      c->d2h(hext.data(), d_ext, hext.size() * sizeof(double), c->side);
-      c->d2h(hbox.data(), d_box, hbox.size() * sizeof(float4), c->side);
+      c->d2h(hext.data(), d_ext, hext.size() * sizeof(double), c->side, side, side);
+      c->d2h(hbox.data(), d_box, hbox.size() * sizeof(float4), c->side, side, side);
+      c->trace(side ? "cells" : "main", "prelude: extents read");
+    };
+    std::promise<void> dop_ready;  // set by the cell thread after its prelude
+    std::unique_ptr<CellBuilder> cells;
+    std::exception_ptr cells_err;
+    struct Joiner {
+      std::thread t;
+      ~Joiner() {
+        if (t.joinable()) t.join();
+      }
+    } cells_thread;
+    if (c->opt.cull_outside == 2) {
+      cells = make_cell_builder(c, xyz, tri, comp_off, hbox, hext, c->side, dop_ready.get_future().share());
+      cells_thread.t = std::thread([&] {
+        try {
+          NM_CUDA(cudaSetDevice(c->opt.device));
+          prelude(true);
+          dop_ready.set_value();
+          cells->prepare();
+        } catch (...) {
+          cells_err = std::current_exception();
+        }
+      });
+    } else {
+      prelude(false);
     }
-    dop_ready.set_value();
-    dop_guard.set = true;
-    lap("dop");
+    lap("prelude");
 
     auto morton = [&](const double* m) {
       std::uint32_t q[3];
@@ -1156,6 +1051,8 @@ int nm_set_surfaces(nm_ctx* c, const double* xyz, std::size_t nv, const std::uin
     c->has_surfaces = true;
     if (cells) cells->finish();  // representatives need the tiles: after the packing
     lap("cells-fin");
+    cells.reset();
+    lap("end");
   });
 }
 

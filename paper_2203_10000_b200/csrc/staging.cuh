@@ -176,8 +176,9 @@ class Stager {
     nvtxRangePushA("nm staged h2d");
     const auto* s = static_cast<const char*>(src);
     auto* d = static_cast<char*>(dst);
-    for (std::size_t off = 0, i = 0; off < bytes; off += kChunk, ++i) {
-      const int b = static_cast<int>(i % kBufs);
+    for (std::size_t off = 0; off < bytes; off += kChunk) {
+      const int b = next_;  // buffers rotate across calls: back-to-back small copies do not wait for each other
+      next_ = (next_ + 1) % kBufs;
       const std::size_t len = std::min(kChunk, bytes - off);
       const auto a0 = std::chrono::steady_clock::now();
       check(cudaEventSynchronize(ev_[b]));  // the buffer's previous DMA is done
@@ -213,6 +214,7 @@ class Stager {
     for (std::size_t i = 0; i < n + 1; ++i) {
       if (i < n) {  // DMA chunk i into its buffer (the buffer's host copy, chunk i - kBufs, is done)
         const int b = static_cast<int>(i % kBufs);
+        check(cudaStreamWaitEvent(st, ev_[b], 0));  // an h2d DMA on another stream may still read the buffer
         check(cudaMemcpyAsync(pin_[b], d + i * kChunk, len_of(i), cudaMemcpyDeviceToHost, st));
         check(cudaEventRecord(ev_[b], st));
       }
@@ -255,6 +257,7 @@ class Stager {
     }();
     return on;
   }
+  int next_ = 0;  // next chunk buffer of h2d
   void* pin_[kBufs] = {};
   cudaEvent_t ev_[kBufs] = {};
 };
