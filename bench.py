@@ -533,10 +533,18 @@ def main():
                     "triangle carry their exact winding number 0/1; only the remaining (point, compartment) "
                     "pairs are evaluated, by the same k_label loop in sparse mode)"}
         for mode in (1, 2):
-            cctx = Context(local, cull_outside=mode)
-            t_set = time.perf_counter()
-            cctx.set_surfaces(S.xyz, S.tri, S.comp_off, S.label_ids)
-            t_set = time.perf_counter() - t_set
+            # set_surfaces on fresh contexts: the first call of the process
+            # (pinned staging buffers, device pool growth, lazy kernel loading)
+            # and the faster of two more (what later contexts pay)
+            t_sets = []
+            for rep in range(3):
+                if rep:
+                    cctx.close()
+                cctx = Context(local, cull_outside=mode)
+                t_set = time.perf_counter()
+                cctx.set_surfaces(S.xyz, S.tri, S.comp_off, S.label_ids)
+                t_sets.append(time.perf_counter() - t_set)
+            t_set_first, t_set = t_sets[0], sorted(t_sets[1:])[0]
             cm = torch.zeros(nsh.per, dtype=torch.int32, device="cuda")
             cctx.label_nodes_device(d_nodes, cm[: nsh.size], stream=sptr, stats=True)
             cl = torch.empty(tsh.size, dtype=torch.int32, device="cuda")
@@ -552,7 +560,7 @@ def main():
                 cms.append(a.elapsed_time(b))
             same = bool(torch.equal(cl, d_labels))
             entry = {"full_mesh_labeling_time_s": sum(cms) / len(cms) / 1e3, "labels_identical": same,
-                     "set_surfaces_s": t_set, "note": notes[mode]}
+                     "set_surfaces_s": t_set, "set_surfaces_first_call_s": t_set_first, "note": notes[mode]}
             if e2e is not None and not use_dist:
                 # the same through the host-buffer C ABI (nm_label_mesh: H2D nodes + tets, D2H labels), wall clock
                 hl, _, _ = cctx.label_mesh(h_nodes.numpy(), h_tets.numpy().view(np.uint32), out=h_labels.numpy())

@@ -104,11 +104,18 @@ class DevicePool {
   static void* alloc(std::size_t bytes, int* dev_out) {
     int dev = 0;
     NM_CUDA(cudaGetDevice(&dev));
+    const auto t0 = std::chrono::steady_clock::now();
     Dev& d = of(dev);
     void* p = nullptr;
     NM_CUDA(cudaMallocFromPoolAsync(&p, bytes, d.pool, d.st));
     NM_CUDA(cudaStreamSynchronize(d.st));
     *dev_out = dev;
+    static const bool tr = [] {
+      const char* v = std::getenv("NM_CELL_VERBOSE");
+      return v && std::atoi(v) >= 3;
+    }();
+    const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    if (tr && ms > 0.5) std::fprintf(stderr, "      [pool] %zu B in %.2f ms\n", bytes, ms);
     return p;
   }
   // caller guarantees no queued work uses p any more

@@ -245,10 +245,14 @@ class Stager {
   }
   void init() {
     if (pin_[0]) return;
+    const auto t0 = std::chrono::steady_clock::now();
     for (int b = 0; b < kBufs; ++b) {
       pin_[b] = PinnedChunks::get().acquire(kChunk);
       check(cudaEventCreateWithFlags(&ev_[b], cudaEventDisableTiming));
     }
+    if (trace_on())
+      std::fprintf(stderr, "      [stager] init (pinned chunks) %.2f ms\n",
+                   std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
   }
   static bool trace_on() {
     static const bool on = [] {
