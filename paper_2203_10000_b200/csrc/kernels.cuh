@@ -784,7 +784,8 @@ struct PredStraddle {
 // triangles (72 B each, file order) through shared memory in tiles of
 // kFixTile, so every triangle load feeds kFixPairs points. Each pair is
 // owned by kFixLanes threads: lane l sums triangles t = l, l + kFixLanes, ...
-// in increasing t, then a fixed xor-butterfly adds the lanes. That order
+// in increasing t into two alternating accumulators (added at the end), then
+// a fixed xor-butterfly adds the lanes. That order
 // depends only on the compartment's triangle count, never on which pairs
 // share the batch, so s is a pure function of (point, compartment).
 // ---------------------------------------------------------------------------
@@ -913,7 +914,7 @@ static __global__ void __launch_bounds__(kFixThreads) k_fixup(const FixupParams 
     }
     const std::uint32_t c0 = lo + chunk * kFixChunk, c1 = min(hi, c0 + kFixChunk);
     NM_DCHECK(c1 <= prm.n_tri && c0 <= c1, "k_fixup: triangle chunk out of range");
-    double sum = 0.0;
+    double sum = 0.0, sum1 = 0.0;  // two independent chains (the fp64 atan2 / sqrt sequences are latency-bound)
     auto load = [&](int buf, std::uint32_t t0) {
       const std::uint32_t m = min(static_cast<std::uint32_t>(kFixTile), c1 - t0);
       const double* src = prm.tri64 + 9 * static_cast<std::size_t>(t0);
@@ -935,15 +936,23 @@ static __global__ void __launch_bounds__(kFixThreads) k_fixup(const FixupParams 
       __syncthreads();  // tile t0 is in buffer buf for every thread
       if (has) {
         const double* tile = s_fix + buf * (kFixTile * 9);
-        for (std::uint32_t u = lane; u < m; u += kFixLanes) {
+        // the oracle's exact operand order inside a term (no FMA): on-surface
+        // points (num = +-0) must get the oracle's atan2 branch
+        std::uint32_t u = lane;
+        for (; u + kFixLanes < m; u += 2 * kFixLanes) {
           const double* e = tile + 9 * u;
-          // the oracle's exact operand order (no FMA): on-surface points
-          // (num = +-0) must get the oracle's atan2 branch
+          const double* f = e + 9 * kFixLanes;
+          sum += vos_half_angle64(e, e + 3, e + 6, px, py, pz);
+          sum1 += vos_half_angle64(f, f + 3, f + 6, px, py, pz);
+        }
+        if (u < m) {
+          const double* e = tile + 9 * u;
           sum += vos_half_angle64(e, e + 3, e + 6, px, py, pz);
         }
       }
       __syncthreads();  // buffer buf is consumed: the next iteration may refill it
     }
+    sum += sum1;
 #pragma unroll
     for (int o = kFixLanes / 2; o > 0; o >>= 1) sum += __shfl_xor_sync(kFull, sum, o, kFixLanes);
     NM_DCHECK(!has || s_po[c] + j * nch + chunk < prm.n_part, "k_fixup: partial slot out of range");
