@@ -84,10 +84,11 @@ struct GpuOptions {
   bool validate_closed = true;  // check the SPEC.md:227 precondition with validate_closed (surface.hpp:80-104)
   std::vector<int> devices;     // > 1 entries: initial_label shards over these devices (SPEC.md:267 --label-workers)
   // Certified cells (cull_outside = 2) cost a one-off grid build per
-  // Labeler (~0.15-0.2 s at 1e6 triangles); one-shot free-function calls with
-  // fewer point-triangle pairs than this use 13-DOP culling alone. Labels are
-  // identical either way.
-  double cell_min_evals = 2e12;
+  // Labeler (~35 ms at 1e6 triangles, ~8 ms at 3.6e4, built on the device);
+  // one-shot free-function calls with fewer point-triangle pairs than this
+  // use 13-DOP culling alone (at 4.2e10 pairs, cfg2: cells 7.8 + 1.4 ms
+  // against 16 ms with 13-DOP culling). Labels are identical either way.
+  double cell_min_evals = 2e10;
   GpuOptions() {
     nm_default_options(&opt);
     opt.cull_outside = 2;  // exact for closed surfaces (13-DOP + certified cells); disabled below whenever
