@@ -411,6 +411,205 @@ static __global__ void k_cell_classify(const ClassifyParams prm) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// Pairs left unknown by k_cell_classify (points in uncertified children),
+// resolved exactly where a surface-free ball joins them to a certified
+// neighbour (round 2): for the 26 neighbour children of the point's child
+// (or their certified parents) with a known w, gap = |p - c_n| - r_n, where
+// B(c_n, r_n) is the neighbour's certified ball (shrunk by a 1e-9 relative +
+// 1e-9 mm margin). If the best gap < 0, p lies in that ball. Otherwise the
+// pair is resolved when B(p, rho), rho just above the gap, meets no triangle
+// of the compartment (the certification test with one ball per lane: warp
+// ball, then superclusters, clusters, triangle spheres in fp32 with margins,
+// then the exact fp64 distance > rho (1 + 1e-9)). Both balls are open,
+// surface-free and overlap, so p and c_n are joined in the complement of
+// the surface: w(p) = w_n exactly. Resolved pairs get their bit (when the
+// caller writes known bits) and s = w, and leave the pair lists.
+// ---------------------------------------------------------------------------
+struct ResolveParams {
+  const double* pts;
+  const std::uint32_t* order;
+  double cx, cy, cz;
+  const CellGrid* grids;
+  const std::uint32_t* code;
+  const std::uint8_t* child;
+  int K;
+  const std::uint32_t* list;           // packed per-compartment lists of evaluation positions
+  std::uint32_t off[33], cnt[32];      // compartment k: list[off[k] .. off[k] + cnt[k])
+  std::uint32_t wfirst[33];            // first warp of compartment k
+  std::uint32_t* unk;                  // per position: unknown compartment bits (cleared when resolved)
+  std::uint32_t* masks;                // by point id
+  double* s_out;
+  int write_known;
+  CertifyParams cl;                    // clusters / superclusters / triangles (coff, soff, sup, clus, clus_tri, tsph, xyz, tri)
+  unsigned long long* counters;        // [0] resolved inside a ball, [1] resolved by a ball query
+};
+
+__device__ __forceinline__ int floor_div4(int x) { return x >= 0 ? x / 4 : -((-x + 3) / 4); }
+
+static __global__ void __launch_bounds__(256) k_pair_resolve(const ResolveParams prm) {
+  const unsigned w = (blockIdx.x * blockDim.x + threadIdx.x) / 32;
+  if (w >= prm.wfirst[prm.K]) return;  // warp-uniform
+  int k = 0;
+  while (k + 1 < prm.K && w >= prm.wfirst[k + 1]) ++k;
+  const int lane = threadIdx.x & 31;
+  const std::uint32_t e = (w - prm.wfirst[k]) * 32 + lane;
+  const bool active = e < prm.cnt[k];
+  const CellGrid g = prm.grids[k];
+  std::uint32_t i = 0, j = 0;
+  double x = 0.0, y = 0.0, z = 0.0;
+  if (active) {
+    i = prm.list[prm.off[k] + e];
+    j = prm.order ? prm.order[i] : i;
+    x = prm.pts[3 * static_cast<std::size_t>(j)] - prm.cx;
+    y = prm.pts[3 * static_cast<std::size_t>(j) + 1] - prm.cy;
+    z = prm.pts[3 * static_cast<std::size_t>(j) + 2] - prm.cz;
+  }
+  // the point's child cell in the compartment's fine lattice (kSubCells per cell)
+  const double b = g.B / kSubCells;
+  const double rl1 = cell_ball(g.B) * (1.0 - 1e-9) - 1e-9, rch = cell_ball(b) * (1.0 - 1e-9) - 1e-9;
+  double best = 1e300;
+  int wbest = -1;
+  if (active) {
+    const double u = (x - g.ox) / g.B, v = (y - g.oy) / g.B, ww = (z - g.oz) / g.B;
+    const int iu = static_cast<int>(u), iv = static_cast<int>(v), iw = static_cast<int>(ww);
+    const int fx = iu * kSubCells + min(static_cast<int>((u - iu) * kSubCells), kSubCells - 1);
+    const int fy = iv * kSubCells + min(static_cast<int>((v - iv) * kSubCells), kSubCells - 1);
+    const int fz = iw * kSubCells + min(static_cast<int>((ww - iw) * kSubCells), kSubCells - 1);
+    for (int dz = -1; dz <= 1; ++dz)
+      for (int dy = -1; dy <= 1; ++dy)
+        for (int dx = -1; dx <= 1; ++dx) {
+          if (!dx && !dy && !dz) continue;
+          const int nx = fx + dx, ny = fy + dy, nz = fz + dz;
+          const int px = floor_div4(nx), py = floor_div4(ny), pz = floor_div4(nz);
+          if (px < 0 || py < 0 || pz < 0 || px >= g.nx || py >= g.ny || pz >= g.nz) continue;
+          const std::uint32_t st = __ldg(prm.code + g.off + (static_cast<std::size_t>(pz) * g.ny + py) * g.nx + px);
+          double ccx, ccy, ccz, r;
+          int wn;
+          if (st == 1u || st == 2u) {  // certified parent: its ball
+            wn = static_cast<int>(st) - 1;
+            ccx = g.ox + (px + 0.5) * g.B;
+            ccy = g.oy + (py + 0.5) * g.B;
+            ccz = g.oz + (pz + 0.5) * g.B;
+            r = rl1;
+          } else if (st >= 3u) {
+            const int sx = nx - px * kSubCells, sy = ny - py * kSubCells, sz = nz - pz * kSubCells;
+            const std::uint8_t cs =
+                __ldg(prm.child + static_cast<std::size_t>(st - 3u) * kChildren + (sz * kSubCells + sy) * kSubCells + sx);
+            if (cs != 1 && cs != 2) continue;
+            wn = cs - 1;
+            ccx = g.ox + px * g.B + (sx + 0.5) * b;
+            ccy = g.oy + py * g.B + (sy + 0.5) * b;
+            ccz = g.oz + pz * g.B + (sz + 0.5) * b;
+            r = rch;
+          } else {
+            continue;
+          }
+          const double gx = x - ccx, gy = y - ccy, gz = z - ccz;
+          const double gap = sqrt(gx * gx + gy * gy + gz * gz) - r;
+          if (gap < best) {
+            best = gap;
+            wbest = wn;
+          }
+        }
+  }
+  bool resolved = active && wbest >= 0 && best < -1e-9;
+  const bool query = active && wbest >= 0 && !resolved && best < 0.25 * g.B;
+  const double rho = query ? fmax(best, 0.0) * (1.0 + 1e-9) + 1e-9 : 0.0;
+  unsigned qm = __ballot_sync(kFull, query);
+  if (qm) {
+    // warp ball over the querying lanes (fp32, with margins)
+    const float fx = static_cast<float>(x), fy = static_cast<float>(y), fz = static_cast<float>(z);
+    float lo[3] = {query ? fx : 3e38f, query ? fy : 3e38f, query ? fz : 3e38f};
+    float hi[3] = {query ? fx : -3e38f, query ? fy : -3e38f, query ? fz : -3e38f};
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        lo[a] = fminf(lo[a], __shfl_xor_sync(kFull, lo[a], o));
+        hi[a] = fmaxf(hi[a], __shfl_xor_sync(kFull, hi[a], o));
+      }
+    const float bx = 0.5f * (lo[0] + hi[0]), by = 0.5f * (lo[1] + hi[1]), bz = 0.5f * (lo[2] + hi[2]);
+    const float frb = static_cast<float>(rho) + 1e-3f + 4e-6f * (fabsf(fx) + fabsf(fy) + fabsf(fz));
+    float reach = 0.0f;
+    if (query) {
+      const float dx = fx - bx, dy = fy - by, dz = fz - bz;
+      reach = sqrtf(dx * dx + dy * dy + dz * dz) * (1.0f + 1e-6f) + frb;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) reach = fmaxf(reach, __shfl_xor_sync(kFull, reach, o));
+    const float fbr = reach + 1e-3f + 4e-6f * (fabsf(bx) + fabsf(by) + fabsf(bz));
+    const std::uint32_t c0 = prm.cl.coff[k];
+    const int nclus = static_cast<int>(prm.cl.coff[k + 1] - c0);
+    const float4* sup = prm.cl.sup + prm.cl.soff[k];
+    const int nsup = static_cast<int>(prm.cl.soff[k + 1] - prm.cl.soff[k]);
+    const float4* clus = prm.cl.clus + c0;
+    const std::uint32_t* ctri = prm.cl.clus_tri + static_cast<std::size_t>(c0) * kCluster;
+    const float4* tsph = prm.cl.tsph + static_cast<std::size_t>(c0) * kCluster;
+    const V3t<double> pt{x + prm.cx, y + prm.cy, z + prm.cz};
+    const double lim = rho * (1.0 + 1e-9);
+    bool hit = !query;
+    for (int g0 = 0; g0 < nsup && !__all_sync(kFull, hit); g0 += 32) {
+      bool scand = false;
+      if (g0 + lane < nsup) {
+        const float4 s4 = __ldg(sup + g0 + lane);
+        const float dx = bx - s4.x, dy = by - s4.y, dz = bz - s4.z;
+        const float R = fbr + s4.w;
+        scand = dx * dx + dy * dy + dz * dz <= R * R;
+      }
+      unsigned sbal = __ballot_sync(kFull, scand);
+      while (sbal) {
+        const int q0 = (g0 + __ffs(sbal) - 1) * 32;
+        sbal &= sbal - 1;
+        bool cand = false;
+        if (q0 + lane < nclus) {
+          const float4 s4 = __ldg(clus + q0 + lane);
+          const float dx = bx - s4.x, dy = by - s4.y, dz = bz - s4.z;
+          const float R = fbr + s4.w;
+          cand = dx * dx + dy * dy + dz * dz <= R * R;
+        }
+        unsigned bal = __ballot_sync(kFull, cand);
+        while (bal) {
+          const int q = q0 + __ffs(bal) - 1;
+          bal &= bal - 1;
+          if (hit) continue;
+          const float4 s4 = __ldg(clus + q);
+          const float dx = fx - s4.x, dy = fy - s4.y, dz = fz - s4.z;
+          const float R = frb + s4.w;
+          if (dx * dx + dy * dy + dz * dz > R * R) continue;
+          for (int t = 0; t < kCluster && !hit; ++t) {
+            const float4 ts = __ldg(tsph + static_cast<std::size_t>(q) * kCluster + t);
+            if (ts.w < 0.0f) break;  // pads close the cluster
+            const float tx = fx - ts.x, ty = fy - ts.y, tz = fz - ts.z;
+            const float TR = frb + ts.w;
+            if (tx * tx + ty * ty + tz * tz > TR * TR) continue;
+            const std::uint32_t tid = __ldg(ctri + static_cast<std::size_t>(q) * kCluster + t);
+            const std::uint32_t* ev = prm.cl.tri + 3 * static_cast<std::size_t>(tid);
+            const double* A = prm.cl.xyz + 3 * static_cast<std::size_t>(ev[0]);
+            const double* Bv = prm.cl.xyz + 3 * static_cast<std::size_t>(ev[1]);
+            const double* Cv = prm.cl.xyz + 3 * static_cast<std::size_t>(ev[2]);
+            const double d2 =
+                point_tri_dist2<double>(pt, {A[0], A[1], A[2]}, {Bv[0], Bv[1], Bv[2]}, {Cv[0], Cv[1], Cv[2]});
+            hit = !(d2 > lim * lim);  // NaN (degenerate) counts as a hit
+          }
+        }
+      }
+    }
+    if (query && !hit) resolved = true;
+    const unsigned nq = __popc(__ballot_sync(kFull, query && !hit));
+    if (prm.counters && lane == 0 && nq) atomicAdd(prm.counters + 1, static_cast<unsigned long long>(nq));
+  }
+  if (prm.counters) {
+    const unsigned nb = __popc(__ballot_sync(kFull, resolved && !query));
+    if (lane == 0 && nb) atomicAdd(prm.counters, static_cast<unsigned long long>(nb));
+  }
+  if (resolved) {
+    atomicAnd(prm.unk + i, ~(1u << k));
+    if (prm.write_known && wbest == 1) atomicOr(prm.masks + j, 1u << k);
+    if (prm.s_out) prm.s_out[static_cast<std::size_t>(j) * prm.K + k] = wbest == 1 ? 1.0 : 0.0;
+  }
+}
+
 struct PredBit {
   const std::uint32_t* v;
   int bit;

@@ -316,6 +316,8 @@ struct nm_ctx {
       l1_rowruns, l1_runfirst, l1_cellrun, l1_parent, l1_runrow, l1_runx, l1_zero, l1_rootval, l1_nruns, clus_sup;
   std::uint64_t cells_total = 0, cells_certified = 0, cell_reps = 0, sparse_pairs = 0, sparse_evals = 0;
   std::uint64_t cells_l1 = 0, cells_children = 0;  // level-1 cells and children (nm_cell_dump)
+  std::uint64_t resolved_pairs = 0;  // pairs of the last node pass resolved by k_pair_resolve
+  bool no_resolve = std::getenv("NM_NO_RESOLVE") != nullptr;  // A/B: skip k_pair_resolve
   double ms_cells = 0.0;  // host wall time of the certification (nm_set_surfaces)
   std::vector<std::uint32_t> comp_off_h;
 

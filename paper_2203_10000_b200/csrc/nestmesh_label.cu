@@ -147,33 +147,84 @@ std::vector<std::uint32_t> classify_cells(nm_ctx* c, const double* d_pts, std::s
   cp.s_out = d_s;
   nm::k_cell_classify<<<grid_for(n, 256, c->sm_count * 16), 256, 0, st>>>(cp);
   ++launches;
-  for (int k = 0; k < K; ++k) {
-    nm::k_select_count<<<static_cast<unsigned>(nb), nm::kSelBlock, 0, st>>>(nm::PredBit{unk, k}, n, chunk + k * nb);
-    nm::k_select_scan<<<1, 1024, 0, st>>>(chunk + k * nb, nb, dcnt + k);
-    launches += 2;
-  }
-  // (through the context's pinned words: a pageable read-back would be a
-  // driver-staged copy, serialised with other host threads' copies)
-  NM_CUDA(cudaMemcpyAsync(c->h_pcnt, dcnt, K * sizeof(std::uint32_t), cudaMemcpyDeviceToHost, st));
-  NM_CUDA(cudaStreamSynchronize(st));
-  std::vector<std::uint32_t> cnt(c->h_pcnt, c->h_pcnt + K);
-  std::size_t total = 0;
-  for (int k = 0; k < K; ++k) total += cnt[k];
-  if (total > 0xffffffffull) throw Error("more than 2^32 (point, compartment) pairs to evaluate in one call");
-  auto* list = c->sp_list.as<std::uint32_t>(std::max<std::size_t>(total, 1));
-  std::size_t off = 0;
-  c->sparse_pairs = total;
-  c->sparse_evals = 0;
-  for (int k = 0; k < K; ++k) {
-    if (cnt[k]) {
-      nm::k_select_write<<<static_cast<unsigned>(nb), nm::kSelBlock, 0, st>>>(nm::PredBit{unk, k}, n, chunk + k * nb,
-                                                                              list + off);
-      ++launches;
+  // per-compartment ordered lists of the unknown pairs (counts read back:
+  // one host synchronisation per list build)
+  std::vector<std::uint32_t> cnt(K);
+  auto build_lists = [&]() {
+    for (int k = 0; k < K; ++k) {
+      nm::k_select_count<<<static_cast<unsigned>(nb), nm::kSelBlock, 0, st>>>(nm::PredBit{unk, k}, n, chunk + k * nb);
+      nm::k_select_scan<<<1, 1024, 0, st>>>(chunk + k * nb, nb, dcnt + k);
+      launches += 2;
     }
-    off += cnt[k];
-    c->sparse_evals += std::uint64_t(cnt[k]) * (c->comp_off_h[k + 1] - c->comp_off_h[k]);
+    // (through the context's pinned words: a pageable read-back would be a
+    // driver-staged copy, serialised with other host threads' copies)
+    NM_CUDA(cudaMemcpyAsync(c->h_pcnt, dcnt, K * sizeof(std::uint32_t), cudaMemcpyDeviceToHost, st));
+    NM_CUDA(cudaStreamSynchronize(st));
+    cnt.assign(c->h_pcnt, c->h_pcnt + K);
+    std::size_t total = 0;
+    for (int k = 0; k < K; ++k) total += cnt[k];
+    if (total > 0xffffffffull) throw Error("more than 2^32 (point, compartment) pairs to evaluate in one call");
+    auto* list = c->sp_list.as<std::uint32_t>(std::max<std::size_t>(total, 1));
+    std::size_t off = 0;
+    c->sparse_pairs = total;
+    c->sparse_evals = 0;
+    for (int k = 0; k < K; ++k) {
+      if (cnt[k]) {
+        nm::k_select_write<<<static_cast<unsigned>(nb), nm::kSelBlock, 0, st>>>(nm::PredBit{unk, k}, n,
+                                                                                chunk + k * nb, list + off);
+        ++launches;
+      }
+      off += cnt[k];
+      c->sparse_evals += std::uint64_t(cnt[k]) * (c->comp_off_h[k + 1] - c->comp_off_h[k]);
+    }
+    NM_CUDA(cudaGetLastError());
+    return total;
+  };
+  const std::size_t total = build_lists();
+  if (c->cells && total && !c->no_resolve) {
+    // pairs of uncertified children joined to a certified neighbour by a
+    // surface-free ball (cells.cuh k_pair_resolve), then the lists again
+    nm::ResolveParams rp{};
+    rp.pts = d_pts;
+    rp.order = order;
+    rp.cx = c->cx;
+    rp.cy = c->cy;
+    rp.cz = c->cz;
+    rp.grids = cp.grids;
+    rp.code = cp.code;
+    rp.child = cp.child;
+    rp.K = K;
+    rp.list = static_cast<const std::uint32_t*>(c->sp_list.p);
+    std::uint32_t o = 0, wsum = 0;
+    for (int k = 0; k < K; ++k) {
+      rp.off[k] = o;
+      rp.cnt[k] = cnt[k];
+      rp.wfirst[k] = wsum;
+      o += cnt[k];
+      wsum += (cnt[k] + 31) / 32;
+    }
+    rp.off[K] = o;
+    rp.wfirst[K] = wsum;
+    rp.unk = unk;
+    rp.masks = d_masks;
+    rp.s_out = d_s;
+    rp.write_known = preset_known ? 1 : 0;
+    rp.cl.coff = static_cast<const std::uint32_t*>(c->cert_coff.p);
+    rp.cl.soff = rp.cl.coff + K + 1;
+    rp.cl.sup = static_cast<const float4*>(c->clus_sup.p);
+    rp.cl.clus = static_cast<const float4*>(c->clus.p);
+    rp.cl.clus_tri = static_cast<const std::uint32_t*>(c->clus_tri.p);
+    rp.cl.tsph = static_cast<const float4*>(c->clus_tsph.p);
+    rp.cl.xyz = static_cast<const double*>(c->xyz64.p);
+    rp.cl.tri = static_cast<const std::uint32_t*>(c->tri_idx.p);
+    rp.counters = nullptr;
+    nm::k_pair_resolve<<<static_cast<unsigned>((std::size_t(wsum) * 32 + 255) / 256), 256, 0, st>>>(rp);
+    ++launches;
+    NM_CUDA(cudaGetLastError());
+    c->resolved_pairs = total - build_lists();
+  } else {
+    c->resolved_pairs = 0;
   }
-  NM_CUDA(cudaGetLastError());
   return cnt;
 }
 

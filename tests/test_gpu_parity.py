@@ -516,6 +516,45 @@ def test_cell_culling_exact(cfg_id, lo, hi):
     np.testing.assert_allclose(s_cell[pick][sel], s_ref[sel], rtol=0, atol=1e-9)
 
 
+@pytest.mark.parametrize("cfg_id,lo,hi", [(3, 3_000_000, 3_400_000), (5, 4_800_000, 5_200_000)])
+def test_pair_resolve_exact(cfg_id, lo, hi, monkeypatch):
+    """Pairs of uncertified children resolved through a surface-free ball
+    to a certified neighbour (cells.cuh k_pair_resolve) get the exact winding
+    number: masks identical to the pass without the step (NM_NO_RESOLVE=1),
+    s identical except on newly resolved pairs, which are exactly 0 or 1 and
+    agree with the fp64 oracle; far fewer pairs are left to evaluate."""
+    from paper_2203_10000_b200._native import Context
+    cfg = synth.config(cfg_id)
+    S = cfg.surfaces
+    nodes = cfg.lattice_nodes()[lo:hi]
+    out = {}
+    for mode in ("off", "on"):
+        if mode == "off":
+            monkeypatch.setenv("NM_NO_RESOLVE", "1")
+        else:
+            monkeypatch.delenv("NM_NO_RESOLVE", raising=False)
+        with Context(0, cull_outside=2) as c:
+            c.set_surfaces(S.xyz, S.tri, S.comp_off, S.label_ids)
+            s, _ = c.enclosure(nodes)
+            pairs = c.cell_info()["last_pairs"]
+            m, _ = c.label_nodes(nodes)
+        out[mode] = (s, m, pairs)
+    s_off, m_off, p_off = out["off"]
+    s_on, m_on, p_on = out["on"]
+    np.testing.assert_array_equal(m_on, m_off)
+    assert p_on < 0.6 * p_off, (p_on, p_off)
+    diff = s_on != s_off
+    assert diff.any()
+    assert np.all((s_on[diff] == 0.0) | (s_on[diff] == 1.0))
+    assert np.max(np.abs(s_on[diff] - s_off[diff])) < 1e-5
+    rng = np.random.default_rng(cfg_id)
+    rows = np.unique(np.nonzero(diff)[0])
+    pick = np.sort(rng.choice(rows, min(200, rows.size), replace=False))
+    _, s_ref = oracle.label_nodes(nodes[pick], S, want_s=True)
+    sel = diff[pick]
+    np.testing.assert_allclose(s_on[pick][sel], s_ref[sel], rtol=0, atol=1e-9)
+
+
 def test_cell_axis_changes_cost_not_results():
     """nm_options.cell_axis (certified-cell grid resolution) is performance
     only: coarser and finer grids certify different cells but give the same
