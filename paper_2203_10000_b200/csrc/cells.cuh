@@ -414,8 +414,9 @@ static __global__ void k_cell_classify(const ClassifyParams prm) {
 // ---------------------------------------------------------------------------
 // Pairs left unknown by k_cell_classify (points in uncertified children),
 // resolved exactly where a surface-free ball joins them to a certified
-// neighbour (round 2): for the 26 neighbour children of the point's child
-// (or their certified parents) with a known w, gap = |p - c_n| - r_n, where
+// neighbour (round 2): for the neighbour children within kResolveReach of
+// the point's child (or their certified parents) with a known w,
+// gap = |p - c_n| - r_n, where
 // B(c_n, r_n) is the neighbour's certified ball (shrunk by a 1e-9 relative +
 // 1e-9 mm margin). If the best gap < 0, p lies in that ball. Otherwise the
 // pair is resolved when B(p, rho), rho just above the gap, meets no triangle
@@ -447,6 +448,12 @@ struct ResolveParams {
 
 __device__ __forceinline__ int floor_div4(int x) { return x >= 0 ? x / 4 : -((-x + 3) / 4); }
 
+#ifndef NM_RESOLVE_REACH
+#define NM_RESOLVE_REACH 1
+#endif
+constexpr int kResolveReach = NM_RESOLVE_REACH;  // neighbour children searched: (2 reach + 1)^3 - 1
+constexpr double kResolveMaxGap = 1.0 * NM_RESOLVE_REACH;  // ball queries only for gaps below this many child edges
+
 static __global__ void __launch_bounds__(256) k_pair_resolve(const ResolveParams prm) {
   const unsigned w = (blockIdx.x * blockDim.x + threadIdx.x) / 32;
   if (w >= prm.wfirst[prm.K]) return;  // warp-uniform
@@ -476,9 +483,9 @@ static __global__ void __launch_bounds__(256) k_pair_resolve(const ResolveParams
     const int fx = iu * kSubCells + min(static_cast<int>((u - iu) * kSubCells), kSubCells - 1);
     const int fy = iv * kSubCells + min(static_cast<int>((v - iv) * kSubCells), kSubCells - 1);
     const int fz = iw * kSubCells + min(static_cast<int>((ww - iw) * kSubCells), kSubCells - 1);
-    for (int dz = -1; dz <= 1; ++dz)
-      for (int dy = -1; dy <= 1; ++dy)
-        for (int dx = -1; dx <= 1; ++dx) {
+    for (int dz = -kResolveReach; dz <= kResolveReach; ++dz)
+      for (int dy = -kResolveReach; dy <= kResolveReach; ++dy)
+        for (int dx = -kResolveReach; dx <= kResolveReach; ++dx) {
           if (!dx && !dy && !dz) continue;
           const int nx = fx + dx, ny = fy + dy, nz = fz + dz;
           const int px = floor_div4(nx), py = floor_div4(ny), pz = floor_div4(nz);
@@ -514,7 +521,7 @@ static __global__ void __launch_bounds__(256) k_pair_resolve(const ResolveParams
         }
   }
   bool resolved = active && wbest >= 0 && best < -1e-9;
-  const bool query = active && wbest >= 0 && !resolved && best < 0.25 * g.B;
+  const bool query = active && wbest >= 0 && !resolved && best < kResolveMaxGap * b;
   const double rho = query ? fmax(best, 0.0) * (1.0 + 1e-9) + 1e-9 : 0.0;
   unsigned qm = __ballot_sync(kFull, query);
   if (qm) {
