@@ -438,6 +438,7 @@ struct ResolveParams {
   const std::uint32_t* list;           // packed per-compartment lists of evaluation positions
   std::uint32_t off[33], cnt[32];      // compartment k: list[off[k] .. off[k] + cnt[k])
   std::uint32_t wfirst[33];            // first warp of compartment k
+  std::uint32_t ntri[32];              // triangles of compartment k
   std::uint32_t* unk;                  // per position: unknown compartment bits (cleared when resolved)
   std::uint32_t* masks;                // by point id
   double* s_out;
@@ -447,6 +448,66 @@ struct ResolveParams {
 };
 
 __device__ __forceinline__ int floor_div4(int x) { return x >= 0 ? x / 4 : -((-x + 3) / 4); }
+
+// Exact distance from q (centred frame) to the nearest triangle of one
+// compartment, or cap when none is closer: superclusters, clusters and
+// triangle spheres pruned in fp32 with the certification margins against the
+// shrinking bound, then the fp64 point-triangle distance.
+static __device__ double nearest_dist_capped(double qx, double qy, double qz, double cap, double cx, double cy, double cz,
+                                      const float4* __restrict__ sup, int nsup, const float4* __restrict__ clus,
+                                      int nclus, const std::uint32_t* __restrict__ ctri,
+                                      const float4* __restrict__ tsph, const double* __restrict__ xyz,
+                                      const std::uint32_t* __restrict__ tri) {
+  const float fx = static_cast<float>(qx), fy = static_cast<float>(qy), fz = static_cast<float>(qz);
+  const float marg = 1e-3f + 4e-6f * (fabsf(fx) + fabsf(fy) + fabsf(fz));
+  const V3t<double> pt{qx + cx, qy + cy, qz + cz};
+  double best = cap;
+  for (int g = 0; g < nsup; ++g) {
+    const float4 s4 = __ldg(sup + g);
+    const float dx = fx - s4.x, dy = fy - s4.y, dz = fz - s4.z;
+    const float R = static_cast<float>(best) + marg + s4.w;
+    if (dx * dx + dy * dy + dz * dz > R * R) continue;
+    const int q1 = min(nclus, (g + 1) * 32);
+    for (int q = g * 32; q < q1; ++q) {
+      const float4 c4 = __ldg(clus + q);
+      const float ux = fx - c4.x, uy = fy - c4.y, uz = fz - c4.z;
+      const float Rc = static_cast<float>(best) + marg + c4.w;
+      if (ux * ux + uy * uy + uz * uz > Rc * Rc) continue;
+      for (int t = 0; t < kCluster; ++t) {
+        const float4 ts = __ldg(tsph + static_cast<std::size_t>(q) * kCluster + t);
+        if (ts.w < 0.0f) break;  // pads close the cluster
+        const float vx = fx - ts.x, vy = fy - ts.y, vz = fz - ts.z;
+        const float Rt = static_cast<float>(best) + marg + ts.w;
+        if (vx * vx + vy * vy + vz * vz > Rt * Rt) continue;
+        const std::uint32_t tid = __ldg(ctri + static_cast<std::size_t>(q) * kCluster + t);
+        const std::uint32_t* ev = tri + 3 * static_cast<std::size_t>(tid);
+        const double* A = xyz + 3 * static_cast<std::size_t>(ev[0]);
+        const double* Bv = xyz + 3 * static_cast<std::size_t>(ev[1]);
+        const double* Cv = xyz + 3 * static_cast<std::size_t>(ev[2]);
+        const double d2 = point_tri_dist2<double>(pt, {A[0], A[1], A[2]}, {Bv[0], Bv[1], Bv[2]}, {Cv[0], Cv[1], Cv[2]});
+        if (!(d2 >= 0.0)) return 0.0;  // NaN (degenerate triangle): no ball
+        best = fmin(best, sqrt(d2));
+      }
+    }
+  }
+  return best;
+}
+
+// Ball chains per pair: at most kTraceSteps balls, and only for compartments
+// of at least kTraceMinTris triangles (below that, evaluating the pair costs
+// less than the chain: profiles/r02/trace_ab.txt)
+#ifndef NM_TRACE_STEPS
+#define NM_TRACE_STEPS 6
+#endif
+constexpr int kTraceSteps = NM_TRACE_STEPS;
+#ifndef NM_TRACE_MIN_TRIS
+#define NM_TRACE_MIN_TRIS 32768
+#endif
+constexpr std::uint32_t kTraceMinTris = NM_TRACE_MIN_TRIS;
+#ifndef NM_TRACE_STEP
+#define NM_TRACE_STEP 0.9
+#endif
+constexpr double kTraceStep = NM_TRACE_STEP;  // next centre at this fraction of the radius (< 1: inside the ball)
 
 #ifndef NM_RESOLVE_REACH
 #define NM_RESOLVE_REACH 1
@@ -475,7 +536,7 @@ static __global__ void __launch_bounds__(256) k_pair_resolve(const ResolveParams
   // the point's child cell in the compartment's fine lattice (kSubCells per cell)
   const double b = g.B / kSubCells;
   const double rl1 = cell_ball(g.B) * (1.0 - 1e-9) - 1e-9, rch = cell_ball(b) * (1.0 - 1e-9) - 1e-9;
-  double best = 1e300;
+  double best = 1e300, tx = 0.0, ty = 0.0, tz = 0.0, tr = 0.0;  // best gap and its certified ball
   int wbest = -1;
   if (active) {
     const double u = (x - g.ox) / g.B, v = (y - g.oy) / g.B, ww = (z - g.oz) / g.B;
@@ -517,6 +578,10 @@ static __global__ void __launch_bounds__(256) k_pair_resolve(const ResolveParams
           if (gap < best) {
             best = gap;
             wbest = wn;
+            tx = ccx;
+            ty = ccy;
+            tz = ccz;
+            tr = r;
           }
         }
   }
@@ -609,6 +674,50 @@ static __global__ void __launch_bounds__(256) k_pair_resolve(const ResolveParams
   if (prm.counters) {
     const unsigned nb = __popc(__ballot_sync(kFull, resolved && !query));
     if (lane == 0 && nb) atomicAdd(prm.counters, static_cast<unsigned long long>(nb));
+  }
+  // Still open: trace a chain of surface-free balls from p towards the best
+  // neighbour's ball. Each ball B(q, r) has r just below q's exact distance
+  // to the compartment's triangles (nearest_dist_capped), the next centre is
+  // 0.9 r further along the line to the neighbour's centre (inside the
+  // current ball, so consecutive balls overlap), and the chain ends when a
+  // ball reaches the neighbour's ball. A line that runs into the surface
+  // stops (radius below 1e-6 child edges or kTraceSteps balls): the pair is
+  // then evaluated as before. Compartments below kTraceMinTris triangles skip
+  // the chains.
+  const bool trace = active && wbest >= 0 && !resolved && prm.ntri[k] >= kTraceMinTris;
+  if (trace) {
+    const float4* sup = prm.cl.sup + prm.cl.soff[k];
+    const int nsup = static_cast<int>(prm.cl.soff[k + 1] - prm.cl.soff[k]);
+    const std::uint32_t c0 = prm.cl.coff[k];
+    const int nclus = static_cast<int>(prm.cl.coff[k + 1] - c0);
+    double qx = x, qy = y, qz = z;
+    const double rmin = 1e-6 * b;
+    for (int step = 0; step < kTraceSteps; ++step) {
+      const double ex = tx - qx, ey = ty - qy, ez = tz - qz;
+      const double len = sqrt(ex * ex + ey * ey + ez * ez);
+      const double need = len - tr;  // a ball of radius > need around q meets the neighbour's ball
+      if (need < -1e-9) {
+        resolved = true;
+        break;
+      }
+      const double d = nearest_dist_capped(qx, qy, qz, need * (1.0 + 1e-6) + 2e-9, prm.cx, prm.cy, prm.cz, sup, nsup,
+                                           prm.cl.clus + c0, nclus, prm.cl.clus_tri + static_cast<std::size_t>(c0) * kCluster,
+                                           prm.cl.tsph + static_cast<std::size_t>(c0) * kCluster, prm.cl.xyz, prm.cl.tri);
+      const double r = d * (1.0 - 1e-9) - 1e-9;
+      if (r > need + 1e-9) {
+        resolved = true;
+        break;
+      }
+      if (r < rmin) break;  // running into the surface
+      const double f = kTraceStep * r / len;
+      qx += f * ex;
+      qy += f * ey;
+      qz += f * ez;
+    }
+  }
+  if (prm.counters) {
+    const unsigned nt = __popc(__ballot_sync(kFull, trace && resolved));
+    if (lane == 0 && nt) atomicAdd(prm.counters + 2, static_cast<unsigned long long>(nt));
   }
   if (resolved) {
     atomicAnd(prm.unk + i, ~(1u << k));

@@ -199,6 +199,7 @@ std::vector<std::uint32_t> classify_cells(nm_ctx* c, const double* d_pts, std::s
     for (int k = 0; k < K; ++k) {
       rp.off[k] = o;
       rp.cnt[k] = cnt[k];
+      rp.ntri[k] = c->comp_off_h[k + 1] - c->comp_off_h[k];
       rp.wfirst[k] = wsum;
       o += cnt[k];
       wsum += (cnt[k] + 31) / 32;
