@@ -681,8 +681,11 @@ static __global__ void __launch_bounds__(kSelBlock) k_select_count(Pred pred, st
   if (threadIdx.x == 0) chunk_counts[blockIdx.x] = static_cast<std::uint32_t>(total);
 }
 
-// Single-CTA exclusive scan of chunk counts; writes the grand total.
+// Single-CTA exclusive scan of chunk counts; writes the grand total. With
+// gridDim.x > 1, CTA k scans counts[k nb, (k + 1) nb) into d_total[k].
 static __global__ void __launch_bounds__(1024) k_select_scan(std::uint32_t* counts, std::size_t nb, std::uint32_t* d_total) {
+  counts += blockIdx.x * nb;
+  d_total += blockIdx.x;
   __shared__ std::uint32_t warp_sums[32];
   __shared__ std::uint32_t carry;
   if (threadIdx.x == 0) carry = 0;
@@ -730,6 +733,49 @@ static __global__ void __launch_bounds__(kSelBlock) k_select_write(Pred pred, st
   for (int j = 0; j < kSelItems; ++j) {
     const std::size_t i = b0 + j * kSelBlock + threadIdx.x;
     const bool p = i < n && pred(i);
+    const unsigned bal = __ballot_sync(kFull, p);
+    if (lane == 0) warp_cnt[w] = __popc(bal);
+    __syncthreads();
+    std::uint32_t before = 0, tot = 0;
+#pragma unroll
+    for (int q = 0; q < kSelBlock / 32; ++q) {
+      const std::uint32_t c = warp_cnt[q];
+      before += q < w ? c : 0u;
+      tot += c;
+    }
+    if (p) out[running + before + __popc(bal & ((1u << lane) - 1u))] = static_cast<std::uint32_t>(i);
+    running += tot;
+    __syncthreads();
+  }
+}
+
+// All compartments' lists in one launch each (gridDim.y = compartments):
+// list k holds the positions with bit k of v set, lists packed in k order.
+static __global__ void __launch_bounds__(kSelBlock) k_select_count_bits(const std::uint32_t* __restrict__ v,
+                                                                         std::size_t n, std::uint32_t* chunk_counts) {
+  const std::size_t b0 = static_cast<std::size_t>(blockIdx.x) * kSelChunk;
+  const unsigned bit = 1u << blockIdx.y;
+  int total = 0;
+#pragma unroll
+  for (int j = 0; j < kSelItems; ++j) {
+    const std::size_t i = b0 + j * kSelBlock + threadIdx.x;
+    total += __syncthreads_count(i < n && (v[i] & bit));
+  }
+  if (threadIdx.x == 0) chunk_counts[static_cast<std::size_t>(blockIdx.y) * gridDim.x + blockIdx.x] = static_cast<std::uint32_t>(total);
+}
+static __global__ void __launch_bounds__(kSelBlock) k_select_write_bits(const std::uint32_t* __restrict__ v, std::size_t n,
+                                                                         const std::uint32_t* chunk_offsets,
+                                                                         const std::uint32_t* totals, std::uint32_t* out) {
+  __shared__ std::uint32_t warp_cnt[kSelBlock / 32];
+  const std::size_t b0 = static_cast<std::size_t>(blockIdx.x) * kSelChunk;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const unsigned bit = 1u << blockIdx.y;
+  std::uint32_t running = chunk_offsets[static_cast<std::size_t>(blockIdx.y) * gridDim.x + blockIdx.x];
+  for (unsigned q = 0; q < blockIdx.y; ++q) running += totals[q];  // the lists before k
+#pragma unroll 1
+  for (int j = 0; j < kSelItems; ++j) {
+    const std::size_t i = b0 + j * kSelBlock + threadIdx.x;
+    const bool p = i < n && (v[i] & bit);
     const unsigned bal = __ballot_sync(kFull, p);
     if (lane == 0) warp_cnt[w] = __popc(bal);
     __syncthreads();

@@ -127,7 +127,6 @@ std::vector<std::uint32_t> classify_cells(nm_ctx* c, const double* d_pts, std::s
   const std::size_t nb = std::max<std::size_t>(1, (n + nm::kSelChunk - 1) / nm::kSelChunk);
   auto* chunk = c->sp_chunk.as<std::uint32_t>(nb * K);
   auto* dcnt = c->sp_cnt.as<std::uint32_t>(K);
-  (void)c->sp_list.as<std::uint32_t>(n);  // grown below if needed (after the sync)
   nm::ClassifyParams cp{};
   cp.pts = d_pts;
   cp.n = n;
@@ -150,32 +149,30 @@ std::vector<std::uint32_t> classify_cells(nm_ctx* c, const double* d_pts, std::s
   // per-compartment ordered lists of the unknown pairs (counts read back:
   // one host synchronisation per list build)
   std::vector<std::uint32_t> cnt(K);
+  // (all compartments in one launch per step; the counts are read back
+  // before the write so the list is sized exactly)
   auto build_lists = [&]() {
-    for (int k = 0; k < K; ++k) {
-      nm::k_select_count<<<static_cast<unsigned>(nb), nm::kSelBlock, 0, st>>>(nm::PredBit{unk, k}, n, chunk + k * nb);
-      nm::k_select_scan<<<1, 1024, 0, st>>>(chunk + k * nb, nb, dcnt + k);
-      launches += 2;
-    }
+    const dim3 g(static_cast<unsigned>(nb), static_cast<unsigned>(K));
+    nm::k_select_count_bits<<<g, nm::kSelBlock, 0, st>>>(unk, n, chunk);
+    nm::k_select_scan<<<K, 1024, 0, st>>>(chunk, nb, dcnt);
+    launches += 2;
     // (through the context's pinned words: a pageable read-back would be a
     // driver-staged copy, serialised with other host threads' copies)
     NM_CUDA(cudaMemcpyAsync(c->h_pcnt, dcnt, K * sizeof(std::uint32_t), cudaMemcpyDeviceToHost, st));
     NM_CUDA(cudaStreamSynchronize(st));
     cnt.assign(c->h_pcnt, c->h_pcnt + K);
     std::size_t total = 0;
-    for (int k = 0; k < K; ++k) total += cnt[k];
-    if (total > 0xffffffffull) throw Error("more than 2^32 (point, compartment) pairs to evaluate in one call");
-    auto* list = c->sp_list.as<std::uint32_t>(std::max<std::size_t>(total, 1));
-    std::size_t off = 0;
-    c->sparse_pairs = total;
     c->sparse_evals = 0;
     for (int k = 0; k < K; ++k) {
-      if (cnt[k]) {
-        nm::k_select_write<<<static_cast<unsigned>(nb), nm::kSelBlock, 0, st>>>(nm::PredBit{unk, k}, n,
-                                                                                chunk + k * nb, list + off);
-        ++launches;
-      }
-      off += cnt[k];
+      total += cnt[k];
       c->sparse_evals += std::uint64_t(cnt[k]) * (c->comp_off_h[k + 1] - c->comp_off_h[k]);
+    }
+    if (total > 0xffffffffull) throw Error("more than 2^32 (point, compartment) pairs to evaluate in one call");
+    c->sparse_pairs = total;
+    auto* list = c->sp_list.as<std::uint32_t>(std::max<std::size_t>(total, 1));
+    if (total) {
+      nm::k_select_write_bits<<<g, nm::kSelBlock, 0, st>>>(unk, n, chunk, dcnt, list);
+      ++launches;
     }
     NM_CUDA(cudaGetLastError());
     return total;
