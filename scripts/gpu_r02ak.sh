@@ -1,0 +1,8 @@
+#!/bin/bash
+# multi-compartment list builds: cell/cull + dropin tests, node pass timings
+cd "$GRAFT_REPO_ROOT"
+O=gpurun_out/r02ak
+mkdir -p $O
+timeout 1800 python -m pytest tests/test_gpu_parity.py tests/test_gpu_parity_scale.py tests/test_gpu_dropin.py -x -q -m gpu > $O/pytest.log 2>&1
+echo "pytest exit $?" >> $O/pytest.log
+for c in 5 3 2; do python scripts/cells_quick.py $c > $O/cells_cfg${c}.txt 2>&1; done
