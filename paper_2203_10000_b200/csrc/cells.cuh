@@ -449,53 +449,57 @@ struct ResolveParams {
 
 __device__ __forceinline__ int floor_div4(int x) { return x >= 0 ? x / 4 : -((-x + 3) / 4); }
 
-// Exact distance from q (centred frame) to the nearest triangle of one
-// compartment, or cap when none is closer: superclusters, clusters and
-// triangle spheres pruned in fp32 with the certification margins against the
-// shrinking bound, then the fp64 point-triangle distance.
-static __device__ double nearest_dist_capped(double qx, double qy, double qz, double cap, double cx, double cy, double cz,
-                                      const float4* __restrict__ sup, int nsup, const float4* __restrict__ clus,
-                                      int nclus, const std::uint32_t* __restrict__ ctri,
-                                      const float4* __restrict__ tsph, const double* __restrict__ xyz,
-                                      const std::uint32_t* __restrict__ tri) {
+// Exact distance from q (centred frame, the same q in every lane) to the
+// nearest triangle of one compartment, or cap when none is closer; the whole
+// warp works on the one query: 32 superclusters, then a candidate's 32
+// clusters, then a cluster's 32 triangle spheres per step, pruned in fp32
+// with the certification margins against the shrinking bound; each lane
+// takes the exact fp64 distance of its candidate triangle, warp minimum.
+static __device__ double warp_nearest_dist(double qx, double qy, double qz, double cap, double cx, double cy, double cz,
+                                           const float4* __restrict__ sup, int nsup, const float4* __restrict__ clus,
+                                           int nclus, const std::uint32_t* __restrict__ ctri,
+                                           const float4* __restrict__ tsph, const double* __restrict__ xyz,
+                                           const std::uint32_t* __restrict__ tri) {
+  const int lane = threadIdx.x & 31;
   const float fx = static_cast<float>(qx), fy = static_cast<float>(qy), fz = static_cast<float>(qz);
   const float marg = 1e-3f + 4e-6f * (fabsf(fx) + fabsf(fy) + fabsf(fz));
   const V3t<double> pt{qx + cx, qy + cy, qz + cz};
-  double best = cap;
-  for (int g = 0; g < nsup; ++g) {
-    const float4 s4 = __ldg(sup + g);
+  double best = cap;  // warp-uniform
+  auto near = [&](const float4& s4) {
     const float dx = fx - s4.x, dy = fy - s4.y, dz = fz - s4.z;
     const float R = static_cast<float>(best) + marg + s4.w;
-    if (dx * dx + dy * dy + dz * dz > R * R) continue;
-    const int q1 = min(nclus, (g + 1) * 32);
-    for (int q = g * 32; q < q1; ++q) {
-      const float4 c4 = __ldg(clus + q);
-      const float ux = fx - c4.x, uy = fy - c4.y, uz = fz - c4.z;
-      const float Rc = static_cast<float>(best) + marg + c4.w;
-      if (ux * ux + uy * uy + uz * uz > Rc * Rc) continue;
-      for (int t = 0; t < kCluster; ++t) {
-        const float4 ts = __ldg(tsph + static_cast<std::size_t>(q) * kCluster + t);
-        if (ts.w < 0.0f) break;  // pads close the cluster
-        const float vx = fx - ts.x, vy = fy - ts.y, vz = fz - ts.z;
-        const float Rt = static_cast<float>(best) + marg + ts.w;
-        if (vx * vx + vy * vy + vz * vz > Rt * Rt) continue;
-        const std::uint32_t tid = __ldg(ctri + static_cast<std::size_t>(q) * kCluster + t);
-        const std::uint32_t* ev = tri + 3 * static_cast<std::size_t>(tid);
-        const double* A = xyz + 3 * static_cast<std::size_t>(ev[0]);
-        const double* Bv = xyz + 3 * static_cast<std::size_t>(ev[1]);
-        const double* Cv = xyz + 3 * static_cast<std::size_t>(ev[2]);
-        const double d2 = point_tri_dist2<double>(pt, {A[0], A[1], A[2]}, {Bv[0], Bv[1], Bv[2]}, {Cv[0], Cv[1], Cv[2]});
-        if (!(d2 >= 0.0)) return 0.0;  // NaN (degenerate triangle): no ball
-        best = fmin(best, sqrt(d2));
+    return dx * dx + dy * dy + dz * dz <= R * R;
+  };
+  for (int g0 = 0; g0 < nsup; g0 += 32) {
+    unsigned sb = __ballot_sync(kFull, g0 + lane < nsup && near(__ldg(sup + g0 + lane)));
+    while (sb) {
+      const int g = g0 + __ffs(sb) - 1;
+      sb &= sb - 1;
+      const int q = g * 32 + lane;
+      unsigned cb = __ballot_sync(kFull, q < nclus && near(__ldg(clus + q)));
+      while (cb) {
+        const int qc = g * 32 + __ffs(cb) - 1;
+        cb &= cb - 1;
+        const float4 ts = __ldg(tsph + static_cast<std::size_t>(qc) * kCluster + lane);
+        double d = 1e300;
+        if (ts.w >= 0.0f && near(ts)) {
+          const std::uint32_t tid = __ldg(ctri + static_cast<std::size_t>(qc) * kCluster + lane);
+          const std::uint32_t* ev = tri + 3 * static_cast<std::size_t>(tid);
+          const double* A = xyz + 3 * static_cast<std::size_t>(ev[0]);
+          const double* Bv = xyz + 3 * static_cast<std::size_t>(ev[1]);
+          const double* Cv = xyz + 3 * static_cast<std::size_t>(ev[2]);
+          const double d2 = point_tri_dist2<double>(pt, {A[0], A[1], A[2]}, {Bv[0], Bv[1], Bv[2]}, {Cv[0], Cv[1], Cv[2]});
+          d = d2 >= 0.0 ? sqrt(d2) : 0.0;  // NaN (degenerate triangle): no ball
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) d = fmin(d, __shfl_xor_sync(kFull, d, o));
+        best = fmin(best, d);
       }
     }
   }
   return best;
 }
 
-// Ball chains per pair: at most kTraceSteps balls, and only for compartments
-// of at least kTraceMinTris triangles (below that, evaluating the pair costs
-// less than the chain: profiles/r02/trace_ab.txt)
 #ifndef NM_TRACE_STEPS
 #define NM_TRACE_STEPS 6
 #endif
@@ -586,138 +590,64 @@ static __global__ void __launch_bounds__(256) k_pair_resolve(const ResolveParams
         }
   }
   bool resolved = active && wbest >= 0 && best < -1e-9;
-  const bool query = active && wbest >= 0 && !resolved && best < kResolveMaxGap * b;
-  const double rho = query ? fmax(best, 0.0) * (1.0 + 1e-9) + 1e-9 : 0.0;
-  unsigned qm = __ballot_sync(kFull, query);
-  if (qm) {
-    // warp ball over the querying lanes (fp32, with margins)
-    const float fx = static_cast<float>(x), fy = static_cast<float>(y), fz = static_cast<float>(z);
-    float lo[3] = {query ? fx : 3e38f, query ? fy : 3e38f, query ? fz : 3e38f};
-    float hi[3] = {query ? fx : -3e38f, query ? fy : -3e38f, query ? fz : -3e38f};
-#pragma unroll
-    for (int a = 0; a < 3; ++a)
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        lo[a] = fminf(lo[a], __shfl_xor_sync(kFull, lo[a], o));
-        hi[a] = fmaxf(hi[a], __shfl_xor_sync(kFull, hi[a], o));
-      }
-    const float bx = 0.5f * (lo[0] + hi[0]), by = 0.5f * (lo[1] + hi[1]), bz = 0.5f * (lo[2] + hi[2]);
-    const float frb = static_cast<float>(rho) + 1e-3f + 4e-6f * (fabsf(fx) + fabsf(fy) + fabsf(fz));
-    float reach = 0.0f;
-    if (query) {
-      const float dx = fx - bx, dy = fy - by, dz = fz - bz;
-      reach = sqrtf(dx * dx + dy * dy + dz * dz) * (1.0f + 1e-6f) + frb;
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) reach = fmaxf(reach, __shfl_xor_sync(kFull, reach, o));
-    const float fbr = reach + 1e-3f + 4e-6f * (fabsf(bx) + fabsf(by) + fabsf(bz));
-    const std::uint32_t c0 = prm.cl.coff[k];
-    const int nclus = static_cast<int>(prm.cl.coff[k + 1] - c0);
+  // Not inside: a chain of surface-free balls from p towards the best
+  // neighbour's ball, one lane's chain at a time with the whole warp on each
+  // nearest-triangle query (warp_nearest_dist). Each ball B(q, r) has r just
+  // below q's exact distance to the compartment's triangles; the next centre
+  // is kTraceStep r further along the line to the neighbour's centre (inside
+  // the current ball, so consecutive balls overlap); the chain succeeds when
+  // a ball reaches the neighbour's ball. The first ball alone is the test
+  // "B(p, gap) meets no triangle"; compartments of at least kTraceMinTris
+  // triangles go on for up to kTraceSteps balls. A line that runs into the
+  // surface stops (radius below 1e-6 child edges): the pair is evaluated.
+  const bool pending = active && wbest >= 0 && !resolved && best < kResolveMaxGap * b;
+  const int steps = prm.ntri[k] >= kTraceMinTris ? kTraceSteps : 1;
+  unsigned pm = __ballot_sync(kFull, pending);
+  if (pm) {
     const float4* sup = prm.cl.sup + prm.cl.soff[k];
     const int nsup = static_cast<int>(prm.cl.soff[k + 1] - prm.cl.soff[k]);
+    const std::uint32_t c0 = prm.cl.coff[k];
+    const int nclus = static_cast<int>(prm.cl.coff[k + 1] - c0);
     const float4* clus = prm.cl.clus + c0;
     const std::uint32_t* ctri = prm.cl.clus_tri + static_cast<std::size_t>(c0) * kCluster;
     const float4* tsph = prm.cl.tsph + static_cast<std::size_t>(c0) * kCluster;
-    const V3t<double> pt{x + prm.cx, y + prm.cy, z + prm.cz};
-    const double lim = rho * (1.0 + 1e-9);
-    bool hit = !query;
-    for (int g0 = 0; g0 < nsup && !__all_sync(kFull, hit); g0 += 32) {
-      bool scand = false;
-      if (g0 + lane < nsup) {
-        const float4 s4 = __ldg(sup + g0 + lane);
-        const float dx = bx - s4.x, dy = by - s4.y, dz = bz - s4.z;
-        const float R = fbr + s4.w;
-        scand = dx * dx + dy * dy + dz * dz <= R * R;
-      }
-      unsigned sbal = __ballot_sync(kFull, scand);
-      while (sbal) {
-        const int q0 = (g0 + __ffs(sbal) - 1) * 32;
-        sbal &= sbal - 1;
-        bool cand = false;
-        if (q0 + lane < nclus) {
-          const float4 s4 = __ldg(clus + q0 + lane);
-          const float dx = bx - s4.x, dy = by - s4.y, dz = bz - s4.z;
-          const float R = fbr + s4.w;
-          cand = dx * dx + dy * dy + dz * dz <= R * R;
-        }
-        unsigned bal = __ballot_sync(kFull, cand);
-        while (bal) {
-          const int q = q0 + __ffs(bal) - 1;
-          bal &= bal - 1;
-          if (hit) continue;
-          const float4 s4 = __ldg(clus + q);
-          const float dx = fx - s4.x, dy = fy - s4.y, dz = fz - s4.z;
-          const float R = frb + s4.w;
-          if (dx * dx + dy * dy + dz * dz > R * R) continue;
-          for (int t = 0; t < kCluster && !hit; ++t) {
-            const float4 ts = __ldg(tsph + static_cast<std::size_t>(q) * kCluster + t);
-            if (ts.w < 0.0f) break;  // pads close the cluster
-            const float tx = fx - ts.x, ty = fy - ts.y, tz = fz - ts.z;
-            const float TR = frb + ts.w;
-            if (tx * tx + ty * ty + tz * tz > TR * TR) continue;
-            const std::uint32_t tid = __ldg(ctri + static_cast<std::size_t>(q) * kCluster + t);
-            const std::uint32_t* ev = prm.cl.tri + 3 * static_cast<std::size_t>(tid);
-            const double* A = prm.cl.xyz + 3 * static_cast<std::size_t>(ev[0]);
-            const double* Bv = prm.cl.xyz + 3 * static_cast<std::size_t>(ev[1]);
-            const double* Cv = prm.cl.xyz + 3 * static_cast<std::size_t>(ev[2]);
-            const double d2 =
-                point_tri_dist2<double>(pt, {A[0], A[1], A[2]}, {Bv[0], Bv[1], Bv[2]}, {Cv[0], Cv[1], Cv[2]});
-            hit = !(d2 > lim * lim);  // NaN (degenerate) counts as a hit
-          }
-        }
-      }
-    }
-    if (query && !hit) resolved = true;
-    const unsigned nq = __popc(__ballot_sync(kFull, query && !hit));
-    if (prm.counters && lane == 0 && nq) atomicAdd(prm.counters + 1, static_cast<unsigned long long>(nq));
-  }
-  if (prm.counters) {
-    const unsigned nb = __popc(__ballot_sync(kFull, resolved && !query));
-    if (lane == 0 && nb) atomicAdd(prm.counters, static_cast<unsigned long long>(nb));
-  }
-  // Still open: trace a chain of surface-free balls from p towards the best
-  // neighbour's ball. Each ball B(q, r) has r just below q's exact distance
-  // to the compartment's triangles (nearest_dist_capped), the next centre is
-  // 0.9 r further along the line to the neighbour's centre (inside the
-  // current ball, so consecutive balls overlap), and the chain ends when a
-  // ball reaches the neighbour's ball. A line that runs into the surface
-  // stops (radius below 1e-6 child edges or kTraceSteps balls): the pair is
-  // then evaluated as before. Compartments below kTraceMinTris triangles skip
-  // the chains.
-  const bool trace = active && wbest >= 0 && !resolved && prm.ntri[k] >= kTraceMinTris;
-  if (trace) {
-    const float4* sup = prm.cl.sup + prm.cl.soff[k];
-    const int nsup = static_cast<int>(prm.cl.soff[k + 1] - prm.cl.soff[k]);
-    const std::uint32_t c0 = prm.cl.coff[k];
-    const int nclus = static_cast<int>(prm.cl.coff[k + 1] - c0);
-    double qx = x, qy = y, qz = z;
     const double rmin = 1e-6 * b;
-    for (int step = 0; step < kTraceSteps; ++step) {
-      const double ex = tx - qx, ey = ty - qy, ez = tz - qz;
-      const double len = sqrt(ex * ex + ey * ey + ez * ez);
-      const double need = len - tr;  // a ball of radius > need around q meets the neighbour's ball
-      if (need < -1e-9) {
-        resolved = true;
-        break;
+    while (pm) {
+      const int L = __ffs(pm) - 1;
+      pm &= pm - 1;
+      double qx = __shfl_sync(kFull, x, L), qy = __shfl_sync(kFull, y, L), qz = __shfl_sync(kFull, z, L);
+      const double ux = __shfl_sync(kFull, tx, L), uy = __shfl_sync(kFull, ty, L), uz = __shfl_sync(kFull, tz, L);
+      const double ur = __shfl_sync(kFull, tr, L);
+      bool ok = false;  // warp-uniform
+      for (int step = 0; step < steps; ++step) {
+        const double ex = ux - qx, ey = uy - qy, ez = uz - qz;
+        const double len = sqrt(ex * ex + ey * ey + ez * ez);
+        const double need = len - ur;  // a ball of radius > need around q meets the neighbour's ball
+        if (need < -1e-9) {
+          ok = true;
+          break;
+        }
+        const double d = warp_nearest_dist(qx, qy, qz, need * (1.0 + 1e-6) + 2e-9, prm.cx, prm.cy, prm.cz, sup, nsup,
+                                           clus, nclus, ctri, tsph, prm.cl.xyz, prm.cl.tri);
+        const double r = d * (1.0 - 1e-9) - 1e-9;
+        if (r > need + 1e-9) {
+          ok = true;
+          break;
+        }
+        if (r < rmin) break;  // running into the surface
+        const double f = kTraceStep * r / len;
+        qx += f * ex;
+        qy += f * ey;
+        qz += f * ez;
       }
-      const double d = nearest_dist_capped(qx, qy, qz, need * (1.0 + 1e-6) + 2e-9, prm.cx, prm.cy, prm.cz, sup, nsup,
-                                           prm.cl.clus + c0, nclus, prm.cl.clus_tri + static_cast<std::size_t>(c0) * kCluster,
-                                           prm.cl.tsph + static_cast<std::size_t>(c0) * kCluster, prm.cl.xyz, prm.cl.tri);
-      const double r = d * (1.0 - 1e-9) - 1e-9;
-      if (r > need + 1e-9) {
-        resolved = true;
-        break;
-      }
-      if (r < rmin) break;  // running into the surface
-      const double f = kTraceStep * r / len;
-      qx += f * ex;
-      qy += f * ey;
-      qz += f * ez;
+      if (lane == L) resolved = ok;
     }
   }
   if (prm.counters) {
-    const unsigned nt = __popc(__ballot_sync(kFull, trace && resolved));
-    if (lane == 0 && nt) atomicAdd(prm.counters + 2, static_cast<unsigned long long>(nt));
+    const unsigned nb = __popc(__ballot_sync(kFull, resolved && !pending));
+    const unsigned nt = __popc(__ballot_sync(kFull, resolved && pending));
+    if (lane == 0 && nb) atomicAdd(prm.counters, static_cast<unsigned long long>(nb));
+    if (lane == 0 && nt) atomicAdd(prm.counters + 1, static_cast<unsigned long long>(nt));
   }
   if (resolved) {
     atomicAnd(prm.unk + i, ~(1u << k));
