@@ -517,7 +517,10 @@ constexpr double kTraceStep = NM_TRACE_STEP;  // next centre at this fraction of
 #define NM_RESOLVE_REACH 1
 #endif
 constexpr int kResolveReach = NM_RESOLVE_REACH;  // neighbour children searched: (2 reach + 1)^3 - 1
-constexpr double kResolveMaxGap = 1.0 * NM_RESOLVE_REACH;  // ball queries only for gaps below this many child edges
+#ifndef NM_RESOLVE_MAXGAP
+#define NM_RESOLVE_MAXGAP 1.0
+#endif
+constexpr double kResolveMaxGap = NM_RESOLVE_MAXGAP;  // ball chains only for gaps below this many child edges
 
 static __global__ void __launch_bounds__(256) k_pair_resolve(const ResolveParams prm) {
   const unsigned w = (blockIdx.x * blockDim.x + threadIdx.x) / 32;
