@@ -438,7 +438,7 @@ struct ResolveParams {
   const std::uint32_t* list;           // packed per-compartment lists of evaluation positions
   std::uint32_t off[33], cnt[32];      // compartment k: list[off[k] .. off[k] + cnt[k])
   std::uint32_t wfirst[33];            // first warp of compartment k
-  std::uint32_t ntri[32];              // triangles of compartment k
+  int trace_steps;                     // balls per chain (1: the ball test alone)
   std::uint32_t* unk;                  // per position: unknown compartment bits (cleared when resolved)
   std::uint32_t* masks;                // by point id
   double* s_out;
@@ -500,14 +500,18 @@ static __device__ double warp_nearest_dist(double qx, double qy, double qz, doub
   return best;
 }
 
+// Ball chains per pair: at most kTraceSteps balls when the listed pairs
+// would cost at least kTraceMinEvals point-triangle evaluations (below that,
+// one ball per pair: evaluating the pairs costs less than the serial chains;
+// profiles/r02/trace_ab_coop.txt). The host picks ResolveParams::trace_steps.
 #ifndef NM_TRACE_STEPS
-#define NM_TRACE_STEPS 6
+#define NM_TRACE_STEPS 12
 #endif
 constexpr int kTraceSteps = NM_TRACE_STEPS;
-#ifndef NM_TRACE_MIN_TRIS
-#define NM_TRACE_MIN_TRIS 32768
+#ifndef NM_TRACE_MIN_EVALS
+#define NM_TRACE_MIN_EVALS 5e8
 #endif
-constexpr std::uint32_t kTraceMinTris = NM_TRACE_MIN_TRIS;
+constexpr double kTraceMinEvals = NM_TRACE_MIN_EVALS;
 #ifndef NM_TRACE_STEP
 #define NM_TRACE_STEP 0.9
 #endif
@@ -600,11 +604,11 @@ static __global__ void __launch_bounds__(256) k_pair_resolve(const ResolveParams
   // is kTraceStep r further along the line to the neighbour's centre (inside
   // the current ball, so consecutive balls overlap); the chain succeeds when
   // a ball reaches the neighbour's ball. The first ball alone is the test
-  // "B(p, gap) meets no triangle"; compartments of at least kTraceMinTris
-  // triangles go on for up to kTraceSteps balls. A line that runs into the
-  // surface stops (radius below 1e-6 child edges): the pair is evaluated.
+  // "B(p, gap) meets no triangle"; calls with enough work go on for up to
+  // kTraceSteps balls. A line that runs into the surface stops (radius below
+  // 1e-6 child edges): the pair is evaluated.
   const bool pending = active && wbest >= 0 && !resolved && best < kResolveMaxGap * b;
-  const int steps = prm.ntri[k] >= kTraceMinTris ? kTraceSteps : 1;
+  const int steps = prm.trace_steps;
   unsigned pm = __ballot_sync(kFull, pending);
   if (pm) {
     const float4* sup = prm.cl.sup + prm.cl.soff[k];

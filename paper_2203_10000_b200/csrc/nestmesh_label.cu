@@ -196,7 +196,6 @@ std::vector<std::uint32_t> classify_cells(nm_ctx* c, const double* d_pts, std::s
     for (int k = 0; k < K; ++k) {
       rp.off[k] = o;
       rp.cnt[k] = cnt[k];
-      rp.ntri[k] = c->comp_off_h[k + 1] - c->comp_off_h[k];
       rp.wfirst[k] = wsum;
       o += cnt[k];
       wsum += (cnt[k] + 31) / 32;
@@ -216,6 +215,7 @@ std::vector<std::uint32_t> classify_cells(nm_ctx* c, const double* d_pts, std::s
     rp.cl.xyz = static_cast<const double*>(c->xyz64.p);
     rp.cl.tri = static_cast<const std::uint32_t*>(c->tri_idx.p);
     rp.counters = nullptr;
+    rp.trace_steps = double(c->sparse_evals) >= nm::kTraceMinEvals ? nm::kTraceSteps : 1;
     nm::k_pair_resolve<<<static_cast<unsigned>((std::size_t(wsum) * 32 + 255) / 256), 256, 0, st>>>(rp);
     ++launches;
     NM_CUDA(cudaGetLastError());
