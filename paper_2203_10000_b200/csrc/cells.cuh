@@ -427,6 +427,12 @@ static __global__ void k_cell_classify(const ClassifyParams prm) {
 // the surface: w(p) = w_n exactly. Resolved pairs get their bit (when the
 // caller writes known bits) and s = w, and leave the pair lists.
 // ---------------------------------------------------------------------------
+struct PendPair {
+  std::uint32_t i, j, k, w;  // evaluation position, point id, compartment, the neighbour's w
+  double p[3];               // point (centred frame)
+  double t[4];               // the neighbour's certified ball: centre, radius
+};
+
 struct ResolveParams {
   const double* pts;
   const std::uint32_t* order;
@@ -438,7 +444,8 @@ struct ResolveParams {
   const std::uint32_t* list;           // packed per-compartment lists of evaluation positions
   std::uint32_t off[33], cnt[32];      // compartment k: list[off[k] .. off[k] + cnt[k])
   std::uint32_t wfirst[33];            // first warp of compartment k
-  int trace_steps;                     // balls per chain (1: the ball test alone)
+  struct PendPair* pend;               // pairs for k_pair_chain (appended)
+  unsigned* npend;
   std::uint32_t* unk;                  // per position: unknown compartment bits (cleared when resolved)
   std::uint32_t* masks;                // by point id
   double* s_out;
@@ -500,18 +507,11 @@ static __device__ double warp_nearest_dist(double qx, double qy, double qz, doub
   return best;
 }
 
-// Ball chains per pair: at most kTraceSteps balls when the listed pairs
-// would cost at least kTraceMinEvals point-triangle evaluations (below that,
-// one ball per pair: evaluating the pairs costs less than the serial chains;
-// profiles/r02/trace_ab_coop.txt). The host picks ResolveParams::trace_steps.
+// balls per chain (k_pair_chain; profiles/r02/trace_ab_coop.txt)
 #ifndef NM_TRACE_STEPS
 #define NM_TRACE_STEPS 12
 #endif
 constexpr int kTraceSteps = NM_TRACE_STEPS;
-#ifndef NM_TRACE_MIN_EVALS
-#define NM_TRACE_MIN_EVALS 5e8
-#endif
-constexpr double kTraceMinEvals = NM_TRACE_MIN_EVALS;
 #ifndef NM_TRACE_STEP
 #define NM_TRACE_STEP 0.9
 #endif
@@ -596,70 +596,83 @@ static __global__ void __launch_bounds__(256) k_pair_resolve(const ResolveParams
           }
         }
   }
-  bool resolved = active && wbest >= 0 && best < -1e-9;
-  // Not inside: a chain of surface-free balls from p towards the best
-  // neighbour's ball, one lane's chain at a time with the whole warp on each
-  // nearest-triangle query (warp_nearest_dist). Each ball B(q, r) has r just
-  // below q's exact distance to the compartment's triangles; the next centre
-  // is kTraceStep r further along the line to the neighbour's centre (inside
-  // the current ball, so consecutive balls overlap); the chain succeeds when
-  // a ball reaches the neighbour's ball. The first ball alone is the test
-  // "B(p, gap) meets no triangle"; calls with enough work go on for up to
-  // kTraceSteps balls. A line that runs into the surface stops (radius below
-  // 1e-6 child edges): the pair is evaluated.
+  const bool resolved = active && wbest >= 0 && best < -1e-9;
+  // not inside: a chain of balls towards the best neighbour (k_pair_chain),
+  // one record per pending pair
   const bool pending = active && wbest >= 0 && !resolved && best < kResolveMaxGap * b;
-  const int steps = prm.trace_steps;
-  unsigned pm = __ballot_sync(kFull, pending);
-  if (pm) {
-    const float4* sup = prm.cl.sup + prm.cl.soff[k];
-    const int nsup = static_cast<int>(prm.cl.soff[k + 1] - prm.cl.soff[k]);
-    const std::uint32_t c0 = prm.cl.coff[k];
-    const int nclus = static_cast<int>(prm.cl.coff[k + 1] - c0);
-    const float4* clus = prm.cl.clus + c0;
-    const std::uint32_t* ctri = prm.cl.clus_tri + static_cast<std::size_t>(c0) * kCluster;
-    const float4* tsph = prm.cl.tsph + static_cast<std::size_t>(c0) * kCluster;
-    const double rmin = 1e-6 * b;
-    while (pm) {
-      const int L = __ffs(pm) - 1;
-      pm &= pm - 1;
-      double qx = __shfl_sync(kFull, x, L), qy = __shfl_sync(kFull, y, L), qz = __shfl_sync(kFull, z, L);
-      const double ux = __shfl_sync(kFull, tx, L), uy = __shfl_sync(kFull, ty, L), uz = __shfl_sync(kFull, tz, L);
-      const double ur = __shfl_sync(kFull, tr, L);
-      bool ok = false;  // warp-uniform
-      for (int step = 0; step < steps; ++step) {
-        const double ex = ux - qx, ey = uy - qy, ez = uz - qz;
-        const double len = sqrt(ex * ex + ey * ey + ez * ez);
-        const double need = len - ur;  // a ball of radius > need around q meets the neighbour's ball
-        if (need < -1e-9) {
-          ok = true;
-          break;
-        }
-        const double d = warp_nearest_dist(qx, qy, qz, need * (1.0 + 1e-6) + 2e-9, prm.cx, prm.cy, prm.cz, sup, nsup,
-                                           clus, nclus, ctri, tsph, prm.cl.xyz, prm.cl.tri);
-        const double r = d * (1.0 - 1e-9) - 1e-9;
-        if (r > need + 1e-9) {
-          ok = true;
-          break;
-        }
-        if (r < rmin) break;  // running into the surface
-        const double f = kTraceStep * r / len;
-        qx += f * ex;
-        qy += f * ey;
-        qz += f * ez;
-      }
-      if (lane == L) resolved = ok;
-    }
-  }
-  if (prm.counters) {
-    const unsigned nb = __popc(__ballot_sync(kFull, resolved && !pending));
-    const unsigned nt = __popc(__ballot_sync(kFull, resolved && pending));
-    if (lane == 0 && nb) atomicAdd(prm.counters, static_cast<unsigned long long>(nb));
-    if (lane == 0 && nt) atomicAdd(prm.counters + 1, static_cast<unsigned long long>(nt));
+  if (pending) {
+    const unsigned r = atomicAdd(prm.npend, 1u);
+    PendPair& q = prm.pend[r];
+    q.i = i;
+    q.j = j;
+    q.k = static_cast<std::uint32_t>(k);
+    q.w = static_cast<std::uint32_t>(wbest);
+    q.p[0] = x;
+    q.p[1] = y;
+    q.p[2] = z;
+    q.t[0] = tx;
+    q.t[1] = ty;
+    q.t[2] = tz;
+    q.t[3] = tr;
   }
   if (resolved) {
     atomicAnd(prm.unk + i, ~(1u << k));
     if (prm.write_known && wbest == 1) atomicOr(prm.masks + j, 1u << k);
     if (prm.s_out) prm.s_out[static_cast<std::size_t>(j) * prm.K + k] = wbest == 1 ? 1.0 : 0.0;
+  }
+}
+
+// A chain of surface-free balls from p towards the certified neighbour's
+// ball, one warp per pending pair, the whole warp on each nearest-triangle
+// query (warp_nearest_dist). Each ball B(q, r) has r just below q's exact
+// distance to the compartment's triangles; the next centre is kTraceStep r
+// further along the line to the neighbour's centre (inside the current
+// ball, so consecutive balls overlap); the chain succeeds when a ball
+// reaches the neighbour's ball. The first ball alone is the test "B(p, gap)
+// meets no triangle". A line that runs into the surface stops (radius below
+// 1e-6 child edges) or gives up after kTraceSteps balls: the pair is
+// evaluated. The outcome depends only on the point and the surfaces.
+static __global__ void __launch_bounds__(256) k_pair_chain(const ResolveParams prm) {
+  const unsigned npend = *prm.npend;
+  const int lane = threadIdx.x & 31;
+  for (unsigned r = (blockIdx.x * blockDim.x + threadIdx.x) / 32; r < npend; r += gridDim.x * blockDim.x / 32) {
+    const PendPair q = prm.pend[r];
+    const int k = static_cast<int>(q.k);
+    const CellGrid g = prm.grids[k];
+    const double b = g.B / kSubCells, rmin = 1e-6 * b;
+    const float4* sup = prm.cl.sup + prm.cl.soff[k];
+    const int nsup = static_cast<int>(prm.cl.soff[k + 1] - prm.cl.soff[k]);
+    const std::uint32_t c0 = prm.cl.coff[k];
+    const int nclus = static_cast<int>(prm.cl.coff[k + 1] - c0);
+    double qx = q.p[0], qy = q.p[1], qz = q.p[2];
+    bool ok = false;  // warp-uniform
+    for (int step = 0; step < kTraceSteps; ++step) {
+      const double ex = q.t[0] - qx, ey = q.t[1] - qy, ez = q.t[2] - qz;
+      const double len = sqrt(ex * ex + ey * ey + ez * ez);
+      const double need = len - q.t[3];  // a ball of radius > need around q meets the neighbour's ball
+      if (need < -1e-9) {
+        ok = true;
+        break;
+      }
+      const double d = warp_nearest_dist(qx, qy, qz, need * (1.0 + 1e-6) + 2e-9, prm.cx, prm.cy, prm.cz, sup, nsup,
+                                         prm.cl.clus + c0, nclus, prm.cl.clus_tri + static_cast<std::size_t>(c0) * kCluster,
+                                         prm.cl.tsph + static_cast<std::size_t>(c0) * kCluster, prm.cl.xyz, prm.cl.tri);
+      const double rr = d * (1.0 - 1e-9) - 1e-9;
+      if (rr > need + 1e-9) {
+        ok = true;
+        break;
+      }
+      if (rr < rmin) break;  // running into the surface
+      const double f = kTraceStep * rr / len;
+      qx += f * ex;
+      qy += f * ey;
+      qz += f * ez;
+    }
+    if (ok && lane == 0) {
+      atomicAnd(prm.unk + q.i, ~(1u << k));
+      if (prm.write_known && q.w == 1u) atomicOr(prm.masks + q.j, 1u << k);
+      if (prm.s_out) prm.s_out[static_cast<std::size_t>(q.j) * prm.K + k] = q.w == 1u ? 1.0 : 0.0;
+    }
   }
 }
 

@@ -215,9 +215,12 @@ std::vector<std::uint32_t> classify_cells(nm_ctx* c, const double* d_pts, std::s
     rp.cl.xyz = static_cast<const double*>(c->xyz64.p);
     rp.cl.tri = static_cast<const std::uint32_t*>(c->tri_idx.p);
     rp.counters = nullptr;
-    rp.trace_steps = double(c->sparse_evals) >= nm::kTraceMinEvals ? nm::kTraceSteps : 1;
+    rp.pend = c->pend.as<nm::PendPair>(std::max<std::size_t>(total, 1));
+    rp.npend = c->pend_n.as<unsigned>(1);
+    NM_CUDA(cudaMemsetAsync(rp.npend, 0, sizeof(unsigned), st));
     nm::k_pair_resolve<<<static_cast<unsigned>((std::size_t(wsum) * 32 + 255) / 256), 256, 0, st>>>(rp);
-    ++launches;
+    nm::k_pair_chain<<<grid_for(total * 32, 256, c->sm_count * 64), 256, 0, st>>>(rp);
+    launches += 2;
     NM_CUDA(cudaGetLastError());
     c->resolved_pairs = total - build_lists();
   } else {
