@@ -125,8 +125,8 @@ class DevicePool {
 };
 
 // Device buffers retired by a DBuf that grew: queued work may still read
-// them, so they are freed per device at the end of the C ABI call (guarded)
-// after one device synchronisation — never by a cudaFree in the middle of a
+// them, so they are freed at the end of the C ABI call (guarded) after one
+// synchronisation of their device — never by a cudaFree in the middle of a
 // call, which would wait for the whole device and block other host threads'
 // CUDA calls meanwhile (the certified-cell thread of nm_set_surfaces beside
 // the main thread's uploads; probes/copy_hol.cu).
@@ -140,25 +140,25 @@ class Retired {
     std::lock_guard<std::mutex> g(m_);
     v_.emplace_back(dev, p);
   }
-  void drain_current_device() {
-    int d = 0;
-    if (cudaGetDevice(&d) != cudaSuccess) return;
-    std::vector<void*> mine;
+  // every device's retired buffers (a group call's worker threads retire on
+  // their own devices); the calling thread's device is restored
+  void drain() {
+    std::vector<std::pair<int, void*>> all;
     {
       std::lock_guard<std::mutex> g(m_);
-      for (std::size_t i = 0; i < v_.size();) {
-        if (v_[i].first == d) {
-          mine.push_back(v_[i].second);
-          v_[i] = v_.back();
-          v_.pop_back();
-        } else {
-          ++i;
-        }
-      }
+      all.swap(v_);
     }
-    if (mine.empty()) return;
-    cudaDeviceSynchronize();
-    for (void* p : mine) DevicePool::free(p, d);
+    if (all.empty()) return;
+    int cur = 0;
+    cudaGetDevice(&cur);
+    std::sort(all.begin(), all.end());
+    for (std::size_t i = 0; i < all.size();) {
+      const int d = all[i].first;
+      cudaSetDevice(d);
+      cudaDeviceSynchronize();
+      for (; i < all.size() && all[i].first == d; ++i) DevicePool::free(all[i].second, d);
+    }
+    cudaSetDevice(cur);
   }
 
  private:
@@ -169,7 +169,7 @@ class Retired {
 template <class F>
 inline int guarded(F&& f) {
   struct Drain {
-    ~Drain() { Retired::get().drain_current_device(); }
+    ~Drain() { Retired::get().drain(); }
   } drain;
   try {
     f();
