@@ -1056,13 +1056,22 @@ static __global__ void k_fix_finalize(const FixupParams prm) {
 // K4: tet labels: highest-priority compartment containing all
 // four nodes, else 0.
 // ---------------------------------------------------------------------------
+// bad (nullable): tets with a node id >= n_nodes get label 0 and set *bad
+// (the caller reports them) instead of reading out of range; without it the
+// ids must have been checked.
 static __global__ void k_label_tets(const uint4* __restrict__ tets, std::size_t nt, const std::uint32_t* __restrict__ masks,
-                             int* __restrict__ labels, const LabelIds ids, std::size_t n_nodes) {
+                             int* __restrict__ labels, const LabelIds ids, std::size_t n_nodes,
+                             std::uint32_t* __restrict__ bad = nullptr) {
   __shared__ int s_ids[32];
   const int* id = stage_ids(ids, s_ids);
   for (std::size_t i = blockIdx.x * static_cast<std::size_t>(blockDim.x) + threadIdx.x; i < nt;
        i += static_cast<std::size_t>(gridDim.x) * blockDim.x) {
     const uint4 t = __ldcs(tets + i);  // read once; the gathered masks stay in L2
+    if (bad && !(t.x < n_nodes && t.y < n_nodes && t.z < n_nodes && t.w < n_nodes)) {
+      atomicOr(bad, 1u);
+      __stcs(labels + i, 0);
+      continue;
+    }
     NM_DCHECK(t.x < n_nodes && t.y < n_nodes && t.z < n_nodes && t.w < n_nodes, "k_label_tets: node id out of range");
     const std::uint32_t m = __ldg(masks + t.x) & __ldg(masks + t.y) & __ldg(masks + t.z) & __ldg(masks + t.w);
     __stcs(labels + i, m ? id[__ffs(m) - 1] : 0);

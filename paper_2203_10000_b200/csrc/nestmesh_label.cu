@@ -1255,10 +1255,6 @@ int nm_label_mesh(nm_ctx* c, const double* nodes, std::size_t n, const std::uint
     auto* d_tets = c->tets.as<std::uint32_t>(4 * std::max<std::size_t>(nt, 1));
     auto* d_labels = c->labels.as<int>(std::max<std::size_t>(nt, 1));
     auto* d_word = c->word.as<std::uint32_t>(1);
-    // tet upload + index validation on the side stream, from a helper host
-    // thread (a pageable tet array is staged by host copies), so it runs under
-    // the whole node pass (which synchronises the host for the fix-up's pair
-    // lists and, with certified cells, for the sparse grid)
     const bool timing = std::getenv("NM_TIMING") != nullptr;
     const auto t_start = std::chrono::steady_clock::now();
     auto lap = [&](const char* what) {
@@ -1267,27 +1263,47 @@ int nm_label_mesh(nm_ctx* c, const double* nodes, std::size_t n, const std::uint
       std::fprintf(stderr, "[nm_label_mesh] %-14s %8.2f ms\n", what,
                    std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count());
     };
-    // the nodes first (every host copy thread on them: the node pass needs
-    // all of them), then the tets on the side thread under the node pass
+    // The nodes first (every host copy thread on them: the node pass needs
+    // all of them). The tets follow in chunks on a helper thread and the side
+    // stream, under the node pass; once the node masks are done, each chunk's
+    // labels are computed as soon as it is on the device and copied back
+    // while the later chunks still upload (H2D and D2H run on separate copy
+    // engines), so the labels' read-back hides under the tet upload. Tets
+    // with a node id >= n get label 0 and are reported after the last chunk.
     c->h2d(d_pts, nodes, 3 * n * sizeof(double), c->stream);
     lap("nodes h2d");
+    constexpr std::size_t kTetChunk = std::size_t(4) << 20;  // tets per chunk (64 MB of indices)
+    const std::size_t nch = nt ? (nt + kTetChunk - 1) / kTetChunk : 0;
+    std::vector<cudaEvent_t> up_ev(nch, nullptr);
+    struct EvGuard {
+      std::vector<cudaEvent_t>& v;
+      ~EvGuard() {
+        for (cudaEvent_t e : v)
+          if (e) cudaEventDestroy(e);
+      }
+    } ev_guard{up_ev};
+    for (auto& e : up_ev) NM_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    NM_CUDA(cudaMemsetAsync(d_word, 0, sizeof(std::uint32_t), c->stream));
+    std::atomic<std::size_t> uploaded{0};
+    std::atomic<bool> side_failed{false};
     std::exception_ptr side_err;
     std::thread side_thread;
     if (nt) {
       side_thread = std::thread([&] {
         try {
           NM_CUDA(cudaSetDevice(c->opt.device));
-          // the main copy pool: the node copies are done, the main thread
-          // only drives the node pass until it joins this thread
-          c->h2d(d_tets, tets, 4 * nt * sizeof(std::uint32_t), c->side, /*side=*/true, /*side_pool=*/false);
-          NM_CUDA(cudaMemsetAsync(d_word, 0, sizeof(std::uint32_t), c->side));
-          nm::k_max_index<<<grid_for(nt, 256, c->sm_count * 8), 256, 0, c->side>>>(
-              reinterpret_cast<const uint4*>(d_tets), nt, d_word);
-          NM_CUDA(cudaGetLastError());
-          NM_CUDA(cudaMemcpyAsync(c->h_word, d_word, sizeof(std::uint32_t), cudaMemcpyDeviceToHost, c->side));
-          NM_CUDA(cudaEventRecord(c->ev_side, c->side));
+          for (std::size_t q = 0; q < nch; ++q) {
+            const std::size_t t0 = q * kTetChunk, m = std::min(kTetChunk, nt - t0);
+            // the main copy pool: the node copies are done, the main thread
+            // copies labels back through the side pool
+            c->h2d(d_tets + 4 * t0, tets + 4 * t0, 4 * m * sizeof(std::uint32_t), c->side, /*side=*/true,
+                   /*side_pool=*/false);
+            NM_CUDA(cudaEventRecord(up_ev[q], c->side));
+            uploaded.store(q + 1, std::memory_order_release);
+          }
         } catch (...) {
           side_err = std::current_exception();
+          side_failed.store(true, std::memory_order_release);
         }
       });
     }
@@ -1299,21 +1315,33 @@ int nm_label_mesh(nm_ctx* c, const double* nodes, std::size_t n, const std::uint
     } join{side_thread};
     label_nodes_dev(c, d_pts, n, T, d_masks, nullptr, c->stream, stats, nullptr, /*stats_deferred=*/true);
     lap("node pass");
-    if (nt) {
-      side_thread.join();
-      lap("tets h2d joined");
-      if (side_err) std::rethrow_exception(side_err);
-      NM_CUDA(cudaStreamWaitEvent(c->stream, c->ev_side, 0));
-      NM_CUDA(cudaEventSynchronize(c->ev_side));
-      if (*c->h_word >= n) {
-        NM_CUDA(cudaStreamSynchronize(c->stream));
-        check_tets(tets, nt, n);  // throws with the offending tet
-      }
-    }
     if (stats && n) read_node_stats(c, n, c->stream, stats);
-    label_tets_dev(c, d_tets, nt, d_masks, d_labels, c->stream, stats, n);
-    lap("tet labels");
-    c->d2h(labels_out, d_labels, nt * sizeof(int), c->stream);
+    if (stats) NM_CUDA(cudaEventRecord(c->ev[4], c->stream));
+    for (std::size_t q = 0; q < nch; ++q) {
+      while (uploaded.load(std::memory_order_acquire) <= q && !side_failed.load(std::memory_order_acquire))
+        std::this_thread::yield();
+      if (side_failed.load(std::memory_order_acquire)) break;
+      const std::size_t t0 = q * kTetChunk, m = std::min(kTetChunk, nt - t0);
+      NM_CUDA(cudaStreamWaitEvent(c->stream, up_ev[q], 0));
+      nm::k_label_tets<<<grid_for(m, 256, c->sm_count * 32), 256, 0, c->stream>>>(
+          reinterpret_cast<const uint4*>(d_tets) + t0, m, d_masks, d_labels + t0, c->ids, n, d_word);
+      NM_CUDA(cudaGetLastError());
+      c->d2h(labels_out + t0, d_labels + t0, m * sizeof(int), c->stream, /*side=*/false, /*side_pool=*/true);
+    }
+    if (side_thread.joinable()) side_thread.join();
+    if (side_err) std::rethrow_exception(side_err);
+    lap("tets + labels");
+    if (stats) {
+      NM_CUDA(cudaEventRecord(c->ev[5], c->stream));
+      NM_CUDA(cudaEventSynchronize(c->ev[5]));
+      float ms = 0;
+      NM_CUDA(cudaEventElapsedTime(&ms, c->ev[4], c->ev[5]));  // labels with the tail of the upload
+      stats->ms_tets += ms;
+      stats->launches += static_cast<std::uint64_t>(nch);
+    }
+    NM_CUDA(cudaMemcpyAsync(c->h_word, d_word, sizeof(std::uint32_t), cudaMemcpyDeviceToHost, c->stream));
+    NM_CUDA(cudaStreamSynchronize(c->stream));
+    if (nt && *c->h_word) check_tets(tets, nt, n);  // throws with the offending tet
     if (masks_out) c->d2h(masks_out, d_masks, n * sizeof(std::uint32_t), c->stream);
     lap("d2h");
     NM_CUDA(cudaStreamSynchronize(c->stream));
