@@ -194,6 +194,28 @@ def test_group_nccl_exchange_one_device(monkeypatch):
     np.testing.assert_array_equal(m, mref)
 
 
+def test_label_mesh_chunked_tets_and_bad_index_in_last_chunk():
+    """nm_label_mesh labels the tets chunk by chunk under their upload: the
+    labels of a multi-chunk mesh (cfg2: 5.8M tets, two 4M-tet chunks) equal
+    the device-buffer path's, and an out-of-range node id in the LAST chunk
+    is still reported with its tet."""
+    from paper_2203_10000_b200._native import Context, NativeError
+    cfg = synth.config(2)
+    S = cfg.surfaces
+    nodes, tets = cfg.lattice_mesh()
+    assert tets.shape[0] > (4 << 20)
+    with Context(0, cull_outside=2) as c:
+        c.set_surfaces(S.xyz, S.tri, S.comp_off, S.label_ids)
+        lab, _, _ = c.label_mesh(nodes, tets)
+        m, _ = c.label_nodes(nodes)
+        ref = c.label_tets(tets, m)
+        np.testing.assert_array_equal(lab, ref)
+        bad = tets.copy()
+        bad[-3, 2] = nodes.shape[0]
+        with pytest.raises(NativeError, match="references node"):
+            c.label_mesh(nodes, bad)
+
+
 def test_abi_input_validation():
     """The C ABI rejects malformed inputs with a message instead of faulting."""
     from paper_2203_10000_b200._native import Context, NativeError
