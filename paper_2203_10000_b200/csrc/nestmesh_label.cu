@@ -1104,6 +1104,14 @@ int nm_set_surfaces(nm_ctx* c, const double* xyz, std::size_t nv, const std::uin
     if (cells) cells->finish();  // representatives need the tiles: after the packing
     lap("cells-fin");
     cells.reset();
+    // the packing's host arrays (~160 MB at cfg5: segments, fp32 records) are
+    // released on a detached thread: unmapping them took milliseconds
+    std::thread([a = std::move(segs), b = std::move(order), t = std::move(htri), u = std::move(hsub)]() mutable {
+      a.clear();
+      b.clear();
+      t.reset();
+      u.reset();
+    }).detach();
     lap("end");
   });
 }
