@@ -146,8 +146,16 @@ class PinnedChunks {
 // One pipeline of pinned chunk buffers bound to one stream at a time.
 class Stager {
  public:
-  static constexpr std::size_t kChunk = std::size_t(16) << 20;
-  static constexpr int kBufs = 3;
+// chunk size x buffers: 8 MB x 4 beat 16 x 3, 16 x 6, 32 x 3/4 and 64 x 3 on
+// node- and label-sized copies (profiles/r02/probe_staging_chunks.txt)
+#ifndef NM_STAGE_CHUNK_MB
+#define NM_STAGE_CHUNK_MB 8
+#endif
+#ifndef NM_STAGE_BUFS
+#define NM_STAGE_BUFS 4
+#endif
+  static constexpr std::size_t kChunk = std::size_t(NM_STAGE_CHUNK_MB) << 20;
+  static constexpr int kBufs = NM_STAGE_BUFS;
 
   Stager() = default;
   ~Stager() { release(); }

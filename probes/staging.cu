@@ -78,6 +78,23 @@ int main() {
     std::printf("stager %2d threads: h2d %.1f ms (%.1f GB/s), d2h %.1f ms (%.1f GB/s)\n", nth, ms(t0, t1),
                 bytes / ms(t0, t1) / 1e6, ms(t1, t2), bytes / ms(t1, t2) / 1e6);
   }
+  {  // the library's main pool (11 workers + the caller) on node- and label-sized copies
+    nmh::CopyPool pool(11);
+    nmh::Stager sg;
+    for (std::size_t sz : {std::size_t(242) << 20, std::size_t(200) << 20, bytes}) {
+      sg.h2d(dev, host.data(), sz, st, pool);
+      cudaStreamSynchronize(st);
+      auto t0 = clk::now();
+      sg.h2d(dev, host.data(), sz, st, pool);
+      cudaStreamSynchronize(st);
+      auto t1 = clk::now();
+      sg.d2h(host.data(), dev, sz, st, pool);
+      auto t2 = clk::now();
+      std::printf("stager 12 threads, %4zu MB: h2d %.2f ms (%.1f GB/s), d2h %.2f ms (%.1f GB/s)  [chunk %zu MB x %d]\n",
+                  sz >> 20, ms(t0, t1), sz / ms(t0, t1) / 1e6, ms(t1, t2), sz / ms(t1, t2) / 1e6,
+                  nmh::Stager::kChunk >> 20, nmh::Stager::kBufs);
+    }
+  }
   std::printf("hardware_concurrency %u\n", std::thread::hardware_concurrency());
   return 0;
 }
