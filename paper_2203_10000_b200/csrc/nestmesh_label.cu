@@ -1280,7 +1280,10 @@ int nm_label_mesh(nm_ctx* c, const double* nodes, std::size_t n, const std::uint
     // with a node id >= n get label 0 and are reported after the last chunk.
     c->h2d(d_pts, nodes, 3 * n * sizeof(double), c->stream);
     lap("nodes h2d");
-    constexpr std::size_t kTetChunk = std::size_t(4) << 20;  // tets per chunk (64 MB of indices)
+#ifndef NM_TET_CHUNK
+#define NM_TET_CHUNK (std::size_t(8) << 20)
+#endif
+    constexpr std::size_t kTetChunk = NM_TET_CHUNK;  // tets per chunk (128 MB of indices; profiles/r02/label_mesh_chunk_ab.txt)
     const std::size_t nch = nt ? (nt + kTetChunk - 1) / kTetChunk : 0;
     std::vector<cudaEvent_t> up_ev(nch, nullptr);
     struct EvGuard {

@@ -4,7 +4,8 @@ import ctypes
 import os
 import sys
 sys.path.insert(0, ".")
-os.environ["NM_TIMING"] = "1"
+if not os.environ.get("NO_NM_TIMING"):
+    os.environ["NM_TIMING"] = "1"
 import numpy as np
 from paper_2203_10000_b200 import synth
 cfg = synth.config(int(sys.argv[1]) if len(sys.argv) > 1 else 5)
