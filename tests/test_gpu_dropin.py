@@ -196,14 +196,14 @@ def test_group_nccl_exchange_one_device(monkeypatch):
 
 def test_label_mesh_chunked_tets_and_bad_index_in_last_chunk():
     """nm_label_mesh labels the tets chunk by chunk under their upload: the
-    labels of a multi-chunk mesh (cfg2: 5.8M tets, two 4M-tet chunks) equal
+    labels of a multi-chunk mesh (cfg3: 38M tets, five 8M-tet chunks) equal
     the device-buffer path's, and an out-of-range node id in the LAST chunk
     is still reported with its tet."""
     from paper_2203_10000_b200._native import Context, NativeError
-    cfg = synth.config(2)
+    cfg = synth.config(3)
     S = cfg.surfaces
     nodes, tets = cfg.lattice_mesh()
-    assert tets.shape[0] > (4 << 20)
+    assert tets.shape[0] > 2 * (8 << 20)  # several 8M-tet chunks
     with Context(0, cull_outside=2) as c:
         c.set_surfaces(S.xyz, S.tri, S.comp_off, S.label_ids)
         lab, _, _ = c.label_mesh(nodes, tets)
