@@ -313,7 +313,7 @@ struct nm_ctx {
   bool cells = false;
   nmh::DBuf dist_clus, dist_slot, dist_ord, sp_part, sp_det, cell_state, cell_child, cell_cert, cell_blk, cell_grids, clus, clus_tri, clus_tsph, unk, sp_list, sp_chunk, sp_cnt, rep_pts, rep_s, rep_m, rep_f,
       cell_unc, cell_blkidx, cell_val, child_val, row_first, rep_cur, rep_w, cell_dop, cell_cnt, cub_tmp2, cell_words, cert_first, cert_first2, cert_coff, ext_items, ext_first, ext_part, ext_val, geo_keys, geo_vals, geo_keys2, geo_vals2,
-      l1_rowruns, l1_runfirst, l1_cellrun, l1_parent, l1_runrow, l1_runx, l1_zero, l1_rootval, l1_nruns, clus_sup, pend, pend_n;
+      l1_rowruns, l1_runfirst, l1_cellrun, l1_parent, l1_runrow, l1_runx, l1_zero, l1_rootval, l1_nruns, clus_sup, pend, pend_n, fix_exact;
   std::uint64_t cells_total = 0, cells_certified = 0, cell_reps = 0, sparse_pairs = 0, sparse_evals = 0;
   std::uint64_t cells_l1 = 0, cells_children = 0;  // level-1 cells and children (nm_cell_dump)
   std::uint64_t resolved_pairs = 0;  // pairs of the last node pass resolved by k_pair_resolve

@@ -852,6 +852,8 @@ struct FixupParams {
   std::uint32_t* masks;
   double* s_out;
   unsigned long long* counters;  // [2] pairs, [3] ties
+  std::uint32_t* exact;          // per pair (packed pair index): 1 = stage 2 (the oracle's terms throughout)
+  int stage;                     // 1: hybrid terms; 2: oracle-order fp64 terms for the pairs marked exact
 };
 
 constexpr int kFixThreads = 128;
@@ -859,7 +861,12 @@ constexpr int kFixLanes = 8;                          // threads per pair
 constexpr int kFixPairs = kFixThreads / kFixLanes;    // pairs per batch
 constexpr int kFixTile = 128;                         // triangles per shared-memory tile (two buffers, 18 KB: ~8 CTAs per SM)
 constexpr int kFixChunk = 2048;                       // triangles per work item (multiple of kFixTile)
-constexpr std::size_t kFixSmem = 2 * kFixTile * 9 * sizeof(double);  // k_fixup dynamic shared memory
+constexpr int kFixRec = 16;                           // doubles per fix-up triangle record (k_deindex64)
+constexpr int kFixStride = kFixRec + 1;               // in shared memory: 136 B, so the 8 lanes of a pair
+                                                      // (records u, u + 1, ...) read 8 different banks
+constexpr std::size_t kFixSmem = 2 * kFixTile * kFixStride * sizeof(double);  // k_fixup dynamic shared memory
+constexpr float kFixFar2f = 64.0f;                    // far term: |A - p| > 8 x the longer edge from A
+constexpr double kFixExactBand = 1e-4;                // stage 1 results this close to T go to stage 2
 
 static __global__ void k_fix_count(const std::uint32_t* list, const std::uint32_t* count, const std::uint32_t* flagmask,
                                    std::uint32_t* pair_cnt) {
@@ -892,12 +899,52 @@ static __global__ void k_fix_fill(const std::uint32_t* list, const std::uint32_t
 }
 
 // de-indexed fp64 triangles for the fix-up (built once by nm_set_surfaces)
+// One fix-up record per triangle (kFixRec doubles, file order): the fp64
+// vertex A, 14 floats for the far evaluator (A, B - A, C - A, N = (B - A) x
+// (C - A) from fp64, the larger squared edge from A rounded up, a pad),
+// then the fp64 vertices B and C.
 static __global__ void k_deindex64(const double* xyz, const std::uint32_t* tri, std::size_t nt, double* tri64) {
-  for (std::size_t q = blockIdx.x * static_cast<std::size_t>(blockDim.x) + threadIdx.x; q < 9 * nt;
-       q += static_cast<std::size_t>(gridDim.x) * blockDim.x) {
-    const std::size_t t = q / 9, r = q % 9;
-    tri64[q] = xyz[3 * static_cast<std::size_t>(tri[3 * t + r / 3]) + r % 3];
+  for (std::size_t t = blockIdx.x * static_cast<std::size_t>(blockDim.x) + threadIdx.x; t < nt;
+       t += static_cast<std::size_t>(gridDim.x) * blockDim.x) {
+    double v[9];
+    for (int r = 0; r < 9; ++r) v[r] = xyz[3 * static_cast<std::size_t>(tri[3 * t + r / 3]) + r % 3];
+    double* o = tri64 + kFixRec * t;
+    for (int r = 0; r < 3; ++r) o[r] = v[r];
+    for (int r = 3; r < 9; ++r) o[7 + r] = v[r];  // B at 10, C at 13
+    const double ba[3] = {v[3] - v[0], v[4] - v[1], v[5] - v[2]}, ca[3] = {v[6] - v[0], v[7] - v[1], v[8] - v[2]};
+    const double n[3] = {ba[1] * ca[2] - ba[2] * ca[1], ba[2] * ca[0] - ba[0] * ca[2], ba[0] * ca[1] - ba[1] * ca[0]};
+    const double e2 = fmax(ba[0] * ba[0] + ba[1] * ba[1] + ba[2] * ba[2], ca[0] * ca[0] + ca[1] * ca[1] + ca[2] * ca[2]);
+    float* f = reinterpret_cast<float*>(o + 3);
+    f[0] = static_cast<float>(v[0]);
+    f[1] = static_cast<float>(v[1]);
+    f[2] = static_cast<float>(v[2]);
+    f[3] = static_cast<float>(ba[0]);
+    f[4] = static_cast<float>(ba[1]);
+    f[5] = static_cast<float>(ba[2]);
+    f[6] = static_cast<float>(ca[0]);
+    f[7] = static_cast<float>(ca[1]);
+    f[8] = static_cast<float>(ca[2]);
+    f[9] = static_cast<float>(n[0]);
+    f[10] = static_cast<float>(n[1]);
+    f[11] = static_cast<float>(n[2]);
+    f[12] = nextafterf(static_cast<float>(e2), INFINITY);
+    f[13] = 0.0f;
   }
+}
+
+// Far term of the hybrid first stage, fp32: R_a = A - p from the rounded
+// vertex and point (|R_a| > 8 edges, so ~1e-6 relative), the record's edges
+// and normal; the triangle subtends < 1/128 sr, so tan of the half angle
+// x = num / den < 1/256 and atan x = x - x^3/3 + x^5/5 to 1e-17.
+__device__ __forceinline__ float vos_far32(const float* f, float ax, float ay, float az, float la2) {
+  const float bx = ax + f[3], by = ay + f[4], bz = az + f[5];
+  const float cx = ax + f[6], cy = ay + f[7], cz = az + f[8];
+  const float la = sqrtf(la2), lb = sqrtf(bx * bx + by * by + bz * bz), lc = sqrtf(cx * cx + cy * cy + cz * cz);
+  const float num = f[9] * ax + f[10] * ay + f[11] * az;  // a . ((a + BA) x (a + CA)) = a . (BA x CA)
+  const float den = la * lb * lc + (ax * bx + ay * by + az * bz) * lc + (ax * cx + ay * cy + az * cz) * lb +
+                    (bx * cx + by * cy + bz * cz) * la;
+  const float x = __fdividef(num, den), x2 = x * x;
+  return x * (1.0f + x2 * (-1.0f / 3.0f + x2 * 0.2f));
 }
 
 // Work item (CTA): compartment c, a batch of kFixPairs of its pairs and a
@@ -948,7 +995,11 @@ static __global__ void __launch_bounds__(kFixThreads) k_fixup(const FixupParams 
     const std::uint32_t nch = fix_nchunk(hi - lo);
     const std::uint32_t l = wk - s_wo[c], batch = l / nch, chunk = l % nch;
     const std::uint32_t j = batch * kFixPairs + slot;
-    const bool has = j < prm.pair_cnt[c];
+    bool has = j < prm.pair_cnt[c];
+    if (prm.stage == 2) {
+      has = has && prm.exact[s_off[c] + j] != 0u;
+      if (!__syncthreads_or(has)) continue;  // no pair of this batch needs the oracle's terms
+    }
     double px = 0.0, py = 0.0, pz = 0.0;
     if (has) {
       const std::uint32_t w = prm.pairs[s_off[c] + j];
@@ -961,11 +1012,14 @@ static __global__ void __launch_bounds__(kFixThreads) k_fixup(const FixupParams 
     const std::uint32_t c0 = lo + chunk * kFixChunk, c1 = min(hi, c0 + kFixChunk);
     NM_DCHECK(c1 <= prm.n_tri && c0 <= c1, "k_fixup: triangle chunk out of range");
     double sum = 0.0, sum1 = 0.0;  // two independent chains (the fp64 atan2 / sqrt sequences are latency-bound)
+    bool near_zero = false;        // stage 1: a near term with num = 0
+    const float pfx = static_cast<float>(px), pfy = static_cast<float>(py), pfz = static_cast<float>(pz);
     auto load = [&](int buf, std::uint32_t t0) {
       const std::uint32_t m = min(static_cast<std::uint32_t>(kFixTile), c1 - t0);
-      const double* src = prm.tri64 + 9 * static_cast<std::size_t>(t0);
-      double* dst = s_fix + buf * (kFixTile * 9);
-      for (std::uint32_t q = threadIdx.x; q < 9 * m; q += kFixThreads) cp_async8(dst + q, src + q);
+      const double* src = prm.tri64 + kFixRec * static_cast<std::size_t>(t0);
+      double* dst = s_fix + buf * (kFixTile * kFixStride);
+      for (std::uint32_t q = threadIdx.x; q < kFixRec * m; q += kFixThreads)
+        cp_async8(dst + (q / kFixRec) * kFixStride + q % kFixRec, src + q);
       cp_async_commit();
     };
     __syncthreads();  // both buffers are free (previous work item done)
@@ -981,20 +1035,32 @@ static __global__ void __launch_bounds__(kFixThreads) k_fixup(const FixupParams 
       }
       __syncthreads();  // tile t0 is in buffer buf for every thread
       if (has) {
-        const double* tile = s_fix + buf * (kFixTile * 9);
-        // the oracle's exact operand order inside a term (no FMA): on-surface
-        // points (num = +-0) must get the oracle's atan2 branch
+        const double* tile = s_fix + buf * (kFixTile * kFixStride);
+        // stage 2: the oracle's exact operand order inside every term (no
+        // FMA): on-surface points (num = +-0) must get the
+        // oracle's atan2 branch. Stage 1: far triangles in fp32
+        // (vos_far32), the others as in stage 2; a near term with num = 0
+        // (the point in a triangle's plane) sends the pair to stage 2.
+        auto term = [&](const double* e) -> double {
+          if (prm.stage == 1) {
+            const float* f = reinterpret_cast<const float*>(e + 3);
+            const float ax = f[0] - pfx, ay = f[1] - pfy, az = f[2] - pfz;
+            const float d2 = ax * ax + ay * ay + az * az;
+            if (d2 > kFixFar2f * f[12]) return static_cast<double>(vos_far32(f, ax, ay, az, d2));
+            double num;
+            const double v = vos_half_angle64(e, e + 10, e + 13, px, py, pz, &num);
+            if (num == 0.0) near_zero = true;
+            return v;
+          }
+          return vos_half_angle64(e, e + 10, e + 13, px, py, pz);
+        };
         std::uint32_t u = lane;
         for (; u + kFixLanes < m; u += 2 * kFixLanes) {
-          const double* e = tile + 9 * u;
-          const double* f = e + 9 * kFixLanes;
-          sum += vos_half_angle64(e, e + 3, e + 6, px, py, pz);
-          sum1 += vos_half_angle64(f, f + 3, f + 6, px, py, pz);
+          const double* e = tile + kFixStride * u;
+          sum += term(e);
+          sum1 += term(e + kFixStride * kFixLanes);
         }
-        if (u < m) {
-          const double* e = tile + 9 * u;
-          sum += vos_half_angle64(e, e + 3, e + 6, px, py, pz);
-        }
+        if (u < m) sum += term(tile + kFixStride * u);
       }
       __syncthreads();  // buffer buf is consumed: the next iteration may refill it
     }
@@ -1003,6 +1069,7 @@ static __global__ void __launch_bounds__(kFixThreads) k_fixup(const FixupParams 
     for (int o = kFixLanes / 2; o > 0; o >>= 1) sum += __shfl_xor_sync(kFull, sum, o, kFixLanes);
     NM_DCHECK(!has || s_po[c] + j * nch + chunk < prm.n_part, "k_fixup: partial slot out of range");
     if (has && lane == 0) prm.part[s_po[c] + j * nch + chunk] = sum;
+    if (has && near_zero) atomicOr(prm.exact + s_off[c] + j, 1u);
   }
 }
 
@@ -1029,6 +1096,7 @@ static __global__ void k_fix_finalize(const FixupParams prm) {
     int c = 0;
     while (c + 1 < K && q >= s_off[c + 1]) ++c;
     const std::uint32_t j = q - s_off[c], nch = s_nch[c];
+    if (prm.stage == 2 && prm.exact[q] == 0u) continue;
     double tot = 0.0;
     NM_DCHECK(s_po[c] + (j + 1) * nch <= prm.n_part, "k_fix_finalize: partials out of range");
     for (std::uint32_t b = 0; b < nch; ++b) tot += prm.part[s_po[c] + j * nch + b];
@@ -1036,6 +1104,10 @@ static __global__ void k_fix_finalize(const FixupParams prm) {
     const std::uint32_t i = prm.order ? prm.order[prm.list[w]] : prm.list[w];
     NM_DCHECK(i < prm.n_pts, "k_fix_finalize: point id out of range");
     const double s = tot / (2.0 * CUDART_PI);
+    if (prm.stage == 1 && (prm.exact[q] != 0u || fabs(s - prm.T) < kFixExactBand)) {
+      prm.exact[q] = 1u;  // decided by stage 2
+      continue;
+    }
     if (s >= prm.T) atomicOr(prm.masks + i, 1u << c);
     else atomicAnd(prm.masks + i, ~(1u << c));
     ++pairs;

@@ -442,11 +442,19 @@ void label_nodes_dev(nm_ctx* c, const double* d_pts, std::size_t n, double T, st
     fp.masks = d_masks;
     fp.s_out = d_s;
     fp.counters = counters;
+    // two stages: hybrid terms (far triangles in fp32) decide the pairs whose
+    // s is not within kFixExactBand of T and whose point lies in no
+    // triangle's plane; the rest get the oracle-order fp64 terms throughout
+    fp.exact = c->fix_exact.as<std::uint32_t>(std::max<std::size_t>(total, 1));
+    NM_CUDA(cudaMemsetAsync(fp.exact, 0, total * sizeof(std::uint32_t), st));
     static_assert(nm::kFixSmem <= 48 * 1024, "k_fixup tiles must fit the default dynamic shared memory");
-    nm::k_fixup<<<grid_for(nwork, 1, c->sm_count * 16), nm::kFixThreads, nm::kFixSmem, st>>>(fp);
-    nm::k_fix_finalize<<<grid_for(total, 256, c->sm_count * 4), 256, 0, st>>>(fp);
+    for (int stage = 1; stage <= 2; ++stage) {
+      fp.stage = stage;
+      nm::k_fixup<<<grid_for(nwork, 1, c->sm_count * 16), nm::kFixThreads, nm::kFixSmem, st>>>(fp);
+      nm::k_fix_finalize<<<grid_for(total, 256, c->sm_count * 4), 256, 0, st>>>(fp);
+    }
     NM_CUDA(cudaGetLastError());
-    launches += 3;
+    launches += 5;
   }
   c->node_launches = launches;
   if (stats) {
@@ -682,9 +690,9 @@ int nm_set_surfaces(nm_ctx* c, const double* xyz, std::size_t nv, const std::uin
       up_on(c->tri_idx, tri, nt * 3 * sizeof(std::uint32_t));
       up_on(c->comp_off, comp_off, (K + 1) * sizeof(std::uint32_t));
       c->trace(side ? "cells" : "main", "prelude: uploads");
-      auto* t64 = c->tri64.as<double>(std::max<std::size_t>(9 * nt, 1));
+      auto* t64 = c->tri64.as<double>(std::max<std::size_t>(nm::kFixRec * nt, 1));
       if (nt)
-        nm::k_deindex64<<<grid_for(9 * nt, 256, c->sm_count * 16), 256, 0, c->side>>>(
+        nm::k_deindex64<<<grid_for(nt, 256, c->sm_count * 16), 256, 0, c->side>>>(
             static_cast<const double*>(c->xyz64.p), static_cast<const std::uint32_t*>(c->tri_idx.p), nt, t64);
       constexpr std::uint32_t kExtChunk = 8192;
       std::vector<nm::ExtentItem> items;

@@ -403,7 +403,7 @@ __device__ __forceinline__ double dot64(double ax, double ay, double az, double 
 }
 
 __device__ __forceinline__ double vos_half_angle64(const double* a, const double* b, const double* c, double px,
-                                                   double py, double pz) {
+                                                   double py, double pz, double* num_out = nullptr) {
   const double x1 = __dsub_rn(a[0], px), y1 = __dsub_rn(a[1], py), z1 = __dsub_rn(a[2], pz);
   const double x2 = __dsub_rn(b[0], px), y2 = __dsub_rn(b[1], py), z2 = __dsub_rn(b[2], pz);
   const double x3 = __dsub_rn(c[0], px), y3 = __dsub_rn(c[1], py), z3 = __dsub_rn(c[2], pz);
@@ -419,6 +419,7 @@ __device__ __forceinline__ double vos_half_angle64(const double* a, const double
   den = __dadd_rn(den, __dmul_rn(dot64(x1, y1, z1, x2, y2, z2), l3));
   den = __dadd_rn(den, __dmul_rn(dot64(x1, y1, z1, x3, y3, z3), l2));
   den = __dadd_rn(den, __dmul_rn(dot64(x2, y2, z2, x3, y3, z3), l1));
+  if (num_out) *num_out = num;
   return atan2(num, den);
 }
 
