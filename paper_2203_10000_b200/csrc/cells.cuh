@@ -451,7 +451,6 @@ struct ResolveParams {
   double* s_out;
   int write_known;
   CertifyParams cl;                    // clusters / superclusters / triangles (coff, soff, sup, clus, clus_tri, tsph, xyz, tri)
-  unsigned long long* counters;        // [0] resolved inside a ball, [1] resolved by a ball query
 };
 
 __device__ __forceinline__ int floor_div4(int x) { return x >= 0 ? x / 4 : -((-x + 3) / 4); }

@@ -214,7 +214,6 @@ std::vector<std::uint32_t> classify_cells(nm_ctx* c, const double* d_pts, std::s
     rp.cl.tsph = static_cast<const float4*>(c->clus_tsph.p);
     rp.cl.xyz = static_cast<const double*>(c->xyz64.p);
     rp.cl.tri = static_cast<const std::uint32_t*>(c->tri_idx.p);
-    rp.counters = nullptr;
     rp.pend = c->pend.as<nm::PendPair>(std::max<std::size_t>(total, 1));
     rp.npend = c->pend_n.as<unsigned>(1);
     NM_CUDA(cudaMemsetAsync(rp.npend, 0, sizeof(unsigned), st));
