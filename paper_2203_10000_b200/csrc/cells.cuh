@@ -512,7 +512,7 @@ static __device__ double warp_nearest_dist(double qx, double qy, double qz, doub
 #endif
 constexpr int kTraceSteps = NM_TRACE_STEPS;
 #ifndef NM_TRACE_STEP
-#define NM_TRACE_STEP 0.9
+#define NM_TRACE_STEP 0.99
 #endif
 constexpr double kTraceStep = NM_TRACE_STEP;  // next centre at this fraction of the radius (< 1: inside the ball)
 
