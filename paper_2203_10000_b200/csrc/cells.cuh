@@ -891,13 +891,22 @@ static __global__ void k_l1_total(const L1Params p, std::uint32_t nrows) {
   *p.nruns = nrows ? p.runfirst[nrows - 1] + p.rowruns[nrows - 1] : 0u;
 }
 
+// root of x without writes: during k_l1_flatten the only store to parent[i]
+// must be thread i's own (a path-halving store from another thread could
+// land after it and leave i pointing at a non-root)
+__device__ __forceinline__ std::uint32_t uf_root(const std::uint32_t* parent, std::uint32_t x) {
+  for (;;) {
+    const std::uint32_t px = __ldcg(parent + x);
+    if (px == x) return x;
+    x = px;
+  }
+}
+
 // parent = root; a component with a known-0 run is 0
 static __global__ void k_l1_flatten(const L1Params p) {
   const std::uint32_t nruns = *p.nruns;
-  for (std::uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nruns; i += gridDim.x * blockDim.x) {
-    const std::uint32_t root = uf_find(p.parent, i);
-    p.parent[i] = root;
-  }
+  for (std::uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nruns; i += gridDim.x * blockDim.x)
+    p.parent[i] = uf_root(p.parent, i);
 }
 static __global__ void k_l1_zero(const L1Params p) {
   const std::uint32_t nruns = *p.nruns;

@@ -108,6 +108,8 @@ class DevicePool {
     Dev& d = of(dev);
     void* p = nullptr;
     NM_CUDA(cudaMallocFromPoolAsync(&p, bytes, d.pool, d.st));
+    static const bool poison = std::getenv("NM_POISON") != nullptr;  // debugging: expose reads of unwritten memory
+    if (poison) NM_CUDA(cudaMemsetAsync(p, 0xa5, bytes, d.st));
     NM_CUDA(cudaStreamSynchronize(d.st));
     *dev_out = dev;
     static const bool tr = [] {
