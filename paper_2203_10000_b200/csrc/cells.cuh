@@ -631,7 +631,14 @@ static __global__ void __launch_bounds__(256) k_pair_resolve(const ResolveParams
 // meets no triangle". A line that runs into the surface stops (radius below
 // 1e-6 child edges) or gives up after kTraceSteps balls: the pair is
 // evaluated. The outcome depends only on the point and the surfaces.
-static __global__ void __launch_bounds__(256) k_pair_chain(const ResolveParams prm) {
+// 4 CTAs per SM (64 registers, small spills): the chains are latency-bound
+// dependent loads; at 116 registers (2 CTAs) the kernel ran at 14 % achieved
+// occupancy and 1.5 ms at cfg5 (profiles/r02/ncu_pair_chain_final.txt,
+// chain_occupancy_ab.txt)
+#ifndef NM_CHAIN_MIN_BLOCKS
+#define NM_CHAIN_MIN_BLOCKS 4
+#endif
+static __global__ void __launch_bounds__(256, NM_CHAIN_MIN_BLOCKS) k_pair_chain(const ResolveParams prm) {
   const unsigned npend = *prm.npend;
   const int lane = threadIdx.x & 31;
   for (unsigned r = (blockIdx.x * blockDim.x + threadIdx.x) / 32; r < npend; r += gridDim.x * blockDim.x / 32) {
