@@ -306,8 +306,14 @@ __device__ __forceinline__ int work_compartment(const CertifyParams& p, unsigned
   return k;
 }
 
+// 4 CTAs per SM: without a bound the certification kernels took 132-133
+// registers, one 256-thread CTA per SM (set_surfaces at cfg5 37.5 -> ~30 ms,
+// cfg3 40.7 -> 26.5 ms: profiles/r02/launch_bounds_ab.txt)
+#ifndef NM_CERT_MIN_BLOCKS
+#define NM_CERT_MIN_BLOCKS 4
+#endif
 // level 1, all compartments: one warp per 4 x 4 x 2 brick (first[] = brick prefix)
-static __global__ void __launch_bounds__(256) k_cell_certify_all(const CertifyParams p) {
+static __global__ void __launch_bounds__(256, NM_CERT_MIN_BLOCKS) k_cell_certify_all(const CertifyParams p) {
   const unsigned long long w = (blockIdx.x * static_cast<unsigned long long>(blockDim.x) + threadIdx.x) / 32;
   if (w >= p.warps) return;  // warp-uniform
   const int k = work_compartment(p, w);
@@ -324,7 +330,7 @@ static __global__ void __launch_bounds__(256) k_cell_certify_all(const CertifyPa
 }
 
 // level 2, all compartments: one warp per half child block (first[] = 2 x block prefix)
-static __global__ void __launch_bounds__(256) k_child_certify_all(const CertifyParams p) {
+static __global__ void __launch_bounds__(256, NM_CERT_MIN_BLOCKS) k_child_certify_all(const CertifyParams p) {
   const unsigned long long w = (blockIdx.x * static_cast<unsigned long long>(blockDim.x) + threadIdx.x) / 32;
   if (w >= p.warps) return;  // warp-uniform
   const int k = work_compartment(p, w);

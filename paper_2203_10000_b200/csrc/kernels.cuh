@@ -968,7 +968,10 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
-static __global__ void __launch_bounds__(kFixThreads) k_fixup(const FixupParams prm) {
+#ifndef NM_FIX_MIN_BLOCKS
+#define NM_FIX_MIN_BLOCKS 1  // 8 measured equal, 12 slower (profiles/r02/launch_bounds_ab.txt)
+#endif
+static __global__ void __launch_bounds__(kFixThreads, NM_FIX_MIN_BLOCKS) k_fixup(const FixupParams prm) {
   extern __shared__ double s_fix[];  // two tiles of kFixTile fp64 triangles (dynamic shared memory)
   __shared__ std::uint32_t s_off[33], s_wo[33], s_po[33];
   const int K = prm.K;
