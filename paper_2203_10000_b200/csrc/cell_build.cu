@@ -232,7 +232,7 @@ class CellBuild : public CellBuilder {
   // compartment k's grid: cubes of edge B = longest box side / cell_axis,
   // one cube of margin around the box
   void compartment_grid(int k) {
-    nm::CellGrid g{0.0, 0.0, 0.0, 1.0, 0, 0, 0, 0u};
+    nm::CellGrid g{0.0, 0.0, 0.0, 1.0, 0, 0, 0, 0u, 1.0};
     if (comp_off_[k + 1] > comp_off_[k]) {
       const double* e = hext_.data() + static_cast<std::size_t>(k) * nm::kExtQ;
       const double lo[3] = {e[0], e[1], e[2]}, hi[3] = {e[nm::kDopDirs], e[nm::kDopDirs + 1], e[nm::kDopDirs + 2]};
@@ -246,6 +246,7 @@ class CellBuild : public CellBuilder {
       g.nx = n3[0];
       g.ny = n3[1];
       g.nz = n3[2];
+      g.invB = 1.0 / g.B;
     }
     G_[k] = g;
   }

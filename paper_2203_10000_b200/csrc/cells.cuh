@@ -40,6 +40,8 @@ struct CellGrid {
   double ox, oy, oz, B;  // origin of cell (0,0,0) in the centred frame, cell edge (mm)
   int nx, ny, nz;
   std::uint32_t off;     // first cell of this compartment in the state array
+  double invB;           // 1 / B: point -> cell lookups multiply (an index one off at a face is
+                         // harmless: the neighbour's certified ball covers the shared face)
 };
 
 // ball radius of a cube of edge B (covers the closed cube, with margin)
@@ -392,7 +394,7 @@ static __global__ void k_cell_classify(const ClassifyParams prm) {
         continue;
       }
       const CellGrid g = prm.grids[c];
-      const double u = (x - g.ox) / g.B, v = (y - g.oy) / g.B, w = (z - g.oz) / g.B;
+      const double u = (x - g.ox) * g.invB, v = (y - g.oy) * g.invB, w = (z - g.oz) * g.invB;
       std::uint32_t st = 0;
       if (u >= 0.0 && v >= 0.0 && w >= 0.0 && u < g.nx && v < g.ny && w < g.nz) {
         const int iu = static_cast<int>(u), iv = static_cast<int>(v), iw = static_cast<int>(w);
@@ -555,7 +557,7 @@ static __global__ void __launch_bounds__(256) k_pair_resolve(const ResolveParams
   double best = 1e300, tx = 0.0, ty = 0.0, tz = 0.0, tr = 0.0;  // best gap and its certified ball
   int wbest = -1;
   if (active) {
-    const double u = (x - g.ox) / g.B, v = (y - g.oy) / g.B, ww = (z - g.oz) / g.B;
+    const double u = (x - g.ox) * g.invB, v = (y - g.oy) * g.invB, ww = (z - g.oz) * g.invB;
     const int iu = static_cast<int>(u), iv = static_cast<int>(v), iw = static_cast<int>(ww);
     const int fx = iu * kSubCells + min(static_cast<int>((u - iu) * kSubCells), kSubCells - 1);
     const int fy = iv * kSubCells + min(static_cast<int>((v - iv) * kSubCells), kSubCells - 1);
