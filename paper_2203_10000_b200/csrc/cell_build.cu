@@ -62,7 +62,8 @@ class CellBuild : public CellBuilder {
   // compartment's local representative r; kRun + q: the value of the
   // compartment's level-1 run q; kLeft / kRight: the neighbour parent's run
   // (resolved once the row is scanned)
-  static constexpr std::int64_t kUnknown = -1, kLeft = -2, kRight = -3, kRep = 1ll << 40, kRun = 1ll << 41;
+  static constexpr std::int64_t kUnknown = -1, kLeft = -2, kRight = -3, kRep = 1ll << 40, kRun = 1ll << 41,
+                                kCell = 1ll << 42;  // kCell + q: the run of level-1 cell q (resolved after the merge)
   static constexpr int S = nm::kSubCells;
   struct FineRun {
     std::size_t row;  // level-1 row base (global cell index of ix = 0)
@@ -663,6 +664,7 @@ class CellBuild : public CellBuilder {
       }
     }
     auto rebase = [&](std::int64_t v, std::size_t i) -> std::int64_t {
+      if (v >= kCell) return v;  // resolved below, once every slab's runs are rebased
       if (v >= kRun) return v + static_cast<std::int64_t>(run_base[i]);
       if (v >= kRep) return v + static_cast<std::int64_t>(rep_base[i]);
       return v;
@@ -674,6 +676,10 @@ class CellBuild : public CellBuilder {
       for (std::int64_t& v : part[i].run_val) v = rebase(v, i);
       for (FineRun& fr : part[i].fine) fr.v = rebase(fr.v, i);
       fine_[i] = std::move(part[i].fine);  // fine runs stay per slab (no copy)
+    });
+    parallel_for(static_cast<int>(ns), [&](int i) {
+      for (FineRun& fr : fine_[i])
+        if (fr.v >= kCell) fr.v = kRun + run_of_[static_cast<std::size_t>(fr.v - kCell)];
     });
     reps_.assign(K_, {});
     run_val_.assign(K_, {});
@@ -808,10 +814,13 @@ class CellBuild : public CellBuilder {
             v = jx == g.nx - 1 ? 0 : kRight;
           } else {
             const double yy = g.oy + iy * g.B + (sy + 0.5) * b, zz = g.oz + iz * g.B + (sz + 0.5) * b;
-            if (outside_dop(k, g.ox + (f + 0.5) * b, yy, zz) || outside_dop(k, g.ox + (e + 0.5) * b, yy, zz))
+            if (outside_dop(k, g.ox + (f + 0.5) * b, yy, zz) || outside_dop(k, g.ox + (e + 0.5) * b, yy, zz)) {
               v = 0;
-            else
-              v = new_rep(out, g.ox + ((f + e) / 2 + 0.5) * b, yy, zz);
+            } else {
+              // a certified parent beyond a y / z face (cells.cuh fine_face_neighbour)
+              const std::size_t nb = nm::fine_face_neighbour(cert1_.get(), g, row, iy, iz, sy, sz, f / S, e / S);
+              v = nb != nm::kNoCell ? kCell + static_cast<std::int64_t>(nb) : new_rep(out, g.ox + ((f + e) / 2 + 0.5) * b, yy, zz);
+            }
           }
           out.fine.push_back({row, f, e, sy, sz, v});
           f = e + 1;

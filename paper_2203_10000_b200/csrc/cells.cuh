@@ -961,6 +961,24 @@ static __global__ void k_l1_cellval(const L1Params p, std::uint32_t nrows) {
   }
 }
 
+constexpr std::size_t kNoCell = ~std::size_t(0);
+
+// The first certified level-1 cell beyond a y / z face of parents q0..q1 of
+// row (iy, iz) that the child sub-row (sy, sz) lies on (order: parents in x,
+// then y-, y+, z-, z+), or kNoCell. The host restatement (cell_build.cu
+// segment_runs) uses the same rule and order.
+__host__ __device__ inline std::size_t fine_face_neighbour(const std::uint8_t* cert, const CellGrid& g, std::size_t row,
+                                                           int iy, int iz, int sy, int sz, int q0, int q1) {
+  const std::size_t plane = static_cast<std::size_t>(g.nx) * g.ny;
+  for (int q = q0; q <= q1; ++q) {
+    if (sy == 0 && iy > 0 && cert[row - g.nx + q]) return row - g.nx + q;
+    if (sy == kSubCells - 1 && iy + 1 < g.ny && cert[row + g.nx + q]) return row + g.nx + q;
+    if (sz == 0 && iz > 0 && cert[row - plane + q]) return row - plane + q;
+    if (sz == kSubCells - 1 && iz + 1 < g.nz && cert[row + plane + q]) return row + plane + q;
+  }
+  return kNoCell;
+}
+
 static __global__ void k_runs_fine(const RunParams p, std::uint32_t nrows) {
   constexpr int S = kSubCells;
   for (std::size_t t = blockIdx.x * static_cast<std::size_t>(blockDim.x) + threadIdx.x; t < std::size_t(nrows) * S * S;
@@ -1000,7 +1018,12 @@ static __global__ void k_runs_fine(const RunParams p, std::uint32_t nrows) {
                      outside_dop_rn(p.dop4, k, __dadd_rn(g.ox, __dmul_rn(e + 0.5, b)), yy, zz)) {
             v = 0;
           } else {
-            v = new_rep(p, k, __dadd_rn(g.ox, __dmul_rn((f + e) / 2 + 0.5, b)), yy, zz);
+            // a run on a y / z face of its parents takes the value of a
+            // certified parent beyond that face (child and parent balls
+            // overlap: centre distance <= 0.82 B); else a representative
+            const std::size_t nb = fine_face_neighbour(p.cert, g, row, iy, iz, sy, sz, f / S, e / S);
+            if (nb != kNoCell) v = p.fill ? p.cellval[nb] : 0;
+            else v = new_rep(p, k, __dadd_rn(g.ox, __dmul_rn((f + e) / 2 + 0.5, b)), yy, zz);
           }
           if (p.fill)
             for (int q = f; q <= e; ++q) p.childval[cidx(q)] = v;
