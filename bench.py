@@ -45,8 +45,13 @@ OPS_PER_EVAL = 57                      # canonical VOS cost (FP3
 # per-opcode thread-instruction counts of one k_label launch of the same build
 # (scripts/ncu_opcounts.sh -> scripts/summarize_ncu.py opcounts), stamped with
 # the SASS hash of k_label<1,true,0>; a capture of another build is refused.
-OPCOUNT_FILE = ROOT / "profiles" / "r02" / "k_label_opcounts_cfg5.json"
-TRAFFIC_FILE = ROOT / "profiles" / "r02" / "k_label_traffic_cfg5.json"
+# One pair per config (cfg5: scripts/gpu_ncu_r02.sh, cfg2/cfg3: gpu_r02bu.sh).
+def opcount_file(cfg):
+    return ROOT / "profiles" / "r02" / f"k_label_opcounts_cfg{cfg}.json"
+
+
+def traffic_file(cfg):
+    return ROOT / "profiles" / "r02" / f"k_label_traffic_cfg{cfg}.json"
 
 
 def stamped(path, sass):
@@ -710,11 +715,12 @@ def main():
         sys.path.insert(0, str(ROOT / "scripts"))
         from kernel_hash import sass_hash
         sass = sass_hash()
+        OPCOUNT_FILE, TRAFFIC_FILE = opcount_file(args.config), traffic_file(args.config)
         ops, ops_why = stamped(OPCOUNT_FILE, sass)
         tr, tr_why = stamped(TRAFFIC_FILE, sass)
         strips = layout == "strips"
-        ops_pe = ops["fp32_lane_ops_per_eval"] if (ops and strips and args.config == 5) else None
-        traffic = tr["traffic_bytes"] * (nsh.size / tr["points"]) if (tr and strips and args.config == 5) else None
+        ops_pe = ops["fp32_lane_ops_per_eval"] if (ops and strips) else None
+        traffic = tr["traffic_bytes"] * (nsh.size / tr["points"]) if (tr and strips) else None
         roof = {
             "bound": "fp32", "kernel": f"k_label<1,{1 if strips else 0},0> (fp32x2 VOS tile loop, {layout} layout)",
             "achieved": achieved * ops_pe if ops_pe else None,

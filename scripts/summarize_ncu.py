@@ -46,7 +46,7 @@ def launches(path):
         print(f"{c:8d} {v / 1e6:12.3f} {100 * v / tot:7.2f}%  {k[:110]}")
 
 
-def traffic(path, sass_hash=None, points=None, note=""):
+def traffic(path, sass_hash=None, points=None, note="", config="5"):
     """k_label DRAM bytes per launch from a launch list taken with
     --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,lts__t_bytes.sum"""
     import json
@@ -65,7 +65,7 @@ def traffic(path, sass_hash=None, points=None, note=""):
     last = per[sorted(per, key=int)[-1]]
     rd, wr = last.get("dram__bytes_read.sum", 0.0), last.get("dram__bytes_write.sum", 0.0)
     pts = int(points) if points else None
-    print(json.dumps({"kernel": "k_label<1,1,0>", "config": 5, "sass_sha16": sass_hash, "points": pts,
+    print(json.dumps({"kernel": "k_label<1,1,0>", "config": int(config), "sass_sha16": sass_hash, "points": pts,
                       "launches_seen": len(per), "dram_bytes_read": rd, "dram_bytes_write": wr,
                       "traffic_bytes": rd + wr,
                       "algorithmic_bytes": pts * (24 + 4 + 8) if pts else None,
