@@ -69,7 +69,7 @@ def compile_label_lib(out: Path, defs=(), log=None):
 def build_label_lib(force=False) -> Path:
     LIB.mkdir(exist_ok=True)
     out = LIB / "libnestmesh_label.so"
-    deps = list(CSRC.glob("*.cu")) + list(CSRC.glob("*.cuh")) + [CSRC / "refine.cpp", ROOT / "include" / "nestmesh_label.h"]
+    deps = list(CSRC.glob("*.cu")) + list(CSRC.glob("*.cuh")) + list(CSRC.glob("*.h")) + [CSRC / "refine.cpp", ROOT / "include" / "nestmesh_label.h"]
     if force or _stale(out, deps):
         compile_label_lib(out, log=LIB / "ptxas_label.log")
     return out
@@ -80,7 +80,7 @@ def build_checked_lib(force=False) -> Path:
     (device-side bounds checks, csrc/check.cuh) for tests/test_gpu_checked.py."""
     out = LIB / "checked" / "libnestmesh_label.so"
     out.parent.mkdir(parents=True, exist_ok=True)
-    deps = list(CSRC.glob("*.cu")) + list(CSRC.glob("*.cuh")) + [CSRC / "refine.cpp", ROOT / "include" / "nestmesh_label.h"]
+    deps = list(CSRC.glob("*.cu")) + list(CSRC.glob("*.cuh")) + list(CSRC.glob("*.h")) + [CSRC / "refine.cpp", ROOT / "include" / "nestmesh_label.h"]
     if force or _stale(out, deps):
         compile_label_lib(out, defs=("NM_CHECKED",), log=out.parent / "ptxas_checked.log")
     return out

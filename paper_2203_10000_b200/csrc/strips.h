@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <cstdint>
 #include <functional>
+#include <memory>
 #include <queue>
 #include <utility>
 #include <vector>
@@ -45,7 +46,7 @@ inline std::vector<Strip> stripify(const std::uint32_t* tri, std::uint32_t t0, s
   struct Inc {
     std::uint32_t t, v[3];
   };
-  std::vector<Inc> inc(3 * std::size_t(m));
+  std::unique_ptr<Inc[]> inc(new Inc[3 * std::size_t(m)]);  // every entry written below
   {
     std::vector<std::uint32_t> cur(start.begin(), start.end() - 1);
     for (std::uint32_t i = 0; i < m; ++i) {
@@ -87,19 +88,55 @@ inline std::vector<Strip> stripify(const std::uint32_t* tri, std::uint32_t t0, s
     }
   }
   // Next start: the unused triangle with the smallest (degree, index).
-  // Degrees only decrease, so degree 3 is a forward scan; degrees 0..2 (and
-  // negative ones, possible only at non-manifold edges) are lazy min-heaps.
-  using MinHeap = std::priority_queue<std::uint32_t, std::vector<std::uint32_t>, std::greater<std::uint32_t>>;
+  // Degrees only decrease, so degree 3 is a forward scan; degrees 0..2 are
+  // two-level bitsets over the triangle index (exactly the unused triangles
+  // of that degree; a lower-bound cursor per degree); negative degrees,
+  // possible only at non-manifold edges, a lazy min-heap.
+  const std::size_t nw = (std::size_t(m) + 63) / 64, ns = (nw + 63) / 64;
+  std::vector<std::uint64_t> word[3], summ[3];
+  std::size_t lo[3] = {nw, nw, nw};  // no set word below lo[b]
+  for (int b = 0; b < 3; ++b) {
+    word[b].assign(nw, 0);
+    summ[b].assign(ns, 0);
+  }
+  auto set_bit = [&](int b, std::uint32_t i) {
+    const std::size_t w = i >> 6;
+    word[b][w] |= std::uint64_t(1) << (i & 63);
+    summ[b][w >> 6] |= std::uint64_t(1) << (w & 63);
+    lo[b] = std::min(lo[b], w);
+  };
+  auto clear_bit = [&](int b, std::uint32_t i) {
+    const std::size_t w = i >> 6;
+    word[b][w] &= ~(std::uint64_t(1) << (i & 63));
+    if (!word[b][w]) summ[b][w >> 6] &= ~(std::uint64_t(1) << (w & 63));
+  };
+  auto first_bit = [&](int b, std::uint32_t& out) {
+    for (std::size_t sw = lo[b] >> 6; sw < ns; ++sw) {
+      std::uint64_t x = summ[b][sw];
+      if (sw == lo[b] >> 6) x &= ~std::uint64_t(0) << (lo[b] & 63);
+      if (!x) continue;
+      const std::size_t w = sw * 64 + static_cast<std::size_t>(__builtin_ctzll(x));
+      lo[b] = w;
+      out = static_cast<std::uint32_t>(w * 64 + static_cast<std::size_t>(__builtin_ctzll(word[b][w])));
+      return true;
+    }
+    lo[b] = nw;
+    return false;
+  };
   using QE = std::pair<int, std::uint32_t>;
-  MinHeap bucket[3];
   std::priority_queue<QE, std::vector<QE>, std::greater<QE>> negative;
   std::uint32_t scan3 = 0;
   for (std::uint32_t i = 0; i < m; ++i)
-    if (deg[i] < 3) bucket[deg[i]].push(i);
+    if (deg[i] < 3) set_bit(deg[i], i);
   auto push = [&](std::uint32_t n) {
     const int d = --deg[n];
-    if (d >= 0) bucket[d].push(n);
+    if (d + 1 >= 0 && d + 1 < 3) clear_bit(d + 1, n);
+    if (d >= 0) set_bit(d, n);
     else negative.emplace(d, n);
+  };
+  auto take = [&](std::uint32_t t) {
+    used[t] = 1;
+    if (deg[t] >= 0 && deg[t] < 3) clear_bit(deg[t], t);
   };
   auto next = [&](std::uint32_t& out) {
     while (!negative.empty()) {
@@ -111,14 +148,7 @@ inline std::vector<Strip> stripify(const std::uint32_t* tri, std::uint32_t t0, s
       negative.pop();
     }
     for (int b = 0; b < 3; ++b)
-      while (!bucket[b].empty()) {
-        const std::uint32_t i = bucket[b].top();
-        if (!used[i] && deg[i] == b) {
-          out = i;
-          return true;
-        }
-        bucket[b].pop();
-      }
+      if (first_bit(b, out)) return true;
     while (scan3 < m && (used[scan3] || deg[scan3] != 3)) ++scan3;
     if (scan3 < m) {
       out = scan3;
@@ -174,7 +204,7 @@ inline std::vector<Strip> stripify(const std::uint32_t* tri, std::uint32_t t0, s
       s.t.insert(s.t.end(), ft.begin() + 1, ft.end());
       std::swap(best, s);
     }
-    for (std::uint32_t t : best.t) used[t] = 1;
+    for (std::uint32_t t : best.t) take(t);
     for (std::uint32_t t : best.t) {
       const std::uint32_t* f = tri + 3 * std::size_t(t0 + t);
       for (int j = 0; j < 3; ++j) {
