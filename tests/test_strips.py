@@ -64,3 +64,19 @@ def test_stripify_ragged_and_nonmanifold(strips_exe, tmp_path):
     r = subprocess.run([str(strips_exe), str(f)], capture_output=True, text=True, timeout=60)
     assert r.returncode == 0, (r.returncode, r.stderr)
     assert int(r.stdout.split()[2]) == 7
+
+
+def test_bitset_buckets_equal_heap_order(tmp_path):
+    """csrc/strips.h's exact bitset degree buckets pick the same next strip
+    start as the lazy heaps they replaced (tests/cpp/strips_heap_ref.h), on
+    random soups with non-manifold edges and degenerate triangles."""
+    cxx = shutil.which("g++")
+    if not cxx:
+        pytest.skip("no g++")
+    exe = tmp_path / "strips_equiv"
+    subprocess.run([cxx, "-O2", "-std=c++17", f"-I{ROOT / 'paper_2203_10000_b200' / 'csrc'}",
+                    f"-I{ROOT / 'tests' / 'cpp'}", str(ROOT / "tests" / "cpp" / "strips_equiv.cpp"), "-o", str(exe)],
+                   check=True)
+    for seed in (7, 11):
+        r = subprocess.run([str(exe), str(seed), "3000"], capture_output=True, text=True, timeout=300)
+        assert r.returncode == 0 and r.stdout.startswith("ok"), r.stdout + r.stderr
